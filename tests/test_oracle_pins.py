@@ -1,0 +1,442 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Each test names the oracle function it pins and what fixes the expected value:
+a worked example (tests/golden/*.json, cited), a closed form, an invariant, a
+library routine for a special case (LAPACK eigh, scipy's normal quantile, torch's
+bf16 cast), or brute force on tiny inputs.  See DESIGN.md §4 for the table.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+from scipy.stats import norm
+
+import oracle as O
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+WE = _gold("worked_examples.json")
+
+
+# ------------------------------------------------------------------ bf16 codec
+def test_bf16_worked_examples():
+    for ex in WE["bf16"]:
+        assert int(O.f64_to_bf16_rne(ex["f32"])) == ex["bits"], ex["cite"]
+        assert O.bf16_to_f64(np.uint16(ex["bits"])) == O.bf16_to_f64(O.f64_to_bf16_rne(ex["f32"]))
+
+
+def test_bf16_exhaustive_roundtrip():
+    """Every finite bf16 bit pattern widens and re-encodes to itself."""
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    v = O.bf16_to_f64(bits)
+    fin = np.isfinite(v)
+    back = O.f64_to_bf16_rne(v[fin])
+    # -0 and +0 keep their own patterns
+    assert np.array_equal(back, bits[fin])
+
+
+def test_bf16_matches_torch_rne_on_fp32_inputs():
+    """torch's float32->bfloat16 cast is RNE; fp32 inputs are exact in fp64 so both
+    see the same value and must agree bit for bit (incl. subnormal range)."""
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(200000, generator=g) * torch.pow(2.0, torch.randint(-140, 60, (200000,), generator=g).float())
+    x = x[torch.isfinite(x)]
+    ref = x.to(torch.bfloat16).view(torch.int16).numpy().astype(np.uint16)
+    got = O.f64_to_bf16_rne(x.numpy().astype(np.float64))
+    finite = np.isfinite(O.bf16_to_f64(ref))
+    assert np.array_equal(got[finite], ref[finite])
+
+
+# ------------------------------------------------------------------ covariance
+def test_covariance_single_token_is_outer_product():
+    x = np.array([[1.0, -2.0, 0.5]])
+    assert np.array_equal(O.covariance([x]), np.outer(x[0], x[0]))
+
+
+def test_covariance_duplicate_sequences_idempotent():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((5, 6))
+    assert np.allclose(O.covariance([x, x]), O.covariance([x]), rtol=0, atol=1e-14)
+
+
+def test_covariance_brute_force_loop():
+    rng = np.random.default_rng(1)
+    seqs = [rng.standard_normal((n, 8)) for n in (3, 5, 2)]
+    c = np.zeros((8, 8))
+    for s in seqs:
+        for t in range(s.shape[0]):
+            for a in range(8):
+                for b in range(8):
+                    c[a, b] += s[t, a] * s[t, b]
+    c /= 3
+    assert np.allclose(O.covariance(seqs), c, rtol=1e-13, atol=1e-13)
+    cc = O.covariance(seqs)
+    assert np.array_equal(cc, cc.T)
+
+
+# ------------------------------------------------------------------ PCA rotation
+@pytest.mark.parametrize("ex", WE["eigh"])
+def test_build_rotation_worked_examples(ex):
+    q, lam = O.build_rotation(np.array(ex["A"]))
+    assert np.allclose(lam, ex["lam"], atol=1e-12)
+    assert np.allclose(q, np.array(ex["Q"]), atol=1e-12), ex["cite"]
+
+
+def test_build_rotation_matches_lapack_distinct_eigenvalues():
+    """Special case that reduces to a library routine: LAPACK eigh (numpy) with the same
+    descending order and sign rule must give the same Q for distinct eigenvalues."""
+    rng = np.random.default_rng(2)
+    d = 32
+    b = rng.standard_normal((d, d))
+    c = b @ b.T / d
+    q, lam = O.build_rotation(c)
+    w, v = np.linalg.eigh(c)
+    order = np.argsort(-w)
+    w, v = w[order], v[:, order]
+    for i in range(d):
+        j = int(np.argmax(np.abs(v[:, i])))
+        if v[j, i] < 0:
+            v[:, i] = -v[:, i]
+    assert np.allclose(lam, w, rtol=1e-10, atol=1e-12)
+    assert np.allclose(q, v, atol=1e-8)
+
+
+@pytest.mark.parametrize("d", [64, 256])
+def test_jacobi_invariants(d):
+    """Q^T Q = I (BASELINE: 1e-6; expect ~1e-14), reconstruction <= 1e-7 ||C||_F,
+    Q^T C Q diagonal with descending diagonal (the defining PCA property)."""
+    rng = np.random.default_rng(d)
+    b = rng.standard_normal((d, d))
+    c = b @ b.T
+    q, lam = O.build_rotation(c)
+    assert np.max(np.abs(q.T @ q - np.eye(d))) < 1e-12
+    assert np.linalg.norm(q @ np.diag(lam) @ q.T - c) <= 1e-7 * np.linalg.norm(c)
+    t = q.T @ c @ q
+    assert np.max(np.abs(t - np.diag(np.diag(t)))) <= 1e-9 * np.linalg.norm(c)
+    assert np.all(np.diff(np.diag(t)) <= 1e-9 * np.linalg.norm(c))
+
+
+def test_toy_calibration_rotation():
+    """C1: the toy calibration set has distinct eigenvalues 2^(-i/4) (scaled), so Q is
+    unique up to sign; rotated coordinates' variances come out descending."""
+    seqs = [s.numpy() for s in synth.toy_calibration()]
+    c = O.covariance(seqs)
+    q, lam = O.build_rotation(c)
+    assert np.max(np.abs(q.T @ q - np.eye(64))) < 1e-12
+    z = np.concatenate(seqs) @ q
+    second_moment = np.mean(z * z, axis=0)
+    # Cov sums each sequence's X^T X and divides by M sequences: lam = N_tok * E[z_i^2]
+    assert np.allclose(second_moment * seqs[0].shape[0], lam, rtol=1e-9)
+    assert np.all(np.diff(lam) <= 0)
+
+
+# ------------------------------------------------------------------ fold / adapter / rotate
+def test_fold_computational_invariance():
+    """(x Q)(Q^T diag(g) Wc) = (x * g) Wc and (y Wc Q) Q^T = y Wc."""
+    rng = np.random.default_rng(3)
+    d, dout = 48, 80
+    q = synth.haar_orthogonal(d, 4).numpy()
+    wc = rng.standard_normal((d, dout))
+    g = 1 + 0.1 * rng.standard_normal(d)
+    x = rng.standard_normal(d)
+    lhs = O.rotate(x, q) @ O.fold_left_qt(q, wc, g)
+    assert np.allclose(lhs, (x * g) @ wc, rtol=0, atol=1e-12 * np.linalg.norm((x * g) @ wc))
+    w2 = rng.standard_normal((dout, d))
+    y = rng.standard_normal(dout)
+    assert np.allclose(O.fold_right_q(w2, q) @ q.T, w2, atol=1e-12)
+    assert np.allclose(y @ O.fold_right_q(w2, q), (y @ w2) @ q, atol=1e-12)
+
+
+def test_fold_identity_is_bit_identical():
+    wc = O.bf16_to_f64(synth.gaussian_bf16((16, 24), 1, 0.25).numpy())
+    assert np.array_equal(O.fold_left_qt(np.eye(16), wc), wc)
+    assert np.array_equal(O.fold_right_q(wc.T, np.eye(16)), wc.T)
+
+
+def test_adapter_identities():
+    q = synth.haar_orthogonal(32, 9).numpy()
+    q2 = synth.haar_orthogonal(32, 10).numpy()
+    assert np.allclose(O.residual_adapter(q, q), np.eye(32), atol=1e-13)
+    a = O.residual_adapter(q, q2)
+    assert np.max(np.abs(a.T @ a - np.eye(32))) < 1e-13
+    assert np.array_equal(O.residual_adapter(np.eye(4), np.eye(4)), np.eye(4))
+
+
+def test_rotate_preserves_norm_and_inverts():
+    rng = np.random.default_rng(4)
+    q = synth.haar_orthogonal(40, 11).numpy()
+    x = rng.standard_normal(40)
+    xr = O.rotate(x, q)
+    assert abs(np.linalg.norm(xr) - np.linalg.norm(x)) < 1e-13 * np.linalg.norm(x)
+    assert np.allclose(xr @ q.T, x, atol=1e-13)
+
+
+def test_rms_scale_closed_form():
+    x = np.full(8, -3.0)
+    assert O.rms_scale(x, 0.0) == pytest.approx(1 / 3.0, rel=1e-15)
+    q = synth.haar_orthogonal(8, 3).numpy()
+    y = np.arange(8.0) - 3
+    assert O.rms_scale(y @ q, 1e-6) == pytest.approx(O.rms_scale(y, 1e-6), rel=1e-13)
+
+
+# ------------------------------------------------------------------ Top-K
+@pytest.mark.parametrize("ex", WE["topk"])
+def test_topk_worked_examples(ex):
+    assert O.topk(np.array(ex["x"]), ex["k"]).tolist() == ex["idx"], ex["cite"]
+
+
+def _brute_topk(x, k):
+    """Z10 characterisation: the lexicographically smallest ascending index set S, |S| = k,
+    with min_{i in S} |x_i| >= max_{j not in S} |x_j|."""
+    n = len(x)
+    a = np.abs(x)
+    for s in itertools.combinations(range(n), k):   # lexicographic order
+        rest = [j for j in range(n) if j not in s]
+        if not s or not rest or min(a[list(s)]) >= max(a[rest]):
+            return list(s)
+    raise AssertionError
+
+
+def test_topk_brute_force_small():
+    rng = np.random.default_rng(6)
+    for trial in range(300):
+        n = int(rng.integers(1, 11))
+        # integer-valued entries with signs: many exact |.| ties, zeros and -0
+        x = rng.integers(-3, 4, n).astype(np.float64)
+        x[rng.random(n) < 0.1] = -0.0
+        k = int(rng.integers(0, n + 1))
+        got = O.topk(x, k).tolist()
+        assert got == _brute_topk(x, k), (x, k)
+
+
+def test_topk_exact_sparsity_every_token():
+    """'TopK 50.0 (+-0.0)': exactly k kept for every token incl. token 0."""
+    x = synth.residual_activation(32, 256, 3).numpy()
+    for t in range(32):
+        idx = O.topk(x[t], 128)
+        dense = np.zeros(256)
+        dense[idx] = x[t][idx]
+        assert len(idx) == 128 and len(set(idx.tolist())) == 128
+        assert O.actual_sparsity(dense) == 0.5
+        assert np.all(np.diff(idx) > 0)
+
+
+def test_topk_mask_bits():
+    m = O.topk_mask([0, 31, 32, 65], 70)
+    assert m.tolist() == [0x80000001, 0x1, 0x2]
+
+
+# ------------------------------------------------------------------ k and alpha
+@pytest.mark.parametrize("ex", WE["compute_k"])
+def test_compute_k_worked_examples(ex):
+    assert O.compute_k(ex["alpha"], ex["p"], ex["d"]) == ex["k"], ex["cite"]
+
+
+def test_alpha_table():
+    """App. B table: alpha2 exact; alpha4 within 0.01 of the printed value
+    (printed to 2 decimals; Z17), with the true M for Qwen2.5-72B (Z18)."""
+    for row in _gold("alpha_table.json")["rows"]:
+        a2, a4 = O.solve_alpha(row["a1"], row["a3"], row["M_true"])
+        assert a2 == pytest.approx(row["a2"], abs=1e-12), row["model"]
+        assert abs(a4 - row["a4"]) <= 0.01, row["model"]
+        assert 3 * row["a1"] + a2 == pytest.approx(4.0, abs=1e-12)
+        assert 2 * row["a3"] + row["M_true"] * a4 == pytest.approx(2 + row["M_true"], abs=1e-12)
+
+
+def test_site_ks_survey_appendix_rows():
+    """Derived k rows of SURVEY App. A (e.g. LLaMA3-8B 40% paper-alpha 1966/3932/1966/9585)
+    follow from the rule; a dropped (1-p) or swapped site would change them."""
+    a2, a4 = O.solve_alpha(0.8, 0.8, 3.5)
+    assert O.site_ks(0.4, (0.8, a2, 0.8, a4), 4096, 14336) == (1966, 3932, 1966, 9585)
+    a2, a4 = O.solve_alpha(0.9, 0.8, 11008 / 4096)
+    assert O.site_ks(0.5, (0.9, a2, 0.8, a4), 4096, 11008) == (1843, 2662, 1638, 6323)
+    assert O.site_ks(0.5, (1, 1, 1, 1), 4096, 11008) == (2048, 2048, 2048, 5504)
+
+
+# ------------------------------------------------------------------ GEMV
+@pytest.mark.parametrize("ex", WE["gemv"])
+def test_gemv_worked_example(ex):
+    wc = np.array(ex["W_pt"]).T
+    assert O.dense_gemv(wc, ex["x"]).tolist() == ex["y"]
+    assert O.sparse_gemv(wc, [0, 1], ex["x"]).tolist() == ex["y"]
+
+
+def test_sparse_gemv_special_cases_vs_loops():
+    rng = np.random.default_rng(8)
+    wc = rng.standard_normal((12, 7))
+    b = rng.standard_normal(7)
+    x = rng.standard_normal(12)
+    # k = D reduces to the dense GEMV, computed here by explicit loops
+    loop = [b[o] + sum(x[j] * wc[j, o] for j in range(12)) for o in range(7)]
+    assert np.allclose(O.sparse_gemv(wc, np.arange(12), x, b), loop, atol=1e-13)
+    assert np.array_equal(O.sparse_gemv(wc, np.arange(0), np.zeros(0), b), b)      # k = 0
+    assert np.allclose(O.sparse_gemv(wc, [5], [2.5]), 2.5 * wc[5], atol=0)        # k = 1
+
+
+# ------------------------------------------------------------------ Theorem A.1
+@pytest.mark.parametrize("ex", WE["normal"])
+def test_normal_functions_worked(ex):
+    if ex["fn"] == "inv_cdf":
+        assert abs(O.std_normal_inv_cdf(ex["u"]) - ex["value"]) <= ex["tol"]
+    else:
+        assert abs(O.std_normal_pdf(ex["t"]) - ex["value"]) <= ex["tol"]
+
+
+def test_inv_cdf_vs_scipy():
+    for u in np.linspace(1e-6, 1 - 1e-6, 501):
+        assert abs(O.std_normal_inv_cdf(u) - norm.ppf(u)) < 1e-8
+        assert abs(O.std_normal_cdf(O.std_normal_inv_cdf(u)) - u) < 1e-12
+
+
+@pytest.mark.parametrize("ex", WE["theorem_a1"])
+def test_theorem_worked(ex):
+    d = 4096
+    k = int(round(ex["keep"] * d))
+    assert abs(O.theory_relative_error(k, d) - ex["value"]) <= ex["tol"], ex["cite"]
+
+
+def test_theorem_monotone():
+    v = [O.theory_relative_error(k, 100) for k in range(101)]
+    assert all(a >= b for a, b in zip(v, v[1:]))
+
+
+def test_theorem_matches_monte_carlo_topk():
+    """The relative error of the oracle's real Top-K on i.i.d. Gaussian x~, W~ matches
+    Theorem A.1 within 2% at D = 4096.  A wrong selection (e.g. k
+    random entries: sqrt(1-k/D)) or a dropped term fails by > 2x."""
+    d, dout, n = 4096, 256, 400
+    g = np.random.default_rng(12)
+    w = g.standard_normal((d, dout))
+    x = g.standard_normal((n, d))
+    y = x @ w
+    for keep in (0.25, 0.5, 0.75):
+        k = int(keep * d)
+        ys = np.stack([O.sparse_gemv(w, s, x[i][s]) for i in range(n) for s in [O.topk(x[i], k)]])
+        num = np.mean(np.linalg.norm(y - ys, axis=1))
+        den = np.mean(np.linalg.norm(y, axis=1))
+        th = O.theory_relative_error(k, d)
+        assert abs(num / den - th) / th < 0.02, (keep, num / den, th)
+        rms = math.sqrt(np.mean(np.sum((y - ys) ** 2, 1)) / np.mean(np.sum(y ** 2, 1)))
+        assert abs(rms - th) / th < 0.02
+
+
+# ------------------------------------------------------------------ glue: RoPE / attention
+def test_rope_closed_forms():
+    v = np.array([1.0, 0.0])                         # hd = 2: a plain 2-D rotation by pos rad
+    assert np.allclose(O.rope(v, 1, 10000.0), [math.cos(1), math.sin(1)], atol=1e-15)
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal(16)
+    assert np.array_equal(O.rope(u, 0, 1e4), u)
+    assert np.allclose(O.rope(O.rope(u, 3, 1e4), 4, 1e4), O.rope(u, 7, 1e4), atol=1e-12)
+    assert abs(np.linalg.norm(O.rope(u, 9, 1e4)) - np.linalg.norm(u)) < 1e-12
+
+
+def test_attention_special_cases():
+    rng = np.random.default_rng(2)
+    q = rng.standard_normal((4, 8))
+    kc = rng.standard_normal((2, 5, 8))
+    vc = rng.standard_normal((2, 5, 8))
+    out = O.decode_attention(q, kc, vc, 1).reshape(4, 8)
+    assert np.allclose(out[0], vc[0, 0]) and np.allclose(out[1], vc[0, 0])   # GQA: heads 0,1 -> kv 0
+    assert np.allclose(out[2], vc[1, 0]) and np.allclose(out[3], vc[1, 0])
+    kc2 = np.repeat(kc[:, :1], 5, axis=1)                                      # equal keys -> mean of v
+    out2 = O.decode_attention(q, kc2, vc, 5).reshape(4, 8)
+    assert np.allclose(out2[3], vc[1].mean(0), atol=1e-14)
+
+
+# ------------------------------------------------------------------ block invariance (O-8)
+def _toy_layer(seed, d=64, inter=128, hq=4, hkv=2, hd=16, bias=False):
+    rng = np.random.default_rng(seed)
+    w = {
+        "wq": rng.standard_normal((d, hq * hd)) / math.sqrt(d),
+        "wk": rng.standard_normal((d, hkv * hd)) / math.sqrt(d),
+        "wv": rng.standard_normal((d, hkv * hd)) / math.sqrt(d),
+        "wo": rng.standard_normal((hq * hd, d)) / math.sqrt(hq * hd),
+        "wg": rng.standard_normal((d, inter)) / math.sqrt(d),
+        "wu": rng.standard_normal((d, inter)) / math.sqrt(d),
+        "wd": rng.standard_normal((inter, d)) / math.sqrt(inter),
+        "gamma1": 1 + 0.1 * rng.standard_normal(d),
+        "gamma2": 1 + 0.1 * rng.standard_normal(d),
+    }
+    if bias:
+        for n, m in (("bq", hq), ("bk", hkv), ("bv", hkv)):
+            w[n] = 0.02 * rng.standard_normal(m * hd)
+    cfg = dict(hq=hq, hkv=hkv, hd=hd, eps=1e-6, theta=10000.0)
+    return w, cfg
+
+
+def _fold_layer(w, q_l):
+    wqkv = np.concatenate([w["wq"], w["wk"], w["wv"]], axis=1)
+    wf = {
+        "wqkv": O.fold_left_qt(q_l, wqkv, w["gamma1"]),
+        "wo": O.fold_right_q(w["wo"], q_l),
+        "wg": O.fold_left_qt(q_l, w["wg"], w["gamma2"]),
+        "wu": O.fold_left_qt(q_l, w["wu"], w["gamma2"]),
+        "wd": O.fold_right_q(w["wd"], q_l),
+    }
+    if "bq" in w:
+        wf["bqkv"] = np.concatenate([w["bq"], w["bk"], w["bv"]])
+    return wf
+
+
+@pytest.mark.parametrize("bias", [False, True])
+def test_block_p0_equals_dense_two_layers(bias):
+    """Computational invariance end to end (S:615 acceptance #1): two rotated
+    folded layers with adapter A_0 = Q_0^T Q_1 at k = D reproduce the dense layers:
+    r_out^larosa = r_out^dense Q_{l+1}, within 1e-10 relative in fp64."""
+    d, ctx = 64, 6
+    layers = [_toy_layer(100 + l, bias=bias) for l in range(2)]
+    qs = [synth.haar_orthogonal(d, 200 + l).numpy() for l in range(3)]
+    cfg = layers[0][1]
+    rng = np.random.default_rng(7)
+    caches_d = [[rng.standard_normal((2, ctx, 16)) for _ in range(2)] for _ in range(2)]
+    caches_r = [[c.copy() for c in cc] for cc in caches_d]
+    r = rng.standard_normal(d)
+    rr = r @ qs[0]
+    pos = ctx - 1
+    full = (d, d, d, 128)
+    for l in range(2):
+        w = layers[l][0]
+        r, _ = O.dense_block(r, w, cfg, caches_d[l][0], caches_d[l][1], pos)
+        rr, _ = O.larosa_block(rr, _fold_layer(w, qs[l]), cfg, full, caches_r[l][0], caches_r[l][1], pos,
+                               adapter=O.residual_adapter(qs[l], qs[l + 1]))
+        assert np.linalg.norm(rr - r @ qs[l + 1]) <= 1e-10 * np.linalg.norm(r)
+    # the rotated embedding/head folds cancel: r_L Q_L^T is the dense output
+    assert np.allclose(rr @ qs[2].T, r, atol=1e-10 * np.linalg.norm(r))
+
+
+def test_block_exact_sparsity_and_monotone_error():
+    """Per-site kept counts are exactly k for every token and the mean relative
+    output error is non-decreasing in p over 5 seeds."""
+    d = 64
+    errs = {p: [] for p in (0.0, 0.25, 0.5, 0.75)}
+    for seed in range(5):
+        w, cfg = _toy_layer(300 + seed)
+        q = synth.haar_orthogonal(d, 400 + seed).numpy()
+        wf = _fold_layer(w, q)
+        rng = np.random.default_rng(seed)
+        kc = rng.standard_normal((2, 8, 16))
+        vc = rng.standard_normal((2, 8, 16))
+        for tok in range(4):
+            r = rng.standard_normal(d) * (1 + 5 * (rng.random(d) < 0.05))
+            ref, _ = O.dense_block(r, w, cfg, kc.copy(), vc.copy(), 7)
+            for p in errs:
+                ks = O.site_ks(p, (1, 1, 1, 1), d, 128)
+                out, inter = O.larosa_block(r @ q, wf, cfg, ks, kc.copy(), vc.copy(), 7)
+                for site, kk in zip(("idx1", "idx2", "idx3", "idx4"), ks):
+                    assert len(inter[site]) == kk
+                errs[p].append(np.linalg.norm(out @ q.T - ref) / np.linalg.norm(ref))
+    means = [np.mean(errs[p]) for p in sorted(errs)]
+    assert means[0] < 1e-12
+    assert all(a <= b for a, b in zip(means, means[1:])), means
