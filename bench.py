@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""LaRoSA decode hot path benchmark (driver contract).
+
+Workload (BASELINE.json configs[1]): one LLaMA2-7B decoder block (d 4096, MLP 11008, MHA
+32x128), batch 1, KV context 256, folded random-init weights, at sparsity p (default 0.5,
+uniform alpha), on 1 B200.  A *step* = one decode token through one block: Top-K(h1) ->
+sparse QKV GEMV (+RoPE, KV append) -> attention -> Top-K(h2) -> sparse O GEMV ->
+Top-K(h3) -> sparse gate|up GEMV (+SiLU*) -> Top-K(h4) -> sparse down GEMV -> dense
+adapter GEMV, all through larosa_sparse_layer (C ABI), replayed as CUDA graphs.  Steps
+cycle over 8 distinct layer copies (3.2 GB of weights >> 126 MB L2), and each step's
+input is the previous step's output residual (fresh Top-K sets every step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--p 0.5] [--impl reference]
+
+N > 1 (torchrun): every rank runs its own independent decode stream (replicas, weak
+scaling; the 7B block does not shard), timed with CUDA events, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode tokens/s (LLaMA2-7B decoder block, batch 1)"
+UNIT = "tok/s"
+CONFIG_NAME = "LLaMA2-7B decoder block (4096 hidden, 11008 MLP) batch 1"
+N_COPIES = 8
+CTX = 256
+
+
+# ------------------------------------------------------------------------------------ utils
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ oracle leg
+def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0):
+    """Time the fp64 oracle (as it stands) on the same block workload: widened folded-like
+    bf16 weights, n_tokens decode steps.  Returns (tok/s, seconds, threads)."""
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    d, inter, nq = shape.d, shape.inter, shape.hq * shape.hd
+    rng = np.random.default_rng(seed)
+
+    def wbits(shape_, std):
+        return O.f64_to_bf16_rne(rng.standard_normal(shape_, dtype=np.float32) * std)
+
+    wf = {"wqkv": O.bf16_to_f64(wbits((d, shape.qkv_out), d ** -0.5)),
+          "wo": O.bf16_to_f64(wbits((nq, d), nq ** -0.5)),
+          "wg": O.bf16_to_f64(wbits((d, inter), d ** -0.5)),
+          "wu": O.bf16_to_f64(wbits((d, inter), d ** -0.5)),
+          "wd": O.bf16_to_f64(wbits((inter, d), inter ** -0.5))}
+    adapter = O.bf16_to_f64(wbits((d, d), d ** -0.5))
+    cfg = dict(hq=shape.hq, hkv=shape.hkv, hd=shape.hd, eps=shape.rms_eps, theta=shape.rope_theta)
+    kc = rng.standard_normal((shape.hkv, CTX, shape.hd))
+    vc = rng.standard_normal((shape.hkv, CTX, shape.hd))
+    r = synth.residual_activation(1, d, seed=1).numpy()[0].astype(np.float64)
+    t0 = time.perf_counter()
+    for _ in range(n_tokens):
+        r, _ = O.larosa_block(r, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True)
+    dt = time.perf_counter() - t0
+    return n_tokens / dt, dt, threads
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    shape = synth.MODELS["llama2-7b"]
+    import oracle as O
+    plan = O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter)
+    oracle_block_sample(shape, plan, 1)                       # warm-up (page in, BLAS init)
+    steps = max(1, args.steps if args.steps <= 8 else 8)      # bounded CPU sample
+    tok_s, dt, threads = oracle_block_sample(shape, plan, steps)
+    out = {"impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "ctx": CTX},
+           "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": f"{steps} decode tokens through one LLaMA2-7B block (fp64 numpy oracle)"},
+           "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ------------------------------------------------------------------------------------ GPU leg
+def build_stack(shape, device, n_copies, seed=0):
+    from paper_2507_01299_b200 import model as M
+    qs = [synth.haar_orthogonal(shape.d, seed=100 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
+    layers = []
+    for i in range(n_copies):
+        orig = M.synth_original_layer(shape, seed + i + 1, device=device)
+        layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1]))
+        del orig
+    torch.cuda.synchronize()
+    return layers
+
+
+def time_gemv_sites(layers, plan, shape, device, reps=40):
+    """Average duration of the standalone sparse GEMV (larosa_sparse_gemv) per site, with
+    CUDA events on the launching stream, cycling layer copies and fresh Top-K inputs."""
+    from paper_2507_01299_b200 import larosa as LZ
+    k1, k2, k3, k4 = plan
+    nq = shape.hq * shape.hd
+    sites = [("qkv", "w_qkv", shape.d, shape.qkv_out, k1), ("o", "w_o", nq, shape.d, k2),
+             ("gate_up", "w_gu", shape.d, 2 * shape.inter, k3), ("down", "w_down", shape.inter, shape.d, k4),
+             ("adapter", "adapter", shape.d, shape.d, shape.d)]
+    res = {}
+    stream = torch.cuda.current_stream()
+    for name, attr, din, dout, k in sites:
+        inputs = []
+        for r in range(8):
+            x = synth.residual_activation(1, din, seed=500 + r).to(device)
+            _, idx, vals, _ = LZ.rotate_topk(x, None, k)
+            inputs.append((idx, vals))
+        y = torch.empty((1, dout), dtype=torch.float32, device=device)
+        for i in range(5):
+            idx, vals = inputs[i % 8]
+            LZ.sparse_gemv(getattr(layers[i % len(layers)], attr), idx, vals, out=y)
+        torch.cuda.synchronize()
+        times = []
+        for i in range(reps):
+            idx, vals = inputs[i % 8]
+            w = getattr(layers[i % len(layers)], attr)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            LZ.sparse_gemv(w, idx, vals, out=y)
+            e1.record(stream)
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        us = float(np.mean([a.elapsed_time(b) * 1e3 for a, b in times]))
+        alg = k * dout * 2 + k * 8 + dout * 4
+        res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_out": dout}
+    return res
+
+
+def cublas_dense_us(layers, shape, device, reps=40):
+    """Dense bf16 GEMV baseline (cuBLAS via torch.matmul) on the same folded weights."""
+    nq = shape.hq * shape.hd
+    mats = [("w_qkv", shape.d), ("w_o", nq), ("w_gu", shape.d), ("w_down", shape.inter)]
+    tot = 0.0
+    per = {}
+    for attr, din in mats:
+        x = torch.randn((1, din), device=device, dtype=torch.bfloat16)
+        ws = [getattr(l, attr).view(torch.bfloat16) for l in layers]
+        for i in range(3):
+            torch.matmul(x, ws[i % len(ws)])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            torch.matmul(x, ws[i % len(ws)])
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        per[attr] = us
+        tot += us
+    return tot, per
+
+
+def capture_graphs(layers, stack_kv, resid, pos, plan, ws_buf):
+    from paper_2507_01299_b200 import larosa as LZ
+    graphs = []
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for w, (kc, vc) in zip(layers, stack_kv):     # warm-up outside capture
+            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos), ws=ws_buf)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for w, (kc, vc) in zip(layers, stack_kv):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos), ws=ws_buf)
+        graphs.append(g)
+    torch.cuda.synchronize()
+    return graphs
+
+
+def run_steps(graphs, k, start):
+    for i in range(k):
+        graphs[(start + i) % len(graphs)].replay()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--p", type=float, default=0.5)
+    ap.add_argument("--impl", default="larosa", choices=["larosa", "reference"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    ws_n, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = f"cuda:{local}"
+    if ws_n > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(device))
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+
+    shape = synth.MODELS["llama2-7b"]
+    layers = build_stack(shape, device, N_COPIES, seed=10 * rank)
+    kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
+           synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(N_COPIES)]
+    pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
+    ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
+    resid0 = synth.residual_activation(1, shape.d, seed=77 + rank).to(device)
+
+    def measure(p):
+        plan = M.site_plan(shape, p)
+        resid = resid0.clone()
+        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
+        run_steps(graphs, args.warmup, 0)
+        torch.cuda.synchronize()
+        if ws_n > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_steps(graphs, args.steps, args.warmup)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if ws_n > 1:
+            t = torch.tensor([ms], device=device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return plan, graphs, resid, ms
+
+    with ClockSampler(local) as clk:
+        plan, graphs, resid, ms = measure(args.p)
+    clocks = clk.summary()
+    ms_per_step = ms / args.steps
+    value = ws_n * args.steps / (ms / 1e3)           # tokens through the block, all ranks
+
+    # ---- end to end through the public API with host buffers (pinned H2D + D2H per step) --
+    h_in = torch.empty((1, shape.d), dtype=torch.float32).pin_memory()
+    h_in.copy_(resid0.cpu())
+    h_out = torch.empty((1, shape.d), dtype=torch.float32).pin_memory()
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        resid.copy_(h_in, non_blocking=True)
+        graphs[i % len(graphs)].replay()
+        h_out.copy_(resid, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if ws_n > 1:
+        t = torch.tensor([e2e_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": ws_n * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": shape.d * 4,
+           "d2h_bytes_per_step": shape.d * 4}
+
+    # ---- dominant kernel (sparse GEMV) roofline, CUDA events on the launching stream -------
+    gem = time_gemv_sites(layers, plan, shape, device)
+    sparse_sites = ["qkv", "o", "gate_up", "down"]
+    bytes_tot = sum(gem[s]["bytes"] for s in sparse_sites)
+    us_tot = sum(gem[s]["us"] for s in sparse_sites)
+    peaks, peak_kind = measured_peaks()
+    achieved = bytes_tot / us_tot / 1e3
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemv_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_step_sparse_gemv")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "kernel": "gemv_kernel (larosa_sparse_gemv), 4 sparse sites of one block summed",
+                "algorithmic_bytes": bytes_tot, "avg_us": us_tot, "peak_kind": f"{peak_kind} copy (hbm_gbs)",
+                "per_site": gem}
+
+    # ---- sparsity sweep (0-60%) and cuBLAS dense baseline ----------------------------------
+    sweep = None
+    if not args.no_sweep:
+        sweep = {}
+        for p in (0.0, 0.25, 0.4, 0.5, 0.6):
+            pl, _, _, msp = measure(p)
+            sweep[str(p)] = {"block_us": 1e3 * msp / args.steps, "tok_s": args.steps / (msp / 1e3),
+                             "plan": list(pl)}
+        dense_us, dense_per = cublas_dense_us(layers, shape, device)
+        sweep["cublas_dense_4gemv_us"] = dense_us
+        sweep["cublas_dense_per_gemv_us"] = dense_per
+
+    cpu = None
+    if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        op = O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter)
+        oracle_block_sample(shape, op, 1)
+        tok_s, dt, threads = oracle_block_sample(shape, op, 4)
+        cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": "4 decode tokens through one LLaMA2-7B block (fp64 numpy oracle), same p"}
+
+    launches_per_step = 10   # 4 Top-K + 5 GEMV + 1 attention per block at batch 1
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws_n, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
+               "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "plan_k": list(plan),
+                          "ctx": CTX, "batch": 1, "layer_copies": N_COPIES,
+                          "l2": "inputs larger than L2: 8 distinct layer copies (3.2 GB) cycled",
+                          "parallelism": f"replicas x{ws_n}" if ws_n > 1 else "single GPU",
+                          "implied_llama2_7b_32_layer_tok_s": value / ws_n / 32},
+               "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+               "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep}
+        print(json.dumps(out))
+    if ws_n > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,215 @@
+/* larosa.h — C ABI of the LaRoSA decode hot path on B200 (sm_100a).
+ *
+ * LaRoSA (arXiv 2507.01299, "Layerwise Rotated Sparse Activation"); PAPER.md line
+ * numbers are cited as P:n.  The method: each token's hidden vector x is rotated by
+ * a layerwise orthogonal Q_l, Top-K magnitude-sparsified with
+ * k = alpha (1 - p) D_in (eq. 2), and the kept entries drive a GEMV over the
+ * folded weights (W Q)^T that streams only the kept weight columns.
+ *
+ * Conventions:
+ *  - Every weight is stored as Wc = W_pt^T, row-major [d_in][ld] bf16 (raw uint16
+ *    bits), i.e. the paper's "column-major W" (P:414 (1)): kept input channel j is
+ *    the contiguous row Wc[j][0 .. d_out).  A projection is y = x . Wc.
+ *  - All pointers are DEVICE pointers unless marked (host).  All calls are
+ *    asynchronous on `stream` and CUDA-graph capturable: no allocation, no host sync,
+ *    no device-wide memset.  The caller owns every buffer.
+ *  - Workspaces: sized by the matching *_workspace_size() query, 256-byte aligned,
+ *    and ZERO-FILLED ONCE by the caller when allocated (kernels keep their tile
+ *    counters self-resetting so the zero state is restored after every call).  A
+ *    workspace may not be used by two calls that can run concurrently.
+ *  - Errors: arguments are validated synchronously and a status is returned; no
+ *    exception crosses the ABI.  Launch errors return LAROSA_ECUDA (from
+ *    cudaGetLastError).  Faults inside kernels surface at the caller's next sync.
+ *    larosa_last_error() gives a thread-local message for the last non-OK status.
+ *  - Preconditions not checked on the hot path: inputs finite,
+ *    per-token index lists ascending and unique.
+ *  - Determinism: every reduction runs in a fixed order (no floating-point atomics),
+ *    so results are bit-reproducible for a given shape and batch.
+ *  - Re-entrant; concurrent calls on different streams with different workspaces
+ *    are allowed.
+ */
+#ifndef LAROSA_H
+#define LAROSA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAROSA_ABI_VERSION 1
+#define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
+#define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
+#define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
+
+typedef struct CUstream_st* larosa_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    LAROSA_OK = 0,
+    LAROSA_EINVAL = 1,       /* null pointer, k > d, d <= 0, batch < 1, misaligned pointer   */
+    LAROSA_ESHAPE = 2,       /* inconsistent dimensions between arguments                     */
+    LAROSA_EUNSUPPORTED = 3, /* e.g. ld % 8 != 0 or d_out % 8 != 0 (16-byte rows), batch > 16 */
+    LAROSA_ECUDA = 4,        /* a CUDA runtime call or kernel launch failed                   */
+    LAROSA_ENCCL = 5,        /* reserved for collective errors (collectives are the caller's) */
+    LAROSA_EWORKSPACE = 6    /* workspace pointer NULL or smaller than the size query         */
+} larosa_status;
+
+int larosa_abi_version(void);
+const char* larosa_status_string(int status);
+/* Thread-local detail of the last non-OK status returned on this thread. */
+const char* larosa_last_error(void);
+
+/* ------------------------------------------------------------------------------
+ * Kept count (host, fp64).  k = alpha (1 - p) D_in.
+ * Rounded half away from zero and clamped to [0, d_in]; p == 0 is
+ * the dense "0%" configuration, k = d_in (Z16).  EINVAL if k_out is NULL, d_in <= 0,
+ * p outside [0, 1] or alpha < 0.
+ * ------------------------------------------------------------------------------ */
+larosa_status larosa_compute_k(double alpha, double p, int64_t d_in, int64_t* k_out /* host */);
+
+/* Sparsity-coefficient constraints (App. B):
+ *   alpha2 = 4 - 3 alpha1,  alpha4 = (2 + M - 2 alpha3) / M.
+ * EINVAL if m <= 0, a pointer is NULL or a resulting coefficient is <= 0. */
+larosa_status larosa_solve_alpha(double alpha1, double alpha3, double m,
+                                 double* alpha2 /* host */, double* alpha4 /* host */);
+
+/* ------------------------------------------------------------------------------
+ * Offline fold (eq. before_merge -> after_merge; §3.2).
+ *  side = LAROSA_LEFT_QT : Wout = Q^T diag(gamma) W.  W [rows = d][cols = d_out],
+ *      Q [d][d] fp32 row-major (Q[:, i] = i-th principal direction),
+ *      gamma [d] fp32 or NULL (RMSNorm gain folded into W's input rows).
+ *      Used for W_qkv (h1) and W_gate|up (h3).
+ *  side = LAROSA_RIGHT_Q : Wout = W Q.  W [rows = d_in][cols = d], Q [d][d]; gamma
+ *      must be NULL.  Used for W_o and W_down so the block output stays in Q_l's
+ *      basis (Z21).
+ *  The residual adapter A_l = Q_l^T Q_{l+1} is LEFT_QT with Q = Q_l and
+ *  W = Q_{l+1} rounded to bf16 (the runtime adapter is bf16 anyway).
+ *  W, Wout bf16 row-major with leading dimension `cols`; Wout must not alias W.
+ *  Arithmetic: Q (times gamma) is split into bf16 hi + lo parts, the products run on
+ *  the tcgen05 tensor cores with fp32 accumulation in TMEM, and Wout is rounded to
+ *  bf16 (RNE) once.  rows, cols must be multiples of 64 (EUNSUPPORTED otherwise).
+ * ------------------------------------------------------------------------------ */
+enum { LAROSA_LEFT_QT = 0, LAROSA_RIGHT_Q = 1 };
+size_t larosa_fold_workspace_size(int64_t rows, int64_t cols, int side);
+larosa_status larosa_fold_rotation(const float* Q, const float* gamma, const uint16_t* W,
+                                   uint16_t* Wout, int64_t rows, int64_t cols, int side,
+                                   void* ws, size_t ws_bytes, larosa_stream_t stream);
+
+/* Pack separate gate and up weights Wg, Wu [d][inter] into the fused layout the layer
+ * uses: Wgu [d][2*inter] with column block t of width 2*LAROSA_GU_BLOCK holding
+ * gate columns [t*B, t*B+B) followed by up columns [t*B, t*B+B) (B = LAROSA_GU_BLOCK),
+ * so one GEMV tile owns matching gate/up pairs for the SiLU(g)*u epilogue.
+ * inter must be a multiple of LAROSA_GU_BLOCK.  Works equally before or after the
+ * (left) fold, which acts on rows. */
+larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t* Wu, uint16_t* Wgu,
+                                  int64_t d, int64_t inter, larosa_stream_t stream);
+
+/* ------------------------------------------------------------------------------
+ * Rotate + Top-K  (RMS scale P:1444-1447).
+ * Per token b in [0, batch):
+ *   xr = x[b] . R            (R bf16 [d][d]; R == NULL -> identity, Top-K only:
+ *                             the h2/h4 sites use Q = I)
+ *   S  = the k largest |xr_i|; ties -> the lower index wins; exactly k
+ *        indices even if some values are 0 (Z11); idx[b][0..k) ascending.
+ *   vals[b][t] = xr[idx[b][t]] * s,  s = 1/sqrt(mean(xr^2) + rms_eps) if rms_eps >= 0
+ *        (RMSNorm with gains folded into the next weights: h1, h3), else s = 1.
+ *   Selection is taken on the unscaled xr (s > 0 cannot reorder).
+ * x fp32 [batch][d]; xr_out fp32 [batch][d] or NULL; idx int32 [batch][k];
+ * vals fp32 [batch][k]; mask uint32 [batch][ceil(d/32)] or NULL (bit i%32 of word
+ * i/32 set iff i kept).  xr_out may alias x only when R == NULL.
+ * Rotation: fp32 accumulation of bf16 R products in a fixed order.  Top-K: exact
+ * radix select on the uint32 keys bits(|xr|) (monotone for finite values).
+ * ------------------------------------------------------------------------------ */
+size_t larosa_rotate_topk_workspace_size(int32_t batch, int64_t d);
+larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, int32_t batch, int64_t d,
+                                 int64_t k, float rms_eps, float* xr_out, int32_t* idx,
+                                 float* vals, uint32_t* mask, void* ws, size_t ws_bytes,
+                                 larosa_stream_t stream);
+
+/* ------------------------------------------------------------------------------
+ * Sparse GEMV over kept columns (eq. after_merge; kernel recipe P:414).
+ *   y[b][o] = (bias ? bias[o] : 0) + sum_{t<k} vals[b][t] * W[idx[b][t]][o],
+ *   o in [0, d_out), b in [0, batch).
+ * W bf16 [d_in][ld]; idx int32 [batch][k] (ascending, unique, < d_in);
+ * vals fp32 [batch][k]; bias bf16 [d_out] or NULL; y fp32 [batch][d_out].
+ * batch > 1 streams the union U of the tokens' kept rows exactly once; a token
+ * contributes 0 on rows it did not keep (per-token results stay exact).
+ * Bytes moved ~ |U| * d_out * 2.  Requires ld % 8 == 0, d_out % 8 == 0 and a
+ * 16-byte aligned W (EUNSUPPORTED / EINVAL otherwise).  k == 0 gives y = bias.
+ * ------------------------------------------------------------------------------ */
+size_t larosa_sparse_gemv_workspace_size(int32_t batch, int64_t d_in, int64_t k, int64_t d_out);
+larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int64_t d_out, int64_t ld,
+                                 const int32_t* idx, const float* vals, int32_t batch, int64_t k,
+                                 const uint16_t* bias, float* y, void* ws, size_t ws_bytes,
+                                 larosa_stream_t stream);
+
+/* ------------------------------------------------------------------------------
+ * One LaRoSA decoder layer on pre-folded weights (Fig. 2; §8(a) a6):
+ *   r (residual, Q_l basis) -> h1: Top-K k_h1 of r, RMS scale -> sparse GEMV W_qkv
+ *   (+bias, RoPE, append k/v at pos) -> GQA decode attention -> h2: Top-K k_h2 ->
+ *   sparse GEMV W_o, r += -> h3: Top-K k_h3 of r, RMS scale -> sparse GEMV W_gate|up,
+ *   h4 = SiLU(g) * u -> Top-K k_h4 -> sparse GEMV W_down, r += ->
+ *   r <- r . A_l (dense adapter GEMV) unless adapter == NULL.
+ * Weights (all bf16, Wc layout):
+ *   w_qkv [d][(Hq + 2 Hkv) hd] = Q_l^T diag(gamma_attn) [Wq | Wk | Wv]
+ *   b_qkv [(Hq + 2 Hkv) hd] or NULL (Qwen2.5; unchanged by an input-side fold, Z28)
+ *   w_o [Hq hd][d] = Wo Q_l;  w_gu [d][2 inter] = packed Q_l^T diag(gamma_mlp) [Wg | Wu]
+ *   w_down [inter][d] = Wd Q_l;  adapter [d][d] = Q_l^T Q_{l+1} or NULL.
+ * Glue (not paper content): RoPE = HF rotate_half with pairs (i, i+hd/2),
+ * inv_freq = theta^(-2i/hd), angle = pos * inv_freq; q-head h reads kv-head
+ * floor(h Hkv / Hq); softmax scale 1/sqrt(hd) in fp32; KV cache bf16.
+ * State: resid fp32 [batch][d] in/out; k_cache, v_cache bf16 [batch][Hkv][max_ctx][hd];
+ * pos int32 [batch] (device): token b is written at position pos[b] and attends to
+ * [0, pos[b]]; requires pos[b] < max_ctx (not checked on device).
+ * Constraints: hd == 128 or 64 (hd % 16 == 0), Hq % Hkv == 0, d % 8 == 0,
+ * inter % LAROSA_GU_BLOCK == 0, Hq*hd and (Hq+2Hkv)*hd multiples of 8.
+ * Taps (optional, may be NULL; each member may be NULL): device buffers that receive
+ * the intermediates for parity checks.  Sharded use: pass this rank's
+ * output rows; collectives are issued by the caller between layers.
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+    const uint16_t* w_qkv;
+    const uint16_t* b_qkv;
+    const uint16_t* w_o;
+    const uint16_t* w_gu;
+    const uint16_t* w_down;
+    const uint16_t* adapter;
+    int64_t d, inter, n_q_heads, n_kv_heads, head_dim;
+    float rope_theta, rms_eps;
+} larosa_layer_weights;
+
+typedef struct {
+    int64_t k_h1, k_h2, k_h3, k_h4;
+} larosa_layer_plan;
+
+typedef struct {
+    float* resid;
+    uint16_t* k_cache;
+    uint16_t* v_cache;
+    const int32_t* pos;
+    int64_t max_ctx;
+    int32_t batch;
+} larosa_layer_state;
+
+typedef struct {
+    int32_t* idx_h1; float* vals_h1;   /* [batch][k_h1] */
+    float* q;                          /* [batch][Hq hd] after bias + RoPE            */
+    float* h2;                         /* [batch][Hq hd] attention output             */
+    int32_t* idx_h2; float* vals_h2;   /* [batch][k_h2]                               */
+    float* r_mid;                      /* [batch][d] residual after the O projection  */
+    int32_t* idx_h3; float* vals_h3;   /* [batch][k_h3]                               */
+    float* h4;                         /* [batch][inter] SiLU(g) * u                  */
+    int32_t* idx_h4; float* vals_h4;   /* [batch][k_h4]                               */
+    float* r_out;                      /* [batch][d] residual before the adapter      */
+} larosa_layer_taps;
+
+size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx);
+larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
+                                  const larosa_layer_state* state, const larosa_layer_taps* taps,
+                                  void* ws, size_t ws_bytes, larosa_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAROSA_H */

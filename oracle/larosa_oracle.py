@@ -369,7 +369,12 @@ def _split_qkv(y, hq, hkv, hd):
     return q, k, v
 
 
-def dense_block(r, w, cfg, k_cache, v_cache, pos: int):
+def _kv_store(x, kv_bf16: bool):
+    """Z27: the KV cache is stored in bf16 (RNE); kv_bf16=False keeps fp64 (pure math)."""
+    return bf16_to_f64(f64_to_bf16_rne(x)) if kv_bf16 else x
+
+
+def dense_block(r, w, cfg, k_cache, v_cache, pos: int, kv_bf16: bool = False):
     """The unrotated, unsparsified pre-norm decoder layer (P:1381 block structure):
     h1 = RMSNorm(r) -> QKV (+bias, RoPE) -> attention -> h2 -> O -> r += ;
     h3 = RMSNorm(r) -> gate|up -> h4 = SiLU(g) * u -> down -> r += .
@@ -383,8 +388,8 @@ def dense_block(r, w, cfg, k_cache, v_cache, pos: int):
     v = dense_gemv(w["wv"], h1, w.get("bv")).reshape(hkv, hd)
     q = np.stack([rope(q[h], pos, theta) for h in range(hq)])
     k = np.stack([rope(k[h], pos, theta) for h in range(hkv)])
-    k_cache[:, pos] = k
-    v_cache[:, pos] = v
+    k_cache[:, pos] = _kv_store(k, kv_bf16)
+    v_cache[:, pos] = _kv_store(v, kv_bf16)
     h2 = decode_attention(q, k_cache, v_cache, pos + 1)
     r = r + dense_gemv(w["wo"], h2)
     h3 = rmsnorm(r, w["gamma2"], eps)
@@ -393,7 +398,7 @@ def dense_block(r, w, cfg, k_cache, v_cache, pos: int):
     return r, {"h1": h1, "h2": h2, "h3": h3, "h4": h4, "q": q}
 
 
-def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None):
+def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf16: bool = False):
     """The LaRoSA layer on folded weights, step by step as Fig. 2 and
     eqs. before/after_merge (P:402-411):
 
@@ -416,8 +421,8 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None):
     q, k, v = _split_qkv(y, hq, hkv, hd)
     q = np.stack([rope(q[h], pos, theta) for h in range(hq)])
     k = np.stack([rope(k[h], pos, theta) for h in range(hkv)])
-    k_cache[:, pos] = k
-    v_cache[:, pos] = v
+    k_cache[:, pos] = _kv_store(k, kv_bf16)
+    v_cache[:, pos] = _kv_store(v, kv_bf16)
     h2 = decode_attention(q, k_cache, v_cache, pos + 1)
     s2 = topk(h2, k2)
     r = r + sparse_gemv(wf["wo"], s2, h2[s2])

@@ -1,0 +1,300 @@
+"""Thin Python binding of the C ABI in include/larosa.h (ctypes).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+``lib/liblarosa.so``.  PyTorch provides device memory and the current CUDA stream.
+There is no CPU fallback: if the library is missing, or a call is made on CPU
+tensors, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "liblarosa.so")
+
+LAROSA_LEFT_QT = 0
+LAROSA_RIGHT_Q = 1
+LAROSA_GU_BLOCK = 64
+LAROSA_MAX_BATCH = 16
+
+_c_i64 = ctypes.c_int64
+_c_i32 = ctypes.c_int32
+_vp = ctypes.c_void_p
+
+
+class LarosaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"status {status}: {msg}")
+        self.status = status
+
+
+class LayerWeightsC(ctypes.Structure):
+    _fields_ = [("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("w_gu", _vp), ("w_down", _vp),
+                ("adapter", _vp), ("d", _c_i64), ("inter", _c_i64), ("n_q_heads", _c_i64),
+                ("n_kv_heads", _c_i64), ("head_dim", _c_i64), ("rope_theta", ctypes.c_float),
+                ("rms_eps", ctypes.c_float)]
+
+
+class LayerPlanC(ctypes.Structure):
+    _fields_ = [("k_h1", _c_i64), ("k_h2", _c_i64), ("k_h3", _c_i64), ("k_h4", _c_i64)]
+
+
+class LayerStateC(ctypes.Structure):
+    _fields_ = [("resid", _vp), ("k_cache", _vp), ("v_cache", _vp), ("pos", _vp),
+                ("max_ctx", _c_i64), ("batch", _c_i32)]
+
+
+class LayerTapsC(ctypes.Structure):
+    _fields_ = [("idx_h1", _vp), ("vals_h1", _vp), ("q", _vp), ("h2", _vp), ("idx_h2", _vp),
+                ("vals_h2", _vp), ("r_mid", _vp), ("idx_h3", _vp), ("vals_h3", _vp), ("h4", _vp),
+                ("idx_h4", _vp), ("vals_h4", _vp), ("r_out", _vp)]
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree liblarosa.so (raises if it was not built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"liblarosa.so not built ({LIB_PATH}); run __graft_entry__.build() or `make`")
+    L = ctypes.CDLL(LIB_PATH)
+    L.larosa_abi_version.restype = ctypes.c_int
+    L.larosa_status_string.restype = ctypes.c_char_p
+    L.larosa_status_string.argtypes = [ctypes.c_int]
+    L.larosa_last_error.restype = ctypes.c_char_p
+    L.larosa_compute_k.argtypes = [ctypes.c_double, ctypes.c_double, _c_i64, ctypes.POINTER(_c_i64)]
+    L.larosa_solve_alpha.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    L.larosa_fold_workspace_size.restype = ctypes.c_size_t
+    L.larosa_fold_workspace_size.argtypes = [_c_i64, _c_i64, ctypes.c_int]
+    L.larosa_fold_rotation.argtypes = [_vp, _vp, _vp, _vp, _c_i64, _c_i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+    L.larosa_pack_gate_up.argtypes = [_vp, _vp, _vp, _c_i64, _c_i64, _vp]
+    L.larosa_rotate_topk_workspace_size.restype = ctypes.c_size_t
+    L.larosa_rotate_topk_workspace_size.argtypes = [_c_i32, _c_i64]
+    L.larosa_rotate_topk.argtypes = [_vp, _vp, _c_i32, _c_i64, _c_i64, ctypes.c_float, _vp, _vp, _vp, _vp, _vp,
+                                     ctypes.c_size_t, _vp]
+    L.larosa_sparse_gemv_workspace_size.restype = ctypes.c_size_t
+    L.larosa_sparse_gemv_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64, _c_i64]
+    L.larosa_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i32, _c_i64, _vp, _vp, _vp,
+                                     ctypes.c_size_t, _vp]
+    L.larosa_layer_workspace_size.restype = ctypes.c_size_t
+    L.larosa_layer_workspace_size.argtypes = [ctypes.POINTER(LayerWeightsC), _c_i32, _c_i64]
+    L.larosa_sparse_layer.argtypes = [ctypes.POINTER(LayerWeightsC), ctypes.POINTER(LayerPlanC),
+                                      ctypes.POINTER(LayerStateC), ctypes.POINTER(LayerTapsC), _vp,
+                                      ctypes.c_size_t, _vp]
+    for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
+                 "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_sparse_layer"):
+        getattr(L, name).restype = ctypes.c_int
+    if L.larosa_abi_version() != 1:
+        raise RuntimeError("liblarosa ABI version mismatch")
+    _LIB = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        L = lib()
+        raise LarosaError(status, f"{L.larosa_status_string(status).decode()} — {L.larosa_last_error().decode()}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("larosa: tensors must live on a CUDA device (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError("larosa: tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Workspace:
+    """A zero-initialised device byte buffer reused across calls (kernels keep its tile
+    counters self-resetting).  Not for concurrent calls."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = {}
+
+
+def _ws(tag: str, nbytes: int, device) -> torch.Tensor:
+    key = (tag, str(device))
+    if key not in _WS:
+        _WS[key] = Workspace()
+    return _WS[key].get(nbytes, device)
+
+
+# ------------------------------------------------------------------------------- host helpers
+def abi_version() -> int:
+    return lib().larosa_abi_version()
+
+
+def compute_k(alpha: float, p: float, d_in: int) -> int:
+    k = _c_i64(0)
+    _check(lib().larosa_compute_k(float(alpha), float(p), int(d_in), ctypes.byref(k)))
+    return k.value
+
+
+def solve_alpha(alpha1: float, alpha3: float, m: float):
+    a2, a4 = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().larosa_solve_alpha(float(alpha1), float(alpha3), float(m), ctypes.byref(a2), ctypes.byref(a4)))
+    return a2.value, a4.value
+
+
+# ------------------------------------------------------------------------------- device calls
+def fold_rotation(Q: torch.Tensor, W: torch.Tensor, side: int, gamma: Optional[torch.Tensor] = None,
+                  out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """LEFT_QT: Q^T diag(gamma) W; RIGHT_Q: W Q.  Q fp32 [d,d]; W bf16 bits (int16) [rows, cols]."""
+    assert Q.dtype == torch.float32 and W.dtype in (torch.int16, torch.bfloat16)
+    rows, cols = W.shape
+    out = out if out is not None else torch.empty((rows, cols), dtype=torch.int16, device=W.device)
+    L = lib()
+    nb = L.larosa_fold_workspace_size(rows, cols, side)
+    ws = _ws("fold", nb, W.device)
+    _check(L.larosa_fold_rotation(_ptr(Q), _ptr(gamma), _ptr(W), _ptr(out), rows, cols, side, _ptr(ws),
+                                  ws.numel(), _stream(stream)))
+    return out
+
+
+def pack_gate_up(Wg: torch.Tensor, Wu: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    d, inter = Wg.shape
+    out = out if out is not None else torch.empty((d, 2 * inter), dtype=torch.int16, device=Wg.device)
+    _check(lib().larosa_pack_gate_up(_ptr(Wg), _ptr(Wu), _ptr(out), d, inter, _stream(stream)))
+    return out
+
+
+def rotate_topk(x: torch.Tensor, R: Optional[torch.Tensor], k: int, rms_eps: float = -1.0,
+                want_xr: bool = False, want_mask: bool = False, stream=None):
+    """Returns (xr or None, idx [B,k] int32, vals [B,k] f32, mask [B,ceil(d/32)] int32 or None)."""
+    assert x.dtype == torch.float32 and x.dim() == 2
+    B, d = x.shape
+    dev = x.device
+    xr = torch.empty((B, d), dtype=torch.float32, device=dev) if want_xr else None
+    idx = torch.empty((B, k), dtype=torch.int32, device=dev)
+    vals = torch.empty((B, k), dtype=torch.float32, device=dev)
+    mask = torch.empty((B, (d + 31) // 32), dtype=torch.int32, device=dev) if want_mask else None
+    L = lib()
+    nb = L.larosa_rotate_topk_workspace_size(B, d)
+    ws = _ws("rotate_topk", nb, dev)
+    _check(L.larosa_rotate_topk(_ptr(x), _ptr(R), B, d, k, float(rms_eps), _ptr(xr), _ptr(idx), _ptr(vals),
+                                _ptr(mask), _ptr(ws), ws.numel(), _stream(stream)))
+    return xr, idx, vals, mask
+
+
+def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Optional[torch.Tensor] = None,
+                d_out: Optional[int] = None, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """y[b] = bias + sum_t vals[b,t] W[idx[b,t]]  (W: bf16 bits [d_in, ld])."""
+    d_in, ld = W.shape
+    d_out = ld if d_out is None else d_out
+    if idx.dim() == 1:
+        idx, vals = idx.unsqueeze(0), vals.unsqueeze(0)
+    B, k = idx.shape
+    dev = W.device
+    y = out if out is not None else torch.empty((B, d_out), dtype=torch.float32, device=dev)
+    L = lib()
+    nb = L.larosa_sparse_gemv_workspace_size(B, d_in, k, d_out)
+    ws = _ws("sparse_gemv", nb, dev)
+    _check(L.larosa_sparse_gemv(_ptr(W), d_in, d_out, ld, _ptr(idx) if k else None, _ptr(vals) if k else None,
+                                B, k, _ptr(bias), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)))
+    return y
+
+
+@dataclass
+class LayerWeights:
+    """Folded bf16 (int16-bit) weights of one decoder layer in the Wc layout."""
+    w_qkv: torch.Tensor
+    w_o: torch.Tensor
+    w_gu: torch.Tensor
+    w_down: torch.Tensor
+    d: int
+    inter: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    rope_theta: float
+    rms_eps: float
+    b_qkv: Optional[torch.Tensor] = None
+    adapter: Optional[torch.Tensor] = None
+
+    def c(self) -> LayerWeightsC:
+        return LayerWeightsC(_ptr(self.w_qkv), _ptr(self.b_qkv), _ptr(self.w_o), _ptr(self.w_gu), _ptr(self.w_down),
+                             _ptr(self.adapter), self.d, self.inter, self.n_q_heads, self.n_kv_heads, self.head_dim,
+                             float(self.rope_theta), float(self.rms_eps))
+
+
+@dataclass
+class LayerState:
+    resid: torch.Tensor      # fp32 [B, d]
+    k_cache: torch.Tensor    # int16 [B, Hkv, max_ctx, hd]
+    v_cache: torch.Tensor
+    pos: torch.Tensor        # int32 [B] on device
+
+    def c(self) -> LayerStateC:
+        B = self.resid.shape[0]
+        return LayerStateC(_ptr(self.resid), _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.pos),
+                           self.k_cache.shape[2], B)
+
+
+TAP_NAMES = [f[0] for f in LayerTapsC._fields_]
+
+
+def make_taps(w: LayerWeights, plan: Sequence[int], batch: int, device) -> dict:
+    k1, k2, k3, k4 = plan
+    nq = w.n_q_heads * w.head_dim
+    f32 = dict(dtype=torch.float32, device=device)
+    i32 = dict(dtype=torch.int32, device=device)
+    return {
+        "idx_h1": torch.empty((batch, k1), **i32), "vals_h1": torch.empty((batch, k1), **f32),
+        "q": torch.empty((batch, nq), **f32), "h2": torch.empty((batch, nq), **f32),
+        "idx_h2": torch.empty((batch, k2), **i32), "vals_h2": torch.empty((batch, k2), **f32),
+        "r_mid": torch.empty((batch, w.d), **f32),
+        "idx_h3": torch.empty((batch, k3), **i32), "vals_h3": torch.empty((batch, k3), **f32),
+        "h4": torch.empty((batch, w.inter), **f32),
+        "idx_h4": torch.empty((batch, k4), **i32), "vals_h4": torch.empty((batch, k4), **f32),
+        "r_out": torch.empty((batch, w.d), **f32),
+    }
+
+
+def layer_workspace_size(w: LayerWeights, batch: int, max_ctx: int) -> int:
+    wc = w.c()
+    return lib().larosa_layer_workspace_size(ctypes.byref(wc), batch, max_ctx)
+
+
+def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: Optional[dict] = None,
+                 ws: Optional[torch.Tensor] = None, stream=None):
+    """One LaRoSA decoder layer in place on ``state`` (resid, KV cache)."""
+    L = lib()
+    wc = w.c()
+    pc = LayerPlanC(*[int(k) for k in plan])
+    sc = state.c()
+    B = state.resid.shape[0]
+    nb = L.larosa_layer_workspace_size(ctypes.byref(wc), B, state.k_cache.shape[2])
+    if ws is None:
+        ws = _ws("layer", nb, state.resid.device)
+    elif ws.numel() < nb:
+        raise ValueError("sparse_layer: workspace too small")
+    tc = None
+    if taps is not None:
+        tc = LayerTapsC(*[_ptr(taps.get(n)) for n in TAP_NAMES])
+    _check(L.larosa_sparse_layer(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sc),
+                                 ctypes.byref(tc) if tc is not None else None, _ptr(ws), ws.numel(),
+                                 _stream(stream)))

@@ -1,0 +1,104 @@
+"""Model assembly for the LaRoSA decode path: synthetic random-init layers of the paper's
+model shapes, folded with the library's own fold (SURVEY §3.1 offline transform), and a
+multi-layer decode stack driven through ``larosa_sparse_layer``.
+
+Everything computed here runs in liblarosa kernels; torch only allocates, draws the
+seeded random weights (synth) and moves tensors.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+import synth
+from . import larosa as LZ
+
+
+@dataclass
+class OriginalLayer:
+    """Unrotated layer weights, Wc layout ([d_in][d_out]) bf16 bits (int16)."""
+    wqkv: torch.Tensor     # [d][(hq + 2 hkv) hd]  = [Wq | Wk | Wv]
+    wo: torch.Tensor       # [hq hd][d]
+    wg: torch.Tensor       # [d][inter]
+    wu: torch.Tensor       # [d][inter]
+    wd: torch.Tensor       # [inter][d]
+    gamma1: torch.Tensor   # fp32 [d]  attention RMSNorm gain
+    gamma2: torch.Tensor   # fp32 [d]  MLP RMSNorm gain
+    bqkv: Optional[torch.Tensor] = None   # bf16 bits [(hq + 2 hkv) hd]
+
+
+def synth_original_layer(shape: synth.ModelShape, seed: int, device="cpu") -> OriginalLayer:
+    """W ~ N(0, 1/D_in) -> bf16, gains 1 + N(0, 0.1^2), QKV bias N(0, 0.02^2)."""
+    d, inter, nq = shape.d, shape.inter, shape.hq * shape.hd
+    s = 1000 * seed
+    return OriginalLayer(
+        wqkv=synth.gaussian_bf16((d, shape.qkv_out), s + 1, d ** -0.5, device),
+        wo=synth.gaussian_bf16((nq, d), s + 2, nq ** -0.5, device),
+        wg=synth.gaussian_bf16((d, inter), s + 3, d ** -0.5, device),
+        wu=synth.gaussian_bf16((d, inter), s + 4, d ** -0.5, device),
+        wd=synth.gaussian_bf16((inter, d), s + 5, inter ** -0.5, device),
+        gamma1=1.0 + 0.1 * synth.gaussian((d,), s + 6, device=device),
+        gamma2=1.0 + 0.1 * synth.gaussian((d,), s + 7, device=device),
+        bqkv=synth.gaussian_bf16((shape.qkv_out,), s + 8, 0.02, device) if shape.qkv_bias else None,
+    )
+
+
+def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
+               q_next: Optional[torch.Tensor]) -> LZ.LayerWeights:
+    """Offline transform of one layer (eqs. before/after_merge P:402-410, §3.2):
+    W_qkv' = Q_l^T diag(g1) W_qkv;  W_o' = W_o Q_l;  W_gate|up' = Q_l^T diag(g2) [Wg | Wu]
+    (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1}.   q_l, q_next: fp32 on device."""
+    dev = orig.wqkv.device
+    L, R = LZ.LAROSA_LEFT_QT, LZ.LAROSA_RIGHT_Q
+    g1 = orig.gamma1.to(dev, torch.float32).contiguous()
+    g2 = orig.gamma2.to(dev, torch.float32).contiguous()
+    w_qkv = LZ.fold_rotation(q_l, orig.wqkv, L, gamma=g1)
+    w_o = LZ.fold_rotation(q_l, orig.wo, R)
+    wg = LZ.fold_rotation(q_l, orig.wg, L, gamma=g2)
+    wu = LZ.fold_rotation(q_l, orig.wu, L, gamma=g2)
+    w_gu = LZ.pack_gate_up(wg, wu)
+    del wg, wu
+    w_down = LZ.fold_rotation(q_l, orig.wd, R)
+    adapter = None
+    if q_next is not None:
+        adapter = LZ.fold_rotation(q_l, synth.bf16_bits(q_next).contiguous(), L)
+    return LZ.LayerWeights(w_qkv=w_qkv, w_o=w_o, w_gu=w_gu, w_down=w_down, d=shape.d, inter=shape.inter,
+                           n_q_heads=shape.hq, n_kv_heads=shape.hkv, head_dim=shape.hd,
+                           rope_theta=shape.rope_theta, rms_eps=shape.rms_eps,
+                           b_qkv=orig.bqkv.contiguous() if orig.bqkv is not None else None, adapter=adapter)
+
+
+def site_plan(shape: synth.ModelShape, p: float, alpha_mode: str = "uniform") -> tuple:
+    """Per-site kept counts (k_h1, k_h2, k_h3, k_h4) via larosa_compute_k with
+    uniform alpha or the paper's App. B coefficients (alpha2/alpha4 from the constraints)."""
+    if alpha_mode == "uniform":
+        a = (1.0, 1.0, 1.0, 1.0)
+    else:
+        a1, a3 = synth.PAPER_ALPHA[shape.name]
+        a2, a4 = LZ.solve_alpha(a1, a3, shape.inter / shape.d)
+        a = (a1, a2, a3, a4)
+    nq = shape.hq * shape.hd
+    return (LZ.compute_k(a[0], p, shape.d), LZ.compute_k(a[1], p, nq), LZ.compute_k(a[2], p, shape.d),
+            LZ.compute_k(a[3], p, shape.inter))
+
+
+class DecodeStack:
+    """A stack of folded LaRoSA layers sharing one workspace; ``step`` runs one decode
+    token (batch B) through all layers with larosa_sparse_layer."""
+
+    def __init__(self, layers: List[LZ.LayerWeights], batch: int, max_ctx: int, device):
+        self.layers = layers
+        self.batch = batch
+        self.max_ctx = max_ctx
+        w0 = layers[0]
+        self.ws = torch.zeros(LZ.layer_workspace_size(w0, batch, max_ctx), dtype=torch.uint8, device=device)
+        self.kv = [(torch.zeros((batch, w.n_kv_heads, max_ctx, w.head_dim), dtype=torch.int16, device=device),
+                    torch.zeros((batch, w.n_kv_heads, max_ctx, w.head_dim), dtype=torch.int16, device=device))
+                   for w in layers]
+
+    def step(self, resid: torch.Tensor, pos: torch.Tensor, plan: Sequence[int], stream=None):
+        for w, (kc, vc) in zip(self.layers, self.kv):
+            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos), ws=self.ws, stream=stream)
+        return resid

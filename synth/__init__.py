@@ -78,12 +78,12 @@ def gaussian_bf16(shape, seed: int, std: float, device: str = "cpu") -> torch.Te
     return bf16_bits(gaussian(shape, seed, std, device=device))
 
 
-def haar_orthogonal(d: int, seed: int) -> torch.Tensor:
-    """A Haar-random orthogonal matrix (fp64 QR of a Gaussian, R-diagonal sign fixed).
+def haar_orthogonal(d: int, seed: int, device: str = "cpu", dtype=torch.float64) -> torch.Tensor:
+    """A Haar-random orthogonal matrix (QR of a Gaussian, R-diagonal sign fixed).
     Stands in for a PCA rotation at model size (Q is an input there)."""
-    a = torch.randn((d, d), generator=gen(seed), dtype=torch.float64)
+    a = torch.randn((d, d), generator=gen(seed, device), dtype=dtype, device=device)
     q, r = torch.linalg.qr(a)
-    return q * torch.sign(torch.diagonal(r)).unsqueeze(0)
+    return (q * torch.sign(torch.diagonal(r)).unsqueeze(0)).contiguous()
 
 
 def residual_activation(batch: int, d: int, seed: int, outlier_frac: float = 0.005,

@@ -1,0 +1,207 @@
+"""GPU parity of the C-ABI calls against the fp64 oracle (SURVEY §8(c) protocol P1-P5).
+
+P1  Top-K selection: the oracle's Top-K on the GPU-exported vector -> identical index lists.
+P2  Rotation: GPU x~ vs oracle x R on the same bf16 R: max|dx| / ||x~|| <= 1e-5.
+P3  Sparse GEMV: oracle GEMV on the GPU's idx/vals/W bits: max|dy| / ||y|| <= 1e-3
+    (BASELINE north_star tolerance; fp32 accumulation gives ~1e-6).
+P4  Fold: GPU W' bits vs RNE_bf16(oracle fp64 fold): >= 99% identical, rest within 1 ulp.
+P5  Independent chain: oracle computes x~ itself; index sets equal except certified
+    near-ties (|x~_i| - |x~_j| within 2 * the observed rotation error).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from paper_2507_01299_b200 import larosa as LZ
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TOL_Y = 1e-3   # max |dy| / ||y||_2  (north_star)
+
+
+def f64(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def w64(bits):
+    return O.bf16_to_f64(bits.detach().cpu().numpy().view(np.uint16))
+
+
+def rel_max(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.linalg.norm(ref), 1e-300))
+
+
+# ------------------------------------------------------------------------------------ Top-K
+@pytest.mark.parametrize("d,k", [(64, 32), (64, 0), (64, 64), (1000, 1), (1000, 999), (4096, 2048), (4096, 1638),
+                                 (11008, 5504), (14336, 8602), (29568, 14784), (3584, 1434)])
+def test_topk_p1_exact(d, k):
+    x = synth.residual_activation(3, d, seed=d + k)
+    xr, idx, vals, mask = LZ.rotate_topk(x.to(DEV), None, k, rms_eps=1e-5, want_xr=True, want_mask=True)
+    torch.cuda.synchronize()
+    assert torch.equal(xr.cpu(), x)
+    for b in range(3):
+        xb = x[b].numpy().astype(np.float64)
+        ref = O.topk(xb, k)
+        assert np.array_equal(idx[b].cpu().numpy(), ref)
+        s = O.rms_scale(xb, 1e-5)
+        assert np.allclose(f64(vals[b]), xb[ref] * s, rtol=2e-6, atol=0)
+        assert np.array_equal(mask[b].cpu().numpy().view(np.uint32), O.topk_mask(ref, d))
+
+
+def test_topk_p1_ties_zeros_and_negative_zero():
+    """Integer-valued vectors: many exact |x| ties across the k-th position, zeros and -0.
+    The GPU must take the lower indices (Z10) and count zeros (Z11)."""
+    g = torch.Generator().manual_seed(3)
+    for trial, d in enumerate([37, 64, 257, 4096, 11008]):
+        x = torch.randint(-4, 5, (4, d), generator=g).float()
+        x[x == 0] = -0.0 if trial % 2 else 0.0
+        for k in (1, d // 3, d // 2, d - 1):
+            _, idx, vals, _ = LZ.rotate_topk(x.to(DEV), None, k)
+            for b in range(4):
+                ref = O.topk(x[b].numpy().astype(np.float64), k)
+                assert np.array_equal(idx[b].cpu().numpy(), ref), (d, k, b)
+                assert np.array_equal(vals[b].cpu().numpy(), x[b].numpy()[ref])
+
+
+def test_topk_p1_all_equal_and_constant():
+    for d in (64, 4096):
+        x = torch.full((2, d), 0.5)
+        _, idx, _, _ = LZ.rotate_topk(x.to(DEV), None, d // 4)
+        assert np.array_equal(idx[0].cpu().numpy(), np.arange(d // 4))
+
+
+# ------------------------------------------------------------------------------------ rotate
+@pytest.mark.parametrize("d,k,batch", [(64, 32, 1), (256, 100, 3), (4096, 2048, 1), (4096, 2458, 4)])
+def test_rotate_topk_p2_p1_p5(d, k, batch):
+    q = synth.haar_orthogonal(d, seed=d)
+    rb = synth.bf16_bits(q.float())
+    x = synth.residual_activation(batch, d, seed=7 + d)
+    xr, idx, vals, _ = LZ.rotate_topk(x.to(DEV), rb.to(DEV), k, rms_eps=1e-5, want_xr=True)
+    torch.cuda.synchronize()
+    r64 = w64(rb)
+    for b in range(batch):
+        ref_xr = O.rotate(x[b].numpy().astype(np.float64), r64)
+        g = f64(xr[b])
+        err = np.abs(g - ref_xr)
+        assert err.max() / np.linalg.norm(ref_xr) <= 1e-5                    # P2
+        assert np.array_equal(idx[b].cpu().numpy(), O.topk(g, k))              # P1
+        s = O.rms_scale(g, 1e-5)
+        ref_idx = O.topk(ref_xr, k)                                            # P5
+        gi = set(idx[b].cpu().numpy().tolist())
+        ri = set(ref_idx.tolist())
+        for i in gi ^ ri:
+            # a swap is only allowed between near-tied magnitudes
+            thr = np.sort(np.abs(ref_xr))[::-1][k - 1]
+            assert abs(abs(ref_xr[i]) - thr) <= 2 * err.max() + 1e-12
+        assert np.allclose(f64(vals[b]), g[idx[b].cpu().numpy()] * s, rtol=2e-6)
+
+
+# ------------------------------------------------------------------------------------ GEMV
+GEMV_CASES = [
+    # d_in, d_out, k, batch, bias
+    (64, 128, 32, 1, False),        # toy C1
+    (64, 128, 0, 1, True),          # k = 0 -> bias only
+    (64, 128, 64, 1, False),        # k = d (dense)
+    (4096, 4096, 2048, 1, False),   # LLaMA2-7B W_o at 50%
+    (4096, 12288, 2048, 1, True),   # W_qkv (+bias)
+    (4096, 22016, 2048, 1, False),  # W_gate|up
+    (11008, 4096, 5504, 1, False),  # W_down
+    (1000, 1000, 333, 1, False),    # ragged: d_out not a tile multiple, odd k
+    (4096, 4096, 2048, 2, False),   # batch union
+    (4096, 4104, 1500, 3, True),    # batch 3, ragged d_out
+    (4096, 4096, 1638, 8, False),
+    (4096, 12288, 2458, 16, False),
+]
+
+
+@pytest.mark.parametrize("d_in,d_out,k,batch,bias", GEMV_CASES)
+def test_sparse_gemv_p3(d_in, d_out, k, batch, bias):
+    W = synth.gaussian_bf16((d_in, d_out), seed=d_in * 7 + d_out, std=d_in ** -0.5)
+    x = synth.residual_activation(batch, d_in, seed=k + batch)
+    idx = torch.stack([torch.from_numpy(O.topk(x[b].numpy().astype(np.float64), k)) for b in range(batch)]).int()
+    vals = torch.gather(x, 1, idx.long()).contiguous() if k else torch.zeros((batch, 0))
+    bb = synth.gaussian_bf16((d_out,), seed=5, std=0.02) if bias else None
+    y = LZ.sparse_gemv(W.to(DEV), idx.to(DEV), vals.to(DEV), bias=bb.to(DEV) if bias else None)
+    torch.cuda.synchronize()
+    W64 = w64(W)
+    for b in range(batch):
+        ref = O.sparse_gemv(W64, idx[b].numpy(), vals[b].numpy(), w64(bb) if bias else None)
+        if k == 0 and not bias:
+            assert np.all(f64(y[b]) == 0)
+            continue
+        assert rel_max(f64(y[b]), ref) <= TOL_Y
+        assert rel_max(f64(y[b]), ref) <= 1e-5     # what fp32 accumulation actually gives
+
+
+def test_sparse_gemv_k_equals_d_is_dense_and_deterministic():
+    """p = 0 (k = D) reproduces the dense GEMV (P:163 '0%' rows); repeated calls are
+    bit-identical (fixed-order split reduction)."""
+    d = 4096
+    W = synth.gaussian_bf16((d, d), seed=1, std=d ** -0.5).to(DEV)
+    x = synth.residual_activation(1, d, seed=2).to(DEV)
+    idx = torch.arange(d, dtype=torch.int32, device=DEV).unsqueeze(0)
+    y1 = LZ.sparse_gemv(W, idx, x)
+    y2 = LZ.sparse_gemv(W, idx, x)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    ref = O.dense_gemv(w64(W.cpu()), f64(x[0]))
+    assert rel_max(f64(y1[0]), ref) <= 1e-5
+
+
+def test_sparse_gemv_theorem_a1_statistics():
+    """P7: Gaussian x~ and W~ at D = 4096: the GPU sparse output's relative error vs the
+    dense output matches Theorem A.1 within 2% (ratio of RMS norms)."""
+    d, dout, n = 4096, 1024, 128
+    W = synth.gaussian_bf16((d, dout), seed=11, std=1.0).to(DEV)
+    x = synth.gaussian((n, d), seed=12)
+    full = torch.arange(d, dtype=torch.int32).expand(n, d).contiguous()
+    for keep in (0.5, 0.75):
+        k = int(keep * d)
+        idx = torch.stack([torch.from_numpy(O.topk(x[i].numpy().astype(np.float64), k)) for i in range(n)]).int()
+        vals = torch.gather(x, 1, idx.long()).contiguous()
+        num = den = 0.0
+        for i in range(0, n, 16):
+            ys = LZ.sparse_gemv(W, idx[i:i + 16].to(DEV), vals[i:i + 16].to(DEV))
+            yd = LZ.sparse_gemv(W, full[i:i + 16].to(DEV), x[i:i + 16].contiguous().to(DEV))
+            num += float(((yd - ys) ** 2).sum())
+            den += float((yd ** 2).sum())
+        th = O.theory_relative_error(k, d)
+        assert abs((num / den) ** 0.5 - th) / th < 0.02
+
+
+# ------------------------------------------------------------------------------------ fold
+@pytest.mark.parametrize("d,cols,side", [(64, 128, 0), (256, 512, 0), (256, 192, 1), (1024, 1024, 0),
+                                         (1024, 2048, 1), (4096, 4096, 0)])
+def test_fold_p4(d, cols, side):
+    q = synth.haar_orthogonal(d, seed=d + side)
+    gamma = (1 + 0.1 * synth.gaussian((d,), seed=3)) if side == 0 else None
+    if side == 0:
+        W = synth.gaussian_bf16((d, cols), seed=4, std=d ** -0.5)
+    else:
+        W = synth.gaussian_bf16((cols, d), seed=4, std=d ** -0.5)
+    qf = q.float()
+    out = LZ.fold_rotation(qf.to(DEV), W.to(DEV), side, gamma=gamma.to(DEV) if gamma is not None else None)
+    torch.cuda.synchronize()
+    q64 = qf.numpy().astype(np.float64)      # the fp32 Q the GPU consumed, widened exactly
+    if side == 0:
+        ref = O.fold_left_qt(q64, w64(W), gamma.numpy().astype(np.float64))
+    else:
+        ref = O.fold_right_q(w64(W), q64)
+    ref_bits = O.f64_to_bf16_rne(ref).view(np.int16)
+    got = out.cpu().numpy()
+    same = np.mean(got == ref_bits)
+    assert same >= 0.99, same
+    # the rest: within one bf16 ulp of the exact value, or (outputs near zero, where the
+    # ulp is tiny) within the fp32-accumulation floor: a K-term fp32 sum carries an error of
+    # ~2^-24 sqrt(K/2) rms (1e-6 rms at K = 4096); 2^-14 rms bounds its maximum over 16M
+    # outputs and is still 64x finer than the bf16 quantum at the rms level
+    gv = O.bf16_to_f64(got.view(np.uint16))
+    _, e = np.frexp(ref)
+    ulp = np.ldexp(1.0, np.maximum(e - 8, -133))
+    floor = 2.0 ** -14 * np.sqrt(np.mean(ref * ref))
+    assert np.all(np.abs(gv - ref) <= np.maximum(ulp, floor))
+    # invariance (P4): (x Q^T-side) through the folded weight reproduces the original map
+    x = np.random.default_rng(0).standard_normal(ref.shape[0])
+    assert np.linalg.norm(x @ gv - x @ ref) <= 3e-3 * np.linalg.norm(x @ ref)
