@@ -179,7 +179,7 @@ def build_stack(shape, device, n_copies, seed=0):
     return layers
 
 
-def time_gemv_sites(layers, plan, shape, device, reps=40):
+def time_gemv_sites(layers, plan, shape, device, reps=64):
     """Average duration of the standalone sparse GEMV (larosa_sparse_gemv) per site, with
     CUDA events on the launching stream, cycling layer copies and fresh Top-K inputs."""
     from paper_2507_01299_b200 import larosa as LZ
@@ -201,17 +201,22 @@ def time_gemv_sites(layers, plan, shape, device, reps=40):
             idx, vals = inputs[i % 8]
             LZ.sparse_gemv(getattr(layers[i % len(layers)], attr), idx, vals, out=y)
         torch.cuda.synchronize()
-        times = []
-        for i in range(reps):
-            idx, vals = inputs[i % 8]
-            w = getattr(layers[i % len(layers)], attr)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            LZ.sparse_gemv(w, idx, vals, out=y)
-            e1.record(stream)
-            times.append((e0, e1))
+        # back-to-back launches captured in a CUDA graph (no host launch gaps), cycling the
+        # layer copies (weights >> L2) and 8 different kept-row sets
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(reps):
+                idx, vals = inputs[i % 8]
+                LZ.sparse_gemv(getattr(layers[i % len(layers)], attr), idx, vals, out=y)
+        g.replay()
         torch.cuda.synchronize()
-        us = float(np.mean([a.elapsed_time(b) * 1e3 for a, b in times]))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
         alg = k * dout * 2 + k * 8 + dout * 4
         res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_out": dout}
     return res

@@ -144,6 +144,12 @@ larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int64_t d_out,
                                  const uint16_t* bias, float* y, void* ws, size_t ws_bytes,
                                  larosa_stream_t stream);
 
+/* Introspection (host): the launch plan larosa_sparse_gemv uses for this shape.
+ * info (host, 8 ints) = {tile columns TN, cluster size CS, row groups RG, warps per CTA,
+ * ring stages per warp, column tiles, dynamic smem bytes, max co-resident clusters
+ * (cudaOccupancyMaxActiveClusters on the current device; 0 if unavailable)}. */
+larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info);
+
 /* ------------------------------------------------------------------------------
  * One LaRoSA decoder layer on pre-folded weights (Fig. 2; §8(a) a6):
  *   r (residual, Q_l basis) -> h1: Top-K k_h1 of r, RMS scale -> sparse GEMV W_qkv

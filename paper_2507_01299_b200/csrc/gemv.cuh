@@ -4,15 +4,25 @@
 //
 //   y[b][o] = sum_{r < nrows} val(r, b) * W[row(r)][o]      (+ epilogue)
 //
-// Work decomposition: the output columns are cut into tiles of TN = 256*NCW columns and
-// the kept-row list into `n_splits` contiguous chunks; CTA (tile, split) streams
-// rows[chunk] x [tile] of W.  Each kept row segment (TN*2 bytes, contiguous because W is
-// stored [d_in][d_out]) is fetched by ONE cp.async.bulk (TMA engine) into a 6-stage shared
-// memory ring guarded by mbarriers; a single producer lane issues the copies (L2
-// evict-first) and NCW consumer warps do fp32 FMAs on the bf16 weights (8 columns per
-// thread, 16-byte shared loads).  Splits are combined deterministically: every CTA writes
-// its fp32 partial tile, and the last CTA of a tile (atomic ticket) sums the partials in
-// split order and runs the epilogue.  No floating-point atomics anywhere.
+// Decomposition (B200: 148 SMs, 227 KB smem, thread-block clusters with DSMEM):
+//  * output columns are cut into tiles of TN (a multiple of 256); the kept-row list into CS
+//    contiguous chunks; the CS CTAs of one tile form a thread-block CLUSTER (CS <= 16), one
+//    CTA per SM with a ~200 KB shared-memory staging ring;
+//  * inside a CTA, warp (cs, rg) owns the 256-column slice cs of the tile and every RG-th
+//    kept row of the CTA's chunk.  Each kept row's 512-byte segment (contiguous in the
+//    [d_in][d_out] layout) is one coalesced warp-wide cp.async (LDGSTS, 16 B per lane) into
+//    the warp's private ring of 4-row stages, up to 16 stages deep.  A lane later reads back
+//    exactly the 16 bytes it copied, so the pipeline needs no barrier, only the lane's own
+//    cp.async groups.  (Measured on B200: the TMA engine retires about one bulk copy per
+//    ~50 cycles per SM, so 0.5-2 KB gathered row segments cap cp.async.bulk at 15-38 GB/s
+//    per SM, below the 44 GB/s/SM that 6.5 TB/s needs; per-thread cp.async has no such cap.)
+//  * fp32 FMAs on the bf16 weights (8 columns per lane); the kept rows' token values come
+//    from a 32-row register window broadcast with shfl;
+//  * the split-K reduction is deterministic and never touches global memory: each CTA
+//    reduces its RG row groups in shared memory, a cluster barrier, then CTA q sums its
+//    share of column PAIRS over the CS CTAs in fixed order through distributed shared
+//    memory (ld.shared::cluster) and runs the epilogue on complete values (pairs
+//    (c, c + po) keep RoPE halves and gate/up blocks together).
 #pragma once
 #include "common.cuh"
 
@@ -20,9 +30,11 @@ namespace larosa {
 
 enum EpKind : int { EP_STORE = 0, EP_RESID = 1, EP_SILU_GU = 2, EP_QKV_ROPE = 3 };
 
-constexpr int kGemvStages = 6;
-constexpr int kGemvStageBytes = 16384;
-constexpr int kGuBlock = 64;   // == LAROSA_GU_BLOCK
+constexpr int kGuBlock = 64;         // == LAROSA_GU_BLOCK
+constexpr int kWarpCols = 256;       // columns per warp slice (8 per lane)
+constexpr int kStageRows = 4;        // rows per stage per warp (one 512-byte copy each)
+constexpr int kStageBytes = kStageRows * kWarpCols * 2;
+constexpr int kGemvMaxWarps = 16;
 
 struct GemvArgs {
     const uint16_t* W;
@@ -34,9 +46,7 @@ struct GemvArgs {
     int nrows;             // row count when nrows_dev == nullptr
     const int* nrows_dev;  // device row count (batch > 1 union), or nullptr
     int batch;             // real tokens (<= template BP)
-    int n_splits;
-    float* partial;        // [n_splits][BP][d_out]
-    unsigned* counters;    // [n_tiles], zero on entry, restored to zero on exit
+    int tn, rg, stages;    // tile width, row groups, ring depth (stages per warp)
     // epilogue
     int ep;
     const uint16_t* bias;  // [d_out] bf16 or nullptr
@@ -53,266 +63,264 @@ struct GemvArgs {
     int64_t max_ctx;
 };
 
-__host__ __device__ constexpr size_t gemv_smem_bytes(int bp, int ncw) {
-    return 128 + (size_t)kGemvStages * kGemvStageBytes + (size_t)bp * ncw * 256 * sizeof(float);
+__host__ __device__ constexpr size_t gemv_ring_bytes(int nwarps, int stages) {
+    return (size_t)nwarps * stages * kStageBytes;
 }
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+// tail scratch (aliases the ring): part [RG][BP][TN] + pred [BP][TN] + fin [TN][BP]
+__host__ __device__ constexpr size_t gemv_tail_bytes(int rg, int bp, int tn) {
+    return ((size_t)rg * bp * tn + 2 * (size_t)bp * tn) * 4;
+}
+__host__ __device__ constexpr size_t gemv_smem_bytes(int nwarps, int stages, int rg, int bp, int tn) {
+    return 1024 + (gemv_ring_bytes(nwarps, stages) > gemv_tail_bytes(rg, bp, tn) ? gemv_ring_bytes(nwarps, stages)
+                                                                                   : gemv_tail_bytes(rg, bp, tn));
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
-template <int BP, int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32) gemv_kernel(const GemvArgs a) {
-    constexpr int TN = NCW * 256;                 // columns per tile
-    constexpr int G = kGemvStageBytes / (TN * 2); // rows per stage
-    constexpr int NC = NCW * 32;                  // consumer threads
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + kGemvStages;
-    int* s_flag = reinterpret_cast<int*>(empty + kGemvStages);
-    unsigned char* wbuf = smem + 128;
-    float* ytile = reinterpret_cast<float*>(wbuf + kGemvStages * kGemvStageBytes);   // [BP][TN]
-
-    const int tile = blockIdx.x, split = blockIdx.y;
-    const int col0 = tile * TN;
-    const int ncols = min(TN, a.d_out - col0);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kGemvStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
-        }
-        fence_mbar_init();
+// cp.async (LDGSTS): 16 bytes global -> shared, bypassing L1 (.cg)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+constexpr int kMaxStagesM1 = 15;   // ring depth <= 16
+// wait until at most n of this thread's most recent groups are pending (n runtime <= MAXN)
+template <int MAXN>
+__device__ __forceinline__ void cp_async_wait(int n) {
+    if constexpr (MAXN <= 0) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else {
+        if (n >= MAXN) asm volatile("cp.async.wait_group %0;" ::"n"(MAXN) : "memory");
+        else cp_async_wait<MAXN - 1>(n);
     }
-    __syncthreads();
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+template <int BP>
+__global__ void __launch_bounds__(BP >= 8 ? 256 : kGemvMaxWarps * 32, 1) gemv_kernel(const GemvArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int CS = gridDim.x;                 // cluster spans x: blockIdx.x == rank
+    const int split = blockIdx.x, tile = blockIdx.y;
+    const int TN = a.tn, RG = a.rg, ST = a.stages;
+    const int slices = TN / kWarpCols;
+    const int nwarps = slices * RG;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cs = warp % slices, rg = warp / slices;
+    unsigned char* ring = smem + 1024;                           // [nwarps][ST][kStageBytes]
+    float* part = reinterpret_cast<float*>(ring);                // reused: [RG][BP][TN]
+
     pdl_wait();       // rows / vals / nrows come from the previous kernel
-    pdl_trigger();    // let the next kernel's CTAs get resident as ours drain
+    pdl_trigger();
 
     const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
-    const int rps = (nrows + a.n_splits - 1) / a.n_splits;
+    const int rps = (nrows + CS - 1) / CS;
     const int r_begin = min(nrows, split * rps);
     const int r_end = min(nrows, r_begin + rps);
-    const int nstages = (r_end - r_begin + G - 1) / G;
+    const int n_my = r_end - r_begin > rg ? (r_end - r_begin - rg + RG - 1) / RG : 0;   // my rows: r_begin + rg + RG*m
+    const int col0 = tile * TN + cs * kWarpCols;
+    const bool lane_on = col0 + lane * 8 < a.d_out;     // this lane's 16-byte chunk exists
+    const int n_st = (n_my + kStageRows - 1) / kStageRows;
+    // each lane copies, and later reads back, only its own 16-byte chunk of every row: the
+    // staging needs no cross-lane synchronisation, only the lane's own cp.async groups
+    unsigned char* mychunk = ring + (size_t)warp * ST * kStageBytes + lane * 16;
+    const uint16_t* wcol = a.W + col0 + lane * 8;
 
-    if (warp == NCW) {
-        // ---------------- producer: one lane streams the kept row segments ----------------
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            const uint32_t seg = (uint32_t)ncols * 2u;
-            for (int st = 0; st < nstages; ++st) {
-                const int slot = st % kGemvStages;
-                if (st >= kGemvStages) mbar_wait(&empty[slot], ((st / kGemvStages) - 1) & 1);
-                const int r0 = r_begin + st * G;
-                const int gc = min(G, r_end - r0);
-                mbar_arrive_expect_tx(&full[slot], (uint32_t)gc * seg);
-                unsigned char* dst = wbuf + slot * kGemvStageBytes;
-                for (int g = 0; g < gc; ++g) {
-                    const int row = a.rows ? __ldg(a.rows + r0 + g) : r0 + g;
-                    bulk_g2s(dst + g * TN * 2, a.W + (size_t)row * a.ld + col0, seg, &full[slot], pol);
-                }
+    // Row indices / token values are read in 32-row windows (lane j holds my-row base + j),
+    // double-buffered: the next window's loads are in flight while the current one is used,
+    // so the steady state never waits on them.
+    auto load_row = [&](int m) -> int {
+        const int r = r_begin + rg + RG * m;
+        return m < n_my ? (a.rows ? __ldg(a.rows + r) : r) : 0;
+    };
+    int iw_base = 0;
+    int iw_row = load_row(lane);
+    int iw_next = load_row(32 + lane);
+    auto issue = [&](int st) {
+        if (st < n_st) {
+            const int m0 = st * kStageRows;
+            if (m0 >= iw_base + 32) {        // advance one window (kStageRows divides 32)
+                iw_base += 32;
+                iw_row = iw_next;
+                iw_next = load_row(iw_base + 32 + lane);
+            }
+            const int gc = min(kStageRows, n_my - m0);
+            unsigned char* dst = mychunk + (size_t)(st % ST) * kStageBytes;
+#pragma unroll
+            for (int g = 0; g < kStageRows; ++g) {
+                const int row = __shfl_sync(0xffffffffu, iw_row, (m0 - iw_base + g) & 31);
+                if (g < gc && lane_on) cp_async16(dst + g * (kWarpCols * 2), wcol + (size_t)row * a.ld);
             }
         }
-        return;
-    }
+        cp_async_commit();   // (possibly empty) group per stage keeps the group count uniform
+    };
+    for (int st = 0; st < ST; ++st) issue(st);
 
-    // ---------------- consumers ----------------
-    const int c = threadIdx.x * 8;   // tile-local first column of this thread
     float acc[BP][8];
 #pragma unroll
     for (int b = 0; b < BP; ++b)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
 
-    // token values of one row are contiguous (union layout [nrows][BP]) -> float4 loads
-    const bool vec4 = (a.vs_b == 1) && (BP % 4 == 0) && (a.vs_r % 4 == 0);
-    for (int st = 0; st < nstages; ++st) {
-        const int slot = st % kGemvStages;
-        const int r0 = r_begin + st * G;
-        const int gc = min(G, r_end - r0);
-        mbar_wait(&full[slot], (st / kGemvStages) & 1);
-        const unsigned char* src = wbuf + slot * kGemvStageBytes + c * 2;
-#pragma unroll 4
-        for (int g = 0; g < gc; ++g) {
-            const uint4 w = lds128(src + g * TN * 2);
-            float wf[8];
-            wf[0] = bf16lo(w.x); wf[1] = bf16hi(w.x);
-            wf[2] = bf16lo(w.y); wf[3] = bf16hi(w.y);
-            wf[4] = bf16lo(w.z); wf[5] = bf16hi(w.z);
-            wf[6] = bf16lo(w.w); wf[7] = bf16hi(w.w);
-            const float* vp = a.vals + (size_t)(r0 + g) * a.vs_r;
-            float v[BP];
-            if constexpr (BP % 4 == 0) {
-                if (vec4) {
+    auto load_vals = [&](int m, float* v) {
+        const size_t r = (size_t)(r_begin + rg + RG * m);
 #pragma unroll
-                    for (int b = 0; b < BP; b += 4) {
-                        float4 t = __ldg(reinterpret_cast<const float4*>(vp) + b / 4);
-                        v[b] = t.x; v[b + 1] = t.y; v[b + 2] = t.z; v[b + 3] = t.w;
-                    }
-                } else {
+        for (int b = 0; b < BP; ++b)
+            v[b] = (m < n_my && b < a.batch) ? __ldg(a.vals + r * a.vs_r + (size_t)b * a.vs_b) : 0.f;
+    };
+    int vw_base = 0;
+    float vwin[BP], vnext[BP];
+    load_vals(lane, vwin);
+    load_vals(32 + lane, vnext);
+    for (int st = 0; st < n_st; ++st) {
+        const int m0 = st * kStageRows;
+        if (m0 >= vw_base + 32) {
+            vw_base += 32;
 #pragma unroll
-                    for (int b = 0; b < BP; ++b) v[b] = b < a.batch ? __ldg(vp + b * a.vs_b) : 0.f;
-                }
-            } else {
-#pragma unroll
-                for (int b = 0; b < BP; ++b) v[b] = b < a.batch ? __ldg(vp + b * a.vs_b) : 0.f;
-            }
-#pragma unroll
-            for (int b = 0; b < BP; ++b)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[b][j] = fmaf(v[b], wf[j], acc[b][j]);
+            for (int b = 0; b < BP; ++b) vwin[b] = vnext[b];
+            load_vals(vw_base + 32 + lane, vnext);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        const int gc = min(kStageRows, n_my - m0);
+        cp_async_wait<kMaxStagesM1>(ST - 1);    // this lane's chunks of stage st have landed
+        const unsigned char* src = mychunk + (size_t)(st % ST) * kStageBytes;
+#pragma unroll
+        for (int g = 0; g < kStageRows; ++g) {
+            if (g < gc) {
+                const uint4 w = lds128(src + g * (kWarpCols * 2));
+                float wf[8];
+                wf[0] = bf16lo(w.x); wf[1] = bf16hi(w.x);
+                wf[2] = bf16lo(w.y); wf[3] = bf16hi(w.y);
+                wf[4] = bf16lo(w.z); wf[5] = bf16hi(w.z);
+                wf[6] = bf16lo(w.w); wf[7] = bf16hi(w.w);
+                const int src_lane = (m0 - vw_base + g) & 31;
+#pragma unroll
+                for (int b = 0; b < BP; ++b) {
+                    const float v = __shfl_sync(0xffffffffu, vwin[b], src_lane);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[b][j] = fmaf(v, wf[j], acc[b][j]);
+                }
+            }
+        }
+        issue(st + ST);
     }
-
-    // ---------------- deterministic split reduction ----------------
-    const bool active = c < ncols;
-    if (a.n_splits == 1) {
+    cp_async_wait<kMaxStagesM1>(0);
+    if (!lane_on) {
 #pragma unroll
         for (int b = 0; b < BP; ++b)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ytile[b * TN + c + j] = acc[b][j];
-    } else {
-        if (active) {
-#pragma unroll
-            for (int b = 0; b < BP; ++b) {
-                if (b >= a.batch) break;
-                float* p = a.partial + ((size_t)split * BP + b) * a.d_out + col0 + c;
-                reinterpret_cast<float4*>(p)[0] = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
-                reinterpret_cast<float4*>(p)[1] = make_float4(acc[b][4], acc[b][5], acc[b][6], acc[b][7]);
-            }
-        }
-        __threadfence();
-        named_bar_sync(1, NC);
-        if (threadIdx.x == 0) {
-            const unsigned prev = atomicAdd(&a.counters[tile], 1u);
-            s_flag[0] = (prev == (unsigned)(a.n_splits - 1));
-        }
-        named_bar_sync(1, NC);
-        if (!s_flag[0]) return;
-        if (threadIdx.x == 0) a.counters[tile] = 0u;   // self-reset for the next call
-        __threadfence();
-        if (active) {
-            for (int b = 0; b < a.batch; ++b) {
-                float y[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) y[j] = 0.f;
-                const float* p = a.partial + (size_t)b * a.d_out + col0 + c;
-                const size_t sstride = (size_t)BP * a.d_out;
-                int s = 0;
-                for (; s + 4 <= a.n_splits; s += 4) {
-                    float4 t[8];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        t[2 * u] = __ldcg(reinterpret_cast<const float4*>(p + (s + u) * sstride));
-                        t[2 * u + 1] = __ldcg(reinterpret_cast<const float4*>(p + (s + u) * sstride) + 1);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        y[0] += t[2 * u].x; y[1] += t[2 * u].y; y[2] += t[2 * u].z; y[3] += t[2 * u].w;
-                        y[4] += t[2 * u + 1].x; y[5] += t[2 * u + 1].y; y[6] += t[2 * u + 1].z; y[7] += t[2 * u + 1].w;
-                    }
-                }
-                for (; s < a.n_splits; ++s) {
-                    float4 t0 = __ldcg(reinterpret_cast<const float4*>(p + s * sstride));
-                    float4 t1 = __ldcg(reinterpret_cast<const float4*>(p + s * sstride) + 1);
-                    y[0] += t0.x; y[1] += t0.y; y[2] += t0.z; y[3] += t0.w;
-                    y[4] += t1.x; y[5] += t1.y; y[6] += t1.z; y[7] += t1.w;
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) ytile[b * TN + c + j] = y[j];
-            }
-        }
+            for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
     }
-    named_bar_sync(1, NC);
 
-    // ---------------- epilogue on the complete tile (tile-local column c .. c+7) ----------------
-    if (!active) return;
-    const int o0 = col0 + c;
-    float bias8[8];
+    // ---------------- publish this CTA's partial tile: part[rg][b][cs*256 + lane*8 + j] --------
+    __syncthreads();   // every warp is done reading its ring (part aliases it)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) bias8[j] = 0.f;
-    if (a.bias && a.ep != EP_SILU_GU) {
-        const uint4 bb = __ldg(reinterpret_cast<const uint4*>(a.bias + o0));
-        bias8[0] = bf16lo(bb.x); bias8[1] = bf16hi(bb.x); bias8[2] = bf16lo(bb.y); bias8[3] = bf16hi(bb.y);
-        bias8[4] = bf16lo(bb.z); bias8[5] = bf16hi(bb.z); bias8[6] = bf16lo(bb.w); bias8[7] = bf16hi(bb.w);
+    for (int b = 0; b < BP; ++b) {
+        float* p = part + ((size_t)rg * BP + b) * TN + cs * kWarpCols + lane * 8;
+        reinterpret_cast<float4*>(p)[0] = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
+        reinterpret_cast<float4*>(p)[1] = make_float4(acc[b][4], acc[b][5], acc[b][6], acc[b][7]);
     }
-    for (int b = 0; b < a.batch; ++b) {
-        const float* yt = ytile + b * TN;
+    __syncthreads();
+    // local row-group reduction (fixed order): pred[b][c] = sum_g part[g][b][c]
+    const int nthreads = nwarps * 32;
+    float* pred = part + (size_t)RG * BP * TN;             // [BP][TN]
+    float* fin = pred + (size_t)BP * TN;                    // [2 * pairs-per-CTA][BP]
+    for (int t = threadIdx.x; t < a.batch * TN; t += nthreads) {
+        const int b = t / TN, c = t % TN;
+        float v = 0.f;
+        for (int g = 0; g < RG; ++g) v += part[((size_t)g * BP + b) * TN + c];
+        pred[(size_t)b * TN + c] = v;
+    }
+    cluster_sync_all();
+
+    // ---------------- cluster reduction over the CS CTAs (fixed order, DSMEM) ----------------
+    const int po = (a.ep == EP_QKV_ROPE) ? (a.hd >> 1) : kGuBlock;   // pair offset
+    const int npairs = TN >> 1;
+    const int ppc = (npairs + CS - 1) / CS;                            // pairs per CTA
+    const int p_begin = min(npairs, split * ppc), p_end = min(npairs, p_begin + ppc);
+    const int nmine = p_end - p_begin;
+    const uint32_t pred_local = smem_u32(pred);
+    for (int t = threadIdx.x; t < nmine * 2 * a.batch; t += nthreads) {
+        const int b = t % a.batch;
+        const int pi = (t / a.batch) >> 1, half = (t / a.batch) & 1;
+        const int pj = p_begin + pi;
+        const int c = (pj / po) * (2 * po) + (pj % po) + half * po;
+        const uint32_t off = (uint32_t)(((size_t)b * TN + c) * 4);
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = q < CS ? ld_dsmem(cluster_map(pred_local + off, (uint32_t)q)) : 0.f;
+        float y = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) y += v[q];
+        fin[(size_t)(pi * 2 + half) * BP + b] = y;
+    }
+    __syncthreads();
+
+    // ---------------- epilogue on complete column pairs (c1, c1 + po) ----------------
+    for (int t = threadIdx.x; t < nmine * a.batch; t += nthreads) {
+        const int b = t % a.batch, pi = t / a.batch;
+        const int pj = p_begin + pi;
+        const int c1 = (pj / po) * (2 * po) + (pj % po);
+        const int c2 = c1 + po;
+        const int o1 = tile * TN + c1, o2 = tile * TN + c2;
+        float y1 = fin[(size_t)(pi * 2) * BP + b];
+        float y2 = fin[(size_t)(pi * 2 + 1) * BP + b];
+        const bool in1 = o1 < a.d_out, in2 = o2 < a.d_out;
+        if (a.bias && a.ep != EP_SILU_GU) {
+            if (in1) y1 += bf16f(a.bias[o1]);
+            if (in2) y2 += bf16f(a.bias[o2]);
+        }
         if (a.ep == EP_STORE || a.ep == EP_RESID) {
-            float r[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = yt[c + j] + bias8[j];
+            float* op = a.out + (size_t)b * a.out_ld;
             if (a.ep == EP_RESID) {
-                const float* rp = a.resid + (size_t)b * a.resid_ld + o0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = rp[j] + r[j];
+                const float* rp = a.resid + (size_t)b * a.resid_ld;
+                if (in1) y1 = rp[o1] + y1;
+                if (in2) y2 = rp[o2] + y2;
             }
-            float* op = a.out + (size_t)b * a.out_ld + o0;
-            reinterpret_cast<float4*>(op)[0] = make_float4(r[0], r[1], r[2], r[3]);
-            reinterpret_cast<float4*>(op)[1] = make_float4(r[4], r[5], r[6], r[7]);
+            if (in1) op[o1] = y1;
+            if (in2) op[o2] = y2;
         } else if (a.ep == EP_SILU_GU) {
-            // fused column o: block t = o / 128 holds gate [t*64, t*64+64) then up of the same rows
-            const int within = o0 % (2 * kGuBlock);
-            if (within < kGuBlock) {
-                const int i0 = (o0 / (2 * kGuBlock)) * kGuBlock + within;
-                float h[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float g = yt[c + j];
-                    const float u = yt[c + kGuBlock + j];
-                    h[j] = silu_f(g) * u;
-                }
-                float* op = a.out + (size_t)b * a.out_ld + i0;
-                reinterpret_cast<float4*>(op)[0] = make_float4(h[0], h[1], h[2], h[3]);
-                reinterpret_cast<float4*>(op)[1] = make_float4(h[4], h[5], h[6], h[7]);
-            }
-        } else {   // EP_QKV_ROPE
-            const int hd = a.hd, half = hd >> 1;
+            // fused block t = o1 / 128: gate [t*64, t*64+64) then up of the same rows
+            const int i = (o1 / (2 * kGuBlock)) * kGuBlock + (o1 % (2 * kGuBlock));
+            a.out[(size_t)b * a.out_ld + i] = silu_f(y1) * y2;
+        } else {   // EP_QKV_ROPE: (o1, o2) = head dims (i, i + hd/2) of one head
+            const int hd = a.hd;
             const int nq = a.hq * hd, nk = a.hkv * hd;
             const int p = a.pos[b];
-            float r[8];
-            const int head_off = o0 % hd;   // 8 consecutive columns lie in one head
-            if (o0 < nq + nk) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int i = head_off + j;
-                    const int fi = i < half ? i : i - half;
-                    const int partner = i < half ? c + j + half : c + j - half;
-                    const double inv_freq = exp(-(2.0 * fi / hd) * log((double)a.theta));
-                    double sn, cs;
-                    sincos((double)p * inv_freq, &sn, &cs);
-                    const float x = yt[c + j] + bias8[j];
-                    float xpart = yt[partner];
-                    if (a.bias) xpart += bf16f(a.bias[col0 + partner]);
-                    const float rot = i < half ? -xpart : xpart;
-                    r[j] = (float)((double)x * cs + (double)rot * sn);
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = yt[c + j] + bias8[j];
+            float r1 = y1, r2 = y2;
+            if (o1 < nq + nk) {
+                const int i = o1 % hd;
+                const double inv_freq = exp(-(2.0 * i / hd) * log((double)a.theta));
+                double sn, cn;
+                sincos((double)p * inv_freq, &sn, &cn);
+                r1 = (float)((double)y1 * cn - (double)y2 * sn);
+                r2 = (float)((double)y2 * cn + (double)y1 * sn);
             }
-            if (o0 < nq) {
-                float* op = a.out + (size_t)b * a.out_ld + o0;
-                reinterpret_cast<float4*>(op)[0] = make_float4(r[0], r[1], r[2], r[3]);
-                reinterpret_cast<float4*>(op)[1] = make_float4(r[4], r[5], r[6], r[7]);
+            if (o1 < nq) {
+                float* op = a.out + (size_t)b * a.out_ld;
+                op[o1] = r1;
+                op[o2] = r2;
             } else {
-                const bool isk = o0 < nq + nk;
-                const int oo = o0 - (isk ? nq : nq + nk);
-                const int kvh = oo / hd;
-                uint16_t* dst = (isk ? a.kc : a.vc) + (((size_t)b * a.hkv + kvh) * a.max_ctx + p) * hd + head_off;
-                uint4 pk;
-                pk.x = (uint32_t)f2bf16_rne(r[0]) | ((uint32_t)f2bf16_rne(r[1]) << 16);
-                pk.y = (uint32_t)f2bf16_rne(r[2]) | ((uint32_t)f2bf16_rne(r[3]) << 16);
-                pk.z = (uint32_t)f2bf16_rne(r[4]) | ((uint32_t)f2bf16_rne(r[5]) << 16);
-                pk.w = (uint32_t)f2bf16_rne(r[6]) | ((uint32_t)f2bf16_rne(r[7]) << 16);
-                *reinterpret_cast<uint4*>(dst) = pk;
+                const bool isk = o1 < nq + nk;
+                const int oo = o1 - (isk ? nq : nq + nk);
+                const int kvh = oo / hd, i = oo % hd;
+                uint16_t* dst = (isk ? a.kc : a.vc) + (((size_t)b * a.hkv + kvh) * a.max_ctx + p) * hd;
+                dst[i] = f2bf16_rne(r1);
+                dst[i + (hd >> 1)] = f2bf16_rne(r2);
             }
         }
     }
+    cluster_sync_all();   // keep every CTA's partial alive until all peers finished reading
 }
 
 }  // namespace larosa

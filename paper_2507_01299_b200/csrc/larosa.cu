@@ -122,57 +122,92 @@ int pad_batch(int b) { return b <= 1 ? 1 : b <= 2 ? 2 : b <= 4 ? 4 : b <= 8 ? 8 
 
 // ============================================================================== GEMV plan
 struct GemvPlan {
-    int ncw, tn, n_tiles, n_splits;
+    int tn, cs, rg, nwarps, stages, n_tiles;
+    size_t smem;
 };
 
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
+constexpr size_t kGemvSmemBudget = 200 * 1024;
+
+// Tile width TN (multiple of 256) x cluster size CS so that n_tiles * CS CTAs fill the SMs
+// once (one CTA per SM, ~200 KB ring); prefer the portable cluster size 8.
 GemvPlan plan_gemv(int64_t d_out, int64_t nrows_max, int bp) {
-    GemvPlan p;
-    p.ncw = d_out >= 16384 ? 4 : d_out >= 8192 ? 2 : 1;
-    p.tn = 256 * p.ncw;
-    p.n_tiles = (int)((d_out + p.tn - 1) / p.tn);
-    const int G = kGemvStageBytes / (p.tn * 2);
-    // ~2 resident CTAs per SM (96 KB stage ring each) at batch 1
-    const int per_sm = bp <= 4 ? 2 : 1;
-    const int target = sm_count() * per_sm;
-    int s = (target + p.n_tiles / 2) / p.n_tiles;
-    const int max_s = (int)std::max<int64_t>(1, nrows_max / G);
-    p.n_splits = std::max(1, std::min(s, max_s));
-    return p;
-}
-
-struct GemvBufs {
-    float* partial;
-    unsigned* counters;
-};
-
-void carve_gemv(Carver& c, const GemvPlan& p, int bp, int64_t d_out, GemvBufs* b) {
-    float* part = c.take<float>((size_t)p.n_splits * bp * d_out);
-    unsigned* cnt = c.counters(kGemvCounterBase);
-    if (b) {
-        b->partial = part;
-        b->counters = cnt;
+    static const int force_cs = env_int("LAROSA_GEMV_CS", 0);     // tuning knobs (0 = auto)
+    static const int force_tn = env_int("LAROSA_GEMV_TN", 0);
+    static const int force_rg = env_int("LAROSA_GEMV_RG", 0);
+    const int sms = sm_count();
+    const int64_t max_cs_rows = std::max<int64_t>(1, nrows_max / 8);
+    GemvPlan best = {256, 1, 1, 1, 2, (int)((d_out + 255) / 256), 0};
+    int best_ctas = 0;
+    const int max_warps = bp >= 8 ? 8 : kGemvMaxWarps;   // matches the kernel's launch bounds
+    const int cs_order[5] = {8, 16, 4, 2, 1};
+    for (int ci = 0; ci < 5; ++ci) {
+        const int cs = cs_order[ci];
+        if (force_cs && cs != force_cs) continue;
+        if (cs > max_cs_rows && cs > 1) continue;
+        for (int tn = 256; tn <= 4096; tn += 256) {
+            if (force_tn && tn != force_tn) continue;
+            const int slices = tn / 256;
+            if (tn - 256 >= d_out) break;
+            const int tiles = (int)((d_out + tn - 1) / tn);
+            const int ctas = tiles * cs;
+            if (ctas > sms) continue;
+            if (slices > max_warps) break;
+            int rg = std::max(1, std::min(8, 8 / slices));
+            if (force_rg) rg = force_rg;
+            rg = std::min(rg, max_warps / slices);
+            if (rg < 1 || rg * slices > max_warps) continue;
+            if (gemv_tail_bytes(rg, bp, tn) > kGemvSmemBudget) continue;
+            if (ctas > best_ctas) {
+                best_ctas = ctas;
+                best.tn = tn;
+                best.cs = cs;
+                best.rg = rg;
+                best.n_tiles = tiles;
+            }
+        }
     }
-}
-
-template <int BP, int NCW>
-larosa_status launch_gemv_t(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
-    auto kern = gemv_kernel<BP, NCW>;
-    const size_t smem = gemv_smem_bytes(BP, NCW);
-    static bool attr_done = false;
-    if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, smem), "cudaFuncSetAttribute(gemv)"));
-        attr_done = true;
-    }
-    return cuda_check(launch(kern, dim3(p.n_tiles, p.n_splits), dim3((NCW + 1) * 32), smem, st, a), "gemv launch");
+    best.nwarps = (best.tn / 256) * best.rg;
+    int st = (int)((kGemvSmemBudget - 1024) / ((size_t)best.nwarps * kStageBytes));
+    st = std::max(2, std::min(st, std::min(16, 128 / best.nwarps)));
+    best.stages = st;
+    best.smem = gemv_smem_bytes(best.nwarps, st, best.rg, bp, best.tn);
+    return best;
 }
 
 template <int BP>
-larosa_status launch_gemv_bp(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
-    switch (p.ncw) {
-        case 1: return launch_gemv_t<BP, 1>(a, p, st);
-        case 2: return launch_gemv_t<BP, 2>(a, p, st);
-        default: return launch_gemv_t<BP, 4>(a, p, st);
+larosa_status launch_gemv_bp(GemvArgs a, const GemvPlan& p, cudaStream_t st) {
+    auto kern = gemv_kernel<BP>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        LAROSA_TRY(cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+                              "cudaFuncSetAttribute(gemv smem)"));
+        LAROSA_TRY(cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                              "cudaFuncSetAttribute(gemv cluster)"));
+        attr_done = true;
     }
+    a.tn = p.tn;
+    a.rg = p.rg;
+    a.stages = p.stages;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.cs, p.n_tiles);
+    cfg.blockDim = dim3(p.nwarps * 32);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "gemv launch");
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
@@ -260,12 +295,9 @@ extern "C" larosa_status larosa_solve_alpha(double a1, double a3, double m, doub
 }
 
 // ============================================================================== sparse GEMV
-static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t k, int64_t d_out, GemvBufs* gb,
-                              uint32_t** mask, int32_t** rows, float** V, int** nrows) {
+static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t k, uint32_t** mask, int32_t** rows,
+                              float** V, int** nrows) {
     const int bp = pad_batch(batch);
-    const int64_t nrows_max = batch == 1 ? k : std::min<int64_t>(d_in, (int64_t)batch * k);
-    GemvPlan p = plan_gemv(d_out, nrows_max, bp);
-    carve_gemv(c, p, bp, d_out, gb);
     if (batch > 1) {
         const int64_t nw = (d_in + 31) / 32;
         uint32_t* m = c.take<uint32_t>((size_t)batch * nw);
@@ -282,7 +314,8 @@ static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t k,
 extern "C" size_t larosa_sparse_gemv_workspace_size(int32_t batch, int64_t d_in, int64_t k, int64_t d_out) {
     if (batch < 1 || d_in <= 0 || d_out <= 0 || k < 0) return 0;
     Carver c(nullptr);
-    carve_sparse_gemv(c, batch, d_in, k, d_out, nullptr, nullptr, nullptr, nullptr, nullptr);
+    (void)d_out;
+    carve_sparse_gemv(c, batch, d_in, k, nullptr, nullptr, nullptr, nullptr);
     return c.size();
 }
 
@@ -306,12 +339,11 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
     Carver c(ws);
-    GemvBufs gb;
     uint32_t* mask = nullptr;
     int32_t* rows = nullptr;
     float* V = nullptr;
     int* nrows = nullptr;
-    carve_sparse_gemv(c, batch, d_in, k, d_out, &gb, &mask, &rows, &V, &nrows);
+    carve_sparse_gemv(c, batch, d_in, k, &mask, &rows, &V, &nrows);
     const int bp = pad_batch(batch);
     const int64_t nrows_max = batch == 1 ? k : std::min<int64_t>(d_in, (int64_t)batch * k);
     GemvPlan p = plan_gemv(d_out, nrows_max, bp);
@@ -321,9 +353,6 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     a.ld = ld;
     a.d_out = (int)d_out;
     a.batch = batch;
-    a.n_splits = p.n_splits;
-    a.partial = gb.partial;
-    a.counters = gb.counters;
     a.bias = bias;
     a.out = y;
     a.out_ld = d_out;
@@ -353,18 +382,57 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     return launch_gemv(a, p, bp, st);
 }
 
+extern "C" larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info) {
+    if (!info || d_out <= 0 || nrows_max < 0 || batch < 1 || batch > LAROSA_MAX_BATCH)
+        return fail(LAROSA_EINVAL, "gemv_plan_info: bad arguments");
+    const int bp = pad_batch(batch);
+    const GemvPlan p = plan_gemv(d_out, nrows_max, bp);
+    info[0] = p.tn;
+    info[1] = p.cs;
+    info[2] = p.rg;
+    info[3] = p.nwarps;
+    info[4] = p.stages;
+    info[5] = p.n_tiles;
+    info[6] = (int32_t)p.smem;
+    info[7] = 0;
+    int dev = -1;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.cs, p.n_tiles);
+        cfg.blockDim = dim3(p.nwarps * 32);
+        cfg.dynamicSmemBytes = p.smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = p.cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        cudaError_t e;
+        switch (bp) {
+            case 1: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<1>, &cfg); break;
+            case 2: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<2>, &cfg); break;
+            case 4: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<4>, &cfg); break;
+            case 8: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<8>, &cfg); break;
+            default: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<16>, &cfg); break;
+        }
+        if (e == cudaSuccess) info[7] = n;
+        cudaGetLastError();
+    }
+    return LAROSA_OK;
+}
+
 // ============================================================================== rotate + Top-K
-static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, float** xr, GemvBufs* gb) {
+static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, float** xr) {
     float* x = c.take<float>((size_t)batch * d);
     if (xr) *xr = x;
-    GemvPlan p = plan_gemv(d, d, pad_batch(batch));
-    carve_gemv(c, p, pad_batch(batch), d, gb);
 }
 
 extern "C" size_t larosa_rotate_topk_workspace_size(int32_t batch, int64_t d) {
     if (batch < 1 || d <= 0) return 0;
     Carver c(nullptr);
-    carve_rotate_topk(c, batch, d, nullptr, nullptr);
+    carve_rotate_topk(c, batch, d, nullptr);
     return c.size();
 }
 
@@ -386,8 +454,7 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
     float* xr_ws;
-    GemvBufs gb;
-    carve_rotate_topk(c, batch, d, &xr_ws, &gb);
+    carve_rotate_topk(c, batch, d, &xr_ws);
 
     const float* src = x;
     if (R) {
@@ -405,9 +472,6 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
         a.vs_b = d;
         a.nrows = (int)d;
         a.batch = batch;
-        a.n_splits = p.n_splits;
-        a.partial = gb.partial;
-        a.counters = gb.counters;
         a.out = xr;
         a.out_ld = d;
         a.ep = EP_STORE;
@@ -484,7 +548,6 @@ struct LayerWs {
     int32_t* urows;
     float* uV;
     int* unrows;
-    GemvBufs gb;
     float* attn_part;
     unsigned* attn_cnt;
 };
@@ -510,7 +573,7 @@ LayerDims layer_dims(const larosa_layer_weights* w) {
 
 int attn_chunk(int64_t max_ctx, int units) {
     // enough CTAs to cover the SMs: units * n_chunks >= sm_count
-    int ch = 128;
+    int ch = 4 * kAttnPosPerWarp;
     while (ch > 16 && units * ((max_ctx + ch - 1) / ch) < sm_count()) ch >>= 1;
     return ch;
 }
@@ -534,18 +597,6 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     o->urows = c.take<int32_t>((size_t)dmax);
     o->uV = c.take<float>((size_t)dmax * bp + 16);
     o->unrows = c.take<int>(4);
-    // partial buffer big enough for every GEMV of the layer
-    size_t part = 0, cnt = 0;
-    const int64_t douts[5] = {L.nqkv, L.d, L.dgu, L.d, L.d};
-    const int64_t nrm[5] = {L.d, L.nq, L.d, L.inter, L.d};
-    for (int i = 0; i < 5; ++i) {
-        GemvPlan p = plan_gemv(douts[i], nrm[i], bp);
-        part = std::max(part, (size_t)p.n_splits * bp * douts[i]);
-        cnt = std::max(cnt, (size_t)p.n_tiles);
-    }
-    o->gb.partial = c.take<float>(part);
-    o->gb.counters = c.counters(kGemvCounterBase);
-    (void)cnt;
     const int ch = attn_chunk(max_ctx, batch * (int)L.hkv);
     const int nch = (int)((max_ctx + ch - 1) / ch);
     o->attn_part = c.take<float>((size_t)batch * L.hkv * nch * L.G * (L.hd + 2));
@@ -650,8 +701,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             a.nrows_dev = W.unrows;
         }
         a.batch = B;
-        a.partial = W.gb.partial;
-        a.counters = W.gb.counters;
         return LAROSA_OK;
     };
     auto nrows_max = [&](int64_t din, int64_t k) { return B == 1 ? k : std::min<int64_t>(din, (int64_t)B * k); };
@@ -664,7 +713,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.W = w->w_qkv;
         a.ld = L.nqkv;
         a.d_out = (int)L.nqkv;
-        a.n_splits = p.n_splits;
         a.ep = EP_QKV_ROPE;
         a.bias = w->b_qkv;
         a.out = W.q;
@@ -711,7 +759,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.W = w->w_o;
         a.ld = L.d;
         a.d_out = (int)L.d;
-        a.n_splits = p.n_splits;
         a.ep = EP_RESID;
         a.resid = s->resid;
         a.resid_ld = L.d;
@@ -730,7 +777,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.W = w->w_gu;
         a.ld = L.dgu;
         a.d_out = (int)L.dgu;
-        a.n_splits = p.n_splits;
         a.ep = EP_SILU_GU;
         a.out = W.h4;
         a.out_ld = L.inter;
@@ -748,7 +794,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.W = w->w_down;
         a.ld = L.d;
         a.d_out = (int)L.d;
-        a.n_splits = p.n_splits;
         a.ep = EP_RESID;
         a.resid = W.rmid;
         a.resid_ld = L.d;
@@ -772,9 +817,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.vs_b = L.d;
         a.nrows = (int)L.d;
         a.batch = B;
-        a.n_splits = p.n_splits;
-        a.partial = W.gb.partial;
-        a.counters = W.gb.counters;
         a.ep = EP_STORE;
         a.out = s->resid;
         a.out_ld = L.d;

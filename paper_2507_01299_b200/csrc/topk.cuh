@@ -2,27 +2,33 @@
 // select on the uint32 keys bits(|x|), with the lower-index tie-break, plus the
 // RMS scale of the h1/h3 sites and stable compaction to ascending indices.
 //
-// One CTA per token.  Keys live in shared memory (padded one word per 32 to keep the
-// contiguous-ownership compaction bank-conflict-light); the histogram passes use strided
-// ownership.  Digits: bits [30:19] (4096 bins), [18:7] (4096), [6:0] (128).  A pass that
-// finds the k-th key's bucket fully inside the selection stops early (typical for
-// continuous data after 2 passes); an exact tie across the k-th key is resolved by index.
+// One CTA (1024 threads) per token, latency-optimised (it sits between two dependent GEMVs):
+//  * thread t owns the contiguous elements [t*EPT, t*EPT + EPT) and keeps their keys in
+//    registers for the whole select (one coalesced float4 load per 4 elements; no shared
+//    memory copy of the vector);
+//  * digits: bits [30:19] (4096 bins), [18:7] (4096), [6:0] (128); a pass whose k-th-key
+//    bucket is taken whole ends the select (continuous data: 2 passes); double-buffered
+//    histograms so the next pass's zeroing overlaps the current one;
+//  * the bucket search is a warp-level suffix scan with one shared exchange of warp totals;
+//  * exact key ties straddling position k are resolved by index (lower index first);
+//  * compaction is one block-wide exclusive scan of per-thread counts (contiguous
+//    ownership keeps the output ascending).
 #pragma once
 #include "common.cuh"
 
 namespace larosa {
 
 constexpr int kTopkThreads = 1024;
+constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kTopkBins = 4096;
 
-__host__ __device__ constexpr int topk_pad(int i) { return i + (i >> 5); }
-
-// dynamic smem bytes for a vector of length d
 __host__ __device__ constexpr size_t topk_smem_bytes(int d) {
-    return sizeof(uint32_t) * (size_t)(topk_pad(d) + 1)            // keys
-           + sizeof(int) * kTopkBins                                // histogram
-           + sizeof(uint32_t) * (size_t)((d + 31) / 32)             // mask words
-           + sizeof(int) * 64;                                      // scan / broadcast scratch
+    return sizeof(int) * 2 * kTopkBins + sizeof(uint32_t) * (size_t)((d + 31) / 32) + sizeof(int) * 160;
+}
+
+// elements per thread (multiple of 4) for a vector of length d
+__host__ __device__ constexpr int topk_ept(int d) {
+    return ((d + 4 * kTopkThreads - 1) / (4 * kTopkThreads)) * 4;
 }
 
 struct TopkOut {
@@ -33,125 +39,162 @@ struct TopkOut {
     float* scale_out;  // [1] the RMS scale s (1 when rms_eps < 0), or nullptr
 };
 
-// Top-K of x[0..d) (global memory, fp32).  Must be called by all kTopkThreads threads.
-__device__ void block_topk(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                           unsigned char* smem_raw) {
-    constexpr int NT = kTopkThreads;
-    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
-    int* hist = reinterpret_cast<int*>(keys + topk_pad(d) + 1);
-    const int nwords = (d + 31) / 32;
-    uint32_t* smask = reinterpret_cast<uint32_t*>(hist + kTopkBins);
-    int* scr = reinterpret_cast<int*>(smask + nwords);   // 64 ints
-    float* fscr = reinterpret_cast<float*>(scr);
-    const int tid = threadIdx.x;
+// exclusive prefix over one int per thread in thread order; 1 __syncthreads.
+__device__ __forceinline__ int topk_excl_scan(int v, int* sw, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int inc = warp_incl_scan(v);
+    if (lane == 31) sw[wid] = inc;
+    __syncthreads();
+    const int t = sw[lane];                       // kTopkWarps == 32
+    const int ti = warp_incl_scan(t);
+    *total = __shfl_sync(0xffffffffu, ti, 31);
+    return __shfl_sync(0xffffffffu, ti - t, wid) + inc - v;
+}
 
-    // 1. keys = bits(|x|) (clears the sign, so -0 == +0), sum of squares for the RMS scale
+template <int EPT>
+__device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
+                             unsigned char* smem_raw) {
+    constexpr int NT = kTopkThreads;
+    int* hist0 = reinterpret_cast<int*>(smem_raw);
+    int* hist1 = hist0 + kTopkBins;
+    const int nwords = (d + 31) / 32;
+    uint32_t* smask = reinterpret_cast<uint32_t*>(hist1 + kTopkBins);
+    int* scr = reinterpret_cast<int*>(smask + nwords);
+    int* s_wtot = scr;                                   // [0, 32)
+    int* s_wtot2 = scr + 32;                             // [32, 64)
+    float* s_ssq = reinterpret_cast<float*>(scr + 64);   // [64, 96)
+    int* s_res = scr + 96;                               // [96, 100)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int i0 = tid * EPT;
+
+    // 1. keys = bits(|x|) in registers (clears the sign: -0 == +0), sum of squares
+    uint32_t key[EPT];
     float ssq = 0.f;
-    for (int i = tid; i < d; i += NT) {
-        float v = __ldg(x + i);
-        keys[topk_pad(i)] = __float_as_uint(v) & 0x7fffffffu;
-        ssq = fmaf(v, v, ssq);
-        if (out.xr_out) out.xr_out[i] = v;
+    const bool vec = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+#pragma unroll
+    for (int c = 0; c < EPT / 4; ++c) {
+        const int i = i0 + 4 * c;
+        float v[4];
+        if (vec && i + 4 <= d) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(x + i));
+            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = (i + u < d) ? __ldg(x + i + u) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            // out-of-range elements get key 0 and are excluded by index checks below
+            key[4 * c + u] = __float_as_uint(v[u]) & 0x7fffffffu;
+            ssq = fmaf(v[u], v[u], ssq);
+            if (out.xr_out && i + u < d) out.xr_out[i + u] = v[u];
+        }
     }
-    for (int w = tid; w < nwords; w += NT) smask[w] = 0u;
-    float scale = 1.f;
-    if (rms_eps >= 0.f) {
-        float tot = block_sum<NT>(ssq, fscr);          // fixed-order, deterministic
-        scale = 1.0f / sqrtf(tot / (float)d + rms_eps);
-    }
+    ssq = warp_sum(ssq);
+    if (lane == 0) s_ssq[wid] = ssq;
+    for (int b = tid; b < kTopkBins; b += NT) hist0[b] = 0;
+    if (out.mask)
+        for (int w = tid; w < nwords; w += NT) smask[w] = 0u;
     __syncthreads();
 
-    // 2. radix select of the k-th largest key.  Selection rule afterwards:
-    //    key > thr, or key == thr and (tie_mode ? among the first `rem` such indices : true)
+    // 2. radix select of the k-th largest key
     uint32_t prefix = 0u, pmask = 0u;
-    int rem = k;              // how many still to take inside the current bucket prefix
-    bool exact_ge = false;    // early exit: select key >= prefix (lower bits free)
-    bool tie_mode = false;
+    int rem = k;
+    bool exact_ge = false;   // select key >= thr (the k-th key's bucket is taken whole)
+    bool tie_mode = false;   // select key > thr, plus the first `rem` keys == thr by index
     if (k <= 0 || k >= d) {
         exact_ge = true;
-        prefix = (k >= d) ? 0u : 0xffffffffu;   // k == 0 selects nothing (keys < 2^31)
+        prefix = (k >= d) ? 0u : 0xffffffffu;   // keys < 2^31, so k == 0 selects nothing
     } else {
-        const int shifts[3] = {19, 7, 0};
-        const int nbits[3] = {12, 12, 7};
+#pragma unroll 1
         for (int pass = 0; pass < 3; ++pass) {
-            const int sh = shifts[pass];
-            const int nb = 1 << nbits[pass];
+            int* hist = (pass & 1) ? hist1 : hist0;
+            int* hnext = (pass & 1) ? hist0 : hist1;
+            const int sh = pass == 0 ? 19 : (pass == 1 ? 7 : 0);
+            const int nb = pass == 2 ? 128 : 4096;
             const uint32_t dmask = (uint32_t)(nb - 1);
-            for (int b = tid; b < nb; b += NT) hist[b] = 0;
+#pragma unroll
+            for (int e = 0; e < EPT; ++e)
+                if (i0 + e < d && (key[e] & pmask) == prefix) atomicAdd(&hist[(key[e] >> sh) & dmask], 1);
+            if (pass < 2)
+                for (int b = tid; b < kTopkBins; b += NT) hnext[b] = 0;
             __syncthreads();
-            for (int i = tid; i < d; i += NT) {
-                uint32_t key = keys[topk_pad(i)];
-                if ((key & pmask) == prefix) atomicAdd(&hist[(key >> sh) & dmask], 1);
-            }
-            __syncthreads();
-            // suffix scan: thread t owns bins [nb - (t+1)*bpt, nb - t*bpt) (top bins first)
-            const int bpt = (nb + NT - 1) / NT;
-            const int hiB = nb - tid * bpt;
-            const int loB = max(0, hiB - bpt);
+            // suffix scan: warp w owns the bins [nb - (w+1)*bpw, nb - w*bpw), top bins first
+            const int bpw = nb / kTopkWarps;              // 128 or 4
+            const int bpl = bpw >= 32 ? bpw / 32 : 1;     // 4 or 1
+            const int lhi = nb - wid * bpw - lane * bpl;  // lane's bins [lhi - bpl, lhi)
             int c = 0;
-            for (int b = hiB - 1; b >= loB; --b) c += hist[b];
-            int tot;
-            int before = block_excl_scan<NT>(c, scr, &tot);
-            if (before < rem && rem <= before + c) {
+            if (lane * bpl < bpw)
+                for (int b = lhi - 1; b >= lhi - bpl; --b) c += hist[b];
+            const int inc = warp_incl_scan(c);
+            if (lane == 31) s_wtot[wid] = inc;
+            __syncthreads();
+            const int t = s_wtot[lane];
+            const int ti = warp_incl_scan(t);
+            const int before = __shfl_sync(0xffffffffu, ti - t, wid) + inc - c;
+            if (c > 0 && before < rem && rem <= before + c) {
                 int acc = before;
-                for (int b = hiB - 1; b >= loB; --b) {
-                    int h = hist[b];
+                for (int b = lhi - 1; b >= lhi - bpl; --b) {
+                    const int h = hist[b];
                     if (acc + h >= rem) {
-                        scr[40] = b;
-                        scr[41] = rem - acc;
-                        scr[42] = h;
+                        s_res[0] = b;
+                        s_res[1] = rem - acc;
+                        s_res[2] = h;
                         break;
                     }
                     acc += h;
                 }
             }
             __syncthreads();
-            const int bstar = scr[40];
-            rem = scr[41];
-            const int cnt = scr[42];
+            const int bstar = s_res[0];
+            rem = s_res[1];
+            const int cnt = s_res[2];
             prefix |= (uint32_t)bstar << sh;
             pmask |= dmask << sh;
-            __syncthreads();    // scr reused by the next scan
-            if (cnt == rem) {   // whole bucket selected: key >= prefix
+            if (cnt == rem) {
                 exact_ge = true;
                 break;
             }
-            if (pass == 2) tie_mode = true;   // exact key tie straddles position k
+            if (pass == 2) tie_mode = true;
         }
     }
     const uint32_t thr = prefix;
+    float tot_ssq = 0.f;
+#pragma unroll
+    for (int w = 0; w < kTopkWarps; ++w) tot_ssq += s_ssq[w];   // fixed order: deterministic
+    const float scale = rms_eps >= 0.f ? 1.0f / sqrtf(tot_ssq / (float)d + rms_eps) : 1.0f;
 
-    // 3. stable compaction, contiguous ownership: thread t owns [t*E, min(d, (t+1)*E))
-    const int E = (d + NT - 1) / NT;
-    const int i0 = min(d, tid * E), i1 = min(d, i0 + E);
+    // 3. stable compaction over the contiguous ownership ranges
     int n_gt = 0, n_eq = 0;
-    for (int i = i0; i < i1; ++i) {
-        uint32_t key = keys[topk_pad(i)];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        if (i0 + e >= d) continue;
         if (exact_ge) {
-            n_gt += (key >= thr);
+            n_gt += key[e] >= thr;
         } else {
-            n_gt += (key > thr);
-            n_eq += (key == thr);
+            n_gt += key[e] > thr;
+            n_eq += key[e] == thr;
         }
     }
     int take_eq = 0;
     if (tie_mode) {
         int tot;
-        int eq_before = block_excl_scan<NT>(n_eq, scr, &tot);
+        const int eq_before = topk_excl_scan(n_eq, s_wtot, &tot);
         take_eq = min(n_eq, max(0, rem - eq_before));
-        __syncthreads();
     }
     int tot_sel;
-    int pos = block_excl_scan<NT>(n_gt + take_eq, scr, &tot_sel);
+    int pos = topk_excl_scan(n_gt + take_eq, tie_mode ? s_wtot2 : s_wtot, &tot_sel);
     int eq_seen = 0;
-    for (int i = i0; i < i1; ++i) {
-        uint32_t key = keys[topk_pad(i)];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const int i = i0 + e;
+        if (i >= d) continue;
         bool sel;
         if (exact_ge) {
-            sel = key >= thr;
-        } else if (key > thr) {
+            sel = key[e] >= thr;
+        } else if (key[e] > thr) {
             sel = true;
-        } else if (key == thr) {
+        } else if (key[e] == thr) {
             sel = eq_seen < take_eq;
             ++eq_seen;
         } else {
@@ -171,6 +214,17 @@ __device__ void block_topk(const float* __restrict__ x, int d, int k, float rms_
     }
 }
 
+__device__ __forceinline__ void block_topk(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
+                                           unsigned char* smem) {
+    const int ept = topk_ept(d);
+    if (ept <= 4) block_topk_t<4>(x, d, k, rms_eps, out, smem);
+    else if (ept <= 8) block_topk_t<8>(x, d, k, rms_eps, out, smem);
+    else if (ept <= 12) block_topk_t<12>(x, d, k, rms_eps, out, smem);
+    else if (ept <= 16) block_topk_t<16>(x, d, k, rms_eps, out, smem);
+    else if (ept <= 24) block_topk_t<24>(x, d, k, rms_eps, out, smem);
+    else block_topk_t<32>(x, d, k, rms_eps, out, smem);
+}
+
 // One CTA per token: x [batch][ldx], outputs strided per token.
 struct TopkKernelArgs {
     const float* x;
@@ -187,6 +241,7 @@ struct TopkKernelArgs {
 __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x;
     const int nwords = (a.d + 31) / 32;
     TopkOut o;
@@ -196,7 +251,6 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
     o.mask = a.mask ? a.mask + (size_t)b * nwords : nullptr;
     o.scale_out = a.scale ? a.scale + b : nullptr;
     block_topk(a.x + (size_t)b * a.ldx, a.d, a.k, a.rms_eps, o, smem);
-    pdl_trigger();
 }
 
 }  // namespace larosa
