@@ -14,9 +14,10 @@
  *    asynchronous on `stream` and CUDA-graph capturable: no allocation, no host sync,
  *    no device-wide memset.  The caller owns every buffer.
  *  - Workspaces: sized by the matching *_workspace_size() query, 256-byte aligned,
- *    and ZERO-FILLED ONCE by the caller when allocated (kernels keep their tile
- *    counters self-resetting so the zero state is restored after every call).  A
- *    workspace may not be used by two calls that can run concurrently.
+ *    and ZERO-FILLED ONCE by the caller when allocated.  They hold the GEMVs' 64-bit
+ *    fixed-point accumulators and tickets, which every call restores to zero, so a
+ *    workspace must be reused only for calls of the same kind and shapes (or be zeroed
+ *    again), and not by two calls that can run concurrently.
  *  - Errors: arguments are validated synchronously and a status is returned; no
  *    exception crosses the ABI.  Launch errors return LAROSA_ECUDA (from
  *    cudaGetLastError).  Faults inside kernels surface at the caller's next sync.
@@ -145,9 +146,8 @@ larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int64_t d_out,
                                  larosa_stream_t stream);
 
 /* Introspection (host): the launch plan larosa_sparse_gemv uses for this shape.
- * info (host, 8 ints) = {tile columns TN, cluster size CS, row groups RG, warps per CTA,
- * ring stages per warp, column tiles, dynamic smem bytes, max co-resident clusters
- * (cudaOccupancyMaxActiveClusters on the current device; 0 if unavailable)}. */
+ * info (host, 8 ints) = {columns per CTA, column slices, kept-row splits, warps per CTA,
+ * cp.async ring stages per warp, rows per stage, dynamic smem bytes, CTAs}. */
 larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info);
 
 /* ------------------------------------------------------------------------------

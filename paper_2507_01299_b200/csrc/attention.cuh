@@ -12,6 +12,7 @@
 // the last chunk CTA to finish (atomic ticket) merges the chunks in order.
 #pragma once
 #include "common.cuh"
+#include "gemv.cuh"
 
 namespace larosa {
 
@@ -20,9 +21,13 @@ constexpr int kAttnPosPerWarp = 16;          // CH <= 4 * 16
 constexpr int kAttnMaxG = 8;
 
 struct AttnArgs {
-    const float* q;        // [batch][hq*hd]
-    const uint16_t* kc;    // [batch][hkv][max_ctx][hd]
-    const uint16_t* vc;
+    const unsigned long long* acc;   // [batch][acc_ld] QKV GEMV fixed-point accumulators
+    int64_t acc_ld;
+    const uint16_t* bias;  // [(hq + 2 hkv) hd] bf16 or null
+    float theta;           // RoPE base
+    float* q_out;          // optional tap: [batch][hq*hd] q after bias + RoPE
+    uint16_t* kc;          // [batch][hkv][max_ctx][hd]; the new k/v row is written at pos
+    uint16_t* vc;
     const int32_t* pos;    // [batch]; attend to [0, pos[b]]
     int64_t max_ctx;
     int hq, hkv, hd;
@@ -34,8 +39,19 @@ struct AttnArgs {
 
 __host__ __device__ inline size_t attn_smem_bytes(int G, int hd, int chunk) {
     (void)chunk;
-    // q [G][hd] + per-warp (m, l) [4][G][2] + per-warp o [4][G][hd] + flag
-    return sizeof(float) * ((size_t)G * hd + 4 * (size_t)G * 2 + 4 * (size_t)G * hd) + 16;
+    // q [G][hd] + per-warp (m, l) [4][G][2] + per-warp o [4][G][hd] + new k/v bf16 [2][hd] + flag
+    return sizeof(float) * ((size_t)G * hd + 4 * (size_t)G * 2 + 4 * (size_t)G * hd) + 4 * (size_t)hd + 16;
+}
+
+// RoPE (HF rotate_half) of the pair (i, i + hd/2) at position p, in fp64
+__device__ __forceinline__ void rope_pair(float& y1, float& y2, int i, int hd, int p, float theta) {
+    const double inv_freq = exp(-(2.0 * i / hd) * log((double)theta));
+    double sn, cn;
+    sincos((double)p * inv_freq, &sn, &cn);
+    const float r1 = (float)((double)y1 * cn - (double)y2 * sn);
+    const float r2 = (float)((double)y2 * cn + (double)y1 * sn);
+    y1 = r1;
+    y2 = r2;
 }
 
 template <int DPL>   // head dims per lane: hd = 32 * DPL (2 -> 64, 4 -> 128)
@@ -45,7 +61,7 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     float* sq = asmem;                         // [G][hd]
     float* sml = sq + G * hd;                  // [4][G][2]
     float* so = sml + 4 * G * 2;               // [4][G][hd]
-    int* sflag = reinterpret_cast<int*>(so + 4 * G * hd);
+    int* sflag = reinterpret_cast<int*>(so + 4 * G * hd + hd);   // after the new k/v bf16 rows
 
     const int bg = blockIdx.x, ch = blockIdx.y;
     const int b = bg / a.hkv, g = bg % a.hkv;
@@ -55,14 +71,65 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     const int n = max(0, min(a.chunk, ctx - start));
     const size_t kvbase = ((size_t)b * a.hkv + g) * a.max_ctx * hd;
 
-    // issue every K/V row load of this warp's positions before any math
+    const int half = hd / 2;
+    const int nq = a.hq * hd, nk = a.hkv * hd;
+    const int pnew = ctx - 1;                                   // the position appended this step
+    const bool has_new = pnew >= start && pnew < start + n;
+    uint16_t* snew = reinterpret_cast<uint16_t*>(so + 4 * G * hd);   // [2][hd] new k, v (bf16)
+    const unsigned long long* accb = a.acc + (size_t)b * a.acc_ld;
+    auto yval = [&](int col) -> float {
+        return fix_to_f(accb[col]) + (a.bias ? bf16f(a.bias[col]) : 0.f);
+    };
+    // q of my G heads (bias + RoPE), and, in the chunk holding pos, the new k / v row
+    for (int t = tid; t < G * half; t += kAttnThreads) {
+        const int j = t / half, i = t % half;
+        const int col = (g * G + j) * hd + i;
+        float y1 = yval(col), y2 = yval(col + half);
+        rope_pair(y1, y2, i, hd, pnew, a.theta);
+        sq[j * hd + i] = y1;
+        sq[j * hd + i + half] = y2;
+        if (a.q_out && ch == 0) {
+            a.q_out[(size_t)b * nq + col] = y1;
+            a.q_out[(size_t)b * nq + col + half] = y2;
+        }
+    }
+    if (has_new) {
+        uint16_t* kdst = a.kc + kvbase + (size_t)pnew * hd;
+        uint16_t* vdst = a.vc + kvbase + (size_t)pnew * hd;
+        for (int i = tid; i < half; i += kAttnThreads) {
+            float y1 = yval(nq + g * hd + i), y2 = yval(nq + g * hd + i + half);
+            rope_pair(y1, y2, i, hd, pnew, a.theta);
+            const uint16_t k1 = f2bf16_rne(y1), k2 = f2bf16_rne(y2);
+            snew[i] = k1;
+            snew[i + half] = k2;
+            kdst[i] = k1;
+            kdst[i + half] = k2;
+        }
+        for (int i = tid; i < hd; i += kAttnThreads) {
+            const uint16_t v = f2bf16_rne(yval(nq + nk + g * hd + i));
+            snew[hd + i] = v;
+            vdst[i] = v;
+        }
+    }
+    __syncthreads();
+
+    // issue every K/V row load of this warp's positions before any math (the new row comes
+    // from shared memory: this CTA just produced it)
     uint32_t kr[kAttnPosPerWarp][DPL / 2], vr[kAttnPosPerWarp][DPL / 2];
 #pragma unroll
     for (int i = 0; i < kAttnPosPerWarp; ++i) {
         const int p = warp + 4 * i;
         if (p < n) {
             const size_t off = kvbase + (size_t)(start + p) * hd + lane * DPL;
-            if constexpr (DPL == 4) {
+            if (start + p == pnew) {
+                const uint32_t* sk = reinterpret_cast<const uint32_t*>(snew + lane * DPL);
+                const uint32_t* sv = reinterpret_cast<const uint32_t*>(snew + hd + lane * DPL);
+#pragma unroll
+                for (int t = 0; t < DPL / 2; ++t) {
+                    kr[i][t] = sk[t];
+                    vr[i][t] = sv[t];
+                }
+            } else if constexpr (DPL == 4) {
                 const uint2 kk = *reinterpret_cast<const uint2*>(a.kc + off);
                 const uint2 vv = *reinterpret_cast<const uint2*>(a.vc + off);
                 kr[i][0] = kk.x; kr[i][1] = kk.y; vr[i][0] = vv.x; vr[i][1] = vv.y;
@@ -72,9 +139,6 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             }
         }
     }
-    for (int i = tid; i < G * hd; i += kAttnThreads)
-        sq[i] = a.q[(size_t)b * a.hq * hd + (size_t)g * G * hd + i];
-    __syncthreads();
 
     const float scale = 1.0f / sqrtf((float)hd);
     for (int j = 0; j < G; ++j) {

@@ -2,6 +2,7 @@
 // baseline.
 #pragma once
 #include "common.cuh"
+#include "gemv.cuh"
 
 namespace larosa {
 
@@ -106,6 +107,45 @@ __global__ void __launch_bounds__(kUnionThreads) union_kernel(const uint32_t* __
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) *nrows = acc;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Finalise fixed-point GEMV accumulators (gemv.cuh) and restore their zero state:
+//   out1[b][i] = [res1[b][i] +] fix^-1(acc1[b][i]) [+ bias1[i]];  acc1 = 0
+//   out2[b][i] = [res2[b][i] +] fix^-1(acc2[b][i])  (out2 may be null);  acc2 = 0 (if given)
+// ------------------------------------------------------------------------------------------
+struct FinalizeArgs {
+    int n, batch;
+    unsigned long long* acc1; int64_t acc1_ld;
+    const float* res1; int64_t res1_ld;
+    const uint16_t* bias1;
+    float* out1; int64_t out1_ld;
+    unsigned long long* acc2; int64_t acc2_ld;
+    const float* res2; int64_t res2_ld;
+    float* out2; int64_t out2_ld;
+};
+
+__global__ void finalize_kernel(const FinalizeArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t total = (int64_t)a.batch * a.n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(t / a.n), i = (int)(t % a.n);
+        if (a.acc1) {
+            unsigned long long* p = a.acc1 + (size_t)b * a.acc1_ld + i;
+            float y = fix_to_f(*p);
+            *p = 0ull;
+            if (a.res1) y = a.res1[(size_t)b * a.res1_ld + i] + y;
+            if (a.bias1) y += bf16f(a.bias1[i]);
+            a.out1[(size_t)b * a.out1_ld + i] = y;
+        }
+        if (a.acc2) {
+            unsigned long long* p = a.acc2 + (size_t)b * a.acc2_ld + i;
+            float y = fix_to_f(*p);
+            *p = 0ull;
+            if (a.out2) a.out2[(size_t)b * a.out2_ld + i] = (a.res2 ? a.res2[(size_t)b * a.res2_ld + i] : 0.f) + y;
+        }
     }
 }
 

@@ -1,326 +1,213 @@
 // gemv.cuh — sparse GEMV over the kept rows of a column-major weight (eq. after_merge,
 // PAPER.md:407-410; kernel recipe P:414: column-major storage, selective loads of the kept
-// columns), with the epilogues the decoder layer fuses into it.
+// columns).
 //
-//   y[b][o] = sum_{r < nrows} val(r, b) * W[row(r)][o]      (+ epilogue)
+//   acc[b][o] += fix( sum_{r in rows} val(r, b) * W[row(r)][o] )        (o in [0, d_out))
 //
-// Decomposition (B200: 148 SMs, 227 KB smem, thread-block clusters with DSMEM):
-//  * output columns are cut into tiles of TN (a multiple of 256); the kept-row list into CS
-//    contiguous chunks; the CS CTAs of one tile form a thread-block CLUSTER (CS <= 16), one
-//    CTA per SM with a ~200 KB shared-memory staging ring;
-//  * inside a CTA, warp (cs, rg) owns the 256-column slice cs of the tile and every RG-th
-//    kept row of the CTA's chunk.  Each kept row's 512-byte segment (contiguous in the
-//    [d_in][d_out] layout) is one coalesced warp-wide cp.async (LDGSTS, 16 B per lane) into
-//    the warp's private ring of 4-row stages, up to 16 stages deep.  A lane later reads back
-//    exactly the 16 bytes it copied, so the pipeline needs no barrier, only the lane's own
-//    cp.async groups.  (Measured on B200: the TMA engine retires about one bulk copy per
-//    ~50 cycles per SM, so 0.5-2 KB gathered row segments cap cp.async.bulk at 15-38 GB/s
-//    per SM, below the 44 GB/s/SM that 6.5 TB/s needs; per-thread cp.async has no such cap.)
-//  * fp32 FMAs on the bf16 weights (8 columns per lane); the kept rows' token values come
-//    from a 32-row register window broadcast with shfl;
-//  * the split-K reduction is deterministic and never touches global memory: each CTA
-//    reduces its RG row groups in shared memory, a cluster barrier, then CTA q sums its
-//    share of column PAIRS over the CS CTAs in fixed order through distributed shared
-//    memory (ld.shared::cluster) and runs the epilogue on complete values (pairs
-//    (c, c + po) keep RoPE halves and gate/up blocks together).
+// The kernel only streams and accumulates; it has no tail.  Partial sums are added into
+// 64-bit fixed-point accumulators (32 fractional bits) with red.global.add.u64: integer
+// addition is associative, so the result is bit-identical whatever order the CTAs finish
+// in (deterministic without a fixed reduction tree), and no CTA waits for another.  The
+// consumer of y (the next kernel: Top-K, attention, finalize) converts acc -> fp32, applies
+// the epilogue (bias / residual / RoPE / SiLU*up) and re-zeroes the accumulators.
+// Fixed-point error: <= 2^-33 absolute per partial (|y| must stay < 2^31).
+//
+// Decomposition (B200: 148 SMs): grid = (column slices of 256, n_splits) with 8 warps per
+// CTA, ~2 CTAs per SM.  CTA (slice, s) owns the s-th contiguous chunk of the kept-row list;
+// warp w takes every 8th row of it.  Each kept row's 512-byte segment (contiguous in the
+// [d_in][d_out] layout) is one coalesced warp-wide cp.async (LDGSTS, 16 B per lane) into the
+// warp's private 4-stage ring; a lane later reads back exactly the 16 bytes it copied, so
+// the pipeline needs no barrier, only the lane's own cp.async groups.  (Measured on B200:
+// the TMA engine retires about one bulk copy per ~50 cycles per SM, so 0.5-2 KB gathered
+// row segments cap cp.async.bulk at 15-38 GB/s per SM, below the 44 GB/s/SM that 6.5 TB/s
+// needs; per-thread cp.async has no such cap.)  Math: bf16 pairs widen with one ALU op per
+// value and accumulate with paired fp32 FMAs (FFMA2).  The 8 warps' partials are summed in
+// shared memory in fixed order before the single red per column.
 #pragma once
 #include "common.cuh"
 
 namespace larosa {
 
-enum EpKind : int { EP_STORE = 0, EP_RESID = 1, EP_SILU_GU = 2, EP_QKV_ROPE = 3 };
-
-constexpr int kGuBlock = 64;         // == LAROSA_GU_BLOCK
-constexpr int kWarpCols = 256;       // columns per warp slice (8 per lane)
-constexpr int kStageRows = 4;        // rows per stage per warp (one 512-byte copy each)
-constexpr int kStageBytes = kStageRows * kWarpCols * 2;
-constexpr int kGemvMaxWarps = 16;
+constexpr int kGuBlock = 64;          // == LAROSA_GU_BLOCK
+constexpr int kSliceCols = 256;       // columns per CTA (8 per lane)
+constexpr int kGemvWarps = 8;
+constexpr int kStageRows = 4;         // rows per stage (one 512-byte warp copy each)
+constexpr int kStages = 4;            // ring depth per warp
+constexpr int kWarpRingBytes = kStages * kStageRows * kSliceCols * 2;   // 8 KB
+constexpr double kFixScale = 4294967296.0;                              // 2^32
 
 struct GemvArgs {
     const uint16_t* W;
     int64_t ld;
     int d_out;
     const int32_t* rows;   // kept row indices (ascending); nullptr -> dense (row r = r)
-    const float* vals;     // val(r, b) = vals[r * vs_r + b * vs_b]
-    int64_t vs_r, vs_b;
     int nrows;             // row count when nrows_dev == nullptr
     const int* nrows_dev;  // device row count (batch > 1 union), or nullptr
+    const float* vals;     // val(r, b) = vals[r * vs_r + b * vs_b] (+ vacc, see below)
+    int64_t vs_r, vs_b;
+    const unsigned long long* vacc;   // optional (dense mode): val += fix^-1(vacc[b * vacc_ld + r])
+    int64_t vacc_ld;
     int batch;             // real tokens (<= template BP)
-    int tn, rg, stages;    // tile width, row groups, ring depth (stages per warp)
-    // epilogue
-    int ep;
-    const uint16_t* bias;  // [d_out] bf16 or nullptr
-    const float* resid;    // EP_RESID: [batch][resid_ld]
-    int64_t resid_ld;
-    float* out;            // [batch][out_ld]
-    int64_t out_ld;
-    // EP_QKV_ROPE
-    int hq, hkv, hd;
-    float theta;
-    const int32_t* pos;    // [batch]
-    uint16_t* kc;          // [batch][hkv][max_ctx][hd]
-    uint16_t* vc;
-    int64_t max_ctx;
+    int n_splits;
+    unsigned long long* acc;          // [batch][acc_ld] fixed-point output accumulators
+    int64_t acc_ld;
 };
 
-__host__ __device__ constexpr size_t gemv_ring_bytes(int nwarps, int stages) {
-    return (size_t)nwarps * stages * kStageBytes;
-}
-// tail scratch (aliases the ring): part [RG][BP][TN] + pred [BP][TN] + fin [TN][BP]
-__host__ __device__ constexpr size_t gemv_tail_bytes(int rg, int bp, int tn) {
-    return ((size_t)rg * bp * tn + 2 * (size_t)bp * tn) * 4;
-}
-__host__ __device__ constexpr size_t gemv_smem_bytes(int nwarps, int stages, int rg, int bp, int tn) {
-    return 1024 + (gemv_ring_bytes(nwarps, stages) > gemv_tail_bytes(rg, bp, tn) ? gemv_ring_bytes(nwarps, stages)
-                                                                                   : gemv_tail_bytes(rg, bp, tn));
+__host__ __device__ constexpr size_t gemv_smem_bytes(int bp) {
+    return (size_t)kGemvWarps * kWarpRingBytes > (size_t)kGemvWarps * bp * kSliceCols * 4
+               ? (size_t)kGemvWarps * kWarpRingBytes
+               : (size_t)kGemvWarps * bp * kSliceCols * 4;
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+__device__ __forceinline__ float fix_to_f(unsigned long long a) {
+    return (float)((double)(long long)a * (1.0 / kFixScale));
+}
+__device__ __forceinline__ unsigned long long f_to_fix(float v) {
+    return (unsigned long long)__float2ll_rn(v * 4294967296.0f);
+}
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
-// cp.async (LDGSTS): 16 bytes global -> shared, bypassing L1 (.cg)
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+// cp.async (LDGSTS): 16 bytes global -> shared, L1 bypass (.cg)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+        "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(smem_u32(smem_dst)),
+        "l"(gsrc), "r"((int)pred)
+        : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-constexpr int kMaxStagesM1 = 15;   // ring depth <= 16
-// wait until at most n of this thread's most recent groups are pending (n runtime <= MAXN)
-template <int MAXN>
-__device__ __forceinline__ void cp_async_wait(int n) {
-    if constexpr (MAXN <= 0) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-    } else {
-        if (n >= MAXN) asm volatile("cp.async.wait_group %0;" ::"n"(MAXN) : "memory");
-        else cp_async_wait<MAXN - 1>(n);
-    }
-}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem_addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
+// paired fp32 FMA (FFMA2): {a.x, a.y} = {w0, w1} * {v, v} + {a.x, a.y}
+__device__ __forceinline__ void ffma2(float2& a, float w0, float w1, float v) {
+    unsigned long long r, wa, va, aa;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(wa) : "f"(w0), "f"(w1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(va) : "f"(v));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(a.x), "f"(a.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(wa), "l"(va), "l"(aa));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
 }
 
 template <int BP>
-__global__ void __launch_bounds__(BP >= 8 ? 256 : kGemvMaxWarps * 32, 1) gemv_kernel(const GemvArgs a) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const int CS = gridDim.x;                 // cluster spans x: blockIdx.x == rank
-    const int split = blockIdx.x, tile = blockIdx.y;
-    const int TN = a.tn, RG = a.rg, ST = a.stages;
-    const int slices = TN / kWarpCols;
-    const int nwarps = slices * RG;
+__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int slice = blockIdx.x, split = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cs = warp % slices, rg = warp / slices;
-    unsigned char* ring = smem + 1024;                           // [nwarps][ST][kStageBytes]
-    float* part = reinterpret_cast<float*>(ring);                // reused: [RG][BP][TN]
 
     pdl_wait();       // rows / vals / nrows come from the previous kernel
     pdl_trigger();
 
     const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
-    const int rps = (nrows + CS - 1) / CS;
+    const int rps = (nrows + a.n_splits - 1) / a.n_splits;
     const int r_begin = min(nrows, split * rps);
     const int r_end = min(nrows, r_begin + rps);
-    const int n_my = r_end - r_begin > rg ? (r_end - r_begin - rg + RG - 1) / RG : 0;   // my rows: r_begin + rg + RG*m
-    const int col0 = tile * TN + cs * kWarpCols;
-    const bool lane_on = col0 + lane * 8 < a.d_out;     // this lane's 16-byte chunk exists
+    // my rows: r_begin + warp + 8*m, m in [0, n_my)
+    const int n_my = r_end - r_begin > warp ? (r_end - r_begin - warp + kGemvWarps - 1) / kGemvWarps : 0;
+    const int col0 = slice * kSliceCols + lane * 8;
+    const bool lane_on = col0 < a.d_out;          // d_out % 8 == 0: a lane's chunk is all-in or all-out
     const int n_st = (n_my + kStageRows - 1) / kStageRows;
-    // each lane copies, and later reads back, only its own 16-byte chunk of every row: the
-    // staging needs no cross-lane synchronisation, only the lane's own cp.async groups
-    unsigned char* mychunk = ring + (size_t)warp * ST * kStageBytes + lane * 16;
-    const uint16_t* wcol = a.W + col0 + lane * 8;
+    unsigned char* mychunk = smem + (size_t)warp * kWarpRingBytes + lane * 16;
+    const uint16_t* wcol = a.W + col0;
 
-    // Row indices / token values are read in 32-row windows (lane j holds my-row base + j),
-    // double-buffered: the next window's loads are in flight while the current one is used,
-    // so the steady state never waits on them.
+    // rows / values in 32-row windows (lane j holds my-row base + j), double-buffered
     auto load_row = [&](int m) -> int {
-        const int r = r_begin + rg + RG * m;
+        const int r = r_begin + warp + kGemvWarps * m;
         return m < n_my ? (a.rows ? __ldg(a.rows + r) : r) : 0;
     };
-    int iw_base = 0;
-    int iw_row = load_row(lane);
-    int iw_next = load_row(32 + lane);
-    auto issue = [&](int st) {
-        if (st < n_st) {
-            const int m0 = st * kStageRows;
-            if (m0 >= iw_base + 32) {        // advance one window (kStageRows divides 32)
-                iw_base += 32;
-                iw_row = iw_next;
-                iw_next = load_row(iw_base + 32 + lane);
-            }
-            const int gc = min(kStageRows, n_my - m0);
-            unsigned char* dst = mychunk + (size_t)(st % ST) * kStageBytes;
-#pragma unroll
-            for (int g = 0; g < kStageRows; ++g) {
-                const int row = __shfl_sync(0xffffffffu, iw_row, (m0 - iw_base + g) & 31);
-                if (g < gc && lane_on) cp_async16(dst + g * (kWarpCols * 2), wcol + (size_t)row * a.ld);
-            }
-        }
-        cp_async_commit();   // (possibly empty) group per stage keeps the group count uniform
-    };
-    for (int st = 0; st < ST; ++st) issue(st);
-
-    float acc[BP][8];
-#pragma unroll
-    for (int b = 0; b < BP; ++b)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
-
     auto load_vals = [&](int m, float* v) {
-        const size_t r = (size_t)(r_begin + rg + RG * m);
+        const int r = r_begin + warp + kGemvWarps * m;
 #pragma unroll
-        for (int b = 0; b < BP; ++b)
-            v[b] = (m < n_my && b < a.batch) ? __ldg(a.vals + r * a.vs_r + (size_t)b * a.vs_b) : 0.f;
+        for (int b = 0; b < BP; ++b) {
+            float x = 0.f;
+            if (m < n_my && b < a.batch) {
+                x = __ldg(a.vals + (size_t)r * a.vs_r + (size_t)b * a.vs_b);
+                if (a.vacc) x += fix_to_f(a.vacc[(size_t)b * a.vacc_ld + r]);
+            }
+            v[b] = x;
+        }
     };
-    int vw_base = 0;
+    int iw_row = load_row(lane), iw_next = load_row(32 + lane);
     float vwin[BP], vnext[BP];
     load_vals(lane, vwin);
     load_vals(32 + lane, vnext);
+
+    // stage st covers my-rows [4 st, 4 st + 4); window w = st / 8 covers my-rows [32 w, 32 w + 32)
+    auto issue = [&](int st) {
+        if (st < n_st) {
+            if (st > 0 && (st & 7) == 0) {
+                iw_row = iw_next;
+                iw_next = load_row(st * kStageRows + 32 + lane);
+            }
+            unsigned char* dst = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
+#pragma unroll
+            for (int g = 0; g < kStageRows; ++g) {
+                const int m = st * kStageRows + g;
+                const int row = __shfl_sync(0xffffffffu, iw_row, m & 31);
+                cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < n_my);
+            }
+        }
+        cp_async_commit();   // one (possibly empty) group per stage keeps the count uniform
+    };
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) issue(st);
+
+    float2 acc[BP][4];
+#pragma unroll
+    for (int b = 0; b < BP; ++b)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[b][j] = make_float2(0.f, 0.f);
+
     for (int st = 0; st < n_st; ++st) {
-        const int m0 = st * kStageRows;
-        if (m0 >= vw_base + 32) {
-            vw_base += 32;
+        if (st > 0 && (st & 7) == 0) {
 #pragma unroll
             for (int b = 0; b < BP; ++b) vwin[b] = vnext[b];
-            load_vals(vw_base + 32 + lane, vnext);
+            load_vals(st * kStageRows + 32 + lane, vnext);
         }
-        const int gc = min(kStageRows, n_my - m0);
-        cp_async_wait<kMaxStagesM1>(ST - 1);    // this lane's chunks of stage st have landed
-        const unsigned char* src = mychunk + (size_t)(st % ST) * kStageBytes;
+        cp_async_wait<kStages - 1>();          // this lane's chunks of stage st have landed
+        const unsigned char* src = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
 #pragma unroll
         for (int g = 0; g < kStageRows; ++g) {
-            if (g < gc) {
-                const uint4 w = lds128(src + g * (kWarpCols * 2));
-                float wf[8];
-                wf[0] = bf16lo(w.x); wf[1] = bf16hi(w.x);
-                wf[2] = bf16lo(w.y); wf[3] = bf16hi(w.y);
-                wf[4] = bf16lo(w.z); wf[5] = bf16hi(w.z);
-                wf[6] = bf16lo(w.w); wf[7] = bf16hi(w.w);
-                const int src_lane = (m0 - vw_base + g) & 31;
+            const int m = st * kStageRows + g;
+            const uint4 w = lds128(src + g * (kSliceCols * 2));
+            const float w0 = bf16lo(w.x), w1 = bf16hi(w.x), w2 = bf16lo(w.y), w3 = bf16hi(w.y);
+            const float w4 = bf16lo(w.z), w5 = bf16hi(w.z), w6 = bf16lo(w.w), w7 = bf16hi(w.w);
+            if (m >= n_my) break;                // short last stage (warp-uniform)
 #pragma unroll
-                for (int b = 0; b < BP; ++b) {
-                    const float v = __shfl_sync(0xffffffffu, vwin[b], src_lane);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[b][j] = fmaf(v, wf[j], acc[b][j]);
-                }
+            for (int b = 0; b < BP; ++b) {
+                const float v = __shfl_sync(0xffffffffu, vwin[b], m & 31);
+                ffma2(acc[b][0], w0, w1, v);
+                ffma2(acc[b][1], w2, w3, v);
+                ffma2(acc[b][2], w4, w5, v);
+                ffma2(acc[b][3], w6, w7, v);
             }
         }
-        issue(st + ST);
+        issue(st + kStages);
     }
-    cp_async_wait<kMaxStagesM1>(0);
-    if (!lane_on) {
-#pragma unroll
-        for (int b = 0; b < BP; ++b)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
-    }
+    cp_async_wait<0>();
+    __syncthreads();   // every warp is done with its ring (the partials alias it)
 
-    // ---------------- publish this CTA's partial tile: part[rg][b][cs*256 + lane*8 + j] --------
-    __syncthreads();   // every warp is done reading its ring (part aliases it)
+    // fixed-order sum of the 8 warps' partials, then one fixed-point red per column
+    float* part = reinterpret_cast<float*>(smem);   // [8][BP][256]
 #pragma unroll
     for (int b = 0; b < BP; ++b) {
-        float* p = part + ((size_t)rg * BP + b) * TN + cs * kWarpCols + lane * 8;
-        reinterpret_cast<float4*>(p)[0] = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
-        reinterpret_cast<float4*>(p)[1] = make_float4(acc[b][4], acc[b][5], acc[b][6], acc[b][7]);
+        float* p = part + ((size_t)warp * BP + b) * kSliceCols + lane * 8;
+        reinterpret_cast<float4*>(p)[0] = make_float4(acc[b][0].x, acc[b][0].y, acc[b][1].x, acc[b][1].y);
+        reinterpret_cast<float4*>(p)[1] = make_float4(acc[b][2].x, acc[b][2].y, acc[b][3].x, acc[b][3].y);
     }
     __syncthreads();
-    // local row-group reduction (fixed order): pred[b][c] = sum_g part[g][b][c]
-    const int nthreads = nwarps * 32;
-    float* pred = part + (size_t)RG * BP * TN;             // [BP][TN]
-    float* fin = pred + (size_t)BP * TN;                    // [2 * pairs-per-CTA][BP]
-    for (int t = threadIdx.x; t < a.batch * TN; t += nthreads) {
-        const int b = t / TN, c = t % TN;
-        float v = 0.f;
-        for (int g = 0; g < RG; ++g) v += part[((size_t)g * BP + b) * TN + c];
-        pred[(size_t)b * TN + c] = v;
-    }
-    cluster_sync_all();
-
-    // ---------------- cluster reduction over the CS CTAs (fixed order, DSMEM) ----------------
-    const int po = (a.ep == EP_QKV_ROPE) ? (a.hd >> 1) : kGuBlock;   // pair offset
-    const int npairs = TN >> 1;
-    const int ppc = (npairs + CS - 1) / CS;                            // pairs per CTA
-    const int p_begin = min(npairs, split * ppc), p_end = min(npairs, p_begin + ppc);
-    const int nmine = p_end - p_begin;
-    const uint32_t pred_local = smem_u32(pred);
-    for (int t = threadIdx.x; t < nmine * 2 * a.batch; t += nthreads) {
-        const int b = t % a.batch;
-        const int pi = (t / a.batch) >> 1, half = (t / a.batch) & 1;
-        const int pj = p_begin + pi;
-        const int c = (pj / po) * (2 * po) + (pj % po) + half * po;
-        const uint32_t off = (uint32_t)(((size_t)b * TN + c) * 4);
-        float v[16];
+    const int c = threadIdx.x;                     // 256 threads <-> 256 columns
+    const int o = slice * kSliceCols + c;
+    if (o < a.d_out && r_end > r_begin) {
+        for (int b = 0; b < a.batch; ++b) {
+            float s = 0.f;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = q < CS ? ld_dsmem(cluster_map(pred_local + off, (uint32_t)q)) : 0.f;
-        float y = 0.f;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) y += v[q];
-        fin[(size_t)(pi * 2 + half) * BP + b] = y;
-    }
-    __syncthreads();
-
-    // ---------------- epilogue on complete column pairs (c1, c1 + po) ----------------
-    for (int t = threadIdx.x; t < nmine * a.batch; t += nthreads) {
-        const int b = t % a.batch, pi = t / a.batch;
-        const int pj = p_begin + pi;
-        const int c1 = (pj / po) * (2 * po) + (pj % po);
-        const int c2 = c1 + po;
-        const int o1 = tile * TN + c1, o2 = tile * TN + c2;
-        float y1 = fin[(size_t)(pi * 2) * BP + b];
-        float y2 = fin[(size_t)(pi * 2 + 1) * BP + b];
-        const bool in1 = o1 < a.d_out, in2 = o2 < a.d_out;
-        if (a.bias && a.ep != EP_SILU_GU) {
-            if (in1) y1 += bf16f(a.bias[o1]);
-            if (in2) y2 += bf16f(a.bias[o2]);
-        }
-        if (a.ep == EP_STORE || a.ep == EP_RESID) {
-            float* op = a.out + (size_t)b * a.out_ld;
-            if (a.ep == EP_RESID) {
-                const float* rp = a.resid + (size_t)b * a.resid_ld;
-                if (in1) y1 = rp[o1] + y1;
-                if (in2) y2 = rp[o2] + y2;
-            }
-            if (in1) op[o1] = y1;
-            if (in2) op[o2] = y2;
-        } else if (a.ep == EP_SILU_GU) {
-            // fused block t = o1 / 128: gate [t*64, t*64+64) then up of the same rows
-            const int i = (o1 / (2 * kGuBlock)) * kGuBlock + (o1 % (2 * kGuBlock));
-            a.out[(size_t)b * a.out_ld + i] = silu_f(y1) * y2;
-        } else {   // EP_QKV_ROPE: (o1, o2) = head dims (i, i + hd/2) of one head
-            const int hd = a.hd;
-            const int nq = a.hq * hd, nk = a.hkv * hd;
-            const int p = a.pos[b];
-            float r1 = y1, r2 = y2;
-            if (o1 < nq + nk) {
-                const int i = o1 % hd;
-                const double inv_freq = exp(-(2.0 * i / hd) * log((double)a.theta));
-                double sn, cn;
-                sincos((double)p * inv_freq, &sn, &cn);
-                r1 = (float)((double)y1 * cn - (double)y2 * sn);
-                r2 = (float)((double)y2 * cn + (double)y1 * sn);
-            }
-            if (o1 < nq) {
-                float* op = a.out + (size_t)b * a.out_ld;
-                op[o1] = r1;
-                op[o2] = r2;
-            } else {
-                const bool isk = o1 < nq + nk;
-                const int oo = o1 - (isk ? nq : nq + nk);
-                const int kvh = oo / hd, i = oo % hd;
-                uint16_t* dst = (isk ? a.kc : a.vc) + (((size_t)b * a.hkv + kvh) * a.max_ctx + p) * hd;
-                dst[i] = f2bf16_rne(r1);
-                dst[i + (hd >> 1)] = f2bf16_rne(r2);
-            }
+            for (int w = 0; w < kGemvWarps; ++w) s += part[((size_t)w * BP + b) * kSliceCols + c];
+            red_add_u64(a.acc + (size_t)b * a.acc_ld + o, f_to_fix(s));
         }
     }
-    cluster_sync_all();   // keep every CTA's partial alive until all peers finished reading
 }
 
 }  // namespace larosa

@@ -94,12 +94,12 @@ cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 // ============================================================================== workspace
-// Every workspace starts with a fixed header of self-resetting counters (zero on entry and
-// on exit of every call).  All other regions come after it, so calls with different
-// shapes can share one workspace without ever clobbering the counters' zero state.
-constexpr size_t kCounterHeaderWords = 8192;   // GEMV tile tickets [0, 4096), attention [4096, 8192)
-constexpr size_t kGemvCounterBase = 0;
-constexpr size_t kAttnCounterBase = 4096;
+// Every workspace starts with a fixed header of self-resetting counters, followed by the
+// call's fixed-point GEMV accumulators; both are zero at rest (kernels restore the zeros),
+// so the caller zero-fills a workspace once.  A workspace must be reused only for calls of
+// the same kind and shapes (other layouts would place live data where accumulators were).
+constexpr size_t kCounterHeaderWords = 8192;   // attention tickets
+constexpr size_t kAttnCounterBase = 0;
 
 struct Carver {
     char* base;      // nullptr -> size query
@@ -122,7 +122,7 @@ int pad_batch(int b) { return b <= 1 ? 1 : b <= 2 ? 2 : b <= 4 ? 4 : b <= 8 ? 8 
 
 // ============================================================================== GEMV plan
 struct GemvPlan {
-    int tn, cs, rg, nwarps, stages, n_tiles;
+    int n_slices, n_splits;
     size_t smem;
 };
 
@@ -131,83 +131,30 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 
-constexpr size_t kGemvSmemBudget = 200 * 1024;
-
-// Tile width TN (multiple of 256) x cluster size CS so that n_tiles * CS CTAs fill the SMs
-// once (one CTA per SM, ~200 KB ring); prefer the portable cluster size 8.
+// 256-column slices x kept-row splits, about `per_sm` 256-thread CTAs per SM in one wave;
+// at least 16 rows per split so each warp has a few rows to pipeline.
 GemvPlan plan_gemv(int64_t d_out, int64_t nrows_max, int bp) {
-    static const int force_cs = env_int("LAROSA_GEMV_CS", 0);     // tuning knobs (0 = auto)
-    static const int force_tn = env_int("LAROSA_GEMV_TN", 0);
-    static const int force_rg = env_int("LAROSA_GEMV_RG", 0);
-    const int sms = sm_count();
-    const int64_t max_cs_rows = std::max<int64_t>(1, nrows_max / 8);
-    GemvPlan best = {256, 1, 1, 1, 2, (int)((d_out + 255) / 256), 0};
-    int best_ctas = 0;
-    const int max_warps = bp >= 8 ? 8 : kGemvMaxWarps;   // matches the kernel's launch bounds
-    const int cs_order[5] = {8, 16, 4, 2, 1};
-    for (int ci = 0; ci < 5; ++ci) {
-        const int cs = cs_order[ci];
-        if (force_cs && cs != force_cs) continue;
-        if (cs > max_cs_rows && cs > 1) continue;
-        for (int tn = 256; tn <= 4096; tn += 256) {
-            if (force_tn && tn != force_tn) continue;
-            const int slices = tn / 256;
-            if (tn - 256 >= d_out) break;
-            const int tiles = (int)((d_out + tn - 1) / tn);
-            const int ctas = tiles * cs;
-            if (ctas > sms) continue;
-            if (slices > max_warps) break;
-            int rg = std::max(1, std::min(8, 8 / slices));
-            if (force_rg) rg = force_rg;
-            rg = std::min(rg, max_warps / slices);
-            if (rg < 1 || rg * slices > max_warps) continue;
-            if (gemv_tail_bytes(rg, bp, tn) > kGemvSmemBudget) continue;
-            if (ctas > best_ctas) {
-                best_ctas = ctas;
-                best.tn = tn;
-                best.cs = cs;
-                best.rg = rg;
-                best.n_tiles = tiles;
-            }
-        }
-    }
-    best.nwarps = (best.tn / 256) * best.rg;
-    int st = (int)((kGemvSmemBudget - 1024) / ((size_t)best.nwarps * kStageBytes));
-    st = std::max(2, std::min(st, std::min(16, 128 / best.nwarps)));
-    best.stages = st;
-    best.smem = gemv_smem_bytes(best.nwarps, st, best.rg, bp, best.tn);
-    return best;
+    static const int per_sm_env = env_int("LAROSA_GEMV_CTAS_PER_SM", 0);   // tuning knob (0 = auto)
+    GemvPlan p;
+    p.n_slices = (int)((d_out + kSliceCols - 1) / kSliceCols);
+    p.smem = gemv_smem_bytes(bp);
+    const int per_sm = per_sm_env > 0 ? per_sm_env : (bp <= 4 ? 3 : 1);
+    const int target = sm_count() * per_sm;
+    const int by_target = std::max(1, (target + p.n_slices / 2) / p.n_slices);
+    const int by_rows = (int)std::max<int64_t>(1, nrows_max / 16);
+    p.n_splits = std::min(by_target, by_rows);
+    return p;
 }
 
 template <int BP>
-larosa_status launch_gemv_bp(GemvArgs a, const GemvPlan& p, cudaStream_t st) {
+larosa_status launch_gemv_bp(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
     auto kern = gemv_kernel<BP>;
     static bool attr_done = false;
     if (!attr_done) {
-        LAROSA_TRY(cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
-                              "cudaFuncSetAttribute(gemv smem)"));
-        LAROSA_TRY(cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                              "cudaFuncSetAttribute(gemv cluster)"));
+        LAROSA_TRY(cuda_check(allow_smem(kern, gemv_smem_bytes(BP)), "cudaFuncSetAttribute(gemv)"));
         attr_done = true;
     }
-    a.tn = p.tn;
-    a.rg = p.rg;
-    a.stages = p.stages;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.cs, p.n_tiles);
-    cfg.blockDim = dim3(p.nwarps * 32);
-    cfg.dynamicSmemBytes = p.smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p.cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "gemv launch");
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvWarps * 32), p.smem, st, a), "gemv launch");
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
@@ -223,11 +170,10 @@ larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStre
 GemvArgs gemv_args_base() {
     GemvArgs a;
     memset(&a, 0, sizeof(a));
-    a.ep = EP_STORE;
     return a;
 }
 
-// ============================================================================== Top-K launch
+// ============================================================================== small launches
 larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
     const size_t smem = topk_smem_bytes(a.d);
     static bool attr_done = false;
@@ -238,12 +184,31 @@ larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
     return cuda_check(launch(topk_kernel, dim3(batch), dim3(kTopkThreads), smem, st, a), "topk launch");
 }
 
+TopkKernelArgs topk_args_base() {
+    TopkKernelArgs t;
+    memset(&t, 0, sizeof(t));
+    t.mode = SRC_PLAIN;
+    return t;
+}
+
 larosa_status launch_union(const uint32_t* mask, int nwords, int batch, int bp, const float* vals, int64_t k, int d,
                            int32_t* rows, float* V, int* nrows, cudaStream_t st) {
     const int grid = (nwords + 31) / 32;
     return cuda_check(launch(union_kernel, dim3(grid), dim3(kUnionThreads), 0, st, mask, nwords, batch, bp, vals, k, d,
                              rows, V, nrows),
                       "union launch");
+}
+
+larosa_status launch_finalize(const FinalizeArgs& f, cudaStream_t st) {
+    const int64_t total = (int64_t)f.batch * f.n;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 2 * sm_count()));
+    return cuda_check(launch(finalize_kernel, dim3(grid), dim3(256), 0, st, f), "finalize launch");
+}
+
+FinalizeArgs finalize_args_base() {
+    FinalizeArgs f;
+    memset(&f, 0, sizeof(f));
+    return f;
 }
 
 }  // namespace
@@ -295,9 +260,11 @@ extern "C" larosa_status larosa_solve_alpha(double a1, double a3, double m, doub
 }
 
 // ============================================================================== sparse GEMV
-static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t k, uint32_t** mask, int32_t** rows,
-                              float** V, int** nrows) {
+static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t d_out, unsigned long long** acc,
+                              uint32_t** mask, int32_t** rows, float** V, int** nrows) {
     const int bp = pad_batch(batch);
+    unsigned long long* a = c.take<unsigned long long>((size_t)batch * d_out);
+    if (acc) *acc = a;
     if (batch > 1) {
         const int64_t nw = (d_in + 31) / 32;
         uint32_t* m = c.take<uint32_t>((size_t)batch * nw);
@@ -314,8 +281,7 @@ static void carve_sparse_gemv(Carver& c, int32_t batch, int64_t d_in, int64_t k,
 extern "C" size_t larosa_sparse_gemv_workspace_size(int32_t batch, int64_t d_in, int64_t k, int64_t d_out) {
     if (batch < 1 || d_in <= 0 || d_out <= 0 || k < 0) return 0;
     Carver c(nullptr);
-    (void)d_out;
-    carve_sparse_gemv(c, batch, d_in, k, nullptr, nullptr, nullptr, nullptr);
+    carve_sparse_gemv(c, batch, d_in, d_out, nullptr, nullptr, nullptr, nullptr, nullptr);
     return c.size();
 }
 
@@ -331,7 +297,8 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "sparse_gemv: k=%lld outside [0, d_in=%lld]", (long long)k, (long long)d_in);
     if (ld < d_out) return fail(LAROSA_ESHAPE, "sparse_gemv: ld < d_out");
     if (ld % 8 || d_out % 8) return fail(LAROSA_EUNSUPPORTED, "sparse_gemv: ld and d_out must be multiples of 8");
-    if (!aligned16(W) || !aligned16(y) || (bias && !aligned16(bias)))
+    if (!aligned16(W)) return fail(LAROSA_EINVAL, "sparse_gemv: W must be 16-byte aligned");
+    if (!aligned16(y) || (bias && !aligned16(bias)))
         return fail(LAROSA_EINVAL, "sparse_gemv: W, y, bias must be 16-byte aligned");
     if (d_in > INT32_MAX || d_out > INT32_MAX) return fail(LAROSA_EUNSUPPORTED, "sparse_gemv: dims too large");
     const size_t need = larosa_sparse_gemv_workspace_size(batch, d_in, k, d_out);
@@ -339,24 +306,24 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
     Carver c(ws);
+    unsigned long long* acc = nullptr;
     uint32_t* mask = nullptr;
     int32_t* rows = nullptr;
     float* V = nullptr;
     int* nrows = nullptr;
-    carve_sparse_gemv(c, batch, d_in, k, &mask, &rows, &V, &nrows);
+    carve_sparse_gemv(c, batch, d_in, d_out, &acc, &mask, &rows, &V, &nrows);
     const int bp = pad_batch(batch);
     const int64_t nrows_max = batch == 1 ? k : std::min<int64_t>(d_in, (int64_t)batch * k);
-    GemvPlan p = plan_gemv(d_out, nrows_max, bp);
+    const GemvPlan p = plan_gemv(d_out, nrows_max, bp);
 
     GemvArgs a = gemv_args_base();
     a.W = W;
     a.ld = ld;
     a.d_out = (int)d_out;
     a.batch = batch;
-    a.bias = bias;
-    a.out = y;
-    a.out_ld = d_out;
-    a.ep = EP_STORE;
+    a.n_splits = p.n_splits;
+    a.acc = acc;
+    a.acc_ld = d_out;
     if (batch == 1) {
         a.rows = idx;
         a.vals = vals;
@@ -379,54 +346,37 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
         a.vs_b = 1;
         a.nrows_dev = nrows;
     }
-    return launch_gemv(a, p, bp, st);
+    LAROSA_TRY(launch_gemv(a, p, bp, st));
+    FinalizeArgs f = finalize_args_base();
+    f.n = (int)d_out;
+    f.batch = batch;
+    f.acc1 = acc;
+    f.acc1_ld = d_out;
+    f.bias1 = bias;
+    f.out1 = y;
+    f.out1_ld = d_out;
+    return launch_finalize(f, st);
 }
 
 extern "C" larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info) {
     if (!info || d_out <= 0 || nrows_max < 0 || batch < 1 || batch > LAROSA_MAX_BATCH)
         return fail(LAROSA_EINVAL, "gemv_plan_info: bad arguments");
-    const int bp = pad_batch(batch);
-    const GemvPlan p = plan_gemv(d_out, nrows_max, bp);
-    info[0] = p.tn;
-    info[1] = p.cs;
-    info[2] = p.rg;
-    info[3] = p.nwarps;
-    info[4] = p.stages;
-    info[5] = p.n_tiles;
+    const GemvPlan p = plan_gemv(d_out, nrows_max, pad_batch(batch));
+    info[0] = kSliceCols;
+    info[1] = p.n_slices;
+    info[2] = p.n_splits;
+    info[3] = kGemvWarps;
+    info[4] = kStages;
+    info[5] = kStageRows;
     info[6] = (int32_t)p.smem;
-    info[7] = 0;
-    int dev = -1;
-    if (cudaGetDevice(&dev) == cudaSuccess) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(p.cs, p.n_tiles);
-        cfg.blockDim = dim3(p.nwarps * 32);
-        cfg.dynamicSmemBytes = p.smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = p.cs;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int n = 0;
-        cudaError_t e;
-        switch (bp) {
-            case 1: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<1>, &cfg); break;
-            case 2: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<2>, &cfg); break;
-            case 4: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<4>, &cfg); break;
-            case 8: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<8>, &cfg); break;
-            default: e = cudaOccupancyMaxActiveClusters(&n, gemv_kernel<16>, &cfg); break;
-        }
-        if (e == cudaSuccess) info[7] = n;
-        cudaGetLastError();
-    }
+    info[7] = p.n_slices * p.n_splits;
     return LAROSA_OK;
 }
 
 // ============================================================================== rotate + Top-K
-static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, float** xr) {
-    float* x = c.take<float>((size_t)batch * d);
-    if (xr) *xr = x;
+static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, unsigned long long** acc) {
+    unsigned long long* a = c.take<unsigned long long>((size_t)batch * d);
+    if (acc) *acc = a;
 }
 
 extern "C" size_t larosa_rotate_topk_workspace_size(int32_t batch, int64_t d) {
@@ -447,48 +397,48 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
     if (d > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "rotate_topk: d > %d", LAROSA_MAX_DIM);
     if (k < 0 || k > d) return fail(LAROSA_EINVAL, "rotate_topk: k outside [0, d]");
     if (R && d % 8) return fail(LAROSA_EUNSUPPORTED, "rotate_topk: d must be a multiple of 8 when R != NULL");
-    if (R && (!aligned16(R) || !aligned16(x))) return fail(LAROSA_EINVAL, "rotate_topk: R, x must be 16-byte aligned");
+    if (R && !aligned16(R)) return fail(LAROSA_EINVAL, "rotate_topk: R must be 16-byte aligned");
     if (R && xr_out == x) return fail(LAROSA_EINVAL, "rotate_topk: xr_out aliases x with R != NULL");
     const size_t need = larosa_rotate_topk_workspace_size(batch, d);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "rotate_topk: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
-    float* xr_ws;
-    carve_rotate_topk(c, batch, d, &xr_ws);
+    unsigned long long* acc;
+    carve_rotate_topk(c, batch, d, &acc);
 
-    const float* src = x;
+    TopkKernelArgs t = topk_args_base();
+    t.ldx = d;
+    t.d = (int)d;
+    t.k = (int)k;
+    t.rms_eps = rms_eps;
+    t.xr_out = xr_out;
+    t.idx = idx;
+    t.vals = vals;
+    t.mask = mask;
     if (R) {
-        // dense rotation GEMV x . R (all d rows, token-major values)
-        float* xr = (xr_out && aligned16(xr_out)) ? xr_out : xr_ws;
+        // dense rotation GEMV x . R over all d rows (token-major values), then the Top-K
+        // kernel finalises the fixed-point accumulators into x~
         const int bp = pad_batch(batch);
-        GemvPlan p = plan_gemv(d, d, bp);
+        const GemvPlan p = plan_gemv(d, d, bp);
         GemvArgs a = gemv_args_base();
         a.W = R;
         a.ld = d;
         a.d_out = (int)d;
-        a.rows = nullptr;
         a.vals = x;
         a.vs_r = 1;
         a.vs_b = d;
         a.nrows = (int)d;
         a.batch = batch;
-        a.out = xr;
-        a.out_ld = d;
-        a.ep = EP_STORE;
+        a.n_splits = p.n_splits;
+        a.acc = acc;
+        a.acc_ld = d;
         LAROSA_TRY(launch_gemv(a, p, bp, st));
-        src = xr;
+        t.mode = SRC_RESID_ACC;
+        t.acc = acc;
+        t.acc_ld = d;
+    } else {
+        t.x = x;
     }
-    TopkKernelArgs t;
-    t.x = src;
-    t.ldx = d;
-    t.d = (int)d;
-    t.k = (int)k;
-    t.rms_eps = rms_eps;
-    t.xr_out = (xr_out && src != xr_out) ? xr_out : nullptr;
-    t.idx = idx;
-    t.vals = vals;
-    t.mask = mask;
-    t.scale = nullptr;
     return launch_topk(t, batch, st);
 }
 
@@ -537,14 +487,13 @@ extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t*
 // ============================================================================== decoder layer
 namespace {
 struct LayerWs {
+    unsigned long long *acc_qkv, *acc_o, *acc_gu, *acc_down, *acc_adp;
     int32_t* idx[4];
     float* vals[4];
     uint32_t* mask[4];
-    float* q;
     float* h2;
     float* rmid;
     float* h4;
-    float* rout;
     int32_t* urows;
     float* uV;
     int* unrows;
@@ -583,16 +532,20 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     LayerWs tmp;
     LayerWs* o = ws ? ws : &tmp;
+    // accumulators first (zero at rest)
+    o->acc_qkv = c.take<unsigned long long>((size_t)batch * L.nqkv);
+    o->acc_o = c.take<unsigned long long>((size_t)batch * L.d);
+    o->acc_gu = c.take<unsigned long long>((size_t)batch * L.dgu);
+    o->acc_down = c.take<unsigned long long>((size_t)batch * L.d);
+    o->acc_adp = c.take<unsigned long long>((size_t)batch * L.d);
     for (int s = 0; s < 4; ++s) {
         o->idx[s] = c.take<int32_t>((size_t)batch * din[s]);
         o->vals[s] = c.take<float>((size_t)batch * din[s]);
         o->mask[s] = c.take<uint32_t>((size_t)batch * ((din[s] + 31) / 32));
     }
-    o->q = c.take<float>((size_t)batch * L.nq);
     o->h2 = c.take<float>((size_t)batch * L.nq);
     o->rmid = c.take<float>((size_t)batch * L.d);
     o->h4 = c.take<float>((size_t)batch * L.inter);
-    o->rout = c.take<float>((size_t)batch * L.d);
     const int64_t dmax = std::max(std::max(L.d, L.nq), L.inter);
     o->urows = c.take<int32_t>((size_t)dmax);
     o->uV = c.take<float>((size_t)dmax * bp + 16);
@@ -612,12 +565,14 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
     if (w->d <= 0 || w->inter <= 0 || w->n_q_heads <= 0 || w->n_kv_heads <= 0 || w->head_dim <= 0)
         return fail(LAROSA_EINVAL, "sparse_layer: dims must be > 0");
     if (w->n_q_heads % w->n_kv_heads) return fail(LAROSA_ESHAPE, "sparse_layer: Hq %% Hkv != 0");
-    if (w->n_q_heads / w->n_kv_heads > 8) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
+    if (w->n_q_heads / w->n_kv_heads > kAttnMaxG) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
     if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: head_dim must be 64 or 128");
     if (w->d % 8 || w->inter % LAROSA_GU_BLOCK) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: d %% 8 or inter %% 64");
     if (w->d > LAROSA_MAX_DIM || w->inter > LAROSA_MAX_DIM || w->n_q_heads * w->head_dim > LAROSA_MAX_DIM)
         return fail(LAROSA_EUNSUPPORTED, "sparse_layer: dimension > %d", LAROSA_MAX_DIM);
     if (s->max_ctx <= 0) return fail(LAROSA_EINVAL, "sparse_layer: max_ctx must be > 0");
+    if ((int64_t)s->batch * w->n_kv_heads > (int64_t)kCounterHeaderWords)
+        return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch * Hkv too large");
     const int64_t nq = w->n_q_heads * w->head_dim;
     if (p->k_h1 < 0 || p->k_h1 > w->d || p->k_h2 < 0 || p->k_h2 > nq || p->k_h3 < 0 || p->k_h3 > w->d || p->k_h4 < 0 ||
         p->k_h4 > w->inter)
@@ -632,15 +587,6 @@ larosa_status tap_copy(void* dst, const void* src, size_t bytes, cudaStream_t st
     if (!dst) return LAROSA_OK;
     return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st), "tap copy");
 }
-
-// Top-K of one site (+ union for batch > 1), then the GEMV over its kept rows.
-struct SiteGemv {
-    const float* x;        // [batch][din]
-    int64_t din;
-    int64_t k;
-    float rms_eps;         // < 0: no RMS scale
-    int site;
-};
 }  // namespace
 
 extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx) {
@@ -650,6 +596,18 @@ extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int
     return c.size();
 }
 
+// Kernel sequence (one decode step of one layer; every kernel is launched with PDL):
+//   topk(h1 = r)            -> idx1, vals1 (RMS-scaled)                 [+ union for batch > 1]
+//   gemv(W_qkv)             -> acc_qkv
+//   attention               <- acc_qkv (+bias, RoPE, KV append)        -> h2
+//   topk(h2), zero acc_qkv  -> idx2, vals2
+//   gemv(W_o)               -> acc_o
+//   topk(h3 = r + acc_o)    -> r_mid, idx3, vals3 (RMS-scaled); zero acc_o
+//   gemv(W_gate|up)         -> acc_gu
+//   topk(h4 = SiLU(g) * u)  -> h4, idx4, vals4; zero acc_gu
+//   gemv(W_down)            -> acc_down
+//   gemv(adapter, dense; values r_mid + acc_down) -> acc_adp            (if adapter)
+//   finalize: r <- acc_adp  (or r_mid + acc_down); zero acc_down, acc_adp
 extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                              const larosa_layer_state* s, const larosa_layer_taps* taps, void* ws,
                                              size_t ws_bytes, larosa_stream_t stream) {
@@ -668,31 +626,25 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     else
         memset(&T, 0, sizeof(T));
 
-    // Top-K at a site; fills the GEMV row source (idx list, or union for batch > 1)
-    auto site = [&](const SiteGemv& sg, GemvArgs& a) -> larosa_status {
-        TopkKernelArgs t;
-        t.x = sg.x;
-        t.ldx = sg.din;
-        t.d = (int)sg.din;
-        t.k = (int)sg.k;
-        t.rms_eps = sg.rms_eps;
-        t.xr_out = nullptr;
-        t.idx = W.idx[sg.site];
-        t.vals = W.vals[sg.site];
-        t.mask = B > 1 ? W.mask[sg.site] : nullptr;
-        t.scale = nullptr;
+    // Top-K at a site (t prepared by the caller), then the GEMV row source for batch 1 or 2+
+    auto site = [&](TopkKernelArgs t, int si, int64_t din, int64_t k, GemvArgs& a) -> larosa_status {
+        t.ldx = din;
+        t.d = (int)din;
+        t.k = (int)k;
+        t.idx = W.idx[si];
+        t.vals = W.vals[si];
+        t.mask = B > 1 ? W.mask[si] : nullptr;
         LAROSA_TRY(launch_topk(t, B, st));
         if (B == 1) {
-            a.rows = W.idx[sg.site];
-            a.vals = W.vals[sg.site];
+            a.rows = W.idx[si];
+            a.vals = W.vals[si];
             a.vs_r = 1;
-            a.vs_b = sg.k;
-            a.nrows = (int)sg.k;
+            a.vs_b = k;
+            a.nrows = (int)k;
             a.nrows_dev = nullptr;
         } else {
-            const int nw = (int)((sg.din + 31) / 32);
-            LAROSA_TRY(launch_union(W.mask[sg.site], nw, B, bp, W.vals[sg.site], sg.k, (int)sg.din, W.urows, W.uV,
-                                    W.unrows, st));
+            const int nw = (int)((din + 31) / 32);
+            LAROSA_TRY(launch_union(W.mask[si], nw, B, bp, W.vals[si], k, (int)din, W.urows, W.uV, W.unrows, st));
             a.rows = W.urows;
             a.vals = W.uV;
             a.vs_r = bp;
@@ -704,36 +656,38 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         return LAROSA_OK;
     };
     auto nrows_max = [&](int64_t din, int64_t k) { return B == 1 ? k : std::min<int64_t>(din, (int64_t)B * k); };
+    auto run_gemv = [&](GemvArgs& a, const uint16_t* Wt, int64_t din, int64_t k, int64_t dout,
+                        unsigned long long* acc) -> larosa_status {
+        const GemvPlan p = plan_gemv(dout, nrows_max(din, k), bp);
+        a.W = Wt;
+        a.ld = dout;
+        a.d_out = (int)dout;
+        a.n_splits = p.n_splits;
+        a.acc = acc;
+        a.acc_ld = dout;
+        return launch_gemv(a, p, bp, st);
+    };
 
-    // ---- h1: Top-K of r (RMS scale), QKV GEMV + bias + RoPE + KV append --------------------
+    // ---- h1: Top-K of r (RMS scale) -> QKV --------------------------------------------------
     {
         GemvArgs a = gemv_args_base();
-        LAROSA_TRY(site({s->resid, L.d, plan->k_h1, w->rms_eps, 0}, a));
-        GemvPlan p = plan_gemv(L.nqkv, nrows_max(L.d, plan->k_h1), bp);
-        a.W = w->w_qkv;
-        a.ld = L.nqkv;
-        a.d_out = (int)L.nqkv;
-        a.ep = EP_QKV_ROPE;
-        a.bias = w->b_qkv;
-        a.out = W.q;
-        a.out_ld = L.nq;
-        a.hq = (int)L.hq;
-        a.hkv = (int)L.hkv;
-        a.hd = (int)L.hd;
-        a.theta = w->rope_theta;
-        a.pos = s->pos;
-        a.kc = s->k_cache;
-        a.vc = s->v_cache;
-        a.max_ctx = s->max_ctx;
-        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        TopkKernelArgs t = topk_args_base();
+        t.x = s->resid;
+        t.rms_eps = w->rms_eps;
+        LAROSA_TRY(site(t, 0, L.d, plan->k_h1, a));
+        LAROSA_TRY(run_gemv(a, w->w_qkv, L.d, plan->k_h1, L.nqkv, W.acc_qkv));
         LAROSA_TRY(tap_copy(T.idx_h1, W.idx[0], sizeof(int32_t) * B * plan->k_h1, st));
         LAROSA_TRY(tap_copy(T.vals_h1, W.vals[0], sizeof(float) * B * plan->k_h1, st));
-        LAROSA_TRY(tap_copy(T.q, W.q, sizeof(float) * B * L.nq, st));
     }
-    // ---- attention ---------------------------------------------------------------------------
+    // ---- attention (finalises q / new k, v from acc_qkv) -------------------------------------
     {
         AttnArgs aa;
-        aa.q = W.q;
+        memset(&aa, 0, sizeof(aa));
+        aa.acc = W.acc_qkv;
+        aa.acc_ld = L.nqkv;
+        aa.bias = w->b_qkv;
+        aa.theta = w->rope_theta;
+        aa.q_out = T.q;
         aa.kc = s->k_cache;
         aa.vc = s->v_cache;
         aa.pos = s->pos;
@@ -751,76 +705,87 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
                               "attention launch"));
         LAROSA_TRY(tap_copy(T.h2, W.h2, sizeof(float) * B * L.nq, st));
     }
-    // ---- h2: Top-K of the attention output, O GEMV, r_mid = r + y ----------------------------
+    // ---- h2: Top-K of the attention output (zero acc_qkv) -> O --------------------------------
     {
         GemvArgs a = gemv_args_base();
-        LAROSA_TRY(site({W.h2, L.nq, plan->k_h2, -1.0f, 1}, a));
-        GemvPlan p = plan_gemv(L.d, nrows_max(L.nq, plan->k_h2), bp);
-        a.W = w->w_o;
-        a.ld = L.d;
-        a.d_out = (int)L.d;
-        a.ep = EP_RESID;
-        a.resid = s->resid;
-        a.resid_ld = L.d;
-        a.out = W.rmid;
-        a.out_ld = L.d;
-        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        TopkKernelArgs t = topk_args_base();
+        t.x = W.h2;
+        t.rms_eps = -1.0f;
+        t.zero = W.acc_qkv;
+        t.zero_ld = L.nqkv;
+        t.zero_n = (int)L.nqkv;
+        LAROSA_TRY(site(t, 1, L.nq, plan->k_h2, a));
+        LAROSA_TRY(run_gemv(a, w->w_o, L.nq, plan->k_h2, L.d, W.acc_o));
         LAROSA_TRY(tap_copy(T.idx_h2, W.idx[1], sizeof(int32_t) * B * plan->k_h2, st));
         LAROSA_TRY(tap_copy(T.vals_h2, W.vals[1], sizeof(float) * B * plan->k_h2, st));
-        LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
     }
-    // ---- h3: Top-K of r_mid (RMS scale), gate|up GEMV, h4 = SiLU(g) * u ----------------------
+    // ---- h3: r_mid = r + y_o; Top-K (RMS scale) -> gate|up ------------------------------------
     {
         GemvArgs a = gemv_args_base();
-        LAROSA_TRY(site({W.rmid, L.d, plan->k_h3, w->rms_eps, 2}, a));
-        GemvPlan p = plan_gemv(L.dgu, nrows_max(L.d, plan->k_h3), bp);
-        a.W = w->w_gu;
-        a.ld = L.dgu;
-        a.d_out = (int)L.dgu;
-        a.ep = EP_SILU_GU;
-        a.out = W.h4;
-        a.out_ld = L.inter;
-        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        TopkKernelArgs t = topk_args_base();
+        t.mode = SRC_RESID_ACC;
+        t.resid = s->resid;
+        t.resid_ld = L.d;
+        t.acc = W.acc_o;
+        t.acc_ld = L.d;
+        t.xr_out = W.rmid;
+        t.rms_eps = w->rms_eps;
+        LAROSA_TRY(site(t, 2, L.d, plan->k_h3, a));
+        LAROSA_TRY(run_gemv(a, w->w_gu, L.d, plan->k_h3, L.dgu, W.acc_gu));
+        LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
         LAROSA_TRY(tap_copy(T.idx_h3, W.idx[2], sizeof(int32_t) * B * plan->k_h3, st));
         LAROSA_TRY(tap_copy(T.vals_h3, W.vals[2], sizeof(float) * B * plan->k_h3, st));
-        LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
     }
-    // ---- h4: Top-K of h4, down GEMV, r_out = r_mid + y ---------------------------------------
-    float* r_out = w->adapter ? W.rout : s->resid;
+    // ---- h4 = SiLU(g) * u; Top-K -> down ---------------------------------------------------------
     {
         GemvArgs a = gemv_args_base();
-        LAROSA_TRY(site({W.h4, L.inter, plan->k_h4, -1.0f, 3}, a));
-        GemvPlan p = plan_gemv(L.d, nrows_max(L.inter, plan->k_h4), bp);
-        a.W = w->w_down;
-        a.ld = L.d;
-        a.d_out = (int)L.d;
-        a.ep = EP_RESID;
-        a.resid = W.rmid;
-        a.resid_ld = L.d;
-        a.out = r_out;
-        a.out_ld = L.d;
-        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        TopkKernelArgs t = topk_args_base();
+        t.mode = SRC_SILU_GU;
+        t.acc = W.acc_gu;
+        t.acc_ld = L.dgu;
+        t.xr_out = W.h4;
+        t.rms_eps = -1.0f;
+        LAROSA_TRY(site(t, 3, L.inter, plan->k_h4, a));
+        LAROSA_TRY(run_gemv(a, w->w_down, L.inter, plan->k_h4, L.d, W.acc_down));
+        LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
         LAROSA_TRY(tap_copy(T.idx_h4, W.idx[3], sizeof(int32_t) * B * plan->k_h4, st));
         LAROSA_TRY(tap_copy(T.vals_h4, W.vals[3], sizeof(float) * B * plan->k_h4, st));
-        LAROSA_TRY(tap_copy(T.r_out, r_out, sizeof(float) * B * L.d, st));
     }
-    // ---- residual adapter r <- r_out . A_l (dense GEMV) -------------------------------
+    // ---- residual adapter r <- (r_mid + y_down) . A_l (dense GEMV), finalize ------------
+    FinalizeArgs f = finalize_args_base();
+    f.n = (int)L.d;
+    f.batch = B;
     if (w->adapter) {
-        GemvPlan p = plan_gemv(L.d, L.d, bp);
         GemvArgs a = gemv_args_base();
-        a.W = w->adapter;
-        a.ld = L.d;
-        a.d_out = (int)L.d;
         a.rows = nullptr;
-        a.vals = W.rout;
+        a.vals = W.rmid;
         a.vs_r = 1;
         a.vs_b = L.d;
+        a.vacc = W.acc_down;
+        a.vacc_ld = L.d;
         a.nrows = (int)L.d;
         a.batch = B;
-        a.ep = EP_STORE;
-        a.out = s->resid;
-        a.out_ld = L.d;
-        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        LAROSA_TRY(run_gemv(a, w->adapter, L.d, L.d, L.d, W.acc_adp));
+        f.acc1 = W.acc_adp;
+        f.acc1_ld = L.d;
+        f.out1 = s->resid;
+        f.out1_ld = L.d;
+        f.acc2 = W.acc_down;          // r_out = r_mid + y_down (tap), then zero
+        f.acc2_ld = L.d;
+        f.res2 = W.rmid;
+        f.res2_ld = L.d;
+        f.out2 = T.r_out;
+        f.out2_ld = L.d;
+        LAROSA_TRY(launch_finalize(f, st));
+    } else {
+        f.acc1 = W.acc_down;
+        f.acc1_ld = L.d;
+        f.res1 = W.rmid;
+        f.res1_ld = L.d;
+        f.out1 = s->resid;
+        f.out1_ld = L.d;
+        LAROSA_TRY(launch_finalize(f, st));
+        LAROSA_TRY(tap_copy(T.r_out, s->resid, sizeof(float) * B * L.d, st));
     }
     return LAROSA_OK;
 }

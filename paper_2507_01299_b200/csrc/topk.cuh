@@ -15,6 +15,7 @@
 //    ownership keeps the output ascending).
 #pragma once
 #include "common.cuh"
+#include "gemv.cuh"   // fixed-point accumulator helpers, kGuBlock
 
 namespace larosa {
 
@@ -31,8 +32,23 @@ __host__ __device__ constexpr int topk_ept(int d) {
     return ((d + 4 * kTopkThreads - 1) / (4 * kTopkThreads)) * 4;
 }
 
+// Where the site's input vector comes from (the producer GEMV leaves fixed-point
+// accumulators; the Top-K kernel finalises them, see gemv.cuh):
+enum TopkSrc : int {
+    SRC_PLAIN = 0,      // x[i]
+    SRC_RESID_ACC = 1,  // [resid[i] +] fix^-1(acc[i])                    (residual add)
+    SRC_SILU_GU = 2,    // SiLU(g_i) * u_i, g/u = fix^-1 of the interleaved gate|up acc
+};
+
+struct TopkSrcArgs {
+    const float* resid;          // SRC_RESID_ACC
+    unsigned long long* acc;     // SRC_RESID_ACC / SRC_SILU_GU: read, then re-zeroed
+    unsigned long long* zero;    // optional extra accumulator to re-zero (zero_n entries)
+    int zero_n;
+};
+
 struct TopkOut {
-    float* xr_out;     // [d] copy of the (rotated) input, or nullptr
+    float* xr_out;     // [d] copy of the (rotated / finalised) input, or nullptr
     int32_t* idx;      // [k]
     float* vals;       // [k]
     uint32_t* mask;    // [ceil(d/32)] or nullptr
@@ -51,9 +67,9 @@ __device__ __forceinline__ int topk_excl_scan(int v, int* sw, int* total) {
     return __shfl_sync(0xffffffffu, ti - t, wid) + inc - v;
 }
 
-template <int EPT>
+template <int EPT, int MODE>
 __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                             unsigned char* smem_raw) {
+                             TopkSrcArgs src, unsigned char* smem_raw) {
     constexpr int NT = kTopkThreads;
     int* hist0 = reinterpret_cast<int*>(smem_raw);
     int* hist1 = hist0 + kTopkBins;
@@ -67,29 +83,55 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int i0 = tid * EPT;
 
-    // 1. keys = bits(|x|) in registers (clears the sign: -0 == +0), sum of squares
-    uint32_t key[EPT];
+    // 1. values (raw fp32 bits) in registers; key = bits & 0x7fffffff (-0 == +0); sum of squares
+    uint32_t xv[EPT];
     float ssq = 0.f;
-    const bool vec = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if constexpr (MODE == SRC_PLAIN) {
+        const bool vec = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 #pragma unroll
-    for (int c = 0; c < EPT / 4; ++c) {
-        const int i = i0 + 4 * c;
-        float v[4];
-        if (vec && i + 4 <= d) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(x + i));
-            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-        } else {
+        for (int c = 0; c < EPT / 4; ++c) {
+            const int i = i0 + 4 * c;
+            float v[4];
+            if (vec && i + 4 <= d) {
+                const float4 f = *reinterpret_cast<const float4*>(x + i);
+                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+            } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = (i + u < d) ? __ldg(x + i + u) : 0.f;
+                for (int u = 0; u < 4; ++u) v[u] = (i + u < d) ? x[i + u] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[4 * c + u] = __float_as_uint(v[u]);
         }
+    } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            // out-of-range elements get key 0 and are excluded by index checks below
-            key[4 * c + u] = __float_as_uint(v[u]) & 0x7fffffffu;
-            ssq = fmaf(v[u], v[u], ssq);
-            if (out.xr_out && i + u < d) out.xr_out[i + u] = v[u];
+        for (int e = 0; e < EPT; ++e) {
+            const int i = i0 + e;
+            float v = 0.f;
+            if (i < d) {
+                if constexpr (MODE == SRC_RESID_ACC) {
+                    v = (src.resid ? src.resid[i] : 0.f) + fix_to_f(src.acc[i]);
+                    src.acc[i] = 0ull;
+                } else {
+                    const int gi = (i / kGuBlock) * (2 * kGuBlock) + (i % kGuBlock);
+                    const float g = fix_to_f(src.acc[gi]);
+                    const float u = fix_to_f(src.acc[gi + kGuBlock]);
+                    src.acc[gi] = 0ull;
+                    src.acc[gi + kGuBlock] = 0ull;
+                    v = g / (1.0f + expf(-g)) * u;
+                }
+            }
+            xv[e] = __float_as_uint(v);
         }
     }
+    if (src.zero)
+        for (int i = tid; i < src.zero_n; i += NT) src.zero[i] = 0ull;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const float v = __uint_as_float(xv[e]);
+        ssq = fmaf(v, v, ssq);
+        if (out.xr_out && i0 + e < d) out.xr_out[i0 + e] = v;
+    }
+#define KEY(e) (xv[e] & 0x7fffffffu)
     ssq = warp_sum(ssq);
     if (lane == 0) s_ssq[wid] = ssq;
     for (int b = tid; b < kTopkBins; b += NT) hist0[b] = 0;
@@ -115,7 +157,7 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
             const uint32_t dmask = (uint32_t)(nb - 1);
 #pragma unroll
             for (int e = 0; e < EPT; ++e)
-                if (i0 + e < d && (key[e] & pmask) == prefix) atomicAdd(&hist[(key[e] >> sh) & dmask], 1);
+                if (i0 + e < d && (KEY(e) & pmask) == prefix) atomicAdd(&hist[(KEY(e) >> sh) & dmask], 1);
             if (pass < 2)
                 for (int b = tid; b < kTopkBins; b += NT) hnext[b] = 0;
             __syncthreads();
@@ -170,10 +212,10 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
     for (int e = 0; e < EPT; ++e) {
         if (i0 + e >= d) continue;
         if (exact_ge) {
-            n_gt += key[e] >= thr;
+            n_gt += KEY(e) >= thr;
         } else {
-            n_gt += key[e] > thr;
-            n_eq += key[e] == thr;
+            n_gt += KEY(e) > thr;
+            n_eq += KEY(e) == thr;
         }
     }
     int take_eq = 0;
@@ -191,10 +233,10 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
         if (i >= d) continue;
         bool sel;
         if (exact_ge) {
-            sel = key[e] >= thr;
-        } else if (key[e] > thr) {
+            sel = KEY(e) >= thr;
+        } else if (KEY(e) > thr) {
             sel = true;
-        } else if (key[e] == thr) {
+        } else if (KEY(e) == thr) {
             sel = eq_seen < take_eq;
             ++eq_seen;
         } else {
@@ -202,7 +244,7 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
         }
         if (sel) {
             out.idx[pos] = i;
-            out.vals[pos] = __ldg(x + i) * scale;
+            out.vals[pos] = __uint_as_float(xv[e]) * scale;
             if (out.mask) atomicOr(&smask[i >> 5], 1u << (i & 31));
             ++pos;
         }
@@ -213,16 +255,18 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
         for (int w = tid; w < nwords; w += NT) out.mask[w] = smask[w];
     }
 }
+#undef KEY
 
-__device__ __forceinline__ void block_topk(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                                           unsigned char* smem) {
+template <int MODE>
+__device__ __forceinline__ void block_topk_m(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
+                                             TopkSrcArgs src, unsigned char* smem) {
     const int ept = topk_ept(d);
-    if (ept <= 4) block_topk_t<4>(x, d, k, rms_eps, out, smem);
-    else if (ept <= 8) block_topk_t<8>(x, d, k, rms_eps, out, smem);
-    else if (ept <= 12) block_topk_t<12>(x, d, k, rms_eps, out, smem);
-    else if (ept <= 16) block_topk_t<16>(x, d, k, rms_eps, out, smem);
-    else if (ept <= 24) block_topk_t<24>(x, d, k, rms_eps, out, smem);
-    else block_topk_t<32>(x, d, k, rms_eps, out, smem);
+    if (ept <= 4) block_topk_t<4, MODE>(x, d, k, rms_eps, out, src, smem);
+    else if (ept <= 8) block_topk_t<8, MODE>(x, d, k, rms_eps, out, src, smem);
+    else if (ept <= 12) block_topk_t<12, MODE>(x, d, k, rms_eps, out, src, smem);
+    else if (ept <= 16) block_topk_t<16, MODE>(x, d, k, rms_eps, out, src, smem);
+    else if (ept <= 24) block_topk_t<24, MODE>(x, d, k, rms_eps, out, src, smem);
+    else block_topk_t<32, MODE>(x, d, k, rms_eps, out, src, smem);
 }
 
 // One CTA per token: x [batch][ldx], outputs strided per token.
@@ -236,6 +280,10 @@ struct TopkKernelArgs {
     float* vals;        // [batch][k]
     uint32_t* mask;     // [batch][ceil(d/32)] or null
     float* scale;       // [batch] or null
+    int mode;           // TopkSrc
+    const float* resid; int64_t resid_ld;                 // SRC_RESID_ACC
+    unsigned long long* acc; int64_t acc_ld;              // SRC_RESID_ACC / SRC_SILU_GU
+    unsigned long long* zero; int64_t zero_ld; int zero_n; // optional extra zeroing per token
 };
 
 __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
@@ -250,7 +298,18 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
     o.vals = a.vals + (size_t)b * a.k;
     o.mask = a.mask ? a.mask + (size_t)b * nwords : nullptr;
     o.scale_out = a.scale ? a.scale + b : nullptr;
-    block_topk(a.x + (size_t)b * a.ldx, a.d, a.k, a.rms_eps, o, smem);
+    TopkSrcArgs src;
+    src.resid = a.resid ? a.resid + (size_t)b * a.resid_ld : nullptr;
+    src.acc = a.acc ? a.acc + (size_t)b * a.acc_ld : nullptr;
+    src.zero = a.zero ? a.zero + (size_t)b * a.zero_ld : nullptr;
+    src.zero_n = a.zero_n;
+    const float* x = a.x ? a.x + (size_t)b * a.ldx : nullptr;
+    if (a.mode == SRC_RESID_ACC)
+        block_topk_m<SRC_RESID_ACC>(x, a.d, a.k, a.rms_eps, o, src, smem);
+    else if (a.mode == SRC_SILU_GU)
+        block_topk_m<SRC_SILU_GU>(x, a.d, a.k, a.rms_eps, o, src, smem);
+    else
+        block_topk_m<SRC_PLAIN>(x, a.d, a.k, a.rms_eps, o, src, smem);
 }
 
 }  // namespace larosa

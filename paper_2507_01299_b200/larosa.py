@@ -136,7 +136,9 @@ class Workspace:
 _WS = {}
 
 
-def _ws(tag: str, nbytes: int, device) -> torch.Tensor:
+def _ws(tag, nbytes: int, device) -> torch.Tensor:
+    """Workspace per (call kind, shape signature): the library keeps accumulators zero
+    between calls only for a fixed layout."""
     key = (tag, str(device))
     if key not in _WS:
         _WS[key] = Workspace()
@@ -169,7 +171,7 @@ def fold_rotation(Q: torch.Tensor, W: torch.Tensor, side: int, gamma: Optional[t
     out = out if out is not None else torch.empty((rows, cols), dtype=torch.int16, device=W.device)
     L = lib()
     nb = L.larosa_fold_workspace_size(rows, cols, side)
-    ws = _ws("fold", nb, W.device)
+    ws = _ws(("fold", rows, cols, side), nb, W.device)
     _check(L.larosa_fold_rotation(_ptr(Q), _ptr(gamma), _ptr(W), _ptr(out), rows, cols, side, _ptr(ws),
                                   ws.numel(), _stream(stream)))
     return out
@@ -194,7 +196,7 @@ def rotate_topk(x: torch.Tensor, R: Optional[torch.Tensor], k: int, rms_eps: flo
     mask = torch.empty((B, (d + 31) // 32), dtype=torch.int32, device=dev) if want_mask else None
     L = lib()
     nb = L.larosa_rotate_topk_workspace_size(B, d)
-    ws = _ws("rotate_topk", nb, dev)
+    ws = _ws(("rotate_topk", B, d), nb, dev)
     _check(L.larosa_rotate_topk(_ptr(x), _ptr(R), B, d, k, float(rms_eps), _ptr(xr), _ptr(idx), _ptr(vals),
                                 _ptr(mask), _ptr(ws), ws.numel(), _stream(stream)))
     return xr, idx, vals, mask
@@ -212,7 +214,7 @@ def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Op
     y = out if out is not None else torch.empty((B, d_out), dtype=torch.float32, device=dev)
     L = lib()
     nb = L.larosa_sparse_gemv_workspace_size(B, d_in, k, d_out)
-    ws = _ws("sparse_gemv", nb, dev)
+    ws = _ws(("sparse_gemv", B, d_in, d_out), nb, dev)
     _check(L.larosa_sparse_gemv(_ptr(W), d_in, d_out, ld, _ptr(idx) if k else None, _ptr(vals) if k else None,
                                 B, k, _ptr(bias), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)))
     return y
@@ -289,7 +291,8 @@ def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: 
     B = state.resid.shape[0]
     nb = L.larosa_layer_workspace_size(ctypes.byref(wc), B, state.k_cache.shape[2])
     if ws is None:
-        ws = _ws("layer", nb, state.resid.device)
+        ws = _ws(("layer", w.d, w.inter, w.n_q_heads, w.n_kv_heads, w.head_dim, B, state.k_cache.shape[2]), nb,
+                 state.resid.device)
     elif ws.numel() < nb:
         raise ValueError("sparse_layer: workspace too small")
     tc = None

@@ -63,7 +63,7 @@ def main():
             us = graph_time(lambda i: LZ.sparse_gemv(ws[i % 8], *ins[i % 8], out=y), args.reps)
             byt = k * dout * 2
             info = (ctypes.c_int32 * 8)()
-            LZ.lib().larosa_gemv_plan_info(ctypes.c_int64(dout), ctypes.c_int64(k), 1, info)
+            LZ.lib().larosa_gemv_plan_info(ctypes.c_int64(dout), ctypes.c_int64(k), 1, info)  # see larosa.h
             res[name] = {"us": round(us, 2), "GBps": round(byt / us / 1e3, 1), "plan": list(info)}
             del ws
         out["gemv"] = res
