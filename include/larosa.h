@@ -211,6 +211,14 @@ typedef struct {
 } larosa_layer_taps;
 
 size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx);
+
+/* Profiling aid (not for production): bitmask of the kernels larosa_sparse_layer launches
+ * (default -1 = all; results are meaningless otherwise).  Bits: 0 Top-K h1, 1 QKV GEMV,
+ * 2 attention, 3 Top-K h2, 4 O GEMV, 5 Top-K h3, 6 gate|up GEMV, 7 Top-K h4, 8 down GEMV,
+ * 9 adapter GEMV, 10 finalize.  Process-wide, not thread-safe.  Also settable through the
+ * LAROSA_LAYER_PHASES environment variable. */
+#define LAROSA_PHASES_GEMV_ONLY 0x352
+void larosa_debug_set_layer_phases(int mask);
 larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                   const larosa_layer_state* state, const larosa_layer_taps* taps,
                                   void* ws, size_t ws_bytes, larosa_stream_t stream);

@@ -235,14 +235,12 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     }
 }
 
+template <int DPL>
 __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const AttnArgs a) {
     extern __shared__ __align__(16) float asmem[];
     pdl_wait();
     pdl_trigger();
-    if (a.hd == 128)
-        attention_body<4>(a, asmem);
-    else
-        attention_body<2>(a, asmem);
+    attention_body<DPL>(a, asmem);
 }
 
 }  // namespace larosa

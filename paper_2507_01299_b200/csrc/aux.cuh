@@ -124,14 +124,20 @@ struct FinalizeArgs {
     unsigned long long* acc2; int64_t acc2_ld;
     const float* res2; int64_t res2_ld;
     float* out2; int64_t out2_ld;
+    unsigned long long* zero3; int64_t zero3_ld; int zero3_n;   // extra accumulator to re-zero
 };
 
 __global__ void finalize_kernel(const FinalizeArgs a) {
     pdl_wait();
     pdl_trigger();
-    const int64_t total = (int64_t)a.batch * a.n;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int b = (int)(t / a.n), i = (int)(t % a.n);
+    const int nz = a.batch * a.zero3_n;
+#pragma unroll 1
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nz; t += gridDim.x * blockDim.x)
+        a.zero3[(size_t)(t / a.zero3_n) * a.zero3_ld + t % a.zero3_n] = 0ull;
+    const int total = a.batch * a.n;
+#pragma unroll 1
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int b = t / a.n, i = t % a.n;
         if (a.acc1) {
             unsigned long long* p = a.acc1 + (size_t)b * a.acc1_ld + i;
             float y = fix_to_f(*p);

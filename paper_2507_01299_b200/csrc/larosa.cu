@@ -174,14 +174,52 @@ GemvArgs gemv_args_base() {
 }
 
 // ============================================================================== small launches
-larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
-    const size_t smem = topk_smem_bytes(a.d);
+template <int MODE, int EPT>
+larosa_status launch_topk_t(const TopkKernelArgs& a, int batch, cudaStream_t st) {
+    auto kern = topk_kernel<MODE, EPT>;
     static bool attr_done = false;
     if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(topk_kernel, topk_smem_bytes(LAROSA_MAX_DIM)), "cudaFuncSetAttribute(topk)"));
+        LAROSA_TRY(cuda_check(allow_smem(kern, topk_smem_bytes(LAROSA_MAX_DIM)), "cudaFuncSetAttribute(topk)"));
         attr_done = true;
     }
-    return cuda_check(launch(topk_kernel, dim3(batch), dim3(kTopkThreads), smem, st, a), "topk launch");
+    // cluster of CS CTAs per token spreads the source finalisation (accumulator reads/zeroing)
+    const int cs = MODE == SRC_PLAIN ? 1 : std::max(1, std::min(8, (a.d + 1535) / 1536));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, batch);
+    cfg.blockDim = dim3(kTopkThreads);
+    cfg.dynamicSmemBytes = topk_smem_bytes(a.d);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (!pdl_enabled()) {
+        at[0] = at[0];
+        cfg.numAttrs = 1;
+    }
+    return cuda_check(cudaLaunchKernelEx(&cfg, kern, a), "topk launch");
+}
+
+template <int MODE>
+larosa_status launch_topk_m(const TopkKernelArgs& a, int batch, cudaStream_t st) {
+    const int ept = topk_ept(a.d);
+    if (ept <= 4) return launch_topk_t<MODE, 4>(a, batch, st);
+    if (ept <= 8) return launch_topk_t<MODE, 8>(a, batch, st);
+    if (ept <= 12) return launch_topk_t<MODE, 12>(a, batch, st);
+    if (ept <= 16) return launch_topk_t<MODE, 16>(a, batch, st);
+    if (ept <= 24) return launch_topk_t<MODE, 24>(a, batch, st);
+    return launch_topk_t<MODE, 32>(a, batch, st);
+}
+
+larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
+    if (a.mode == SRC_RESID_ACC) return launch_topk_m<SRC_RESID_ACC>(a, batch, st);
+    if (a.mode == SRC_SILU_GU) return launch_topk_m<SRC_SILU_GU>(a, batch, st);
+    return launch_topk_m<SRC_PLAIN>(a, batch, st);
 }
 
 TopkKernelArgs topk_args_base() {
@@ -200,7 +238,7 @@ larosa_status launch_union(const uint32_t* mask, int nwords, int batch, int bp, 
 }
 
 larosa_status launch_finalize(const FinalizeArgs& f, cudaStream_t st) {
-    const int64_t total = (int64_t)f.batch * f.n;
+    const int64_t total = (int64_t)f.batch * std::max(f.n, f.zero3_n);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 2 * sm_count()));
     return cuda_check(launch(finalize_kernel, dim3(grid), dim3(256), 0, st, f), "finalize launch");
 }
@@ -374,15 +412,17 @@ extern "C" larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max,
 }
 
 // ============================================================================== rotate + Top-K
-static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, unsigned long long** acc) {
+static void carve_rotate_topk(Carver& c, int32_t batch, int64_t d, unsigned long long** acc, float** xbuf) {
     unsigned long long* a = c.take<unsigned long long>((size_t)batch * d);
+    float* x = c.take<float>((size_t)batch * d);
     if (acc) *acc = a;
+    if (xbuf) *xbuf = x;
 }
 
 extern "C" size_t larosa_rotate_topk_workspace_size(int32_t batch, int64_t d) {
     if (batch < 1 || d <= 0) return 0;
     Carver c(nullptr);
-    carve_rotate_topk(c, batch, d, nullptr);
+    carve_rotate_topk(c, batch, d, nullptr, nullptr);
     return c.size();
 }
 
@@ -404,7 +444,8 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
     unsigned long long* acc;
-    carve_rotate_topk(c, batch, d, &acc);
+    float* xbuf;
+    carve_rotate_topk(c, batch, d, &acc, &xbuf);
 
     TopkKernelArgs t = topk_args_base();
     t.ldx = d;
@@ -436,6 +477,7 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
         t.mode = SRC_RESID_ACC;
         t.acc = acc;
         t.acc_ld = d;
+        if (!xr_out) t.xr_out = xbuf;   // the finalised x~ must be materialised for the select
     } else {
         t.x = x;
     }
@@ -589,6 +631,14 @@ larosa_status tap_copy(void* dst, const void* src, size_t bytes, cudaStream_t st
 }
 }  // namespace
 
+// profiling aid: bitmask of the layer's kernels that are launched (default: all)
+static int g_phase_mask = -2;
+static int layer_phase_mask() {
+    if (g_phase_mask == -2) g_phase_mask = env_int("LAROSA_LAYER_PHASES", -1);
+    return g_phase_mask;
+}
+extern "C" void larosa_debug_set_layer_phases(int mask) { g_phase_mask = mask; }
+
 extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx) {
     if (!w || batch < 1 || max_ctx <= 0) return 0;
     Carver c(nullptr);
@@ -612,6 +662,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
                                              const larosa_layer_state* s, const larosa_layer_taps* taps, void* ws,
                                              size_t ws_bytes, larosa_stream_t stream) {
     LAROSA_TRY(validate_layer(w, plan, s));
+    const int phases = layer_phase_mask();
+    auto on = [&](int bit) { return (phases >> bit) & 1; };
     const size_t need = larosa_layer_workspace_size(w, s->batch, s->max_ctx);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "sparse_layer: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -634,7 +686,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         t.idx = W.idx[si];
         t.vals = W.vals[si];
         t.mask = B > 1 ? W.mask[si] : nullptr;
-        LAROSA_TRY(launch_topk(t, B, st));
+        if (on(2 * si + (si > 0 ? 1 : 0))) LAROSA_TRY(launch_topk(t, B, st));
         if (B == 1) {
             a.rows = W.idx[si];
             a.vals = W.vals[si];
@@ -657,7 +709,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     };
     auto nrows_max = [&](int64_t din, int64_t k) { return B == 1 ? k : std::min<int64_t>(din, (int64_t)B * k); };
     auto run_gemv = [&](GemvArgs& a, const uint16_t* Wt, int64_t din, int64_t k, int64_t dout,
-                        unsigned long long* acc) -> larosa_status {
+                        unsigned long long* acc, int bit) -> larosa_status {
+        if (!on(bit)) return LAROSA_OK;
         const GemvPlan p = plan_gemv(dout, nrows_max(din, k), bp);
         a.W = Wt;
         a.ld = dout;
@@ -675,7 +728,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         t.x = s->resid;
         t.rms_eps = w->rms_eps;
         LAROSA_TRY(site(t, 0, L.d, plan->k_h1, a));
-        LAROSA_TRY(run_gemv(a, w->w_qkv, L.d, plan->k_h1, L.nqkv, W.acc_qkv));
+        LAROSA_TRY(run_gemv(a, w->w_qkv, L.d, plan->k_h1, L.nqkv, W.acc_qkv, 1));
         LAROSA_TRY(tap_copy(T.idx_h1, W.idx[0], sizeof(int32_t) * B * plan->k_h1, st));
         LAROSA_TRY(tap_copy(T.vals_h1, W.vals[0], sizeof(float) * B * plan->k_h1, st));
     }
@@ -701,8 +754,12 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         aa.counters = W.attn_cnt;
         aa.out = W.h2;
         const size_t smem = attn_smem_bytes(L.G, (int)L.hd, aa.chunk);
-        LAROSA_TRY(cuda_check(launch(attention_kernel, dim3(B * (int)L.hkv, aa.n_chunks), dim3(kAttnThreads), smem, st, aa),
-                              "attention launch"));
+        const dim3 grid(B * (int)L.hkv, aa.n_chunks);
+        if (!on(2)) {
+        } else if (L.hd == 128)
+            LAROSA_TRY(cuda_check(launch(attention_kernel<4>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch"));
+        else
+            LAROSA_TRY(cuda_check(launch(attention_kernel<2>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch"));
         LAROSA_TRY(tap_copy(T.h2, W.h2, sizeof(float) * B * L.nq, st));
     }
     // ---- h2: Top-K of the attention output (zero acc_qkv) -> O --------------------------------
@@ -711,11 +768,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         TopkKernelArgs t = topk_args_base();
         t.x = W.h2;
         t.rms_eps = -1.0f;
-        t.zero = W.acc_qkv;
-        t.zero_ld = L.nqkv;
-        t.zero_n = (int)L.nqkv;
         LAROSA_TRY(site(t, 1, L.nq, plan->k_h2, a));
-        LAROSA_TRY(run_gemv(a, w->w_o, L.nq, plan->k_h2, L.d, W.acc_o));
+        LAROSA_TRY(run_gemv(a, w->w_o, L.nq, plan->k_h2, L.d, W.acc_o, 4));
         LAROSA_TRY(tap_copy(T.idx_h2, W.idx[1], sizeof(int32_t) * B * plan->k_h2, st));
         LAROSA_TRY(tap_copy(T.vals_h2, W.vals[1], sizeof(float) * B * plan->k_h2, st));
     }
@@ -731,7 +785,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         t.xr_out = W.rmid;
         t.rms_eps = w->rms_eps;
         LAROSA_TRY(site(t, 2, L.d, plan->k_h3, a));
-        LAROSA_TRY(run_gemv(a, w->w_gu, L.d, plan->k_h3, L.dgu, W.acc_gu));
+        LAROSA_TRY(run_gemv(a, w->w_gu, L.d, plan->k_h3, L.dgu, W.acc_gu, 6));
         LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
         LAROSA_TRY(tap_copy(T.idx_h3, W.idx[2], sizeof(int32_t) * B * plan->k_h3, st));
         LAROSA_TRY(tap_copy(T.vals_h3, W.vals[2], sizeof(float) * B * plan->k_h3, st));
@@ -746,7 +800,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         t.xr_out = W.h4;
         t.rms_eps = -1.0f;
         LAROSA_TRY(site(t, 3, L.inter, plan->k_h4, a));
-        LAROSA_TRY(run_gemv(a, w->w_down, L.inter, plan->k_h4, L.d, W.acc_down));
+        LAROSA_TRY(run_gemv(a, w->w_down, L.inter, plan->k_h4, L.d, W.acc_down, 8));
         LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
         LAROSA_TRY(tap_copy(T.idx_h4, W.idx[3], sizeof(int32_t) * B * plan->k_h4, st));
         LAROSA_TRY(tap_copy(T.vals_h4, W.vals[3], sizeof(float) * B * plan->k_h4, st));
@@ -765,7 +819,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.vacc_ld = L.d;
         a.nrows = (int)L.d;
         a.batch = B;
-        LAROSA_TRY(run_gemv(a, w->adapter, L.d, L.d, L.d, W.acc_adp));
+        LAROSA_TRY(run_gemv(a, w->adapter, L.d, L.d, L.d, W.acc_adp, 9));
         f.acc1 = W.acc_adp;
         f.acc1_ld = L.d;
         f.out1 = s->resid;
@@ -776,7 +830,10 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         f.res2_ld = L.d;
         f.out2 = T.r_out;
         f.out2_ld = L.d;
-        LAROSA_TRY(launch_finalize(f, st));
+        f.zero3 = W.acc_qkv;          // attention read it; zero it for the next step
+        f.zero3_ld = L.nqkv;
+        f.zero3_n = (int)L.nqkv;
+        if (on(10)) LAROSA_TRY(launch_finalize(f, st));
     } else {
         f.acc1 = W.acc_down;
         f.acc1_ld = L.d;
@@ -784,7 +841,10 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         f.res1_ld = L.d;
         f.out1 = s->resid;
         f.out1_ld = L.d;
-        LAROSA_TRY(launch_finalize(f, st));
+        f.zero3 = W.acc_qkv;
+        f.zero3_ld = L.nqkv;
+        f.zero3_n = (int)L.nqkv;
+        if (on(10)) LAROSA_TRY(launch_finalize(f, st));
         LAROSA_TRY(tap_copy(T.r_out, s->resid, sizeof(float) * B * L.d, st));
     }
     return LAROSA_OK;

@@ -24,10 +24,10 @@ constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kTopkBins = 4096;
 
 __host__ __device__ constexpr size_t topk_smem_bytes(int d) {
-    return sizeof(int) * 2 * kTopkBins + sizeof(uint32_t) * (size_t)((d + 31) / 32) + sizeof(int) * 160;
+    return sizeof(int) * 2 * kTopkBins + sizeof(int) * 256 + 0 * (size_t)d;
 }
 
-// elements per thread (multiple of 4) for a vector of length d
+// elements per thread (rounded up to an instantiated size) for a vector of length d
 __host__ __device__ constexpr int topk_ept(int d) {
     return ((d + 4 * kTopkThreads - 1) / (4 * kTopkThreads)) * 4;
 }
@@ -67,76 +67,36 @@ __device__ __forceinline__ int topk_excl_scan(int v, int* sw, int* total) {
     return __shfl_sync(0xffffffffu, ti - t, wid) + inc - v;
 }
 
-template <int EPT, int MODE>
+template <int EPT>
 __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                             TopkSrcArgs src, unsigned char* smem_raw) {
+                             unsigned char* smem_raw) {
     constexpr int NT = kTopkThreads;
     int* hist0 = reinterpret_cast<int*>(smem_raw);
     int* hist1 = hist0 + kTopkBins;
-    const int nwords = (d + 31) / 32;
-    uint32_t* smask = reinterpret_cast<uint32_t*>(hist1 + kTopkBins);
-    int* scr = reinterpret_cast<int*>(smask + nwords);
-    int* s_wtot = scr;                                   // [0, 32)
-    int* s_wtot2 = scr + 32;                             // [32, 64)
-    float* s_ssq = reinterpret_cast<float*>(scr + 64);   // [64, 96)
-    int* s_res = scr + 96;                               // [96, 100)
+    int* scr = hist1 + kTopkBins;
+    int* s_wtot = scr;                                   // [0, 32)   scan scratch (select)
+    int* s_cnt = scr + 32;                               // [32, 160) per-round warp counts, 2 x [2][32]
+    float* s_ssq = reinterpret_cast<float*>(scr + 160);  // [160, 192)
+    int* s_res = scr + 192;                              // [192, 196) bucket result
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int i0 = tid * EPT;
 
-    // 1. values (raw fp32 bits) in registers; key = bits & 0x7fffffff (-0 == +0); sum of squares
+    // 1. strided ownership: element j*NT + tid lives in xv[j] (raw fp32 bits) -- coalesced
+    //    loads, and each warp-round of 32 consecutive elements is one mask word.
+    //    (L2 loads: the vector may have been written by other CTAs of this kernel's cluster.)
     uint32_t xv[EPT];
     float ssq = 0.f;
-    if constexpr (MODE == SRC_PLAIN) {
-        const bool vec = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 #pragma unroll
-        for (int c = 0; c < EPT / 4; ++c) {
-            const int i = i0 + 4 * c;
-            float v[4];
-            if (vec && i + 4 <= d) {
-                const float4 f = *reinterpret_cast<const float4*>(x + i);
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = (i + u < d) ? x[i + u] : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) xv[4 * c + u] = __float_as_uint(v[u]);
-        }
-    } else {
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = i0 + e;
-            float v = 0.f;
-            if (i < d) {
-                if constexpr (MODE == SRC_RESID_ACC) {
-                    v = (src.resid ? src.resid[i] : 0.f) + fix_to_f(src.acc[i]);
-                    src.acc[i] = 0ull;
-                } else {
-                    const int gi = (i / kGuBlock) * (2 * kGuBlock) + (i % kGuBlock);
-                    const float g = fix_to_f(src.acc[gi]);
-                    const float u = fix_to_f(src.acc[gi + kGuBlock]);
-                    src.acc[gi] = 0ull;
-                    src.acc[gi + kGuBlock] = 0ull;
-                    v = g / (1.0f + expf(-g)) * u;
-                }
-            }
-            xv[e] = __float_as_uint(v);
-        }
-    }
-    if (src.zero)
-        for (int i = tid; i < src.zero_n; i += NT) src.zero[i] = 0ull;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-        const float v = __uint_as_float(xv[e]);
+    for (int j = 0; j < EPT; ++j) {
+        const int i = j * NT + tid;
+        const float v = i < d ? __ldcg(x + i) : 0.f;
+        xv[j] = __float_as_uint(v);
         ssq = fmaf(v, v, ssq);
-        if (out.xr_out && i0 + e < d) out.xr_out[i0 + e] = v;
+        if (out.xr_out && i < d) out.xr_out[i] = v;
     }
-#define KEY(e) (xv[e] & 0x7fffffffu)
+#define KEY(j) (xv[j] & 0x7fffffffu)
     ssq = warp_sum(ssq);
     if (lane == 0) s_ssq[wid] = ssq;
     for (int b = tid; b < kTopkBins; b += NT) hist0[b] = 0;
-    if (out.mask)
-        for (int w = tid; w < nwords; w += NT) smask[w] = 0u;
     __syncthreads();
 
     // 2. radix select of the k-th largest key
@@ -156,8 +116,8 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
             const int nb = pass == 2 ? 128 : 4096;
             const uint32_t dmask = (uint32_t)(nb - 1);
 #pragma unroll
-            for (int e = 0; e < EPT; ++e)
-                if (i0 + e < d && (KEY(e) & pmask) == prefix) atomicAdd(&hist[(KEY(e) >> sh) & dmask], 1);
+            for (int j = 0; j < EPT; ++j)
+                if (j * NT + tid < d && (KEY(j) & pmask) == prefix) atomicAdd(&hist[(KEY(j) >> sh) & dmask], 1);
             if (pass < 2)
                 for (int b = tid; b < kTopkBins; b += NT) hnext[b] = 0;
             __syncthreads();
@@ -206,76 +166,63 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
     for (int w = 0; w < kTopkWarps; ++w) tot_ssq += s_ssq[w];   // fixed order: deterministic
     const float scale = rms_eps >= 0.f ? 1.0f / sqrtf(tot_ssq / (float)d + rms_eps) : 1.0f;
 
-    // 3. stable compaction over the contiguous ownership ranges
-    int n_gt = 0, n_eq = 0;
+    // 3. stable compaction, one round of NT consecutive elements at a time: warp ballots give
+    //    in-warp ranks, warp counts exchanged through shared memory (double-buffered, one
+    //    __syncthreads per round) give the block offsets; the stores are consecutive.
+    const uint32_t lt = (1u << lane) - 1u;
+    int base = 0, eq_base = 0;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-        if (i0 + e >= d) continue;
+    for (int j = 0; j < EPT; ++j) {
+        const int i = j * NT + tid;
+        const bool valid = i < d;
+        const uint32_t key = KEY(j);
+        bool gt, eq;
         if (exact_ge) {
-            n_gt += KEY(e) >= thr;
+            gt = valid && key >= thr;
+            eq = false;
         } else {
-            n_gt += KEY(e) > thr;
-            n_eq += KEY(e) == thr;
+            gt = valid && key > thr;
+            eq = valid && key == thr;
         }
-    }
-    int take_eq = 0;
-    if (tie_mode) {
-        int tot;
-        const int eq_before = topk_excl_scan(n_eq, s_wtot, &tot);
-        take_eq = min(n_eq, max(0, rem - eq_before));
-    }
-    int tot_sel;
-    int pos = topk_excl_scan(n_gt + take_eq, tie_mode ? s_wtot2 : s_wtot, &tot_sel);
-    int eq_seen = 0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-        const int i = i0 + e;
-        if (i >= d) continue;
-        bool sel;
-        if (exact_ge) {
-            sel = KEY(e) >= thr;
-        } else if (KEY(e) > thr) {
-            sel = true;
-        } else if (KEY(e) == thr) {
-            sel = eq_seen < take_eq;
-            ++eq_seen;
-        } else {
-            sel = false;
+        const uint32_t bgt = __ballot_sync(0xffffffffu, gt);
+        const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+        int* cnt = s_cnt + (j & 1) * 64;
+        if (lane == 0) {
+            cnt[wid] = __popc(bgt);
+            cnt[32 + wid] = __popc(beq);
         }
+        __syncthreads();
+        const int cg = cnt[lane], ce = cnt[32 + lane];
+        const int ig = warp_incl_scan(cg), ie = warp_incl_scan(ce);
+        const int wg = __shfl_sync(0xffffffffu, ig - cg, wid);        // gt before my warp
+        const int we = __shfl_sync(0xffffffffu, ie - ce, wid);        // eq before my warp
+        const int tg = __shfl_sync(0xffffffffu, ig, 31), te = __shfl_sync(0xffffffffu, ie, 31);
+        // eq element selected iff its index-ordered rank among eq elements is < rem
+        const int erank = eq_base + we + __popc(beq & lt);
+        const bool sel = gt || (eq && tie_mode && erank < rem);
+        const uint32_t bsel = __ballot_sync(0xffffffffu, sel);
+        // selected before me = gt before + min(eq before, rem) (eq are taken in index order)
+        const int eq_before_warp = eq_base + we;
+        const int sel_before_warp = base + wg + (tie_mode ? max(0, min(eq_before_warp, rem) - min(eq_base, rem)) : 0);
+        const int pos = sel_before_warp + __popc(bsel & lt);
         if (sel) {
             out.idx[pos] = i;
-            out.vals[pos] = __uint_as_float(xv[e]) * scale;
-            if (out.mask) atomicOr(&smask[i >> 5], 1u << (i & 31));
-            ++pos;
+            out.vals[pos] = __uint_as_float(xv[j]) * scale;
         }
+        if (out.mask && lane == 0 && j * NT + wid * 32 < d) out.mask[(j * NT + wid * 32) >> 5] = bsel;
+        base += tg + (tie_mode ? max(0, min(eq_base + te, rem) - min(eq_base, rem)) : 0);
+        eq_base += te;
     }
     if (out.scale_out && tid == 0) *out.scale_out = scale;
-    if (out.mask) {
-        __syncthreads();
-        for (int w = tid; w < nwords; w += NT) out.mask[w] = smask[w];
-    }
-}
 #undef KEY
-
-template <int MODE>
-__device__ __forceinline__ void block_topk_m(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                                             TopkSrcArgs src, unsigned char* smem) {
-    const int ept = topk_ept(d);
-    if (ept <= 4) block_topk_t<4, MODE>(x, d, k, rms_eps, out, src, smem);
-    else if (ept <= 8) block_topk_t<8, MODE>(x, d, k, rms_eps, out, src, smem);
-    else if (ept <= 12) block_topk_t<12, MODE>(x, d, k, rms_eps, out, src, smem);
-    else if (ept <= 16) block_topk_t<16, MODE>(x, d, k, rms_eps, out, src, smem);
-    else if (ept <= 24) block_topk_t<24, MODE>(x, d, k, rms_eps, out, src, smem);
-    else block_topk_t<32, MODE>(x, d, k, rms_eps, out, src, smem);
 }
 
-// One CTA per token: x [batch][ldx], outputs strided per token.
 struct TopkKernelArgs {
     const float* x;
     int64_t ldx;
     int d, k;
     float rms_eps;
-    float* xr_out;      // [batch][d] or null
+    float* xr_out;      // [batch][d]: copy of x (plain) / the finalised vector (other modes)
     int32_t* idx;       // [batch][k]
     float* vals;        // [batch][k]
     uint32_t* mask;     // [batch][ceil(d/32)] or null
@@ -286,30 +233,74 @@ struct TopkKernelArgs {
     unsigned long long* zero; int64_t zero_ld; int zero_n; // optional extra zeroing per token
 };
 
+// Source finalisation, spread over the CTAs of the token's cluster (coalesced): element i
+// of the site's input is computed from the producer GEMV's fixed-point accumulators, written
+// to xbuf (the materialised vector the layer keeps: r_mid, h4, x~) and the accumulators are
+// re-zeroed.  Then a cluster barrier and CTA 0 runs the select on the whole vector.
+template <int MODE>
+__device__ void topk_finalize_share(int d, int rank, int cs, TopkSrcArgs src, float* xbuf) {
+    const int chunk = (d + cs - 1) / cs;
+    const int lo = rank * chunk, hi = min(d, lo + chunk);
+#pragma unroll 1
+    for (int i = lo + (int)threadIdx.x; i < hi; i += kTopkThreads) {
+        float v;
+        if constexpr (MODE == SRC_RESID_ACC) {
+            v = (src.resid ? src.resid[i] : 0.f) + fix_to_f(src.acc[i]);
+            src.acc[i] = 0ull;
+        } else {
+            const int gi = (i / kGuBlock) * (2 * kGuBlock) + (i % kGuBlock);
+            const float g = fix_to_f(src.acc[gi]);
+            const float u = fix_to_f(src.acc[gi + kGuBlock]);
+            src.acc[gi] = 0ull;
+            src.acc[gi + kGuBlock] = 0ull;
+            v = g / (1.0f + expf(-g)) * u;
+        }
+        xbuf[i] = v;
+    }
+    if (src.zero) {
+        const int zc = (src.zero_n + cs - 1) / cs;
+        const int zlo = rank * zc, zhi = min(src.zero_n, zlo + zc);
+        for (int i = zlo + (int)threadIdx.x; i < zhi; i += kTopkThreads) src.zero[i] = 0ull;
+    }
+}
+
+__device__ __forceinline__ void topk_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// grid = (CS, batch), cluster (CS, 1, 1): one cluster per token.  One kernel per (source
+// mode, elements per thread) so each launch only fetches its own (small) code: these
+// latency-bound kernels stalled on instruction-cache misses when one body held every variant.
+template <int MODE, int EPT>
 __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     pdl_wait();
     pdl_trigger();
-    const int b = blockIdx.x;
+    const int b = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
     const int nwords = (a.d + 31) / 32;
     TopkOut o;
-    o.xr_out = a.xr_out ? a.xr_out + (size_t)b * a.d : nullptr;
+    o.xr_out = nullptr;
     o.idx = a.idx + (size_t)b * a.k;
     o.vals = a.vals + (size_t)b * a.k;
     o.mask = a.mask ? a.mask + (size_t)b * nwords : nullptr;
     o.scale_out = a.scale ? a.scale + b : nullptr;
-    TopkSrcArgs src;
-    src.resid = a.resid ? a.resid + (size_t)b * a.resid_ld : nullptr;
-    src.acc = a.acc ? a.acc + (size_t)b * a.acc_ld : nullptr;
-    src.zero = a.zero ? a.zero + (size_t)b * a.zero_ld : nullptr;
-    src.zero_n = a.zero_n;
-    const float* x = a.x ? a.x + (size_t)b * a.ldx : nullptr;
-    if (a.mode == SRC_RESID_ACC)
-        block_topk_m<SRC_RESID_ACC>(x, a.d, a.k, a.rms_eps, o, src, smem);
-    else if (a.mode == SRC_SILU_GU)
-        block_topk_m<SRC_SILU_GU>(x, a.d, a.k, a.rms_eps, o, src, smem);
-    else
-        block_topk_m<SRC_PLAIN>(x, a.d, a.k, a.rms_eps, o, src, smem);
+    const float* x;
+    if constexpr (MODE == SRC_PLAIN) {
+        x = a.x + (size_t)b * a.ldx;
+        o.xr_out = a.xr_out ? a.xr_out + (size_t)b * a.d : nullptr;
+    } else {
+        TopkSrcArgs src;
+        src.resid = a.resid ? a.resid + (size_t)b * a.resid_ld : nullptr;
+        src.acc = a.acc + (size_t)b * a.acc_ld;
+        src.zero = a.zero ? a.zero + (size_t)b * a.zero_ld : nullptr;
+        src.zero_n = a.zero_n;
+        float* xbuf = a.xr_out + (size_t)b * a.d;
+        topk_finalize_share<MODE>(a.d, rank, cs, src, xbuf);
+        topk_cluster_sync();
+        x = xbuf;
+    }
+    if (rank != 0) return;
+    block_topk_t<EPT>(x, a.d, a.k, a.rms_eps, o, smem);
 }
 
 }  // namespace larosa

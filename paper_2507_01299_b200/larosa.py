@@ -85,6 +85,10 @@ def lib() -> ctypes.CDLL:
     L.larosa_sparse_gemv_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64, _c_i64]
     L.larosa_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i32, _c_i64, _vp, _vp, _vp,
                                      ctypes.c_size_t, _vp]
+    L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
+    L.larosa_debug_set_layer_phases.restype = None
+    L.larosa_gemv_plan_info.argtypes = [_c_i64, _c_i64, _c_i32, ctypes.POINTER(_c_i32)]
+    L.larosa_gemv_plan_info.restype = ctypes.c_int
     L.larosa_layer_workspace_size.restype = ctypes.c_size_t
     L.larosa_layer_workspace_size.argtypes = [ctypes.POINTER(LayerWeightsC), _c_i32, _c_i64]
     L.larosa_sparse_layer.argtypes = [ctypes.POINTER(LayerWeightsC), ctypes.POINTER(LayerPlanC),
