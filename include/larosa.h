@@ -219,6 +219,9 @@ size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch,
  * LAROSA_LAYER_PHASES environment variable. */
 #define LAROSA_PHASES_GEMV_ONLY 0x352
 void larosa_debug_set_layer_phases(int mask);
+/* Profiling aid: device buffer of 4 x 16 uint64 receiving %globaltimer stamps of the
+ * threshold kernels' last CTA (NULL disables). */
+void larosa_debug_set_thresh_stamps(void* dev_buf);
 larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                   const larosa_layer_state* state, const larosa_layer_taps* taps,
                                   void* ws, size_t ws_bytes, larosa_stream_t stream);

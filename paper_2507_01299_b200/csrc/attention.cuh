@@ -205,7 +205,7 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             myp[j * (hd + 2) + 1] = L;
         }
     }
-    __threadfence();
+    fence_acq_rel_gpu();
     __syncthreads();
     if (tid == 0) {
         const unsigned prev = atomicAdd(&a.counters[bg], 1u);
@@ -214,22 +214,39 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     __syncthreads();
     if (!sflag[0]) return;
     if (tid == 0) a.counters[bg] = 0u;
-    __threadfence();
+    fence_acq_rel_gpu();
 
-    // merge the chunks in order
+    // merge the chunks in order (each batch of chunk records is loaded before it is used:
+    // __ldcg is a volatile load, so a load->use loop would serialise the L2 round trips)
     const float* pb = a.part + (size_t)bg * a.n_chunks * G * (hd + 2);
     for (int i = tid; i < G * hd; i += kAttnThreads) {
         const int j = i / hd, dd = i % hd;
-        float M = -INFINITY;
-        for (int c = 0; c < a.n_chunks; ++c) M = fmaxf(M, __ldcg(pb + ((size_t)c * G + j) * (hd + 2)));
-        float L = 0.f, Ov = 0.f;
-        for (int c = 0; c < a.n_chunks; ++c) {
-            const float* r = pb + ((size_t)c * G + j) * (hd + 2);
-            const float l = __ldcg(r + 1);
-            if (l == 0.f) continue;
-            const float w = expf(__ldcg(r) - M);
-            L = fmaf(l, w, L);
-            Ov = fmaf(__ldcg(r + 2 + dd), w, Ov);
+        float M = -INFINITY, L = 0.f, Ov = 0.f;
+        for (int c0 = 0; c0 < a.n_chunks; c0 += 16) {
+            float mc[16], lc[16], oc[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const float* r = pb + ((size_t)(c0 + u) * G + j) * (hd + 2);
+                const bool ok = c0 + u < a.n_chunks;
+                mc[u] = ok ? __ldcg(r) : -INFINITY;
+                lc[u] = ok ? __ldcg(r + 1) : 0.f;
+                oc[u] = ok ? __ldcg(r + 2 + dd) : 0.f;
+            }
+            float Mn = M;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) Mn = fmaxf(Mn, lc[u] == 0.f ? -INFINITY : mc[u]);
+            if (Mn == -INFINITY) continue;
+            const float rescale = M == -INFINITY ? 0.f : expf(M - Mn);
+            L *= rescale;
+            Ov *= rescale;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (lc[u] == 0.f) continue;
+                const float w = expf(mc[u] - Mn);
+                L = fmaf(lc[u], w, L);
+                Ov = fmaf(oc[u], w, Ov);
+            }
+            M = Mn;
         }
         a.out[(size_t)b * a.hq * hd + (size_t)(g * G + j) * hd + dd] = Ov / L;
     }

@@ -36,27 +36,54 @@ constexpr int kStages = 4;            // ring depth per warp
 constexpr int kWarpRingBytes = kStages * kStageRows * kSliceCols * 2;   // 8 KB
 constexpr double kFixScale = 4294967296.0;                              // 2^32
 
+enum GemvMode : int {
+    GEMV_LIST = 0,     // kept rows given as a list (rows[], vals) -- split by list position
+    GEMV_THRESH = 1,   // kept rows selected in-kernel from x by the Top-K rule (thresh.cuh)
+    GEMV_DENSE = 2,    // every row, value x (+ vacc) -- the residual adapter
+};
+
+// the per-token Top-K rule produced by thresh.cuh: keep row i iff
+// key_i > tk or (key_i == tk and i <= ti), key = bits(|x_i|); value x_i * scale
+struct ThreshOut {
+    uint32_t tk;       // key threshold
+    int32_t ti;        // index threshold for key == tk (inclusive)
+    float scale;       // RMS scale (1 if no RMS)
+    int32_t pad;
+};
+
 struct GemvArgs {
     const uint16_t* W;
     int64_t ld;
     int d_out;
-    const int32_t* rows;   // kept row indices (ascending); nullptr -> dense (row r = r)
+    int mode;              // GemvMode
+    // GEMV_LIST
+    const int32_t* rows;   // kept row indices (ascending)
     int nrows;             // row count when nrows_dev == nullptr
     const int* nrows_dev;  // device row count (batch > 1 union), or nullptr
-    const float* vals;     // val(r, b) = vals[r * vs_r + b * vs_b] (+ vacc, see below)
+    const float* vals;     // val(r, b) = vals[r * vs_r + b * vs_b]
     int64_t vs_r, vs_b;
-    const unsigned long long* vacc;   // optional (dense mode): val += fix^-1(vacc[b * vacc_ld + r])
+    // GEMV_THRESH / GEMV_DENSE: input x [batch][ldx] over rows [0, d_in)
+    const float* x;
+    int64_t ldx;
+    int d_in;
+    const ThreshOut* thr;              // THRESH: per-token rule + RMS scale
+    const unsigned long long* vacc;    // DENSE (optional): val += fix^-1(vacc[b * vacc_ld + r])
     int64_t vacc_ld;
     int batch;             // real tokens (<= template BP)
     int n_splits;
+    int list_cap;          // rows of the per-CTA shared list (host-checked >= rows per split)
     unsigned long long* acc;          // [batch][acc_ld] fixed-point output accumulators
     int64_t acc_ld;
 };
 
-__host__ __device__ constexpr size_t gemv_smem_bytes(int bp) {
+// ring (aliased by the warp partials at the end) + the CTA's row list [cap] and values [cap][bp]
+__host__ __device__ constexpr size_t gemv_ring_bytes(int bp) {
     return (size_t)kGemvWarps * kWarpRingBytes > (size_t)kGemvWarps * bp * kSliceCols * 4
                ? (size_t)kGemvWarps * kWarpRingBytes
                : (size_t)kGemvWarps * bp * kSliceCols * 4;
+}
+__host__ __device__ constexpr size_t gemv_smem_bytes(int bp, int list_cap) {
+    return gemv_ring_bytes(bp) + (size_t)list_cap * (4 + 4 * (size_t)bp) + 128;
 }
 
 __device__ __forceinline__ float fix_to_f(unsigned long long a) {
@@ -96,56 +123,94 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
     extern __shared__ __align__(128) unsigned char smem[];
     const int slice = blockIdx.x, split = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* lrow = reinterpret_cast<int*>(smem + gemv_ring_bytes(BP));           // [cap]
+    float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                // [cap][BP]
+    int* s_cnt = reinterpret_cast<int*>(lval + (size_t)a.list_cap * BP);      // [2][8] + [1]
 
-    pdl_wait();       // rows / vals / nrows come from the previous kernel
+    pdl_wait();       // the row source comes from the previous kernel
     pdl_trigger();
 
-    const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
-    const int rps = (nrows + a.n_splits - 1) / a.n_splits;
-    const int r_begin = min(nrows, split * rps);
-    const int r_end = min(nrows, r_begin + rps);
-    // my rows: r_begin + warp + 8*m, m in [0, n_my)
-    const int n_my = r_end - r_begin > warp ? (r_end - r_begin - warp + kGemvWarps - 1) / kGemvWarps : 0;
+    // ---- 1. this CTA's row list in shared memory (ascending) ------------------------------
+    int n_list = 0;
+    if (a.mode == GEMV_LIST) {
+        const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
+        const int rps = (nrows + a.n_splits - 1) / a.n_splits;
+        const int r_begin = min(nrows, split * rps);
+        n_list = min(nrows, r_begin + rps) - r_begin;
+        for (int t = threadIdx.x; t < n_list; t += kGemvWarps * 32) {
+            const int r = r_begin + t;
+            lrow[t] = __ldg(a.rows + r);
+#pragma unroll
+            for (int b = 0; b < BP; ++b)
+                lval[t * BP + b] = b < a.batch ? __ldg(a.vals + (size_t)r * a.vs_r + (size_t)b * a.vs_b) : 0.f;
+        }
+    } else {
+        // input range of this split; keep a row if any token keeps it (THRESH rule) or always
+        const int rng = (a.d_in + a.n_splits - 1) / a.n_splits;
+        const int lo = min(a.d_in, split * rng), hi = min(a.d_in, lo + rng);
+        const ThreshOut* thr = a.thr;
+        int base = 0;
+        for (int r0 = lo, rnd = 0; r0 < hi; r0 += kGemvWarps * 32, ++rnd) {
+            const int i = r0 + (int)threadIdx.x;
+            float v[BP];
+            bool any = false;
+#pragma unroll
+            for (int b = 0; b < BP; ++b) {
+                float x = 0.f;
+                bool keep = false;
+                if (i < hi && b < a.batch) {
+                    x = a.x[(size_t)b * a.ldx + i];
+                    if (a.vacc) x += fix_to_f(a.vacc[(size_t)b * a.vacc_ld + i]);
+                    if (a.mode == GEMV_DENSE) {
+                        keep = true;
+                    } else {
+                        const uint32_t key = __float_as_uint(x) & 0x7fffffffu;
+                        keep = key > thr[b].tk || (key == thr[b].tk && i <= thr[b].ti);
+                        x *= thr[b].scale;
+                    }
+                }
+                v[b] = keep ? x : 0.f;
+                any |= keep;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, any);
+            int* cnt = s_cnt + (rnd & 1) * 8;
+            if (lane == 0) cnt[warp] = __popc(bal);
+            __syncthreads();
+            int before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < kGemvWarps; ++w) {
+                const int cw = cnt[w];
+                before += w < warp ? cw : 0;
+                total += cw;
+            }
+            if (any) {
+                const int pos = base + before + __popc(bal & ((1u << lane) - 1u));
+                lrow[pos] = i;
+#pragma unroll
+                for (int b = 0; b < BP; ++b) lval[pos * BP + b] = v[b];
+            }
+            base += total;
+        }
+        n_list = base;
+    }
+    __syncthreads();
+
+    // my rows: list entries warp + 8*m, m in [0, n_my)
+    const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
     const int col0 = slice * kSliceCols + lane * 8;
     const bool lane_on = col0 < a.d_out;          // d_out % 8 == 0: a lane's chunk is all-in or all-out
     const int n_st = (n_my + kStageRows - 1) / kStageRows;
     unsigned char* mychunk = smem + (size_t)warp * kWarpRingBytes + lane * 16;
     const uint16_t* wcol = a.W + col0;
 
-    // rows / values in 32-row windows (lane j holds my-row base + j), double-buffered
-    auto load_row = [&](int m) -> int {
-        const int r = r_begin + warp + kGemvWarps * m;
-        return m < n_my ? (a.rows ? __ldg(a.rows + r) : r) : 0;
-    };
-    auto load_vals = [&](int m, float* v) {
-        const int r = r_begin + warp + kGemvWarps * m;
-#pragma unroll
-        for (int b = 0; b < BP; ++b) {
-            float x = 0.f;
-            if (m < n_my && b < a.batch) {
-                x = __ldg(a.vals + (size_t)r * a.vs_r + (size_t)b * a.vs_b);
-                if (a.vacc) x += fix_to_f(a.vacc[(size_t)b * a.vacc_ld + r]);
-            }
-            v[b] = x;
-        }
-    };
-    int iw_row = load_row(lane), iw_next = load_row(32 + lane);
-    float vwin[BP], vnext[BP];
-    load_vals(lane, vwin);
-    load_vals(32 + lane, vnext);
-
-    // stage st covers my-rows [4 st, 4 st + 4); window w = st / 8 covers my-rows [32 w, 32 w + 32)
+    // stage st covers my-rows [4 st, 4 st + 4)
     auto issue = [&](int st) {
         if (st < n_st) {
-            if (st > 0 && (st & 7) == 0) {
-                iw_row = iw_next;
-                iw_next = load_row(st * kStageRows + 32 + lane);
-            }
             unsigned char* dst = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
 #pragma unroll
             for (int g = 0; g < kStageRows; ++g) {
                 const int m = st * kStageRows + g;
-                const int row = __shfl_sync(0xffffffffu, iw_row, m & 31);
+                const int row = m < n_my ? lrow[warp + kGemvWarps * m] : 0;
                 cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < n_my);
             }
         }
@@ -161,23 +226,19 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
         for (int j = 0; j < 4; ++j) acc[b][j] = make_float2(0.f, 0.f);
 
     for (int st = 0; st < n_st; ++st) {
-        if (st > 0 && (st & 7) == 0) {
-#pragma unroll
-            for (int b = 0; b < BP; ++b) vwin[b] = vnext[b];
-            load_vals(st * kStageRows + 32 + lane, vnext);
-        }
         cp_async_wait<kStages - 1>();          // this lane's chunks of stage st have landed
         const unsigned char* src = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
 #pragma unroll
         for (int g = 0; g < kStageRows; ++g) {
             const int m = st * kStageRows + g;
+            if (m >= n_my) break;                // short last stage (warp-uniform)
             const uint4 w = lds128(src + g * (kSliceCols * 2));
             const float w0 = bf16lo(w.x), w1 = bf16hi(w.x), w2 = bf16lo(w.y), w3 = bf16hi(w.y);
             const float w4 = bf16lo(w.z), w5 = bf16hi(w.z), w6 = bf16lo(w.w), w7 = bf16hi(w.w);
-            if (m >= n_my) break;                // short last stage (warp-uniform)
+            const float* vrow = lval + (size_t)(warp + kGemvWarps * m) * BP;
 #pragma unroll
             for (int b = 0; b < BP; ++b) {
-                const float v = __shfl_sync(0xffffffffu, vwin[b], m & 31);
+                const float v = vrow[b];             // shared-memory broadcast
                 ffma2(acc[b][0], w0, w1, v);
                 ffma2(acc[b][1], w2, w3, v);
                 ffma2(acc[b][2], w4, w5, v);
@@ -200,7 +261,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
     __syncthreads();
     const int c = threadIdx.x;                     // 256 threads <-> 256 columns
     const int o = slice * kSliceCols + c;
-    if (o < a.d_out && r_end > r_begin) {
+    if (o < a.d_out && n_list > 0) {
         for (int b = 0; b < a.batch; ++b) {
             float s = 0.f;
 #pragma unroll

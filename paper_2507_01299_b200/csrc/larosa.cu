@@ -16,6 +16,7 @@
 #include "gemv.cuh"
 #include "attention.cuh"
 #include "aux.cuh"
+#include "thresh.cuh"
 #include "fold_tc.cuh"
 
 using namespace larosa;
@@ -122,7 +123,7 @@ int pad_batch(int b) { return b <= 1 ? 1 : b <= 2 ? 2 : b <= 4 ? 4 : b <= 8 ? 8 
 
 // ============================================================================== GEMV plan
 struct GemvPlan {
-    int n_slices, n_splits;
+    int n_slices, n_splits, list_cap;
     size_t smem;
 };
 
@@ -131,18 +132,24 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 
-// 256-column slices x kept-row splits, about `per_sm` 256-thread CTAs per SM in one wave;
-// at least 16 rows per split so each warp has a few rows to pipeline.
-GemvPlan plan_gemv(int64_t d_out, int64_t nrows_max, int bp) {
+int gemv_list_max(int bp) { return bp <= 2 ? 2048 : 1024; }
+
+// 256-column slices x row splits, about `per_sm` 256-thread CTAs per SM in one wave.
+// rows_per_split_src: the number of candidate rows a split may hold (list length for
+// GEMV_LIST, input length for GEMV_THRESH / GEMV_DENSE), bounded by the shared list.
+GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp) {
     static const int per_sm_env = env_int("LAROSA_GEMV_CTAS_PER_SM", 0);   // tuning knob (0 = auto)
     GemvPlan p;
     p.n_slices = (int)((d_out + kSliceCols - 1) / kSliceCols);
-    p.smem = gemv_smem_bytes(bp);
-    const int per_sm = per_sm_env > 0 ? per_sm_env : (bp <= 4 ? 3 : 1);
+    const int per_sm = per_sm_env > 0 ? per_sm_env : (bp <= 4 ? 2 : 1);
     const int target = sm_count() * per_sm;
     const int by_target = std::max(1, (target + p.n_slices / 2) / p.n_slices);
-    const int by_rows = (int)std::max<int64_t>(1, nrows_max / 16);
-    p.n_splits = std::min(by_target, by_rows);
+    const int by_rows = (int)std::max<int64_t>(1, rows_src / 16);
+    const int lmax = gemv_list_max(bp);
+    const int by_cap = (int)std::max<int64_t>(1, (rows_src + lmax - 1) / lmax);
+    p.n_splits = std::max(by_cap, std::min(by_target, by_rows));
+    p.list_cap = (int)std::max<int64_t>(32, (rows_src + p.n_splits - 1) / p.n_splits);
+    p.smem = gemv_smem_bytes(bp, p.list_cap);
     return p;
 }
 
@@ -151,10 +158,13 @@ larosa_status launch_gemv_bp(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     auto kern = gemv_kernel<BP>;
     static bool attr_done = false;
     if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, gemv_smem_bytes(BP)), "cudaFuncSetAttribute(gemv)"));
+        LAROSA_TRY(cuda_check(allow_smem(kern, gemv_smem_bytes(BP, gemv_list_max(BP))), "cudaFuncSetAttribute(gemv)"));
         attr_done = true;
     }
-    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvWarps * 32), p.smem, st, a), "gemv launch");
+    GemvArgs aa = a;
+    aa.n_splits = p.n_splits;
+    aa.list_cap = p.list_cap;
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvWarps * 32), p.smem, st, aa), "gemv launch");
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
@@ -182,8 +192,7 @@ larosa_status launch_topk_t(const TopkKernelArgs& a, int batch, cudaStream_t st)
         LAROSA_TRY(cuda_check(allow_smem(kern, topk_smem_bytes(LAROSA_MAX_DIM)), "cudaFuncSetAttribute(topk)"));
         attr_done = true;
     }
-    // cluster of CS CTAs per token spreads the source finalisation (accumulator reads/zeroing)
-    const int cs = MODE == SRC_PLAIN ? 1 : std::max(1, std::min(8, (a.d + 1535) / 1536));
+    const int cs = topk_cluster_size(a.d);   // one cluster of cs CTAs per token
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, batch);
     cfg.blockDim = dim3(kTopkThreads);
@@ -208,12 +217,10 @@ larosa_status launch_topk_t(const TopkKernelArgs& a, int batch, cudaStream_t st)
 template <int MODE>
 larosa_status launch_topk_m(const TopkKernelArgs& a, int batch, cudaStream_t st) {
     const int ept = topk_ept(a.d);
+    if (ept <= 2) return launch_topk_t<MODE, 2>(a, batch, st);
     if (ept <= 4) return launch_topk_t<MODE, 4>(a, batch, st);
-    if (ept <= 8) return launch_topk_t<MODE, 8>(a, batch, st);
-    if (ept <= 12) return launch_topk_t<MODE, 12>(a, batch, st);
-    if (ept <= 16) return launch_topk_t<MODE, 16>(a, batch, st);
-    if (ept <= 24) return launch_topk_t<MODE, 24>(a, batch, st);
-    return launch_topk_t<MODE, 32>(a, batch, st);
+    if (ept <= 6) return launch_topk_t<MODE, 6>(a, batch, st);
+    return launch_topk_t<MODE, 8>(a, batch, st);
 }
 
 larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
@@ -358,8 +365,8 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     a.W = W;
     a.ld = ld;
     a.d_out = (int)d_out;
+    a.mode = GEMV_LIST;
     a.batch = batch;
-    a.n_splits = p.n_splits;
     a.acc = acc;
     a.acc_ld = d_out;
     if (batch == 1) {
@@ -465,12 +472,11 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
         a.W = R;
         a.ld = d;
         a.d_out = (int)d;
-        a.vals = x;
-        a.vs_r = 1;
-        a.vs_b = d;
-        a.nrows = (int)d;
+        a.mode = GEMV_DENSE;
+        a.x = x;
+        a.ldx = d;
+        a.d_in = (int)d;
         a.batch = batch;
-        a.n_splits = p.n_splits;
         a.acc = acc;
         a.acc_ld = d;
         LAROSA_TRY(launch_gemv(a, p, bp, st));
@@ -528,17 +534,19 @@ extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t*
 
 // ============================================================================== decoder layer
 namespace {
+struct SiteWs {
+    uint32_t* ghist;      // [B][4096]  zero at rest
+    unsigned* ticket;     // [B]        zero at rest
+    float* ssq;           // [B][NB]
+    ThreshOut* thr;       // [B]
+};
+
 struct LayerWs {
     unsigned long long *acc_qkv, *acc_o, *acc_gu, *acc_down, *acc_adp;
-    int32_t* idx[4];
-    float* vals[4];
-    uint32_t* mask[4];
+    SiteWs site[4];
     float* h2;
     float* rmid;
     float* h4;
-    int32_t* urows;
-    float* uV;
-    int* unrows;
     float* attn_part;
     unsigned* attn_cnt;
 };
@@ -570,28 +578,26 @@ int attn_chunk(int64_t max_ctx, int units) {
 }
 
 void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, LayerWs* ws) {
-    const int bp = pad_batch(batch);
     const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     LayerWs tmp;
     LayerWs* o = ws ? ws : &tmp;
-    // accumulators first (zero at rest)
+    // zero-at-rest state first: GEMV accumulators, threshold histograms and tickets
     o->acc_qkv = c.take<unsigned long long>((size_t)batch * L.nqkv);
     o->acc_o = c.take<unsigned long long>((size_t)batch * L.d);
     o->acc_gu = c.take<unsigned long long>((size_t)batch * L.dgu);
     o->acc_down = c.take<unsigned long long>((size_t)batch * L.d);
     o->acc_adp = c.take<unsigned long long>((size_t)batch * L.d);
     for (int s = 0; s < 4; ++s) {
-        o->idx[s] = c.take<int32_t>((size_t)batch * din[s]);
-        o->vals[s] = c.take<float>((size_t)batch * din[s]);
-        o->mask[s] = c.take<uint32_t>((size_t)batch * ((din[s] + 31) / 32));
+        o->site[s].ghist = c.take<uint32_t>((size_t)batch * kThrBins);
+        o->site[s].ticket = c.take<unsigned>((size_t)batch);
+    }
+    for (int s = 0; s < 4; ++s) {
+        o->site[s].ssq = c.take<float>((size_t)batch * thresh_nb((int)din[s]));
+        o->site[s].thr = c.take<ThreshOut>((size_t)batch);
     }
     o->h2 = c.take<float>((size_t)batch * L.nq);
     o->rmid = c.take<float>((size_t)batch * L.d);
     o->h4 = c.take<float>((size_t)batch * L.inter);
-    const int64_t dmax = std::max(std::max(L.d, L.nq), L.inter);
-    o->urows = c.take<int32_t>((size_t)dmax);
-    o->uV = c.take<float>((size_t)dmax * bp + 16);
-    o->unrows = c.take<int>(4);
     const int ch = attn_chunk(max_ctx, batch * (int)L.hkv);
     const int nch = (int)((max_ctx + ch - 1) / ch);
     o->attn_part = c.take<float>((size_t)batch * L.hkv * nch * L.G * (L.hd + 2));
@@ -629,15 +635,38 @@ larosa_status tap_copy(void* dst, const void* src, size_t bytes, cudaStream_t st
     if (!dst) return LAROSA_OK;
     return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st), "tap copy");
 }
-}  // namespace
+
+template <int MODE>
+larosa_status launch_thresh_m(const ThreshArgs& t, int batch, cudaStream_t st) {
+    return cuda_check(launch(thresh_kernel<MODE>, dim3(thresh_nb(t.d), batch), dim3(kThrThreads), 0, st, t),
+                      "thresh launch");
+}
+larosa_status launch_thresh(const ThreshArgs& t, int batch, cudaStream_t st) {
+    if (t.mode == THR_RESID_ACC) return launch_thresh_m<THR_RESID_ACC>(t, batch, st);
+    if (t.mode == THR_SILU_GU) return launch_thresh_m<THR_SILU_GU>(t, batch, st);
+    return launch_thresh_m<THR_PLAIN>(t, batch, st);
+}
+
+static_assert((int)THR_PLAIN == (int)SRC_PLAIN && (int)THR_RESID_ACC == (int)SRC_RESID_ACC &&
+                  (int)THR_SILU_GU == (int)SRC_SILU_GU,
+              "source enums must agree");
+// the single-wave ticket threshold kernel (thresh.cuh) instead of the cluster Top-K
+bool use_ticket_thresh() {
+    static const int v = env_int("LAROSA_THRESH_KERNEL", 0);
+    return v != 0;
+}
 
 // profiling aid: bitmask of the layer's kernels that are launched (default: all)
-static int g_phase_mask = -2;
-static int layer_phase_mask() {
+int g_phase_mask = -2;
+unsigned long long* g_thr_dbg = nullptr;   // device buffer [4][16] of threshold-kernel stamps
+int layer_phase_mask() {
     if (g_phase_mask == -2) g_phase_mask = env_int("LAROSA_LAYER_PHASES", -1);
     return g_phase_mask;
 }
+}  // namespace
+
 extern "C" void larosa_debug_set_layer_phases(int mask) { g_phase_mask = mask; }
+extern "C" void larosa_debug_set_thresh_stamps(void* dev_buf) { g_thr_dbg = static_cast<unsigned long long*>(dev_buf); }
 
 extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx) {
     if (!w || batch < 1 || max_ctx <= 0) return 0;
@@ -647,17 +676,18 @@ extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int
 }
 
 // Kernel sequence (one decode step of one layer; every kernel is launched with PDL):
-//   topk(h1 = r)            -> idx1, vals1 (RMS-scaled)                 [+ union for batch > 1]
-//   gemv(W_qkv)             -> acc_qkv
-//   attention               <- acc_qkv (+bias, RoPE, KV append)        -> h2
-//   topk(h2), zero acc_qkv  -> idx2, vals2
-//   gemv(W_o)               -> acc_o
-//   topk(h3 = r + acc_o)    -> r_mid, idx3, vals3 (RMS-scaled); zero acc_o
-//   gemv(W_gate|up)         -> acc_gu
-//   topk(h4 = SiLU(g) * u)  -> h4, idx4, vals4; zero acc_gu
-//   gemv(W_down)            -> acc_down
-//   gemv(adapter, dense; values r_mid + acc_down) -> acc_adp            (if adapter)
-//   finalize: r <- acc_adp  (or r_mid + acc_down); zero acc_down, acc_adp
+//   thresh(h1 = r, RMS)                       -> rule T1, s1
+//   gemv(W_qkv, THRESH: rows kept by T1)      -> acc_qkv
+//   attention <- acc_qkv (+bias, RoPE, KV append)          -> h2
+//   thresh(h2)                                -> T2
+//   gemv(W_o, THRESH)                         -> acc_o
+//   thresh(h3 = r + acc_o, RMS; zero acc_o)   -> r_mid, T3, s3
+//   gemv(W_gate|up, THRESH)                   -> acc_gu
+//   thresh(h4 = SiLU(g) * u; zero acc_gu)     -> h4, T4
+//   gemv(W_down, THRESH)                      -> acc_down
+//   gemv(adapter, DENSE; values r_mid + acc_down)          -> acc_adp          (if adapter)
+//   finalize: r <- acc_adp  (or r_mid + acc_down); zero acc_down, acc_adp, acc_qkv
+// Taps (parity checks) add exact index-list Top-K launches on the materialised inputs.
 extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                              const larosa_layer_state* s, const larosa_layer_taps* taps, void* ws,
                                              size_t ws_bytes, larosa_stream_t stream) {
@@ -678,59 +708,75 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     else
         memset(&T, 0, sizeof(T));
 
-    // Top-K at a site (t prepared by the caller), then the GEMV row source for batch 1 or 2+
-    auto site = [&](TopkKernelArgs t, int si, int64_t din, int64_t k, GemvArgs& a) -> larosa_status {
-        t.ldx = din;
+    // one site: threshold kernel, optional exact index-list tap, THRESH GEMV
+    auto site = [&](int si, ThreshArgs t, int64_t din, int64_t k, const float* xmat, int32_t* tap_idx,
+                    float* tap_vals, const uint16_t* Wt, int64_t dout, unsigned long long* acc) -> larosa_status {
         t.d = (int)din;
         t.k = (int)k;
-        t.idx = W.idx[si];
-        t.vals = W.vals[si];
-        t.mask = B > 1 ? W.mask[si] : nullptr;
-        if (on(2 * si + (si > 0 ? 1 : 0))) LAROSA_TRY(launch_topk(t, B, st));
-        if (B == 1) {
-            a.rows = W.idx[si];
-            a.vals = W.vals[si];
-            a.vs_r = 1;
-            a.vs_b = k;
-            a.nrows = (int)k;
-            a.nrows_dev = nullptr;
+        t.ghist = W.site[si].ghist;
+        t.ticket = W.site[si].ticket;
+        t.ssq_part = W.site[si].ssq;
+        t.out = W.site[si].thr;
+        t.dbg = g_thr_dbg ? g_thr_dbg + 32 * si : nullptr;
+        if (!on(si == 0 ? 0 : 2 * si + 1)) {
+        } else if (use_ticket_thresh()) {
+            LAROSA_TRY(launch_thresh(t, B, st));
         } else {
-            const int nw = (int)((din + 31) / 32);
-            LAROSA_TRY(launch_union(W.mask[si], nw, B, bp, W.vals[si], k, (int)din, W.urows, W.uV, W.unrows, st));
-            a.rows = W.urows;
-            a.vals = W.uV;
-            a.vs_r = bp;
-            a.vs_b = 1;
-            a.nrows = 0;
-            a.nrows_dev = W.unrows;
+            // cluster Top-K in rule mode: finalises the fused source, emits (Tk, Ti, s)
+            TopkKernelArgs r = topk_args_base();
+            r.mode = t.mode;   // ThrSrc and TopkSrc share their numbering
+            r.x = t.x;
+            r.ldx = t.ldx;
+            r.d = (int)din;
+            r.k = (int)k;
+            r.rms_eps = t.rms_eps;
+            r.xr_out = t.xout;
+            r.resid = t.resid;
+            r.resid_ld = t.resid_ld;
+            r.acc = t.acc;
+            r.acc_ld = t.acc_ld;
+            r.rule_out = W.site[si].thr;
+            LAROSA_TRY(launch_topk(r, B, st));
         }
-        a.batch = B;
-        return LAROSA_OK;
-    };
-    auto nrows_max = [&](int64_t din, int64_t k) { return B == 1 ? k : std::min<int64_t>(din, (int64_t)B * k); };
-    auto run_gemv = [&](GemvArgs& a, const uint16_t* Wt, int64_t din, int64_t k, int64_t dout,
-                        unsigned long long* acc, int bit) -> larosa_status {
+        if (tap_idx || tap_vals) {
+            // exact ascending index list + values (same rule) for parity checks
+            TopkKernelArgs tk = topk_args_base();
+            tk.x = xmat;
+            tk.ldx = din;
+            tk.d = (int)din;
+            tk.k = (int)k;
+            tk.rms_eps = t.rms_eps;
+            tk.idx = tap_idx;
+            tk.vals = tap_vals;
+            if (tap_idx && tap_vals) LAROSA_TRY(launch_topk(tk, B, st));
+        }
+        const int bit = si == 0 ? 1 : (si == 1 ? 4 : (si == 2 ? 6 : 8));
         if (!on(bit)) return LAROSA_OK;
-        const GemvPlan p = plan_gemv(dout, nrows_max(din, k), bp);
+        const GemvPlan p = plan_gemv(dout, din, bp);
+        GemvArgs a = gemv_args_base();
         a.W = Wt;
         a.ld = dout;
         a.d_out = (int)dout;
-        a.n_splits = p.n_splits;
+        a.mode = GEMV_THRESH;
+        a.x = xmat;
+        a.ldx = din;
+        a.d_in = (int)din;
+        a.thr = W.site[si].thr;
+        a.batch = B;
         a.acc = acc;
         a.acc_ld = dout;
         return launch_gemv(a, p, bp, st);
     };
 
-    // ---- h1: Top-K of r (RMS scale) -> QKV --------------------------------------------------
+    // ---- h1: r (RMS scale) -> QKV -------------------------------------------------------------
     {
-        GemvArgs a = gemv_args_base();
-        TopkKernelArgs t = topk_args_base();
+        ThreshArgs t;
+        memset(&t, 0, sizeof(t));
+        t.mode = THR_PLAIN;
         t.x = s->resid;
+        t.ldx = L.d;
         t.rms_eps = w->rms_eps;
-        LAROSA_TRY(site(t, 0, L.d, plan->k_h1, a));
-        LAROSA_TRY(run_gemv(a, w->w_qkv, L.d, plan->k_h1, L.nqkv, W.acc_qkv, 1));
-        LAROSA_TRY(tap_copy(T.idx_h1, W.idx[0], sizeof(int32_t) * B * plan->k_h1, st));
-        LAROSA_TRY(tap_copy(T.vals_h1, W.vals[0], sizeof(float) * B * plan->k_h1, st));
+        LAROSA_TRY(site(0, t, L.d, plan->k_h1, s->resid, T.idx_h1, T.vals_h1, w->w_qkv, L.nqkv, W.acc_qkv));
     }
     // ---- attention (finalises q / new k, v from acc_qkv) -------------------------------------
     {
@@ -762,64 +808,67 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             LAROSA_TRY(cuda_check(launch(attention_kernel<2>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch"));
         LAROSA_TRY(tap_copy(T.h2, W.h2, sizeof(float) * B * L.nq, st));
     }
-    // ---- h2: Top-K of the attention output (zero acc_qkv) -> O --------------------------------
+    // ---- h2: attention output -> O -------------------------------------------------------------
     {
-        GemvArgs a = gemv_args_base();
-        TopkKernelArgs t = topk_args_base();
+        ThreshArgs t;
+        memset(&t, 0, sizeof(t));
+        t.mode = THR_PLAIN;
         t.x = W.h2;
+        t.ldx = L.nq;
         t.rms_eps = -1.0f;
-        LAROSA_TRY(site(t, 1, L.nq, plan->k_h2, a));
-        LAROSA_TRY(run_gemv(a, w->w_o, L.nq, plan->k_h2, L.d, W.acc_o, 4));
-        LAROSA_TRY(tap_copy(T.idx_h2, W.idx[1], sizeof(int32_t) * B * plan->k_h2, st));
-        LAROSA_TRY(tap_copy(T.vals_h2, W.vals[1], sizeof(float) * B * plan->k_h2, st));
+        LAROSA_TRY(site(1, t, L.nq, plan->k_h2, W.h2, T.idx_h2, T.vals_h2, w->w_o, L.d, W.acc_o));
     }
-    // ---- h3: r_mid = r + y_o; Top-K (RMS scale) -> gate|up ------------------------------------
+    // ---- h3: r_mid = r + y_o (RMS scale) -> gate|up --------------------------------------------
     {
-        GemvArgs a = gemv_args_base();
-        TopkKernelArgs t = topk_args_base();
-        t.mode = SRC_RESID_ACC;
+        ThreshArgs t;
+        memset(&t, 0, sizeof(t));
+        t.mode = THR_RESID_ACC;
         t.resid = s->resid;
         t.resid_ld = L.d;
         t.acc = W.acc_o;
         t.acc_ld = L.d;
-        t.xr_out = W.rmid;
+        t.xout = W.rmid;
         t.rms_eps = w->rms_eps;
-        LAROSA_TRY(site(t, 2, L.d, plan->k_h3, a));
-        LAROSA_TRY(run_gemv(a, w->w_gu, L.d, plan->k_h3, L.dgu, W.acc_gu, 6));
+        LAROSA_TRY(site(2, t, L.d, plan->k_h3, W.rmid, T.idx_h3, T.vals_h3, w->w_gu, L.dgu, W.acc_gu));
         LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
-        LAROSA_TRY(tap_copy(T.idx_h3, W.idx[2], sizeof(int32_t) * B * plan->k_h3, st));
-        LAROSA_TRY(tap_copy(T.vals_h3, W.vals[2], sizeof(float) * B * plan->k_h3, st));
     }
-    // ---- h4 = SiLU(g) * u; Top-K -> down ---------------------------------------------------------
+    // ---- h4 = SiLU(g) * u -> down --------------------------------------------------------------
     {
-        GemvArgs a = gemv_args_base();
-        TopkKernelArgs t = topk_args_base();
-        t.mode = SRC_SILU_GU;
+        ThreshArgs t;
+        memset(&t, 0, sizeof(t));
+        t.mode = THR_SILU_GU;
         t.acc = W.acc_gu;
         t.acc_ld = L.dgu;
-        t.xr_out = W.h4;
+        t.xout = W.h4;
         t.rms_eps = -1.0f;
-        LAROSA_TRY(site(t, 3, L.inter, plan->k_h4, a));
-        LAROSA_TRY(run_gemv(a, w->w_down, L.inter, plan->k_h4, L.d, W.acc_down, 8));
+        LAROSA_TRY(site(3, t, L.inter, plan->k_h4, W.h4, T.idx_h4, T.vals_h4, w->w_down, L.d, W.acc_down));
         LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
-        LAROSA_TRY(tap_copy(T.idx_h4, W.idx[3], sizeof(int32_t) * B * plan->k_h4, st));
-        LAROSA_TRY(tap_copy(T.vals_h4, W.vals[3], sizeof(float) * B * plan->k_h4, st));
     }
     // ---- residual adapter r <- (r_mid + y_down) . A_l (dense GEMV), finalize ------------
     FinalizeArgs f = finalize_args_base();
     f.n = (int)L.d;
     f.batch = B;
+    f.zero3 = W.acc_qkv;          // attention read it; zero it for the next step
+    f.zero3_ld = L.nqkv;
+    f.zero3_n = (int)L.nqkv;
     if (w->adapter) {
-        GemvArgs a = gemv_args_base();
-        a.rows = nullptr;
-        a.vals = W.rmid;
-        a.vs_r = 1;
-        a.vs_b = L.d;
-        a.vacc = W.acc_down;
-        a.vacc_ld = L.d;
-        a.nrows = (int)L.d;
-        a.batch = B;
-        LAROSA_TRY(run_gemv(a, w->adapter, L.d, L.d, L.d, W.acc_adp, 9));
+        if (on(9)) {
+            const GemvPlan p = plan_gemv(L.d, L.d, bp);
+            GemvArgs a = gemv_args_base();
+            a.W = w->adapter;
+            a.ld = L.d;
+            a.d_out = (int)L.d;
+            a.mode = GEMV_DENSE;
+            a.x = W.rmid;
+            a.ldx = L.d;
+            a.d_in = (int)L.d;
+            a.vacc = W.acc_down;
+            a.vacc_ld = L.d;
+            a.batch = B;
+            a.acc = W.acc_adp;
+            a.acc_ld = L.d;
+            LAROSA_TRY(launch_gemv(a, p, bp, st));
+        }
         f.acc1 = W.acc_adp;
         f.acc1_ld = L.d;
         f.out1 = s->resid;
@@ -830,9 +879,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         f.res2_ld = L.d;
         f.out2 = T.r_out;
         f.out2_ld = L.d;
-        f.zero3 = W.acc_qkv;          // attention read it; zero it for the next step
-        f.zero3_ld = L.nqkv;
-        f.zero3_n = (int)L.nqkv;
         if (on(10)) LAROSA_TRY(launch_finalize(f, st));
     } else {
         f.acc1 = W.acc_down;
@@ -841,9 +887,6 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         f.res1_ld = L.d;
         f.out1 = s->resid;
         f.out1_ld = L.d;
-        f.zero3 = W.acc_qkv;
-        f.zero3_ld = L.nqkv;
-        f.zero3_n = (int)L.nqkv;
         if (on(10)) LAROSA_TRY(launch_finalize(f, st));
         LAROSA_TRY(tap_copy(T.r_out, s->resid, sizeof(float) * B * L.d, st));
     }

@@ -1,35 +1,47 @@
-// topk.cuh — exact per-token Top-K (S_k of eq. 2) as a block-wide radix
-// select on the uint32 keys bits(|x|), with the lower-index tie-break, plus the
-// RMS scale of the h1/h3 sites and stable compaction to ascending indices.
+// topk.cuh — exact per-token Top-K (S_k of eq. 2) as a radix select on
+// the uint32 keys bits(|x|) with the lower-index tie-break, the RMS scale of the
+// h1/h3 sites, and stable compaction to ascending indices.
 //
-// One CTA (1024 threads) per token, latency-optimised (it sits between two dependent GEMVs):
-//  * thread t owns the contiguous elements [t*EPT, t*EPT + EPT) and keeps their keys in
-//    registers for the whole select (one coalesced float4 load per 4 elements; no shared
-//    memory copy of the vector);
-//  * digits: bits [30:19] (4096 bins), [18:7] (4096), [6:0] (128); a pass whose k-th-key
-//    bucket is taken whole ends the select (continuous data: 2 passes); double-buffered
-//    histograms so the next pass's zeroing overlaps the current one;
-//  * the bucket search is a warp-level suffix scan with one shared exchange of warp totals;
-//  * exact key ties straddling position k are resolved by index (lower index first);
-//  * compaction is one block-wide exclusive scan of per-thread counts (contiguous
-//    ownership keeps the output ascending).
+// Latency-optimised and distributed over a thread-block CLUSTER per token (it sits between
+// two dependent GEMVs on the critical path; one SM alone is issue- and bandwidth-limited):
+//  * CTA r of the cluster owns the contiguous chunk [r*C, r*C + C) of the vector (C a
+//    multiple of 32), element r*C + j*512 + t lives in register xv[j] of thread t
+//    (coalesced loads; each warp-round of 32 consecutive elements is one mask word);
+//  * fused source finalisation: the site's input is computed from the producer GEMV's
+//    fixed-point accumulators (residual add, or SiLU(g)*u), written to the layer's buffer
+//    and the accumulators are re-zeroed, by all CTAs of the cluster in parallel;
+//  * digits: bits [30:19] (4096 bins), [18:7] (4096), [6:0] (128); each CTA histograms its
+//    own candidates locally, CTA r merges bin slice r over the cluster through distributed
+//    shared memory, the CTA whose slice holds the k-th key finds its bucket (block suffix
+//    scan) and all CTAs read the result back through DSMEM; a pass whose bucket is taken
+//    whole ends the select (continuous data: 2 passes), an exact key tie at position k is
+//    resolved by index;  (remote atomics into one CTA's histogram were tried: Gaussian
+//    keys crowd a few bins and the DSMEM reductions serialise);
+//  * compaction: per-CTA counts and sum-of-squares partials are exchanged through DSMEM
+//    (fixed order, deterministic), then per-round warp ballots give coalesced stores.
 #pragma once
 #include "common.cuh"
 #include "gemv.cuh"   // fixed-point accumulator helpers, kGuBlock
 
 namespace larosa {
 
-constexpr int kTopkThreads = 1024;
+constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kTopkBins = 4096;
+constexpr int kTopkMaxCluster = 8;
 
 __host__ __device__ constexpr size_t topk_smem_bytes(int d) {
-    return sizeof(int) * 2 * kTopkBins + sizeof(int) * 256 + 0 * (size_t)d;
+    return sizeof(int) * 3 * kTopkBins + sizeof(int) * 128 + 0 * (size_t)d;
 }
 
-// elements per thread (rounded up to an instantiated size) for a vector of length d
+// cluster size for a vector of length d: ~1024 elements per CTA, at most 8 CTAs
+__host__ __device__ constexpr int topk_cluster_size(int d) {
+    return d <= 1024 ? 1 : ((d + 1023) / 1024 < kTopkMaxCluster ? (d + 1023) / 1024 : kTopkMaxCluster);
+}
+// per-CTA chunk (multiple of 32) and elements per thread (rounded to an instantiated size)
+__host__ __device__ constexpr int topk_chunk(int d, int cs) { return (((d + cs - 1) / cs) + 31) / 32 * 32; }
 __host__ __device__ constexpr int topk_ept(int d) {
-    return ((d + 4 * kTopkThreads - 1) / (4 * kTopkThreads)) * 4;
+    return ((topk_chunk(d, topk_cluster_size(d)) + kTopkThreads - 1) / kTopkThreads + 1) / 2 * 2;
 }
 
 // Where the site's input vector comes from (the producer GEMV leaves fixed-point
@@ -40,66 +52,128 @@ enum TopkSrc : int {
     SRC_SILU_GU = 2,    // SiLU(g_i) * u_i, g/u = fix^-1 of the interleaved gate|up acc
 };
 
-struct TopkSrcArgs {
-    const float* resid;          // SRC_RESID_ACC
-    unsigned long long* acc;     // SRC_RESID_ACC / SRC_SILU_GU: read, then re-zeroed
-    unsigned long long* zero;    // optional extra accumulator to re-zero (zero_n entries)
-    int zero_n;
+struct TopkKernelArgs {
+    const float* x;
+    int64_t ldx;
+    int d, k;
+    float rms_eps;
+    float* xr_out;      // [batch][d]: copy of x (plain) / the finalised vector (other modes)
+    int32_t* idx;       // [batch][k]
+    float* vals;        // [batch][k]
+    uint32_t* mask;     // [batch][ceil(d/32)] or null
+    float* scale;       // [batch] or null
+    int mode;           // TopkSrc
+    const float* resid; int64_t resid_ld;                 // SRC_RESID_ACC
+    unsigned long long* acc; int64_t acc_ld;              // SRC_RESID_ACC / SRC_SILU_GU
+    unsigned long long* zero; int64_t zero_ld; int zero_n; // optional extra zeroing per token
+    ThreshOut* rule_out;  // [batch] if set: emit the selection rule (no idx/vals lists)
 };
 
-struct TopkOut {
-    float* xr_out;     // [d] copy of the (rotated / finalised) input, or nullptr
-    int32_t* idx;      // [k]
-    float* vals;       // [k]
-    uint32_t* mask;    // [ceil(d/32)] or nullptr
-    float* scale_out;  // [1] the RMS scale s (1 when rms_eps < 0), or nullptr
-};
-
-// exclusive prefix over one int per thread in thread order; 1 __syncthreads.
-__device__ __forceinline__ int topk_excl_scan(int v, int* sw, int* total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int inc = warp_incl_scan(v);
-    if (lane == 31) sw[wid] = inc;
-    __syncthreads();
-    const int t = sw[lane];                       // kTopkWarps == 32
-    const int ti = warp_incl_scan(t);
-    *total = __shfl_sync(0xffffffffu, ti, 31);
-    return __shfl_sync(0xffffffffu, ti - t, wid) + inc - v;
+__device__ __forceinline__ void topk_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t topk_mapa(const void* local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void topk_red_remote(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// (no "memory" clobber: the loads of a batch may issue back to back; the cluster barriers
+// carry the ordering)
+__device__ __forceinline__ uint32_t topk_ld_remote(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 
-template <int EPT>
-__device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rms_eps, TopkOut out,
-                             unsigned char* smem_raw) {
-    constexpr int NT = kTopkThreads;
-    int* hist0 = reinterpret_cast<int*>(smem_raw);
+// grid = (CS, batch), cluster (CS, 1, 1): one cluster per token.  One kernel per (source
+// mode, elements per thread) so each launch only fetches its own (small) code.
+template <int MODE, int EPT>
+__global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* hist0 = reinterpret_cast<int*>(smem);                 // local histograms (double-buffered)
     int* hist1 = hist0 + kTopkBins;
     int* scr = hist1 + kTopkBins;
-    int* s_wtot = scr;                                   // [0, 32)   scan scratch (select)
-    int* s_cnt = scr + 32;                               // [32, 160) per-round warp counts, 2 x [2][32]
-    float* s_ssq = reinterpret_cast<float*>(scr + 160);  // [160, 192)
-    int* s_res = scr + 192;                              // [192, 196) bucket result
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int* s_wtot = scr;                                          // [0, 16)    scan scratch
+    int* s_cnt = scr + 16;                                      // [16, 80)   per-round warp counts 2 x [2][16]
+    int* s_red = scr + 80;                                      // [80, 96)   block-reduction scratch
+    int* s_pub = scr + 96;                                      // [96, 100)  published: n_gt, n_eq, ssq bits
+    int* s_res = scr + 100;                                     // [100, 104) bucket result (owner CTA)
+    int* mh = scr + 128;                                        // merged histogram slice (<= 4096)
+    pdl_wait();
+    pdl_trigger();
 
-    // 1. strided ownership: element j*NT + tid lives in xv[j] (raw fp32 bits) -- coalesced
-    //    loads, and each warp-round of 32 consecutive elements is one mask word.
-    //    (L2 loads: the vector may have been written by other CTAs of this kernel's cluster.)
+    const int d = a.d, k = a.k;
+    const int b = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int C = topk_chunk(d, cs);
+    const int lo = rank * C;
+    constexpr int NT = kTopkThreads;
+    const int nwords = (d + 31) / 32;
+    int32_t* out_idx = a.idx + (size_t)b * k;
+    float* out_vals = a.vals + (size_t)b * k;
+    uint32_t* out_mask = a.mask ? a.mask + (size_t)b * nwords : nullptr;
+
+    // ---- 1. this CTA's values (raw fp32 bits) in registers; finalise fused sources -------
     uint32_t xv[EPT];
     float ssq = 0.f;
+    const float* x = a.x ? a.x + (size_t)b * a.ldx : nullptr;
+    float* xout = a.xr_out ? a.xr_out + (size_t)b * d : nullptr;
+    const float* resid = a.resid ? a.resid + (size_t)b * a.resid_ld : nullptr;
+    unsigned long long* acc = a.acc ? a.acc + (size_t)b * a.acc_ld : nullptr;
 #pragma unroll
     for (int j = 0; j < EPT; ++j) {
-        const int i = j * NT + tid;
-        const float v = i < d ? __ldcg(x + i) : 0.f;
+        const int i = lo + j * NT + tid;
+        float v = 0.f;
+        if (j * NT + tid < C && i < d) {
+            if constexpr (MODE == SRC_PLAIN) {
+                v = x[i];
+            } else if constexpr (MODE == SRC_RESID_ACC) {
+                v = (resid ? resid[i] : 0.f) + fix_to_f(acc[i]);
+                acc[i] = 0ull;
+            } else {
+                const int gi = (i / kGuBlock) * (2 * kGuBlock) + (i % kGuBlock);
+                const float g = fix_to_f(acc[gi]);
+                const float u = fix_to_f(acc[gi + kGuBlock]);
+                acc[gi] = 0ull;
+                acc[gi + kGuBlock] = 0ull;
+                v = g / (1.0f + expf(-g)) * u;
+            }
+            if (xout) xout[i] = v;
+        }
         xv[j] = __float_as_uint(v);
         ssq = fmaf(v, v, ssq);
-        if (out.xr_out && i < d) out.xr_out[i] = v;
+    }
+    if (a.zero) {
+        unsigned long long* z = a.zero + (size_t)b * a.zero_ld;
+        const int zc = (a.zero_n + cs - 1) / cs;
+        for (int i = rank * zc + tid; i < min(a.zero_n, rank * zc + zc); i += NT) z[i] = 0ull;
     }
 #define KEY(j) (xv[j] & 0x7fffffffu)
+#define VALID(j) ((j) * NT + tid < C && lo + (j) * NT + tid < d)
+    // per-CTA sum of squares (fixed order) -> published for the cluster
     ssq = warp_sum(ssq);
-    if (lane == 0) s_ssq[wid] = ssq;
-    for (int b = tid; b < kTopkBins; b += NT) hist0[b] = 0;
+    if (lane == 0) reinterpret_cast<float*>(s_red)[wid] = ssq;
+    for (int i = tid; i < kTopkBins; i += NT) hist0[i] = 0;
     __syncthreads();
+    if (tid == 0) {
+        float t = 0.f;
+        for (int w = 0; w < kTopkWarps; ++w) t += reinterpret_cast<float*>(s_red)[w];
+        s_pub[2] = __float_as_int(t);
+    }
+    topk_cluster_sync();   // CTA 0's histograms are zero before anyone adds into them
 
-    // 2. radix select of the k-th largest key
+    // ---- 2. radix select of the k-th largest key ----------------------------------------
+    // per pass: local histograms (smem atomics) -> cluster barrier -> CTA r merges bin slice
+    // r over all CTAs through DSMEM and publishes the slice total -> barrier -> the CTA whose
+    // slice holds the k-th key scans it and publishes (b*, rem', count) -> barrier -> read.
     uint32_t prefix = 0u, pmask = 0u;
     int rem = k;
     bool exact_ge = false;   // select key >= thr (the k-th key's bucket is taken whole)
@@ -117,40 +191,78 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
             const uint32_t dmask = (uint32_t)(nb - 1);
 #pragma unroll
             for (int j = 0; j < EPT; ++j)
-                if (j * NT + tid < d && (KEY(j) & pmask) == prefix) atomicAdd(&hist[(KEY(j) >> sh) & dmask], 1);
-            if (pass < 2)
-                for (int b = tid; b < kTopkBins; b += NT) hnext[b] = 0;
+                if (VALID(j) && (KEY(j) & pmask) == prefix) atomicAdd(&hist[(KEY(j) >> sh) & dmask], 1);
+            topk_cluster_sync();                                  // (A) all local histograms complete
+            // merge my bin slice [s_lo, s_hi) over the cluster (fixed order) into mh
+            const int spc = (nb + cs - 1) / cs;
+            const int s_lo = min(nb, rank * spc), s_hi = min(nb, s_lo + spc);
+            int tot = 0;
+            for (int bb = s_lo + tid; bb < s_hi; bb += NT) {
+                uint32_t hv[kTopkMaxCluster];          // issue all remote loads, then sum
+#pragma unroll
+                for (int q = 0; q < kTopkMaxCluster; ++q)
+                    hv[q] = q < cs ? topk_ld_remote(topk_mapa(hist + bb, (uint32_t)q)) : 0u;
+                int m = 0;
+#pragma unroll
+                for (int q = 0; q < kTopkMaxCluster; ++q) m += (int)hv[q];
+                mh[bb - s_lo] = m;
+                tot += m;
+            }
+            tot = warp_sum_i(tot);
+            if (lane == 0) s_red[wid] = tot;
+            for (int i = tid; i < kTopkBins; i += NT) hnext[i] = 0;   // next pass's local histogram
             __syncthreads();
-            // suffix scan: warp w owns the bins [nb - (w+1)*bpw, nb - w*bpw), top bins first
-            const int bpw = nb / kTopkWarps;              // 128 or 4
-            const int bpl = bpw >= 32 ? bpw / 32 : 1;     // 4 or 1
-            const int lhi = nb - wid * bpw - lane * bpl;  // lane's bins [lhi - bpl, lhi)
-            int c = 0;
-            if (lane * bpl < bpw)
-                for (int b = lhi - 1; b >= lhi - bpl; --b) c += hist[b];
-            const int inc = warp_incl_scan(c);
-            if (lane == 31) s_wtot[wid] = inc;
-            __syncthreads();
-            const int t = s_wtot[lane];
-            const int ti = warp_incl_scan(t);
-            const int before = __shfl_sync(0xffffffffu, ti - t, wid) + inc - c;
-            if (c > 0 && before < rem && rem <= before + c) {
-                int acc = before;
-                for (int b = lhi - 1; b >= lhi - bpl; --b) {
-                    const int h = hist[b];
-                    if (acc + h >= rem) {
-                        s_res[0] = b;
-                        s_res[1] = rem - acc;
-                        s_res[2] = h;
-                        break;
+            if (tid == 0) {
+                int t = 0;
+                for (int w = 0; w < kTopkWarps; ++w) t += s_red[w];
+                s_pub[3] = t;
+            }
+            topk_cluster_sync();                                  // (B) slice totals published
+            // which slice holds the rem-th key (slices cs-1 .. 0 cover bins top-down)?
+            uint32_t tq[kTopkMaxCluster];
+#pragma unroll
+            for (int q = 0; q < kTopkMaxCluster; ++q) tq[q] = q < cs ? topk_ld_remote(topk_mapa(s_pub + 3, (uint32_t)q)) : 0u;
+            int above = 0, owner = -1, rem_in = 0;
+#pragma unroll
+            for (int q = kTopkMaxCluster - 1; q >= 0; --q) {
+                if (q < cs && owner < 0 && above + (int)tq[q] >= rem) {
+                    owner = q;
+                    rem_in = rem - above;
+                }
+                above += (int)tq[q];
+            }
+            if (rank == owner) {
+                // block suffix scan over my merged slice (top bins first), 512 threads
+                const int nsl = s_hi - s_lo;
+                const int bpt = (nsl + NT - 1) / NT;
+                const int thi = nsl - tid * bpt;                 // thread's bins [thi - bpt, thi) (slice-local)
+                int c = 0;
+                for (int bb = thi - 1; bb >= max(0, thi - bpt); --bb) c += mh[bb];
+                const int inc = warp_incl_scan(c);
+                if (lane == 31) s_wtot[wid] = inc;
+                __syncthreads();
+                const int t = lane < kTopkWarps ? s_wtot[lane] : 0;
+                const int ti = warp_incl_scan(t);
+                const int before = __shfl_sync(0xffffffffu, ti - t, wid) + inc - c;
+                if (c > 0 && before < rem_in && rem_in <= before + c) {
+                    int accu = before;
+                    for (int bb = thi - 1; bb >= max(0, thi - bpt); --bb) {
+                        const int h = mh[bb];
+                        if (accu + h >= rem_in) {
+                            s_res[0] = s_lo + bb;
+                            s_res[1] = rem_in - accu;
+                            s_res[2] = h;
+                            break;
+                        }
+                        accu += h;
                     }
-                    acc += h;
                 }
             }
-            __syncthreads();
-            const int bstar = s_res[0];
-            rem = s_res[1];
-            const int cnt = s_res[2];
+            topk_cluster_sync();                                  // (C) result published by the owner
+            const uint32_t res_remote = topk_mapa(s_res, (uint32_t)owner);
+            const int bstar = (int)topk_ld_remote(res_remote);
+            rem = (int)topk_ld_remote(res_remote + 4);
+            const int cnt = (int)topk_ld_remote(res_remote + 8);
             prefix |= (uint32_t)bstar << sh;
             pmask |= dmask << sh;
             if (cnt == rem) {
@@ -161,20 +273,96 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
         }
     }
     const uint32_t thr = prefix;
-    float tot_ssq = 0.f;
-#pragma unroll
-    for (int w = 0; w < kTopkWarps; ++w) tot_ssq += s_ssq[w];   // fixed order: deterministic
-    const float scale = rms_eps >= 0.f ? 1.0f / sqrtf(tot_ssq / (float)d + rms_eps) : 1.0f;
 
-    // 3. stable compaction, one round of NT consecutive elements at a time: warp ballots give
-    //    in-warp ranks, warp counts exchanged through shared memory (double-buffered, one
-    //    __syncthreads per round) give the block offsets; the stores are consecutive.
-    const uint32_t lt = (1u << lane) - 1u;
-    int base = 0, eq_base = 0;
+    // ---- rule mode: publish (Tk, Ti, s) instead of the index list ------------------------
+    // keep i iff key > Tk or (key == Tk and i <= Ti)  (the consumer GEMV selects its rows)
+    if (a.rule_out && (exact_ge || !tie_mode)) {
+        if (rank == 0 && tid == 0) {
+            float tot = 0.f;
+            uint32_t psq[kTopkMaxCluster];
+#pragma unroll
+            for (int q = 0; q < kTopkMaxCluster; ++q)
+                psq[q] = q < cs ? topk_ld_remote(topk_mapa(s_pub + 2, (uint32_t)q)) : 0u;
+#pragma unroll
+            for (int q = 0; q < kTopkMaxCluster; ++q)
+                if (q < cs) tot += __uint_as_float(psq[q]);
+            ThreshOut r;
+            r.tk = thr;
+            r.ti = 0x7fffffff;   // key == Tk (the bucket's lower edge) is kept too
+            r.scale = a.rms_eps >= 0.f ? 1.0f / sqrtf(tot / (float)d + a.rms_eps) : 1.0f;
+            r.pad = 0;
+            a.rule_out[b] = r;
+        }
+        topk_cluster_sync();   // rank 0 read the others' published partials
+        return;
+    }
+
+    // ---- 3. compaction: cluster-wide prefix of counts, then per-round ballots ------------
+    int my_gt = 0, my_eq = 0;
 #pragma unroll
     for (int j = 0; j < EPT; ++j) {
-        const int i = j * NT + tid;
-        const bool valid = i < d;
+        if (!VALID(j)) continue;
+        if (exact_ge) {
+            my_gt += KEY(j) >= thr;
+        } else {
+            my_gt += KEY(j) > thr;
+            my_eq += KEY(j) == thr;
+        }
+    }
+    {
+        int g2 = my_gt, e2 = my_eq;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            g2 += __shfl_xor_sync(0xffffffffu, g2, o);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        }
+        __syncthreads();   // s_red reuse
+        if (lane == 0) {
+            s_red[wid] = g2;
+            s_cnt[wid] = e2;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int tg = 0, te = 0;
+            for (int w = 0; w < kTopkWarps; ++w) {
+                tg += s_red[w];
+                te += s_cnt[w];
+            }
+            s_pub[0] = tg;
+            s_pub[1] = te;
+        }
+    }
+    topk_cluster_sync();
+    // counts of lower-rank CTAs (index order) and the total sum of squares (fixed order)
+    int gt_before = 0, eq_before = 0;
+    float tot_ssq = 0.f;
+    uint32_t pg[kTopkMaxCluster], pe[kTopkMaxCluster], ps[kTopkMaxCluster];
+#pragma unroll
+    for (int q = 0; q < kTopkMaxCluster; ++q) {
+        const uint32_t pub = topk_mapa(s_pub, (uint32_t)(q < cs ? q : 0));
+        pg[q] = q < cs ? topk_ld_remote(pub) : 0u;
+        pe[q] = q < cs ? topk_ld_remote(pub + 4) : 0u;
+        ps[q] = q < cs ? topk_ld_remote(pub + 8) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kTopkMaxCluster; ++q) {
+        if (q < rank) {
+            gt_before += (int)pg[q];
+            eq_before += (int)pe[q];
+        }
+        if (q < cs) tot_ssq += __uint_as_float(ps[q]);
+    }
+    const float scale = a.rms_eps >= 0.f ? 1.0f / sqrtf(tot_ssq / (float)d + a.rms_eps) : 1.0f;
+    // selected before this CTA = gt before + (eq taken in index order: the first rem overall)
+    const int take_eq_before = tie_mode ? min(eq_before, rem) : 0;
+    int base = gt_before + take_eq_before, eq_base = eq_before;
+    const uint32_t lt = (1u << lane) - 1u;
+    __syncthreads();   // s_cnt reuse
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+        const int off = j * NT + tid;
+        const int i = lo + off;
+        const bool valid = VALID(j);
         const uint32_t key = KEY(j);
         bool gt, eq;
         if (exact_ge) {
@@ -186,121 +374,44 @@ __device__ void block_topk_t(const float* __restrict__ x, int d, int k, float rm
         }
         const uint32_t bgt = __ballot_sync(0xffffffffu, gt);
         const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-        int* cnt = s_cnt + (j & 1) * 64;
+        int* cnt = s_cnt + (j & 1) * 32;
         if (lane == 0) {
             cnt[wid] = __popc(bgt);
-            cnt[32 + wid] = __popc(beq);
+            cnt[16 + wid] = __popc(beq);
         }
         __syncthreads();
-        const int cg = cnt[lane], ce = cnt[32 + lane];
+        const int cg = lane < kTopkWarps ? cnt[lane] : 0, ce = lane < kTopkWarps ? cnt[16 + lane] : 0;
         const int ig = warp_incl_scan(cg), ie = warp_incl_scan(ce);
-        const int wg = __shfl_sync(0xffffffffu, ig - cg, wid);        // gt before my warp
-        const int we = __shfl_sync(0xffffffffu, ie - ce, wid);        // eq before my warp
+        const int wg = __shfl_sync(0xffffffffu, ig - cg, wid);
+        const int we = __shfl_sync(0xffffffffu, ie - ce, wid);
         const int tg = __shfl_sync(0xffffffffu, ig, 31), te = __shfl_sync(0xffffffffu, ie, 31);
-        // eq element selected iff its index-ordered rank among eq elements is < rem
         const int erank = eq_base + we + __popc(beq & lt);
         const bool sel = gt || (eq && tie_mode && erank < rem);
         const uint32_t bsel = __ballot_sync(0xffffffffu, sel);
-        // selected before me = gt before + min(eq before, rem) (eq are taken in index order)
-        const int eq_before_warp = eq_base + we;
-        const int sel_before_warp = base + wg + (tie_mode ? max(0, min(eq_before_warp, rem) - min(eq_base, rem)) : 0);
-        const int pos = sel_before_warp + __popc(bsel & lt);
-        if (sel) {
-            out.idx[pos] = i;
-            out.vals[pos] = __uint_as_float(xv[j]) * scale;
+        const int eq_sel_before_warp = tie_mode ? max(0, min(eq_base + we, rem) - min(eq_base, rem)) : 0;
+        const int pos = base + wg + eq_sel_before_warp + __popc(bsel & lt);
+        if (a.rule_out) {
+            if (eq && tie_mode && erank == rem - 1) {   // the k-th element: Ti = its index
+                ThreshOut r;
+                r.tk = thr;
+                r.ti = i;
+                r.scale = scale;
+                r.pad = 0;
+                a.rule_out[b] = r;
+            }
+        } else if (sel) {
+            out_idx[pos] = i;
+            out_vals[pos] = __uint_as_float(xv[j]) * scale;
         }
-        if (out.mask && lane == 0 && j * NT + wid * 32 < d) out.mask[(j * NT + wid * 32) >> 5] = bsel;
+        if (out_mask && lane == 0 && j * NT + wid * 32 < C && lo + j * NT + wid * 32 < d)
+            out_mask[(lo + j * NT + wid * 32) >> 5] = bsel;
         base += tg + (tie_mode ? max(0, min(eq_base + te, rem) - min(eq_base, rem)) : 0);
         eq_base += te;
     }
-    if (out.scale_out && tid == 0) *out.scale_out = scale;
+    if (a.scale && rank == 0 && tid == 0) a.scale[b] = scale;
 #undef KEY
-}
-
-struct TopkKernelArgs {
-    const float* x;
-    int64_t ldx;
-    int d, k;
-    float rms_eps;
-    float* xr_out;      // [batch][d]: copy of x (plain) / the finalised vector (other modes)
-    int32_t* idx;       // [batch][k]
-    float* vals;        // [batch][k]
-    uint32_t* mask;     // [batch][ceil(d/32)] or null
-    float* scale;       // [batch] or null
-    int mode;           // TopkSrc
-    const float* resid; int64_t resid_ld;                 // SRC_RESID_ACC
-    unsigned long long* acc; int64_t acc_ld;              // SRC_RESID_ACC / SRC_SILU_GU
-    unsigned long long* zero; int64_t zero_ld; int zero_n; // optional extra zeroing per token
-};
-
-// Source finalisation, spread over the CTAs of the token's cluster (coalesced): element i
-// of the site's input is computed from the producer GEMV's fixed-point accumulators, written
-// to xbuf (the materialised vector the layer keeps: r_mid, h4, x~) and the accumulators are
-// re-zeroed.  Then a cluster barrier and CTA 0 runs the select on the whole vector.
-template <int MODE>
-__device__ void topk_finalize_share(int d, int rank, int cs, TopkSrcArgs src, float* xbuf) {
-    const int chunk = (d + cs - 1) / cs;
-    const int lo = rank * chunk, hi = min(d, lo + chunk);
-#pragma unroll 1
-    for (int i = lo + (int)threadIdx.x; i < hi; i += kTopkThreads) {
-        float v;
-        if constexpr (MODE == SRC_RESID_ACC) {
-            v = (src.resid ? src.resid[i] : 0.f) + fix_to_f(src.acc[i]);
-            src.acc[i] = 0ull;
-        } else {
-            const int gi = (i / kGuBlock) * (2 * kGuBlock) + (i % kGuBlock);
-            const float g = fix_to_f(src.acc[gi]);
-            const float u = fix_to_f(src.acc[gi + kGuBlock]);
-            src.acc[gi] = 0ull;
-            src.acc[gi + kGuBlock] = 0ull;
-            v = g / (1.0f + expf(-g)) * u;
-        }
-        xbuf[i] = v;
-    }
-    if (src.zero) {
-        const int zc = (src.zero_n + cs - 1) / cs;
-        const int zlo = rank * zc, zhi = min(src.zero_n, zlo + zc);
-        for (int i = zlo + (int)threadIdx.x; i < zhi; i += kTopkThreads) src.zero[i] = 0ull;
-    }
-}
-
-__device__ __forceinline__ void topk_cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// grid = (CS, batch), cluster (CS, 1, 1): one cluster per token.  One kernel per (source
-// mode, elements per thread) so each launch only fetches its own (small) code: these
-// latency-bound kernels stalled on instruction-cache misses when one body held every variant.
-template <int MODE, int EPT>
-__global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    pdl_wait();
-    pdl_trigger();
-    const int b = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
-    const int nwords = (a.d + 31) / 32;
-    TopkOut o;
-    o.xr_out = nullptr;
-    o.idx = a.idx + (size_t)b * a.k;
-    o.vals = a.vals + (size_t)b * a.k;
-    o.mask = a.mask ? a.mask + (size_t)b * nwords : nullptr;
-    o.scale_out = a.scale ? a.scale + b : nullptr;
-    const float* x;
-    if constexpr (MODE == SRC_PLAIN) {
-        x = a.x + (size_t)b * a.ldx;
-        o.xr_out = a.xr_out ? a.xr_out + (size_t)b * a.d : nullptr;
-    } else {
-        TopkSrcArgs src;
-        src.resid = a.resid ? a.resid + (size_t)b * a.resid_ld : nullptr;
-        src.acc = a.acc + (size_t)b * a.acc_ld;
-        src.zero = a.zero ? a.zero + (size_t)b * a.zero_ld : nullptr;
-        src.zero_n = a.zero_n;
-        float* xbuf = a.xr_out + (size_t)b * a.d;
-        topk_finalize_share<MODE>(a.d, rank, cs, src, xbuf);
-        topk_cluster_sync();
-        x = xbuf;
-    }
-    if (rank != 0) return;
-    block_topk_t<EPT>(x, a.d, a.k, a.rms_eps, o, smem);
+#undef VALID
+    topk_cluster_sync();   // peers may still read this CTA's published counts
 }
 
 }  // namespace larosa

@@ -31,6 +31,14 @@ __global__ void k_load(const float* x, float* y, int n) {
     if (a == 12345.f) y[0] = a;
 }
 
+__global__ void k_csync(int* p, int n) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int i = 0; i < n; ++i)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x == 0 && blockIdx.x == 0 && p) p[0] += 1;
+}
+
 template <typename F>
 float time_chain(F launch, int n, bool graph) {
     cudaStream_t st;
@@ -81,6 +89,23 @@ void launch_ex(void (*k)(KA...), dim3 g, dim3 b, cudaStream_t st, bool pdl, A...
     cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k, args...);
 }
+template <typename... KA, typename... A>
+void launch_cl(void (*k)(KA...), int cs, dim3 b, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = b;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cs;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 int main() {
     int* p;
@@ -90,6 +115,14 @@ int main() {
     cudaMalloc(&y, 4096);
     cudaMemset(x, 0, 1 << 20);
     const int N = 200;
+    for (int cs : {1, 2, 4, 8}) {
+        for (int nt : {128, 512, 1024}) {
+            for (int ns : {0, 10, 40}) {
+                float us = time_chain([&](cudaStream_t st) { launch_cl(k_csync, cs, dim3(nt), st, p, ns); }, N, true);
+                printf("cluster %d x %4d thr, %2d cluster syncs: %6.2f us\n", cs, nt, ns, us);
+            }
+        }
+    }
     for (int pdl = 0; pdl < 2; ++pdl) {
         for (int graph = 0; graph < 2; ++graph) {
             printf("pdl=%d graph=%d\n", pdl, graph);
