@@ -145,6 +145,23 @@ larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int64_t d_out,
                                  const uint16_t* bias, float* y, void* ws, size_t ws_bytes,
                                  larosa_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * Fused Top-K + sparse GEMV, batch 1 (P:414 (2): sparsification fused into the GEMV;
+ * SPEC fused_topk_gemv S:397-405):
+ *   S = Top-K of |x| (k largest, ties -> lower index), s as in rotate_topk,
+ *   y[o] = (bias ? bias[o] : 0) + sum_{j in S} x[j] * s * W[j][o].
+ * No index list is materialised: a preparation kernel builds the 4096-bin histogram of
+ * the keys' top 12 bits (and the RMS partials), then every CTA of the GEMV derives the
+ * exact selection rule itself and streams an exactly balanced share of the kept rows.
+ * x fp32 [d_in] (d_in % 4 == 0, 16-byte aligned); W bf16 [d_in][ld]; y fp32 [d_out].
+ * Same W / ld / d_out / alignment requirements as larosa_sparse_gemv.
+ * ------------------------------------------------------------------------------ */
+size_t larosa_topk_sparse_gemv_workspace_size(int64_t d_in, int64_t d_out);
+larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                      const uint16_t* W, int64_t d_out, int64_t ld,
+                                      const uint16_t* bias, float* y, void* ws, size_t ws_bytes,
+                                      larosa_stream_t stream);
+
 /* Introspection (host): the launch plan larosa_sparse_gemv uses for this shape.
  * info (host, 8 ints) = {columns per CTA, column slices, kept-row splits, warps per CTA,
  * cp.async ring stages per warp, rows per stage, dynamic smem bytes, CTAs}. */
@@ -196,6 +213,11 @@ typedef struct {
     const int32_t* pos;
     int64_t max_ctx;
     int32_t batch;
+    /* Batch 1 only: nonzero iff `resid` is exactly what the previous larosa_sparse_layer
+     * call on this same workspace wrote (the next layer of a decode step), untouched since.
+     * That call's last epilogue already produced the h1 key histogram and RMS partials of
+     * resid, so the preparation kernel is skipped.  0 is always correct. */
+    int32_t chained;
 } larosa_layer_state;
 
 typedef struct {
@@ -213,15 +235,19 @@ typedef struct {
 size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx);
 
 /* Profiling aid (not for production): bitmask of the kernels larosa_sparse_layer launches
- * (default -1 = all; results are meaningless otherwise).  Bits: 0 Top-K h1, 1 QKV GEMV,
- * 2 attention, 3 Top-K h2, 4 O GEMV, 5 Top-K h3, 6 gate|up GEMV, 7 Top-K h4, 8 down GEMV,
- * 9 adapter GEMV, 10 finalize.  Process-wide, not thread-safe.  Also settable through the
- * LAROSA_LAYER_PHASES environment variable. */
+ * (default -1 = all; results are meaningless otherwise).  Bits: 0 h1 preparation (batch 1)
+ * or Top-K h1 (batch > 1), 1 QKV GEMV, 2 attention, 3 Top-K h2 (batch > 1), 4 O GEMV,
+ * 5 Top-K h3 (batch > 1), 6 gate|up GEMV, 7 Top-K h4 (batch > 1), 8 down GEMV, 9 adapter
+ * GEMV.  Process-wide, not thread-safe.  Also settable through the LAROSA_LAYER_PHASES
+ * environment variable. */
 #define LAROSA_PHASES_GEMV_ONLY 0x352
 void larosa_debug_set_layer_phases(int mask);
-/* Profiling aid: device buffer of 4 x 16 uint64 receiving %globaltimer stamps of the
- * threshold kernels' last CTA (NULL disables). */
-void larosa_debug_set_thresh_stamps(void* dev_buf);
+/* Profiling aid: device buffer of n_slots x 1024 x 8 uint64 %globaltimer stamps (ns), one
+ * block per kernel of a batch-1 larosa_sparse_layer call (0 QKV, 1 attention, 2 O, 3 gate|up,
+ * 4 down, 5 adapter), one row per CTA (linear id < 1024): [0] entry, [1] after the dependency
+ * wait, [2] after the prologue, [3] after the main loop, [4] exit.  NULL disables.
+ * Process-wide, not thread-safe. */
+void larosa_debug_set_timeline(void* dev_buf, int n_slots);
 larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                   const larosa_layer_state* state, const larosa_layer_taps* taps,
                                   void* ws, size_t ws_bytes, larosa_stream_t stream);

@@ -21,7 +21,7 @@ constexpr int kAttnPosPerWarp = 16;          // CH <= 4 * 16
 constexpr int kAttnMaxG = 8;
 
 struct AttnArgs {
-    const unsigned long long* acc;   // [batch][acc_ld] QKV GEMV fixed-point accumulators
+    unsigned long long* acc;         // [batch][acc_ld] QKV GEMV fixed-point accumulators (re-zeroed)
     int64_t acc_ld;
     const uint16_t* bias;  // [(hq + 2 hkv) hd] bf16 or null
     float theta;           // RoPE base
@@ -35,6 +35,10 @@ struct AttnArgs {
     float* part;           // [batch*hkv][n_chunks][G][hd + 2]
     unsigned* counters;    // [batch*hkv]
     float* out;            // [batch][hq*hd]
+    SiteSel out_sel;       // batch 1: selection data of h2 for the next GEMV (hist null = none)
+    uint32_t* zero_hist;   // optional histogram to re-zero (its consumer has completed)
+    int zero_words;
+    unsigned long long* tl;   // debug timeline slot or null
 };
 
 __host__ __device__ inline size_t attn_smem_bytes(int G, int hd, int chunk) {
@@ -248,16 +252,32 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             }
             M = Mn;
         }
-        a.out[(size_t)b * a.hq * hd + (size_t)(g * G + j) * hd + dd] = Ov / L;
+        const float hv = Ov / L;
+        a.out[(size_t)b * a.hq * hd + (size_t)(g * G + j) * hd + dd] = hv;
+        if (a.out_sel.hist) hist_push(a.out_sel, hv, (g * G + j) * hd + dd);
+    }
+    // every chunk CTA of this kv group has read its q / new k, v accumulators: re-zero them
+    unsigned long long* accz = a.acc + (size_t)b * a.acc_ld;
+    for (int i = tid; i < G * hd; i += kAttnThreads) accz[(size_t)g * G * hd + i] = 0ull;
+    for (int i = tid; i < hd; i += kAttnThreads) {
+        accz[nq + (size_t)g * hd + i] = 0ull;
+        accz[nq + nk + (size_t)g * hd + i] = 0ull;
     }
 }
 
 template <int DPL>
 __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const AttnArgs a) {
     extern __shared__ __align__(16) float asmem[];
+    tl_stamp(a.tl, 0);
     pdl_wait();
     pdl_trigger();
+    tl_stamp(a.tl, 1);
+    if (a.zero_hist) {
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kAttnThreads + threadIdx.x; i < a.zero_words; i += nct * kAttnThreads) a.zero_hist[i] = 0u;
+    }
     attention_body<DPL>(a, asmem);
+    tl_stamp(a.tl, 4);
 }
 
 }  // namespace larosa

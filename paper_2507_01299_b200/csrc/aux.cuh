@@ -111,51 +111,6 @@ __global__ void __launch_bounds__(kUnionThreads) union_kernel(const uint32_t* __
 }
 
 // ------------------------------------------------------------------------------------------
-// Finalise fixed-point GEMV accumulators (gemv.cuh) and restore their zero state:
-//   out1[b][i] = [res1[b][i] +] fix^-1(acc1[b][i]) [+ bias1[i]];  acc1 = 0
-//   out2[b][i] = [res2[b][i] +] fix^-1(acc2[b][i])  (out2 may be null);  acc2 = 0 (if given)
-// ------------------------------------------------------------------------------------------
-struct FinalizeArgs {
-    int n, batch;
-    unsigned long long* acc1; int64_t acc1_ld;
-    const float* res1; int64_t res1_ld;
-    const uint16_t* bias1;
-    float* out1; int64_t out1_ld;
-    unsigned long long* acc2; int64_t acc2_ld;
-    const float* res2; int64_t res2_ld;
-    float* out2; int64_t out2_ld;
-    unsigned long long* zero3; int64_t zero3_ld; int zero3_n;   // extra accumulator to re-zero
-};
-
-__global__ void finalize_kernel(const FinalizeArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    const int nz = a.batch * a.zero3_n;
-#pragma unroll 1
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nz; t += gridDim.x * blockDim.x)
-        a.zero3[(size_t)(t / a.zero3_n) * a.zero3_ld + t % a.zero3_n] = 0ull;
-    const int total = a.batch * a.n;
-#pragma unroll 1
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int b = t / a.n, i = t % a.n;
-        if (a.acc1) {
-            unsigned long long* p = a.acc1 + (size_t)b * a.acc1_ld + i;
-            float y = fix_to_f(*p);
-            *p = 0ull;
-            if (a.res1) y = a.res1[(size_t)b * a.res1_ld + i] + y;
-            if (a.bias1) y += bf16f(a.bias1[i]);
-            a.out1[(size_t)b * a.out1_ld + i] = y;
-        }
-        if (a.acc2) {
-            unsigned long long* p = a.acc2 + (size_t)b * a.acc2_ld + i;
-            float y = fix_to_f(*p);
-            *p = 0ull;
-            if (a.out2) a.out2[(size_t)b * a.out2_ld + i] = (a.res2 ? a.res2[(size_t)b * a.res2_ld + i] : 0.f) + y;
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
 // Wgu[r][t*2B + j] = j < B ? Wg[r][t*B + j] : Wu[r][t*B + j - B]   (B = kGuBlock)
 // ------------------------------------------------------------------------------------------
 __global__ void pack_gate_up_kernel(const uint16_t* __restrict__ wg, const uint16_t* __restrict__ wu,

@@ -1,20 +1,17 @@
 // gemv.cuh — sparse GEMV over the kept rows of a column-major weight (eq. after_merge,
 // PAPER.md:407-410; kernel recipe P:414: column-major storage, selective loads of the kept
-// columns).
+// columns), with the site's Top-K selection fused into its prologue and the next site's
+// inputs produced by its epilogue.
 //
 //   acc[b][o] += fix( sum_{r in rows} val(r, b) * W[row(r)][o] )        (o in [0, d_out))
 //
-// The kernel only streams and accumulates; it has no tail.  Partial sums are added into
-// 64-bit fixed-point accumulators (32 fractional bits) with red.global.add.u64: integer
-// addition is associative, so the result is bit-identical whatever order the CTAs finish
-// in (deterministic without a fixed reduction tree), and no CTA waits for another.  The
-// consumer of y (the next kernel: Top-K, attention, finalize) converts acc -> fp32, applies
-// the epilogue (bias / residual / RoPE / SiLU*up) and re-zeroes the accumulators.
+// Streaming.  Partial sums are added into 64-bit fixed-point accumulators (32 fractional
+// bits) with red.global.add.u64: integer addition is associative, so the result is
+// bit-identical whatever order the CTAs finish in and no CTA waits for another.
 // Fixed-point error: <= 2^-33 absolute per partial (|y| must stay < 2^31).
-//
 // Decomposition (B200: 148 SMs): grid = (column slices of 256, n_splits) with 8 warps per
-// CTA, ~2 CTAs per SM.  CTA (slice, s) owns the s-th contiguous chunk of the kept-row list;
-// warp w takes every 8th row of it.  Each kept row's 512-byte segment (contiguous in the
+// CTA, ~2 CTAs per SM.  CTA (slice, s) owns the s-th share of the kept-row list; warp w
+// takes every 8th row of it.  Each kept row's 512-byte segment (contiguous in the
 // [d_in][d_out] layout) is one coalesced warp-wide cp.async (LDGSTS, 16 B per lane) into the
 // warp's private 4-stage ring; a lane later reads back exactly the 16 bytes it copied, so
 // the pipeline needs no barrier, only the lane's own cp.async groups.  (Measured on B200:
@@ -23,27 +20,63 @@
 // needs; per-thread cp.async has no such cap.)  Math: bf16 pairs widen with one ALU op per
 // value and accumulate with paired fp32 FMAs (FFMA2).  The 8 warps' partials are summed in
 // shared memory in fixed order before the single red per column.
+//
+// Row sources (GemvMode):
+//   LIST    kept rows given as (rows[], vals) — the standalone larosa_sparse_gemv;
+//   THRESH  per-token selection rules (Tk, Ti, s) from the Top-K kernel (batch > 1);
+//   DENSE   every input row (the residual adapter, the rotation);
+//   SELECT  batch 1: every CTA derives the exact Top-K rule itself (S_k, lower
+//           index wins ties) from the site's 4096-bin global histogram of the
+//           key bits [30:19] (accumulated by the producer's epilogue) and the site vector x
+//           staged in shared memory: the histogram suffix scan gives the bucket of the k-th
+//           key; radix refinement over bits [18:7] and [6:0] of the staged x, then an index
+//           tie-break, make it exact.  The CTA then takes an exactly balanced share of the
+//           kept rows (block prefix count in index order).  No Top-K kernel, index list or
+//           extra grid-wide dependency sits between two GEMVs.
+// Epilogue (GemvEpi): the last split CTA of each column slice (ticket) converts the slice's
+// accumulators to fp32, applies the site glue (bias / residual add / SiLU(g)*u), writes the
+// next site's vector, re-zeroes the accumulators and, at batch 1, adds the values' key bins
+// into the next site's histogram and writes the slice's sum of squares (for the RMS scale)
+// — the next GEMV's SELECT prologue consumes exactly these.
 #pragma once
 #include "common.cuh"
+#include "larosa.h"
 
 namespace larosa {
 
 constexpr int kGuBlock = 64;          // == LAROSA_GU_BLOCK
 constexpr int kSliceCols = 256;       // columns per CTA (8 per lane)
 constexpr int kGemvWarps = 8;
+constexpr int kGemvThreads = kGemvWarps * 32;
 constexpr int kStageRows = 4;         // rows per stage (one 512-byte warp copy each)
 constexpr int kStages = 4;            // ring depth per warp
 constexpr int kWarpRingBytes = kStages * kStageRows * kSliceCols * 2;   // 8 KB
 constexpr double kFixScale = 4294967296.0;                              // 2^32
+constexpr int kSelBins = 4096;        // histogram of key bits [30:19]
+constexpr int kSelShift = 19;
+constexpr int kGemvMisc = 64;         // ints of scratch
+constexpr int kPoolCap = 512;         // (key, index) entries kept per histogram bucket
 
-enum GemvMode : int {
-    GEMV_LIST = 0,     // kept rows given as a list (rows[], vals) -- split by list position
-    GEMV_THRESH = 1,   // kept rows selected in-kernel from x by the Top-K rule (thresh.cuh)
-    GEMV_DENSE = 2,    // every row, value x (+ vacc) -- the residual adapter
+enum GemvMode : int { GEMV_LIST = 0, GEMV_THRESH = 1, GEMV_DENSE = 2, GEMV_SELECT = 3 };
+enum GemvEpi : int { EPI_NONE = 0, EPI_STORE = 1, EPI_RESID = 2, EPI_SILU = 3 };
+
+// Selection data of one batch-1 site, produced by the site's producer (GEMV epilogue,
+// attention merge, or the standalone preparation kernel) and consumed by the SELECT prologue:
+//   hist  [4096 fine bins of key bits 30:19][256 coarse bins of bits 30:23]   zero at rest
+//   pool  [4096][kPoolCap] (key, index) of each fine bucket's first entries
+//   x16   [d] key >> 15 (the top 16 key bits) of every element
+//   ssq   [ceil(d / 256)] per-slice sums of squares (RMS sites)
+struct SiteSel {
+    uint32_t* hist;
+    uint2* pool;
+    uint16_t* x16;
+    float* ssq;
 };
+constexpr int kSelCoarse = 256;
+constexpr int kSelHistTotal = 4096 + kSelCoarse;
 
-// the per-token Top-K rule produced by thresh.cuh: keep row i iff
-// key_i > tk or (key_i == tk and i <= ti), key = bits(|x_i|); value x_i * scale
+// the per-token Top-K rule: keep row i iff key_i > tk or (key_i == tk and i <= ti),
+// key = bits(|x_i|); value x_i * scale
 struct ThreshOut {
     uint32_t tk;       // key threshold
     int32_t ti;        // index threshold for key == tk (inclusive)
@@ -62,28 +95,55 @@ struct GemvArgs {
     const int* nrows_dev;  // device row count (batch > 1 union), or nullptr
     const float* vals;     // val(r, b) = vals[r * vs_r + b * vs_b]
     int64_t vs_r, vs_b;
-    // GEMV_THRESH / GEMV_DENSE: input x [batch][ldx] over rows [0, d_in)
+    // GEMV_THRESH / GEMV_DENSE / GEMV_SELECT: input x [batch][ldx] over rows [0, d_in)
     const float* x;
     int64_t ldx;
     int d_in;
     const ThreshOut* thr;              // THRESH: per-token rule + RMS scale
-    const unsigned long long* vacc;    // DENSE (optional): val += fix^-1(vacc[b * vacc_ld + r])
-    int64_t vacc_ld;
+    // GEMV_SELECT (batch 1): the site's selection data; sel.ssq null unless RMS site
+    SiteSel sel;
+    int sel_nssq;
+    int sel_k;
+    float sel_eps;                     // < 0: no RMS scale
     int batch;             // real tokens (<= template BP)
     int n_splits;
     int list_cap;          // rows of the per-CTA shared list (host-checked >= rows per split)
     unsigned long long* acc;          // [batch][acc_ld] fixed-point output accumulators
     int64_t acc_ld;
+    // epilogue (GemvEpi); EPI_NONE leaves the accumulators to the consumer kernel
+    int epi;
+    unsigned* tickets;                 // [n_slices], zero at rest
+    const uint16_t* bias;              // [d_out] bf16 or null       (STORE / RESID)
+    const float* res;                  // [batch][res_ld] or null    (RESID)
+    int64_t res_ld;
+    float* out;                        // [batch][out_ld]
+    int64_t out_ld;
+    SiteSel out_sel;                   // batch 1: next site's selection data (hist null = none)
+    float* out_ssq;                    // [batch][out_ssq_ld] per-slice sums of squares or null
+    int64_t out_ssq_ld;
+    uint32_t* zero_hist;               // optional: histogram words to re-zero (free by now)
+    int zero_words;
+    unsigned long long* tl;            // debug timeline slot (5 x u64) or null
+    int sel_dbg;                       // profiling: bitmask of select phases to skip (0 = none)
 };
 
-// ring (aliased by the warp partials at the end) + the CTA's row list [cap] and values [cap][bp]
+__host__ __device__ constexpr size_t gemv_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// shared memory: [ring | staged x (SELECT)] [hist (SELECT)] [row list + values] [misc]
 __host__ __device__ constexpr size_t gemv_ring_bytes(int bp) {
     return (size_t)kGemvWarps * kWarpRingBytes > (size_t)kGemvWarps * bp * kSliceCols * 4
                ? (size_t)kGemvWarps * kWarpRingBytes
                : (size_t)kGemvWarps * bp * kSliceCols * 4;
 }
-__host__ __device__ constexpr size_t gemv_smem_bytes(int bp, int list_cap) {
-    return gemv_ring_bytes(bp) + (size_t)list_cap * (4 + 4 * (size_t)bp) + 128;
+__host__ __device__ constexpr size_t sel_region_bytes(int d);
+// region A: the weight ring, aliased in SELECT mode by the staged selection data
+__host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in);
+__host__ __device__ constexpr size_t gemv_list_off(int bp, int mode, int d_in) { return gemv_x_bytes(bp, mode, d_in); }
+__host__ __device__ constexpr size_t gemv_misc_off(int bp, int mode, int d_in, int list_cap) {
+    return gemv_align(gemv_list_off(bp, mode, d_in) + (size_t)list_cap * (4 + 4 * (size_t)bp), 16);
+}
+__host__ __device__ constexpr size_t gemv_smem_bytes(int bp, int list_cap, int mode = GEMV_LIST, int d_in = 0) {
+    return gemv_misc_off(bp, mode, d_in, list_cap) + (size_t)kGemvMisc * 4;
 }
 
 __device__ __forceinline__ float fix_to_f(unsigned long long a) {
@@ -95,6 +155,32 @@ __device__ __forceinline__ unsigned long long f_to_fix(float v) {
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
+    asm volatile("red.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ uint32_t key_of(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+// producer side of a site: element i of value v.  Fine-bin count (its old value is the
+// pool slot), coarse-bin count (warp-aggregated: a few exponents hold most elements), the
+// (key, i) pool entry and the 16-bit key.
+__device__ __forceinline__ void hist_push(const SiteSel& o, float v, int i) {
+    const uint32_t key = key_of(v), bin = key >> 19;
+    const uint32_t slot = atomicAdd(o.hist + bin, 1u);
+    if (slot < (uint32_t)kPoolCap) o.pool[(size_t)bin * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
+    const unsigned am = __activemask();
+    const unsigned peers = __match_any_sync(am, bin >> 4);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + 4096 + (bin >> 4), __popc(peers));
+    o.x16[i] = (uint16_t)(key >> 15);
+}
 
 // cp.async (LDGSTS): 16 bytes global -> shared, L1 bypass (.cg)
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool pred) {
@@ -103,6 +189,10 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, boo
         "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(smem_u32(smem_dst)),
         "l"(gsrc), "r"((int)pred)
         : "memory");
+}
+// cp.async 4 bytes (L1-allocating .ca is the only variant below 16 bytes)
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -118,39 +208,403 @@ __device__ __forceinline__ void ffma2(float2& a, float w0, float w1, float v) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
 }
 
+// Sum of squares of one 256-value slice (value c of the slice in thread c of 8 warps): a
+// butterfly per warp, then the 8 warp sums in order.  The SELECT prologue's RMS scale sums
+// these partials; the standalone prep kernel reproduces the exact same arithmetic.
+__device__ __forceinline__ float slice_ssq_warp(float v) { return warp_sum(v * v); }
+__device__ __forceinline__ float slice_ssq_combine(const float* w8) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += w8[w];
+    return t;
+}
+// RMS scale from the per-slice partials (fixed order; identical in every CTA)
+__device__ __forceinline__ float rms_scale_from_parts(const float* parts, int n, int d, float eps, int lane) {
+    float s = 0.f;
+    for (int i = lane; i < n; i += 32) s += __ldcg(parts + i);
+    s = warp_sum(s);
+    return 1.0f / sqrtf(s / (float)d + eps);
+}
+
+// Histograms in shared memory are padded (one word per 16 bins) so that a thread reading
+// its 16 consecutive bins is bank-conflict free.
+__host__ __device__ constexpr int hpad(int b) { return b + (b >> 4); }
+constexpr int kSelHistWords = 1024 + 1024 / 16;   // refinement histograms (<= 1024 bins)
+constexpr int kSelCandCap = kPoolCap;
+
+// Suffix search over `nb` (<= 4096, multiple of 16 or < 16 per thread) padded bins
+// (bins[hpad(nb-1)] = largest keys): the bin holding the rem-th largest key.  Thread t owns
+// bins [nb - bpt (t+1), nb - bpt t).  Writes misc[0] = bin, misc[1] = rem within the bin,
+// misc[2] = bin count (0, 0, 0 if the histogram holds fewer than rem keys).  Block-wide.
+template <int NT>
+__device__ void suffix_find(const int* bins, int nb, int rem, int* misc, int* scan_scratch) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {   // defined result (keep-all, bounded work) even on an inconsistent histogram
+        misc[0] = 0;
+        misc[1] = 0;
+        misc[2] = 0;
+    }
+    const int bpt = (nb + NT - 1) / NT;
+    const int hi = max(0, nb - bpt * tid), lo = max(0, nb - bpt * (tid + 1));
+    int c = 0;
+    for (int bb = hi - 1; bb >= lo; --bb) c += bins[hpad(bb)];
+    int total;
+    const int before = block_excl_scan<NT>(c, scan_scratch, &total);
+    if (c > 0 && before < rem && rem <= before + c) {
+        int accu = before;
+        for (int bb = hi - 1; bb >= lo; --bb) {
+            const int h = bins[hpad(bb)];
+            if (accu + h >= rem) {
+                misc[0] = bb;
+                misc[1] = rem - accu;
+                misc[2] = h;
+                break;
+            }
+            accu += h;
+        }
+    }
+    __syncthreads();
+}
+
+// ---- SELECT prologue (batch 1): exact Top-K rule + this CTA's balanced share of rows ------
+// Shared memory (region A, aliased later by the weight ring): the staged 16-bit keys [d], a
+// padded refinement histogram, the bucket's candidates, per-word keep masks.
+// the CTA's own words: every n_splits-th 32-index word (at most kSelMaxWords)
+constexpr int kSelMaxWords = 256;
+__host__ __device__ constexpr size_t sel_hist_off(int d) { return (size_t)kSelMaxWords * 64; }
+__host__ __device__ constexpr size_t sel_cand_off(int d) { return sel_hist_off(d) + (size_t)kSelHistWords * 4; }
+__host__ __device__ constexpr size_t sel_mask_off(int d) { return sel_cand_off(d) + (size_t)kSelCandCap * 8; }
+__host__ __device__ constexpr size_t sel_region_bytes(int d) {
+    return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 8, 128);
+}
+__host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
+    return mode == GEMV_SELECT && sel_region_bytes(d_in) > gemv_ring_bytes(bp) ? sel_region_bytes(d_in)
+                                                                               : gemv_ring_bytes(bp);
+}
+
+// Returns the number of rows placed in lrow / lval (values x_i * s).
+//  1. coarse suffix scan (256 bins, one per thread) -> coarse bucket; one warp scans its 16
+//     fine bins -> fine bucket b* of the k-th key, rem = how many of it to keep;
+//  2. if b* is not taken whole: its candidates from the pool (<= kPoolCap; else the whole x)
+//     refined over key bits [18:9] and [8:0], then an index tie-break -> (tk, ti);
+//  3. keep masks per 32-element word from the 16-bit keys (exact comparison from x only
+//     where the 16-bit key equals tk's), warp prefix counts, the balanced share [P0, P1).
+__device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, float* lval, int* misc,
+                                        int split, int n_splits) {
+    constexpr int NT = kGemvThreads, NW = kGemvWarps;
+    static_assert(NT == kSelCoarse, "one coarse bin per thread");
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int d = a.d_in, k = a.sel_k;
+    uint16_t* xs = reinterpret_cast<uint16_t*>(region);
+    int* shist = reinterpret_cast<int*>(region + sel_hist_off(d));
+    uint32_t* ckey = reinterpret_cast<uint32_t*>(region + sel_cand_off(d));
+    int* cidx = reinterpret_cast<int*>(ckey + kSelCandCap);
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(region + sel_mask_off(d));
+    int* scan = misc + 8;          // block scan scratch (NW + 1)
+    float* fmisc = reinterpret_cast<float*>(misc);
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t* hist = a.sel.hist;
+
+    // ---- 1. stage the 16-bit keys; coarse then fine suffix search ---------------------------
+    // this CTA's words: w_j = split + n_splits j, j < nj (their 16-bit keys, 64 B each)
+    const int nwords = (d + 31) / 32;
+    const int nj = nwords > split ? (nwords - 1 - split) / n_splits + 1 : 0;
+    for (int c = tid; c < 4 * nj; c += NT) {
+        const int j = c >> 2, w = split + n_splits * j;
+        const int i0 = 32 * w + 8 * (c & 3);
+        cp_async16(xs + 32 * j + 8 * (c & 3), a.sel.x16 + i0, i0 < d);
+    }
+    cp_async_commit();
+    const int cc = (int)__ldcg(hist + 4096 + (kSelCoarse - 1 - tid));   // thread 0: top coarse bin
+    if (wid == NW - 1) {
+        const float s = a.sel_eps >= 0.f ? rms_scale_from_parts(a.sel.ssq, a.sel_nssq, d, a.sel_eps, lane) : 1.0f;
+        if (lane == 0) fmisc[4] = s;
+    }
+    if (tid == 0) {
+        misc[0] = 0;
+        misc[1] = 0;
+        misc[2] = 0;
+        misc[5] = -1;
+        misc[60] = 0;
+    }
+    {
+        int total;
+        const int before = block_excl_scan<NT>(cc, scan, &total);
+        if (k > 0 && k < d && cc > 0 && before < k && k <= before + cc) {
+            misc[5] = kSelCoarse - 1 - tid;   // coarse bucket
+            misc[6] = k - before;             // rank inside it
+        }
+    }
+    __syncthreads();
+    if (wid == 0 && misc[5] >= 0) {
+        const int cb = misc[5], r1 = misc[6];
+        const int f = lane < 16 ? (int)__ldcg(hist + 16 * cb + 15 - lane) : 0;   // lane 0: top fine bin
+        const int inc = warp_incl_scan(f);
+        if (f > 0 && inc - f < r1 && r1 <= inc) {
+            misc[0] = 16 * cb + 15 - lane;
+            misc[1] = r1 - (inc - f);
+            misc[2] = f;
+        }
+    }
+    __syncthreads();
+    tl_stamp(a.tl, 5);
+
+    // ---- 2. the rule (tk, ti): keep i iff key > tk or (key == tk and i <= ti) ----------------
+    uint32_t tk = 0u;
+    int ti = 0x7fffffff;
+    bool all = false, none = false;
+    if (k <= 0) {
+        none = true;
+    } else if (k >= d) {
+        all = true;
+    } else {
+        const int bstar = misc[0] & (kSelBins - 1);
+        int rem = misc[1], cnt = misc[2];
+        uint32_t prefix = (uint32_t)bstar << kSelShift, pmask = 0xfffu << kSelShift;
+        if (cnt != rem) {
+            // the bucket's candidates: from the producer's pool, or (bucket larger than the
+            // pool, e.g. constant vectors) every element of x (slow path)
+            const bool pooled = cnt <= kPoolCap;
+            const int ncand = cnt;
+            if (tid == 0) misc[60] = pooled ? ncand : 0;   // (misc[8..16] is scan scratch)
+            if (pooled) {
+                const uint2* pool = a.sel.pool + (size_t)bstar * kPoolCap;
+                for (int t = tid; t < cnt; t += NT) {
+                    const uint2 e = __ldcg(pool + t);
+                    ckey[t] = e.x;
+                    cidx[t] = (int)e.y;
+                }
+            }
+            // refine over bits [18:9] (1024 bins) then [8:0] (512 bins)
+#pragma unroll 1
+            for (int pass = 0; pass < 2 && cnt != rem; ++pass) {
+                const int sh = pass == 0 ? 9 : 0;
+                const int nb = pass == 0 ? 1024 : 512;
+                const uint32_t dm = (uint32_t)(nb - 1);
+                for (int i = tid; i < hpad(nb - 1) + 1; i += NT) shist[i] = 0;
+                __syncthreads();
+                const int n = pooled ? ncand : d;
+                for (int i = tid; i < n; i += NT) {
+                    const uint32_t key = pooled ? ckey[i] : key_of(__ldcg(a.x + i));
+                    if ((key & pmask) == prefix) atomicAdd(&shist[hpad((key >> sh) & dm)], 1);
+                }
+                __syncthreads();
+                suffix_find<NT>(shist, nb, rem, misc, scan);
+                prefix |= (uint32_t)misc[0] << sh;
+                pmask |= dm << sh;
+                rem = misc[1];
+                cnt = misc[2];
+                __syncthreads();
+            }
+            tk = prefix;
+            if (cnt != rem) {
+                // exact key tie at position k: ti = index of the rem-th element with key == tk
+                if (tid == 0) misc[3] = 0x7fffffff;
+                __syncthreads();
+                if (pooled) {
+                    for (int t = tid; t < ncand; t += NT) {
+                        if (ckey[t] != tk) continue;
+                        const int it = cidx[t];
+                        int r = 0;
+                        for (int q = 0; q < ncand; ++q) r += (ckey[q] == tk && cidx[q] < it);
+                        if (r == rem - 1) misc[3] = it;
+                    }
+                } else if (wid == 0) {
+                    // slow path: one warp walks x in index order
+                    int seen = 0;
+                    for (int i0 = 0; i0 < d; i0 += 32) {
+                        const int i = i0 + lane;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, i < d && key_of(__ldcg(a.x + i)) == tk);
+                        if (seen + __popc(bal) >= rem) {
+                            uint32_t m = bal;   // the (rem - seen)-th set bit
+                            for (int q = 1; q < min(rem - seen, 32); ++q) m &= m - 1;
+                            if (lane == 0) misc[3] = i0 + __ffs(m) - 1;
+                            break;
+                        }
+                        seen += __popc(bal);
+                    }
+                }
+                __syncthreads();
+                ti = misc[3];
+            }
+        } else {
+            tk = prefix;           // bucket b* taken whole: key >= b* << 19
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    tl_stamp(a.tl, 6);
+
+    // ---- 3. keep masks from the 16-bit keys, warp prefix counts, balanced share ------------
+    // A 16-bit key equal to tk's top 16 bits is decided exactly from the bucket's candidates
+    // (all such elements lie in bucket b*; table btab in shared memory), unless b* was taken
+    // whole (then every such key is >= tk) or the bucket overflowed the pool (rare: exact
+    // keys are then read from x).
+    const uint32_t t16 = tk >> 15;
+    int* btab = scan + 32;         // [n][2] (index, keep) pairs, at most 8
+    const bool edge_all = (tk & 0x7fffu) == 0u && ti == 0x7fffffff;
+    int nb_tab = 0;
+    if (!all && !none && !edge_all) {
+        if (tid == 0) misc[7] = 0;
+        __syncthreads();
+        const int ncand = misc[60];
+        for (int t = tid; t < ncand; t += NT) {
+            const uint32_t kt = ckey[t];
+            if ((kt >> 15) == t16) {
+                const int slot = atomicAdd(&misc[7], 1);
+                if (slot < 8) {
+                    const int it = cidx[t];
+                    btab[2 * slot] = it;
+                    btab[2 * slot + 1] = kt > tk || (kt == tk && it <= ti);
+                }
+            }
+        }
+        __syncthreads();
+        nb_tab = ncand > 0 ? misc[7] : 1000;   // > 8 or no candidate list: exact reads from x
+    }
+    auto keep16 = [&](uint32_t k16, int i) -> bool {
+        if (k16 != t16) return k16 > t16;
+        if (edge_all) return true;
+        if (nb_tab <= 8) {
+            for (int q = 0; q < nb_tab; ++q)
+                if (btab[2 * q] == i) return btab[2 * q + 1] != 0;
+            return false;
+        }
+        const uint32_t key = key_of(__ldcg(a.x + i));
+        return key > tk || (key == tk && i <= ti);
+    };
+    // keep masks of the CTA's own words (one word per warp at a time), then the rows in index
+    // order: word j's kept rows start at the exclusive prefix of the word counts
+    uint32_t* wmk = wmask;               // [nj] masks
+    int* wcnt = reinterpret_cast<int*>(wmask + kSelMaxWords);   // [nj] counts
+    for (int j = wid; j < nj; j += NW) {
+        const int i = 32 * (split + n_splits * j) + lane;
+        bool kp = false;
+        if (i < d) kp = all ? true : (none ? false : keep16(xs[32 * j + lane], i));
+        const uint32_t m = __ballot_sync(0xffffffffu, kp);
+        if (lane == 0) {
+            wmk[j] = m;
+            wcnt[j] = __popc(m);
+        }
+    }
+    __syncthreads();
+    tl_stamp(a.tl, 7);
+    int total;
+    const int cj = tid < nj ? wcnt[tid] : 0;
+    const int before = block_excl_scan<NT>(cj, scan, &total);
+    __syncthreads();
+    if (tid < nj) wcnt[tid] = before;
+    __syncthreads();
+    for (int j = wid; j < nj; j += NW) {
+        const uint32_t m = wmk[j];
+        if ((m >> lane) & 1u) lrow[wcnt[j] + __popc(m & lt)] = 32 * (split + n_splits * j) + lane;
+    }
+    __syncthreads();   // list complete; the staged region (aliased by the ring) is dead
+    return total;
+}
+
+// ---- epilogue: the last split CTA of a slice finalises its columns ------------------------
 template <int BP>
-__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a) {
+__device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred) {
+    const int c = threadIdx.x, lane = c & 31, wid = c >> 5;
+    const int base = slice * kSliceCols;
+    for (int b = 0; b < a.batch; ++b) {
+        unsigned long long* acc = a.acc + (size_t)b * a.acc_ld;
+        float v = 0.f;
+        bool has = false;
+        if (a.epi == EPI_SILU) {
+            // slice = 2 gate|up blocks of 128 columns (64 gate, then the matching 64 up)
+            if (c < 2 * kGuBlock) {
+                const int blk = c / kGuBlock, q = c % kGuBlock;
+                const int og = base + blk * 2 * kGuBlock + q;
+                if (og < a.d_out) {
+                    const float g = fix_to_f(__ldcg(acc + og));
+                    const float u = fix_to_f(__ldcg(acc + og + kGuBlock));
+                    acc[og] = 0ull;
+                    acc[og + kGuBlock] = 0ull;
+                    v = g / (1.0f + expf(-g)) * u;
+                    a.out[(size_t)b * a.out_ld + slice * 2 * kGuBlock + blk * kGuBlock + q] = v;
+                    has = true;
+                }
+            }
+        } else {
+            const int o = base + c;
+            if (o < a.d_out) {
+                const float y = fix_to_f(__ldcg(acc + o));
+                acc[o] = 0ull;
+                v = y;
+                if (a.bias) v += bf16f(a.bias[o]);
+                if (a.res) v = a.res[(size_t)b * a.res_ld + o] + v;
+                a.out[(size_t)b * a.out_ld + o] = v;
+                has = true;
+            }
+        }
+        if (has && a.out_sel.hist && a.batch == 1) {
+            const int idx = a.epi == EPI_SILU ? slice * 2 * kGuBlock + (c / kGuBlock) * kGuBlock + c % kGuBlock
+                                              : base + c;
+            hist_push(a.out_sel, v, idx);
+        }
+        if (a.out_ssq) {
+            const float w = slice_ssq_warp(v);
+            if (lane == 0) sred[wid] = w;
+            __syncthreads();
+            if (c == 0) a.out_ssq[(size_t)b * a.out_ssq_ld + slice] = slice_ssq_combine(sred);
+            __syncthreads();
+        }
+    }
+}
+
+// One instantiation per (padded batch, row source) keeps each kernel's code small: these
+// launches are latency-bound and start on a cold instruction cache.
+template <int BP, int MODE>
+__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int slice = blockIdx.x, split = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* lrow = reinterpret_cast<int*>(smem + gemv_ring_bytes(BP));           // [cap]
-    float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                // [cap][BP]
-    int* s_cnt = reinterpret_cast<int*>(lval + (size_t)a.list_cap * BP);      // [2][8] + [1]
+    constexpr int mode = MODE;
+    int* lrow = reinterpret_cast<int*>(smem + gemv_list_off(BP, mode, a.d_in));       // [cap]
+    float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                        // [cap][BP]
+    int* misc = reinterpret_cast<int*>(smem + gemv_misc_off(BP, mode, a.d_in, a.list_cap));
 
+    tl_stamp(a.tl, 0);
     pdl_wait();       // the row source comes from the previous kernel
     pdl_trigger();
+    tl_stamp(a.tl, 1);
+    if (a.zero_hist) {   // a histogram whose consumer has completed (kernel-boundary ordered)
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;
+    }
 
     // ---- 1. this CTA's row list in shared memory (ascending) ------------------------------
     int n_list = 0;
-    if (a.mode == GEMV_LIST) {
+    if constexpr (MODE == GEMV_SELECT) {
+        static_assert(BP == 1, "SELECT is the batch-1 path");
+#ifdef LAROSA_EXP_TWICE
+        n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
+        __syncthreads();
+        tl_stamp(a.tl, 3);
+#endif
+        n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
+    } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
         const int rps = (nrows + a.n_splits - 1) / a.n_splits;
         const int r_begin = min(nrows, split * rps);
         n_list = min(nrows, r_begin + rps) - r_begin;
-        for (int t = threadIdx.x; t < n_list; t += kGemvWarps * 32) {
+        for (int t = threadIdx.x; t < n_list; t += kGemvThreads) {
             const int r = r_begin + t;
             lrow[t] = __ldg(a.rows + r);
 #pragma unroll
             for (int b = 0; b < BP; ++b)
                 lval[t * BP + b] = b < a.batch ? __ldg(a.vals + (size_t)r * a.vs_r + (size_t)b * a.vs_b) : 0.f;
         }
+        __syncthreads();
     } else {
         // input range of this split; keep a row if any token keeps it (THRESH rule) or always
         const int rng = (a.d_in + a.n_splits - 1) / a.n_splits;
         const int lo = min(a.d_in, split * rng), hi = min(a.d_in, lo + rng);
         const ThreshOut* thr = a.thr;
         int base = 0;
-        for (int r0 = lo, rnd = 0; r0 < hi; r0 += kGemvWarps * 32, ++rnd) {
+        for (int r0 = lo, rnd = 0; r0 < hi; r0 += kGemvThreads, ++rnd) {
             const int i = r0 + (int)threadIdx.x;
             float v[BP];
             bool any = false;
@@ -160,11 +614,10 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
                 bool keep = false;
                 if (i < hi && b < a.batch) {
                     x = a.x[(size_t)b * a.ldx + i];
-                    if (a.vacc) x += fix_to_f(a.vacc[(size_t)b * a.vacc_ld + i]);
-                    if (a.mode == GEMV_DENSE) {
+                    if constexpr (MODE == GEMV_DENSE) {
                         keep = true;
                     } else {
-                        const uint32_t key = __float_as_uint(x) & 0x7fffffffu;
+                        const uint32_t key = key_of(x);
                         keep = key > thr[b].tk || (key == thr[b].tk && i <= thr[b].ti);
                         x *= thr[b].scale;
                     }
@@ -173,7 +626,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
                 any |= keep;
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, any);
-            int* cnt = s_cnt + (rnd & 1) * 8;
+            int* cnt = misc + 32 + (rnd & 1) * 8;
             if (lane == 0) cnt[warp] = __popc(bal);
             __syncthreads();
             int before = 0, total = 0;
@@ -192,9 +645,12 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
             base += total;
         }
         n_list = base;
+        __syncthreads();
     }
-    __syncthreads();
 
+    tl_stamp(a.tl, 2);
+    float sel_scale = 1.f;
+    if constexpr (MODE == GEMV_SELECT) sel_scale = reinterpret_cast<const float*>(misc)[4];
     // my rows: list entries warp + 8*m, m in [0, n_my)
     const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
     const int col0 = slice * kSliceCols + lane * 8;
@@ -212,6 +668,8 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
                 const int m = st * kStageRows + g;
                 const int row = m < n_my ? lrow[warp + kGemvWarps * m] : 0;
                 cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < n_my);
+                if constexpr (MODE == GEMV_SELECT)   // the row's activation rides in the same group
+                    if (lane == g && m < n_my) cp_async4(lval + warp + kGemvWarps * m, a.x + row);
             }
         }
         cp_async_commit();   // one (possibly empty) group per stage keeps the count uniform
@@ -227,6 +685,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
 
     for (int st = 0; st < n_st; ++st) {
         cp_async_wait<kStages - 1>();          // this lane's chunks of stage st have landed
+        if constexpr (MODE == GEMV_SELECT) __syncwarp();   // lanes 0-3 copied the stage's values
         const unsigned char* src = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
 #pragma unroll
         for (int g = 0; g < kStageRows; ++g) {
@@ -238,7 +697,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
             const float* vrow = lval + (size_t)(warp + kGemvWarps * m) * BP;
 #pragma unroll
             for (int b = 0; b < BP; ++b) {
-                const float v = vrow[b];             // shared-memory broadcast
+                const float v = MODE == GEMV_SELECT ? vrow[b] * sel_scale : vrow[b];   // smem broadcast
                 ffma2(acc[b][0], w0, w1, v);
                 ffma2(acc[b][1], w2, w3, v);
                 ffma2(acc[b][2], w4, w5, v);
@@ -249,6 +708,9 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
     }
     cp_async_wait<0>();
     __syncthreads();   // every warp is done with its ring (the partials alias it)
+#ifndef LAROSA_EXP_TWICE
+    tl_stamp(a.tl, 3);
+#endif
 
     // fixed-order sum of the 8 warps' partials, then one fixed-point red per column
     float* part = reinterpret_cast<float*>(smem);   // [8][BP][256]
@@ -268,6 +730,68 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const GemvArgs a)
             for (int w = 0; w < kGemvWarps; ++w) s += part[((size_t)w * BP + b) * kSliceCols + c];
             red_add_u64(a.acc + (size_t)b * a.acc_ld + o, f_to_fix(s));
         }
+    }
+    if (a.epi == EPI_NONE) {
+        tl_stamp(a.tl, 4);
+        return;
+    }
+
+    // ---- epilogue: the last split of this slice finalises it ------------------------------
+    // (bar.sync orders the CTA's reds before thread 0's release; its acquire plus the next
+    // bar.sync order the other splits' reds before this CTA's accumulator reads)
+    __syncthreads();
+    if (threadIdx.x == 0) misc[0] = atom_add_acq_rel_gpu(a.tickets + slice, 1u) == gridDim.y - 1u;
+    __syncthreads();
+    if (!misc[0]) {
+        tl_stamp(a.tl, 4);
+        return;
+    }
+    if (threadIdx.x == 0) a.tickets[slice] = 0u;
+    gemv_epilogue<BP>(a, slice, reinterpret_cast<float*>(misc + 16));
+    tl_stamp(a.tl, 4);
+}
+
+// ---- standalone SELECT preparation: histogram + per-slice sums of squares of x ------------
+// (batch 1, when the site vector was not produced by a GEMV epilogue).  One CTA of 1024
+// threads; overwrites the 4096-bin histogram and writes ceil(d / 256) partials with the
+// exact arithmetic of gemv_epilogue.
+constexpr int kPrepThreads = 1024;
+__global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* __restrict__ x, int d, SiteSel o) {
+    __shared__ int sh[kSelBins];
+    __shared__ float sgrp[LAROSA_MAX_DIM / 32];
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < kSelBins; i += kPrepThreads) sh[i] = 0;
+    __syncthreads();
+    const int ngrp = (d + 31) / 32;
+    for (int g = wid; g < ngrp; g += kPrepThreads / 32) {
+        const int i = g * 32 + lane;
+        const float v = i < d ? x[i] : 0.f;
+        if (i < d) {
+            const uint32_t key = key_of(v), bin = key >> kSelShift;
+            const int slot = atomicAdd(&sh[bin], 1);
+            if (slot < kPoolCap) o.pool[(size_t)bin * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
+            o.x16[i] = (uint16_t)(key >> 15);
+        }
+        const float w = slice_ssq_warp(v);
+        if (lane == 0) sgrp[g] = w;
+    }
+    __syncthreads();
+    if (o.ssq) {
+        const int nsl = (d + kSliceCols - 1) / kSliceCols;
+        for (int s = tid; s < nsl; s += kPrepThreads) {
+            float w8[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) w8[w] = 8 * s + w < ngrp ? sgrp[8 * s + w] : 0.f;
+            o.ssq[s] = slice_ssq_combine(w8);
+        }
+    }
+    for (int i = tid; i < kSelBins; i += kPrepThreads) o.hist[i] = (uint32_t)sh[i];
+    for (int c = tid; c < kSelCoarse; c += kPrepThreads) {
+        int t = 0;
+        for (int j = 0; j < 16; ++j) t += sh[16 * c + j];
+        o.hist[4096 + c] = (uint32_t)t;
     }
 }
 

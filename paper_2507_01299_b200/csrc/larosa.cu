@@ -16,7 +16,6 @@
 #include "gemv.cuh"
 #include "attention.cuh"
 #include "aux.cuh"
-#include "thresh.cuh"
 #include "fold_tc.cuh"
 
 using namespace larosa;
@@ -100,7 +99,8 @@ cudaError_t allow_smem(K kern, size_t bytes) {
 // so the caller zero-fills a workspace once.  A workspace must be reused only for calls of
 // the same kind and shapes (other layouts would place live data where accumulators were).
 constexpr size_t kCounterHeaderWords = 8192;   // attention tickets
-constexpr size_t kAttnCounterBase = 0;
+constexpr size_t kAttnCounterBase = 0;        // [0, 4096): attention group tickets
+constexpr size_t kGemvTicketBase = 4096;      // + 256 j: slice tickets of the j-th epilogue GEMV
 
 struct Carver {
     char* base;      // nullptr -> size query
@@ -134,37 +134,66 @@ int env_int(const char* name, int dflt) {
 
 int gemv_list_max(int bp) { return bp <= 2 ? 2048 : 1024; }
 
-// 256-column slices x row splits, about `per_sm` 256-thread CTAs per SM in one wave.
-// rows_per_split_src: the number of candidate rows a split may hold (list length for
-// GEMV_LIST, input length for GEMV_THRESH / GEMV_DENSE), bounded by the shared list.
-GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp) {
+// 256-column slices x row splits, as many 256-thread CTAs per SM as fit (at most 2), one
+// wave.  rows_src: candidate rows (list length for LIST, k for SELECT, input length for
+// THRESH / DENSE).  LIST/THRESH/DENSE lists are bounded by gemv_list_max.
+GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp, int mode = GEMV_LIST, int64_t d_in = 0) {
     static const int per_sm_env = env_int("LAROSA_GEMV_CTAS_PER_SM", 0);   // tuning knob (0 = auto)
     GemvPlan p;
     p.n_slices = (int)((d_out + kSliceCols - 1) / kSliceCols);
-    const int per_sm = per_sm_env > 0 ? per_sm_env : (bp <= 4 ? 2 : 1);
-    const int target = sm_count() * per_sm;
-    const int by_target = std::max(1, (target + p.n_slices / 2) / p.n_slices);
+    int per_sm = per_sm_env > 0 ? per_sm_env : (bp <= 4 ? 2 : 1);
     const int by_rows = (int)std::max<int64_t>(1, rows_src / 16);
-    const int lmax = gemv_list_max(bp);
-    const int by_cap = (int)std::max<int64_t>(1, (rows_src + lmax - 1) / lmax);
-    p.n_splits = std::max(by_cap, std::min(by_target, by_rows));
-    p.list_cap = (int)std::max<int64_t>(32, (rows_src + p.n_splits - 1) / p.n_splits);
-    p.smem = gemv_smem_bytes(bp, p.list_cap);
+    int by_cap = 1;
+    const int64_t nwords = (d_in + 31) / 32;
+    if (mode != GEMV_SELECT) {
+        const int lmax = gemv_list_max(bp);
+        by_cap = (int)std::max<int64_t>(1, (rows_src + lmax - 1) / lmax);
+    } else {
+        by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);   // words per CTA
+    }
+    for (int it = 0; it < 2; ++it) {
+        const int target = sm_count() * per_sm;
+        const int by_target = std::max(1, target / p.n_slices);   // one wave: slices x splits <= target
+        p.n_splits = std::max(by_cap, std::min(by_target, by_rows));
+        p.list_cap = mode == GEMV_SELECT ? (int)(32 * ((nwords + p.n_splits - 1) / p.n_splits))   // interleaved words
+                                         : (int)std::max<int64_t>(32, (rows_src + p.n_splits - 1) / p.n_splits + 1);
+        p.smem = gemv_smem_bytes(bp, p.list_cap, mode, (int)d_in);
+        // B200: 228 KB of shared memory per SM, 1 KB reserved per CTA
+        const int fit = (int)(233472 / (p.smem + 1024));
+        if (fit >= per_sm || per_sm == 1) break;
+        per_sm = std::max(1, fit);
+    }
     return p;
+}
+
+template <int BP, int MODE>
+larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
+    auto kern = gemv_kernel<BP, MODE>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv)"));
+        attr_done = true;
+    }
+    if (p.smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "gemv: shared memory plan %zu B too large", p.smem);
+    GemvArgs aa = a;
+    aa.n_splits = p.n_splits;
+    aa.list_cap = p.list_cap;
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvThreads), p.smem, st, aa), "gemv launch");
 }
 
 template <int BP>
 larosa_status launch_gemv_bp(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
-    auto kern = gemv_kernel<BP>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, gemv_smem_bytes(BP, gemv_list_max(BP))), "cudaFuncSetAttribute(gemv)"));
-        attr_done = true;
+    switch (a.mode) {
+        case GEMV_LIST: return launch_gemv_bm<BP, GEMV_LIST>(a, p, st);
+        case GEMV_DENSE: return launch_gemv_bm<BP, GEMV_DENSE>(a, p, st);
+        case GEMV_THRESH:
+            if constexpr (BP > 1) return launch_gemv_bm<BP, GEMV_THRESH>(a, p, st);
+            return fail(LAROSA_EUNSUPPORTED, "gemv: THRESH needs batch > 1");
+        case GEMV_SELECT:
+            if constexpr (BP == 1) return launch_gemv_bm<1, GEMV_SELECT>(a, p, st);
+            return fail(LAROSA_EUNSUPPORTED, "gemv: SELECT is batch 1 only");
+        default: return fail(LAROSA_EINVAL, "gemv: bad mode");
     }
-    GemvArgs aa = a;
-    aa.n_splits = p.n_splits;
-    aa.list_cap = p.list_cap;
-    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvWarps * 32), p.smem, st, aa), "gemv launch");
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
@@ -242,18 +271,6 @@ larosa_status launch_union(const uint32_t* mask, int nwords, int batch, int bp, 
     return cuda_check(launch(union_kernel, dim3(grid), dim3(kUnionThreads), 0, st, mask, nwords, batch, bp, vals, k, d,
                              rows, V, nrows),
                       "union launch");
-}
-
-larosa_status launch_finalize(const FinalizeArgs& f, cudaStream_t st) {
-    const int64_t total = (int64_t)f.batch * std::max(f.n, f.zero3_n);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 2 * sm_count()));
-    return cuda_check(launch(finalize_kernel, dim3(grid), dim3(256), 0, st, f), "finalize launch");
-}
-
-FinalizeArgs finalize_args_base() {
-    FinalizeArgs f;
-    memset(&f, 0, sizeof(f));
-    return f;
 }
 
 }  // namespace
@@ -391,16 +408,78 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
         a.vs_b = 1;
         a.nrows_dev = nrows;
     }
-    LAROSA_TRY(launch_gemv(a, p, bp, st));
-    FinalizeArgs f = finalize_args_base();
-    f.n = (int)d_out;
-    f.batch = batch;
-    f.acc1 = acc;
-    f.acc1_ld = d_out;
-    f.bias1 = bias;
-    f.out1 = y;
-    f.out1_ld = d_out;
-    return launch_finalize(f, st);
+    a.epi = EPI_STORE;
+    a.tickets = c.counters(kGemvTicketBase);
+    a.bias = bias;
+    a.out = y;
+    a.out_ld = d_out;
+    return launch_gemv(a, p, bp, st);
+}
+
+// ============================================================================== fused Top-K + GEMV
+static void carve_topk_gemv(Carver& c, int64_t d_in, int64_t d_out, unsigned long long** acc, SiteSel* sel) {
+    unsigned long long* a = c.take<unsigned long long>((size_t)d_out);
+    SiteSel q;
+    q.hist = c.take<uint32_t>(kSelHistTotal);
+    q.pool = c.take<uint2>((size_t)kSelBins * kPoolCap);
+    q.x16 = c.take<uint16_t>((size_t)d_in);
+    q.ssq = c.take<float>((size_t)(d_in + kSliceCols - 1) / kSliceCols);
+    if (acc) *acc = a;
+    if (sel) *sel = q;
+}
+
+extern "C" size_t larosa_topk_sparse_gemv_workspace_size(int64_t d_in, int64_t d_out) {
+    if (d_in <= 0 || d_out <= 0) return 0;
+    Carver c(nullptr);
+    carve_topk_gemv(c, d_in, d_out, nullptr, nullptr);
+    return c.size();
+}
+
+extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                                 const uint16_t* W, int64_t d_out, int64_t ld, const uint16_t* bias,
+                                                 float* y, void* ws, size_t ws_bytes, larosa_stream_t stream) {
+    if (!x || !W || !y) return fail(LAROSA_EINVAL, "topk_sparse_gemv: NULL pointer");
+    if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "topk_sparse_gemv: d_in, d_out must be > 0");
+    if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "topk_sparse_gemv: k outside [0, d_in]");
+    if (d_in > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv: d_in > %d", LAROSA_MAX_DIM);
+    if (d_in % 8) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv: d_in %% 8 != 0");
+    if (ld < d_out) return fail(LAROSA_ESHAPE, "topk_sparse_gemv: ld < d_out");
+    if (ld % 8 || d_out % 8) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv: ld and d_out must be multiples of 8");
+    if (d_out > (int64_t)256 * kSliceCols) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv: d_out > 65536");
+    if (!aligned16(W) || !aligned16(x) || !aligned16(y) || (bias && !aligned16(bias)))
+        return fail(LAROSA_EINVAL, "topk_sparse_gemv: pointers must be 16-byte aligned");
+    const size_t need = larosa_topk_sparse_gemv_workspace_size(d_in, d_out);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "topk_sparse_gemv: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Carver c(ws);
+    unsigned long long* acc;
+    SiteSel sel;
+    carve_topk_gemv(c, d_in, d_out, &acc, &sel);
+    if (rms_eps < 0.f) sel.ssq = nullptr;
+    LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)d_in, sel),
+                          "select prep launch"));
+    const GemvPlan p = plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
+    GemvArgs a = gemv_args_base();
+    a.W = W;
+    a.ld = ld;
+    a.d_out = (int)d_out;
+    a.mode = GEMV_SELECT;
+    a.x = x;
+    a.ldx = d_in;
+    a.d_in = (int)d_in;
+    a.sel = sel;
+    a.sel_nssq = (int)((d_in + kSliceCols - 1) / kSliceCols);
+    a.sel_k = (int)k;
+    a.sel_eps = rms_eps;
+    a.batch = 1;
+    a.acc = acc;
+    a.acc_ld = d_out;
+    a.epi = EPI_STORE;
+    a.tickets = c.counters(kGemvTicketBase);
+    a.bias = bias;
+    a.out = y;
+    a.out_ld = d_out;
+    return launch_gemv(a, p, 1, st);
 }
 
 extern "C" larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info) {
@@ -534,21 +613,17 @@ extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t*
 
 // ============================================================================== decoder layer
 namespace {
-struct SiteWs {
-    uint32_t* ghist;      // [B][4096]  zero at rest
-    unsigned* ticket;     // [B]        zero at rest
-    float* ssq;           // [B][NB]
-    ThreshOut* thr;       // [B]
-};
-
 struct LayerWs {
     unsigned long long *acc_qkv, *acc_o, *acc_gu, *acc_down, *acc_adp;
-    SiteWs site[4];
+    SiteSel sel[4];       // batch 1: selection data of the site inputs h1..h4 (gemv.cuh)
+    ThreshOut* thr[4];    // batch > 1: per-token Top-K rules
     float* h2;
     float* rmid;
     float* h4;
+    float* radp;          // r_mid + y_down, the adapter's input
     float* attn_part;
     unsigned* attn_cnt;
+    unsigned* tickets[4]; // slice tickets of the O, gate|up, down, adapter GEMV epilogues
 };
 
 struct LayerDims {
@@ -577,31 +652,35 @@ int attn_chunk(int64_t max_ctx, int units) {
     return ch;
 }
 
+int n_slices(int64_t n) { return (int)((n + kSliceCols - 1) / kSliceCols); }
+
 void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, LayerWs* ws) {
-    const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     LayerWs tmp;
     LayerWs* o = ws ? ws : &tmp;
-    // zero-at-rest state first: GEMV accumulators, threshold histograms and tickets
+    // zero-at-rest state first: GEMV accumulators and histograms
     o->acc_qkv = c.take<unsigned long long>((size_t)batch * L.nqkv);
     o->acc_o = c.take<unsigned long long>((size_t)batch * L.d);
     o->acc_gu = c.take<unsigned long long>((size_t)batch * L.dgu);
     o->acc_down = c.take<unsigned long long>((size_t)batch * L.d);
     o->acc_adp = c.take<unsigned long long>((size_t)batch * L.d);
+    const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     for (int s = 0; s < 4; ++s) {
-        o->site[s].ghist = c.take<uint32_t>((size_t)batch * kThrBins);
-        o->site[s].ticket = c.take<unsigned>((size_t)batch);
+        SiteSel& q = o->sel[s];
+        q.hist = c.take<uint32_t>(kSelHistTotal);
+        q.pool = batch == 1 ? c.take<uint2>((size_t)kSelBins * kPoolCap) : nullptr;
+        q.x16 = batch == 1 ? c.take<uint16_t>((size_t)din[s]) : nullptr;
+        q.ssq = (s == 0 || s == 2) ? c.take<float>((size_t)batch * n_slices(L.d)) : nullptr;
     }
-    for (int s = 0; s < 4; ++s) {
-        o->site[s].ssq = c.take<float>((size_t)batch * thresh_nb((int)din[s]));
-        o->site[s].thr = c.take<ThreshOut>((size_t)batch);
-    }
+    for (int s = 0; s < 4; ++s) o->thr[s] = c.take<ThreshOut>((size_t)batch);
     o->h2 = c.take<float>((size_t)batch * L.nq);
     o->rmid = c.take<float>((size_t)batch * L.d);
     o->h4 = c.take<float>((size_t)batch * L.inter);
+    o->radp = c.take<float>((size_t)batch * L.d);
     const int ch = attn_chunk(max_ctx, batch * (int)L.hkv);
     const int nch = (int)((max_ctx + ch - 1) / ch);
     o->attn_part = c.take<float>((size_t)batch * L.hkv * nch * L.G * (L.hd + 2));
     o->attn_cnt = c.counters(kAttnCounterBase);
+    for (int j = 0; j < 4; ++j) o->tickets[j] = c.counters(kGemvTicketBase + 256 * j);
 }
 
 larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_plan* p, const larosa_layer_state* s) {
@@ -619,7 +698,7 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
     if (w->d > LAROSA_MAX_DIM || w->inter > LAROSA_MAX_DIM || w->n_q_heads * w->head_dim > LAROSA_MAX_DIM)
         return fail(LAROSA_EUNSUPPORTED, "sparse_layer: dimension > %d", LAROSA_MAX_DIM);
     if (s->max_ctx <= 0) return fail(LAROSA_EINVAL, "sparse_layer: max_ctx must be > 0");
-    if ((int64_t)s->batch * w->n_kv_heads > (int64_t)kCounterHeaderWords)
+    if ((int64_t)s->batch * w->n_kv_heads > (int64_t)kGemvTicketBase)
         return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch * Hkv too large");
     const int64_t nq = w->n_q_heads * w->head_dim;
     if (p->k_h1 < 0 || p->k_h1 > w->d || p->k_h2 < 0 || p->k_h2 > nq || p->k_h3 < 0 || p->k_h3 > w->d || p->k_h4 < 0 ||
@@ -636,29 +715,10 @@ larosa_status tap_copy(void* dst, const void* src, size_t bytes, cudaStream_t st
     return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st), "tap copy");
 }
 
-template <int MODE>
-larosa_status launch_thresh_m(const ThreshArgs& t, int batch, cudaStream_t st) {
-    return cuda_check(launch(thresh_kernel<MODE>, dim3(thresh_nb(t.d), batch), dim3(kThrThreads), 0, st, t),
-                      "thresh launch");
-}
-larosa_status launch_thresh(const ThreshArgs& t, int batch, cudaStream_t st) {
-    if (t.mode == THR_RESID_ACC) return launch_thresh_m<THR_RESID_ACC>(t, batch, st);
-    if (t.mode == THR_SILU_GU) return launch_thresh_m<THR_SILU_GU>(t, batch, st);
-    return launch_thresh_m<THR_PLAIN>(t, batch, st);
-}
-
-static_assert((int)THR_PLAIN == (int)SRC_PLAIN && (int)THR_RESID_ACC == (int)SRC_RESID_ACC &&
-                  (int)THR_SILU_GU == (int)SRC_SILU_GU,
-              "source enums must agree");
-// the single-wave ticket threshold kernel (thresh.cuh) instead of the cluster Top-K
-bool use_ticket_thresh() {
-    static const int v = env_int("LAROSA_THRESH_KERNEL", 0);
-    return v != 0;
-}
-
 // profiling aid: bitmask of the layer's kernels that are launched (default: all)
 int g_phase_mask = -2;
-unsigned long long* g_thr_dbg = nullptr;   // device buffer [4][16] of threshold-kernel stamps
+unsigned long long* g_tl = nullptr;   // debug timeline: [n][1024 CTAs][8] u64, one block per layer kernel
+int g_tl_n = 0;
 int layer_phase_mask() {
     if (g_phase_mask == -2) g_phase_mask = env_int("LAROSA_LAYER_PHASES", -1);
     return g_phase_mask;
@@ -666,7 +726,10 @@ int layer_phase_mask() {
 }  // namespace
 
 extern "C" void larosa_debug_set_layer_phases(int mask) { g_phase_mask = mask; }
-extern "C" void larosa_debug_set_thresh_stamps(void* dev_buf) { g_thr_dbg = static_cast<unsigned long long*>(dev_buf); }
+extern "C" void larosa_debug_set_timeline(void* dev_buf, int n_slots) {
+    g_tl = static_cast<unsigned long long*>(dev_buf);
+    g_tl_n = n_slots;
+}
 
 extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch, int64_t max_ctx) {
     if (!w || batch < 1 || max_ctx <= 0) return 0;
@@ -675,18 +738,18 @@ extern "C" size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int
     return c.size();
 }
 
-// Kernel sequence (one decode step of one layer; every kernel is launched with PDL):
-//   thresh(h1 = r, RMS)                       -> rule T1, s1
-//   gemv(W_qkv, THRESH: rows kept by T1)      -> acc_qkv
-//   attention <- acc_qkv (+bias, RoPE, KV append)          -> h2
-//   thresh(h2)                                -> T2
-//   gemv(W_o, THRESH)                         -> acc_o
-//   thresh(h3 = r + acc_o, RMS; zero acc_o)   -> r_mid, T3, s3
-//   gemv(W_gate|up, THRESH)                   -> acc_gu
-//   thresh(h4 = SiLU(g) * u; zero acc_gu)     -> h4, T4
-//   gemv(W_down, THRESH)                      -> acc_down
-//   gemv(adapter, DENSE; values r_mid + acc_down)          -> acc_adp          (if adapter)
-//   finalize: r <- acc_adp  (or r_mid + acc_down); zero acc_down, acc_adp, acc_qkv
+// Kernel sequence of one decode step of one layer (every kernel launched with PDL).
+// Batch 1 (the Top-K selection of each site is fused into the consuming GEMV, SELECT):
+//   [prep(h1 = r): histogram + RMS partials]          unless state->chained
+//   gemv W_qkv   SELECT(h1, k1, RMS)  -> acc_qkv                 (EPI_NONE)
+//   attention    <- acc_qkv (+bias, RoPE, KV append) -> h2, hist(h2); re-zero acc_qkv
+// (each histogram is re-zeroed by a later kernel once its consumer has completed)
+//   gemv W_o     SELECT(h2, k2)       -> r_mid = r + y, hist(h3), RMS partials(h3)
+//   gemv W_gu    SELECT(h3, k3, RMS)  -> h4 = SiLU(g) u, hist(h4)
+//   gemv W_down  SELECT(h4, k4)       -> r_adp = r_mid + y          [no adapter: -> r, hist(h1)]
+//   gemv A_l     DENSE(r_adp)         -> r = y, hist(h1'), RMS partials(h1')  (next layer's h1)
+// Batch > 1: the same GEMVs in THRESH mode, each preceded by the cluster Top-K kernel that
+// publishes every token's rule (Tk, Ti, s) from the materialised site vector.
 // Taps (parity checks) add exact index-list Top-K launches on the materialised inputs.
 extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_layer_plan* plan,
                                              const larosa_layer_state* s, const larosa_layer_taps* taps, void* ws,
@@ -699,6 +762,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const LayerDims L = layer_dims(w);
     const int B = s->batch, bp = pad_batch(B);
+    const bool fused = B == 1;
     Carver c(ws);
     LayerWs W;
     carve_layer(c, L, B, s->max_ctx, &W);
@@ -707,78 +771,95 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         T = *taps;
     else
         memset(&T, 0, sizeof(T));
+    const int nsl_d = n_slices(L.d);
+    auto tl_slot = [&](int i) -> unsigned long long* { return g_tl && i < g_tl_n ? g_tl + 8192 * i : nullptr; };
 
-    // one site: threshold kernel, optional exact index-list tap, THRESH GEMV
-    auto site = [&](int si, ThreshArgs t, int64_t din, int64_t k, const float* xmat, int32_t* tap_idx,
-                    float* tap_vals, const uint16_t* Wt, int64_t dout, unsigned long long* acc) -> larosa_status {
-        t.d = (int)din;
-        t.k = (int)k;
-        t.ghist = W.site[si].ghist;
-        t.ticket = W.site[si].ticket;
-        t.ssq_part = W.site[si].ssq;
-        t.out = W.site[si].thr;
-        t.dbg = g_thr_dbg ? g_thr_dbg + 32 * si : nullptr;
-        if (!on(si == 0 ? 0 : 2 * si + 1)) {
-        } else if (use_ticket_thresh()) {
-            LAROSA_TRY(launch_thresh(t, B, st));
-        } else {
-            // cluster Top-K in rule mode: finalises the fused source, emits (Tk, Ti, s)
-            TopkKernelArgs r = topk_args_base();
-            r.mode = t.mode;   // ThrSrc and TopkSrc share their numbering
-            r.x = t.x;
-            r.ldx = t.ldx;
-            r.d = (int)din;
-            r.k = (int)k;
-            r.rms_eps = t.rms_eps;
-            r.xr_out = t.xout;
-            r.resid = t.resid;
-            r.resid_ld = t.resid_ld;
-            r.acc = t.acc;
-            r.acc_ld = t.acc_ld;
-            r.rule_out = W.site[si].thr;
-            LAROSA_TRY(launch_topk(r, B, st));
-        }
-        if (tap_idx || tap_vals) {
-            // exact ascending index list + values (same rule) for parity checks
-            TopkKernelArgs tk = topk_args_base();
-            tk.x = xmat;
-            tk.ldx = din;
-            tk.d = (int)din;
-            tk.k = (int)k;
-            tk.rms_eps = t.rms_eps;
-            tk.idx = tap_idx;
-            tk.vals = tap_vals;
-            if (tap_idx && tap_vals) LAROSA_TRY(launch_topk(tk, B, st));
-        }
-        const int bit = si == 0 ? 1 : (si == 1 ? 4 : (si == 2 ? 6 : 8));
-        if (!on(bit)) return LAROSA_OK;
-        const GemvPlan p = plan_gemv(dout, din, bp);
+    // exact index-list Top-K of a materialised site vector (parity taps only)
+    auto tap_topk = [&](const float* x, int64_t din, int64_t k, float eps, int32_t* idx, float* vals) -> larosa_status {
+        if (!idx || !vals) return LAROSA_OK;
+        TopkKernelArgs tk = topk_args_base();
+        tk.x = x;
+        tk.ldx = din;
+        tk.d = (int)din;
+        tk.k = (int)k;
+        tk.rms_eps = eps;
+        tk.idx = idx;
+        tk.vals = vals;
+        return launch_topk(tk, B, st);
+    };
+    // batch > 1: every token's selection rule from the cluster Top-K kernel
+    auto rule_topk = [&](int si, const float* x, int64_t din, int64_t k, float eps) -> larosa_status {
+        TopkKernelArgs r = topk_args_base();
+        r.x = x;
+        r.ldx = din;
+        r.d = (int)din;
+        r.k = (int)k;
+        r.rms_eps = eps;
+        r.rule_out = W.thr[si];
+        return launch_topk(r, B, st);
+    };
+    // the GEMV of site si on the site vector x (SELECT at batch 1, THRESH otherwise)
+    auto site_gemv = [&](int si, const float* x, int64_t din, int64_t k, float eps, const uint16_t* Wt, int64_t dout,
+                         unsigned long long* acc) {
         GemvArgs a = gemv_args_base();
         a.W = Wt;
         a.ld = dout;
         a.d_out = (int)dout;
-        a.mode = GEMV_THRESH;
-        a.x = xmat;
+        a.x = x;
         a.ldx = din;
         a.d_in = (int)din;
-        a.thr = W.site[si].thr;
         a.batch = B;
         a.acc = acc;
         a.acc_ld = dout;
-        return launch_gemv(a, p, bp, st);
+        if (fused) {
+            a.mode = GEMV_SELECT;
+            a.sel = W.sel[si];
+            if (eps < 0.f) a.sel.ssq = nullptr;
+            a.sel_nssq = nsl_d;
+            a.sel_k = (int)k;
+            a.sel_eps = eps;
+        } else {
+            a.mode = GEMV_THRESH;
+            a.thr = W.thr[si];
+        }
+        return a;
+    };
+    auto plan_site = [&](int64_t dout, int64_t din, int64_t k) {
+        return fused ? plan_gemv(dout, k, 1, GEMV_SELECT, din) : plan_gemv(dout, din, bp, GEMV_THRESH, din);
+    };
+    // epilogue of a site GEMV; `next` = the site whose selection data it produces (-1: none)
+    auto epi = [&](GemvArgs& a, int j, int mode, const float* res, float* out, int next) {
+        a.epi = mode;
+        a.tickets = W.tickets[j];
+        a.res = res;
+        a.res_ld = L.d;
+        a.out = out;
+        a.out_ld = mode == EPI_SILU ? L.inter : L.d;
+        if (fused && next >= 0) {
+            a.out_sel = W.sel[next];
+            a.out_ssq = W.sel[next].ssq;   // RMS partials for h1 / h3
+            a.out_ssq_ld = nsl_d;
+        }
     };
 
-    // ---- h1: r (RMS scale) -> QKV -------------------------------------------------------------
-    {
-        ThreshArgs t;
-        memset(&t, 0, sizeof(t));
-        t.mode = THR_PLAIN;
-        t.x = s->resid;
-        t.ldx = L.d;
-        t.rms_eps = w->rms_eps;
-        LAROSA_TRY(site(0, t, L.d, plan->k_h1, s->resid, T.idx_h1, T.vals_h1, w->w_qkv, L.nqkv, W.acc_qkv));
+    // ---- h1: r (RMS) -> QKV ---------------------------------------------------------------------
+    if (fused) {
+        if (!s->chained && on(0))
+            LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, (const float*)s->resid,
+                                         (int)L.d, W.sel[0]),
+                                  "select prep launch"));
+    } else if (on(0)) {
+        LAROSA_TRY(rule_topk(0, s->resid, L.d, plan->k_h1, w->rms_eps));
     }
-    // ---- attention (finalises q / new k, v from acc_qkv) -------------------------------------
+    LAROSA_TRY(tap_topk(s->resid, L.d, plan->k_h1, w->rms_eps, T.idx_h1, T.vals_h1));
+    if (on(1)) {
+        GemvArgs a = site_gemv(0, s->resid, L.d, plan->k_h1, w->rms_eps, w->w_qkv, L.nqkv, W.acc_qkv);
+        a.zero_hist = fused ? W.sel[3].hist : nullptr;   // h4's consumer (previous layer's down GEMV) is done
+        a.tl = tl_slot(0);
+        a.zero_words = kSelHistTotal;
+        LAROSA_TRY(launch_gemv(a, plan_site(L.nqkv, L.d, plan->k_h1), fused ? 1 : bp, st));
+    }
+    // ---- attention (finalises q / new k, v from acc_qkv, re-zeroes it) -> h2 ---------------------
     {
         AttnArgs aa;
         memset(&aa, 0, sizeof(aa));
@@ -799,6 +880,9 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         aa.part = W.attn_part;
         aa.counters = W.attn_cnt;
         aa.out = W.h2;
+        if (fused) aa.out_sel = W.sel[1];
+        aa.tl = tl_slot(1);
+
         const size_t smem = attn_smem_bytes(L.G, (int)L.hd, aa.chunk);
         const dim3 grid(B * (int)L.hkv, aa.n_chunks);
         if (!on(2)) {
@@ -808,86 +892,65 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             LAROSA_TRY(cuda_check(launch(attention_kernel<2>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch"));
         LAROSA_TRY(tap_copy(T.h2, W.h2, sizeof(float) * B * L.nq, st));
     }
-    // ---- h2: attention output -> O -------------------------------------------------------------
-    {
-        ThreshArgs t;
-        memset(&t, 0, sizeof(t));
-        t.mode = THR_PLAIN;
-        t.x = W.h2;
-        t.ldx = L.nq;
-        t.rms_eps = -1.0f;
-        LAROSA_TRY(site(1, t, L.nq, plan->k_h2, W.h2, T.idx_h2, T.vals_h2, w->w_o, L.d, W.acc_o));
+    // ---- h2 -> O; epilogue r_mid = r + y_o (h3) -------------------------------------------------
+    if (!fused && on(3)) LAROSA_TRY(rule_topk(1, W.h2, L.nq, plan->k_h2, -1.0f));
+    LAROSA_TRY(tap_topk(W.h2, L.nq, plan->k_h2, -1.0f, T.idx_h2, T.vals_h2));
+    if (on(4)) {
+        GemvArgs a = site_gemv(1, W.h2, L.nq, plan->k_h2, -1.0f, w->w_o, L.d, W.acc_o);
+        epi(a, 0, EPI_RESID, s->resid, W.rmid, 2);
+        a.tl = tl_slot(2);
+        a.zero_hist = fused ? W.sel[0].hist : nullptr;   // h1's consumer (QKV) is done
+        a.zero_words = kSelHistTotal;
+        LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.nq, plan->k_h2), fused ? 1 : bp, st));
     }
-    // ---- h3: r_mid = r + y_o (RMS scale) -> gate|up --------------------------------------------
-    {
-        ThreshArgs t;
-        memset(&t, 0, sizeof(t));
-        t.mode = THR_RESID_ACC;
-        t.resid = s->resid;
-        t.resid_ld = L.d;
-        t.acc = W.acc_o;
-        t.acc_ld = L.d;
-        t.xout = W.rmid;
-        t.rms_eps = w->rms_eps;
-        LAROSA_TRY(site(2, t, L.d, plan->k_h3, W.rmid, T.idx_h3, T.vals_h3, w->w_gu, L.dgu, W.acc_gu));
-        LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
+    LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
+    // ---- h3 (RMS) -> gate|up; epilogue h4 = SiLU(g) u ----------------------------------------------
+    if (!fused && on(5)) LAROSA_TRY(rule_topk(2, W.rmid, L.d, plan->k_h3, w->rms_eps));
+    LAROSA_TRY(tap_topk(W.rmid, L.d, plan->k_h3, w->rms_eps, T.idx_h3, T.vals_h3));
+    if (on(6)) {
+        GemvArgs a = site_gemv(2, W.rmid, L.d, plan->k_h3, w->rms_eps, w->w_gu, L.dgu, W.acc_gu);
+        epi(a, 1, EPI_SILU, nullptr, W.h4, 3);
+        a.tl = tl_slot(3);
+        a.zero_hist = fused ? W.sel[1].hist : nullptr;   // h2's consumer (O) is done
+        a.zero_words = kSelHistTotal;
+        LAROSA_TRY(launch_gemv(a, plan_site(L.dgu, L.d, plan->k_h3), fused ? 1 : bp, st));
     }
-    // ---- h4 = SiLU(g) * u -> down --------------------------------------------------------------
-    {
-        ThreshArgs t;
-        memset(&t, 0, sizeof(t));
-        t.mode = THR_SILU_GU;
-        t.acc = W.acc_gu;
-        t.acc_ld = L.dgu;
-        t.xout = W.h4;
-        t.rms_eps = -1.0f;
-        LAROSA_TRY(site(3, t, L.inter, plan->k_h4, W.h4, T.idx_h4, T.vals_h4, w->w_down, L.d, W.acc_down));
-        LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
+    LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
+    // ---- h4 -> down; epilogue r_mid + y_down (-> adapter input, or the next layer's r) ------------
+    if (!fused && on(7)) LAROSA_TRY(rule_topk(3, W.h4, L.inter, plan->k_h4, -1.0f));
+    LAROSA_TRY(tap_topk(W.h4, L.inter, plan->k_h4, -1.0f, T.idx_h4, T.vals_h4));
+    if (on(8)) {
+        GemvArgs a = site_gemv(3, W.h4, L.inter, plan->k_h4, -1.0f, w->w_down, L.d, W.acc_down);
+        if (w->adapter)
+            epi(a, 2, EPI_RESID, W.rmid, W.radp, -1);
+        else
+            epi(a, 2, EPI_RESID, W.rmid, s->resid, 0);
+        a.zero_hist = fused ? W.sel[2].hist : nullptr;   // h3's consumer (gate|up) is done
+        a.tl = tl_slot(4);
+        a.zero_words = kSelHistTotal;
+        LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.inter, plan->k_h4), fused ? 1 : bp, st));
     }
-    // ---- residual adapter r <- (r_mid + y_down) . A_l (dense GEMV), finalize ------------
-    FinalizeArgs f = finalize_args_base();
-    f.n = (int)L.d;
-    f.batch = B;
-    f.zero3 = W.acc_qkv;          // attention read it; zero it for the next step
-    f.zero3_ld = L.nqkv;
-    f.zero3_n = (int)L.nqkv;
+    // ---- residual adapter r <- (r_mid + y_down) . A_l (dense GEMV) -------------------------
     if (w->adapter) {
+        LAROSA_TRY(tap_copy(T.r_out, W.radp, sizeof(float) * B * L.d, st));
         if (on(9)) {
-            const GemvPlan p = plan_gemv(L.d, L.d, bp);
+            const GemvPlan p = plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d);
             GemvArgs a = gemv_args_base();
             a.W = w->adapter;
             a.ld = L.d;
             a.d_out = (int)L.d;
             a.mode = GEMV_DENSE;
-            a.x = W.rmid;
+            a.x = W.radp;
             a.ldx = L.d;
             a.d_in = (int)L.d;
-            a.vacc = W.acc_down;
-            a.vacc_ld = L.d;
             a.batch = B;
             a.acc = W.acc_adp;
             a.acc_ld = L.d;
+            epi(a, 3, EPI_STORE, nullptr, s->resid, 0);
+            a.tl = tl_slot(5);
             LAROSA_TRY(launch_gemv(a, p, bp, st));
         }
-        f.acc1 = W.acc_adp;
-        f.acc1_ld = L.d;
-        f.out1 = s->resid;
-        f.out1_ld = L.d;
-        f.acc2 = W.acc_down;          // r_out = r_mid + y_down (tap), then zero
-        f.acc2_ld = L.d;
-        f.res2 = W.rmid;
-        f.res2_ld = L.d;
-        f.out2 = T.r_out;
-        f.out2_ld = L.d;
-        if (on(10)) LAROSA_TRY(launch_finalize(f, st));
     } else {
-        f.acc1 = W.acc_down;
-        f.acc1_ld = L.d;
-        f.res1 = W.rmid;
-        f.res1_ld = L.d;
-        f.out1 = s->resid;
-        f.out1_ld = L.d;
-        if (on(10)) LAROSA_TRY(launch_finalize(f, st));
         LAROSA_TRY(tap_copy(T.r_out, s->resid, sizeof(float) * B * L.d, st));
     }
     return LAROSA_OK;

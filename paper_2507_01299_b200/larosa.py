@@ -46,7 +46,7 @@ class LayerPlanC(ctypes.Structure):
 
 class LayerStateC(ctypes.Structure):
     _fields_ = [("resid", _vp), ("k_cache", _vp), ("v_cache", _vp), ("pos", _vp),
-                ("max_ctx", _c_i64), ("batch", _c_i32)]
+                ("max_ctx", _c_i64), ("batch", _c_i32), ("chained", _c_i32)]
 
 
 class LayerTapsC(ctypes.Structure):
@@ -85,6 +85,10 @@ def lib() -> ctypes.CDLL:
     L.larosa_sparse_gemv_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64, _c_i64]
     L.larosa_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i32, _c_i64, _vp, _vp, _vp,
                                      ctypes.c_size_t, _vp]
+    L.larosa_topk_sparse_gemv_workspace_size.restype = ctypes.c_size_t
+    L.larosa_topk_sparse_gemv_workspace_size.argtypes = [_c_i64, _c_i64]
+    L.larosa_topk_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp, _vp,
+                                          ctypes.c_size_t, _vp]
     L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
     L.larosa_debug_set_layer_phases.restype = None
     L.larosa_gemv_plan_info.argtypes = [_c_i64, _c_i64, _c_i32, ctypes.POINTER(_c_i32)]
@@ -95,7 +99,7 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(LayerStateC), ctypes.POINTER(LayerTapsC), _vp,
                                       ctypes.c_size_t, _vp]
     for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
-                 "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_sparse_layer"):
+                 "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer"):
         getattr(L, name).restype = ctypes.c_int
     if L.larosa_abi_version() != 1:
         raise RuntimeError("liblarosa ABI version mismatch")
@@ -224,6 +228,23 @@ def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Op
     return y
 
 
+def topk_sparse_gemv(x: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = -1.0,
+                     bias: Optional[torch.Tensor] = None, d_out: Optional[int] = None,
+                     out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Batch 1: y = bias + sum_{j in TopK_k(|x|)} x_j s W[j]  (selection fused into the GEMV)."""
+    x = x.reshape(-1)
+    d_in, ld = W.shape
+    d_out = ld if d_out is None else d_out
+    assert x.dtype == torch.float32 and x.numel() == d_in
+    y = out if out is not None else torch.empty((d_out,), dtype=torch.float32, device=W.device)
+    L = lib()
+    nb = L.larosa_topk_sparse_gemv_workspace_size(d_in, d_out)
+    ws = _ws(("topk_sparse_gemv", d_in, d_out), nb, W.device)
+    _check(L.larosa_topk_sparse_gemv(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), d_out, ld, _ptr(bias), _ptr(y),
+                                     _ptr(ws), ws.numel(), _stream(stream)))
+    return y
+
+
 @dataclass
 class LayerWeights:
     """Folded bf16 (int16-bit) weights of one decoder layer in the Wc layout."""
@@ -253,11 +274,12 @@ class LayerState:
     k_cache: torch.Tensor    # int16 [B, Hkv, max_ctx, hd]
     v_cache: torch.Tensor
     pos: torch.Tensor        # int32 [B] on device
+    chained: bool = False    # resid was written by the previous layer call on the same workspace
 
     def c(self) -> LayerStateC:
         B = self.resid.shape[0]
         return LayerStateC(_ptr(self.resid), _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.pos),
-                           self.k_cache.shape[2], B)
+                           self.k_cache.shape[2], B, int(self.chained))
 
 
 TAP_NAMES = [f[0] for f in LayerTapsC._fields_]

@@ -205,3 +205,55 @@ def test_fold_p4(d, cols, side):
     # invariance (P4): (x Q^T-side) through the folded weight reproduces the original map
     x = np.random.default_rng(0).standard_normal(ref.shape[0])
     assert np.linalg.norm(x @ gv - x @ ref) <= 3e-3 * np.linalg.norm(x @ ref)
+
+
+# ------------------------------------------------------------------------------------ fused Top-K + GEMV
+def _fused_ref(x, k, Wb, eps, bias=None):
+    """Oracle: exact Top-K (Z10) of x, RMS scale, masked GEMV, all fp64 (O-5..O-7)."""
+    xd = x.numpy().astype(np.float64)
+    idx = O.topk(xd, k)
+    s = O.rms_scale(xd, eps) if eps >= 0 else 1.0
+    return O.sparse_gemv(w64(Wb), idx, xd[idx] * s, w64(bias) if bias is not None else None)
+
+
+@pytest.mark.parametrize("d_in,d_out,k,eps", [(64, 128, 32, -1.0), (64, 128, 0, -1.0), (64, 128, 64, 1e-5),
+                                              (1000, 1000, 333, 1e-5), (4096, 12288, 2048, 1e-5),
+                                              (4096, 4096, 1638, -1.0), (11008, 4096, 5504, -1.0),
+                                              (14336, 4096, 8602, -1.0), (29568, 1024, 14784, -1.0)])
+def test_topk_sparse_gemv_select_p3(d_in, d_out, k, eps):
+    """SELECT prologue (every CTA derives the exact rule) + balanced split + EPI_STORE."""
+    x = synth.residual_activation(1, d_in, seed=d_in + k)[0]
+    Wb = synth.gaussian_bf16((d_in, d_out), 40 + d_in, d_in ** -0.5)
+    bias = synth.gaussian_bf16((d_out,), 41, 0.02) if d_out == 12288 else None
+    y = LZ.topk_sparse_gemv(x.to(DEV), k, Wb.to(DEV), rms_eps=eps, bias=bias.to(DEV) if bias is not None else None)
+    ref = _fused_ref(x, k, Wb, eps, bias)
+    assert rel_max(f64(y), ref) <= 1e-5
+
+
+def test_topk_sparse_gemv_select_ties_zeros_constant():
+    """Exact |x| ties across the k-th position, zeros, -0 and constant vectors: the fused
+    selection must equal the oracle's lower-index tie-break (Z10, Z11) -- checked through a
+    GEMV whose rows identify the kept set (W = distinct powers of two per row block)."""
+    g = torch.Generator().manual_seed(5)
+    cases = []
+    for d in (64, 1000, 4096, 11008):
+        xi = torch.randint(-4, 5, (d,), generator=g).float()
+        xi[xi == 0] = -0.0 if d % 3 else 0.0
+        cases += [(xi, k) for k in (1, d // 3, d // 2, d - 1)]
+        cases.append((torch.full((d,), 0.5), d // 4))
+    for x, k in cases:
+        d = x.numel()
+        # y[o] = sum over kept j of x_j * W[j][o]; W random -> distinct kept sets give distinct y
+        Wb = synth.gaussian_bf16((d, 256), 7 + d, 1.0)
+        y = LZ.topk_sparse_gemv(x.to(DEV), k, Wb.to(DEV))
+        ref = _fused_ref(x, k, Wb, -1.0)
+        assert rel_max(f64(y), ref) <= 1e-5, (d, k)
+
+
+def test_topk_sparse_gemv_repeatable():
+    """Bit-identical across calls (fixed-point accumulation, deterministic selection)."""
+    x = synth.residual_activation(1, 4096, seed=3)[0].to(DEV)
+    Wb = synth.gaussian_bf16((4096, 4096), 4, 4096 ** -0.5).to(DEV)
+    y0 = LZ.topk_sparse_gemv(x, 2048, Wb, rms_eps=1e-5).clone()
+    for _ in range(3):
+        assert torch.equal(LZ.topk_sparse_gemv(x, 2048, Wb, rms_eps=1e-5), y0)

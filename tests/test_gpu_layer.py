@@ -176,3 +176,24 @@ def test_layer_p0_equals_original_dense_layer(shape):
         got = f64(st.resid[b])
         err = np.linalg.norm(got - ref @ qn) / np.linalg.norm(ref)
         assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("shape,p", [(SMALL, 0.5), (synth.MODELS["llama2-7b"], 0.5)])
+def test_layer_chained_equals_prepared(shape, p):
+    """Batch 1: a layer whose h1 histogram / RMS partials come from the previous layer's
+    adapter epilogue (chained) gives bit-identical results to the same layer run with the
+    standalone preparation kernel on the same residual."""
+    batch, ctx, max_ctx = 1, 20, 32
+    _, _, _, lw1, plan, resid, kc0, vc0, pos = build(shape, 11, batch, ctx, max_ctx, p)
+    _, _, _, lw2, _, _, _, _, _ = build(shape, 12, batch, ctx, max_ctx, p)
+    ws = torch.zeros(LZ.layer_workspace_size(lw1, 1, max_ctx), dtype=torch.uint8, device=DEV)
+    kv = [(kc0.clone().to(DEV), vc0.clone().to(DEV)) for _ in range(4)]
+    r = resid.clone().to(DEV)
+    LZ.sparse_layer(lw1, plan, LZ.LayerState(r, *kv[0], pos.to(DEV)), ws=ws)
+    r_mid = r.clone()
+    LZ.sparse_layer(lw2, plan, LZ.LayerState(r, *kv[1], pos.to(DEV), chained=True), ws=ws)
+    r2 = r_mid.clone()
+    LZ.sparse_layer(lw2, plan, LZ.LayerState(r2, *kv[2], pos.to(DEV), chained=False), ws=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(r, r2)
+    assert torch.equal(kv[1][0], kv[2][0])

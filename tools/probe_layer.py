@@ -22,7 +22,7 @@ pos = torch.full((1,), ctx - 1, dtype=torch.int32, device=dev)
 resid = synth.residual_activation(1, shape.d, 5).to(dev)
 plan = M.site_plan(shape, p)
 torch.cuda.synchronize()
-for _ in range(6):
-    LZ.sparse_layer(lw, plan, LZ.LayerState(resid, kc, vc, pos))
+for i in range(6):
+    LZ.sparse_layer(lw, plan, LZ.LayerState(resid, kc, vc, pos, chained=i > 0))
 torch.cuda.synchronize()
 print("probe ok")
