@@ -570,9 +570,93 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
 }
 
 // ============================================================================== fold
+namespace {
+using PFN_encodeTiled_t = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_t tensor_map_encoder() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    }
+    return fn;
+}
+// K-major bf16 matrix [rows][K]: boxes of 64 (K) x box_rows, 128-byte swizzle
+bool make_kmajor_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows) {
+    PFN_encodeTiled_t enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kFoldBK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+int fold_bn(int64_t n) { return n % 256 == 0 ? 256 : (n % 128 == 0 ? 128 : 0); }
+// output [rows][cols] = M x N; K = d (rows for LEFT, cols for RIGHT)
+bool fold_tc_supported(int64_t rows, int64_t cols, bool left) {
+    const int64_t K = left ? rows : cols;
+    return rows % kFoldBM == 0 && fold_bn(cols) != 0 && K % kFoldBK == 0 && env_int("LAROSA_FOLD_SIMT", 0) == 0;
+}
+size_t fold_ws_bytes(int64_t rows, int64_t cols, bool left) {
+    if (!fold_tc_supported(rows, cols, left)) return 256;
+    const int64_t d = left ? rows : cols;
+    return (size_t)2 * d * d * 2 + (left ? (size_t)cols * rows * 2 : 0) + 1024;
+}
+
+template <int BN, bool AS, bool BS>
+cudaError_t launch_fold_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+                           uint16_t* out, int M, int N, int K, cudaStream_t st) {
+    auto kern = fold_tc_kernel<BN, AS, BS>;
+    constexpr int smem = fold_smem_bytes<BN, AS, BS>();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<dim3(N / BN, M / kFoldBM), kFoldThreads, smem, st>>>(a0, a1, b0, b1, out, N, K);
+    return cudaGetLastError();
+}
+
+// LEFT : out[d][cols]  = (Q diag gamma)^T W      A = split((Q diag gamma)^T) [d][d], B = W^T [cols][d]
+// RIGHT: out[rows][d]  = W Q                     A = W [rows][d],                B = split(Q^T) [d][d]
+cudaError_t fold_tc_run(const float* Q, const float* gamma, const uint16_t* W, uint16_t* out, int64_t rows,
+                        int64_t cols, bool left, void* ws, cudaStream_t st) {
+    const int64_t d = left ? rows : cols;
+    uint16_t* s_hi = static_cast<uint16_t*>(ws);
+    uint16_t* s_lo = s_hi + (size_t)d * d;
+    const dim3 tb(32, 8), tg((unsigned)((d + 31) / 32), (unsigned)((d + 31) / 32));
+    split_transpose_kernel<<<tg, tb, 0, st>>>(Q, left ? gamma : nullptr, s_hi, s_lo, (int)d, (int)d);
+    CUtensorMap a0, a1, b0, b1;
+    const int M = (int)rows, N = (int)cols, K = (int)d;
+    const int bn = fold_bn(N);
+    if (left) {
+        uint16_t* wt = s_lo + (size_t)d * d;
+        transpose_bf16_kernel<<<dim3((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32)), tb, 0, st>>>(
+            W, wt, (int)rows, (int)cols);
+        if (!make_kmajor_map(&a0, s_hi, M, K, kFoldBM) || !make_kmajor_map(&a1, s_lo, M, K, kFoldBM) ||
+            !make_kmajor_map(&b0, wt, N, K, bn))
+            return cudaErrorInvalidValue;
+        b1 = b0;
+        return bn == 256 ? launch_fold_tc<256, true, false>(a0, a1, b0, b1, out, M, N, K, st)
+                         : launch_fold_tc<128, true, false>(a0, a1, b0, b1, out, M, N, K, st);
+    }
+    if (!make_kmajor_map(&a0, W, M, K, kFoldBM) || !make_kmajor_map(&b0, s_hi, N, K, bn) ||
+        !make_kmajor_map(&b1, s_lo, N, K, bn))
+        return cudaErrorInvalidValue;
+    a1 = a0;
+    return bn == 256 ? launch_fold_tc<256, false, true>(a0, a1, b0, b1, out, M, N, K, st)
+                     : launch_fold_tc<128, false, true>(a0, a1, b0, b1, out, M, N, K, st);
+}
+}  // namespace
+
 extern "C" size_t larosa_fold_workspace_size(int64_t rows, int64_t cols, int side) {
     if (rows <= 0 || cols <= 0) return 0;
-    return fold_tc_workspace_bytes(rows, cols, side == LAROSA_LEFT_QT);
+    return fold_ws_bytes(rows, cols, side == LAROSA_LEFT_QT);
 }
 
 extern "C" larosa_status larosa_fold_rotation(const float* Q, const float* gamma, const uint16_t* W, uint16_t* Wout,
@@ -585,19 +669,19 @@ extern "C" larosa_status larosa_fold_rotation(const float* Q, const float* gamma
     if ((const void*)W == (const void*)Wout) return fail(LAROSA_EINVAL, "fold: Wout aliases W");
     if (rows % 64 || cols % 64) return fail(LAROSA_EUNSUPPORTED, "fold: rows and cols must be multiples of 64");
     if (rows > INT32_MAX / 2 || cols > INT32_MAX / 2) return fail(LAROSA_EUNSUPPORTED, "fold: dims too large");
+    if (!aligned16(W) || !aligned16(Wout)) return fail(LAROSA_EINVAL, "fold: W, Wout must be 16-byte aligned");
+    const bool left = side == LAROSA_LEFT_QT;
     const size_t need = larosa_fold_workspace_size(rows, cols, side);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "fold: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const char* simt = getenv("LAROSA_FOLD_SIMT");
-    if (simt && simt[0] == '1') {
-        const bool left = side == LAROSA_LEFT_QT;
-        const int M = (int)rows, N = (int)cols, K = left ? (int)rows : (int)cols;
-        dim3 grid((N + 63) / 64, (M + 63) / 64);
-        if (left)
-            return cuda_check(launch(fold_simt_kernel<true>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
-        return cuda_check(launch(fold_simt_kernel<false>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
-    }
-    return cuda_check(fold_tc_run(Q, gamma, W, Wout, rows, cols, side == LAROSA_LEFT_QT, ws, st), "fold (tcgen05)");
+    if (fold_tc_supported(rows, cols, left))
+        return cuda_check(fold_tc_run(Q, gamma, W, Wout, rows, cols, left, ws, st), "fold (tcgen05)");
+    // CUDA-core fp32 kernel: shapes without full 128 x 128 tiles (toy layers), or LAROSA_FOLD_SIMT=1
+    const int M = (int)rows, N = (int)cols, K = left ? (int)rows : (int)cols;
+    dim3 grid((N + 63) / 64, (M + 63) / 64);
+    if (left)
+        return cuda_check(launch(fold_simt_kernel<true>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
+    return cuda_check(launch(fold_simt_kernel<false>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
 }
 
 extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t* Wu, uint16_t* Wgu, int64_t d,

@@ -173,8 +173,11 @@ def test_sparse_gemv_theorem_a1_statistics():
 
 # ------------------------------------------------------------------------------------ fold
 @pytest.mark.parametrize("d,cols,side", [(64, 128, 0), (256, 512, 0), (256, 192, 1), (1024, 1024, 0),
-                                         (1024, 2048, 1), (4096, 4096, 0)])
+                                         (1024, 2048, 1), (4096, 4096, 0), (512, 384, 0), (384, 256, 1),
+                                         (2048, 1280, 1)])
 def test_fold_p4(d, cols, side):
+    """Shapes with 128-row / 128-column tiles run the tcgen05 kernel (TMA + TMEM), the others
+    the CUDA-core kernel; both must meet the same P4 bound."""
     q = synth.haar_orthogonal(d, seed=d + side)
     gamma = (1 + 0.1 * synth.gaussian((d,), seed=3)) if side == 0 else None
     if side == 0:
