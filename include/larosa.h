@@ -168,6 +168,24 @@ larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, f
 larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info);
 
 /* ------------------------------------------------------------------------------
+ * Decode-step ends (Q_0 is merged into the embedding, Q_L into
+ * the head; the head is dense, the paper does not sparsify it).
+ * larosa_embed: resid[b][:] = E'[tokens[b]][:] as fp32, E' = E Q_0 bf16 [vocab][d];
+ *   tokens int32 [batch] in [0, vocab) (not checked on device).
+ * larosa_lm_head: logits[b] = (r_b s_b) H' with s_b = 1/sqrt(mean(r_b^2) + rms_eps) (final
+ *   RMSNorm; its gain is folded into H' = Q_L^T diag(gamma_f) H, LEFT fold), dense GEMV over
+ *   H' bf16 [d][vocab] (fixed-point accumulation, fp32 out); next_token[b] = arg-max of
+ *   logits[b], the lowest index on exact ties.  logits may be NULL (workspace scratch).
+ *   vocab % 8 == 0, d % 8 == 0, batch <= 16.
+ * ------------------------------------------------------------------------------ */
+larosa_status larosa_embed(const uint16_t* E, int64_t vocab, int64_t d, const int32_t* tokens, int32_t batch,
+                           float* resid, larosa_stream_t stream);
+size_t larosa_lm_head_workspace_size(int32_t batch, int64_t d, int64_t vocab);
+larosa_status larosa_lm_head(const float* resid, int32_t batch, int64_t d, const uint16_t* H, int64_t vocab,
+                             float rms_eps, float* logits, int32_t* next_token, void* ws, size_t ws_bytes,
+                             larosa_stream_t stream);
+
+/* ------------------------------------------------------------------------------
  * One LaRoSA decoder layer on pre-folded weights (Fig. 2; §8(a) a6):
  *   r (residual, Q_l basis) -> h1: Top-K k_h1 of r, RMS scale -> sparse GEMV W_qkv
  *   (+bias, RoPE, append k/v at pos) -> GQA decode attention -> h2: Top-K k_h2 ->

@@ -29,7 +29,7 @@ __all__ = [
     "topk_mask", "sparse_gemv", "dense_gemv", "compute_k", "solve_alpha", "site_ks",
     "std_normal_pdf", "std_normal_cdf", "std_normal_inv_cdf", "theory_relative_error",
     "rope", "decode_attention", "silu", "rmsnorm", "dense_block", "larosa_block",
-    "actual_sparsity",
+    "actual_sparsity", "embed", "lm_head", "greedy", "larosa_decode_step",
 ]
 
 
@@ -436,3 +436,41 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
     if adapter is not None:
         r = rotate(r, adapter)
     return r, out
+
+
+# ----------------------------------------------------------------------------------
+# decode step: embedding -> L LaRoSA layers -> final RMS -> LM head
+# ----------------------------------------------------------------------------------
+def embed(e_folded, token: int) -> np.ndarray:
+    """The residual stream enters layer 0 in Q_0's basis: r_0 = e_token Q_0, i.e. the row
+    of the folded embedding E' = E Q_0 ("Q_0 ... merged into the embedding")."""
+    return np.asarray(e_folded, dtype=np.float64)[int(token)].copy()
+
+
+def lm_head(r, h_folded, eps: float) -> np.ndarray:
+    """logits = RMSNorm(r_L) H with r_L in Q_L's basis and the final RMSNorm gain and Q_L
+    folded into the head, H' = Q_L^T diag(gamma_f) H (Z6 for the gain): since Q_L
+    is orthogonal, RMSNorm commutes with it and only the scale s remains:
+    logits = (r s) H'.  The head is dense (the paper does not sparsify it)."""
+    r = np.asarray(r, dtype=np.float64)
+    return dense_gemv(h_folded, r * rms_scale(r, eps))
+
+
+def greedy(logits) -> int:
+    """Greedy decoding: the arg-max logit, the lowest index on exact ties."""
+    logits = np.asarray(logits, dtype=np.float64)
+    return int(np.flatnonzero(logits == logits.max())[0])
+
+
+def larosa_decode_step(token: int, e_folded, layers, cfg, ks, caches, pos: int, h_folded, eps: float,
+                       kv_bf16: bool = False):
+    """One decode token through the whole model (a7): r = embed; for each layer,
+    larosa_block (its own adapter A_l into the next layer's basis; the last layer's adapter
+    is None when the head holds Q_L); logits = lm_head(r); next token = greedy(logits).
+    ``layers``: list of (wf, adapter) pairs; ``caches``: list of (k_cache, v_cache),
+    updated at ``pos``.  Returns (next_token, logits, final residual)."""
+    r = embed(e_folded, token)
+    for (wf, adapter), (kc, vc) in zip(layers, caches):
+        r, _ = larosa_block(r, wf, cfg, ks, kc, vc, pos, adapter=adapter, kv_bf16=kv_bf16)
+    logits = lm_head(r, h_folded, eps)
+    return greedy(logits), logits, r

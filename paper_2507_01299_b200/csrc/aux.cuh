@@ -111,6 +111,71 @@ __global__ void __launch_bounds__(kUnionThreads) union_kernel(const uint32_t* __
 }
 
 // ------------------------------------------------------------------------------------------
+// Decode-step glue.
+// resid[b][i] = E'[tokens[b]][i]  (the folded embedding E' = E Q_0, bf16 -> fp32)
+// ------------------------------------------------------------------------------------------
+__global__ void embed_kernel(const uint16_t* __restrict__ E, const int32_t* __restrict__ tokens, int d,
+                             float* __restrict__ resid) {
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.y;
+    const uint16_t* row = E + (size_t)tokens[b] * d;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        resid[(size_t)b * d + i] = bf16f(row[i]);
+}
+
+// xs[b][i] = x[b][i] * s_b,  s_b = 1 / sqrt(mean_i x[b][i]^2 + eps)   (one CTA per token,
+// fixed-order reduction; the final RMSNorm whose gain is folded into the head)
+constexpr int kRowThreads = 1024;
+__global__ void __launch_bounds__(kRowThreads) rms_rows_kernel(const float* __restrict__ x, int d, float eps,
+                                                               float* __restrict__ xs) {
+    __shared__ float sw[32];
+    pdl_wait();
+    pdl_trigger();
+    const float* xr = x + (size_t)blockIdx.x * d;
+    float ssq = 0.f;
+    for (int i = threadIdx.x; i < d; i += kRowThreads) ssq = fmaf(xr[i], xr[i], ssq);
+    const float tot = block_sum<kRowThreads>(ssq, sw);
+    const float s = 1.0f / sqrtf(tot / (float)d + eps);
+    for (int i = threadIdx.x; i < d; i += kRowThreads) xs[(size_t)blockIdx.x * d + i] = xr[i] * s;
+}
+
+// out[b] = argmax_i logits[b][i], the lowest index on exact ties (greedy decoding)
+__device__ __forceinline__ void argmax_merge(float& v, int& i, float v2, int i2) {
+    if (v2 > v || (v2 == v && i2 < i)) {
+        v = v2;
+        i = i2;
+    }
+}
+__global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* __restrict__ logits, int64_t ld, int n,
+                                                             int32_t* __restrict__ out) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    pdl_wait();
+    pdl_trigger();
+    const float* row = logits + (size_t)blockIdx.x * ld;
+    float v = -INFINITY;
+    int idx = 0x7fffffff;
+    for (int i = threadIdx.x; i < n; i += kRowThreads) argmax_merge(v, idx, row[i], i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+        argmax_merge(v, idx, v2, i2);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        sv[wid] = v;
+        si[wid] = idx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kRowThreads / 32; ++w) argmax_merge(v, idx, sv[w], si[w]);
+        out[blockIdx.x] = idx;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // Wgu[r][t*2B + j] = j < B ? Wg[r][t*B + j] : Wu[r][t*B + j - B]   (B = kGuBlock)
 // ------------------------------------------------------------------------------------------
 __global__ void pack_gate_up_kernel(const uint16_t* __restrict__ wg, const uint16_t* __restrict__ wu,

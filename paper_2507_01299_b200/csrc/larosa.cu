@@ -695,6 +695,78 @@ extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t*
     return cuda_check(launch(pack_gate_up_kernel, dim3(grid), dim3(256), 0, st, Wg, Wu, Wgu, d, inter), "pack_gate_up");
 }
 
+// ============================================================================== decode-step ends
+extern "C" larosa_status larosa_embed(const uint16_t* E, int64_t vocab, int64_t d, const int32_t* tokens,
+                                      int32_t batch, float* resid, larosa_stream_t stream) {
+    if (!E || !tokens || !resid) return fail(LAROSA_EINVAL, "embed: NULL pointer");
+    if (vocab <= 0 || d <= 0 || batch < 1) return fail(LAROSA_EINVAL, "embed: bad sizes");
+    if (batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "embed: batch > %d", LAROSA_MAX_BATCH);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return cuda_check(launch(embed_kernel, dim3((unsigned)((d + 1023) / 1024), batch), dim3(1024), 0, st, E, tokens,
+                             (int)d, resid),
+                      "embed launch");
+}
+
+static void carve_lm_head(Carver& c, int32_t batch, int64_t d, int64_t vocab, unsigned long long** acc, float** xs,
+                          float** logits) {
+    unsigned long long* a = c.take<unsigned long long>((size_t)batch * vocab);
+    float* x = c.take<float>((size_t)batch * d);
+    float* l = c.take<float>((size_t)batch * vocab);
+    if (acc) *acc = a;
+    if (xs) *xs = x;
+    if (logits) *logits = l;
+}
+
+extern "C" size_t larosa_lm_head_workspace_size(int32_t batch, int64_t d, int64_t vocab) {
+    if (batch < 1 || d <= 0 || vocab <= 0) return 0;
+    Carver c(nullptr);
+    carve_lm_head(c, batch, d, vocab, nullptr, nullptr, nullptr);
+    return c.size();
+}
+
+extern "C" larosa_status larosa_lm_head(const float* resid, int32_t batch, int64_t d, const uint16_t* H, int64_t vocab,
+                                        float rms_eps, float* logits, int32_t* next_token, void* ws, size_t ws_bytes,
+                                        larosa_stream_t stream) {
+    if (!resid || !H || !next_token) return fail(LAROSA_EINVAL, "lm_head: NULL pointer");
+    if (batch < 1 || d <= 0 || vocab <= 0) return fail(LAROSA_EINVAL, "lm_head: bad sizes");
+    if (batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "lm_head: batch > %d", LAROSA_MAX_BATCH);
+    if (vocab % 8 || d % 8) return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab and d must be multiples of 8");
+    if ((vocab + kSliceCols - 1) / kSliceCols > (int64_t)(kCounterHeaderWords - kGemvTicketBase))
+        return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab too large");
+    if (!aligned16(H) || (logits && !aligned16(logits))) return fail(LAROSA_EINVAL, "lm_head: H, logits must be 16-byte aligned");
+    const size_t need = larosa_lm_head_workspace_size(batch, d, vocab);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "lm_head: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Carver c(ws);
+    unsigned long long* acc;
+    float *xs, *lg;
+    carve_lm_head(c, batch, d, vocab, &acc, &xs, &lg);
+    if (!logits) logits = lg;
+    LAROSA_TRY(cuda_check(launch(rms_rows_kernel, dim3(batch), dim3(kRowThreads), 0, st, resid, (int)d, rms_eps, xs),
+                          "rms launch"));
+    const int bp = pad_batch(batch);
+    const GemvPlan p = plan_gemv(vocab, d, bp, GEMV_DENSE, d);
+    GemvArgs a = gemv_args_base();
+    a.W = H;
+    a.ld = vocab;
+    a.d_out = (int)vocab;
+    a.mode = GEMV_DENSE;
+    a.x = xs;
+    a.ldx = d;
+    a.d_in = (int)d;
+    a.batch = batch;
+    a.acc = acc;
+    a.acc_ld = vocab;
+    a.epi = EPI_STORE;
+    a.tickets = c.counters(kGemvTicketBase);
+    a.out = logits;
+    a.out_ld = vocab;
+    LAROSA_TRY(launch_gemv(a, p, bp, st));
+    return cuda_check(launch(argmax_kernel, dim3(batch), dim3(kRowThreads), 0, st, (const float*)logits, vocab,
+                             (int)vocab, next_token),
+                      "argmax launch");
+}
+
 // ============================================================================== decoder layer
 namespace {
 struct LayerWs {

@@ -89,6 +89,10 @@ def lib() -> ctypes.CDLL:
     L.larosa_topk_sparse_gemv_workspace_size.argtypes = [_c_i64, _c_i64]
     L.larosa_topk_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp, _vp,
                                           ctypes.c_size_t, _vp]
+    L.larosa_embed.argtypes = [_vp, _c_i64, _c_i64, _vp, _c_i32, _vp, _vp]
+    L.larosa_lm_head_workspace_size.restype = ctypes.c_size_t
+    L.larosa_lm_head_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64]
+    L.larosa_lm_head.argtypes = [_vp, _c_i32, _c_i64, _vp, _c_i64, ctypes.c_float, _vp, _vp, _vp, ctypes.c_size_t, _vp]
     L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
     L.larosa_debug_set_layer_phases.restype = None
     L.larosa_gemv_plan_info.argtypes = [_c_i64, _c_i64, _c_i32, ctypes.POINTER(_c_i32)]
@@ -99,7 +103,8 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(LayerStateC), ctypes.POINTER(LayerTapsC), _vp,
                                       ctypes.c_size_t, _vp]
     for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
-                 "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer"):
+                 "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
+                 "larosa_embed", "larosa_lm_head"):
         getattr(L, name).restype = ctypes.c_int
     if L.larosa_abi_version() != 1:
         raise RuntimeError("liblarosa ABI version mismatch")
@@ -243,6 +248,32 @@ def topk_sparse_gemv(x: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = 
     _check(L.larosa_topk_sparse_gemv(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), d_out, ld, _ptr(bias), _ptr(y),
                                      _ptr(ws), ws.numel(), _stream(stream)))
     return y
+
+
+def embed(E: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """resid[b] = E'[tokens[b]] (E' = E Q_0, bf16 bits [vocab, d]; tokens int32 [B] on device)."""
+    vocab, d = E.shape
+    B = tokens.numel()
+    out = out if out is not None else torch.empty((B, d), dtype=torch.float32, device=E.device)
+    _check(lib().larosa_embed(_ptr(E), vocab, d, _ptr(tokens), B, _ptr(out), _stream(stream)))
+    return out
+
+
+def lm_head(resid: torch.Tensor, H: torch.Tensor, rms_eps: float, logits: Optional[torch.Tensor] = None,
+            next_token: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, stream=None):
+    """Final RMS scale + dense head GEMV (H' bf16 bits [d, vocab]) + greedy arg-max.
+    Returns (next_token int32 [B], logits fp32 [B, vocab] or None)."""
+    B, d = resid.shape
+    vocab = H.shape[1]
+    dev = resid.device
+    nt = next_token if next_token is not None else torch.empty((B,), dtype=torch.int32, device=dev)
+    L = lib()
+    nb = L.larosa_lm_head_workspace_size(B, d, vocab)
+    if ws is None:
+        ws = _ws(("lm_head", B, d, vocab), nb, dev)
+    _check(L.larosa_lm_head(_ptr(resid), B, d, _ptr(H), vocab, float(rms_eps), _ptr(logits), _ptr(nt), _ptr(ws),
+                            ws.numel(), _stream(stream)))
+    return nt, logits
 
 
 @dataclass

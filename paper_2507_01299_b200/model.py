@@ -1,6 +1,6 @@
 """Model assembly for the LaRoSA decode path: synthetic random-init layers of the paper's
 model shapes, folded with the library's own fold (SURVEY §3.1 offline transform), and a
-multi-layer decode stack driven through ``larosa_sparse_layer``.
+whole-model decode runner (embedding -> layers -> LM head) driven through the C ABI.
 
 Everything computed here runs in liblarosa kernels; torch only allocates, draws the
 seeded random weights (synth) and moves tensors.
@@ -84,21 +84,71 @@ def site_plan(shape: synth.ModelShape, p: float, alpha_mode: str = "uniform") ->
             LZ.compute_k(a[3], p, shape.inter))
 
 
-class DecodeStack:
-    """A stack of folded LaRoSA layers sharing one workspace; ``step`` runs one decode
-    token (batch B) through all layers with larosa_sparse_layer."""
+@dataclass
+class DecodeModel:
+    """A whole LaRoSA model for decoding: folded embedding E' = E Q_0,
+    L folded layers (layer l's adapter A_l = Q_l^T Q_{l+1}; the last layer has none), and the
+    folded head H' = Q_{L-1}^T diag(gamma_f) H."""
+    shape: synth.ModelShape
+    embed: torch.Tensor            # bf16 bits [vocab, d]
+    layers: List[LZ.LayerWeights]
+    head: torch.Tensor             # bf16 bits [d, vocab]
 
-    def __init__(self, layers: List[LZ.LayerWeights], batch: int, max_ctx: int, device):
-        self.layers = layers
+
+def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int = 0,
+                       vocab: Optional[int] = None) -> DecodeModel:
+    """Random-init model of the given shape (synthetic weights), folded with
+    the library's own tensor-core fold."""
+    vocab = vocab or shape.vocab
+    d = shape.d
+    qs = [synth.haar_orthogonal(d, 7000 + 100 * seed + l, device=device, dtype=torch.float32)
+          for l in range(n_layers)]
+    E = synth.gaussian_bf16((vocab, d), 9000 + seed, 1.0, device)
+    e_f = LZ.fold_rotation(qs[0], E, LZ.LAROSA_RIGHT_Q)
+    del E
+    layers = []
+    for l in range(n_layers):
+        orig = synth_original_layer(shape, 10 * seed + l + 1, device=device)
+        layers.append(fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None))
+        del orig
+    H = synth.gaussian_bf16((d, vocab), 9100 + seed, d ** -0.5, device)
+    gf = (1.0 + 0.1 * synth.gaussian((d,), 9200 + seed, device=device)).float().contiguous()
+    h_f = LZ.fold_rotation(qs[-1], H, LZ.LAROSA_LEFT_QT, gamma=gf)
+    del H
+    return DecodeModel(shape=shape, embed=e_f, layers=layers, head=h_f)
+
+
+class DecodeRunner:
+    """Runs decode steps of a DecodeModel through the C ABI: embed -> larosa_sparse_layer per
+    layer (batch 1: layers after the first reuse the previous layer's selection data) ->
+    larosa_lm_head (greedy).  All buffers are preallocated so a step is CUDA-graph capturable."""
+
+    def __init__(self, model: DecodeModel, batch: int, max_ctx: int, device):
+        self.m = model
         self.batch = batch
         self.max_ctx = max_ctx
-        w0 = layers[0]
+        s = model.shape
+        w0 = model.layers[0]
         self.ws = torch.zeros(LZ.layer_workspace_size(w0, batch, max_ctx), dtype=torch.uint8, device=device)
         self.kv = [(torch.zeros((batch, w.n_kv_heads, max_ctx, w.head_dim), dtype=torch.int16, device=device),
                     torch.zeros((batch, w.n_kv_heads, max_ctx, w.head_dim), dtype=torch.int16, device=device))
-                   for w in layers]
+                   for w in model.layers]
+        self.resid = torch.zeros((batch, s.d), dtype=torch.float32, device=device)
+        self.tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.next_tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.pos = torch.zeros((batch,), dtype=torch.int32, device=device)
+        vocab = model.head.shape[1]
+        self.logits = torch.zeros((batch, vocab), dtype=torch.float32, device=device)
+        self.head_ws = torch.zeros(LZ.lib().larosa_lm_head_workspace_size(batch, s.d, vocab), dtype=torch.uint8,
+                                   device=device)
 
-    def step(self, resid: torch.Tensor, pos: torch.Tensor, plan: Sequence[int], stream=None):
-        for w, (kc, vc) in zip(self.layers, self.kv):
-            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos), ws=self.ws, stream=stream)
-        return resid
+    def step(self, plan: Sequence[int], taps: Optional[List[dict]] = None, stream=None):
+        """One token for every sequence: reads self.tokens / self.pos, writes self.next_tokens
+        and self.logits (and the KV caches at pos)."""
+        LZ.embed(self.m.embed, self.tokens, out=self.resid, stream=stream)
+        for l, (w, (kc, vc)) in enumerate(zip(self.m.layers, self.kv)):
+            st = LZ.LayerState(self.resid, kc, vc, self.pos, chained=l > 0)
+            LZ.sparse_layer(w, plan, st, taps=taps[l] if taps else None, ws=self.ws, stream=stream)
+        LZ.lm_head(self.resid, self.m.head, self.m.shape.rms_eps, logits=self.logits, next_token=self.next_tokens,
+                   ws=self.head_ws, stream=stream)
+        return self.next_tokens

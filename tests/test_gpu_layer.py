@@ -67,7 +67,8 @@ def run_layer(lw, plan, resid, kc, vc, pos):
 
 
 @pytest.mark.parametrize("shape,batch,ctx,p", [(SMALL, 1, 7, 0.5), (SMALL, 3, 40, 0.4), (SMALL_MHA, 2, 100, 0.25),
-                                               (synth.MODELS["llama2-7b"], 1, 256, 0.5)])
+                                               (SMALL, 16, 30, 0.5), (synth.MODELS["llama2-7b"], 1, 256, 0.5),
+                                               (synth.MODELS["llama3-8b"], 4, 64, 0.4)])
 def test_layer_p6_sitewise(shape, batch, ctx, p):
     max_ctx = max(ctx, 64)
     orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p)

@@ -440,3 +440,44 @@ def test_block_exact_sparsity_and_monotone_error():
     means = [np.mean(errs[p]) for p in sorted(errs)]
     assert means[0] < 1e-12
     assert all(a <= b for a, b in zip(means, means[1:])), means
+
+
+def test_greedy_lowest_index_on_ties():
+    assert O.greedy([1.0, 3.0, 3.0, 2.0]) == 1
+    assert O.greedy([-5.0, -1.0, -1.0]) == 1
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        v = rng.integers(-3, 4, 17).astype(np.float64)
+        best = max(range(17), key=lambda i: (v[i], -i))        # brute force: max value, lowest index
+        assert O.greedy(v) == best
+
+
+def test_decode_step_p0_equals_dense_model():
+    """a7 end to end at k = D: embedding E' = E Q_0, two folded layers
+    (adapter A_0 = Q_0^T Q_1, the last layer's basis folded into the head
+    H' = Q_1^T diag(gamma_f) H) reproduce the dense model's logits within 1e-10 relative and
+    pick the same greedy token."""
+    d, ctx, vocab = 64, 6, 50
+    layers = [_toy_layer(500 + l) for l in range(2)]
+    cfg = layers[0][1]
+    qs = [synth.haar_orthogonal(d, 600 + l).numpy() for l in range(2)]
+    rng = np.random.default_rng(11)
+    E = rng.standard_normal((vocab, d))
+    H = rng.standard_normal((d, vocab)) / math.sqrt(d)
+    gf = 1 + 0.1 * rng.standard_normal(d)
+    caches_d = [[rng.standard_normal((2, ctx, 16)) for _ in range(2)] for _ in range(2)]
+    caches_r = [[c.copy() for c in cc] for cc in caches_d]
+    pos, tok = ctx - 1, 17
+    # dense reference
+    r = E[tok].copy()
+    for l in range(2):
+        r, _ = O.dense_block(r, layers[l][0], cfg, caches_d[l][0], caches_d[l][1], pos)
+    ref_logits = O.dense_gemv(H, O.rmsnorm(r, gf, cfg["eps"]))
+    # LaRoSA model on folded weights
+    folded = [(_fold_layer(layers[0][0], qs[0]), O.residual_adapter(qs[0], qs[1])),
+              (_fold_layer(layers[1][0], qs[1]), None)]
+    e_f = E @ qs[0]
+    h_f = O.fold_left_qt(qs[1], H, gf)
+    nxt, logits, _ = O.larosa_decode_step(tok, e_f, folded, cfg, (d, d, d, 128), caches_r, pos, h_f, cfg["eps"])
+    assert np.linalg.norm(logits - ref_logits) <= 1e-10 * np.linalg.norm(ref_logits)
+    assert nxt == int(np.argmax(ref_logits))
