@@ -274,6 +274,88 @@ def run_steps(graphs, k, start):
         graphs[(start + i) % len(graphs)].replay()
 
 
+def run_sharded(args):
+    """LLaMA3-70B layer (d 8192, MLP 28672, GQA 64/8) row-sharded over the WORLD_SIZE ranks,
+    batch 1, p = args.p: per layer the 5 library phases of larosa_sparse_layer_shard_phase,
+    each followed by torch.distributed.all_gather_into_tensor (NCCL over NVLink), the whole
+    step captured in one CUDA graph per layer copy.  value = layer tokens/s (strong scaling:
+    the same layer work split over the ranks); max over ranks of the CUDA-event time."""
+    import torch.distributed as dist
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    ws_n, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = f"cuda:{local}"
+    if ws_n > 1:
+        dist.init_process_group("nccl", device_id=torch.device(device))
+    shape = synth.MODELS["llama3-70b"]
+    n_copies, max_ctx = 4, 256
+    qs = [synth.haar_orthogonal(shape.d, 300 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
+    shards, kvs = [], []
+    for i in range(n_copies):
+        full = M.fold_layer(M.synth_original_layer(shape, 50 + i, device=device), shape, qs[i], qs[i + 1])
+        shards.append(M.ShardedLayer(M.shard_layer(full, rank, ws_n), rank, ws_n, max_ctx, device))
+        del full
+        torch.cuda.empty_cache()
+        hk = shape.hkv // ws_n
+        kvs.append((synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 900 + i, 1.0, device),
+                    synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 950 + i, 1.0, device)))
+    plan = M.site_plan(shape, args.p)
+    pos = torch.full((1,), max_ctx - 1, dtype=torch.int32, device=device)
+    r = synth.residual_activation(1, shape.d, 7)[0].to(device)
+
+    def allgather(local_t, full_t):
+        if ws_n > 1:
+            dist.all_gather_into_tensor(full_t, local_t)
+        else:
+            full_t.copy_(local_t)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for sh, (kc, vc) in zip(shards, kvs):
+            sh.forward(r, kc, vc, pos, plan, allgather)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graphs = []
+    for sh, (kc, vc) in zip(shards, kvs):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            sh.forward(r, kc, vc, pos, plan, allgather)
+        graphs.append(g)
+    for i in range(args.warmup):
+        graphs[i % n_copies].replay()
+    torch.cuda.synchronize()
+    if ws_n > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for i in range(args.steps):
+            graphs[i % n_copies].replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if ws_n > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        out = {"metric": "decode tokens/s (LLaMA3-70B layer, row-sharded, batch 1)", "value": args.steps / (ms / 1e3),
+               "unit": "tok/s", "n_gpus": ws_n, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
+               "config": {"workload": "LLaMA3-70B decoder layer (8192 hidden, 28672 MLP, GQA 64/8) batch 1, "
+                                      "row-sharded", "sparsity": args.p, "plan_k": list(plan), "ctx": max_ctx,
+                          "layer_copies": n_copies, "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x5/layer)",
+                          "l2": "inputs larger than L2: 4 distinct layer shards cycled"},
+               "gpu_launches": (5 * 2 + 1) * args.steps, "clocks": clk.summary()}
+        print(json.dumps(out))
+    if ws_n > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -283,6 +365,9 @@ def main():
     ap.add_argument("--impl", default="larosa", choices=["larosa", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="block", choices=["block", "sharded-70b"],
+                    help="block: LLaMA2-7B block (headline; N > 1 = replicas); sharded-70b: one LLaMA3-70B "
+                         "layer row-sharded over the N ranks with NCCL all-gathers (SURVEY §8(e))")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -290,6 +375,9 @@ def main():
         run_reference(args)
         return
 
+    if args.workload == "sharded-70b":
+        run_sharded(args)
+        return
     ws_n, rank, local = dist_env()
     torch.cuda.set_device(local)
     device = f"cuda:{local}"

@@ -270,6 +270,40 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
                                   const larosa_layer_state* state, const larosa_layer_taps* taps,
                                   void* ws, size_t ws_bytes, larosa_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * Row-sharded layer for multi-GPU decode (batch 1).  Every rank holds the
+ * output columns ("rows" of nn.Linear) of each projection and the replicated residual:
+ *   w_qkv  [d][(Hq/n + 2 Hkv/n) hd]   this rank's q heads [r Hq/n, ..) | k heads | v heads
+ *   b_qkv  [(Hq/n + 2 Hkv/n) hd] or NULL
+ *   w_o    [Hq hd][d/n]    w_gu [d][2 inter/n] (packed as larosa_pack_gate_up, the same
+ *   inter/n range of gate and up)    w_down [inter][d/n]    adapter [d][d/n] or NULL
+ * (the larosa_layer_weights struct keeps the FULL model dims; shard->world = n).
+ * The layer runs as 5 phases; after each the caller all-gathers `out` (rank-major = column
+ * order at batch 1) into the next phase's `x`:
+ *   0: x = r (full)      -> Top-K h1 (RMS) -> QKV (local heads, RoPE, local KV append)
+ *                           -> attention (local heads)                 -> out = h2 [Hq hd / n]
+ *   1: x = h2 (full)     -> Top-K h2 -> O (local cols)    -> out = r_mid cols = r + y_o [d/n]
+ *   2: x = r_mid (full)  -> Top-K h3 (RMS) -> gate|up (local) -> out = SiLU(g) u [inter/n]
+ *   3: x = h4 (full)     -> Top-K h4 -> down (local cols) -> out = r_mid + y_down [d/n]
+ *   4: x = that (full)   -> adapter (dense, local cols)   -> out = r_next cols [d/n]
+ *      (phase 4 is skipped when adapter == NULL: phase 3's output is r_next)
+ * resid = the full residual r (phases 1, 3 read r resp. r_mid from it: pass phase 0's x for
+ * phase 1 and phase 2's x for phase 3).  Every rank derives the identical Top-K rule from
+ * the identical gathered vector, so kept sets agree across ranks by construction.
+ * k_cache / v_cache: this rank's [1][Hkv/n][max_ctx][hd].  Requires Hq % n == 0,
+ * Hkv % n == 0, d % (8 n) == 0, inter % (64 n) == 0.  One workspace per rank (size query
+ * with the shard), zero-filled once.
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+    int32_t rank, world;
+} larosa_shard;
+size_t larosa_shard_workspace_size(const larosa_layer_weights* w, const larosa_shard* shard, int64_t max_ctx);
+larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, const larosa_layer_plan* plan,
+                                              const larosa_shard* shard, int32_t phase, const float* x,
+                                              const float* resid, float* out, uint16_t* k_cache,
+                                              uint16_t* v_cache, const int32_t* pos, int64_t max_ctx, void* ws,
+                                              size_t ws_bytes, larosa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

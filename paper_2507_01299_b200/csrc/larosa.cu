@@ -1111,3 +1111,164 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     }
     return LAROSA_OK;
 }
+
+// ============================================================================== sharded layer
+namespace {
+struct ShardWs {
+    SiteSel sel;                       // selection data of the phase input (rebuilt each phase)
+    unsigned long long* acc;           // local projection accumulators (largest phase)
+    float* attn_part;
+    unsigned* attn_cnt;
+    unsigned* tickets;
+};
+struct ShardDims {
+    int64_t d, inter, nq, hq_l, hkv_l, hd, dl, il, qkv_l;
+    int G;
+};
+ShardDims shard_dims(const larosa_layer_weights* w, const larosa_shard* sh) {
+    ShardDims S;
+    const int64_t n = sh->world;
+    S.d = w->d;
+    S.inter = w->inter;
+    S.hd = w->head_dim;
+    S.nq = w->n_q_heads * w->head_dim;
+    S.hq_l = w->n_q_heads / n;
+    S.hkv_l = w->n_kv_heads / n;
+    S.dl = w->d / n;
+    S.il = w->inter / n;
+    S.qkv_l = (S.hq_l + 2 * S.hkv_l) * S.hd;
+    S.G = (int)(S.hkv_l > 0 ? S.hq_l / S.hkv_l : 1);
+    return S;
+}
+void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
+    ShardWs tmp;
+    ShardWs* q = o ? o : &tmp;
+    const int64_t dmax = std::max(std::max(S.d, S.nq), S.inter);
+    const int64_t omax = std::max(std::max(S.qkv_l, S.dl), 2 * S.il);
+    q->acc = c.take<unsigned long long>((size_t)omax);
+    q->sel.hist = c.take<uint32_t>(kSelHistTotal);
+    q->sel.pool = c.take<uint2>((size_t)kSelBins * kPoolCap);
+    q->sel.x16 = c.take<uint16_t>((size_t)dmax);
+    q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
+    const int ch = attn_chunk(max_ctx, (int)S.hkv_l);
+    const int nch = (int)((max_ctx + ch - 1) / ch);
+    q->attn_part = c.take<float>((size_t)S.hkv_l * nch * S.G * (S.hd + 2));
+    q->attn_cnt = c.counters(kAttnCounterBase);
+    q->tickets = c.counters(kGemvTicketBase);
+}
+larosa_status validate_shard(const larosa_layer_weights* w, const larosa_shard* sh) {
+    if (!w || !sh) return fail(LAROSA_EINVAL, "shard: NULL struct");
+    const int64_t n = sh->world;
+    if (n < 1 || sh->rank < 0 || sh->rank >= n) return fail(LAROSA_EINVAL, "shard: bad rank/world");
+    if (w->n_q_heads % n || w->n_kv_heads % n) return fail(LAROSA_EUNSUPPORTED, "shard: heads %% world != 0");
+    if (w->d % (8 * n)) return fail(LAROSA_EUNSUPPORTED, "shard: d %% (8 world) != 0");
+    if (w->inter % (LAROSA_GU_BLOCK * n)) return fail(LAROSA_EUNSUPPORTED, "shard: inter %% (64 world) != 0");
+    if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "shard: head_dim must be 64 or 128");
+    if (w->d > LAROSA_MAX_DIM || w->inter > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "shard: dims too large");
+    return LAROSA_OK;
+}
+}  // namespace
+
+extern "C" size_t larosa_shard_workspace_size(const larosa_layer_weights* w, const larosa_shard* shard,
+                                              int64_t max_ctx) {
+    if (validate_shard(w, shard) != LAROSA_OK || max_ctx <= 0) return 0;
+    Carver c(nullptr);
+    carve_shard(c, shard_dims(w, shard), max_ctx, nullptr);
+    return c.size();
+}
+
+extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, const larosa_layer_plan* plan,
+                                                         const larosa_shard* sh, int32_t phase, const float* x,
+                                                         const float* resid, float* out, uint16_t* k_cache,
+                                                         uint16_t* v_cache, const int32_t* pos, int64_t max_ctx,
+                                                         void* ws, size_t ws_bytes, larosa_stream_t stream) {
+    LAROSA_TRY(validate_shard(w, sh));
+    if (!plan || !x || !out) return fail(LAROSA_EINVAL, "shard_phase: NULL pointer");
+    if (phase < 0 || phase > 4) return fail(LAROSA_EINVAL, "shard_phase: phase must be 0..4");
+    if ((phase == 1 || phase == 3) && !resid) return fail(LAROSA_EINVAL, "shard_phase: phase %d needs resid", phase);
+    if (phase == 0 && (!k_cache || !v_cache || !pos || max_ctx <= 0)) return fail(LAROSA_EINVAL, "shard_phase: KV state");
+    const size_t need = larosa_shard_workspace_size(w, sh, max_ctx > 0 ? max_ctx : 1);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "shard_phase: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const ShardDims S = shard_dims(w, sh);
+    Carver c(ws);
+    ShardWs W;
+    carve_shard(c, S, max_ctx > 0 ? max_ctx : 1, &W);
+    const int r = sh->rank;
+    // phase -> (site input width, k, RMS eps, weights, local output width)
+    int64_t din = S.d, k = 0, dout = 0;
+    float eps = -1.0f;
+    const uint16_t* Wt = nullptr;
+    switch (phase) {
+        case 0: din = S.d; k = plan->k_h1; eps = w->rms_eps; Wt = w->w_qkv; dout = S.qkv_l; break;
+        case 1: din = S.nq; k = plan->k_h2; Wt = w->w_o; dout = S.dl; break;
+        case 2: din = S.d; k = plan->k_h3; eps = w->rms_eps; Wt = w->w_gu; dout = 2 * S.il; break;
+        case 3: din = S.inter; k = plan->k_h4; Wt = w->w_down; dout = S.dl; break;
+        default: din = S.d; Wt = w->adapter; dout = S.dl; break;
+    }
+    if (!Wt) return fail(LAROSA_EINVAL, "shard_phase: NULL weight for phase %d", phase);
+    if (k < 0 || k > din) return fail(LAROSA_EINVAL, "shard_phase: k outside [0, D_in]");
+    GemvArgs a = gemv_args_base();
+    a.W = Wt;
+    a.ld = dout;
+    a.d_out = (int)dout;
+    a.x = x;
+    a.ldx = din;
+    a.d_in = (int)din;
+    a.batch = 1;
+    a.acc = W.acc;
+    a.acc_ld = dout;
+    GemvPlan p;
+    if (phase == 4) {
+        a.mode = GEMV_DENSE;
+        p = plan_gemv(dout, din, 1, GEMV_DENSE, din);
+    } else {
+        // the gathered vector is identical on every rank -> identical selection data
+        SiteSel sel = W.sel;
+        if (eps < 0.f) sel.ssq = nullptr;
+        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)din, sel),
+                              "select prep launch"));
+        a.mode = GEMV_SELECT;
+        a.sel = sel;
+        a.sel_nssq = (int)((din + kSliceCols - 1) / kSliceCols);
+        a.sel_k = (int)k;
+        a.sel_eps = eps;
+        p = plan_gemv(dout, k, 1, GEMV_SELECT, din);
+    }
+    if (phase != 0) {
+        a.epi = phase == 2 ? EPI_SILU : (phase == 4 ? EPI_STORE : EPI_RESID);
+        a.tickets = W.tickets;
+        if (phase == 1 || phase == 3) {
+            a.res = resid + (size_t)r * S.dl;   // this rank's columns of r (phase 1) / r_mid (phase 3)
+            a.res_ld = S.d;
+        }
+        a.out = out;
+        a.out_ld = phase == 2 ? S.il : S.dl;
+        return launch_gemv(a, p, 1, st);
+    }
+    // phase 0: QKV over the local heads (EPI_NONE) then attention writes the local h2
+    LAROSA_TRY(launch_gemv(a, p, 1, st));
+    AttnArgs aa;
+    memset(&aa, 0, sizeof(aa));
+    aa.acc = W.acc;
+    aa.acc_ld = S.qkv_l;
+    aa.bias = w->b_qkv;
+    aa.theta = w->rope_theta;
+    aa.kc = k_cache;
+    aa.vc = v_cache;
+    aa.pos = pos;
+    aa.max_ctx = max_ctx;
+    aa.hq = (int)S.hq_l;
+    aa.hkv = (int)S.hkv_l;
+    aa.hd = (int)S.hd;
+    aa.chunk = attn_chunk(max_ctx, (int)S.hkv_l);
+    aa.n_chunks = (int)((max_ctx + aa.chunk - 1) / aa.chunk);
+    aa.part = W.attn_part;
+    aa.counters = W.attn_cnt;
+    aa.out = out;
+    const size_t smem = attn_smem_bytes(S.G, (int)S.hd, aa.chunk);
+    const dim3 grid((unsigned)S.hkv_l, aa.n_chunks);
+    if (S.hd == 128)
+        return cuda_check(launch(attention_kernel<4>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch");
+    return cuda_check(launch(attention_kernel<2>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch");
+}

@@ -55,6 +55,10 @@ class LayerTapsC(ctypes.Structure):
                 ("idx_h4", _vp), ("vals_h4", _vp), ("r_out", _vp)]
 
 
+class ShardC(ctypes.Structure):
+    _fields_ = [("rank", _c_i32), ("world", _c_i32)]
+
+
 _LIB = None
 
 
@@ -93,6 +97,11 @@ def lib() -> ctypes.CDLL:
     L.larosa_lm_head_workspace_size.restype = ctypes.c_size_t
     L.larosa_lm_head_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64]
     L.larosa_lm_head.argtypes = [_vp, _c_i32, _c_i64, _vp, _c_i64, ctypes.c_float, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+    L.larosa_shard_workspace_size.restype = ctypes.c_size_t
+    L.larosa_shard_workspace_size.argtypes = [ctypes.POINTER(LayerWeightsC), ctypes.POINTER(ShardC), _c_i64]
+    L.larosa_sparse_layer_shard_phase.argtypes = [ctypes.POINTER(LayerWeightsC), ctypes.POINTER(LayerPlanC),
+                                                  ctypes.POINTER(ShardC), _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                  _c_i64, _vp, ctypes.c_size_t, _vp]
     L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
     L.larosa_debug_set_layer_phases.restype = None
     L.larosa_gemv_plan_info.argtypes = [_c_i64, _c_i64, _c_i32, ctypes.POINTER(_c_i32)]
@@ -104,7 +113,7 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_size_t, _vp]
     for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
-                 "larosa_embed", "larosa_lm_head"):
+                 "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
         getattr(L, name).restype = ctypes.c_int
     if L.larosa_abi_version() != 1:
         raise RuntimeError("liblarosa ABI version mismatch")
@@ -358,3 +367,27 @@ def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: 
     _check(L.larosa_sparse_layer(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sc),
                                  ctypes.byref(tc) if tc is not None else None, _ptr(ws), ws.numel(),
                                  _stream(stream)))
+
+
+# ------------------------------------------------------------------------------- sharding
+def shard_workspace_size(w: LayerWeights, rank: int, world: int, max_ctx: int) -> int:
+    wc = w.c()
+    sh = ShardC(rank, world)
+    n = lib().larosa_shard_workspace_size(ctypes.byref(wc), ctypes.byref(sh), max_ctx)
+    if n == 0:
+        raise LarosaError(3, "shard configuration unsupported (see larosa.h)")
+    return n
+
+
+def shard_phase(w: LayerWeights, plan: Sequence[int], rank: int, world: int, phase: int, x: torch.Tensor,
+                out: torch.Tensor, ws: torch.Tensor, resid: Optional[torch.Tensor] = None,
+                k_cache: Optional[torch.Tensor] = None, v_cache: Optional[torch.Tensor] = None,
+                pos: Optional[torch.Tensor] = None, max_ctx: int = 0, stream=None):
+    """One phase of the row-sharded layer (larosa_sparse_layer_shard_phase); ``w`` holds this
+    rank's shard with the FULL model dims."""
+    wc = w.c()
+    pc = LayerPlanC(*[int(k) for k in plan])
+    sh = ShardC(rank, world)
+    _check(lib().larosa_sparse_layer_shard_phase(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sh), int(phase),
+                                                 _ptr(x), _ptr(resid), _ptr(out), _ptr(k_cache), _ptr(v_cache),
+                                                 _ptr(pos), int(max_ctx), _ptr(ws), ws.numel(), _stream(stream)))

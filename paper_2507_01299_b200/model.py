@@ -152,3 +152,85 @@ class DecodeRunner:
         LZ.lm_head(self.resid, self.m.head, self.m.shape.rms_eps, logits=self.logits, next_token=self.next_tokens,
                    ws=self.head_ws, stream=stream)
         return self.next_tokens
+
+
+# ------------------------------------------------------------------------------- multi-GPU
+def shard_layer(w: LZ.LayerWeights, rank: int, world: int) -> LZ.LayerWeights:
+    """This rank's output columns of every projection (SURVEY §8(e) partitioning; offline data
+    layout, like loading a checkpoint shard): q heads [r Hq/n, (r+1) Hq/n) with the matching
+    kv heads, d/n columns of W_o / W_down / adapter, the same inter/n range of gate and up (a
+    contiguous column range of the packed W_gate|up).  Dims stay the full model's."""
+    n, hd = world, w.head_dim
+    nq, nk = w.n_q_heads * hd, w.n_kv_heads * hd
+    ql, kl = nq // n, nk // n
+    dl, il = w.d // n, w.inter // n
+
+    def cols(t, a, b):
+        return t[..., a:b].contiguous() if t is not None else None
+
+    def qkv(t):
+        if t is None:
+            return None
+        return torch.cat([t[..., rank * ql:(rank + 1) * ql], t[..., nq + rank * kl:nq + (rank + 1) * kl],
+                          t[..., nq + nk + rank * kl:nq + nk + (rank + 1) * kl]], dim=-1).contiguous()
+
+    return LZ.LayerWeights(w_qkv=qkv(w.w_qkv), w_o=cols(w.w_o, rank * dl, (rank + 1) * dl),
+                           w_gu=cols(w.w_gu, rank * 2 * il, (rank + 1) * 2 * il),
+                           w_down=cols(w.w_down, rank * dl, (rank + 1) * dl), d=w.d, inter=w.inter,
+                           n_q_heads=w.n_q_heads, n_kv_heads=w.n_kv_heads, head_dim=hd, rope_theta=w.rope_theta,
+                           rms_eps=w.rms_eps, b_qkv=qkv(w.b_qkv),
+                           adapter=cols(w.adapter, rank * dl, (rank + 1) * dl))
+
+
+def shard_kv(cache: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    """This rank's kv heads of a [B][Hkv][ctx][hd] cache."""
+    h = cache.shape[1] // world
+    return cache[:, rank * h:(rank + 1) * h].contiguous()
+
+
+class ShardedLayer:
+    """One rank's view of a row-sharded LaRoSA layer at batch 1: five library phases, each
+    followed by an all-gather of the phase output (rank-major concatenation = column order).
+    ``allgather(local, full)`` is torch.distributed.all_gather_into_tensor over NCCL on a real
+    multi-GPU run (CUDA-graph capturable)."""
+
+    def __init__(self, w_shard: LZ.LayerWeights, rank: int, world: int, max_ctx: int, device):
+        self.w, self.rank, self.world, self.max_ctx = w_shard, rank, world, max_ctx
+        d, nq, inter = w_shard.d, w_shard.n_q_heads * w_shard.head_dim, w_shard.inter
+        n = world
+        f32 = dict(dtype=torch.float32, device=device)
+        self.ws = torch.zeros(LZ.shard_workspace_size(w_shard, rank, world, max_ctx), dtype=torch.uint8, device=device)
+        self.local = {0: torch.zeros(nq // n, **f32), 1: torch.zeros(d // n, **f32), 2: torch.zeros(inter // n, **f32),
+                      3: torch.zeros(d // n, **f32), 4: torch.zeros(d // n, **f32)}
+        self.full = {0: torch.zeros(nq, **f32), 1: torch.zeros(d, **f32), 2: torch.zeros(inter, **f32),
+                     3: torch.zeros(d, **f32)}
+
+    def run_phase(self, phase: int, x: torch.Tensor, resid: Optional[torch.Tensor], k_cache, v_cache, pos,
+                  plan, stream=None) -> torch.Tensor:
+        LZ.shard_phase(self.w, plan, self.rank, self.world, phase, x, self.local[phase], self.ws, resid=resid,
+                       k_cache=k_cache, v_cache=v_cache, pos=pos, max_ctx=self.max_ctx, stream=stream)
+        return self.local[phase]
+
+    def n_phases(self) -> int:
+        return 5 if self.w.adapter is not None else 4
+
+    def inputs(self, phase: int, r: torch.Tensor):
+        """(x, resid) of a phase given the layer input r and the gathered earlier outputs."""
+        if phase == 0:
+            return r, None
+        if phase == 1:
+            return self.full[0], r
+        if phase == 2:
+            return self.full[1], None
+        if phase == 3:
+            return self.full[2], self.full[1]
+        return self.full[3], None
+
+    def forward(self, r: torch.Tensor, k_cache, v_cache, pos, plan, allgather, stream=None) -> torch.Tensor:
+        """r: the full residual [d] (replicated); returns it updated in place (next layer's input)."""
+        last = self.n_phases() - 1
+        for ph in range(last + 1):
+            x, res = self.inputs(ph, r)
+            out = self.run_phase(ph, x, res, k_cache, v_cache, pos, plan, stream)
+            allgather(out, r if ph == last else self.full[ph])
+        return r

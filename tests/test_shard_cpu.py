@@ -1,0 +1,159 @@
+"""Host logic of the row-sharded multi-GPU layer, on CPU with a real gloo
+process group (world size 2): every rank takes its shard with model.shard_layer, computes
+each of the five phases on it with the fp64 ORACLE primitives (the same phase contract as
+larosa_sparse_layer_shard_phase), and all-gathers the phase outputs with
+torch.distributed.all_gather_into_tensor.  The gathered result must equal the unsharded
+oracle layer bit for bit: the column partition (heads, d/n, packed gate|up blocks), the
+phase inputs and the rank-major gather order are what is under test."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import synth
+from paper_2507_01299_b200 import larosa as LZ
+from paper_2507_01299_b200 import model as M
+
+D, INTER, HQ, HKV, HD, CTX = 128, 256, 4, 2, 16, 6
+B_GU = LZ.LAROSA_GU_BLOCK
+
+
+def pack_gu(wg, wu):
+    d, inter = wg.shape
+    return np.stack([wg.reshape(d, inter // B_GU, B_GU), wu.reshape(d, inter // B_GU, B_GU)], axis=2).reshape(d, -1)
+
+
+def unpack_gu(wgu):
+    d = wgu.shape[0]
+    blk = wgu.reshape(d, -1, 2, B_GU)
+    return blk[:, :, 0, :].reshape(d, -1), blk[:, :, 1, :].reshape(d, -1)
+
+
+def toy(seed):
+    rng = np.random.default_rng(seed)
+    nq, nk = HQ * HD, HKV * HD
+    w = {"wqkv": rng.standard_normal((D, nq + 2 * nk)) / math.sqrt(D),
+         "bqkv": 0.02 * rng.standard_normal(nq + 2 * nk),
+         "wo": rng.standard_normal((nq, D)) / math.sqrt(nq),
+         "wg": rng.standard_normal((D, INTER)) / math.sqrt(D),
+         "wu": rng.standard_normal((D, INTER)) / math.sqrt(D),
+         "wd": rng.standard_normal((INTER, D)) / math.sqrt(INTER),
+         "adapter": synth.haar_orthogonal(D, seed + 1).numpy()}
+    kc = rng.standard_normal((HKV, CTX, HD))
+    vc = rng.standard_normal((HKV, CTX, HD))
+    r = rng.standard_normal(D)
+    return w, kc, vc, r
+
+
+def layer_weights(w):
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))   # noqa: E731
+    return LZ.LayerWeights(w_qkv=t(w["wqkv"]), w_o=t(w["wo"]), w_gu=t(pack_gu(w["wg"], w["wu"])), w_down=t(w["wd"]),
+                           d=D, inter=INTER, n_q_heads=HQ, n_kv_heads=HKV, head_dim=HD, rope_theta=10000.0,
+                           rms_eps=1e-6, b_qkv=t(w["bqkv"]), adapter=t(w["adapter"]))
+
+
+def oracle_phase(ph, ws, plan, x, resid, kc, vc, pos, rank, world):
+    """The phase contract of larosa_sparse_layer_shard_phase, computed with oracle primitives."""
+    k1, k2, k3, k4 = plan
+    n = lambda t: t.numpy()   # noqa: E731
+    dl = D // world
+    if ph == 0:
+        s = O.topk(x, k1)
+        y = O.sparse_gemv(n(ws.w_qkv), s, x[s] * O.rms_scale(x, 1e-6), n(ws.b_qkv))
+        hq, hkv = HQ // world, HKV // world
+        q = y[:hq * HD].reshape(hq, HD)
+        k = y[hq * HD:(hq + hkv) * HD].reshape(hkv, HD)
+        v = y[(hq + hkv) * HD:].reshape(hkv, HD)
+        q = np.stack([O.rope(q[h], pos, 10000.0) for h in range(hq)])
+        k = np.stack([O.rope(k[h], pos, 10000.0) for h in range(hkv)])
+        kc[:, pos] = k
+        vc[:, pos] = v
+        return O.decode_attention(q, kc, vc, pos + 1)
+    if ph == 1:
+        s = O.topk(x, k2)
+        return resid[rank * dl:(rank + 1) * dl] + O.sparse_gemv(n(ws.w_o), s, x[s])
+    if ph == 2:
+        s = O.topk(x, k3)
+        wg, wu = unpack_gu(n(ws.w_gu))
+        v = x[s] * O.rms_scale(x, 1e-6)
+        return O.silu(O.sparse_gemv(wg, s, v)) * O.sparse_gemv(wu, s, v)
+    if ph == 3:
+        s = O.topk(x, k4)
+        return resid[rank * dl:(rank + 1) * dl] + O.sparse_gemv(n(ws.w_down), s, x[s])
+    return O.dense_gemv(n(ws.adapter), x)
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, kc, vc, r = toy(5)
+        plan = O.site_ks(0.5, (1, 1, 1, 1), D, INTER)
+        plan = (plan[0], O.compute_k(1.0, 0.5, HQ * HD), plan[2], plan[3])
+        ws = M.shard_layer(layer_weights(w), rank, world)
+        hk = HKV // world
+        kc_l, vc_l = kc[rank * hk:(rank + 1) * hk].copy(), vc[rank * hk:(rank + 1) * hk].copy()
+        pos = CTX - 1
+        full = {}
+        x = r.copy()
+        for ph in range(5):
+            xin = {0: r, 1: full.get(0), 2: full.get(1), 3: full.get(2), 4: full.get(3)}[ph]
+            res = {1: r, 3: full.get(1)}.get(ph)
+            out = torch.from_numpy(oracle_phase(ph, ws, plan, xin, res, kc_l, vc_l, pos, rank, world))
+            g = torch.empty(out.numel() * world, dtype=out.dtype)
+            dist.all_gather_into_tensor(g, out)
+            full[ph] = g.numpy()
+        # unsharded reference
+        wf = {"wqkv": w["wqkv"], "bqkv": w["bqkv"], "wo": w["wo"], "wg": w["wg"], "wu": w["wu"], "wd": w["wd"]}
+        cfg = dict(hq=HQ, hkv=HKV, hd=HD, eps=1e-6, theta=10000.0)
+        ref, inter = O.larosa_block(r, wf, cfg, plan, kc.copy(), vc.copy(), pos, adapter=w["adapter"])
+        ok = (np.array_equal(full[0], inter["h2"]) and np.array_equal(full[1], inter["r_mid"])
+              and np.array_equal(full[2], inter["h4"]) and np.array_equal(full[3], inter["r_out"])
+              and np.array_equal(full[4], ref))
+        q.put((rank, ok, float(np.max(np.abs(full[4] - ref)))))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_layer_gloo_equals_unsharded(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+
+
+def test_shard_layer_partition_covers_columns():
+    """Concatenating the shards' columns in rank order rebuilds every projection (the gather
+    order the phases rely on); q/k/v heads stay grouped per rank."""
+    w, *_ = toy(9)
+    lw = layer_weights(w)
+    for world in (1, 2):
+        sh = [M.shard_layer(lw, r, world) for r in range(world)]
+        for name in ("w_o", "w_gu", "w_down", "adapter"):
+            assert torch.equal(torch.cat([getattr(s, name) for s in sh], dim=1), getattr(lw, name))
+        nq, nk = HQ * HD, HKV * HD
+        ql, kl = nq // world, nk // world
+        cat = torch.cat([s.w_qkv for s in sh], dim=1)
+        q = torch.cat([cat[:, r * (ql + 2 * kl):r * (ql + 2 * kl) + ql] for r in range(world)], dim=1)
+        assert torch.equal(q, lw.w_qkv[:, :nq])
