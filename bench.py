@@ -179,36 +179,33 @@ def build_stack(shape, device, n_copies, seed=0):
     return layers
 
 
-def time_gemv_sites(layers, plan, shape, device, reps=64):
-    """Average duration of a standalone larosa_sparse_gemv call per site (one GEMV launch
-    with its finalising epilogue), CUDA events on the launching stream, cycling layer copies and fresh
-    Top-K inputs."""
+def time_gemv_sites(layers, plan, shape, device, reps=48):
+    """The dominant kernel in isolation: the batch-1 SELECT GEMV (gemv_kernel<1, SELECT>, the
+    exact kernel of the layer step: fused Top-K prologue + kept-row stream + epilogue) per
+    site, on selection data prepared once per input (larosa_topk_sparse_gemv prepared=1),
+    back-to-back launches (PDL) in a CUDA graph, cycling the layer copies (weights >> L2) and
+    8 inputs; CUDA events on the launching stream.  The adapter site runs at k = D."""
     from paper_2507_01299_b200 import larosa as LZ
     k1, k2, k3, k4 = plan
     nq = shape.hq * shape.hd
-    sites = [("qkv", "w_qkv", shape.d, shape.qkv_out, k1), ("o", "w_o", nq, shape.d, k2),
-             ("gate_up", "w_gu", shape.d, 2 * shape.inter, k3), ("down", "w_down", shape.inter, shape.d, k4),
-             ("adapter", "adapter", shape.d, shape.d, shape.d)]
+    sites = [("qkv", "w_qkv", shape.d, shape.qkv_out, k1, shape.rms_eps), ("o", "w_o", nq, shape.d, k2, -1.0),
+             ("gate_up", "w_gu", shape.d, 2 * shape.inter, k3, shape.rms_eps),
+             ("down", "w_down", shape.inter, shape.d, k4, -1.0), ("adapter", "adapter", shape.d, shape.d, shape.d, -1.0)]
     res = {}
     stream = torch.cuda.current_stream()
-    for name, attr, din, dout, k in sites:
-        inputs = []
-        for r in range(8):
-            x = synth.residual_activation(1, din, seed=500 + r).to(device)
-            _, idx, vals, _ = LZ.rotate_topk(x, None, k)
-            inputs.append((idx, vals))
-        y = torch.empty((1, dout), dtype=torch.float32, device=device)
-        for i in range(5):
-            idx, vals = inputs[i % 8]
-            LZ.sparse_gemv(getattr(layers[i % len(layers)], attr), idx, vals, out=y)
+    n_in = 8
+    for name, attr, din, dout, k, eps in sites:
+        xs = [synth.residual_activation(1, din, seed=500 + r)[0].to(device) for r in range(n_in)]
+        wss = [LZ.topk_sparse_gemv_workspace(din, dout, device) for _ in range(n_in)]
+        y = torch.empty((dout,), dtype=torch.float32, device=device)
+        for i in range(n_in):   # prepare each input's selection data once
+            LZ.topk_sparse_gemv(xs[i], k, getattr(layers[0], attr), rms_eps=eps, out=y, ws=wss[i])
         torch.cuda.synchronize()
-        # back-to-back launches captured in a CUDA graph (no host launch gaps), cycling the
-        # layer copies (weights >> L2) and 8 different kept-row sets
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for i in range(reps):
-                idx, vals = inputs[i % 8]
-                LZ.sparse_gemv(getattr(layers[i % len(layers)], attr), idx, vals, out=y)
+                LZ.topk_sparse_gemv(xs[i % n_in], k, getattr(layers[i % len(layers)], attr), rms_eps=eps, out=y,
+                                    ws=wss[i % n_in], prepared=True)
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -218,8 +215,72 @@ def time_gemv_sites(layers, plan, shape, device, reps=64):
         e1.record(stream)
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
-        alg = k * dout * 2 + k * 8 + dout * 4
-        res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_out": dout}
+        alg = k * dout * 2 + din * 2 + dout * 4      # kept rows + 16-bit keys + y
+        res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_in": din, "d_out": dout}
+    return res
+
+
+def decode_step_extra(device, batches=(1, 16), ps=(0.4, 0.0), reps=20):
+    """BASELINE configs[2]: the LLaMA3-8B-shaped full decode step (32 folded layers + LM head,
+    greedy), KV context 256, one CUDA graph per step; tok/s per (batch, p)."""
+    from paper_2507_01299_b200 import model as M
+    shape = synth.MODELS["llama3-8b"]
+    model = M.synth_decode_model(shape, shape.layers, device, seed=1)
+    out = {}
+    for B in batches:
+        run = M.DecodeRunner(model, B, 256, device)
+        for kc, vc in run.kv:
+            kc.copy_(synth.gaussian_bf16(kc.shape, 5, 1.0, device))
+            vc.copy_(synth.gaussian_bf16(vc.shape, 6, 1.0, device))
+        run.tokens.copy_(torch.arange(B, dtype=torch.int32) * 37 + 11)
+        run.pos.fill_(255)
+        for p in ps:
+            plan = M.site_plan(shape, p)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                run.step(plan)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                run.step(plan)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            out[f"B{B}_p{p}"] = {"ms_per_step": ms, "tok_s": B * 1e3 / ms, "plan": list(plan)}
+        del run
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
+def fold_extra(device):
+    """larosa_fold_rotation on LLaMA2-7B layer shapes: tcgen05 TFLOP/s (2 M N K of the fold)."""
+    from paper_2507_01299_b200 import larosa as LZ
+    d = 4096
+    q = synth.haar_orthogonal(d, 1, device=device, dtype=torch.float32)
+    g = torch.ones(d, device=device)
+    res = {}
+    for name, rows, cols, side in (("w_qkv_left", 4096, 12288, 0), ("w_down_right", 11008, 4096, 1)):
+        W = synth.gaussian_bf16((rows, cols), 2, 0.02, device)
+        out = torch.empty_like(W)
+        LZ.fold_rotation(q, W, side, gamma=g if side == 0 else None, out=out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            LZ.fold_rotation(q, W, side, gamma=g if side == 0 else None, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        res[name] = {"ms": ms, "tflops": 2.0 * rows * cols * d / ms / 1e9}
     return res
 
 
@@ -450,16 +511,10 @@ def main():
     e2e = {"value": ws_n * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": shape.d * 4,
            "d2h_bytes_per_step": shape.d * 4}
 
-    # ---- dominant kernel (the GEMV) roofline: the same step graph with only the 5 GEMV
-    # launches kept (larosa_debug_set_layer_phases), CUDA events on the replay stream -------
-    LZ.lib().larosa_debug_set_layer_phases(0x352)
-    _, _, _, ms_gemv = measure(args.p)
-    LZ.lib().larosa_debug_set_layer_phases(-1)
-    k1, k2, k3, k4 = plan
-    nq = shape.hq * shape.hd
-    gemv_sites = [(k1, shape.qkv_out), (k2, shape.d), (k3, 2 * shape.inter), (k4, shape.d), (shape.d, shape.d)]
-    bytes_step = sum(k * dout * 2 + k * 8 + dout * 8 for k, dout in gemv_sites)
-    us_gemv = 1e3 * ms_gemv / args.steps
+    # ---- dominant kernel roofline: the SELECT GEMV per site, timed live in isolation --------
+    gem = time_gemv_sites(layers, plan, shape, device)
+    bytes_step = sum(v["bytes"] for v in gem.values())
+    us_gemv = sum(v["us"] for v in gem.values())
     peaks, peak_kind = measured_peaks()
     achieved = bytes_step / us_gemv / 1e3
     traffic = None
@@ -468,14 +523,13 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_step_gemv")
     except Exception:
         pass
-    gem = time_gemv_sites(layers, plan, shape, device)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": "gemv_kernel: the 5 GEMV launches of one block step (QKV, O, gate|up, down sparse; "
-                          "adapter dense), timed as the step graph with only those launches",
+                "kernel": "gemv_kernel<1, SELECT>: fused Top-K prologue + kept-row stream + epilogue; the 5 "
+                          "site launches of one block step (QKV, O, gate|up, down at their k; adapter at k = D), "
+                          "each timed back to back in a CUDA graph",
                 "algorithmic_bytes_per_step": bytes_step, "gemv_us_per_step": us_gemv, "launches_per_step": 5,
-                "peak_kind": f"{peak_kind} copy (hbm_gbs)",
-                "standalone_sparse_gemv_per_site": gem}
+                "peak_kind": f"{peak_kind} copy (hbm_gbs)", "per_site": gem}
 
     # ---- sparsity sweep (0-60%) and cuBLAS dense baseline ----------------------------------
     sweep = None
@@ -488,6 +542,10 @@ def main():
         dense_us, dense_per = cublas_dense_us(layers, shape, device)
         sweep["cublas_dense_4gemv_us"] = dense_us
         sweep["cublas_dense_per_gemv_us"] = dense_per
+
+    extras = None
+    if not args.no_sweep:
+        extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device), "fold_tcgen05": fold_extra(device)}
 
     cpu = None
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
@@ -509,7 +567,7 @@ def main():
                           "parallelism": f"replicas x{ws_n}" if ws_n > 1 else "single GPU",
                           "implied_llama2_7b_32_layer_tok_s": value / ws_n / 32},
                "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-               "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep}
+               "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep, "extras": extras}
         print(json.dumps(out))
     if ws_n > 1:
         torch.distributed.destroy_process_group()

@@ -157,10 +157,12 @@ larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int64_t d_out,
  * Same W / ld / d_out / alignment requirements as larosa_sparse_gemv.
  * ------------------------------------------------------------------------------ */
 size_t larosa_topk_sparse_gemv_workspace_size(int64_t d_in, int64_t d_out);
+/* prepared != 0: the workspace already holds x's selection data from an earlier call with
+ * the same x and rms_eps sign (then only the GEMV kernel is launched). */
 larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
                                       const uint16_t* W, int64_t d_out, int64_t ld,
-                                      const uint16_t* bias, float* y, void* ws, size_t ws_bytes,
-                                      larosa_stream_t stream);
+                                      const uint16_t* bias, float* y, int32_t prepared, void* ws,
+                                      size_t ws_bytes, larosa_stream_t stream);
 
 /* Introspection (host): the launch plan larosa_sparse_gemv uses for this shape.
  * info (host, 8 ints) = {columns per CTA, column slices, kept-row splits, warps per CTA,

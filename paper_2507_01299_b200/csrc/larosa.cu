@@ -437,7 +437,8 @@ extern "C" size_t larosa_topk_sparse_gemv_workspace_size(int64_t d_in, int64_t d
 
 extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
                                                  const uint16_t* W, int64_t d_out, int64_t ld, const uint16_t* bias,
-                                                 float* y, void* ws, size_t ws_bytes, larosa_stream_t stream) {
+                                                 float* y, int32_t prepared, void* ws, size_t ws_bytes,
+                                                 larosa_stream_t stream) {
     if (!x || !W || !y) return fail(LAROSA_EINVAL, "topk_sparse_gemv: NULL pointer");
     if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "topk_sparse_gemv: d_in, d_out must be > 0");
     if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "topk_sparse_gemv: k outside [0, d_in]");
@@ -456,8 +457,9 @@ extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, i
     SiteSel sel;
     carve_topk_gemv(c, d_in, d_out, &acc, &sel);
     if (rms_eps < 0.f) sel.ssq = nullptr;
-    LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)d_in, sel),
-                          "select prep launch"));
+    if (!prepared)
+        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)d_in, sel),
+                              "select prep launch"));
     const GemvPlan p = plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
     GemvArgs a = gemv_args_base();
     a.W = W;

@@ -91,8 +91,8 @@ def lib() -> ctypes.CDLL:
                                      ctypes.c_size_t, _vp]
     L.larosa_topk_sparse_gemv_workspace_size.restype = ctypes.c_size_t
     L.larosa_topk_sparse_gemv_workspace_size.argtypes = [_c_i64, _c_i64]
-    L.larosa_topk_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp, _vp,
-                                          ctypes.c_size_t, _vp]
+    L.larosa_topk_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp,
+                                          _c_i32, _vp, ctypes.c_size_t, _vp]
     L.larosa_embed.argtypes = [_vp, _c_i64, _c_i64, _vp, _c_i32, _vp, _vp]
     L.larosa_lm_head_workspace_size.restype = ctypes.c_size_t
     L.larosa_lm_head_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64]
@@ -242,10 +242,16 @@ def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Op
     return y
 
 
+def topk_sparse_gemv_workspace(d_in: int, d_out: int, device) -> torch.Tensor:
+    return torch.zeros(lib().larosa_topk_sparse_gemv_workspace_size(d_in, d_out), dtype=torch.uint8, device=device)
+
+
 def topk_sparse_gemv(x: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = -1.0,
                      bias: Optional[torch.Tensor] = None, d_out: Optional[int] = None,
-                     out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """Batch 1: y = bias + sum_{j in TopK_k(|x|)} x_j s W[j]  (selection fused into the GEMV)."""
+                     out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, prepared: bool = False,
+                     stream=None) -> torch.Tensor:
+    """Batch 1: y = bias + sum_{j in TopK_k(|x|)} x_j s W[j]  (selection fused into the GEMV).
+    prepared=True: ``ws`` already holds x's selection data (only the GEMV kernel launches)."""
     x = x.reshape(-1)
     d_in, ld = W.shape
     d_out = ld if d_out is None else d_out
@@ -253,9 +259,10 @@ def topk_sparse_gemv(x: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = 
     y = out if out is not None else torch.empty((d_out,), dtype=torch.float32, device=W.device)
     L = lib()
     nb = L.larosa_topk_sparse_gemv_workspace_size(d_in, d_out)
-    ws = _ws(("topk_sparse_gemv", d_in, d_out), nb, W.device)
+    if ws is None:
+        ws = _ws(("topk_sparse_gemv", d_in, d_out), nb, W.device)
     _check(L.larosa_topk_sparse_gemv(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), d_out, ld, _ptr(bias), _ptr(y),
-                                     _ptr(ws), ws.numel(), _stream(stream)))
+                                     int(prepared), _ptr(ws), ws.numel(), _stream(stream)))
     return y
 
 
