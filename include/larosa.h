@@ -224,6 +224,7 @@ typedef struct {
 
 typedef struct {
     int64_t k_h1, k_h2, k_h3, k_h4;
+    int64_t k_next_h1;   /* reserved (0) */
 } larosa_layer_plan;
 
 typedef struct {

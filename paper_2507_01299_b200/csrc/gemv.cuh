@@ -52,10 +52,8 @@ constexpr int kStageRows = 4;         // rows per stage (one 512-byte warp copy 
 constexpr int kStages = 4;            // ring depth per warp
 constexpr int kWarpRingBytes = kStages * kStageRows * kSliceCols * 2;   // 8 KB
 constexpr double kFixScale = 4294967296.0;                              // 2^32
-constexpr int kSelBins = 4096;        // histogram of key bits [30:19]
-constexpr int kSelShift = 19;
-constexpr int kGemvMisc = 64;         // ints of scratch
-constexpr int kPoolCap = 512;         // (key, index) entries kept per histogram bucket
+constexpr int kGemvMisc = 128;        // ints of scratch
+constexpr int kPoolCap = 64;          // (key, index) entries kept per 16-bit histogram bucket
 
 enum GemvMode : int { GEMV_LIST = 0, GEMV_THRESH = 1, GEMV_DENSE = 2, GEMV_SELECT = 3 };
 enum GemvEpi : int { EPI_NONE = 0, EPI_STORE = 1, EPI_RESID = 2, EPI_SILU = 3 };
@@ -66,14 +64,33 @@ enum GemvEpi : int { EPI_NONE = 0, EPI_STORE = 1, EPI_RESID = 2, EPI_SILU = 3 };
 //   pool  [4096][kPoolCap] (key, index) of each fine bucket's first entries
 //   x16   [d] key >> 15 (the top 16 key bits) of every element
 //   ssq   [ceil(d / 256)] per-slice sums of squares (RMS sites)
+// The site's exact Top-K rule (compute_rule, by every consuming CTA):
+// keep i iff key_i > tk or (key_i == tk and i <= ti); value x_i * scale.  Consumers decide
+// from the 16-bit keys; an element whose 16-bit key equals tk's top 16 bits is decided by the
+// boundary table (idx, keep) -- or, if flags & kRuleExact, from its exact key in x.
+constexpr int kRuleAll = 1, kRuleNone = 2, kRuleEdgeAll = 4, kRuleExact = 8;
+constexpr int kRuleTable = 64;
+struct __align__(16) SelRule {
+    uint32_t tk;
+    int32_t ti;
+    float scale;
+    int32_t flags;
+    int32_t nb;                 // boundary table entries (the k-th key's 16-bit bucket)
+    int32_t pad;
+    unsigned long long keep;    // bit t: idx[t] is kept
+    int32_t idx[kRuleTable];
+};
 struct SiteSel {
     uint32_t* hist;
     uint2* pool;
     uint16_t* x16;
     float* ssq;
 };
+// histogram levels: 65536 fine bins of key bits [30:15] (the 16-bit key), then 256 coarse
+// bins of bits [30:23]
+constexpr int kSelFine = 65536;
 constexpr int kSelCoarse = 256;
-constexpr int kSelHistTotal = 4096 + kSelCoarse;
+constexpr int kSelHistTotal = kSelFine + kSelCoarse;
 
 // the per-token Top-K rule: keep row i iff key_i > tk or (key_i == tk and i <= ti),
 // key = bits(|x_i|); value x_i * scale
@@ -169,17 +186,17 @@ __device__ __forceinline__ int warp_sum_int(int v) {
     return v;
 }
 __device__ __forceinline__ uint32_t key_of(float v) { return __float_as_uint(v) & 0x7fffffffu; }
-// producer side of a site: element i of value v.  Fine-bin count (its old value is the
-// pool slot), coarse-bin count (warp-aggregated: a few exponents hold most elements), the
-// (key, i) pool entry and the 16-bit key.
+// producer side of a site: element i of value v.  Fine-bin count of its 16-bit key (the old
+// value is the pool slot), coarse-bin count (warp-aggregated: a few exponents hold most
+// elements), the (key, i) pool entry and the 16-bit key.
 __device__ __forceinline__ void hist_push(const SiteSel& o, float v, int i) {
-    const uint32_t key = key_of(v), bin = key >> 19;
-    const uint32_t slot = atomicAdd(o.hist + bin, 1u);
-    if (slot < (uint32_t)kPoolCap) o.pool[(size_t)bin * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
+    const uint32_t key = key_of(v), k16 = key >> 15;
+    const uint32_t slot = atomicAdd(o.hist + k16, 1u);
+    if (slot < (uint32_t)kPoolCap) o.pool[(size_t)k16 * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
     const unsigned am = __activemask();
-    const unsigned peers = __match_any_sync(am, bin >> 4);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + 4096 + (bin >> 4), __popc(peers));
-    o.x16[i] = (uint16_t)(key >> 15);
+    const unsigned peers = __match_any_sync(am, k16 >> 8);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + kSelFine + (k16 >> 8), __popc(peers));
+    o.x16[i] = (uint16_t)k16;
 }
 
 // cp.async (LDGSTS): 16 bytes global -> shared, L1 bypass (.cg)
@@ -229,8 +246,6 @@ __device__ __forceinline__ float rms_scale_from_parts(const float* parts, int n,
 // Histograms in shared memory are padded (one word per 16 bins) so that a thread reading
 // its 16 consecutive bins is bank-conflict free.
 __host__ __device__ constexpr int hpad(int b) { return b + (b >> 4); }
-constexpr int kSelHistWords = 1024 + 1024 / 16;   // refinement histograms (<= 1024 bins)
-constexpr int kSelCandCap = kPoolCap;
 
 // Suffix search over `nb` (<= 4096, multiple of 16 or < 16 per thread) padded bins
 // (bins[hpad(nb-1)] = largest keys): the bin holding the rem-th largest key.  Thread t owns
@@ -266,47 +281,216 @@ __device__ void suffix_find(const int* bins, int nb, int rem, int* misc, int* sc
     __syncthreads();
 }
 
-// ---- SELECT prologue (batch 1): exact Top-K rule + this CTA's balanced share of rows ------
-// Shared memory (region A, aliased later by the weight ring): the staged 16-bit keys [d], a
-// padded refinement histogram, the bucket's candidates, per-word keep masks.
-// the CTA's own words: every n_splits-th 32-index word (at most kSelMaxWords)
+// ---- the exact rule of a site (one CTA, NT threads, after every producer has pushed) ------
+// Fast path, one warp, no block barrier:
+//  1. coarse suffix search (256 bins of key bits 30:23, 8 per lane) -> coarse bucket; the
+//     same over its 256 fine bins (bits 30:15) -> the 16-bit bucket b16 of the k-th key and
+//     rem = how many of it to keep;
+//  2. if b16 is not taken whole and holds <= kPoolCap elements: lane l ranks pool entries
+//     l and l + 32 exactly (key desc, index asc) -> the rem-th one is (tk, ti); the bucket's
+//     entries with their keep bits form the consumers' boundary table;
+//  3. otherwise (rare: more than kPoolCap elements share the 16-bit key, e.g. constant
+//     vectors): block-wide radix refinement over bits [14:7], [6:0] of x, then an index walk.
+// The RMS scale (fixed-order sum of the slice partials) comes from another warp.
+__host__ __device__ constexpr size_t rule_scratch_bytes() { return (size_t)(16 + 272 + 16) * 4 + 64; }
+
+// warp-wide suffix search over 256 bins at `bins` (global, 16-byte aligned; bin 255 = largest
+// keys): the bin holding the rem-th largest element.  Returns true and (bin, rem in bin,
+// count) on every lane; false if the bins hold fewer than rem elements.
+__device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, int& bin, int& rem_in, int& cnt) {
+    const int lane = threadIdx.x & 31;
+    const uint4* p = reinterpret_cast<const uint4*>(bins + 256 - 8 * (lane + 1));
+    const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+    const int c[8] = {(int)a.x, (int)a.y, (int)a.z, (int)a.w, (int)b.x, (int)b.y, (int)b.z, (int)b.w};
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum += c[j];
+    const int incl = warp_incl_scan(sum);
+    const int before = incl - sum;
+    int mb = 0, mr = 0, mc = 0;
+    const bool mine = sum > 0 && before < rem && rem <= incl;
+    if (mine) {
+        int accu = before;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            if (accu >= 0 && accu + c[j] >= rem) {
+                mb = 256 - 8 * (lane + 1) + j;
+                mr = rem - accu;
+                mc = c[j];
+                accu = -(1 << 30);
+            }
+            accu += c[j];
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+    if (!bal) return false;
+    const int src = __ffs(bal) - 1;
+    bin = __shfl_sync(0xffffffffu, mb, src);
+    rem_in = __shfl_sync(0xffffffffu, mr, src);
+    cnt = __shfl_sync(0xffffffffu, mc, src);
+    return true;
+}
+
+template <int NT>
+__device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
+                             unsigned char* scratch, SelRule* R) {
+    static_assert(NT >= 64, "two warps");
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
+    int* shist = misc + 16;                                 // fallback: <= 256 padded bins
+    int* scan = shist + 272;
+    float* fmisc = reinterpret_cast<float*>(misc);
+    if (wid == 1) {
+        const float sc = eps >= 0.f ? rms_scale_from_parts(sel.ssq, nssq, d, eps, lane) : 1.0f;
+        if (lane == 0) fmisc[4] = sc;
+    }
+    if (wid == 0) {
+        uint32_t tk = 0u;
+        int ti = 0x7fffffff, flags = 0, nb = 0, status = 0;
+        unsigned long long keep = 0ull;
+        int b16 = 0, rem = 0, cnt = 0;
+        if (k <= 0) {
+            flags = kRuleNone;
+            tk = 0xffffffffu;
+            ti = -1;
+        } else if (k >= d) {
+            flags = kRuleAll;
+        } else {
+            int cb = 0, r1 = 0, cc = 0, fb = 0;
+            const bool ok1 = warp_suffix256(sel.hist + kSelFine, k, cb, r1, cc);
+            const bool ok2 = ok1 && warp_suffix256(sel.hist + 256 * cb, r1, fb, rem, cnt);
+            if (!ok1 || !ok2) {
+                flags = kRuleAll;   // inconsistent histogram: keep-all (bounded, never faults)
+            } else {
+                b16 = 256 * cb + fb;
+                if (cnt == rem) {
+                    tk = (uint32_t)b16 << 15;   // the 16-bit bucket is taken whole: key >= tk
+                    flags = kRuleEdgeAll;
+                } else if (cnt <= kPoolCap) {
+                    const uint2* pool = sel.pool + (size_t)b16 * kPoolCap;
+                    const uint2 e0 = lane < cnt ? __ldcg(pool + lane) : make_uint2(0u, 0x7fffffffu);
+                    const uint2 e1 = lane + 32 < cnt ? __ldcg(pool + lane + 32) : make_uint2(0u, 0x7fffffffu);
+                    int r0 = 0, r1b = 0;
+                    for (int q = 0; q < cnt; ++q) {
+                        const uint32_t kq = __shfl_sync(0xffffffffu, q < 32 ? e0.x : e1.x, q & 31);
+                        const uint32_t iq = __shfl_sync(0xffffffffu, q < 32 ? e0.y : e1.y, q & 31);
+                        r0 += kq > e0.x || (kq == e0.x && iq < e0.y);
+                        r1b += kq > e1.x || (kq == e1.x && iq < e1.y);
+                    }
+                    const bool h0 = lane < cnt && r0 == rem - 1, h1 = lane + 32 < cnt && r1b == rem - 1;
+                    const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
+                    const int s0 = __ffs(b0 ? b0 : b1) - 1;
+                    const uint32_t hk0 = __shfl_sync(0xffffffffu, e0.x, s0), hi0 = __shfl_sync(0xffffffffu, e0.y, s0);
+                    const uint32_t hk1 = __shfl_sync(0xffffffffu, e1.x, s0), hi1 = __shfl_sync(0xffffffffu, e1.y, s0);
+                    tk = b0 ? hk0 : hk1;
+                    ti = (int)(b0 ? hi0 : hi1);
+                    nb = cnt;
+                    const unsigned k0 = __ballot_sync(0xffffffffu, lane < cnt && r0 < rem);
+                    const unsigned k1 = __ballot_sync(0xffffffffu, lane + 32 < cnt && r1b < rem);
+                    keep = (unsigned long long)k0 | ((unsigned long long)k1 << 32);
+                    if (lane < cnt) R->idx[lane] = (int)e0.y;
+                    if (lane + 32 < cnt) R->idx[lane + 32] = (int)e1.y;
+                } else {
+                    status = 1;      // overflow: block-wide fallback below
+                }
+            }
+        }
+        if (lane == 0) {
+            misc[0] = status;
+            misc[1] = b16;
+            misc[2] = rem;
+            misc[3] = cnt;
+            if (!status) {
+                R->tk = tk;
+                R->ti = ti;
+                R->flags = flags;
+                R->nb = nb;
+                R->keep = keep;
+            }
+        }
+    }
+    __syncthreads();
+    if (misc[0]) {
+        // fallback: radix refinement of the 16-bit bucket over x, then the index walk
+        uint32_t prefix = (uint32_t)misc[1] << 15, pmask = 0xffffu << 15;
+        int rem = misc[2], cnt = misc[3];
+#pragma unroll 1
+        for (int pass = 0; pass < 2 && cnt != rem; ++pass) {
+            const int sh = pass == 0 ? 7 : 0;
+            const int nbins = pass == 0 ? 256 : 128;
+            const uint32_t dm = (uint32_t)(nbins - 1);
+            for (int i = tid; i < hpad(nbins - 1) + 1; i += NT) shist[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < d; i += NT) {
+                const uint32_t key = key_of(__ldcg(x + i));
+                if ((key & pmask) == prefix) atomicAdd(&shist[hpad((key >> sh) & dm)], 1);
+            }
+            __syncthreads();
+            suffix_find<NT>(shist, nbins, rem, misc + 8, scan);
+            prefix |= (uint32_t)misc[8] << sh;
+            pmask |= dm << sh;
+            rem = misc[9];
+            cnt = misc[10];
+            __syncthreads();
+        }
+        int ti = 0x7fffffff;
+        if (cnt != rem) {
+            if (wid == 0) {
+                int seen = 0, at = -1;
+                for (int i0 = 0; i0 < d; i0 += 32) {
+                    const int i = i0 + lane;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, i < d && key_of(__ldcg(x + i)) == prefix);
+                    if (seen + __popc(bal) >= rem) {
+                        uint32_t m = bal;
+                        for (int q = 1; q < min(rem - seen, 32); ++q) m &= m - 1;
+                        at = i0 + __ffs(m) - 1;
+                        break;
+                    }
+                    seen += __popc(bal);
+                }
+                if (lane == 0) misc[11] = at;
+            }
+            __syncthreads();
+            ti = misc[11];
+        }
+        if (tid == 0) {
+            R->tk = prefix;
+            R->ti = ti;
+            R->flags = kRuleExact;
+            R->nb = 0;
+            R->keep = 0ull;
+        }
+    }
+    if (tid == 0) R->scale = fmisc[4];
+    __syncthreads();
+}
+
+// ---- SELECT prologue (batch 1): this CTA's rows of the site's kept set -------------------
+// Shared memory (region A, aliased later by the weight ring): the 16-bit keys of the CTA's
+// words and their keep masks / counts.  The CTA's words: w_j = split + n_splits j (32-index
+// words round-robin over the splits: balanced in expectation, robust to index-correlated
+// keep rates such as PCA-ordered channels).
 constexpr int kSelMaxWords = 256;
-__host__ __device__ constexpr size_t sel_hist_off(int d) { return (size_t)kSelMaxWords * 64; }
-__host__ __device__ constexpr size_t sel_cand_off(int d) { return sel_hist_off(d) + (size_t)kSelHistWords * 4; }
-__host__ __device__ constexpr size_t sel_mask_off(int d) { return sel_cand_off(d) + (size_t)kSelCandCap * 8; }
+__host__ __device__ constexpr size_t sel_mask_off(int d) { return (size_t)kSelMaxWords * 64; }
 __host__ __device__ constexpr size_t sel_region_bytes(int d) {
-    return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 8, 128);
+    return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 8 + rule_scratch_bytes(), 128);
 }
 __host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
     return mode == GEMV_SELECT && sel_region_bytes(d_in) > gemv_ring_bytes(bp) ? sel_region_bytes(d_in)
                                                                                : gemv_ring_bytes(bp);
 }
 
-// Returns the number of rows placed in lrow / lval (values x_i * s).
-//  1. coarse suffix scan (256 bins, one per thread) -> coarse bucket; one warp scans its 16
-//     fine bins -> fine bucket b* of the k-th key, rem = how many of it to keep;
-//  2. if b* is not taken whole: its candidates from the pool (<= kPoolCap; else the whole x)
-//     refined over key bits [18:9] and [8:0], then an index tie-break -> (tk, ti);
-//  3. keep masks per 32-element word from the 16-bit keys (exact comparison from x only
-//     where the 16-bit key equals tk's), warp prefix counts, the balanced share [P0, P1).
-__device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, float* lval, int* misc,
-                                        int split, int n_splits) {
+// Returns the number of rows placed in lrow (ascending); misc[4] receives the RMS scale.
+__device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, int* misc, int split,
+                                           int n_splits) {
     constexpr int NT = kGemvThreads, NW = kGemvWarps;
-    static_assert(NT == kSelCoarse, "one coarse bin per thread");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int d = a.d_in, k = a.sel_k;
+    const int d = a.d_in;
     uint16_t* xs = reinterpret_cast<uint16_t*>(region);
-    int* shist = reinterpret_cast<int*>(region + sel_hist_off(d));
-    uint32_t* ckey = reinterpret_cast<uint32_t*>(region + sel_cand_off(d));
-    int* cidx = reinterpret_cast<int*>(ckey + kSelCandCap);
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(region + sel_mask_off(d));
-    int* scan = misc + 8;          // block scan scratch (NW + 1)
-    float* fmisc = reinterpret_cast<float*>(misc);
+    uint32_t* wmk = reinterpret_cast<uint32_t*>(region + sel_mask_off(d));
+    int* wcnt = reinterpret_cast<int*>(wmk + kSelMaxWords);
+    int* scan = misc + 8;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t* hist = a.sel.hist;
-
-    // ---- 1. stage the 16-bit keys; coarse then fine suffix search ---------------------------
-    // this CTA's words: w_j = split + n_splits j, j < nj (their 16-bit keys, 64 B each)
     const int nwords = (d + 31) / 32;
     const int nj = nwords > split ? (nwords - 1 - split) / n_splits + 1 : 0;
     for (int c = tid; c < 4 * nj; c += NT) {
@@ -315,168 +499,32 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
         cp_async16(xs + 32 * j + 8 * (c & 3), a.sel.x16 + i0, i0 < d);
     }
     cp_async_commit();
-    const int cc = (int)__ldcg(hist + 4096 + (kSelCoarse - 1 - tid));   // thread 0: top coarse bin
-    if (wid == NW - 1) {
-        const float s = a.sel_eps >= 0.f ? rms_scale_from_parts(a.sel.ssq, a.sel_nssq, d, a.sel_eps, lane) : 1.0f;
-        if (lane == 0) fmisc[4] = s;
-    }
-    if (tid == 0) {
-        misc[0] = 0;
-        misc[1] = 0;
-        misc[2] = 0;
-        misc[5] = -1;
-        misc[60] = 0;
-    }
-    {
-        int total;
-        const int before = block_excl_scan<NT>(cc, scan, &total);
-        if (k > 0 && k < d && cc > 0 && before < k && k <= before + cc) {
-            misc[5] = kSelCoarse - 1 - tid;   // coarse bucket
-            misc[6] = k - before;             // rank inside it
-        }
-    }
-    __syncthreads();
-    if (wid == 0 && misc[5] >= 0) {
-        const int cb = misc[5], r1 = misc[6];
-        const int f = lane < 16 ? (int)__ldcg(hist + 16 * cb + 15 - lane) : 0;   // lane 0: top fine bin
-        const int inc = warp_incl_scan(f);
-        if (f > 0 && inc - f < r1 && r1 <= inc) {
-            misc[0] = 16 * cb + 15 - lane;
-            misc[1] = r1 - (inc - f);
-            misc[2] = f;
-        }
-    }
-    __syncthreads();
-    tl_stamp(a.tl, 5);
-
-    // ---- 2. the rule (tk, ti): keep i iff key > tk or (key == tk and i <= ti) ----------------
-    uint32_t tk = 0u;
-    int ti = 0x7fffffff;
-    bool all = false, none = false;
-    if (k <= 0) {
-        none = true;
-    } else if (k >= d) {
-        all = true;
-    } else {
-        const int bstar = misc[0] & (kSelBins - 1);
-        int rem = misc[1], cnt = misc[2];
-        uint32_t prefix = (uint32_t)bstar << kSelShift, pmask = 0xfffu << kSelShift;
-        if (cnt != rem) {
-            // the bucket's candidates: from the producer's pool, or (bucket larger than the
-            // pool, e.g. constant vectors) every element of x (slow path)
-            const bool pooled = cnt <= kPoolCap;
-            const int ncand = cnt;
-            if (tid == 0) misc[60] = pooled ? ncand : 0;   // (misc[8..16] is scan scratch)
-            if (pooled) {
-                const uint2* pool = a.sel.pool + (size_t)bstar * kPoolCap;
-                for (int t = tid; t < cnt; t += NT) {
-                    const uint2 e = __ldcg(pool + t);
-                    ckey[t] = e.x;
-                    cidx[t] = (int)e.y;
-                }
-            }
-            // refine over bits [18:9] (1024 bins) then [8:0] (512 bins)
-#pragma unroll 1
-            for (int pass = 0; pass < 2 && cnt != rem; ++pass) {
-                const int sh = pass == 0 ? 9 : 0;
-                const int nb = pass == 0 ? 1024 : 512;
-                const uint32_t dm = (uint32_t)(nb - 1);
-                for (int i = tid; i < hpad(nb - 1) + 1; i += NT) shist[i] = 0;
-                __syncthreads();
-                const int n = pooled ? ncand : d;
-                for (int i = tid; i < n; i += NT) {
-                    const uint32_t key = pooled ? ckey[i] : key_of(__ldcg(a.x + i));
-                    if ((key & pmask) == prefix) atomicAdd(&shist[hpad((key >> sh) & dm)], 1);
-                }
-                __syncthreads();
-                suffix_find<NT>(shist, nb, rem, misc, scan);
-                prefix |= (uint32_t)misc[0] << sh;
-                pmask |= dm << sh;
-                rem = misc[1];
-                cnt = misc[2];
-                __syncthreads();
-            }
-            tk = prefix;
-            if (cnt != rem) {
-                // exact key tie at position k: ti = index of the rem-th element with key == tk
-                if (tid == 0) misc[3] = 0x7fffffff;
-                __syncthreads();
-                if (pooled) {
-                    for (int t = tid; t < ncand; t += NT) {
-                        if (ckey[t] != tk) continue;
-                        const int it = cidx[t];
-                        int r = 0;
-                        for (int q = 0; q < ncand; ++q) r += (ckey[q] == tk && cidx[q] < it);
-                        if (r == rem - 1) misc[3] = it;
-                    }
-                } else if (wid == 0) {
-                    // slow path: one warp walks x in index order
-                    int seen = 0;
-                    for (int i0 = 0; i0 < d; i0 += 32) {
-                        const int i = i0 + lane;
-                        const uint32_t bal = __ballot_sync(0xffffffffu, i < d && key_of(__ldcg(a.x + i)) == tk);
-                        if (seen + __popc(bal) >= rem) {
-                            uint32_t m = bal;   // the (rem - seen)-th set bit
-                            for (int q = 1; q < min(rem - seen, 32); ++q) m &= m - 1;
-                            if (lane == 0) misc[3] = i0 + __ffs(m) - 1;
-                            break;
-                        }
-                        seen += __popc(bal);
-                    }
-                }
-                __syncthreads();
-                ti = misc[3];
-            }
-        } else {
-            tk = prefix;           // bucket b* taken whole: key >= b* << 19
-        }
-    }
+    // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the 16-bit keys land
+    SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
+    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R);
+    const uint32_t tk = R->tk;
+    const int ti = R->ti;
+    const int flags = R->flags;
+    const int nbt = R->nb;
+    const unsigned long long keepm = R->keep;
+    const int* tab = R->idx;
+    if (tid == 0) reinterpret_cast<float*>(misc)[4] = R->scale;
+    const uint32_t t16 = tk >> 15;
     cp_async_wait<0>();
     __syncthreads();
-    tl_stamp(a.tl, 6);
-
-    // ---- 3. keep masks from the 16-bit keys, warp prefix counts, balanced share ------------
-    // A 16-bit key equal to tk's top 16 bits is decided exactly from the bucket's candidates
-    // (all such elements lie in bucket b*; table btab in shared memory), unless b* was taken
-    // whole (then every such key is >= tk) or the bucket overflowed the pool (rare: exact
-    // keys are then read from x).
-    const uint32_t t16 = tk >> 15;
-    int* btab = scan + 32;         // [n][2] (index, keep) pairs, at most 8
-    const bool edge_all = (tk & 0x7fffu) == 0u && ti == 0x7fffffff;
-    int nb_tab = 0;
-    if (!all && !none && !edge_all) {
-        if (tid == 0) misc[7] = 0;
-        __syncthreads();
-        const int ncand = misc[60];
-        for (int t = tid; t < ncand; t += NT) {
-            const uint32_t kt = ckey[t];
-            if ((kt >> 15) == t16) {
-                const int slot = atomicAdd(&misc[7], 1);
-                if (slot < 8) {
-                    const int it = cidx[t];
-                    btab[2 * slot] = it;
-                    btab[2 * slot + 1] = kt > tk || (kt == tk && it <= ti);
-                }
-            }
-        }
-        __syncthreads();
-        nb_tab = ncand > 0 ? misc[7] : 1000;   // > 8 or no candidate list: exact reads from x
-    }
+    tl_stamp(a.tl, 5);
     auto keep16 = [&](uint32_t k16, int i) -> bool {
         if (k16 != t16) return k16 > t16;
-        if (edge_all) return true;
-        if (nb_tab <= 8) {
-            for (int q = 0; q < nb_tab; ++q)
-                if (btab[2 * q] == i) return btab[2 * q + 1] != 0;
+        if (flags & kRuleEdgeAll) return true;
+        if (!(flags & kRuleExact)) {
+            for (int q = 0; q < nbt; ++q)
+                if (tab[q] == i) return (keepm >> q) & 1ull;
             return false;
         }
         const uint32_t key = key_of(__ldcg(a.x + i));
         return key > tk || (key == tk && i <= ti);
     };
-    // keep masks of the CTA's own words (one word per warp at a time), then the rows in index
-    // order: word j's kept rows start at the exclusive prefix of the word counts
-    uint32_t* wmk = wmask;               // [nj] masks
-    int* wcnt = reinterpret_cast<int*>(wmask + kSelMaxWords);   // [nj] counts
+    const bool all = flags & kRuleAll, none = flags & kRuleNone;
     for (int j = wid; j < nj; j += NW) {
         const int i = 32 * (split + n_splits * j) + lane;
         bool kp = false;
@@ -579,12 +627,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     int n_list = 0;
     if constexpr (MODE == GEMV_SELECT) {
         static_assert(BP == 1, "SELECT is the batch-1 path");
-#ifdef LAROSA_EXP_TWICE
-        n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
-        __syncthreads();
-        tl_stamp(a.tl, 3);
-#endif
-        n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
+        n_list = select_rows(a, smem, lrow, misc, split, a.n_splits);
     } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
         const int rps = (nrows + a.n_splits - 1) / a.n_splits;
@@ -708,9 +751,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();   // every warp is done with its ring (the partials alias it)
-#ifndef LAROSA_EXP_TWICE
     tl_stamp(a.tl, 3);
-#endif
 
     // fixed-order sum of the 8 warps' partials, then one fixed-point red per column
     float* part = reinterpret_cast<float*>(smem);   // [8][BP][256]
@@ -757,23 +798,18 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 // exact arithmetic of gemv_epilogue.
 constexpr int kPrepThreads = 1024;
 __global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* __restrict__ x, int d, SiteSel o) {
-    __shared__ int sh[kSelBins];
     __shared__ float sgrp[LAROSA_MAX_DIM / 32];
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < kSelBins; i += kPrepThreads) sh[i] = 0;
+    for (int i = tid; i < kSelHistTotal / 4; i += kPrepThreads) reinterpret_cast<uint4*>(o.hist)[i] = make_uint4(0, 0, 0, 0);
+    __threadfence();
     __syncthreads();
     const int ngrp = (d + 31) / 32;
     for (int g = wid; g < ngrp; g += kPrepThreads / 32) {
         const int i = g * 32 + lane;
         const float v = i < d ? x[i] : 0.f;
-        if (i < d) {
-            const uint32_t key = key_of(v), bin = key >> kSelShift;
-            const int slot = atomicAdd(&sh[bin], 1);
-            if (slot < kPoolCap) o.pool[(size_t)bin * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
-            o.x16[i] = (uint16_t)(key >> 15);
-        }
+        if (i < d) hist_push(o, v, i);
         const float w = slice_ssq_warp(v);
         if (lane == 0) sgrp[g] = w;
     }
@@ -786,12 +822,6 @@ __global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* 
             for (int w = 0; w < 8; ++w) w8[w] = 8 * s + w < ngrp ? sgrp[8 * s + w] : 0.f;
             o.ssq[s] = slice_ssq_combine(w8);
         }
-    }
-    for (int i = tid; i < kSelBins; i += kPrepThreads) o.hist[i] = (uint32_t)sh[i];
-    for (int c = tid; c < kSelCoarse; c += kPrepThreads) {
-        int t = 0;
-        for (int j = 0; j < 16; ++j) t += sh[16 * c + j];
-        o.hist[4096 + c] = (uint32_t)t;
     }
 }
 

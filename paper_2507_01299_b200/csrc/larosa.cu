@@ -421,7 +421,7 @@ static void carve_topk_gemv(Carver& c, int64_t d_in, int64_t d_out, unsigned lon
     unsigned long long* a = c.take<unsigned long long>((size_t)d_out);
     SiteSel q;
     q.hist = c.take<uint32_t>(kSelHistTotal);
-    q.pool = c.take<uint2>((size_t)kSelBins * kPoolCap);
+    q.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q.x16 = c.take<uint16_t>((size_t)d_in);
     q.ssq = c.take<float>((size_t)(d_in + kSliceCols - 1) / kSliceCols);
     if (acc) *acc = a;
@@ -825,7 +825,7 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     for (int s = 0; s < 4; ++s) {
         SiteSel& q = o->sel[s];
         q.hist = c.take<uint32_t>(kSelHistTotal);
-        q.pool = batch == 1 ? c.take<uint2>((size_t)kSelBins * kPoolCap) : nullptr;
+        q.pool = batch == 1 ? c.take<uint2>((size_t)kSelFine * kPoolCap) : nullptr;
         q.x16 = batch == 1 ? c.take<uint16_t>((size_t)din[s]) : nullptr;
         q.ssq = (s == 0 || s == 2) ? c.take<float>((size_t)batch * n_slices(L.d)) : nullptr;
     }
@@ -860,7 +860,7 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
         return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch * Hkv too large");
     const int64_t nq = w->n_q_heads * w->head_dim;
     if (p->k_h1 < 0 || p->k_h1 > w->d || p->k_h2 < 0 || p->k_h2 > nq || p->k_h3 < 0 || p->k_h3 > w->d || p->k_h4 < 0 ||
-        p->k_h4 > w->inter)
+        p->k_h4 > w->inter || p->k_next_h1 > w->d)
         return fail(LAROSA_EINVAL, "sparse_layer: a k is outside [0, D_in of its site]");
     const void* ptrs[] = {w->w_qkv, w->w_o, w->w_gu, w->w_down, w->adapter, w->b_qkv, s->resid, s->k_cache, s->v_cache};
     for (const void* q : ptrs)
@@ -1149,7 +1149,7 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     const int64_t omax = std::max(std::max(S.qkv_l, S.dl), 2 * S.il);
     q->acc = c.take<unsigned long long>((size_t)omax);
     q->sel.hist = c.take<uint32_t>(kSelHistTotal);
-    q->sel.pool = c.take<uint2>((size_t)kSelBins * kPoolCap);
+    q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q->sel.x16 = c.take<uint16_t>((size_t)dmax);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
     const int ch = attn_chunk(max_ctx, (int)S.hkv_l);
@@ -1274,3 +1274,5 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         return cuda_check(launch(attention_kernel<4>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch");
     return cuda_check(launch(attention_kernel<2>, grid, dim3(kAttnThreads), smem, st, aa), "attention launch");
 }
+
+

@@ -41,7 +41,7 @@ class LayerWeightsC(ctypes.Structure):
 
 
 class LayerPlanC(ctypes.Structure):
-    _fields_ = [("k_h1", _c_i64), ("k_h2", _c_i64), ("k_h3", _c_i64), ("k_h4", _c_i64)]
+    _fields_ = [("k_h1", _c_i64), ("k_h2", _c_i64), ("k_h3", _c_i64), ("k_h4", _c_i64), ("k_next_h1", _c_i64)]
 
 
 class LayerStateC(ctypes.Structure):
@@ -359,7 +359,7 @@ def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: 
     """One LaRoSA decoder layer in place on ``state`` (resid, KV cache)."""
     L = lib()
     wc = w.c()
-    pc = LayerPlanC(*[int(k) for k in plan])
+    pc = LayerPlanC(*[int(k) for k in plan[:5]], *([0] if len(plan) < 5 else []))
     sc = state.c()
     B = state.resid.shape[0]
     nb = L.larosa_layer_workspace_size(ctypes.byref(wc), B, state.k_cache.shape[2])
@@ -393,7 +393,7 @@ def shard_phase(w: LayerWeights, plan: Sequence[int], rank: int, world: int, pha
     """One phase of the row-sharded layer (larosa_sparse_layer_shard_phase); ``w`` holds this
     rank's shard with the FULL model dims."""
     wc = w.c()
-    pc = LayerPlanC(*[int(k) for k in plan])
+    pc = LayerPlanC(*[int(k) for k in plan[:5]], *([0] if len(plan) < 5 else []))
     sh = ShardC(rank, world)
     _check(lib().larosa_sparse_layer_shard_phase(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sh), int(phase),
                                                  _ptr(x), _ptr(resid), _ptr(out), _ptr(k_cache), _ptr(v_cache),

@@ -71,7 +71,7 @@ def main():
                 cur = a[li][k]
                 live = cur[:, 0] > 0
                 c = cur[live] - t0
-                for i, key in enumerate(["entry", "wait", "prologue", "loop", "exit", "sel_hist", "sel_rule", "sel_mask"]):
+                for i, key in enumerate(["entry", "wait", "prologue", "loop", "exit", "sel_hist", "rule_start", "sel_mask"]):
                     col = c[:, i]
                     col = col[cur[live][:, i] > 0]
                     if col.size:
