@@ -39,21 +39,28 @@ struct AttnArgs {
     uint32_t* zero_hist;   // optional histogram to re-zero (its consumer has completed)
     int zero_words;
     unsigned long long* tl;   // debug timeline slot or null
+    int cluster;           // 1: the n_chunks CTAs of a kv group form a cluster; merge via DSMEM
 };
 
 __host__ __device__ inline size_t attn_smem_bytes(int G, int hd, int chunk) {
     (void)chunk;
     // q [G][hd] + per-warp (m, l) [4][G][2] + per-warp o [4][G][hd] + new k/v bf16 [2][hd] + flag
-    return sizeof(float) * ((size_t)G * hd + 4 * (size_t)G * 2 + 4 * (size_t)G * hd) + 4 * (size_t)hd + 16;
+    // + this chunk's merged partial [G][hd + 2] (read by the cluster leader through DSMEM)
+    return sizeof(float) * ((size_t)G * hd + 4 * (size_t)G * 2 + 4 * (size_t)G * hd + (size_t)G * (hd + 2)) +
+           4 * (size_t)hd + 16;
 }
 
 // RoPE (HF rotate_half) of the pair (i, i + hd/2) at position p, in fp64
+// (inverse frequency and angle in fp64, reduced to [-pi, pi] in fp64, then fp32 sincos:
+// accurate to a few fp32 ulp at any position, without the long fp64 sincos routine)
 __device__ __forceinline__ void rope_pair(float& y1, float& y2, int i, int hd, int p, float theta) {
     const double inv_freq = exp(-(2.0 * i / hd) * log((double)theta));
-    double sn, cn;
-    sincos((double)p * inv_freq, &sn, &cn);
-    const float r1 = (float)((double)y1 * cn - (double)y2 * sn);
-    const float r2 = (float)((double)y2 * cn + (double)y1 * sn);
+    double ang = (double)p * inv_freq;
+    ang = fma(-6.283185307179586476925, rint(ang * 0.15915494309189533577), ang);
+    float sn, cn;
+    sincosf((float)ang, &sn, &cn);
+    const float r1 = fmaf(y1, cn, -y2 * sn);
+    const float r2 = fmaf(y2, cn, y1 * sn);
     y1 = r1;
     y2 = r2;
 }
@@ -80,6 +87,34 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     const int pnew = ctx - 1;                                   // the position appended this step
     const bool has_new = pnew >= start && pnew < start + n;
     uint16_t* snew = reinterpret_cast<uint16_t*>(so + 4 * G * hd);   // [2][hd] new k, v (bf16)
+    // every K/V row of this warp's positions except the one appended this step: issued
+    // BEFORE the dependency wait (earlier steps wrote them; with programmatic dependent launch
+    // these loads overlap the QKV GEMV still streaming)
+    uint32_t kr[kAttnPosPerWarp][DPL / 2], vr[kAttnPosPerWarp][DPL / 2];
+#pragma unroll
+    for (int i = 0; i < kAttnPosPerWarp; ++i) {
+        const int p = warp + 4 * i;
+#pragma unroll
+        for (int t = 0; t < DPL / 2; ++t) kr[i][t] = vr[i][t] = 0u;
+        if (p < n && start + p != pnew) {
+            const size_t off = kvbase + (size_t)(start + p) * hd + lane * DPL;
+            if constexpr (DPL == 4) {
+                const uint2 kk = *reinterpret_cast<const uint2*>(a.kc + off);
+                const uint2 vv = *reinterpret_cast<const uint2*>(a.vc + off);
+                kr[i][0] = kk.x; kr[i][1] = kk.y; vr[i][0] = vv.x; vr[i][1] = vv.y;
+            } else {
+                kr[i][0] = *reinterpret_cast<const uint32_t*>(a.kc + off);
+                vr[i][0] = *reinterpret_cast<const uint32_t*>(a.vc + off);
+            }
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
+    tl_stamp(a.tl, 1);
+    if (a.zero_hist) {
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kAttnThreads + threadIdx.x; i < a.zero_words; i += nct * kAttnThreads) a.zero_hist[i] = 0u;
+    }
     const unsigned long long* accb = a.acc + (size_t)b * a.acc_ld;
     auto yval = [&](int col) -> float {
         return fix_to_f(accb[col]) + (a.bias ? bf16f(a.bias[col]) : 0.f);
@@ -117,29 +152,17 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     }
     __syncthreads();
 
-    // issue every K/V row load of this warp's positions before any math (the new row comes
-    // from shared memory: this CTA just produced it)
-    uint32_t kr[kAttnPosPerWarp][DPL / 2], vr[kAttnPosPerWarp][DPL / 2];
+    // the new row (computed above into shared memory) replaces the stale cache entry
 #pragma unroll
     for (int i = 0; i < kAttnPosPerWarp; ++i) {
         const int p = warp + 4 * i;
-        if (p < n) {
-            const size_t off = kvbase + (size_t)(start + p) * hd + lane * DPL;
-            if (start + p == pnew) {
-                const uint32_t* sk = reinterpret_cast<const uint32_t*>(snew + lane * DPL);
-                const uint32_t* sv = reinterpret_cast<const uint32_t*>(snew + hd + lane * DPL);
+        if (p < n && start + p == pnew) {
+            const uint32_t* sk = reinterpret_cast<const uint32_t*>(snew + lane * DPL);
+            const uint32_t* sv = reinterpret_cast<const uint32_t*>(snew + hd + lane * DPL);
 #pragma unroll
-                for (int t = 0; t < DPL / 2; ++t) {
-                    kr[i][t] = sk[t];
-                    vr[i][t] = sv[t];
-                }
-            } else if constexpr (DPL == 4) {
-                const uint2 kk = *reinterpret_cast<const uint2*>(a.kc + off);
-                const uint2 vv = *reinterpret_cast<const uint2*>(a.vc + off);
-                kr[i][0] = kk.x; kr[i][1] = kk.y; vr[i][0] = vv.x; vr[i][1] = vv.y;
-            } else {
-                kr[i][0] = *reinterpret_cast<const uint32_t*>(a.kc + off);
-                vr[i][0] = *reinterpret_cast<const uint32_t*>(a.vc + off);
+            for (int t = 0; t < DPL / 2; ++t) {
+                kr[i][t] = sk[t];
+                vr[i][t] = sv[t];
             }
         }
     }
@@ -187,8 +210,10 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     }
     __syncthreads();
 
-    // merge the 4 warps (fixed order) -> this chunk's (m, l, o)
-    float* myp = a.part + ((size_t)bg * a.n_chunks + ch) * G * (hd + 2);
+    // merge the 4 warps (fixed order) -> this chunk's (m, l, o): in shared memory for the
+    // cluster leader, else in the global workspace for the last-arriving chunk CTA
+    float* spart = reinterpret_cast<float*>(sflag + 4);
+    float* myp = a.cluster ? spart : a.part + ((size_t)bg * a.n_chunks + ch) * G * (hd + 2);
     for (int i = tid; i < G * hd; i += kAttnThreads) {
         const int j = i / hd, dd = i % hd;
         float M = -INFINITY;
@@ -209,16 +234,24 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             myp[j * (hd + 2) + 1] = L;
         }
     }
-    fence_acq_rel_gpu();
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned prev = atomicAdd(&a.counters[bg], 1u);
-        sflag[0] = prev == (unsigned)(a.n_chunks - 1);
+    if (a.cluster) {
+        cluster_sync_all();                       // every chunk's partial is in its shared memory
+        if (cluster_ctarank() != 0) {
+            cluster_sync_all();                   // keep it alive until the leader has read it
+            return;
+        }
+    } else {
+        fence_acq_rel_gpu();
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned prev = atomicAdd(&a.counters[bg], 1u);
+            sflag[0] = prev == (unsigned)(a.n_chunks - 1);
+        }
+        __syncthreads();
+        if (!sflag[0]) return;
+        if (tid == 0) a.counters[bg] = 0u;
+        fence_acq_rel_gpu();
     }
-    __syncthreads();
-    if (!sflag[0]) return;
-    if (tid == 0) a.counters[bg] = 0u;
-    fence_acq_rel_gpu();
 
     // merge the chunks in order (each batch of chunk records is loaded before it is used:
     // __ldcg is a volatile load, so a load->use loop would serialise the L2 round trips)
@@ -230,11 +263,18 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             float mc[16], lc[16], oc[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-                const float* r = pb + ((size_t)(c0 + u) * G + j) * (hd + 2);
                 const bool ok = c0 + u < a.n_chunks;
-                mc[u] = ok ? __ldcg(r) : -INFINITY;
-                lc[u] = ok ? __ldcg(r + 1) : 0.f;
-                oc[u] = ok ? __ldcg(r + 2 + dd) : 0.f;
+                if (a.cluster) {   // chunk c0 + u = cluster CTA rank c0 + u (c0 == 0, n_chunks <= 8)
+                    const uint32_t r = dsmem_addr(spart + (size_t)j * (hd + 2), ok ? (uint32_t)(c0 + u) : 0u);
+                    mc[u] = ok ? dsmem_ld_f32(r) : -INFINITY;
+                    lc[u] = ok ? dsmem_ld_f32(r + 4) : 0.f;
+                    oc[u] = ok ? dsmem_ld_f32(r + 4 * (2 + dd)) : 0.f;
+                } else {
+                    const float* r = pb + ((size_t)(c0 + u) * G + j) * (hd + 2);
+                    mc[u] = ok ? __ldcg(r) : -INFINITY;
+                    lc[u] = ok ? __ldcg(r + 1) : 0.f;
+                    oc[u] = ok ? __ldcg(r + 2 + dd) : 0.f;
+                }
             }
             float Mn = M;
 #pragma unroll
@@ -256,6 +296,7 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
         a.out[(size_t)b * a.hq * hd + (size_t)(g * G + j) * hd + dd] = hv;
         if (a.out_sel.hist) hist_push(a.out_sel, hv, (g * G + j) * hd + dd);
     }
+    if (a.cluster) cluster_sync_all();             // the other chunks' shared memory may go
     // every chunk CTA of this kv group has read its q / new k, v accumulators: re-zero them
     unsigned long long* accz = a.acc + (size_t)b * a.acc_ld;
     for (int i = tid; i < G * hd; i += kAttnThreads) accz[(size_t)g * G * hd + i] = 0ull;
@@ -269,14 +310,7 @@ template <int DPL>
 __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const AttnArgs a) {
     extern __shared__ __align__(16) float asmem[];
     tl_stamp(a.tl, 0);
-    pdl_wait();
-    pdl_trigger();
-    tl_stamp(a.tl, 1);
-    if (a.zero_hist) {
-        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
-        for (int i = cta * kAttnThreads + threadIdx.x; i < a.zero_words; i += nct * kAttnThreads) a.zero_hist[i] = 0u;
-    }
-    attention_body<DPL>(a, asmem);
+    attention_body<DPL>(a, asmem);   // waits on the QKV GEMV inside, after prefetching K/V
     tl_stamp(a.tl, 4);
 }
 

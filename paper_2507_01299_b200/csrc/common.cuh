@@ -50,6 +50,27 @@ __device__ __forceinline__ void tl_stamp(unsigned long long* tl, int i) {
     }
 }
 
+// ---- thread-block clusters / distributed shared memory -----------------------------------
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `local` (this CTA's shared memory) in cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 // ---- fences ---------------------------------------------------------------------------------
 // acquire-release fence at GPU scope (the ticket / last-CTA patterns need no more than
 // this; __threadfence() is a sequentially consistent fence, ~3x slower on B200)

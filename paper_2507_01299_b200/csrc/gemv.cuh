@@ -91,6 +91,11 @@ struct SiteSel {
 constexpr int kSelFine = 65536;
 constexpr int kSelCoarse = 256;
 constexpr int kSelHistTotal = kSelFine + kSelCoarse;
+// fine bin of 16-bit key k16 at k16 (a coarse bucket's 256 fine bins are contiguous), coarse
+// bin cb at kSelFine + cb, pool entry (k16, slot) at k16 * kPoolCap + slot
+__host__ __device__ constexpr int sel_fine_idx(uint32_t k16) { return (int)k16; }
+__host__ __device__ constexpr int sel_coarse_idx(uint32_t cb) { return kSelFine + (int)cb; }
+__host__ __device__ constexpr size_t sel_pool_idx(uint32_t k16, uint32_t slot) { return (size_t)k16 * kPoolCap + slot; }
 
 // the per-token Top-K rule: keep row i iff key_i > tk or (key_i == tk and i <= ti),
 // key = bits(|x_i|); value x_i * scale
@@ -191,11 +196,11 @@ __device__ __forceinline__ uint32_t key_of(float v) { return __float_as_uint(v) 
 // elements), the (key, i) pool entry and the 16-bit key.
 __device__ __forceinline__ void hist_push(const SiteSel& o, float v, int i) {
     const uint32_t key = key_of(v), k16 = key >> 15;
-    const uint32_t slot = atomicAdd(o.hist + k16, 1u);
-    if (slot < (uint32_t)kPoolCap) o.pool[(size_t)k16 * kPoolCap + slot] = make_uint2(key, (uint32_t)i);
+    const uint32_t slot = atomicAdd(o.hist + sel_fine_idx(k16), 1u);
+    if (slot < (uint32_t)kPoolCap) o.pool[sel_pool_idx(k16, slot)] = make_uint2(key, (uint32_t)i);
     const unsigned am = __activemask();
     const unsigned peers = __match_any_sync(am, k16 >> 8);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + kSelFine + (k16 >> 8), __popc(peers));
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + sel_coarse_idx(k16 >> 8), __popc(peers));
     o.x16[i] = (uint16_t)k16;
 }
 
@@ -294,13 +299,15 @@ __device__ void suffix_find(const int* bins, int nb, int rem, int* misc, int* sc
 // The RMS scale (fixed-order sum of the slice partials) comes from another warp.
 __host__ __device__ constexpr size_t rule_scratch_bytes() { return (size_t)(16 + 272 + 16) * 4 + 64; }
 
-// warp-wide suffix search over 256 bins at `bins` (global, 16-byte aligned; bin 255 = largest
-// keys): the bin holding the rem-th largest element.  Returns true and (bin, rem in bin,
-// count) on every lane; false if the bins hold fewer than rem elements.
+// warp-wide suffix search over 256 contiguous bins (bin 255 = largest keys; two 16-byte loads
+// per lane through L1, so the CTAs sharing an SM hit): the bin holding the rem-th largest
+// element.  Returns true and (bin, rem in bin, count) on every lane; false if the bins hold
+// fewer than rem elements.
 __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, int& bin, int& rem_in, int& cnt) {
     const int lane = threadIdx.x & 31;
-    const uint4* p = reinterpret_cast<const uint4*>(bins + 256 - 8 * (lane + 1));
-    const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+    const int j0 = 256 - 8 * (lane + 1);
+    const uint4* p = reinterpret_cast<const uint4*>(bins + j0);
+    const uint4 a = __ldca(p), b = __ldca(p + 1);
     const int c[8] = {(int)a.x, (int)a.y, (int)a.z, (int)a.w, (int)b.x, (int)b.y, (int)b.z, (int)b.w};
     int sum = 0;
 #pragma unroll
@@ -314,7 +321,7 @@ __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, in
 #pragma unroll
         for (int j = 7; j >= 0; --j) {
             if (accu >= 0 && accu + c[j] >= rem) {
-                mb = 256 - 8 * (lane + 1) + j;
+                mb = j0 + j;
                 mr = rem - accu;
                 mc = c[j];
                 accu = -(1 << 30);
@@ -367,9 +374,9 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
                     tk = (uint32_t)b16 << 15;   // the 16-bit bucket is taken whole: key >= tk
                     flags = kRuleEdgeAll;
                 } else if (cnt <= kPoolCap) {
-                    const uint2* pool = sel.pool + (size_t)b16 * kPoolCap;
-                    const uint2 e0 = lane < cnt ? __ldcg(pool + lane) : make_uint2(0u, 0x7fffffffu);
-                    const uint2 e1 = lane + 32 < cnt ? __ldcg(pool + lane + 32) : make_uint2(0u, 0x7fffffffu);
+                    const uint2 e0 = lane < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane)) : make_uint2(0u, 0x7fffffffu);
+                    const uint2 e1 = lane + 32 < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane + 32))
+                                                     : make_uint2(0u, 0x7fffffffu);
                     int r0 = 0, r1b = 0;
                     for (int q = 0; q < cnt; ++q) {
                         const uint32_t kq = __shfl_sync(0xffffffffu, q < 32 ? e0.x : e1.x, q & 31);
