@@ -147,6 +147,7 @@ struct GemvArgs {
     int zero_words;
     unsigned long long* tl;            // debug timeline slot (5 x u64) or null
     int sel_dbg;                       // profiling: bitmask of select phases to skip (0 = none)
+    int tc_dbg;                        // profiling (tcgen05 GEMV): 1 skip MMAs, 2 skip values, 4 skip A copies
 };
 
 __host__ __device__ constexpr size_t gemv_align(size_t v, size_t a) { return (v + a - 1) / a * a; }

@@ -17,6 +17,7 @@
 #include "attention.cuh"
 #include "aux.cuh"
 #include "fold_tc.cuh"
+#include "gemv_tc.cuh"
 
 using namespace larosa;
 
@@ -196,7 +197,56 @@ larosa_status launch_gemv_bp(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     }
 }
 
+// ---- batch >= 8: the tcgen05 GEMV (gemv_tc.cuh), 128-column slices -------------------------
+bool use_tc_gemv(int bp) {
+    static const int v = env_int("LAROSA_GEMV_TC", 1);
+    return v != 0 && bp >= 8;
+}
+GemvPlan plan_gemv_tc(int64_t d_out, int64_t rows_src) {
+    GemvPlan p;
+    p.n_slices = (int)((d_out + kTcCols - 1) / kTcCols);
+    const int target = sm_count() * 2;
+    const int by_target = std::max(1, target / p.n_slices);
+    const int by_rows = (int)std::max<int64_t>(1, rows_src / 64);
+    const int by_cap = (int)std::max<int64_t>(1, (rows_src + 8191) / 8192);   // <= 8192 rows per CTA
+    p.n_splits = std::max(by_cap, std::min(by_target, by_rows));
+    p.list_cap = (int)std::max<int64_t>(64, (rows_src + p.n_splits - 1) / p.n_splits + 1);
+    p.smem = gemv_tc_smem_bytes(p.list_cap);
+    return p;
+}
+template <int BP, int MODE>
+larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
+    const int64_t rows_src = MODE == GEMV_LIST ? (a.nrows_dev ? a.d_in : a.nrows) : a.d_in;
+    const GemvPlan p = plan_gemv_tc(a.d_out, rows_src);
+    auto kern = gemv_tc_kernel<BP, MODE>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv_tc)"));
+        attr_done = true;
+    }
+    if (p.smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "gemv_tc: shared memory plan %zu B too large", p.smem);
+    GemvArgs aa = a;
+    aa.n_splits = p.n_splits;
+    aa.list_cap = p.list_cap;
+    static const int tc_dbg = env_int("LAROSA_TC_DBG", 0);   // profiling only
+    aa.tc_dbg = tc_dbg;
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kTcThreads), p.smem, st, aa), "gemv_tc launch");
+}
+template <int BP>
+larosa_status launch_gemv_tc(const GemvArgs& a, cudaStream_t st) {
+    switch (a.mode) {
+        case GEMV_LIST: return launch_gemv_tc_bm<BP, GEMV_LIST>(a, st);
+        case GEMV_DENSE: return launch_gemv_tc_bm<BP, GEMV_DENSE>(a, st);
+        case GEMV_THRESH: return launch_gemv_tc_bm<BP, GEMV_THRESH>(a, st);
+        default: return fail(LAROSA_EUNSUPPORTED, "gemv_tc: bad mode");
+    }
+}
+
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
+    if (use_tc_gemv(bp) && a.mode != GEMV_SELECT && (a.epi != EPI_SILU || true)) {
+        if (bp == 8) return launch_gemv_tc<8>(a, st);
+        return launch_gemv_tc<16>(a, st);
+    }
     switch (bp) {
         case 1: return launch_gemv_bp<1>(a, p, st);
         case 2: return launch_gemv_bp<2>(a, p, st);
@@ -414,6 +464,7 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     a.ld = ld;
     a.d_out = (int)d_out;
     a.mode = GEMV_LIST;
+    a.d_in = (int)d_in;                  // bounds the union's row count (tcgen05 plan)
     a.batch = batch;
     a.acc = acc;
     a.acc_ld = d_out;
