@@ -398,7 +398,8 @@ def dense_block(r, w, cfg, k_cache, v_cache, pos: int, kv_bf16: bool = False):
     return r, {"h1": h1, "h2": h2, "h3": h3, "h4": h4, "q": q}
 
 
-def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf16: bool = False):
+def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf16: bool = False,
+                 adapter_in_down: bool = False):
     """The LaRoSA layer on folded weights, step by step as Fig. 2 and
     eqs. before/after_merge (P:402-411):
 
@@ -411,7 +412,13 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
       adapter: r_next = r A_l, A_l = Q_l^T Q_{l+1}   (Z20)
 
     ``wf``: dict of float64 folded matrices wqkv/wo/wg/wu/wd (+ bqkv);
-    ``ks``: (k1, k2, k3, k4).  Returns (r_next, intermediates incl. idx per site)."""
+    ``ks``: (k1, k2, k3, k4).  Returns (r_next, intermediates incl. idx per site).
+
+    ``adapter_in_down``: the adapter is folded into the down projection's output side,
+    wd = Wd Q_{l+1} = (Wd Q_l) A_l (the "4-gather form"; reading R4).
+    By linearity of the adapter, (r_mid + y_down Q_l-basis) A_l = r_mid A_l + y_down',
+    so r_next = r_mid A_l + h4[S4] wd; the down site's selection S4 is unchanged (it is taken
+    on h4, before the projection)."""
     hq, hkv, hd, eps, theta = cfg["hq"], cfg["hkv"], cfg["hd"], cfg["eps"], cfg["theta"]
     k1, k2, k3, k4 = ks
     out = {}
@@ -431,7 +438,14 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
     v3 = r[s3] * rms_scale(r, eps)
     h4 = silu(sparse_gemv(wf["wg"], s3, v3)) * sparse_gemv(wf["wu"], s3, v3)
     s4 = topk(h4, k4)
-    r = r + sparse_gemv(wf["wd"], s4, h4[s4])
+    y_down = sparse_gemv(wf["wd"], s4, h4[s4])
+    if adapter_in_down:
+        if adapter is None:
+            raise ValueError("adapter_in_down needs the adapter A_l")
+        r = rotate(r_mid, adapter) + y_down
+        out.update(idx1=s1, idx2=s2, idx3=s3, idx4=s4, q=q, h2=h2, r_mid=r_mid, h4=h4, r_out=None)
+        return r, out
+    r = r + y_down
     out.update(idx1=s1, idx2=s2, idx3=s3, idx4=s4, q=q, h2=h2, r_mid=r_mid, h4=h4, r_out=r.copy())
     if adapter is not None:
         r = rotate(r, adapter)

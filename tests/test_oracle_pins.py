@@ -376,14 +376,14 @@ def _toy_layer(seed, d=64, inter=128, hq=4, hkv=2, hd=16, bias=False):
     return w, cfg
 
 
-def _fold_layer(w, q_l):
+def _fold_layer(w, q_l, q_down=None):
     wqkv = np.concatenate([w["wq"], w["wk"], w["wv"]], axis=1)
     wf = {
         "wqkv": O.fold_left_qt(q_l, wqkv, w["gamma1"]),
         "wo": O.fold_right_q(w["wo"], q_l),
         "wg": O.fold_left_qt(q_l, w["wg"], w["gamma2"]),
         "wu": O.fold_left_qt(q_l, w["wu"], w["gamma2"]),
-        "wd": O.fold_right_q(w["wd"], q_l),
+        "wd": O.fold_right_q(w["wd"], q_l if q_down is None else q_down),
     }
     if "bq" in w:
         wf["bqkv"] = np.concatenate([w["bq"], w["bk"], w["bv"]])
@@ -414,6 +414,33 @@ def test_block_p0_equals_dense_two_layers(bias):
         assert np.linalg.norm(rr - r @ qs[l + 1]) <= 1e-10 * np.linalg.norm(r)
     # the rotated embedding/head folds cancel: r_L Q_L^T is the dense output
     assert np.allclose(rr @ qs[2].T, r, atol=1e-10 * np.linalg.norm(r))
+
+
+@pytest.mark.parametrize("p", [0.0, 0.5])
+def test_block_adapter_in_down_equals_adapter_form(p):
+    """The adapter folded into the down projection (wd = Wd Q_{l+1}) equals the
+    paper's literal form r_next = (r_mid + y_down) A_l (Z20) at any sparsity: the same
+    index sets at every site and r_next within 1e-12 relative (fp64, linearity of A_l).  At
+    p = 0 both reproduce the dense layer rotated into Q_{l+1}'s basis."""
+    d, ctx = 64, 6
+    w, cfg = _toy_layer(700, bias=True)
+    q0, q1 = (synth.haar_orthogonal(d, 710 + i).numpy() for i in range(2))
+    rng = np.random.default_rng(3)
+    kc, vc = rng.standard_normal((2, ctx, 16)), rng.standard_normal((2, ctx, 16))
+    r = rng.standard_normal(d) * (1 + 5 * (rng.random(d) < 0.05))
+    ks = O.site_ks(p, (1, 1, 1, 1), d, 128)
+    a = O.residual_adapter(q0, q1)
+    lit, i_lit = O.larosa_block(r @ q0, _fold_layer(w, q0), cfg, ks, kc.copy(), vc.copy(), ctx - 1, adapter=a)
+    mrg, i_mrg = O.larosa_block(r @ q0, _fold_layer(w, q0, q1), cfg, ks, kc.copy(), vc.copy(), ctx - 1, adapter=a,
+                                adapter_in_down=True)
+    for site in ("idx1", "idx2", "idx3", "idx4"):
+        assert np.array_equal(i_lit[site], i_mrg[site])
+    assert np.linalg.norm(mrg - lit) <= 1e-12 * np.linalg.norm(lit)
+    if p == 0.0:
+        ref, _ = O.dense_block(r, w, cfg, kc.copy(), vc.copy(), ctx - 1)
+        assert np.linalg.norm(mrg - ref @ q1) <= 1e-10 * np.linalg.norm(ref)
+    with pytest.raises(ValueError):
+        O.larosa_block(r @ q0, _fold_layer(w, q0, q1), cfg, ks, kc.copy(), vc.copy(), ctx - 1, adapter_in_down=True)
 
 
 def test_block_exact_sparsity_and_monotone_error():
