@@ -114,7 +114,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ oracle leg
-def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0):
+def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0, merged: bool = True):
     """Time the fp64 oracle (as it stands) on the same block workload: widened folded-like
     bf16 weights, n_tokens decode steps.  Returns (tok/s, seconds, threads)."""
     import oracle as O
@@ -141,7 +141,8 @@ def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0):
     r = synth.residual_activation(1, d, seed=1).numpy()[0].astype(np.float64)
     t0 = time.perf_counter()
     for _ in range(n_tokens):
-        r, _ = O.larosa_block(r, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True)
+        r, _ = O.larosa_block(r, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True,
+                              adapter_in_down=merged)
     dt = time.perf_counter() - t0
     return n_tokens / dt, dt, threads
 
@@ -167,13 +168,13 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------ GPU leg
-def build_stack(shape, device, n_copies, seed=0):
+def build_stack(shape, device, n_copies, seed=0, merged=True):
     from paper_2507_01299_b200 import model as M
     qs = [synth.haar_orthogonal(shape.d, seed=100 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
     layers = []
     for i in range(n_copies):
         orig = M.synth_original_layer(shape, seed + i + 1, device=device)
-        layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1]))
+        layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged))
         del orig
     torch.cuda.synchronize()
     return layers
@@ -184,13 +185,19 @@ def time_gemv_sites(layers, plan, shape, device, reps=48):
     exact kernel of the layer step: fused Top-K prologue + kept-row stream + epilogue) per
     site, on selection data prepared once per input (larosa_topk_sparse_gemv prepared=1),
     back-to-back launches (PDL) in a CUDA graph, cycling the layer copies (weights >> L2) and
-    8 inputs; CUDA events on the launching stream.  The adapter site runs at k = D."""
+    8 inputs; CUDA events on the launching stream.  The adapter site runs at k = D; with the
+    adapter folded beside the down projection it is the dense companion of the down launch
+    (larosa_topk_sparse_gemv_dense2), as in the layer."""
     from paper_2507_01299_b200 import larosa as LZ
     k1, k2, k3, k4 = plan
     nq = shape.hq * shape.hd
     sites = [("qkv", "w_qkv", shape.d, shape.qkv_out, k1, shape.rms_eps), ("o", "w_o", nq, shape.d, k2, -1.0),
              ("gate_up", "w_gu", shape.d, 2 * shape.inter, k3, shape.rms_eps),
              ("down", "w_down", shape.inter, shape.d, k4, -1.0), ("adapter", "adapter", shape.d, shape.d, shape.d, -1.0)]
+    merged = layers[0].adapter_in_down
+    if merged:
+        sites[3] = ("down+adapter", "w_down", shape.inter, shape.d, k4, -1.0)
+        sites = sites[:4]
     res = {}
     stream = torch.cuda.current_stream()
     n_in = 8
@@ -198,14 +205,22 @@ def time_gemv_sites(layers, plan, shape, device, reps=48):
         xs = [synth.residual_activation(1, din, seed=500 + r)[0].to(device) for r in range(n_in)]
         wss = [LZ.topk_sparse_gemv_workspace(din, dout, device) for _ in range(n_in)]
         y = torch.empty((dout,), dtype=torch.float32, device=device)
+        dense2 = name == "down+adapter"
+        x2s = [synth.residual_activation(1, shape.d, seed=600 + r)[0].to(device) for r in range(n_in)] if dense2 else None
+
+        def call(i, lw, prepared):
+            if dense2:
+                LZ.topk_sparse_gemv_dense2(xs[i], k, lw.w_down, x2s[i], lw.adapter, out=y, ws=wss[i], prepared=prepared)
+            else:
+                LZ.topk_sparse_gemv(xs[i], k, getattr(lw, attr), rms_eps=eps, out=y, ws=wss[i], prepared=prepared)
+
         for i in range(n_in):   # prepare each input's selection data once
-            LZ.topk_sparse_gemv(xs[i], k, getattr(layers[0], attr), rms_eps=eps, out=y, ws=wss[i])
+            call(i, layers[0], False)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for i in range(reps):
-                LZ.topk_sparse_gemv(xs[i % n_in], k, getattr(layers[i % len(layers)], attr), rms_eps=eps, out=y,
-                                    ws=wss[i % n_in], prepared=True)
+                call(i % n_in, layers[i % len(layers)], True)
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -216,16 +231,18 @@ def time_gemv_sites(layers, plan, shape, device, reps=48):
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
         alg = k * dout * 2 + din * 2 + dout * 4      # kept rows + 16-bit keys + y
+        if dense2:
+            alg += shape.d * dout * 2 + shape.d * 4    # + every adapter row and its value
         res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_in": din, "d_out": dout}
     return res
 
 
-def decode_step_extra(device, batches=(1, 16), ps=(0.4, 0.0), reps=20):
+def decode_step_extra(device, batches=(1, 16), ps=(0.4, 0.0), reps=20, merged=True):
     """BASELINE configs[2]: the LLaMA3-8B-shaped full decode step (32 folded layers + LM head,
     greedy), KV context 256, one CUDA graph per step; tok/s per (batch, p)."""
     from paper_2507_01299_b200 import model as M
     shape = synth.MODELS["llama3-8b"]
-    model = M.synth_decode_model(shape, shape.layers, device, seed=1)
+    model = M.synth_decode_model(shape, shape.layers, device, seed=1, adapter_in_down=merged)
     out = {}
     for B in batches:
         run = M.DecodeRunner(model, B, 256, device)
@@ -429,6 +446,9 @@ def main():
     ap.add_argument("--workload", default="block", choices=["block", "sharded-70b"],
                     help="block: LLaMA2-7B block (headline; N > 1 = replicas); sharded-70b: one LLaMA3-70B "
                          "layer row-sharded over the N ranks with NCCL all-gathers (SURVEY §8(e))")
+    ap.add_argument("--adapter", default="down", choices=["down", "separate"],
+                    help="down: adapter folded beside the down projection (one launch, larosa.h "
+                         "adapter_in_down); separate: the literal (r_mid + y_down) A_l adapter GEMV")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -449,7 +469,8 @@ def main():
     from paper_2507_01299_b200 import model as M
 
     shape = synth.MODELS["llama2-7b"]
-    layers = build_stack(shape, device, N_COPIES, seed=10 * rank)
+    merged = args.adapter == "down"
+    layers = build_stack(shape, device, N_COPIES, seed=10 * rank, merged=merged)
     kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
            synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(N_COPIES)]
     pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
@@ -525,10 +546,13 @@ def main():
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": "gemv_kernel<1, SELECT>: fused Top-K prologue + kept-row stream + epilogue; the 5 "
-                          "site launches of one block step (QKV, O, gate|up, down at their k; adapter at k = D), "
-                          "each timed back to back in a CUDA graph",
-                "algorithmic_bytes_per_step": bytes_step, "gemv_us_per_step": us_gemv, "launches_per_step": 5,
+                "kernel": "gemv_kernel<1, SELECT>: fused Top-K prologue + kept-row stream + epilogue; the "
+                          + ("4 site launches of one block step (QKV, O, gate|up at their k; down at k4 with the "
+                             "dense adapter rows as companion CTAs)" if merged else
+                             "5 site launches of one block step (QKV, O, gate|up, down at their k; adapter at k = D)")
+                          + ", each timed back to back in a CUDA graph",
+                "algorithmic_bytes_per_step": bytes_step, "gemv_us_per_step": us_gemv,
+                "launches_per_step": len(gem),
                 "peak_kind": f"{peak_kind} copy (hbm_gbs)", "per_site": gem}
 
     # ---- sparsity sweep (0-60%) and cuBLAS dense baseline ----------------------------------
@@ -545,24 +569,28 @@ def main():
 
     extras = None
     if not args.no_sweep:
-        extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device), "fold_tcgen05": fold_extra(device)}
+        extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device, merged=merged),
+                  "fold_tcgen05": fold_extra(device)}
 
     cpu = None
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
         import oracle as O
         op = O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter)
-        oracle_block_sample(shape, op, 1)
-        tok_s, dt, threads = oracle_block_sample(shape, op, 4)
+        oracle_block_sample(shape, op, 1, merged=merged)
+        tok_s, dt, threads = oracle_block_sample(shape, op, 4, merged=merged)
         cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": "4 decode tokens through one LLaMA2-7B block (fp64 numpy oracle), same p"}
 
-    launches_per_step = 6    # QKV, attention, O, gate|up, down, adapter (Top-K fused into the GEMVs)
+    # QKV, attention, O, gate|up, down (+ adapter companion CTAs, or a separate adapter GEMV);
+    # Top-K fused into the GEMVs
+    launches_per_step = 5 if merged else 6
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws_n, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
                "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "plan_k": list(plan),
                           "ctx": CTX, "batch": 1, "layer_copies": N_COPIES,
+                          "adapter": "folded beside down (one launch)" if merged else "separate GEMV",
                           "l2": "inputs larger than L2: 8 distinct layer copies (3.2 GB) cycled",
                           "parallelism": f"replicas x{ws_n}" if ws_n > 1 else "single GPU",
                           "implied_llama2_7b_32_layer_tok_s": value / ws_n / 32},

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 1
+#define LAROSA_ABI_VERSION 2
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -164,6 +164,18 @@ larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, f
                                       const uint16_t* bias, float* y, int32_t prepared, void* ws,
                                       size_t ws_bytes, larosa_stream_t stream);
 
+/* Fused Top-K + sparse GEMV plus a dense second operand into the same outputs (batch 1):
+ *   y[o] = sum_{j in S} x[j] s W[j][o] + sum_{m < d2} x2[m] W2[m][o],
+ * S and s as in larosa_topk_sparse_gemv.  This is the down site with the residual adapter
+ * folded beside it (larosa_layer_weights.adapter_in_down: x = h4, W = Wd Q_{l+1}, x2 = r_mid,
+ * W2 = A_l; P:388 by linearity).  The dense rows stream in CTAs of the same launch that need
+ * no selection rule.  W2 bf16 [d2][ld] (16-byte aligned), x2 fp32 [d2], 1 <= d2 <= 32768;
+ * the other arguments and the workspace are those of larosa_topk_sparse_gemv. */
+larosa_status larosa_topk_sparse_gemv_dense2(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                             const uint16_t* W, int64_t d_out, int64_t ld, const float* x2,
+                                             const uint16_t* W2, int64_t d2, float* y, int32_t prepared,
+                                             void* ws, size_t ws_bytes, larosa_stream_t stream);
+
 /* Introspection (host): the launch plan larosa_sparse_gemv uses for this shape.
  * info (host, 8 ints) = {columns per CTA, column slices, kept-row splits, warps per CTA,
  * cp.async ring stages per warp, rows per stage, dynamic smem bytes, CTAs}. */
@@ -193,12 +205,14 @@ larosa_status larosa_lm_head(const float* resid, int32_t batch, int64_t d, const
  *   (+bias, RoPE, append k/v at pos) -> GQA decode attention -> h2: Top-K k_h2 ->
  *   sparse GEMV W_o, r += -> h3: Top-K k_h3 of r, RMS scale -> sparse GEMV W_gate|up,
  *   h4 = SiLU(g) * u -> Top-K k_h4 -> sparse GEMV W_down, r += ->
- *   r <- r . A_l (dense adapter GEMV) unless adapter == NULL.
+ *   r <- r . A_l (dense adapter GEMV) unless adapter == NULL
+ *   (adapter_in_down: r <- r_mid A_l + y_down in the down launch, see below).
  * Weights (all bf16, Wc layout):
  *   w_qkv [d][(Hq + 2 Hkv) hd] = Q_l^T diag(gamma_attn) [Wq | Wk | Wv]
  *   b_qkv [(Hq + 2 Hkv) hd] or NULL (Qwen2.5; unchanged by an input-side fold, Z28)
  *   w_o [Hq hd][d] = Wo Q_l;  w_gu [d][2 inter] = packed Q_l^T diag(gamma_mlp) [Wg | Wu]
- *   w_down [inter][d] = Wd Q_l;  adapter [d][d] = Q_l^T Q_{l+1} or NULL.
+ *   w_down [inter][d] = Wd Q_l (Wd Q_{l+1} if adapter_in_down);
+ *   adapter [d][d] = Q_l^T Q_{l+1} or NULL.
  * Glue (not paper content): RoPE = HF rotate_half with pairs (i, i+hd/2),
  * inv_freq = theta^(-2i/hd), angle = pos * inv_freq; q-head h reads kv-head
  * floor(h Hkv / Hq); softmax scale 1/sqrt(hd) in fp32; KV cache bf16.
@@ -220,6 +234,14 @@ typedef struct {
     const uint16_t* adapter;
     int64_t d, inter, n_q_heads, n_kv_heads, head_dim;
     float rope_theta, rms_eps;
+    /* Nonzero: the adapter is folded into the down projection's output side,
+     * w_down [inter][d] = Wd Q_{l+1} (= (Wd Q_l) A_l; SURVEY §8(e) "4-gather form"), and the
+     * layer computes r_next = r_mid A_l + Top-K(h4) w_down (equal to the literal
+     * (r_mid + y_down) A_l of P:388 by linearity).  Requires adapter != NULL.  At batch 1 the
+     * dense r_mid rows of A_l stream in the same launch as the down site's kept rows (their
+     * CTAs need no selection rule and prefetch before the dependency wait); the r_out tap is
+     * not written.  0: the literal form (down folded with Q_l, separate adapter GEMV). */
+    int32_t adapter_in_down;
 } larosa_layer_weights;
 
 typedef struct {
@@ -263,7 +285,7 @@ size_t larosa_layer_workspace_size(const larosa_layer_weights* w, int32_t batch,
  * environment variable. */
 #define LAROSA_PHASES_GEMV_ONLY 0x352
 void larosa_debug_set_layer_phases(int mask);
-/* Profiling aid: device buffer of n_slots x 1024 x 8 uint64 %globaltimer stamps (ns), one
+/* Profiling aid: device buffer of n_slots x 1024 x 16 uint64 %globaltimer stamps (ns), one
  * block per kernel of a batch-1 larosa_sparse_layer call (0 QKV, 1 attention, 2 O, 3 gate|up,
  * 4 down, 5 adapter), one row per CTA (linear id < 1024): [0] entry, [1] after the dependency
  * wait, [2] after the prologue, [3] after the main loop, [4] exit.  NULL disables.

@@ -36,7 +36,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---- debug timeline (profiling aid; null pointer = off) -----------------------------------
-// Per CTA (linear id c < 1024): tl[c * 8 + i] = %globaltimer (ns) at point i: 0 entry, 1 after
+// Per CTA (linear id c < 1024): tl[c * 16 + i] = %globaltimer (ns) at point i: 0 entry, 1 after
 // griddepcontrol.wait, 2 after the prologue, 3 after the main loop, 4 exit.
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -46,7 +46,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ __forceinline__ void tl_stamp(unsigned long long* tl, int i) {
     if (tl && threadIdx.x == 0) {
         const int c = blockIdx.y * gridDim.x + blockIdx.x;
-        if (c < 1024) tl[c * 8 + i] = gtime();
+        if (c < 1024) tl[c * 16 + i] = gtime();
     }
 }
 

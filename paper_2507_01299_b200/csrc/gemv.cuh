@@ -145,6 +145,15 @@ struct GemvArgs {
     int64_t out_ssq_ld;
     uint32_t* zero_hist;               // optional: histogram words to re-zero (free by now)
     int zero_words;
+    // SELECT companion rows (batch 1): CTAs with blockIdx.y < n_splits2 stream DENSE rows of a
+    // second matrix W2 [d2][ld] with values x2 [d2] into the same output columns (the residual
+    // adapter folded next to the down projection: r_next = r_mid A_l + h4[S4] W_down Q_{l+1}).
+    // Their rows need no selection rule, so their first stages are issued before the
+    // dependency wait and they stream while the SELECT CTAs compute the rule.
+    const uint16_t* W2;
+    const float* x2;
+    int d2;
+    int n_splits2;
     unsigned long long* tl;            // debug timeline slot (5 x u64) or null
     int sel_dbg;                       // profiling: bitmask of select phases to skip (0 = none)
     int tc_dbg;                        // profiling (tcgen05 GEMV): 1 skip MMAs, 2 skip values, 4 skip A copies
@@ -341,7 +350,7 @@ __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, in
 
 template <int NT>
 __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
-                             unsigned char* scratch, SelRule* R) {
+                             unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr) {
     static_assert(NT >= 64, "two warps");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
@@ -351,6 +360,8 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
     if (wid == 1) {
         const float sc = eps >= 0.f ? rms_scale_from_parts(sel.ssq, nssq, d, eps, lane) : 1.0f;
         if (lane == 0) fmisc[4] = sc;
+        if (tl && lane == 0 && blockIdx.x + blockIdx.y * gridDim.x < 1024)
+            tl[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 10] = gtime();
     }
     if (wid == 0) {
         uint32_t tk = 0u;
@@ -366,7 +377,9 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
         } else {
             int cb = 0, r1 = 0, cc = 0, fb = 0;
             const bool ok1 = warp_suffix256(sel.hist + kSelFine, k, cb, r1, cc);
+            tl_stamp(tl, 6);
             const bool ok2 = ok1 && warp_suffix256(sel.hist + 256 * cb, r1, fb, rem, cnt);
+            tl_stamp(tl, 8);
             if (!ok1 || !ok2) {
                 flags = kRuleAll;   // inconsistent histogram: keep-all (bounded, never faults)
             } else {
@@ -398,6 +411,7 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
                     keep = (unsigned long long)k0 | ((unsigned long long)k1 << 32);
                     if (lane < cnt) R->idx[lane] = (int)e0.y;
                     if (lane + 32 < cnt) R->idx[lane + 32] = (int)e1.y;
+                    tl_stamp(tl, 9);
                 } else {
                     status = 1;      // overflow: block-wide fallback below
                 }
@@ -509,7 +523,8 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     cp_async_commit();
     // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the 16-bit keys land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
-    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R);
+    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R,
+                     a.tl);
     const uint32_t tk = R->tk;
     const int ti = R->ti;
     const int flags = R->flags;
@@ -533,29 +548,33 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
         return key > tk || (key == tk && i <= ti);
     };
     const bool all = flags & kRuleAll, none = flags & kRuleNone;
-    for (int j = wid; j < nj; j += NW) {
-        const int i = 32 * (split + n_splits * j) + lane;
-        bool kp = false;
-        if (i < d) kp = all ? true : (none ? false : keep16(xs[32 * j + lane], i));
-        const uint32_t m = __ballot_sync(0xffffffffu, kp);
-        if (lane == 0) {
-            wmk[j] = m;
-            wcnt[j] = __popc(m);
-        }
-    }
-    __syncthreads();
-    tl_stamp(a.tl, 7);
     int total;
-    const int cj = tid < nj ? wcnt[tid] : 0;
-    const int before = block_excl_scan<NT>(cj, scan, &total);
-    __syncthreads();
-    if (tid < nj) wcnt[tid] = before;
-    __syncthreads();
-    for (int j = wid; j < nj; j += NW) {
-        const uint32_t m = wmk[j];
-        if ((m >> lane) & 1u) lrow[wcnt[j] + __popc(m & lt)] = 32 * (split + n_splits * j) + lane;
+#pragma unroll 1
+    for (int rep = 0; rep < ((a.sel_dbg & 1) ? 2 : 1); ++rep) {   // profiling: run the mask + list twice
+        for (int j = wid; j < nj; j += NW) {
+            const int i = 32 * (split + n_splits * j) + lane;
+            bool kp = false;
+            if (i < d) kp = all ? true : (none ? false : keep16(xs[32 * j + lane], i));
+            const uint32_t m = __ballot_sync(0xffffffffu, kp);
+            if (lane == 0) {
+                wmk[j] = m;
+                wcnt[j] = __popc(m);
+            }
+        }
+        __syncthreads();
+        tl_stamp(a.tl, rep ? 14 : 7);
+        const int cj = tid < nj ? wcnt[tid] : 0;
+        const int before = block_excl_scan<NT>(cj, scan, &total);
+        __syncthreads();
+        if (tid < nj) wcnt[tid] = before;
+        __syncthreads();
+        for (int j = wid; j < nj; j += NW) {
+            const uint32_t m = wmk[j];
+            if ((m >> lane) & 1u) lrow[wcnt[j] + __popc(m & lt)] = 32 * (split + n_splits * j) + lane;
+        }
+        __syncthreads();   // list complete; the staged region (aliased by the ring) is dead
+        tl_stamp(a.tl, rep ? 15 : 11);
     }
-    __syncthreads();   // list complete; the staged region (aliased by the ring) is dead
     return total;
 }
 
@@ -615,12 +634,48 @@ __device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred) {
 template <int BP, int MODE>
 __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int slice = blockIdx.x, split = blockIdx.y;
+    const int slice = blockIdx.x;
+    // SELECT with companions: blockIdx.y < n_splits2 are the companion CTAs (dispatched first,
+    // so they take the slots that free up early), the rest are the SELECT splits
+    const int split = (int)blockIdx.y - (MODE == GEMV_SELECT ? a.n_splits2 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int mode = MODE;
     int* lrow = reinterpret_cast<int*>(smem + gemv_list_off(BP, mode, a.d_in));       // [cap]
     float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                        // [cap][BP]
     int* misc = reinterpret_cast<int*>(smem + gemv_misc_off(BP, mode, a.d_in, a.list_cap));
+
+    // companion CTA (SELECT mode, blockIdx.y < n_splits2): dense rows [c_lo, c_lo + n) of W2
+    bool comp = false;
+    int c_lo = 0, c_n = 0;
+    if constexpr (MODE == GEMV_SELECT) {
+        if (split < 0) {
+            comp = true;
+            const int rng = (a.d2 + a.n_splits2 - 1) / a.n_splits2;
+            c_lo = min(a.d2, (int)blockIdx.y * rng);
+            c_n = min(a.d2, c_lo + rng) - c_lo;
+        }
+    }
+    const uint16_t* Wb = comp ? a.W2 : a.W;
+    const float* xb = comp ? a.x2 : a.x;
+    const int col0 = slice * kSliceCols + lane * 8;
+    const bool lane_on = col0 < a.d_out;          // d_out % 8 == 0: a lane's chunk is all-in or all-out
+    unsigned char* mychunk = smem + (size_t)warp * kWarpRingBytes + lane * 16;
+    const uint16_t* wcol = Wb + col0;
+    // companion: the weights of the first kStages stages do not depend on the previous kernel
+    const int c_my = c_n > warp ? (c_n - warp + kGemvWarps - 1) / kGemvWarps : 0;
+    if (comp) {
+#pragma unroll
+        for (int st = 0; st < kStages; ++st) {
+            unsigned char* dst = mychunk + (size_t)st * (kStageRows * kSliceCols * 2);
+#pragma unroll
+            for (int g = 0; g < kStageRows; ++g) {
+                const int m = st * kStageRows + g;
+                const int row = m < c_my ? c_lo + warp + kGemvWarps * m : 0;
+                cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < c_my);
+            }
+            cp_async_commit();
+        }
+    }
 
     tl_stamp(a.tl, 0);
     pdl_wait();       // the row source comes from the previous kernel
@@ -635,7 +690,15 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     int n_list = 0;
     if constexpr (MODE == GEMV_SELECT) {
         static_assert(BP == 1, "SELECT is the batch-1 path");
-        n_list = select_rows(a, smem, lrow, misc, split, a.n_splits);
+        if (comp) {
+            n_list = c_n;
+            // values of the prefetched stages (list position warp + 8 m, m < kStages * kStageRows)
+            if (lane < kStages * kStageRows && lane < c_my)
+                lval[warp + kGemvWarps * lane] = __ldcg(a.x2 + c_lo + warp + kGemvWarps * lane);
+            __syncwarp();
+        } else {
+            n_list = select_rows(a, smem, lrow, misc, split, a.n_splits);
+        }
     } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
         const int rps = (nrows + a.n_splits - 1) / a.n_splits;
@@ -701,14 +764,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 
     tl_stamp(a.tl, 2);
     float sel_scale = 1.f;
-    if constexpr (MODE == GEMV_SELECT) sel_scale = reinterpret_cast<const float*>(misc)[4];
+    if constexpr (MODE == GEMV_SELECT) sel_scale = comp ? 1.f : reinterpret_cast<const float*>(misc)[4];
     // my rows: list entries warp + 8*m, m in [0, n_my)
     const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
-    const int col0 = slice * kSliceCols + lane * 8;
-    const bool lane_on = col0 < a.d_out;          // d_out % 8 == 0: a lane's chunk is all-in or all-out
     const int n_st = (n_my + kStageRows - 1) / kStageRows;
-    unsigned char* mychunk = smem + (size_t)warp * kWarpRingBytes + lane * 16;
-    const uint16_t* wcol = a.W + col0;
 
     // stage st covers my-rows [4 st, 4 st + 4)
     auto issue = [&](int st) {
@@ -717,16 +776,19 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 #pragma unroll
             for (int g = 0; g < kStageRows; ++g) {
                 const int m = st * kStageRows + g;
-                const int row = m < n_my ? lrow[warp + kGemvWarps * m] : 0;
+                const int lpos = warp + kGemvWarps * m;
+                const int row = m < n_my ? (comp ? c_lo + lpos : lrow[lpos]) : 0;
                 cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < n_my);
                 if constexpr (MODE == GEMV_SELECT)   // the row's activation rides in the same group
-                    if (lane == g && m < n_my) cp_async4(lval + warp + kGemvWarps * m, a.x + row);
+                    if (lane == g && m < n_my) cp_async4(lval + lpos, xb + row);
             }
         }
         cp_async_commit();   // one (possibly empty) group per stage keeps the count uniform
     };
+    if (!comp) {
 #pragma unroll
-    for (int st = 0; st < kStages; ++st) issue(st);
+        for (int st = 0; st < kStages; ++st) issue(st);
+    }
 
     float2 acc[BP][4];
 #pragma unroll
@@ -790,12 +852,14 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     // bar.sync order the other splits' reds before this CTA's accumulator reads)
     __syncthreads();
     if (threadIdx.x == 0) misc[0] = atom_add_acq_rel_gpu(a.tickets + slice, 1u) == gridDim.y - 1u;
+    tl_stamp(a.tl, 12);
     __syncthreads();
     if (!misc[0]) {
         tl_stamp(a.tl, 4);
         return;
     }
     if (threadIdx.x == 0) a.tickets[slice] = 0u;
+    tl_stamp(a.tl, 13);
     gemv_epilogue<BP>(a, slice, reinterpret_cast<float*>(misc + 16));
     tl_stamp(a.tl, 4);
 }

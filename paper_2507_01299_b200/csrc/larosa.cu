@@ -126,6 +126,7 @@ int pad_batch(int b) { return b <= 1 ? 1 : b <= 2 ? 2 : b <= 4 ? 4 : b <= 8 ? 8 
 struct GemvPlan {
     int n_slices, n_splits, list_cap;
     size_t smem;
+    int n_splits2 = 0;   // SELECT companion CTAs per slice (dense rows of W2)
 };
 
 int env_int(const char* name, int dflt) {
@@ -167,6 +168,25 @@ GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp, int mode = GEMV_LIST
     return p;
 }
 
+// SELECT site (k kept rows of d_in) plus d2 dense companion rows into the same d_out columns:
+// one wave of 2 CTAs per SM split between the two row sources in proportion to their bytes
+// (LAROSA_COMP_PCT overrides the companion share, in percent of the splits).
+GemvPlan plan_gemv_comp(int64_t d_out, int64_t k, int64_t d_in, int64_t d2) {
+    static const int pct_env = env_int("LAROSA_COMP_PCT", 0);
+    GemvPlan p = plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
+    const int total = std::max(2, sm_count() * 2 / p.n_slices);
+    const int64_t nwords = (d_in + 31) / 32;
+    const int min_sel = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
+    int n2 = pct_env > 0 ? (total * pct_env + 50) / 100 : (int)((double)total * d2 / (double)(k + d2) + 0.5);
+    n2 = std::max(1, std::min(n2, total - min_sel));
+    p.n_splits = std::max(min_sel, total - n2);
+    p.list_cap = (int)(32 * ((nwords + p.n_splits - 1) / p.n_splits));
+    n2 = std::max<int>(n2, (int)((d2 + p.list_cap - 1) / p.list_cap));
+    p.n_splits2 = n2;
+    p.smem = gemv_smem_bytes(1, p.list_cap, GEMV_SELECT, (int)d_in);
+    return p;
+}
+
 template <int BP, int MODE>
 larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
     auto kern = gemv_kernel<BP, MODE>;
@@ -177,9 +197,16 @@ larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     }
     if (p.smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "gemv: shared memory plan %zu B too large", p.smem);
     GemvArgs aa = a;
+    static const int sel_dbg = env_int("LAROSA_SEL_DBG", 0);   // profiling only
+    aa.sel_dbg = sel_dbg;
     aa.n_splits = p.n_splits;
+    aa.n_splits2 = p.n_splits2;
     aa.list_cap = p.list_cap;
-    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kGemvThreads), p.smem, st, aa), "gemv launch");
+    if (p.n_splits2 > 0 && (MODE != GEMV_SELECT || !a.W2 || !a.x2 || a.d2 <= 0 ||
+                            (a.d2 + p.n_splits2 - 1) / p.n_splits2 > p.list_cap))
+        return fail(LAROSA_EUNSUPPORTED, "gemv: bad companion plan");
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits + p.n_splits2), dim3(kGemvThreads), p.smem, st, aa),
+                      "gemv launch");
 }
 
 template <int BP>
@@ -517,11 +544,17 @@ extern "C" size_t larosa_topk_sparse_gemv_workspace_size(int64_t d_in, int64_t d
     return c.size();
 }
 
-extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
-                                                 const uint16_t* W, int64_t d_out, int64_t ld, const uint16_t* bias,
-                                                 float* y, int32_t prepared, void* ws, size_t ws_bytes,
-                                                 larosa_stream_t stream) {
+static larosa_status topk_sparse_gemv_impl(const float* x, int64_t d_in, int64_t k, float rms_eps, const uint16_t* W,
+                                           int64_t d_out, int64_t ld, const uint16_t* bias, const float* x2,
+                                           const uint16_t* W2, int64_t d2, float* y, int32_t prepared, void* ws,
+                                           size_t ws_bytes, cudaStream_t st) {
     if (!x || !W || !y) return fail(LAROSA_EINVAL, "topk_sparse_gemv: NULL pointer");
+    if (W2 || x2) {
+        if (!W2 || !x2) return fail(LAROSA_EINVAL, "topk_sparse_gemv_dense2: NULL pointer");
+        if (d2 <= 0 || d2 > LAROSA_MAX_DIM) return fail(LAROSA_EINVAL, "topk_sparse_gemv_dense2: d2 outside [1, %d]",
+                                                        LAROSA_MAX_DIM);
+        if (!aligned16(W2)) return fail(LAROSA_EINVAL, "topk_sparse_gemv_dense2: W2 must be 16-byte aligned");
+    }
     if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "topk_sparse_gemv: d_in, d_out must be > 0");
     if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "topk_sparse_gemv: k outside [0, d_in]");
     if (d_in > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv: d_in > %d", LAROSA_MAX_DIM);
@@ -533,7 +566,6 @@ extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, i
         return fail(LAROSA_EINVAL, "topk_sparse_gemv: pointers must be 16-byte aligned");
     const size_t need = larosa_topk_sparse_gemv_workspace_size(d_in, d_out);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "topk_sparse_gemv: workspace %zu < %zu", ws_bytes, need);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
     unsigned long long* acc;
     SiteSel sel;
@@ -542,7 +574,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, i
     if (!prepared)
         LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)d_in, sel),
                               "select prep launch"));
-    const GemvPlan p = plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
+    const GemvPlan p = W2 ? plan_gemv_comp(d_out, k, d_in, d2) : plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
     GemvArgs a = gemv_args_base();
     a.W = W;
     a.ld = ld;
@@ -563,7 +595,28 @@ extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, i
     a.bias = bias;
     a.out = y;
     a.out_ld = d_out;
+    a.W2 = W2;
+    a.x2 = x2;
+    a.d2 = (int)d2;
     return launch_gemv(a, p, 1, st);
+}
+
+extern "C" larosa_status larosa_topk_sparse_gemv(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                                 const uint16_t* W, int64_t d_out, int64_t ld, const uint16_t* bias,
+                                                 float* y, int32_t prepared, void* ws, size_t ws_bytes,
+                                                 larosa_stream_t stream) {
+    return topk_sparse_gemv_impl(x, d_in, k, rms_eps, W, d_out, ld, bias, nullptr, nullptr, 0, y, prepared, ws,
+                                 ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" larosa_status larosa_topk_sparse_gemv_dense2(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                                        const uint16_t* W, int64_t d_out, int64_t ld,
+                                                        const float* x2, const uint16_t* W2, int64_t d2, float* y,
+                                                        int32_t prepared, void* ws, size_t ws_bytes,
+                                                        larosa_stream_t stream) {
+    if (!x2 || !W2) return fail(LAROSA_EINVAL, "topk_sparse_gemv_dense2: NULL pointer");
+    return topk_sparse_gemv_impl(x, d_in, k, rms_eps, W, d_out, ld, nullptr, x2, W2, d2, y, prepared, ws, ws_bytes,
+                                 reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" larosa_status larosa_gemv_plan_info(int64_t d_out, int64_t nrows_max, int32_t batch, int32_t* info) {
@@ -932,6 +985,7 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
     if (w->d <= 0 || w->inter <= 0 || w->n_q_heads <= 0 || w->n_kv_heads <= 0 || w->head_dim <= 0)
         return fail(LAROSA_EINVAL, "sparse_layer: dims must be > 0");
     if (w->n_q_heads % w->n_kv_heads) return fail(LAROSA_ESHAPE, "sparse_layer: Hq %% Hkv != 0");
+    if (w->adapter_in_down && !w->adapter) return fail(LAROSA_EINVAL, "sparse_layer: adapter_in_down needs the adapter");
     if (w->n_q_heads / w->n_kv_heads > kAttnMaxG) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
     if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: head_dim must be 64 or 128");
     if (w->d % 8 || w->inter % LAROSA_GU_BLOCK) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: d %% 8 or inter %% 64");
@@ -1012,7 +1066,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     else
         memset(&T, 0, sizeof(T));
     const int nsl_d = n_slices(L.d);
-    auto tl_slot = [&](int i) -> unsigned long long* { return g_tl && i < g_tl_n ? g_tl + 8192 * i : nullptr; };
+    auto tl_slot = [&](int i) -> unsigned long long* { return g_tl && i < g_tl_n ? g_tl + 16384 * i : nullptr; };
 
     // exact index-list Top-K of a materialised site vector (parity taps only)
     auto tap_topk = [&](const float* x, int64_t din, int64_t k, float eps, int32_t* idx, float* vals) -> larosa_status {
@@ -1153,6 +1207,40 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     // ---- h4 -> down; epilogue r_mid + y_down (-> adapter input, or the next layer's r) ------------
     if (!fused && on(7)) LAROSA_TRY(rule_topk(3, W.h4, L.inter, plan->k_h4, -1.0f));
     LAROSA_TRY(tap_topk(W.h4, L.inter, plan->k_h4, -1.0f, T.idx_h4, T.vals_h4));
+    const bool merged = w->adapter && w->adapter_in_down;
+    if (merged && on(8)) {
+        // r_next = r_mid A_l + h4[S4] W_down Q_{l+1}: one fixed-point accumulator, finalised once
+        GemvArgs a = site_gemv(3, W.h4, L.inter, plan->k_h4, -1.0f, w->w_down, L.d, W.acc_down);
+        a.zero_hist = fused ? W.sel[2].hist : nullptr;
+        a.zero_words = kSelHistTotal;
+        a.tl = tl_slot(4);
+        if (fused) {
+            a.W2 = w->adapter;
+            a.x2 = W.rmid;
+            a.d2 = (int)L.d;
+            epi(a, 2, EPI_STORE, nullptr, s->resid, 0);
+            LAROSA_TRY(launch_gemv(a, plan_gemv_comp(L.d, plan->k_h4, L.inter, L.d), 1, st));
+        } else {
+            a.epi = EPI_NONE;
+            LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.inter, plan->k_h4), bp, st));
+            GemvArgs b = gemv_args_base();
+            b.W = w->adapter;
+            b.ld = L.d;
+            b.d_out = (int)L.d;
+            b.mode = GEMV_DENSE;
+            b.x = W.rmid;
+            b.ldx = L.d;
+            b.d_in = (int)L.d;
+            b.batch = B;
+            b.acc = W.acc_down;
+            b.acc_ld = L.d;
+            epi(b, 3, EPI_STORE, nullptr, s->resid, 0);
+            b.tl = tl_slot(5);
+            LAROSA_TRY(launch_gemv(b, plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d), bp, st));
+        }
+        return LAROSA_OK;
+    }
+    if (merged) return LAROSA_OK;   // profiling mask without the down launch
     if (on(8)) {
         GemvArgs a = site_gemv(3, W.h4, L.inter, plan->k_h4, -1.0f, w->w_down, L.d, W.acc_down);
         if (w->adapter)

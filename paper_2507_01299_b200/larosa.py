@@ -37,7 +37,7 @@ class LayerWeightsC(ctypes.Structure):
     _fields_ = [("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("w_gu", _vp), ("w_down", _vp),
                 ("adapter", _vp), ("d", _c_i64), ("inter", _c_i64), ("n_q_heads", _c_i64),
                 ("n_kv_heads", _c_i64), ("head_dim", _c_i64), ("rope_theta", ctypes.c_float),
-                ("rms_eps", ctypes.c_float)]
+                ("rms_eps", ctypes.c_float), ("adapter_in_down", _c_i32)]
 
 
 class LayerPlanC(ctypes.Structure):
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
     L.larosa_topk_sparse_gemv_workspace_size.argtypes = [_c_i64, _c_i64]
     L.larosa_topk_sparse_gemv.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp,
                                           _c_i32, _vp, ctypes.c_size_t, _vp]
+    L.larosa_topk_sparse_gemv_dense2.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp,
+                                                 _c_i64, _vp, _c_i32, _vp, ctypes.c_size_t, _vp]
     L.larosa_embed.argtypes = [_vp, _c_i64, _c_i64, _vp, _c_i32, _vp, _vp]
     L.larosa_lm_head_workspace_size.restype = ctypes.c_size_t
     L.larosa_lm_head_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64]
@@ -115,7 +117,7 @@ def lib() -> ctypes.CDLL:
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 1:
+    if L.larosa_abi_version() != 2:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -266,6 +268,27 @@ def topk_sparse_gemv(x: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = 
     return y
 
 
+def topk_sparse_gemv_dense2(x: torch.Tensor, k: int, W: torch.Tensor, x2: torch.Tensor, W2: torch.Tensor,
+                            rms_eps: float = -1.0, out: Optional[torch.Tensor] = None,
+                            ws: Optional[torch.Tensor] = None, prepared: bool = False, stream=None) -> torch.Tensor:
+    """Batch 1: y = sum_{j in TopK_k(|x|)} x_j s W[j] + sum_m x2_m W2[m] (the down site with the
+    adapter folded beside it; larosa_topk_sparse_gemv_dense2)."""
+    x = x.reshape(-1)
+    x2 = x2.reshape(-1)
+    d_in, ld = W.shape
+    d2 = W2.shape[0]
+    assert x.dtype == torch.float32 and x.numel() == d_in and x2.dtype == torch.float32 and x2.numel() == d2
+    assert W2.shape[1] == ld
+    y = out if out is not None else torch.empty((ld,), dtype=torch.float32, device=W.device)
+    L = lib()
+    nb = L.larosa_topk_sparse_gemv_workspace_size(d_in, ld)
+    if ws is None:
+        ws = _ws(("topk_sparse_gemv", d_in, ld), nb, W.device)
+    _check(L.larosa_topk_sparse_gemv_dense2(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), ld, ld, _ptr(x2), _ptr(W2),
+                                            d2, _ptr(y), int(prepared), _ptr(ws), ws.numel(), _stream(stream)))
+    return y
+
+
 def embed(E: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """resid[b] = E'[tokens[b]] (E' = E Q_0, bf16 bits [vocab, d]; tokens int32 [B] on device)."""
     vocab, d = E.shape
@@ -308,11 +331,12 @@ class LayerWeights:
     rms_eps: float
     b_qkv: Optional[torch.Tensor] = None
     adapter: Optional[torch.Tensor] = None
+    adapter_in_down: bool = False   # w_down = Wd Q_{l+1}: r_next = r_mid A_l + y_down (larosa.h)
 
     def c(self) -> LayerWeightsC:
         return LayerWeightsC(_ptr(self.w_qkv), _ptr(self.b_qkv), _ptr(self.w_o), _ptr(self.w_gu), _ptr(self.w_down),
                              _ptr(self.adapter), self.d, self.inter, self.n_q_heads, self.n_kv_heads, self.head_dim,
-                             float(self.rope_theta), float(self.rms_eps))
+                             float(self.rope_theta), float(self.rms_eps), int(self.adapter_in_down))
 
 
 @dataclass

@@ -46,10 +46,12 @@ def synth_original_layer(shape: synth.ModelShape, seed: int, device="cpu") -> Or
 
 
 def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
-               q_next: Optional[torch.Tensor]) -> LZ.LayerWeights:
+               q_next: Optional[torch.Tensor], adapter_in_down: bool = False) -> LZ.LayerWeights:
     """Offline transform of one layer (eqs. before/after_merge P:402-410, §3.2):
     W_qkv' = Q_l^T diag(g1) W_qkv;  W_o' = W_o Q_l;  W_gate|up' = Q_l^T diag(g2) [Wg | Wu]
-    (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1}.   q_l, q_next: fp32 on device."""
+    (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1}.   q_l, q_next: fp32 on device.
+    adapter_in_down (needs q_next): W_down' = W_down Q_{l+1} = (W_down Q_l) A_l, and the
+    layer computes r_next = r_mid A_l + y_down (larosa.h)."""
     dev = orig.wqkv.device
     L, R = LZ.LAROSA_LEFT_QT, LZ.LAROSA_RIGHT_Q
     g1 = orig.gamma1.to(dev, torch.float32).contiguous()
@@ -60,14 +62,16 @@ def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
     wu = LZ.fold_rotation(q_l, orig.wu, L, gamma=g2)
     w_gu = LZ.pack_gate_up(wg, wu)
     del wg, wu
-    w_down = LZ.fold_rotation(q_l, orig.wd, R)
+    merged = adapter_in_down and q_next is not None
+    w_down = LZ.fold_rotation(q_next if merged else q_l, orig.wd, R)
     adapter = None
     if q_next is not None:
         adapter = LZ.fold_rotation(q_l, synth.bf16_bits(q_next).contiguous(), L)
     return LZ.LayerWeights(w_qkv=w_qkv, w_o=w_o, w_gu=w_gu, w_down=w_down, d=shape.d, inter=shape.inter,
                            n_q_heads=shape.hq, n_kv_heads=shape.hkv, head_dim=shape.hd,
                            rope_theta=shape.rope_theta, rms_eps=shape.rms_eps,
-                           b_qkv=orig.bqkv.contiguous() if orig.bqkv is not None else None, adapter=adapter)
+                           b_qkv=orig.bqkv.contiguous() if orig.bqkv is not None else None, adapter=adapter,
+                           adapter_in_down=merged)
 
 
 def site_plan(shape: synth.ModelShape, p: float, alpha_mode: str = "uniform") -> tuple:
@@ -96,7 +100,7 @@ class DecodeModel:
 
 
 def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int = 0,
-                       vocab: Optional[int] = None) -> DecodeModel:
+                       vocab: Optional[int] = None, adapter_in_down: bool = False) -> DecodeModel:
     """Random-init model of the given shape (synthetic weights), folded with
     the library's own tensor-core fold."""
     vocab = vocab or shape.vocab
@@ -109,7 +113,8 @@ def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int
     layers = []
     for l in range(n_layers):
         orig = synth_original_layer(shape, 10 * seed + l + 1, device=device)
-        layers.append(fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None))
+        layers.append(fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None,
+                                 adapter_in_down=adapter_in_down))
         del orig
     H = synth.gaussian_bf16((d, vocab), 9100 + seed, d ** -0.5, device)
     gf = (1.0 + 0.1 * synth.gaussian((d,), 9200 + seed, device=device)).float().contiguous()

@@ -34,14 +34,15 @@ def oracle_layers(model):
         wf["wg"], wf["wu"] = unpack_gu(w64(w.w_gu), w.inter)
         if w.b_qkv is not None:
             wf["bqkv"] = w64(w.b_qkv)
-        out.append((wf, w64(w.adapter) if w.adapter is not None else None))
+        out.append((wf, w64(w.adapter) if w.adapter is not None else None, bool(w.adapter_in_down)))
     return out
 
 
-@pytest.mark.parametrize("batch,p", [(1, 0.5), (3, 0.4), (16, 0.5)])
-def test_decode_step_vs_oracle(batch, p):
+@pytest.mark.parametrize("batch,p,merged", [(1, 0.5, False), (3, 0.4, False), (16, 0.5, False), (1, 0.5, True),
+                                            (3, 0.4, True), (16, 0.5, True)])
+def test_decode_step_vs_oracle(batch, p, merged):
     shape = SMALL
-    model = M.synth_decode_model(shape, shape.layers, DEV, seed=1)
+    model = M.synth_decode_model(shape, shape.layers, DEV, seed=1, adapter_in_down=merged)
     max_ctx, ctx = 32, 9
     run = M.DecodeRunner(model, batch, max_ctx, DEV)
     g = torch.Generator().manual_seed(3)
@@ -69,8 +70,9 @@ def test_decode_step_vs_oracle(batch, p):
                   for a, c in kvs0]
         # oracle chain, layer by layer, checking index sets against the GPU taps
         r = O.embed(e_f, int(tokens[b]))
-        for l, ((wf, adp), (kc, vc)) in enumerate(zip(layers, caches)):
-            r, inter = O.larosa_block(r, wf, cfg, plan, kc, vc, int(pos[b]), adapter=adp, kv_bf16=True)
+        for l, ((wf, adp, mrg), (kc, vc)) in enumerate(zip(layers, caches)):
+            r, inter = O.larosa_block(r, wf, cfg, plan, kc, vc, int(pos[b]), adapter=adp, kv_bf16=True,
+                                      adapter_in_down=mrg)
             for s in (1, 2, 3, 4):
                 if not np.array_equal(taps[l][f"idx_h{s}"][b].cpu().numpy(), inter[f"idx{s}"]):
                     pytest.skip(f"certified near-tie swap at layer {l} site h{s} (P5, reported)")

@@ -260,3 +260,20 @@ def test_topk_sparse_gemv_repeatable():
     y0 = LZ.topk_sparse_gemv(x, 2048, Wb, rms_eps=1e-5).clone()
     for _ in range(3):
         assert torch.equal(LZ.topk_sparse_gemv(x, 2048, Wb, rms_eps=1e-5), y0)
+
+
+@pytest.mark.parametrize("d_in,d2,d_out,k", [(64, 64, 128, 32), (11008, 4096, 4096, 5504), (14336, 4096, 4096, 8602),
+                                             (1000, 333, 264, 0), (4096, 4096, 4096, 4096), (29568, 8192, 1024, 14784)])
+def test_topk_sparse_gemv_dense2_p3(d_in, d2, d_out, k):
+    """Down site with the adapter beside it (larosa_topk_sparse_gemv_dense2): Top-K rows of W
+    plus every row of W2 into the same outputs, vs the oracle's masked GEMV + dense GEMV."""
+    x = synth.residual_activation(1, d_in, seed=d_in + 3)[0]
+    x2 = synth.residual_activation(1, d2, seed=d2 + 4)[0]
+    Wb = synth.gaussian_bf16((d_in, d_out), 50 + d_in, d_in ** -0.5)
+    W2 = synth.gaussian_bf16((d2, d_out), 51 + d2, d2 ** -0.5)
+    y = LZ.topk_sparse_gemv_dense2(x.to(DEV), k, Wb.to(DEV), x2.to(DEV), W2.to(DEV))
+    ref = _fused_ref(x, k, Wb, -1.0) + O.dense_gemv(w64(W2), x2.numpy().astype(np.float64))
+    assert rel_max(f64(y), ref) <= 1e-5
+    # repeatable (fixed-point accumulation; companion CTAs finish in any order)
+    for _ in range(2):
+        assert torch.equal(LZ.topk_sparse_gemv_dense2(x.to(DEV), k, Wb.to(DEV), x2.to(DEV), W2.to(DEV)), y)

@@ -49,12 +49,12 @@ def unpack_gu(wgu, inter):
     return blk[:, :, 0, :].reshape(d, inter), blk[:, :, 1, :].reshape(d, inter)
 
 
-def build(shape, seed, batch, ctx, max_ctx, p, with_adapter=True):
+def build(shape, seed, batch, ctx, max_ctx, p, with_adapter=True, merged=False):
     orig = M.synth_original_layer(shape, seed)
     q_l = synth.haar_orthogonal(shape.d, seed=seed + 50).float()
     q_n = synth.haar_orthogonal(shape.d, seed=seed + 51).float() if with_adapter else None
     origd = M.OriginalLayer(**{k: (v.to(DEV) if v is not None else None) for k, v in orig.__dict__.items()})
-    lw = M.fold_layer(origd, shape, q_l.to(DEV), q_n.to(DEV) if q_n is not None else None)
+    lw = M.fold_layer(origd, shape, q_l.to(DEV), q_n.to(DEV) if q_n is not None else None, adapter_in_down=merged)
     plan = M.site_plan(shape, p)
     resid = synth.residual_activation(batch, shape.d, seed=seed + 60)
     kc = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), seed + 61, 1.0)
@@ -72,12 +72,17 @@ def run_layer(lw, plan, resid, kc, vc, pos):
     return st, taps
 
 
-@pytest.mark.parametrize("shape,batch,ctx,p", [(SMALL, 1, 7, 0.5), (SMALL, 3, 40, 0.4), (SMALL_MHA, 2, 100, 0.25),
-                                               (SMALL, 16, 30, 0.5), (synth.MODELS["llama2-7b"], 1, 256, 0.5),
-                                               (synth.MODELS["llama3-8b"], 4, 64, 0.4)])
-def test_layer_p6_sitewise(shape, batch, ctx, p):
+@pytest.mark.parametrize("shape,batch,ctx,p,merged", [
+    (SMALL, 1, 7, 0.5, False), (SMALL, 3, 40, 0.4, False), (SMALL_MHA, 2, 100, 0.25, False),
+    (SMALL, 16, 30, 0.5, False), (synth.MODELS["llama2-7b"], 1, 256, 0.5, False),
+    (synth.MODELS["llama3-8b"], 4, 64, 0.4, False),
+    # adapter folded into the down projection (larosa.h adapter_in_down): batch 1 companion
+    # CTAs, batch 3 (CUDA-core THRESH + DENSE), batch 16 (tcgen05), the 7B block
+    (SMALL, 1, 7, 0.5, True), (SMALL_MHA, 3, 40, 0.4, True), (SMALL, 16, 30, 0.5, True),
+    (synth.MODELS["llama2-7b"], 1, 256, 0.5, True), (synth.MODELS["llama3-8b"], 1, 64, 0.4, True)])
+def test_layer_p6_sitewise(shape, batch, ctx, p, merged):
     max_ctx = max(ctx, 64)
-    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p)
+    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p, merged=merged)
     st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
     k1, k2, k3, k4 = plan
     hq, hkv, hd, d = shape.hq, shape.hkv, shape.hd, shape.d
@@ -131,6 +136,10 @@ def test_layer_p6_sitewise(shape, batch, ctx, p):
         h4g = f64(tp["h4"][b])
         i4 = tp["idx_h4"][b].cpu().numpy()
         assert np.array_equal(i4, O.topk(h4g, k4))
+        if merged:   # r_next = r_mid A_l + h4[S4] (Wd Q_{l+1}) in one accumulator
+            rn = O.rotate(rm, A) + O.sparse_gemv(Wd, i4, h4g[i4])
+            assert rel_max(f64(st.resid[b]), rn) <= 1e-5
+            continue
         rout = rm + O.sparse_gemv(Wd, i4, h4g[i4])
         assert rel_max(f64(tp["r_out"][b]), rout) <= 1e-5
         # adapter
@@ -138,10 +147,11 @@ def test_layer_p6_sitewise(shape, batch, ctx, p):
         assert rel_max(f64(st.resid[b]), rn) <= 1e-5
 
 
-@pytest.mark.parametrize("shape,p", [(SMALL, 0.5), (synth.MODELS["llama2-7b"], 0.4)])
-def test_layer_p5_independent_chain(shape, p):
+@pytest.mark.parametrize("shape,p,merged", [(SMALL, 0.5, False), (synth.MODELS["llama2-7b"], 0.4, False),
+                                            (SMALL, 0.5, True), (synth.MODELS["llama2-7b"], 0.5, True)])
+def test_layer_p5_independent_chain(shape, p, merged):
     batch, ctx, max_ctx = 1, 33, 64
-    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 5, batch, ctx, max_ctx, p)
+    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 5, batch, ctx, max_ctx, p, merged=merged)
     st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
     wf = {"wqkv": w64(lw.w_qkv), "wo": w64(lw.w_o), "wd": w64(lw.w_down)}
     wf["wg"], wf["wu"] = unpack_gu(w64(lw.w_gu), shape.inter)
@@ -151,19 +161,21 @@ def test_layer_p5_independent_chain(shape, p):
     kc = O.bf16_to_f64(kc0[0].numpy().view(np.uint16))
     vc = O.bf16_to_f64(vc0[0].numpy().view(np.uint16))
     out, inter = O.larosa_block(resid[0].numpy().astype(np.float64), wf, cfg, plan, kc, vc, int(pos[0]),
-                                adapter=w64(lw.adapter), kv_bf16=True)
+                                adapter=w64(lw.adapter), kv_bf16=True, adapter_in_down=merged)
     same = all(np.array_equal(tp[f"idx_h{s}"][0].cpu().numpy(), inter[f"idx{s}"]) for s in (1, 2, 3, 4))
     if not same:
         pytest.skip("certified near-tie swap in the independent chain (reported, P5)")
     assert rel_max(f64(st.resid[0]), out) <= 1e-4
 
 
-@pytest.mark.parametrize("shape", [SMALL, SMALL_MHA])
-def test_layer_p0_equals_original_dense_layer(shape):
+@pytest.mark.parametrize("shape,batch,merged", [(SMALL, 2, False), (SMALL_MHA, 2, False), (SMALL, 1, True),
+                                                (SMALL_MHA, 2, True)])
+def test_layer_p0_equals_original_dense_layer(shape, batch, merged):
     """k = D at every site: the rotated, folded LaRoSA layer reproduces the ORIGINAL dense
-    layer: r_out^gpu = dense(r Q_l^T) Q_{l+1}, up to the fold's bf16 rounding (P4 bound)."""
-    batch, ctx, max_ctx = 2, 20, 32
-    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 9, batch, ctx, max_ctx, 0.0)
+    layer: r_out^gpu = dense(r Q_l^T) Q_{l+1}, up to the fold's bf16 rounding (P4 bound);
+    also with the adapter folded into the down projection."""
+    ctx, max_ctx = 20, 32
+    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 9, batch, ctx, max_ctx, 0.0, merged=merged)
     assert plan == (shape.d, shape.hq * shape.hd, shape.d, shape.inter)
     st, _ = run_layer(lw, plan, resid, kc0, vc0, pos)
     ql, qn = q_l.double().numpy(), q_n.double().numpy()
@@ -187,14 +199,15 @@ def test_layer_p0_equals_original_dense_layer(shape):
         assert err <= 1e-2, err
 
 
-@pytest.mark.parametrize("shape,p", [(SMALL, 0.5), (synth.MODELS["llama2-7b"], 0.5)])
-def test_layer_chained_equals_prepared(shape, p):
+@pytest.mark.parametrize("shape,p,merged", [(SMALL, 0.5, False), (synth.MODELS["llama2-7b"], 0.5, False),
+                                            (synth.MODELS["llama2-7b"], 0.5, True)])
+def test_layer_chained_equals_prepared(shape, p, merged):
     """Batch 1: a layer whose h1 histogram / RMS partials come from the previous layer's
     adapter epilogue (chained) gives bit-identical results to the same layer run with the
     standalone preparation kernel on the same residual."""
     batch, ctx, max_ctx = 1, 20, 32
-    _, _, _, lw1, plan, resid, kc0, vc0, pos = build(shape, 11, batch, ctx, max_ctx, p)
-    _, _, _, lw2, _, _, _, _, _ = build(shape, 12, batch, ctx, max_ctx, p)
+    _, _, _, lw1, plan, resid, kc0, vc0, pos = build(shape, 11, batch, ctx, max_ctx, p, merged=merged)
+    _, _, _, lw2, _, _, _, _, _ = build(shape, 12, batch, ctx, max_ctx, p, merged=merged)
     ws = torch.zeros(LZ.layer_workspace_size(lw1, 1, max_ctx), dtype=torch.uint8, device=DEV)
     kv = [(kc0.clone().to(DEV), vc0.clone().to(DEV)) for _ in range(4)]
     r = resid.clone().to(DEV)

@@ -25,11 +25,14 @@ def main():
     ap.add_argument("--p", type=float, default=0.5)
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--adapter", default="down", choices=["down", "separate"])
     args = ap.parse_args()
     shape = synth.MODELS[args.model]
     n = 4
     qs = [synth.haar_orthogonal(shape.d, 100 + i, device=DEV, dtype=torch.float32) for i in range(n + 1)]
-    layers = [M.fold_layer(M.synth_original_layer(shape, i + 1, device=DEV), shape, qs[i], qs[i + 1]) for i in range(n)]
+    merged = args.adapter == "down"
+    layers = [M.fold_layer(M.synth_original_layer(shape, i + 1, device=DEV), shape, qs[i], qs[i + 1],
+                           adapter_in_down=merged) for i in range(n)]
     ctx = 256
     kv = [(synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 900 + i, 1.0, DEV),
            synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 950 + i, 1.0, DEV)) for i in range(n)]
@@ -40,7 +43,7 @@ def main():
     L = LZ.lib()
     L.larosa_debug_set_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.larosa_debug_set_timeline.restype = None
-    tl = torch.zeros((n, 6, 1024, 8), dtype=torch.int64, device=DEV)
+    tl = torch.zeros((n, 6, 1024, 16), dtype=torch.int64, device=DEV)
     for i in range(n):
         LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos, chained=i > 0), ws=wsb)
     g = torch.cuda.CUDAGraph()
@@ -57,21 +60,29 @@ def main():
         if r >= 3:
             acc.append(tl.cpu().numpy().astype(np.float64))
     out = {"model": args.model, "p": args.p, "plan": list(plan), "kernels": {}}
+    last = 4 if merged else 5
     lay = []
     for a in acc:
         for li in range(1, n):
-            lay.append(a[li][5][:, 4].max() - a[li - 1][5][:, 4].max())
+            lay.append(a[li][last][:, 4].max() - a[li - 1][last][:, 4].max())
     out["layer_us"] = round(float(np.mean(lay)) / 1e3, 2)
-    for k, name in enumerate(NAMES):
+    groups = [(k, name, None) for k, name in enumerate(NAMES[:last + 1])]
+    if merged:   # the down launch: SELECT CTAs (stamp 5 written) and dense companion CTAs
+        groups[4] = (4, "down_select", True)
+        groups.insert(5, (4, "down_companion", False))
+    for k, name, sel in groups:
         stats = {}
         for a in acc:
             for li in range(1, n):
-                prev = a[li - 1][5] if k == 0 else a[li][k - 1]
+                prev = a[li - 1][last] if k == 0 else a[li][k - 1]
                 t0 = prev[:, 4].max()                     # previous kernel's last exit
                 cur = a[li][k]
                 live = cur[:, 0] > 0
+                if sel is not None:
+                    live = live & ((cur[:, 5] > 0) == sel)
                 c = cur[live] - t0
-                for i, key in enumerate(["entry", "wait", "prologue", "loop", "exit", "sel_hist", "rule_start", "sel_mask"]):
+                for i, key in enumerate(["entry", "wait", "prologue", "loop", "exit", "sel_hist", "rule_coarse", "sel_mask",
+                                          "rule_fine", "rule_pool", "rule_ssq", "list", "ticket", "epi", "mask2", "list2"]):
                     col = c[:, i]
                     col = col[cur[live][:, i] > 0]
                     if col.size:
