@@ -493,7 +493,7 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
 // words round-robin over the splits: balanced in expectation, robust to index-correlated
 // keep rates such as PCA-ordered channels).
 constexpr int kSelMaxWords = 256;
-__host__ __device__ constexpr size_t sel_mask_off(int d) { return (size_t)kSelMaxWords * 64; }
+__host__ __device__ constexpr size_t sel_mask_off(int d) { return (size_t)kSelMaxWords * 128; }
 __host__ __device__ constexpr size_t sel_region_bytes(int d) {
     return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 8 + rule_scratch_bytes(), 128);
 }
@@ -503,25 +503,25 @@ __host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
 }
 
 // Returns the number of rows placed in lrow (ascending); misc[4] receives the RMS scale.
-__device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, int* misc, int split,
-                                           int n_splits) {
+__device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, float* lval, int* misc,
+                                           int split, int n_splits) {
     constexpr int NT = kGemvThreads, NW = kGemvWarps;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int d = a.d_in;
-    uint16_t* xs = reinterpret_cast<uint16_t*>(region);
+    float* xs = reinterpret_cast<float*>(region);   // the CTA's words of x (keys and values)
     uint32_t* wmk = reinterpret_cast<uint32_t*>(region + sel_mask_off(d));
     int* wcnt = reinterpret_cast<int*>(wmk + kSelMaxWords);
     int* scan = misc + 8;
     const uint32_t lt = (1u << lane) - 1u;
     const int nwords = (d + 31) / 32;
     const int nj = nwords > split ? (nwords - 1 - split) / n_splits + 1 : 0;
-    for (int c = tid; c < 4 * nj; c += NT) {
-        const int j = c >> 2, w = split + n_splits * j;
-        const int i0 = 32 * w + 8 * (c & 3);
-        cp_async16(xs + 32 * j + 8 * (c & 3), a.sel.x16 + i0, i0 < d);
+    for (int c = tid; c < 8 * nj; c += NT) {
+        const int j = c >> 3, w = split + n_splits * j;
+        const int i0 = 32 * w + 4 * (c & 7);
+        cp_async16(xs + 32 * j + 4 * (c & 7), a.x + i0, i0 < d);
     }
     cp_async_commit();
-    // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the 16-bit keys land
+    // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the CTA's words land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
     compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R,
                      a.tl);
@@ -536,7 +536,8 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     cp_async_wait<0>();
     __syncthreads();
     tl_stamp(a.tl, 5);
-    auto keep16 = [&](uint32_t k16, int i) -> bool {
+    auto keep16 = [&](uint32_t key, int i) -> bool {
+        const uint32_t k16 = key >> 15;
         if (k16 != t16) return k16 > t16;
         if (flags & kRuleEdgeAll) return true;
         if (!(flags & kRuleExact)) {
@@ -544,7 +545,6 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
                 if (tab[q] == i) return (keepm >> q) & 1ull;
             return false;
         }
-        const uint32_t key = key_of(__ldcg(a.x + i));
         return key > tk || (key == tk && i <= ti);
     };
     const bool all = flags & kRuleAll, none = flags & kRuleNone;
@@ -554,7 +554,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
         for (int j = wid; j < nj; j += NW) {
             const int i = 32 * (split + n_splits * j) + lane;
             bool kp = false;
-            if (i < d) kp = all ? true : (none ? false : keep16(xs[32 * j + lane], i));
+            if (i < d) kp = all ? true : (none ? false : keep16(key_of(xs[32 * j + lane]), i));
             const uint32_t m = __ballot_sync(0xffffffffu, kp);
             if (lane == 0) {
                 wmk[j] = m;
@@ -570,7 +570,11 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
         __syncthreads();
         for (int j = wid; j < nj; j += NW) {
             const uint32_t m = wmk[j];
-            if ((m >> lane) & 1u) lrow[wcnt[j] + __popc(m & lt)] = 32 * (split + n_splits * j) + lane;
+            if ((m >> lane) & 1u) {   // the row index and its activation (the value rides with the list)
+                const int pos = wcnt[j] + __popc(m & lt);
+                lrow[pos] = 32 * (split + n_splits * j) + lane;
+                lval[pos] = xs[32 * j + lane];
+            }
         }
         __syncthreads();   // list complete; the staged region (aliased by the ring) is dead
         tl_stamp(a.tl, rep ? 15 : 11);
@@ -656,7 +660,6 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
         }
     }
     const uint16_t* Wb = comp ? a.W2 : a.W;
-    const float* xb = comp ? a.x2 : a.x;
     const int col0 = slice * kSliceCols + lane * 8;
     const bool lane_on = col0 < a.d_out;          // d_out % 8 == 0: a lane's chunk is all-in or all-out
     unsigned char* mychunk = smem + (size_t)warp * kWarpRingBytes + lane * 16;
@@ -692,12 +695,11 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
         static_assert(BP == 1, "SELECT is the batch-1 path");
         if (comp) {
             n_list = c_n;
-            // values of the prefetched stages (list position warp + 8 m, m < kStages * kStageRows)
-            if (lane < kStages * kStageRows && lane < c_my)
-                lval[warp + kGemvWarps * lane] = __ldcg(a.x2 + c_lo + warp + kGemvWarps * lane);
-            __syncwarp();
+            // every value of the CTA's dense rows, once (list position t = row c_lo + t)
+            for (int t = threadIdx.x; t < c_n; t += kGemvThreads) lval[t] = __ldcg(a.x2 + c_lo + t);
+            __syncthreads();
         } else {
-            n_list = select_rows(a, smem, lrow, misc, split, a.n_splits);
+            n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
         }
     } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
@@ -779,8 +781,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
                 const int lpos = warp + kGemvWarps * m;
                 const int row = m < n_my ? (comp ? c_lo + lpos : lrow[lpos]) : 0;
                 cp_async16(dst + g * (kSliceCols * 2), wcol + (size_t)row * a.ld, lane_on && m < n_my);
-                if constexpr (MODE == GEMV_SELECT)   // the row's activation rides in the same group
-                    if (lane == g && m < n_my) cp_async4(lval + lpos, xb + row);
+
             }
         }
         cp_async_commit();   // one (possibly empty) group per stage keeps the count uniform
@@ -798,7 +799,6 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 
     for (int st = 0; st < n_st; ++st) {
         cp_async_wait<kStages - 1>();          // this lane's chunks of stage st have landed
-        if constexpr (MODE == GEMV_SELECT) __syncwarp();   // lanes 0-3 copied the stage's values
         const unsigned char* src = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
 #pragma unroll
         for (int g = 0; g < kStageRows; ++g) {
