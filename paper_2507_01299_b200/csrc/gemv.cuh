@@ -62,7 +62,6 @@ enum GemvEpi : int { EPI_NONE = 0, EPI_STORE = 1, EPI_RESID = 2, EPI_SILU = 3 };
 // attention merge, or the standalone preparation kernel) and consumed by the SELECT prologue:
 //   hist  [4096 fine bins of key bits 30:19][256 coarse bins of bits 30:23]   zero at rest
 //   pool  [4096][kPoolCap] (key, index) of each fine bucket's first entries
-//   x16   [d] key >> 15 (the top 16 key bits) of every element
 //   ssq   [ceil(d / 256)] per-slice sums of squares (RMS sites)
 // The site's exact Top-K rule (compute_rule, by every consuming CTA):
 // keep i iff key_i > tk or (key_i == tk and i <= ti); value x_i * scale.  Consumers decide
@@ -83,7 +82,6 @@ struct __align__(16) SelRule {
 struct SiteSel {
     uint32_t* hist;
     uint2* pool;
-    uint16_t* x16;
     float* ssq;
 };
 // histogram levels: 65536 fine bins of key bits [30:15] (the 16-bit key), then 256 coarse
@@ -203,15 +201,14 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 __device__ __forceinline__ uint32_t key_of(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 // producer side of a site: element i of value v.  Fine-bin count of its 16-bit key (the old
 // value is the pool slot), coarse-bin count (warp-aggregated: a few exponents hold most
-// elements), the (key, i) pool entry and the 16-bit key.
+// elements) and the (key, i) pool entry.
 __device__ __forceinline__ void hist_push(const SiteSel& o, float v, int i) {
     const uint32_t key = key_of(v), k16 = key >> 15;
-    const uint32_t slot = atomicAdd(o.hist + sel_fine_idx(k16), 1u);
-    if (slot < (uint32_t)kPoolCap) o.pool[sel_pool_idx(k16, slot)] = make_uint2(key, (uint32_t)i);
     const unsigned am = __activemask();
     const unsigned peers = __match_any_sync(am, k16 >> 8);
     if ((threadIdx.x & 31) == __ffs(peers) - 1) red_add_u32(o.hist + sel_coarse_idx(k16 >> 8), __popc(peers));
-    o.x16[i] = (uint16_t)k16;
+    const uint32_t slot = atomicAdd(o.hist + sel_fine_idx(k16), 1u);
+    if (slot < (uint32_t)kPoolCap) o.pool[sel_pool_idx(k16, slot)] = make_uint2(key, (uint32_t)i);
 }
 
 // cp.async (LDGSTS): 16 bytes global -> shared, L1 bypass (.cg)

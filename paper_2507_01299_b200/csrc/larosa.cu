@@ -531,7 +531,6 @@ static void carve_topk_gemv(Carver& c, int64_t d_in, int64_t d_out, unsigned lon
     SiteSel q;
     q.hist = c.take<uint32_t>(kSelHistTotal);
     q.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
-    q.x16 = c.take<uint16_t>((size_t)d_in);
     q.ssq = c.take<float>((size_t)(d_in + kSliceCols - 1) / kSliceCols);
     if (acc) *acc = a;
     if (sel) *sel = q;
@@ -961,7 +960,6 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
         SiteSel& q = o->sel[s];
         q.hist = c.take<uint32_t>(kSelHistTotal);
         q.pool = batch == 1 ? c.take<uint2>((size_t)kSelFine * kPoolCap) : nullptr;
-        q.x16 = batch == 1 ? c.take<uint16_t>((size_t)din[s]) : nullptr;
         q.ssq = (s == 0 || s == 2) ? c.take<float>((size_t)batch * n_slices(L.d)) : nullptr;
     }
     for (int s = 0; s < 4; ++s) o->thr[s] = c.take<ThreshOut>((size_t)batch);
@@ -1314,7 +1312,6 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     q->acc = c.take<unsigned long long>((size_t)omax);
     q->sel.hist = c.take<uint32_t>(kSelHistTotal);
     q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
-    q->sel.x16 = c.take<uint16_t>((size_t)dmax);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
     const int ch = attn_chunk(max_ctx, (int)S.hkv_l);
     const int nch = (int)((max_ctx + ch - 1) / ch);

@@ -14,7 +14,7 @@ p = float(sys.argv[1]) if len(sys.argv) > 1 else 0.5
 dev = "cuda:0"
 q0 = synth.haar_orthogonal(shape.d, 1, device=dev, dtype=torch.float32)
 q1 = synth.haar_orthogonal(shape.d, 2, device=dev, dtype=torch.float32)
-lw = M.fold_layer(M.synth_original_layer(shape, 1, device=dev), shape, q0, q1)
+lw = M.fold_layer(M.synth_original_layer(shape, 1, device=dev), shape, q0, q1, adapter_in_down=True)
 ctx = 256
 kc = synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 3, 1.0, dev)
 vc = synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 4, 1.0, dev)
