@@ -89,6 +89,7 @@ struct SiteSel {
 constexpr int kSelFine = 65536;
 constexpr int kSelCoarse = 256;
 constexpr int kSelHistTotal = kSelFine + kSelCoarse;
+constexpr int kSelHistAlloc = kSelHistTotal + 32;   // + the coarse-bucket guess word (not zeroed with the bins)
 // fine bin of 16-bit key k16 at k16 (a coarse bucket's 256 fine bins are contiguous), coarse
 // bin cb at kSelFine + cb, pool entry (k16, slot) at k16 * kPoolCap + slot
 __host__ __device__ constexpr int sel_fine_idx(uint32_t k16) { return (int)k16; }
@@ -310,11 +311,15 @@ __host__ __device__ constexpr size_t rule_scratch_bytes() { return (size_t)(16 +
 // per lane through L1, so the CTAs sharing an SM hit): the bin holding the rem-th largest
 // element.  Returns true and (bin, rem in bin, count) on every lane; false if the bins hold
 // fewer than rem elements.
-__device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, int& bin, int& rem_in, int& cnt) {
+__device__ __forceinline__ void load256(const uint32_t* bins, uint4& a, uint4& b) {
+    const int lane = threadIdx.x & 31;
+    const uint4* p = reinterpret_cast<const uint4*>(bins + 256 - 8 * (lane + 1));
+    a = __ldca(p);
+    b = __ldca(p + 1);
+}
+__device__ __forceinline__ bool suffix256(const uint4& a, const uint4& b, int rem, int& bin, int& rem_in, int& cnt) {
     const int lane = threadIdx.x & 31;
     const int j0 = 256 - 8 * (lane + 1);
-    const uint4* p = reinterpret_cast<const uint4*>(bins + j0);
-    const uint4 a = __ldca(p), b = __ldca(p + 1);
     const int c[8] = {(int)a.x, (int)a.y, (int)a.z, (int)a.w, (int)b.x, (int)b.y, (int)b.z, (int)b.w};
     int sum = 0;
 #pragma unroll
@@ -344,10 +349,15 @@ __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, in
     cnt = __shfl_sync(0xffffffffu, mc, src);
     return true;
 }
+__device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, int& bin, int& rem_in, int& cnt) {
+    uint4 a, b;
+    load256(bins, a, b);
+    return suffix256(a, b, rem, bin, rem_in, cnt);
+}
 
 template <int NT>
 __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
-                             unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr) {
+                             unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr, int guess = 0) {
     static_assert(NT >= 64, "two warps");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
@@ -372,10 +382,34 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
         } else if (k >= d) {
             flags = kRuleAll;
         } else {
+            // lookup 1 reads the coarse bins together with the fine bins of the coarse buckets
+            // around the previous call's (guess = cb + 1 of this site's last consumer): when the
+            // k-th key's bucket is among them, lookup 2 costs no extra round trip
             int cb = 0, r1 = 0, cc = 0, fb = 0;
-            const bool ok1 = warp_suffix256(sel.hist + kSelFine, k, cb, r1, cc);
+            const int g = __shfl_sync(0xffffffffu, guess, 0) - 1;
+            uint4 ca, cbv, f0a, f0b, f1a, f1b, f2a, f2b;
+            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+            load256(sel.hist + kSelFine, ca, cbv);
+            f0a = f0b = f1a = f1b = f2a = f2b = z;
+            if (g >= 0 && g < 256) load256(sel.hist + 256 * g, f0a, f0b);
+            if (g >= 1 && g < 257) load256(sel.hist + 256 * (g - 1), f1a, f1b);
+            if (g >= -1 && g < 255) load256(sel.hist + 256 * (g + 1), f2a, f2b);
+            const bool ok1 = suffix256(ca, cbv, k, cb, r1, cc);
             tl_stamp(tl, 6);
-            const bool ok2 = ok1 && warp_suffix256(sel.hist + 256 * cb, r1, fb, rem, cnt);
+            bool ok2 = false;
+            if (ok1) {
+                if (cb == g) {
+                    ok2 = suffix256(f0a, f0b, r1, fb, rem, cnt);
+                } else if (cb == g - 1) {
+                    ok2 = suffix256(f1a, f1b, r1, fb, rem, cnt);
+                } else if (cb == g + 1) {
+                    ok2 = suffix256(f2a, f2b, r1, fb, rem, cnt);
+                } else {
+                    ok2 = warp_suffix256(sel.hist + 256 * cb, r1, fb, rem, cnt);
+                }
+                if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && cb + 1 != guess)
+                    sel.hist[kSelHistTotal] = (uint32_t)(cb + 1);   // next call's guess (not zeroed with the bins)
+            }
             tl_stamp(tl, 8);
             if (!ok1 || !ok2) {
                 flags = kRuleAll;   // inconsistent histogram: keep-all (bounded, never faults)
@@ -501,7 +535,7 @@ __host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
 
 // Returns the number of rows placed in lrow (ascending); misc[4] receives the RMS scale.
 __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, float* lval, int* misc,
-                                           int split, int n_splits) {
+                                           int split, int n_splits, int guess) {
     constexpr int NT = kGemvThreads, NW = kGemvWarps;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int d = a.d_in;
@@ -521,7 +555,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the CTA's words land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
     compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R,
-                     a.tl);
+                     a.tl, guess);
     const uint32_t tk = R->tk;
     const int ti = R->ti;
     const int flags = R->flags;
@@ -677,6 +711,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
         }
     }
 
+    // SELECT: the coarse-bucket guess left by this site's previous consumer (written by a kernel
+    // that completed before the previous one; any value is safe, a wrong one costs a round trip)
+    int sel_guess = 0;
+    if constexpr (MODE == GEMV_SELECT)
+        if (!comp && threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
+
     tl_stamp(a.tl, 0);
     pdl_wait();       // the row source comes from the previous kernel
     pdl_trigger();
@@ -696,7 +736,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
             for (int t = threadIdx.x; t < c_n; t += kGemvThreads) lval[t] = __ldcg(a.x2 + c_lo + t);
             __syncthreads();
         } else {
-            n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits);
+            n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
         }
     } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;

@@ -529,7 +529,7 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
 static void carve_topk_gemv(Carver& c, int64_t d_in, int64_t d_out, unsigned long long** acc, SiteSel* sel) {
     unsigned long long* a = c.take<unsigned long long>((size_t)d_out);
     SiteSel q;
-    q.hist = c.take<uint32_t>(kSelHistTotal);
+    q.hist = c.take<uint32_t>(kSelHistAlloc);
     q.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q.ssq = c.take<float>((size_t)(d_in + kSliceCols - 1) / kSliceCols);
     if (acc) *acc = a;
@@ -958,7 +958,7 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     for (int s = 0; s < 4; ++s) {
         SiteSel& q = o->sel[s];
-        q.hist = c.take<uint32_t>(kSelHistTotal);
+        q.hist = c.take<uint32_t>(kSelHistAlloc);
         q.pool = batch == 1 ? c.take<uint2>((size_t)kSelFine * kPoolCap) : nullptr;
         q.ssq = (s == 0 || s == 2) ? c.take<float>((size_t)batch * n_slices(L.d)) : nullptr;
     }
@@ -1310,7 +1310,7 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     const int64_t dmax = std::max(std::max(S.d, S.nq), S.inter);
     const int64_t omax = std::max(std::max(S.qkv_l, S.dl), 2 * S.il);
     q->acc = c.take<unsigned long long>((size_t)omax);
-    q->sel.hist = c.take<uint32_t>(kSelHistTotal);
+    q->sel.hist = c.take<uint32_t>(kSelHistAlloc);
     q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
     const int ch = attn_chunk(max_ctx, (int)S.hkv_l);
