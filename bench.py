@@ -278,6 +278,52 @@ def decode_step_extra(device, batches=(1, 16), ps=(0.4, 0.0), reps=20, merged=Tr
     return out
 
 
+def model_sweep_extra(device, models=("mistral-7b", "qwen2.5-7b"), ps=(0.0, 0.25, 0.4, 0.5, 0.6), steps=400,
+                      copies=4, merged=True):
+    """BASELINE configs[3]: per-layer sparsity sweep of the Mistral-7B and Qwen2.5-7B blocks (batch 1,
+    ctx 256, uniform alpha, plus the paper's alpha at p = 0.5) against the dense bf16 GEMV time
+    (cuBLAS on the same folded weights) and the HBM byte roofline of each plan."""
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    peaks, _ = measured_peaks()
+    out = {}
+    for name in models:
+        shape = synth.MODELS[name]
+        layers = build_stack(shape, device, copies, seed=500, merged=merged)
+        kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
+               synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(copies)]
+        pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
+        ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
+        res = {}
+        plans = [(str(p), M.site_plan(shape, p)) for p in ps] + [("0.5_paper_alpha", M.site_plan(shape, 0.5, "paper"))]
+        nq = shape.hq * shape.hd
+        for key, plan in plans:
+            resid = synth.residual_activation(1, shape.d, seed=77).to(device)
+            graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
+            run_steps(graphs, 50, 0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run_steps(graphs, steps, 0)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / steps
+            k1, k2, k3, k4 = plan
+            wbytes = 2 * (k1 * shape.qkv_out + k2 * shape.d + k3 * 2 * shape.inter + k4 * shape.d + shape.d * shape.d)
+            kvb = 2 * 2 * shape.hkv * shape.hd * CTX
+            res[key] = {"block_us": us, "tok_s": 1e6 / us, "plan": list(plan), "bytes": wbytes + kvb,
+                        "roofline_us": (wbytes + kvb) / peaks["hbm_gbs"] / 1e3,
+                        "frac_of_roofline": (wbytes + kvb) / peaks["hbm_gbs"] / 1e3 / us}
+            del graphs
+        dense_us, _ = cublas_dense_us(layers, shape, device)
+        res["cublas_dense_4gemv_us"] = dense_us
+        res["speedup_vs_dense_at_0.5"] = dense_us / res["0.5"]["block_us"]
+        out[name] = res
+        del layers, kv, ws_buf
+        torch.cuda.empty_cache()
+    return out
+
+
 def fold_extra(device):
     """larosa_fold_rotation on LLaMA2-7B layer shapes: tcgen05 TFLOP/s (2 M N K of the fold)."""
     from paper_2507_01299_b200 import larosa as LZ
@@ -570,7 +616,8 @@ def main():
     extras = None
     if not args.no_sweep:
         extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device, merged=merged),
-                  "fold_tcgen05": fold_extra(device)}
+                  "fold_tcgen05": fold_extra(device),
+                  "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
 
     cpu = None
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:

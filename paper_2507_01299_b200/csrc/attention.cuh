@@ -3,13 +3,14 @@
 // decoder layer (not LaRoSA content; conventions SURVEY Z27): q-head h reads kv-head
 // floor(h * Hkv / Hq), scale 1/sqrt(hd), fp32 softmax.
 //
-// grid = (batch * Hkv, n_chunks), 4 warps.  CTA (b, g, c) handles positions
-// [c*CH, c*CH + CH) (CH <= 64) of the G = Hq/Hkv query heads that share kv-head g.  Warp w
-// owns positions c*CH + w + 4*i: it issues ALL its K and V row loads up front (one 16-byte
-// or 8-byte load per lane per row, so the rows' DRAM latencies overlap), computes scores
-// (lanes over head dims + warp reduction), a warp-local softmax and P.V; the 4 warps then
-// merge in shared memory.  The chunk's (m, l, o[hd]) per head goes to the workspace and
-// the last chunk CTA to finish (atomic ticket) merges the chunks in order.
+// grid = (batch * Hq, n_chunks), 4 warps.  CTA (b, h, c) handles positions [c*CH, c*CH + CH)
+// (CH <= 64) of query head h (one head per CTA: GQA groups of G heads share the K/V rows
+// through L2, and no CTA loops over a group's heads).  Warp w owns positions c*CH + w + 4*i:
+// it issues ALL its K and V row loads up front (one 16-byte or 8-byte load per lane per row,
+// so the rows' DRAM latencies overlap), computes scores (lanes over head dims, the positions'
+// butterfly reductions interleaved), a warp-local softmax and P.V; the 4 warps then merge in
+// shared memory.  The chunk's (m, l, o[hd]) goes to the workspace and the last chunk CTA of
+// the head (atomic ticket) merges the chunks in order.
 #pragma once
 #include "common.cuh"
 #include "gemv.cuh"
@@ -32,22 +33,19 @@ struct AttnArgs {
     int64_t max_ctx;
     int hq, hkv, hd;
     int chunk, n_chunks;
-    float* part;           // [batch*hkv][n_chunks][G][hd + 2]
-    unsigned* counters;    // [batch*hkv]
+    float* part;           // [batch*hq][n_chunks][hd + 2]
+    unsigned* counters;    // [batch*hq] head tickets, + kAttnGroupCounterOff: [batch*hkv] group tickets
     float* out;            // [batch][hq*hd]
     SiteSel out_sel;       // batch 1: selection data of h2 for the next GEMV (hist null = none)
     uint32_t* zero_hist;   // optional histogram to re-zero (its consumer has completed)
     int zero_words;
     unsigned long long* tl;   // debug timeline slot or null
-    int cluster;           // 1: the n_chunks CTAs of a kv group form a cluster; merge via DSMEM
 };
 
-__host__ __device__ inline size_t attn_smem_bytes(int G, int hd, int chunk) {
-    (void)chunk;
-    // q [G][hd] + per-warp (m, l) [4][G][2] + per-warp o [4][G][hd] + new k/v bf16 [2][hd] + flag
-    // + this chunk's merged partial [G][hd + 2] (read by the cluster leader through DSMEM)
-    return sizeof(float) * ((size_t)G * hd + 4 * (size_t)G * 2 + 4 * (size_t)G * hd + (size_t)G * (hd + 2)) +
-           4 * (size_t)hd + 16;
+constexpr int kAttnGroupCounterOff = 2048;   // counters: [0, B Hq) head tickets, then group tickets
+__host__ __device__ inline size_t attn_smem_bytes(int hd) {
+    // q [hd] + per-warp (m, l) [4][2] + per-warp o [4][hd] + new k/v bf16 [2][hd] + flags
+    return sizeof(float) * ((size_t)hd + 8 + 4 * (size_t)hd) + 4 * (size_t)hd + 16;
 }
 
 // RoPE (HF rotate_half) of the pair (i, i + hd/2) at position p, in fp64
@@ -69,13 +67,15 @@ template <int DPL>   // head dims per lane: hd = 32 * DPL (2 -> 64, 4 -> 128)
 __device__ void attention_body(const AttnArgs& a, float* asmem) {
     const int G = a.hq / a.hkv;
     constexpr int hd = 32 * DPL;
-    float* sq = asmem;                         // [G][hd]
-    float* sml = sq + G * hd;                  // [4][G][2]
-    float* so = sml + 4 * G * 2;               // [4][G][hd]
-    int* sflag = reinterpret_cast<int*>(so + 4 * G * hd + hd);   // after the new k/v bf16 rows
+    float* sq = asmem;                         // [hd]
+    float* sml = sq + hd;                      // [4][2]
+    float* so = sml + 8;                       // [4][hd]
+    uint16_t* snew = reinterpret_cast<uint16_t*>(so + 4 * hd);   // [2][hd] new k, v (bf16)
+    int* sflag = reinterpret_cast<int*>(snew + 2 * hd);
 
-    const int bg = blockIdx.x, ch = blockIdx.y;
-    const int b = bg / a.hkv, g = bg % a.hkv;
+    // one CTA per (token b, query head h, context chunk): kv head g = floor(h / G)
+    const int bh = blockIdx.x, ch = blockIdx.y;
+    const int b = bh / a.hq, h = bh % a.hq, g = h / G;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ctx = a.pos[b] + 1;
     const int start = ch * a.chunk;
@@ -86,7 +86,6 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     const int nq = a.hq * hd, nk = a.hkv * hd;
     const int pnew = ctx - 1;                                   // the position appended this step
     const bool has_new = pnew >= start && pnew < start + n;
-    uint16_t* snew = reinterpret_cast<uint16_t*>(so + 4 * G * hd);   // [2][hd] new k, v (bf16)
     // every K/V row of this warp's positions except the one appended this step: issued
     // BEFORE the dependency wait (earlier steps wrote them; with programmatic dependent launch
     // these loads overlap the QKV GEMV still streaming)
@@ -117,22 +116,23 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     }
     const unsigned long long* accb = a.acc + (size_t)b * a.acc_ld;
     auto yval = [&](int col) -> float {
-        return fix_to_f(accb[col]) + (a.bias ? bf16f(a.bias[col]) : 0.f);
+        return fix_to_f(__ldcg(accb + col)) + (a.bias ? bf16f(a.bias[col]) : 0.f);
     };
-    // q of my G heads (bias + RoPE), and, in the chunk holding pos, the new k / v row
-    for (int t = tid; t < G * half; t += kAttnThreads) {
-        const int j = t / half, i = t % half;
-        const int col = (g * G + j) * hd + i;
+    // q of head h (bias + RoPE) and, in the chunk holding pos, the new k / v row of kv head g
+    // (every query head of the group computes it; the group's first head writes it to the cache)
+    for (int i = tid; i < half; i += kAttnThreads) {
+        const int col = h * hd + i;
         float y1 = yval(col), y2 = yval(col + half);
         rope_pair(y1, y2, i, hd, pnew, a.theta);
-        sq[j * hd + i] = y1;
-        sq[j * hd + i + half] = y2;
+        sq[i] = y1;
+        sq[i + half] = y2;
         if (a.q_out && ch == 0) {
             a.q_out[(size_t)b * nq + col] = y1;
             a.q_out[(size_t)b * nq + col + half] = y2;
         }
     }
     if (has_new) {
+        const bool writer = h % G == 0;
         uint16_t* kdst = a.kc + kvbase + (size_t)pnew * hd;
         uint16_t* vdst = a.vc + kvbase + (size_t)pnew * hd;
         for (int i = tid; i < half; i += kAttnThreads) {
@@ -141,16 +141,19 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             const uint16_t k1 = f2bf16_rne(y1), k2 = f2bf16_rne(y2);
             snew[i] = k1;
             snew[i + half] = k2;
-            kdst[i] = k1;
-            kdst[i + half] = k2;
+            if (writer) {
+                kdst[i] = k1;
+                kdst[i + half] = k2;
+            }
         }
         for (int i = tid; i < hd; i += kAttnThreads) {
             const uint16_t v = f2bf16_rne(yval(nq + nk + g * hd + i));
             snew[hd + i] = v;
-            vdst[i] = v;
+            if (writer) vdst[i] = v;
         }
     }
     __syncthreads();
+    tl_stamp(a.tl, 2);
 
     // the new row (computed above into shared memory) replaces the stale cache entry
 #pragma unroll
@@ -168,10 +171,10 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
     }
 
     const float scale = 1.0f / sqrtf((float)hd);
-    for (int j = 0; j < G; ++j) {
+    {
         float qf[DPL];
 #pragma unroll
-        for (int t = 0; t < DPL; ++t) qf[t] = sq[j * hd + lane * DPL + t];
+        for (int t = 0; t < DPL; ++t) qf[t] = sq[lane * DPL + t];
         float s[kAttnPosPerWarp];
         float m = -INFINITY;
 #pragma unroll
@@ -182,8 +185,16 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
                 acc = fmaf(qf[2 * t], bf16lo(kr[i][t]), acc);
                 acc = fmaf(qf[2 * t + 1], bf16hi(kr[i][t]), acc);
             }
-            acc = warp_sum(acc) * scale;
-            s[i] = (warp + 4 * i < n) ? acc : -INFINITY;
+            s[i] = acc;
+        }
+        // the positions' butterflies interleaved (independent shuffles in flight together)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < kAttnPosPerWarp; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+#pragma unroll
+        for (int i = 0; i < kAttnPosPerWarp; ++i) {
+            s[i] = (warp + 4 * i < n) ? s[i] * scale : -INFINITY;
             m = fmaxf(m, s[i]);
         }
         float l = 0.f, o[DPL];
@@ -202,79 +213,61 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             }
         }
         if (lane == 0) {
-            sml[(warp * G + j) * 2 + 0] = m;
-            sml[(warp * G + j) * 2 + 1] = l;
+            sml[warp * 2 + 0] = m;
+            sml[warp * 2 + 1] = l;
         }
 #pragma unroll
-        for (int t = 0; t < DPL; ++t) so[(warp * G + j) * hd + lane * DPL + t] = o[t];
+        for (int t = 0; t < DPL; ++t) so[warp * hd + lane * DPL + t] = o[t];
     }
     __syncthreads();
+    tl_stamp(a.tl, 3);
 
-    // merge the 4 warps (fixed order) -> this chunk's (m, l, o): in shared memory for the
-    // cluster leader, else in the global workspace for the last-arriving chunk CTA
-    float* spart = reinterpret_cast<float*>(sflag + 4);
-    float* myp = a.cluster ? spart : a.part + ((size_t)bg * a.n_chunks + ch) * G * (hd + 2);
-    for (int i = tid; i < G * hd; i += kAttnThreads) {
-        const int j = i / hd, dd = i % hd;
+    // merge the 4 warps (fixed order) -> this chunk's (m, l, o) in the workspace
+    float* myp = a.part + ((size_t)bh * a.n_chunks + ch) * (hd + 2);
+    for (int dd = tid; dd < hd; dd += kAttnThreads) {
         float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, sml[(w * G + j) * 2]);
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sml[w * 2]);
         float L = 0.f, Ov = 0.f;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-            const float lw = sml[(w * G + j) * 2 + 1];
+            const float lw = sml[w * 2 + 1];
             if (lw == 0.f) continue;
-            const float e = expf(sml[(w * G + j) * 2] - M);
+            const float e = expf(sml[w * 2] - M);
             L = fmaf(lw, e, L);
-            Ov = fmaf(so[(w * G + j) * hd + dd], e, Ov);
+            Ov = fmaf(so[w * hd + dd], e, Ov);
         }
-        myp[j * (hd + 2) + 2 + dd] = Ov;
+        myp[2 + dd] = Ov;
         if (dd == 0) {
-            myp[j * (hd + 2) + 0] = M;
-            myp[j * (hd + 2) + 1] = L;
+            myp[0] = M;
+            myp[1] = L;
         }
     }
-    if (a.cluster) {
-        cluster_sync_all();                       // every chunk's partial is in its shared memory
-        if (cluster_ctarank() != 0) {
-            cluster_sync_all();                   // keep it alive until the leader has read it
-            return;
-        }
-    } else {
-        fence_acq_rel_gpu();
-        __syncthreads();
-        if (tid == 0) {
-            const unsigned prev = atomicAdd(&a.counters[bg], 1u);
-            sflag[0] = prev == (unsigned)(a.n_chunks - 1);
-        }
-        __syncthreads();
-        if (!sflag[0]) return;
-        if (tid == 0) a.counters[bg] = 0u;
-        fence_acq_rel_gpu();
+    fence_acq_rel_gpu();
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(&a.counters[bh], 1u);
+        sflag[0] = prev == (unsigned)(a.n_chunks - 1);
     }
+    __syncthreads();
+    if (!sflag[0]) return;
+    if (tid == 0) a.counters[bh] = 0u;
+    fence_acq_rel_gpu();
+    tl_stamp(a.tl, 5);
 
-    // merge the chunks in order (each batch of chunk records is loaded before it is used:
-    // __ldcg is a volatile load, so a load->use loop would serialise the L2 round trips)
-    const float* pb = a.part + (size_t)bg * a.n_chunks * G * (hd + 2);
-    for (int i = tid; i < G * hd; i += kAttnThreads) {
-        const int j = i / hd, dd = i % hd;
+    // the last chunk CTA of head h merges the chunks in order (all records loaded up front)
+    const float* pb = a.part + (size_t)bh * a.n_chunks * (hd + 2);
+    for (int dd = tid; dd < hd; dd += kAttnThreads) {
         float M = -INFINITY, L = 0.f, Ov = 0.f;
         for (int c0 = 0; c0 < a.n_chunks; c0 += 16) {
             float mc[16], lc[16], oc[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const bool ok = c0 + u < a.n_chunks;
-                if (a.cluster) {   // chunk c0 + u = cluster CTA rank c0 + u (c0 == 0, n_chunks <= 8)
-                    const uint32_t r = dsmem_addr(spart + (size_t)j * (hd + 2), ok ? (uint32_t)(c0 + u) : 0u);
-                    mc[u] = ok ? dsmem_ld_f32(r) : -INFINITY;
-                    lc[u] = ok ? dsmem_ld_f32(r + 4) : 0.f;
-                    oc[u] = ok ? dsmem_ld_f32(r + 4 * (2 + dd)) : 0.f;
-                } else {
-                    const float* r = pb + ((size_t)(c0 + u) * G + j) * (hd + 2);
-                    mc[u] = ok ? __ldcg(r) : -INFINITY;
-                    lc[u] = ok ? __ldcg(r + 1) : 0.f;
-                    oc[u] = ok ? __ldcg(r + 2 + dd) : 0.f;
-                }
+                const float* r = pb + (size_t)(c0 + u) * (hd + 2);
+                mc[u] = ok ? __ldcg(r) : -INFINITY;
+                lc[u] = ok ? __ldcg(r + 1) : 0.f;
+                oc[u] = ok ? __ldcg(r + 2 + dd) : 0.f;
             }
             float Mn = M;
 #pragma unroll
@@ -293,13 +286,24 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
             M = Mn;
         }
         const float hv = Ov / L;
-        a.out[(size_t)b * a.hq * hd + (size_t)(g * G + j) * hd + dd] = hv;
-        if (a.out_sel.hist) hist_push(a.out_sel, hv, (g * G + j) * hd + dd);
+        a.out[(size_t)b * a.hq * hd + (size_t)h * hd + dd] = hv;
+        if (a.out_sel.hist) hist_push(a.out_sel, hv, h * hd + dd);
     }
-    if (a.cluster) cluster_sync_all();             // the other chunks' shared memory may go
-    // every chunk CTA of this kv group has read its q / new k, v accumulators: re-zero them
+    tl_stamp(a.tl, 6);
+    // every chunk CTA of head h has read its q accumulators: re-zero them.  The group's k / v
+    // accumulators are read by all G heads: the last head merger of the group re-zeroes them.
     unsigned long long* accz = a.acc + (size_t)b * a.acc_ld;
-    for (int i = tid; i < G * hd; i += kAttnThreads) accz[(size_t)g * G * hd + i] = 0ull;
+    for (int i = tid; i < hd; i += kAttnThreads) accz[(size_t)h * hd + i] = 0ull;
+    fence_acq_rel_gpu();
+    __syncthreads();
+    unsigned* gcnt = a.counters + kAttnGroupCounterOff + (size_t)b * a.hkv + g;
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(gcnt, 1u);
+        sflag[1] = prev == (unsigned)(G - 1);
+    }
+    __syncthreads();
+    if (!sflag[1]) return;
+    if (tid == 0) *gcnt = 0u;
     for (int i = tid; i < hd; i += kAttnThreads) {
         accz[nq + (size_t)g * hd + i] = 0ull;
         accz[nq + nk + (size_t)g * hd + i] = 0ull;

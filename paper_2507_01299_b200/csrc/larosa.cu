@@ -345,23 +345,15 @@ TopkKernelArgs topk_args_base() {
 // attention: the n_chunks CTAs of a kv group form one thread-block cluster when n_chunks <= 8
 // (split-KV merge through distributed shared memory), else the ticket merge
 larosa_status launch_attention(AttnArgs aa, int units, int hd, int G, cudaStream_t st) {
-    const size_t smem = attn_smem_bytes(G, hd, aa.chunk);
-    // measured (LLaMA2-7B, ctx 256): cluster merge 8.6 us vs ticket merge 7.7 us per attention -> opt-in
-    aa.cluster = aa.n_chunks <= 8 && env_int("LAROSA_ATTN_CLUSTER", 0) != 0;
+    (void)G;
+    const size_t smem = attn_smem_bytes(hd);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units, aa.n_chunks);
     cfg.blockDim = dim3(kAttnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];
     int na = 0;
-    if (aa.cluster) {
-        at[na].id = cudaLaunchAttributeClusterDimension;
-        at[na].val.clusterDim.x = 1;
-        at[na].val.clusterDim.y = aa.n_chunks;
-        at[na].val.clusterDim.z = 1;
-        ++na;
-    }
     if (pdl_enabled()) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
@@ -967,9 +959,9 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     o->rmid = c.take<float>((size_t)batch * L.d);
     o->h4 = c.take<float>((size_t)batch * L.inter);
     o->radp = c.take<float>((size_t)batch * L.d);
-    const int ch = attn_chunk(max_ctx, batch * (int)L.hkv);
+    const int ch = attn_chunk(max_ctx, batch * (int)L.hq);
     const int nch = (int)((max_ctx + ch - 1) / ch);
-    o->attn_part = c.take<float>((size_t)batch * L.hkv * nch * L.G * (L.hd + 2));
+    o->attn_part = c.take<float>((size_t)batch * L.hq * nch * (L.hd + 2));
     o->attn_cnt = c.counters(kAttnCounterBase);
     for (int j = 0; j < 4; ++j) o->tickets[j] = c.counters(kGemvTicketBase + 256 * j);
 }
@@ -990,8 +982,8 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
     if (w->d > LAROSA_MAX_DIM || w->inter > LAROSA_MAX_DIM || w->n_q_heads * w->head_dim > LAROSA_MAX_DIM)
         return fail(LAROSA_EUNSUPPORTED, "sparse_layer: dimension > %d", LAROSA_MAX_DIM);
     if (s->max_ctx <= 0) return fail(LAROSA_EINVAL, "sparse_layer: max_ctx must be > 0");
-    if ((int64_t)s->batch * w->n_kv_heads > (int64_t)kGemvTicketBase)
-        return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch * Hkv too large");
+    if ((int64_t)s->batch * w->n_q_heads > (int64_t)kAttnGroupCounterOff)
+        return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch * Hq too large");
     const int64_t nq = w->n_q_heads * w->head_dim;
     if (p->k_h1 < 0 || p->k_h1 > w->d || p->k_h2 < 0 || p->k_h2 > nq || p->k_h3 < 0 || p->k_h3 > w->d || p->k_h4 < 0 ||
         p->k_h4 > w->inter || p->k_next_h1 > w->d)
@@ -1167,7 +1159,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         aa.hq = (int)L.hq;
         aa.hkv = (int)L.hkv;
         aa.hd = (int)L.hd;
-        aa.chunk = attn_chunk(s->max_ctx, B * (int)L.hkv);
+        aa.chunk = attn_chunk(s->max_ctx, B * (int)L.hq);
         aa.n_chunks = (int)((s->max_ctx + aa.chunk - 1) / aa.chunk);
         aa.part = W.attn_part;
         aa.counters = W.attn_cnt;
@@ -1175,7 +1167,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         if (fused) aa.out_sel = W.sel[1];
         aa.tl = tl_slot(1);
 
-        if (on(2)) LAROSA_TRY(launch_attention(aa, B * (int)L.hkv, (int)L.hd, L.G, st));
+        if (on(2)) LAROSA_TRY(launch_attention(aa, B * (int)L.hq, (int)L.hd, L.G, st));
         LAROSA_TRY(tap_copy(T.h2, W.h2, sizeof(float) * B * L.nq, st));
     }
     // ---- h2 -> O; epilogue r_mid = r + y_o (h3) -------------------------------------------------
@@ -1313,9 +1305,9 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     q->sel.hist = c.take<uint32_t>(kSelHistAlloc);
     q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
-    const int ch = attn_chunk(max_ctx, (int)S.hkv_l);
+    const int ch = attn_chunk(max_ctx, (int)S.hq_l);
     const int nch = (int)((max_ctx + ch - 1) / ch);
-    q->attn_part = c.take<float>((size_t)S.hkv_l * nch * S.G * (S.hd + 2));
+    q->attn_part = c.take<float>((size_t)S.hq_l * nch * (S.hd + 2));
     q->attn_cnt = c.counters(kAttnCounterBase);
     q->tickets = c.counters(kGemvTicketBase);
 }
@@ -1424,12 +1416,12 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     aa.hq = (int)S.hq_l;
     aa.hkv = (int)S.hkv_l;
     aa.hd = (int)S.hd;
-    aa.chunk = attn_chunk(max_ctx, (int)S.hkv_l);
+    aa.chunk = attn_chunk(max_ctx, (int)S.hq_l);
     aa.n_chunks = (int)((max_ctx + aa.chunk - 1) / aa.chunk);
     aa.part = W.attn_part;
     aa.counters = W.attn_cnt;
     aa.out = out;
-    return launch_attention(aa, (int)S.hkv_l, (int)S.hd, S.G, st);
+    return launch_attention(aa, (int)S.hq_l, (int)S.hd, S.G, st);
 }
 
 

@@ -79,7 +79,11 @@ def run_layer(lw, plan, resid, kc, vc, pos):
     # adapter folded into the down projection (larosa.h adapter_in_down): batch 1 companion
     # CTAs, batch 3 (CUDA-core THRESH + DENSE), batch 16 (tcgen05), the 7B block
     (SMALL, 1, 7, 0.5, True), (SMALL_MHA, 3, 40, 0.4, True), (SMALL, 16, 30, 0.5, True),
-    (synth.MODELS["llama2-7b"], 1, 256, 0.5, True), (synth.MODELS["llama3-8b"], 1, 64, 0.4, True)])
+    (synth.MODELS["llama2-7b"], 1, 256, 0.5, True), (synth.MODELS["llama3-8b"], 1, 64, 0.4, True),
+    # BASELINE configs[3] shapes: Mistral-7B (GQA 32/8, theta 1e6) and Qwen2.5-7B (d 3584, GQA 28/4,
+    # QKV bias, eps 1e-6), batch 1 at 60% / 25% and batch 3
+    (synth.MODELS["mistral-7b"], 1, 100, 0.6, True), (synth.MODELS["qwen2.5-7b"], 1, 77, 0.25, True),
+    (synth.MODELS["qwen2.5-7b"], 3, 50, 0.5, False)])
 def test_layer_p6_sitewise(shape, batch, ctx, p, merged):
     max_ctx = max(ctx, 64)
     orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p, merged=merged)
