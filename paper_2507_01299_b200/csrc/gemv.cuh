@@ -902,35 +902,43 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 }
 
 // ---- standalone SELECT preparation: histogram + per-slice sums of squares of x ------------
-// (batch 1, when the site vector was not produced by a GEMV epilogue).  One CTA of 1024
-// threads; overwrites the 4096-bin histogram and writes ceil(d / 256) partials with the
-// exact arithmetic of gemv_epilogue.
-constexpr int kPrepThreads = 1024;
-__global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* __restrict__ x, int d, SiteSel o) {
-    __shared__ float sgrp[LAROSA_MAX_DIM / 32];
+// (batch 1, when the site vector was not produced by a GEMV epilogue).  One 256-thread CTA per
+// 256-element slice: the CTAs zero the bins, meet at a grid barrier (all CTAs are co-resident:
+// d <= 32768 -> <= 128 small CTAs), then each pushes its slice's elements and writes the slice's
+// sum of squares with the exact arithmetic of gemv_epilogue.  bar: 2 zero-at-rest words.
+constexpr int kPrepThreads = kSliceCols;
+__global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* __restrict__ x, int d, SiteSel o,
+                                                                   unsigned* bar) {
+    __shared__ float sred[kPrepThreads / 32];
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int i = tid; i < kSelHistTotal / 4; i += kPrepThreads) reinterpret_cast<uint4*>(o.hist)[i] = make_uint4(0, 0, 0, 0);
-    __threadfence();
+    const int nct = gridDim.x, cta = blockIdx.x;
+    for (int i = cta * kPrepThreads + tid; i < kSelHistTotal / 4; i += nct * kPrepThreads)
+        reinterpret_cast<uint4*>(o.hist)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    const int ngrp = (d + 31) / 32;
-    for (int g = wid; g < ngrp; g += kPrepThreads / 32) {
-        const int i = g * 32 + lane;
-        const float v = i < d ? x[i] : 0.f;
-        if (i < d) hist_push(o, v, i);
-        const float w = slice_ssq_warp(v);
-        if (lane == 0) sgrp[g] = w;
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(&bar[0], 1u);
+        unsigned seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+            if (seen < (unsigned)nct) __nanosleep(64);
+        } while (seen < (unsigned)nct);
     }
     __syncthreads();
+    const int i = cta * kPrepThreads + tid;
+    const float v = i < d ? x[i] : 0.f;
+    if (i < d) hist_push(o, v, i);
     if (o.ssq) {
-        const int nsl = (d + kSliceCols - 1) / kSliceCols;
-        for (int s = tid; s < nsl; s += kPrepThreads) {
-            float w8[8];
-#pragma unroll
-            for (int w = 0; w < 8; ++w) w8[w] = 8 * s + w < ngrp ? sgrp[8 * s + w] : 0.f;
-            o.ssq[s] = slice_ssq_combine(w8);
-        }
+        const float w = slice_ssq_warp(v);
+        if (lane == 0) sred[wid] = w;
+        __syncthreads();
+        if (tid == 0) o.ssq[cta] = slice_ssq_combine(sred);
+    }
+    if (tid == 0 && atomicAdd(&bar[1], 1u) == (unsigned)nct - 1u) {   // every CTA is past the barrier
+        bar[0] = 0u;
+        bar[1] = 0u;
     }
 }
 

@@ -102,6 +102,7 @@ cudaError_t allow_smem(K kern, size_t bytes) {
 constexpr size_t kCounterHeaderWords = 8192;   // attention tickets
 constexpr size_t kAttnCounterBase = 0;        // [0, 4096): attention group tickets
 constexpr size_t kGemvTicketBase = 4096;      // + 256 j: slice tickets of the j-th epilogue GEMV
+constexpr size_t kPrepBarrier = 6000;         // 2 words: grid barrier of select_prep_kernel
 
 struct Carver {
     char* base;      // nullptr -> size query
@@ -120,6 +121,7 @@ struct Carver {
     size_t size() const { return (off + 255) & ~size_t(255); }
 };
 
+int n_slices_of(int64_t n) { return (int)((n + kSliceCols - 1) / kSliceCols); }
 int pad_batch(int b) { return b <= 1 ? 1 : b <= 2 ? 2 : b <= 4 ? 4 : b <= 8 ? 8 : 16; }
 
 // ============================================================================== GEMV plan
@@ -563,7 +565,8 @@ static larosa_status topk_sparse_gemv_impl(const float* x, int64_t d_in, int64_t
     carve_topk_gemv(c, d_in, d_out, &acc, &sel);
     if (rms_eps < 0.f) sel.ssq = nullptr;
     if (!prepared)
-        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)d_in, sel),
+        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(d_in)), dim3(kPrepThreads), 0, st, x, (int)d_in,
+                                     sel, c.counters(kPrepBarrier)),
                               "select prep launch"));
     const GemvPlan p = W2 ? plan_gemv_comp(d_out, k, d_in, d2) : plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
     GemvArgs a = gemv_args_base();
@@ -1129,8 +1132,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     // ---- h1: r (RMS) -> QKV ---------------------------------------------------------------------
     if (fused) {
         if (!s->chained && on(0))
-            LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, (const float*)s->resid,
-                                         (int)L.d, W.sel[0]),
+            LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(L.d)), dim3(kPrepThreads), 0, st,
+                                         (const float*)s->resid, (int)L.d, W.sel[0], c.counters(kPrepBarrier)),
                                   "select prep launch"));
     } else if (on(0)) {
         LAROSA_TRY(rule_topk(0, s->resid, L.d, plan->k_h1, w->rms_eps));
@@ -1381,7 +1384,8 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         // the gathered vector is identical on every rank -> identical selection data
         SiteSel sel = W.sel;
         if (eps < 0.f) sel.ssq = nullptr;
-        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(1), dim3(kPrepThreads), 0, st, x, (int)din, sel),
+        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(din)), dim3(kPrepThreads), 0, st, x, (int)din,
+                                     sel, c.counters(kPrepBarrier)),
                               "select prep launch"));
         a.mode = GEMV_SELECT;
         a.sel = sel;
