@@ -417,7 +417,8 @@ def run_sharded(args):
     qs = [synth.haar_orthogonal(shape.d, 300 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
     shards, kvs = [], []
     for i in range(n_copies):
-        full = M.fold_layer(M.synth_original_layer(shape, 50 + i, device=device), shape, qs[i], qs[i + 1])
+        full = M.fold_layer(M.synth_original_layer(shape, 50 + i, device=device), shape, qs[i], qs[i + 1],
+                            adapter_in_down=args.adapter == "down")
         shards.append(M.ShardedLayer(M.shard_layer(full, rank, ws_n), rank, ws_n, max_ctx, device))
         del full
         torch.cuda.empty_cache()
@@ -472,9 +473,10 @@ def run_sharded(args):
                "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
                "config": {"workload": "LLaMA3-70B decoder layer (8192 hidden, 28672 MLP, GQA 64/8) batch 1, "
                                       "row-sharded", "sparsity": args.p, "plan_k": list(plan), "ctx": max_ctx,
-                          "layer_copies": n_copies, "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x5/layer)",
+                          "layer_copies": n_copies,
+                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{shards[0].n_phases()}/layer)",
                           "l2": "inputs larger than L2: 4 distinct layer shards cycled"},
-               "gpu_launches": (5 * 2 + 1) * args.steps, "clocks": clk.summary()}
+               "gpu_launches": (2 * shards[0].n_phases() + 1) * args.steps, "clocks": clk.summary()}
         print(json.dumps(out))
     if ws_n > 1:
         dist.destroy_process_group()

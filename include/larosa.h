@@ -312,6 +312,9 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
  *   3: x = h4 (full)     -> Top-K h4 -> down (local cols) -> out = r_mid + y_down [d/n]
  *   4: x = that (full)   -> adapter (dense, local cols)   -> out = r_next cols [d/n]
  *      (phase 4 is skipped when adapter == NULL: phase 3's output is r_next)
+ * With adapter_in_down (w_down = Wd Q_{l+1}, SURVEY §8(e) "4-gather form"): phase 3 computes
+ *   out = r_next cols = r_mid A_l[:, cols] + Top-K(h4) w_down[:, cols] (resid = the full r_mid),
+ *   and there is no phase 4 (EINVAL): 4 all-gathers per layer.
  * resid = the full residual r (phases 1, 3 read r resp. r_mid from it: pass phase 0's x for
  * phase 1 and phase 2's x for phase 3).  Every rank derives the identical Top-K rule from
  * the identical gathered vector, so kept sets agree across ranks by construction.

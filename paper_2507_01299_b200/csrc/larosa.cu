@@ -1353,6 +1353,8 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     ShardWs W;
     carve_shard(c, S, max_ctx > 0 ? max_ctx : 1, &W);
     const int r = sh->rank;
+    const bool merged = w->adapter && w->adapter_in_down;   // 4 phases: the adapter rides with phase 3
+    if (merged && phase == 4) return fail(LAROSA_EINVAL, "shard_phase: no phase 4 when adapter_in_down");
     // phase -> (site input width, k, RMS eps, weights, local output width)
     int64_t din = S.d, k = 0, dout = 0;
     float eps = -1.0f;
@@ -1393,11 +1395,17 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         a.sel_k = (int)k;
         a.sel_eps = eps;
         p = plan_gemv(dout, k, 1, GEMV_SELECT, din);
+        if (phase == 3 && merged) {   // + the dense r_mid rows of this rank's adapter columns
+            a.W2 = w->adapter;
+            a.x2 = resid;
+            a.d2 = (int)S.d;
+            p = plan_gemv_comp(dout, k, din, S.d);
+        }
     }
     if (phase != 0) {
-        a.epi = phase == 2 ? EPI_SILU : (phase == 4 ? EPI_STORE : EPI_RESID);
+        a.epi = phase == 2 ? EPI_SILU : ((phase == 4 || (phase == 3 && merged)) ? EPI_STORE : EPI_RESID);
         a.tickets = W.tickets;
-        if (phase == 1 || phase == 3) {
+        if (phase == 1 || (phase == 3 && !merged)) {
             a.res = resid + (size_t)r * S.dl;   // this rank's columns of r (phase 1) / r_mid (phase 3)
             a.res_ld = S.d;
         }

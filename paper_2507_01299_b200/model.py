@@ -184,7 +184,7 @@ def shard_layer(w: LZ.LayerWeights, rank: int, world: int) -> LZ.LayerWeights:
                            w_down=cols(w.w_down, rank * dl, (rank + 1) * dl), d=w.d, inter=w.inter,
                            n_q_heads=w.n_q_heads, n_kv_heads=w.n_kv_heads, head_dim=hd, rope_theta=w.rope_theta,
                            rms_eps=w.rms_eps, b_qkv=qkv(w.b_qkv),
-                           adapter=cols(w.adapter, rank * dl, (rank + 1) * dl))
+                           adapter=cols(w.adapter, rank * dl, (rank + 1) * dl), adapter_in_down=w.adapter_in_down)
 
 
 def shard_kv(cache: torch.Tensor, rank: int, world: int) -> torch.Tensor:
@@ -217,7 +217,8 @@ class ShardedLayer:
         return self.local[phase]
 
     def n_phases(self) -> int:
-        return 5 if self.w.adapter is not None else 4
+        """5 with the literal adapter phase; 4 without an adapter or with it folded beside down."""
+        return 5 if self.w.adapter is not None and not self.w.adapter_in_down else 4
 
     def inputs(self, phase: int, r: torch.Tensor):
         """(x, resid) of a phase given the layer input r and the gathered earlier outputs."""

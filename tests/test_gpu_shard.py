@@ -36,13 +36,15 @@ def unpack_gu(wgu):
     return blk[:, :, 0, :].reshape(d, -1), blk[:, :, 1, :].reshape(d, -1)
 
 
-@pytest.mark.parametrize("world,p", [(1, 0.5), (2, 0.5), (4, 0.4)])
-def test_shard_phases_emulated(world, p):
+@pytest.mark.parametrize("world,p,merged", [(1, 0.5, False), (2, 0.5, False), (4, 0.4, False), (1, 0.5, True),
+                                            (2, 0.5, True), (4, 0.4, True)])
+def test_shard_phases_emulated(world, p, merged):
+    """merged: the adapter folded beside down (4 phases / 4 all-gathers)."""
     shape = SMALL_MHA
     orig = M.synth_original_layer(shape, 21, device=DEV)
     q_l = synth.haar_orthogonal(shape.d, 31, device=DEV, dtype=torch.float32)
     q_n = synth.haar_orthogonal(shape.d, 32, device=DEV, dtype=torch.float32)
-    lw = M.fold_layer(orig, shape, q_l, q_n)
+    lw = M.fold_layer(orig, shape, q_l, q_n, adapter_in_down=merged)
     plan = M.site_plan(shape, p)
     max_ctx, pos = 32, 20
     kc = synth.gaussian_bf16((1, shape.hkv, max_ctx, shape.hd), 41, 1.0, DEV)
@@ -93,6 +95,10 @@ def test_shard_phases_emulated(world, p):
                 wg, wu = unpack_gu(w64(w.w_gu))
                 v = x_np[s] * O.rms_scale(x_np, cfg_eps)
                 ref = O.silu(O.sparse_gemv(wg, s, v)) * O.sparse_gemv(wu, s, v)
+                tol = 1e-5
+            elif ph == 3 and merged:   # r_next cols = r_mid A_l[:, cols] + h4[S4] (Wd Q_{l+1})[:, cols]
+                s = O.topk(x_np, k4)
+                ref = O.dense_gemv(w64(w.adapter), res_np) + O.sparse_gemv(w64(w.w_down), s, x_np[s])
                 tol = 1e-5
             elif ph == 3:
                 s = O.topk(x_np, k4)

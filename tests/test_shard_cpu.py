@@ -51,14 +51,14 @@ def toy(seed):
     return w, kc, vc, r
 
 
-def layer_weights(w):
+def layer_weights(w, merged=False):
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a))   # noqa: E731
     return LZ.LayerWeights(w_qkv=t(w["wqkv"]), w_o=t(w["wo"]), w_gu=t(pack_gu(w["wg"], w["wu"])), w_down=t(w["wd"]),
                            d=D, inter=INTER, n_q_heads=HQ, n_kv_heads=HKV, head_dim=HD, rope_theta=10000.0,
-                           rms_eps=1e-6, b_qkv=t(w["bqkv"]), adapter=t(w["adapter"]))
+                           rms_eps=1e-6, b_qkv=t(w["bqkv"]), adapter=t(w["adapter"]), adapter_in_down=merged)
 
 
-def oracle_phase(ph, ws, plan, x, resid, kc, vc, pos, rank, world):
+def oracle_phase(ph, ws, plan, x, resid, kc, vc, pos, rank, world, merged=False):
     """The phase contract of larosa_sparse_layer_shard_phase, computed with oracle primitives."""
     k1, k2, k3, k4 = plan
     n = lambda t: t.numpy()   # noqa: E731
@@ -83,40 +83,45 @@ def oracle_phase(ph, ws, plan, x, resid, kc, vc, pos, rank, world):
         wg, wu = unpack_gu(n(ws.w_gu))
         v = x[s] * O.rms_scale(x, 1e-6)
         return O.silu(O.sparse_gemv(wg, s, v)) * O.sparse_gemv(wu, s, v)
+    if ph == 3 and merged:   # adapter folded beside down: r_next cols = r_mid A[:, cols] + y_down cols
+        s = O.topk(x, k4)
+        return O.rotate(resid, n(ws.adapter)) + O.sparse_gemv(n(ws.w_down), s, x[s])
     if ph == 3:
         s = O.topk(x, k4)
         return resid[rank * dl:(rank + 1) * dl] + O.sparse_gemv(n(ws.w_down), s, x[s])
     return O.dense_gemv(n(ws.adapter), x)
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, merged=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         w, kc, vc, r = toy(5)
         plan = O.site_ks(0.5, (1, 1, 1, 1), D, INTER)
         plan = (plan[0], O.compute_k(1.0, 0.5, HQ * HD), plan[2], plan[3])
-        ws = M.shard_layer(layer_weights(w), rank, world)
+        ws = M.shard_layer(layer_weights(w, merged), rank, world)
         hk = HKV // world
         kc_l, vc_l = kc[rank * hk:(rank + 1) * hk].copy(), vc[rank * hk:(rank + 1) * hk].copy()
         pos = CTX - 1
         full = {}
         x = r.copy()
-        for ph in range(5):
+        for ph in range(4 if merged else 5):
             xin = {0: r, 1: full.get(0), 2: full.get(1), 3: full.get(2), 4: full.get(3)}[ph]
             res = {1: r, 3: full.get(1)}.get(ph)
-            out = torch.from_numpy(oracle_phase(ph, ws, plan, xin, res, kc_l, vc_l, pos, rank, world))
+            out = torch.from_numpy(oracle_phase(ph, ws, plan, xin, res, kc_l, vc_l, pos, rank, world, merged))
             g = torch.empty(out.numel() * world, dtype=out.dtype)
             dist.all_gather_into_tensor(g, out)
             full[ph] = g.numpy()
         # unsharded reference
         wf = {"wqkv": w["wqkv"], "bqkv": w["bqkv"], "wo": w["wo"], "wg": w["wg"], "wu": w["wu"], "wd": w["wd"]}
         cfg = dict(hq=HQ, hkv=HKV, hd=HD, eps=1e-6, theta=10000.0)
-        ref, inter = O.larosa_block(r, wf, cfg, plan, kc.copy(), vc.copy(), pos, adapter=w["adapter"])
+        ref, inter = O.larosa_block(r, wf, cfg, plan, kc.copy(), vc.copy(), pos, adapter=w["adapter"],
+                                    adapter_in_down=merged)
+        last = full[3] if merged else full[4]
         ok = (np.array_equal(full[0], inter["h2"]) and np.array_equal(full[1], inter["r_mid"])
-              and np.array_equal(full[2], inter["h4"]) and np.array_equal(full[3], inter["r_out"])
-              and np.array_equal(full[4], ref))
-        q.put((rank, ok, float(np.max(np.abs(full[4] - ref)))))
+              and np.array_equal(full[2], inter["h4"]) and np.array_equal(last, ref)
+              and (merged or np.array_equal(full[3], inter["r_out"])))
+        q.put((rank, ok, float(np.max(np.abs(last - ref)))))
     finally:
         dist.destroy_process_group()
 
@@ -129,12 +134,13 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_layer_gloo_equals_unsharded(world):
+@pytest.mark.parametrize("world,merged", [(2, False), (2, True)])
+def test_sharded_layer_gloo_equals_unsharded(world, merged):
+    """merged: the adapter folded beside down -- 4 phases / 4 all-gathers."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, q, merged)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
