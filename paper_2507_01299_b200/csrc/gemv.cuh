@@ -156,6 +156,10 @@ struct GemvArgs {
     unsigned long long* tl;            // debug timeline slot (5 x u64) or null
     int sel_dbg;                       // profiling: bitmask of select phases to skip (0 = none)
     int tc_dbg;                        // profiling (tcgen05 GEMV): 1 skip MMAs, 2 skip values, 4 skip A copies
+    // batch-1 split-K reduction through distributed shared memory: the gridDim.y CTAs of a
+    // slice form one thread-block cluster (cluster != 0); rank 0 sums the CTAs' fp32 column
+    // partials in rank order and finalises the slice itself (no global accumulators, no ticket)
+    int cluster;
 };
 
 __host__ __device__ constexpr size_t gemv_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -614,8 +618,10 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
 }
 
 // ---- epilogue: the last split CTA of a slice finalises its columns ------------------------
+// tot == nullptr: the slice's sums are in the global fixed-point accumulators (re-zeroed here);
+// else tot[256] (shared memory, batch 1) holds them in fp32 (cluster reduction).
 template <int BP>
-__device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred) {
+__device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred, const float* tot = nullptr) {
     const int c = threadIdx.x, lane = c & 31, wid = c >> 5;
     const int base = slice * kSliceCols;
     for (int b = 0; b < a.batch; ++b) {
@@ -628,10 +634,16 @@ __device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred) {
                 const int blk = c / kGuBlock, q = c % kGuBlock;
                 const int og = base + blk * 2 * kGuBlock + q;
                 if (og < a.d_out) {
-                    const float g = fix_to_f(__ldcg(acc + og));
-                    const float u = fix_to_f(__ldcg(acc + og + kGuBlock));
-                    acc[og] = 0ull;
-                    acc[og + kGuBlock] = 0ull;
+                    float g, u;
+                    if (tot) {
+                        g = tot[og - base];
+                        u = tot[og - base + kGuBlock];
+                    } else {
+                        g = fix_to_f(__ldcg(acc + og));
+                        u = fix_to_f(__ldcg(acc + og + kGuBlock));
+                        acc[og] = 0ull;
+                        acc[og + kGuBlock] = 0ull;
+                    }
                     v = g / (1.0f + expf(-g)) * u;
                     a.out[(size_t)b * a.out_ld + slice * 2 * kGuBlock + blk * kGuBlock + q] = v;
                     has = true;
@@ -640,8 +652,13 @@ __device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred) {
         } else {
             const int o = base + c;
             if (o < a.d_out) {
-                const float y = fix_to_f(__ldcg(acc + o));
-                acc[o] = 0ull;
+                float y;
+                if (tot) {
+                    y = tot[c];
+                } else {
+                    y = fix_to_f(__ldcg(acc + o));
+                    acc[o] = 0ull;
+                }
                 v = y;
                 if (a.bias) v += bf16f(a.bias[o]);
                 if (a.res) v = a.res[(size_t)b * a.res_ld + o] + v;
@@ -871,6 +888,45 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     __syncthreads();
     const int c = threadIdx.x;                     // 256 threads <-> 256 columns
     const int o = slice * kSliceCols + c;
+    if constexpr (BP == 1) {
+        if (a.cluster) {
+            // cluster split-K: every CTA's column partials in its own shared memory, rank 0 sums
+            // them in rank order (deterministic) and finalises; the others wait until it has read
+            float* cpart = part + kGemvWarps * kSliceCols;   // [256]
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < kGemvWarps; ++w) s += part[(size_t)w * kSliceCols + c];
+            cpart[c] = n_list > 0 ? s : 0.f;
+            cluster_sync_all();
+            const uint32_t rank = cluster_ctarank();
+            if (rank != 0) {
+                cluster_sync_all();
+                tl_stamp(a.tl, 4);
+                return;
+            }
+            tl_stamp(a.tl, 12);
+            float t = 0.f;
+            const uint32_t my = smem_u32(cpart + c);
+            for (int r = 0; r < a.cluster; ++r) {
+                uint32_t addr;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(my), "r"(r));
+                t += dsmem_ld_f32(addr);
+            }
+            cluster_sync_all();                              // the peers may exit now
+            float* tot = cpart + kSliceCols;                  // [256]
+            tot[c] = t;
+            if (a.epi == EPI_NONE) {                         // the consumer kernel reads the accumulators
+                if (o < a.d_out) a.acc[o] = f_to_fix(t);
+                tl_stamp(a.tl, 4);
+                return;
+            }
+            __syncthreads();
+            tl_stamp(a.tl, 13);
+            gemv_epilogue<BP>(a, slice, reinterpret_cast<float*>(misc + 16), tot);
+            tl_stamp(a.tl, 4);
+            return;
+        }
+    }
     if (o < a.d_out && n_list > 0) {
         for (int b = 0; b < a.batch; ++b) {
             float s = 0.f;

@@ -277,3 +277,25 @@ def test_topk_sparse_gemv_dense2_p3(d_in, d2, d_out, k):
     # repeatable (fixed-point accumulation; companion CTAs finish in any order)
     for _ in range(2):
         assert torch.equal(LZ.topk_sparse_gemv_dense2(x.to(DEV), k, Wb.to(DEV), x2.to(DEV), W2.to(DEV)), y)
+
+
+def test_topk_sparse_gemv_cluster_reduction_matches():
+    """The opt-in cluster split-K reduction (LAROSA_GEMV_CLUSTER=1) against the oracle, in a
+    subprocess (the library reads the switch once per process)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import synth, oracle as O; from paper_2507_01299_b200 import larosa as LZ;"
+        "x = synth.residual_activation(1, 11008, seed=9)[0]; W = synth.gaussian_bf16((11008, 4096), 8, 11008 ** -0.5);"
+        "x2 = synth.residual_activation(1, 4096, seed=10)[0]; W2 = synth.gaussian_bf16((4096, 4096), 11, 4096 ** -0.5);"
+        "y = LZ.topk_sparse_gemv_dense2(x.cuda(), 5504, W.cuda(), x2.cuda(), W2.cuda()).cpu().numpy().astype(np.float64);"
+        "xd = x.numpy().astype(np.float64); idx = O.topk(xd, 5504);"
+        "w64 = lambda t: O.bf16_to_f64(t.numpy().view(np.uint16));"
+        "ref = O.sparse_gemv(w64(W), idx, xd[idx]) + O.dense_gemv(w64(W2), x2.numpy().astype(np.float64));"
+        "err = np.max(np.abs(y - ref)) / np.linalg.norm(ref); print(err); assert err <= 1e-5")
+    import os
+    env = dict(os.environ, LAROSA_GEMV_CLUSTER="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout + r.stderr
