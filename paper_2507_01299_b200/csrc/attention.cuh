@@ -40,6 +40,7 @@ struct AttnArgs {
     uint32_t* zero_hist;   // optional histogram to re-zero (its consumer has completed)
     int zero_words;
     unsigned long long* tl;   // debug timeline slot or null
+    int keep_acc;          // 1: leave the QKV accumulators to the next kernel to re-zero (batch-1 layer)
 };
 
 constexpr int kAttnGroupCounterOff = 2048;   // counters: [0, B Hq) head tickets, then group tickets
@@ -290,6 +291,7 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
         if (a.out_sel.hist) hist_push(a.out_sel, hv, h * hd + dd);
     }
     tl_stamp(a.tl, 6);
+    if (a.keep_acc) return;   // the O GEMV re-zeroes the QKV accumulators after this kernel
     // every chunk CTA of head h has read its q accumulators: re-zero them.  The group's k / v
     // accumulators are read by all G heads: the last head merger of the group re-zeroes them.
     unsigned long long* accz = a.acc + (size_t)b * a.acc_ld;

@@ -144,6 +144,8 @@ struct GemvArgs {
     int64_t out_ssq_ld;
     uint32_t* zero_hist;               // optional: histogram words to re-zero (free by now)
     int zero_words;
+    unsigned long long* zero_acc;      // optional: accumulators to re-zero (their consumer has completed)
+    int zero_acc_words;
     // SELECT companion rows (batch 1): CTAs with blockIdx.y < n_splits2 stream DENSE rows of a
     // second matrix W2 [d2][ld] with values x2 [d2] into the same output columns (the residual
     // adapter folded next to the down projection: r_next = r_mid A_l + h4[S4] W_down Q_{l+1}).
@@ -741,6 +743,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     if (a.zero_hist) {   // a histogram whose consumer has completed (kernel-boundary ordered)
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
         for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;
+    }
+    if (a.zero_acc) {    // accumulators whose consumer has completed
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_acc_words; i += nct * kGemvThreads) a.zero_acc[i] = 0ull;
     }
 
     // ---- 1. this CTA's row list in shared memory (ascending) ------------------------------

@@ -1210,6 +1210,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         aa.counters = W.attn_cnt;
         aa.out = W.h2;
         if (fused) aa.out_sel = W.sel[1];
+        aa.keep_acc = fused && on(4);   // batch 1: the O GEMV re-zeroes acc_qkv
         aa.tl = tl_slot(1);
 
         if (on(2)) LAROSA_TRY(launch_attention(aa, B * (int)L.hq, (int)L.hd, L.G, st));
@@ -1221,6 +1222,10 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     if (on(4)) {
         GemvArgs a = site_gemv(1, W.h2, L.nq, plan->k_h2, -1.0f, w->w_o, L.d, W.acc_o);
         epi(a, 0, EPI_RESID, s->resid, W.rmid, 2);
+        if (fused) {   // attention (complete by now) left the QKV accumulators to be re-zeroed here
+            a.zero_acc = W.acc_qkv;
+            a.zero_acc_words = (int)L.nqkv;
+        }
         a.tl = tl_slot(2);
         a.zero_hist = fused ? W.sel[0].hist : nullptr;   // h1's consumer (QKV) is done
         a.zero_words = kSelHistTotal;
