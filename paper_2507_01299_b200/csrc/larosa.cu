@@ -166,7 +166,8 @@ GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp, int mode = GEMV_LIST
         by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);   // words per CTA
     }
     for (int it = 0; it < 2; ++it) {
-        const int target = sm_count() * per_sm;
+        static const int sel_wave_pct = env_int("LAROSA_SEL_WAVE_PCT", 100);   // SELECT: waves of CTAs (tuning)
+        const int target = mode == GEMV_SELECT ? sm_count() * per_sm * sel_wave_pct / 100 : sm_count() * per_sm;
         int by_target = std::max(1, target / p.n_slices);   // one wave: slices x splits <= target
         // SELECT: cap the splits at the cluster size when that keeps >= 85% of the wave's slots
         if (mode == GEMV_SELECT && gemv_cluster_enabled() && by_target > kMaxGemvCluster &&
@@ -190,16 +191,25 @@ GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp, int mode = GEMV_LIST
 GemvPlan plan_gemv_comp(int64_t d_out, int64_t k, int64_t d_in, int64_t d2) {
     static const int pct_env = env_int("LAROSA_COMP_PCT", 0);
     GemvPlan p = plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
-    int total = std::max(2, sm_count() * 2 / p.n_slices);
+    // ~1.3 waves of 2 CTAs per SM, one third companions (measured on the LLaMA2-7B block: the
+    // companions finish early and free their slots; more, shorter SELECT CTAs shorten the tail)
+    static const int wave_pct = env_int("LAROSA_COMP_WAVE_PCT", 130);
+    int total = std::max(2, (sm_count() * 2 * wave_pct / 100 + p.n_slices - 1) / p.n_slices);
     if (gemv_cluster_enabled() && total > kMaxGemvCluster && p.n_slices * kMaxGemvCluster * 100 >= sm_count() * 2 * 85)
         total = kMaxGemvCluster;
     const int64_t nwords = (d_in + 31) / 32;
     const int min_sel = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
-    int n2 = pct_env > 0 ? (total * pct_env + 50) / 100 : (int)((double)total * d2 / (double)(k + d2) + 0.5);
+    int n2 = pct_env > 0 ? (total * pct_env + 50) / 100 : (total + 1) / 3;
     n2 = std::max(1, std::min(n2, total - min_sel));
     p.n_splits = std::max(min_sel, total - n2);
     p.list_cap = (int)(32 * ((nwords + p.n_splits - 1) / p.n_splits));
     n2 = std::max<int>(n2, (int)((d2 + p.list_cap - 1) / p.list_cap));
+    static const int sel_env = env_int("LAROSA_COMP_SEL", 0), n2_env = env_int("LAROSA_COMP_N", 0);   // tuning
+    if (sel_env > 0) {
+        p.n_splits = std::max(min_sel, sel_env);
+        p.list_cap = (int)(32 * ((nwords + p.n_splits - 1) / p.n_splits));
+    }
+    if (n2_env > 0) n2 = std::max<int>(n2_env, (int)((d2 + p.list_cap - 1) / p.list_cap));
     p.n_splits2 = n2;
     p.smem = gemv_smem_bytes(1, p.list_cap, GEMV_SELECT, (int)d_in);
     return p;

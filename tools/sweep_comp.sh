@@ -1,2 +1,1 @@
-for pct in 0 35 45 50 55 65; do LAROSA_COMP_PCT=$pct TAG=pct$pct python tools/layer_us.py 0.5 2000; done
-ADAPTER=separate TAG=separate python tools/layer_us.py 0.5 2000
+for w in 100 115 130 150; do LAROSA_SEL_WAVE_PCT=$w TAG=selwave$w python tools/layer_us.py 0.5 3000; done
