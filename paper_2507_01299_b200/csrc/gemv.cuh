@@ -49,7 +49,10 @@ constexpr int kSliceCols = 256;       // columns per CTA (8 per lane)
 constexpr int kGemvWarps = 8;
 constexpr int kGemvThreads = kGemvWarps * 32;
 constexpr int kStageRows = 4;         // rows per stage (one 512-byte warp copy each)
-constexpr int kStages = 4;            // ring depth per warp
+#ifndef LAROSA_GEMV_STAGES
+#define LAROSA_GEMV_STAGES 4
+#endif
+constexpr int kStages = LAROSA_GEMV_STAGES;   // ring depth per warp
 constexpr int kWarpRingBytes = kStages * kStageRows * kSliceCols * 2;   // 8 KB
 constexpr double kFixScale = 4294967296.0;                              // 2^32
 constexpr int kGemvMisc = 128;        // ints of scratch
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     // stage st covers my-rows [4 st, 4 st + 4)
     auto issue = [&](int st) {
         if (st < n_st) {
-            unsigned char* dst = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
+            unsigned char* dst = mychunk + (size_t)(st % kStages) * (kStageRows * kSliceCols * 2);
 #pragma unroll
             for (int g = 0; g < kStageRows; ++g) {
                 const int m = st * kStageRows + g;
@@ -859,7 +862,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 
     for (int st = 0; st < n_st; ++st) {
         cp_async_wait<kStages - 1>();          // this lane's chunks of stage st have landed
-        const unsigned char* src = mychunk + (size_t)(st & (kStages - 1)) * (kStageRows * kSliceCols * 2);
+        const unsigned char* src = mychunk + (size_t)(st % kStages) * (kStageRows * kSliceCols * 2);
 #pragma unroll
         for (int g = 0; g < kStageRows; ++g) {
             const int m = st * kStageRows + g;

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liblarosa.so")
+LIB_PATH = os.environ.get("LAROSA_LIB") or os.path.join(_HERE, "lib", "liblarosa.so")   # env: experiments only
 
 LAROSA_LEFT_QT = 0
 LAROSA_RIGHT_Q = 1
