@@ -324,6 +324,28 @@ def model_sweep_extra(device, models=("mistral-7b", "qwen2.5-7b"), ps=(0.0, 0.25
     return out
 
 
+def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
+    """SURVEY §8(f) N1 at the paper's calibration size (16 sequences x 2048 tokens) for
+    a d = 4096 layer: covariance on tcgen05 (TFLOP/s of 2 n d^2) and the fp64 PCA rotation."""
+    from paper_2507_01299_b200 import larosa as LZ
+    X = synth.gaussian_bf16((n_seq * n_tok, d), 3, 1.0, device)
+    C = torch.zeros((d, d), dtype=torch.float32, device=device)
+    LZ.calib_covariance(X, scale=1.0 / n_seq, out=C)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        LZ.calib_covariance(X, scale=1.0 / n_seq, out=C)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    t0 = time.perf_counter()
+    LZ.pca_rotation(C)
+    pca_ms = (time.perf_counter() - t0) * 1e3
+    return {"d": d, "tokens": n_seq * n_tok, "covariance_ms": ms, "covariance_tflops": 2.0 * n_seq * n_tok * d * d / ms / 1e9,
+            "pca_rotation_ms": pca_ms}
+
+
 def fold_extra(device):
     """larosa_fold_rotation on LLaMA2-7B layer shapes: tcgen05 TFLOP/s (2 M N K of the fold)."""
     from paper_2507_01299_b200 import larosa as LZ
@@ -625,6 +647,7 @@ def main():
     if not args.no_sweep:
         extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device, merged=merged),
                   "fold_tcgen05": fold_extra(device),
+                  "calibration_n1": calibration_extra(device),
                   "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
 
     cpu = None

@@ -332,6 +332,27 @@ larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, con
                                               uint16_t* v_cache, const int32_t* pos, int64_t max_ctx, void* ws,
                                               size_t ws_bytes, larosa_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * Calibration of the rotation (§4.2, eq. 1):
+ * larosa_calib_covariance: C[d][d] fp32 = scale * X^T X (+ C if accumulate != 0) over
+ *   calibration activations X bf16 [n_tok][d] row-major (one layer's residual-stream inputs).
+ *   Eq. 1 is Cov = (1/M) sum_i X_i^T X_i over M sequences, uncentered: pass
+ *   scale = 1/M and accumulate the sequences (or any batching of their tokens).  tcgen05
+ *   path when d % 128 == 0, n_tok % 64 == 0 and X, C are 16-byte aligned (workspace: the
+ *   size query); otherwise a CUDA-core kernel (no workspace needed).  Asynchronous.
+ * larosa_pca_rotation: Q fp32 [d][d] row-major with Q[:, i] the eigenvector of the i-th
+ *   largest eigenvalue of C (symmetrised), lam fp32 [d] the eigenvalues descending (negative
+ *   round-off clamped to 0); each eigenvector's largest-|entry| component is positive (lowest
+ *   row on ties) -- SURVEY Z7.  fp64 symmetric eigensolver (cuSOLVER syevd).  Synchronises the
+ *   stream; LAROSA_ECUDA if the solver does not converge.  Offline (calibration) path.
+ * ------------------------------------------------------------------------------ */
+size_t larosa_calib_covariance_workspace_size(int64_t n_tok, int64_t d);
+larosa_status larosa_calib_covariance(const uint16_t* X, int64_t n_tok, int64_t d, float scale, int32_t accumulate,
+                                      float* C, void* ws, size_t ws_bytes, larosa_stream_t stream);
+size_t larosa_pca_rotation_workspace_size(int64_t d);
+larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q, float* lam, void* ws, size_t ws_bytes,
+                                  larosa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,11 +85,13 @@ __host__ __device__ constexpr int fold_smem_bytes() {
     return 1024 + fold_stages<BN, ASPLIT, BSPLIT>() * fold_stage_bytes<BN, ASPLIT, BSPLIT>() + 128;
 }
 
-template <int BN, bool ASPLIT, bool BSPLIT>
+// F32OUT: the epilogue stores fp32 out[m][n] = scale * acc (+ out[m][n] if accumulate) -- the
+// calibration covariance X^T X (N1); else bf16 RNE (the fold).
+template <int BN, bool ASPLIT, bool BSPLIT, bool F32OUT = false>
 __global__ void __launch_bounds__(kFoldThreads, 1)
     fold_tc_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
                    const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1,
-                   uint16_t* __restrict__ out, int N, int K) {
+                   void* __restrict__ out_raw, int N, int K, float scale = 1.0f, int accumulate = 0) {
     extern __shared__ __align__(1024) unsigned char fold_smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(fold_smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_BYTES = kFoldBM * kFoldBK * 2;
@@ -165,7 +167,8 @@ __global__ void __launch_bounds__(kFoldThreads, 1)
         tc_fence_after();
         const int q = warp & 3;
         const int row = m0 + 32 * q + lane;
-        uint16_t* orow = out + (size_t)row * N + n0;
+        uint16_t* orow = reinterpret_cast<uint16_t*>(out_raw) + (size_t)row * N + n0;
+        float* frow = reinterpret_cast<float*>(out_raw) + (size_t)row * N + n0;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
             uint32_t v[32];
@@ -179,6 +182,23 @@ __global__ void __launch_bounds__(kFoldThreads, 1)
                   "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                 : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if constexpr (F32OUT) {
+                float4* fd = reinterpret_cast<float4*>(frow + c0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float4 o = make_float4(scale * __uint_as_float(v[4 * j]), scale * __uint_as_float(v[4 * j + 1]),
+                                           scale * __uint_as_float(v[4 * j + 2]), scale * __uint_as_float(v[4 * j + 3]));
+                    if (accumulate) {
+                        const float4 pv = fd[j];
+                        o.x += pv.x;
+                        o.y += pv.y;
+                        o.z += pv.z;
+                        o.w += pv.w;
+                    }
+                    fd[j] = o;
+                }
+                continue;
+            }
             uint32_t p[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j)

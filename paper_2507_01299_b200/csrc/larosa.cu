@@ -18,6 +18,10 @@
 #include "aux.cuh"
 #include "fold_tc.cuh"
 #include "gemv_tc.cuh"
+#include "calib.cuh"
+
+#include <cusolverDn.h>
+#include <mutex>
 
 using namespace larosa;
 
@@ -794,14 +798,14 @@ size_t fold_ws_bytes(int64_t rows, int64_t cols, bool left) {
     return (size_t)2 * d * d * 2 + (left ? (size_t)cols * rows * 2 : 0) + 1024;
 }
 
-template <int BN, bool AS, bool BS>
+template <int BN, bool AS, bool BS, bool F32OUT = false>
 cudaError_t launch_fold_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
-                           uint16_t* out, int M, int N, int K, cudaStream_t st) {
-    auto kern = fold_tc_kernel<BN, AS, BS>;
+                           void* out, int M, int N, int K, cudaStream_t st, float scale = 1.0f, int accumulate = 0) {
+    auto kern = fold_tc_kernel<BN, AS, BS, F32OUT>;
     constexpr int smem = fold_smem_bytes<BN, AS, BS>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3(N / BN, M / kFoldBM), kFoldThreads, smem, st>>>(a0, a1, b0, b1, out, N, K);
+    kern<<<dim3(N / BN, M / kFoldBM), kFoldThreads, smem, st>>>(a0, a1, b0, b1, out, N, K, scale, accumulate);
     return cudaGetLastError();
 }
 
@@ -1494,3 +1498,100 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
 }
 
 
+
+// ============================================================================== N1 calibration
+extern "C" size_t larosa_calib_covariance_workspace_size(int64_t n_tok, int64_t d) {
+    if (n_tok <= 0 || d <= 0) return 0;
+    return (size_t)n_tok * d * 2 + 1024;   // X^T (bf16) for the tensor-core path
+}
+
+extern "C" larosa_status larosa_calib_covariance(const uint16_t* X, int64_t n_tok, int64_t d, float scale,
+                                                 int32_t accumulate, float* C, void* ws, size_t ws_bytes,
+                                                 larosa_stream_t stream) {
+    if (!X || !C) return fail(LAROSA_EINVAL, "calib_covariance: NULL pointer");
+    if (n_tok <= 0 || d <= 0) return fail(LAROSA_EINVAL, "calib_covariance: n_tok, d must be > 0");
+    if (d > 65536 || n_tok > (1 << 30)) return fail(LAROSA_EUNSUPPORTED, "calib_covariance: too large");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const bool tc = d % kFoldBM == 0 && n_tok % kFoldBK == 0 && fold_bn(d) != 0 && aligned16(X) && aligned16(C) &&
+                    env_int("LAROSA_FOLD_SIMT", 0) == 0;
+    if (!tc) {
+        const dim3 g((unsigned)((d + 31) / 32), (unsigned)((d + 31) / 32));
+        covariance_simt_kernel<<<g, 256, 0, st>>>(X, (int)n_tok, (int)d, scale, accumulate, C);
+        return cuda_check(cudaGetLastError(), "covariance kernel");
+    }
+    const size_t need = larosa_calib_covariance_workspace_size(n_tok, d);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "calib_covariance: workspace %zu < %zu", ws_bytes, need);
+    // X^T [d][n] (K = tokens contiguous) serves as both K-major operands: C = Xt . Xt^T
+    uint16_t* xt = static_cast<uint16_t*>(ws);
+    const dim3 tb(32, 8);
+    transpose_bf16_kernel<<<dim3((unsigned)((d + 31) / 32), (unsigned)((n_tok + 31) / 32)), tb, 0, st>>>(
+        X, xt, (int)n_tok, (int)d);
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "transpose"));
+    CUtensorMap a0, b0;
+    const int bn = fold_bn(d);
+    if (!make_kmajor_map(&a0, xt, d, n_tok, kFoldBM) || !make_kmajor_map(&b0, xt, d, n_tok, bn))
+        return fail(LAROSA_ECUDA, "calib_covariance: tensor map");
+    const cudaError_t e =
+        bn == 256 ? launch_fold_tc<256, false, false, true>(a0, a0, b0, b0, C, (int)d, (int)d, (int)n_tok, st, scale,
+                                                             accumulate)
+                  : launch_fold_tc<128, false, false, true>(a0, a0, b0, b0, C, (int)d, (int)d, (int)n_tok, st, scale,
+                                                             accumulate);
+    return cuda_check(e, "covariance tcgen05 launch");
+}
+
+namespace {
+std::mutex g_solver_mu;
+cusolverDnHandle_t solver_handle() {
+    static cusolverDnHandle_t h = nullptr;
+    if (!h && cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) h = nullptr;
+    return h;
+}
+int64_t pca_lwork(int64_t d) {
+    cusolverDnHandle_t h = solver_handle();
+    if (!h) return -1;
+    int lwork = 0;
+    if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d,
+                                    nullptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
+        return -1;
+    return lwork;
+}
+}  // namespace
+
+extern "C" size_t larosa_pca_rotation_workspace_size(int64_t d) {
+    if (d <= 0 || d > 32768) return 0;
+    std::lock_guard<std::mutex> lk(g_solver_mu);
+    const int64_t lw = pca_lwork(d);
+    if (lw < 0) return 0;
+    return (size_t)d * d * 8 + (size_t)d * 8 + 256 + (size_t)lw * 8 + 1024;
+}
+
+extern "C" larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q, float* lam, void* ws,
+                                             size_t ws_bytes, larosa_stream_t stream) {
+    if (!C || !Q || !lam) return fail(LAROSA_EINVAL, "pca_rotation: NULL pointer");
+    if (d <= 0) return fail(LAROSA_EINVAL, "pca_rotation: d must be > 0");
+    if (d > 32768) return fail(LAROSA_EUNSUPPORTED, "pca_rotation: d > 32768");
+    const size_t need = larosa_pca_rotation_workspace_size(d);
+    if (need == 0) return fail(LAROSA_ECUDA, "pca_rotation: cuSOLVER unavailable");
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "pca_rotation: workspace %zu < %zu", ws_bytes, need);
+    std::lock_guard<std::mutex> lk(g_solver_mu);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    double* A = static_cast<double*>(ws);
+    double* w = A + (size_t)d * d;
+    int* info = reinterpret_cast<int*>(w + d);
+    double* work = reinterpret_cast<double*>(reinterpret_cast<char*>(info) + 256);
+    const int64_t lw = pca_lwork(d);
+    f32_to_f64_sym_kernel<<<1024, 256, 0, st>>>(C, A, (int)d);
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "pca: symmetrise"));
+    cusolverDnHandle_t h = solver_handle();
+    if (cusolverDnSetStream(h, st) != CUSOLVER_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "pca: cusolverDnSetStream");
+    if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, A, (int)d, w, work, (int)lw,
+                         info) != CUSOLVER_STATUS_SUCCESS)
+        return fail(LAROSA_ECUDA, "pca: cusolverDnDsyevd");
+    pca_order_sign_kernel<<<(unsigned)d, 256, 0, st>>>(A, w, (int)d, Q, lam);
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "pca: order/sign"));
+    int hinfo = 0;
+    LAROSA_TRY(cuda_check(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st), "pca: info"));
+    LAROSA_TRY(cuda_check(cudaStreamSynchronize(st), "pca: synchronize"));
+    if (hinfo != 0) return fail(LAROSA_ECUDA, "pca: eigensolver did not converge (info %d)", hinfo);
+    return LAROSA_OK;
+}

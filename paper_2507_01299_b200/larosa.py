@@ -96,6 +96,12 @@ def lib() -> ctypes.CDLL:
     L.larosa_topk_sparse_gemv_dense2.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp,
                                                  _c_i64, _vp, _c_i32, _vp, ctypes.c_size_t, _vp]
     L.larosa_embed.argtypes = [_vp, _c_i64, _c_i64, _vp, _c_i32, _vp, _vp]
+    L.larosa_calib_covariance_workspace_size.restype = ctypes.c_size_t
+    L.larosa_calib_covariance_workspace_size.argtypes = [_c_i64, _c_i64]
+    L.larosa_calib_covariance.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _c_i32, _vp, _vp, ctypes.c_size_t, _vp]
+    L.larosa_pca_rotation_workspace_size.restype = ctypes.c_size_t
+    L.larosa_pca_rotation_workspace_size.argtypes = [_c_i64]
+    L.larosa_pca_rotation.argtypes = [_vp, _c_i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]
     L.larosa_lm_head_workspace_size.restype = ctypes.c_size_t
     L.larosa_lm_head_workspace_size.argtypes = [_c_i32, _c_i64, _c_i64]
     L.larosa_lm_head.argtypes = [_vp, _c_i32, _c_i64, _vp, _c_i64, ctypes.c_float, _vp, _vp, _vp, ctypes.c_size_t, _vp]
@@ -287,6 +293,35 @@ def topk_sparse_gemv_dense2(x: torch.Tensor, k: int, W: torch.Tensor, x2: torch.
     _check(L.larosa_topk_sparse_gemv_dense2(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), ld, ld, _ptr(x2), _ptr(W2),
                                             d2, _ptr(y), int(prepared), _ptr(ws), ws.numel(), _stream(stream)))
     return y
+
+
+def calib_covariance(X: torch.Tensor, scale: float = 1.0, out: Optional[torch.Tensor] = None,
+                     accumulate: bool = False, stream=None) -> torch.Tensor:
+    """C = scale * X^T X (+ C): X bf16 bits (int16) [n_tok, d] of calibration activations (eq. 1,
+    P:380-383; pass scale = 1/M and accumulate over the M sequences)."""
+    n, d = X.shape
+    C = out if out is not None else torch.zeros((d, d), dtype=torch.float32, device=X.device)
+    L = lib()
+    nb = L.larosa_calib_covariance_workspace_size(n, d)
+    ws = _ws(("calib_cov", n, d), nb, X.device)
+    _check(L.larosa_calib_covariance(_ptr(X), n, d, float(scale), int(accumulate), _ptr(C), _ptr(ws), ws.numel(),
+                                     _stream(stream)))
+    return C
+
+
+def pca_rotation(C: torch.Tensor, stream=None):
+    """(Q, lam): eigenvectors of C as columns, eigenvalues descending, largest-|entry| component
+    positive.  Synchronises the stream."""
+    d = C.shape[0]
+    L = lib()
+    nb = L.larosa_pca_rotation_workspace_size(d)
+    if nb == 0:
+        raise LarosaError(4, "pca_rotation: cuSOLVER unavailable")
+    ws = _ws(("pca", d), nb, C.device)
+    Q = torch.empty((d, d), dtype=torch.float32, device=C.device)
+    lam = torch.empty((d,), dtype=torch.float32, device=C.device)
+    _check(L.larosa_pca_rotation(_ptr(C.contiguous()), d, _ptr(Q), _ptr(lam), _ptr(ws), ws.numel(), _stream(stream)))
+    return Q, lam
 
 
 def embed(E: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

@@ -1,0 +1,76 @@
+"""GPU parity of the calibration path (§4.2):
+larosa_calib_covariance (eq. 1, tcgen05 and CUDA-core paths) against the oracle's covariance on
+the same bf16 activations, and larosa_pca_rotation against the oracle's Jacobi build_rotation
+(order, sign convention Z7) where the eigenvalues are distinct, plus the pipeline
+activations -> C -> Q -> fold -> computational invariance."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from paper_2507_01299_b200 import larosa as LZ
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def w64(bits):
+    return O.bf16_to_f64(bits.detach().cpu().numpy().view(np.uint16))
+
+
+def toy_bits(d, n_seq, n_tok, seed):
+    """The toy calibration recipe (distinct eigenvalues), rounded to bf16 like real activations."""
+    seqs = synth.toy_calibration(d=d, n_seq=n_seq, n_tok=n_tok, seed=seed)
+    return [synth.bf16_bits(s.float()) for s in seqs]
+
+
+@pytest.mark.parametrize("d,n_seq,n_tok", [(64, 16, 16), (256, 8, 64), (512, 4, 128), (200, 3, 40)])
+def test_covariance_vs_oracle(d, n_seq, n_tok):
+    """C = (1/M) sum_i X_i^T X_i accumulated sequence by sequence (eq. 1; Z2-Z4)."""
+    seqs = toy_bits(d, n_seq, n_tok, seed=3 + d)
+    C = torch.zeros((d, d), dtype=torch.float32, device=DEV)
+    for i, x in enumerate(seqs):
+        LZ.calib_covariance(x.to(DEV).contiguous(), scale=1.0 / n_seq, out=C, accumulate=i > 0)
+    torch.cuda.synchronize()
+    ref = O.covariance([w64(x) for x in seqs])
+    got = C.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(got - ref)) <= 2e-6 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_pca_rotation_vs_oracle_jacobi(d):
+    """Distinct eigenvalues: Q is unique up to sign, fixed by Z7 -> element-wise parity with the
+    oracle's Jacobi solver on the same (fp32) covariance; eigenvalues descending."""
+    seqs = toy_bits(d, 16, 32, seed=5)
+    C = O.covariance([w64(x) for x in seqs])
+    Cf = torch.from_numpy(C.astype(np.float32))
+    q_ref, lam_ref = O.build_rotation(Cf.double().numpy())
+    Q, lam = LZ.pca_rotation(Cf.to(DEV))
+    Q, lam = Q.cpu().double().numpy(), lam.cpu().double().numpy()
+    assert np.all(np.diff(lam) <= 0)
+    assert np.max(np.abs(lam - lam_ref)) <= 1e-6 * lam_ref[0]
+    assert np.max(np.abs(Q - q_ref)) <= 1e-5
+    assert np.max(np.abs(Q.T @ Q - np.eye(d))) <= 1e-6
+
+
+def test_calibration_pipeline_invariance():
+    """activations -> covariance (tcgen05) -> Q (PCA) -> fold W' = Q^T W (tcgen05): x Q . W' equals
+    x . W up to the fold's bf16 rounding (computational invariance), and the
+    rotated activations have descending second moments (the PCA's defining property)."""
+    d, cols = 256, 512
+    seqs = toy_bits(d, 8, 128, seed=9)
+    C = torch.zeros((d, d), dtype=torch.float32, device=DEV)
+    for i, x in enumerate(seqs):
+        LZ.calib_covariance(x.to(DEV).contiguous(), scale=1.0 / len(seqs), out=C, accumulate=i > 0)
+    Q, lam = LZ.pca_rotation(C)
+    W = synth.gaussian_bf16((d, cols), 4, d ** -0.5, DEV)
+    Wf = LZ.fold_rotation(Q, W, LZ.LAROSA_LEFT_QT)
+    x = np.concatenate([w64(s) for s in seqs])
+    q = Q.cpu().double().numpy()
+    z = x @ q
+    m2 = np.mean(z * z, axis=0)
+    assert np.all(np.diff(m2) <= 1e-6 * m2[0])
+    y_ref = x @ w64(W)
+    y = z @ w64(Wf)
+    assert np.linalg.norm(y - y_ref) <= 3e-3 * np.linalg.norm(y_ref)
