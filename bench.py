@@ -346,6 +346,32 @@ def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
             "pca_rotation_ms": pca_ms}
 
 
+def latency_consistency_extra(layers, kv, pos, ws_buf, shape, device, steps=600):
+    """SURVEY §8(f) N4 / P:369-370: with exact per-token Top-K every token moves the
+    same bytes, so per-token latency should be as steady as the dense step's.  Per-step device
+    times (CUDA events around each chained step, fresh Top-K sets every step) at p = 0.5 and
+    p = 0: percentiles and the coefficient of variation."""
+    from paper_2507_01299_b200 import model as M
+    out = {}
+    for p in (0.5, 0.0):
+        plan = M.site_plan(shape, p)
+        resid = synth.residual_activation(1, shape.d, seed=91).to(device)
+        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
+        run_steps(graphs, 50, 0)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        torch.cuda.synchronize()
+        evs[0].record()
+        for i in range(steps):
+            graphs[i % len(graphs)].replay()
+            evs[i + 1].record()
+        torch.cuda.synchronize()
+        t = np.array([evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(steps)])
+        out[str(p)] = {"p10_us": float(np.percentile(t, 10)), "p50_us": float(np.percentile(t, 50)),
+                       "p90_us": float(np.percentile(t, 90)), "p99_us": float(np.percentile(t, 99)),
+                       "cv": float(np.std(t) / np.mean(t))}
+    return out
+
+
 def fold_extra(device):
     """larosa_fold_rotation on LLaMA2-7B layer shapes: tcgen05 TFLOP/s (2 M N K of the fold)."""
     from paper_2507_01299_b200 import larosa as LZ
@@ -648,6 +674,7 @@ def main():
         extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device, merged=merged),
                   "fold_tcgen05": fold_extra(device),
                   "calibration_n1": calibration_extra(device),
+                  "latency_consistency": latency_consistency_extra(layers, kv, pos, ws_buf, shape, device),
                   "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
 
     cpu = None

