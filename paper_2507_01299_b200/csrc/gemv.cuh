@@ -165,6 +165,7 @@ struct GemvArgs {
     // slice form one thread-block cluster (cluster != 0); rank 0 sums the CTAs' fp32 column
     // partials in rank order and finalises the slice itself (no global accumulators, no ticket)
     int cluster;
+    int late_trigger;                  // tuning: 1 = release dependents after the main loop, not at entry
 };
 
 __host__ __device__ constexpr size_t gemv_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -741,7 +742,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 
     tl_stamp(a.tl, 0);
     pdl_wait();       // the row source comes from the previous kernel
-    pdl_trigger();
+    if (!a.late_trigger) pdl_trigger();
     tl_stamp(a.tl, 1);
     if (a.zero_hist) {   // a histogram whose consumer has completed (kernel-boundary ordered)
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -884,6 +885,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();   // every warp is done with its ring (the partials alias it)
+    if (a.late_trigger) pdl_trigger();
     tl_stamp(a.tl, 3);
 
     // fixed-order sum of the 8 warps' partials, then one fixed-point red per column

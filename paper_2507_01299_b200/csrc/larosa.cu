@@ -231,6 +231,8 @@ larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     GemvArgs aa = a;
     static const int sel_dbg = env_int("LAROSA_SEL_DBG", 0);   // profiling only
     aa.sel_dbg = sel_dbg;
+    static const int late = env_int("LAROSA_PDL_LATE", 0);    // tuning
+    aa.late_trigger = late;
     aa.n_splits = p.n_splits;
     aa.n_splits2 = p.n_splits2;
     aa.list_cap = p.list_cap;
