@@ -399,7 +399,7 @@ def dense_block(r, w, cfg, k_cache, v_cache, pos: int, kv_bf16: bool = False):
 
 
 def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf16: bool = False,
-                 adapter_in_down: bool = False):
+                 adapter_in_down: bool = False, adapter_mid=None):
     """The LaRoSA layer on folded weights, step by step as Fig. 2 and
     eqs. before/after_merge (P:402-411):
 
@@ -418,7 +418,13 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
     wd = Wd Q_{l+1} = (Wd Q_l) A_l (the "4-gather form"; reading R4).
     By linearity of the adapter, (r_mid + y_down Q_l-basis) A_l = r_mid A_l + y_down',
     so r_next = r_mid A_l + h4[S4] wd; the down site's selection S4 is unchanged (it is taken
-    on h4, before the projection)."""
+    on h4, before the projection).
+
+    ``adapter_mid``: the block-wise rotation Q_B of the paper's ablation (Table 6, P:204-215;
+    SURVEY §8(f) N4): the attention block runs in Q_a's basis and the MLP block in Q_m's, with
+    A_mid = Q_a^T Q_m applied to the residual between them, folded beside O like the adapter
+    beside down: wo = Wo Q_m, r_mid = r A_mid + h2[S2] wo; gate|up are folded with Q_m (input
+    side) and down / the closing adapter carry the residual from Q_m's basis onward."""
     hq, hkv, hd, eps, theta = cfg["hq"], cfg["hkv"], cfg["hd"], cfg["eps"], cfg["theta"]
     k1, k2, k3, k4 = ks
     out = {}
@@ -432,7 +438,10 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
     v_cache[:, pos] = _kv_store(v, kv_bf16)
     h2 = decode_attention(q, k_cache, v_cache, pos + 1)
     s2 = topk(h2, k2)
-    r = r + sparse_gemv(wf["wo"], s2, h2[s2])
+    if adapter_mid is not None:
+        r = rotate(r, adapter_mid) + sparse_gemv(wf["wo"], s2, h2[s2])
+    else:
+        r = r + sparse_gemv(wf["wo"], s2, h2[s2])
     r_mid = r.copy()
     s3 = topk(r, k3)
     v3 = r[s3] * rms_scale(r, eps)

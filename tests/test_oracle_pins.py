@@ -443,6 +443,38 @@ def test_block_adapter_in_down_equals_adapter_form(p):
         O.larosa_block(r @ q0, _fold_layer(w, q0, q1), cfg, ks, kc.copy(), vc.copy(), ctx - 1, adapter_in_down=True)
 
 
+@pytest.mark.parametrize("merged", [False, True])
+def test_block_wise_rotation_qb_p0_equals_dense(merged):
+    """Q_B (Table 6): the attention block in Q_a's basis, the MLP block in Q_m's,
+    A_mid = Q_a^T Q_m folded beside O (wo = Wo Q_m, r_mid = r A_mid + y_o) and the closing
+    adapter Q_m^T Q_a' (or wd = Wd Q_a' beside down).  At k = D two chained layers reproduce the
+    dense layers rotated into the next layer's attention basis (computational invariance,
+    P:1444-1448), to 1e-10 in fp64."""
+    d, ctx = 64, 6
+    layers = [_toy_layer(800 + l, bias=True) for l in range(2)]
+    qa = [synth.haar_orthogonal(d, 810 + l).numpy() for l in range(3)]
+    qm = [synth.haar_orthogonal(d, 820 + l).numpy() for l in range(2)]
+    cfg = layers[0][1]
+    rng = np.random.default_rng(8)
+    caches_d = [[rng.standard_normal((2, ctx, 16)) for _ in range(2)] for _ in range(2)]
+    caches_r = [[c.copy() for c in cc] for cc in caches_d]
+    r = rng.standard_normal(d)
+    rr = r @ qa[0]
+    full = (d, d, d, 128)
+    for l in range(2):
+        w = layers[l][0]
+        r, _ = O.dense_block(r, w, cfg, caches_d[l][0], caches_d[l][1], ctx - 1)
+        wqkv = np.concatenate([w["wq"], w["wk"], w["wv"]], axis=1)
+        wf = {"wqkv": O.fold_left_qt(qa[l], wqkv, w["gamma1"]), "wo": O.fold_right_q(w["wo"], qm[l]),
+              "wg": O.fold_left_qt(qm[l], w["wg"], w["gamma2"]), "wu": O.fold_left_qt(qm[l], w["wu"], w["gamma2"]),
+              "wd": O.fold_right_q(w["wd"], qa[l + 1] if merged else qm[l]),
+              "bqkv": np.concatenate([w["bq"], w["bk"], w["bv"]])}
+        rr, _ = O.larosa_block(rr, wf, cfg, full, caches_r[l][0], caches_r[l][1], ctx - 1,
+                               adapter=O.residual_adapter(qm[l], qa[l + 1]), adapter_in_down=merged,
+                               adapter_mid=O.residual_adapter(qa[l], qm[l]))
+        assert np.linalg.norm(rr - r @ qa[l + 1]) <= 1e-10 * np.linalg.norm(r)
+
+
 def test_block_exact_sparsity_and_monotone_error():
     """Per-site kept counts are exactly k for every token and the mean relative
     output error is non-decreasing in p over 5 seeds."""
