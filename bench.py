@@ -168,13 +168,21 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------ GPU leg
-def build_stack(shape, device, n_copies, seed=0, merged=True):
+def build_stack(shape, device, n_copies, seed=0, merged=True, variant="QL"):
+    """variant: QL (one rotation per layer, the paper's method), QB (block-wise: attention and MLP
+    blocks in their own bases, A_mid beside O), QM (one rotation for the whole model: no adapter)."""
     from paper_2507_01299_b200 import model as M
     qs = [synth.haar_orthogonal(shape.d, seed=100 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
     layers = []
     for i in range(n_copies):
         orig = M.synth_original_layer(shape, seed + i + 1, device=device)
-        layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged))
+        if variant == "QM":
+            layers.append(M.fold_layer(orig, shape, qs[0], None))
+        elif variant == "QB":
+            qm = synth.haar_orthogonal(shape.d, seed=300 + i, device=device, dtype=torch.float32)
+            layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged, q_mlp=qm))
+        else:
+            layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged))
         del orig
     torch.cuda.synchronize()
     return layers
@@ -344,6 +352,35 @@ def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
     pca_ms = (time.perf_counter() - t0) * 1e3
     return {"d": d, "tokens": n_seq * n_tok, "covariance_ms": ms, "covariance_tflops": 2.0 * n_seq * n_tok * d * d / ms / 1e9,
             "pca_rotation_ms": pca_ms}
+
+
+def rotation_variants_extra(device, shape, steps=1000, copies=4, p=0.5):
+    """Table 6's rotation variants on the LLaMA2-7B block (batch 1, ctx 256, p = 0.5): Q_L (one
+    rotation per layer), Q_B (attention / MLP blocks rotated separately: one more D x D adapter,
+    riding in the O launch) and Q_M (one rotation for the model: no adapter)."""
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    plan = M.site_plan(shape, p)
+    out = {}
+    for v in ("QL", "QB", "QM"):
+        layers = build_stack(shape, device, copies, seed=700, merged=True, variant=v)
+        kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
+               synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(copies)]
+        pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
+        ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
+        resid = synth.residual_activation(1, shape.d, seed=77).to(device)
+        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
+        run_steps(graphs, 50, 0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_steps(graphs, steps, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        out[v] = {"block_us": e0.elapsed_time(e1) * 1e3 / steps}
+        del layers, kv, graphs, ws_buf
+        torch.cuda.empty_cache()
+    return out
 
 
 def latency_consistency_extra(layers, kv, pos, ws_buf, shape, device, steps=600):
@@ -675,6 +712,7 @@ def main():
                   "fold_tcgen05": fold_extra(device),
                   "calibration_n1": calibration_extra(device),
                   "latency_consistency": latency_consistency_extra(layers, kv, pos, ws_buf, shape, device),
+                  "rotation_variants": rotation_variants_extra(device, shape),
                   "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
 
     cpu = None

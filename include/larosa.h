@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 2
+#define LAROSA_ABI_VERSION 3
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -242,6 +242,13 @@ typedef struct {
      * CTAs need no selection rule and prefetch before the dependency wait); the r_out tap is
      * not written.  0: the literal form (down folded with Q_l, separate adapter GEMV). */
     int32_t adapter_in_down;
+    /* Block-wise rotation Q_B (Table 6): [d][d] = Q_a^T Q_m or NULL.  When set, the
+     * attention block runs in Q_a's basis and the MLP block in Q_m's: w_o = Wo Q_m (output side),
+     * w_gu folded with Q_m (input side), and r_mid = r A_mid + Top-K(h2) w_o (the dense r rows of
+     * A_mid ride in the O launch like the adapter beside down); adapter / w_down then close from
+     * Q_m's basis (adapter = Q_m^T Q_a', or w_down = Wd Q_a' with adapter_in_down).  NULL: Q_L
+     * (one rotation per layer).  Not supported by larosa_sparse_layer_shard_phase. */
+    const uint16_t* adapter_mid;
 } larosa_layer_weights;
 
 typedef struct {

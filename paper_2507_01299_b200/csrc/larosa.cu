@@ -1049,7 +1049,8 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
     if (p->k_h1 < 0 || p->k_h1 > w->d || p->k_h2 < 0 || p->k_h2 > nq || p->k_h3 < 0 || p->k_h3 > w->d || p->k_h4 < 0 ||
         p->k_h4 > w->inter || p->k_next_h1 > w->d)
         return fail(LAROSA_EINVAL, "sparse_layer: a k is outside [0, D_in of its site]");
-    const void* ptrs[] = {w->w_qkv, w->w_o, w->w_gu, w->w_down, w->adapter, w->b_qkv, s->resid, s->k_cache, s->v_cache};
+    const void* ptrs[] = {w->w_qkv, w->w_o, w->w_gu, w->w_down, w->adapter, w->b_qkv, s->resid, s->k_cache, s->v_cache,
+                          w->adapter_mid};
     for (const void* q : ptrs)
         if (q && !aligned16(q)) return fail(LAROSA_EINVAL, "sparse_layer: pointers must be 16-byte aligned");
     return LAROSA_OK;
@@ -1237,7 +1238,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     LAROSA_TRY(tap_topk(W.h2, L.nq, plan->k_h2, -1.0f, T.idx_h2, T.vals_h2));
     if (on(4)) {
         GemvArgs a = site_gemv(1, W.h2, L.nq, plan->k_h2, -1.0f, w->w_o, L.d, W.acc_o);
-        epi(a, 0, EPI_RESID, s->resid, W.rmid, 2);
+        const bool qb = w->adapter_mid != nullptr;   // r_mid = r A_mid + y_o (block-wise rotation)
+        epi(a, 0, EPI_RESID, qb ? nullptr : s->resid, W.rmid, 2);
         if (fused) {   // attention (complete by now) left the QKV accumulators to be re-zeroed here
             a.zero_acc = W.acc_qkv;
             a.zero_acc_words = (int)L.nqkv;
@@ -1245,7 +1247,31 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.tl = tl_slot(2);
         a.zero_hist = fused ? W.sel[0].hist : nullptr;   // h1's consumer (QKV) is done
         a.zero_words = kSelHistTotal;
-        LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.nq, plan->k_h2), fused ? 1 : bp, st));
+        if (qb && fused) {   // the dense r rows of A_mid as companion CTAs of the O launch
+            a.W2 = w->adapter_mid;
+            a.x2 = s->resid;
+            a.d2 = (int)L.d;
+            LAROSA_TRY(launch_gemv(a, plan_gemv_comp(L.d, plan->k_h2, L.nq, L.d), 1, st));
+        } else if (qb) {     // batch > 1: the O GEMV leaves its sums, the dense A_mid GEMV finalises
+            const int epi_mode = a.epi;
+            a.epi = EPI_NONE;
+            LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.nq, plan->k_h2), bp, st));
+            GemvArgs b = gemv_args_base();
+            b.W = w->adapter_mid;
+            b.ld = L.d;
+            b.d_out = (int)L.d;
+            b.mode = GEMV_DENSE;
+            b.x = s->resid;
+            b.ldx = L.d;
+            b.d_in = (int)L.d;
+            b.batch = B;
+            b.acc = W.acc_o;
+            b.acc_ld = L.d;
+            epi(b, 0, epi_mode, nullptr, W.rmid, 2);
+            LAROSA_TRY(launch_gemv(b, plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d), bp, st));
+        } else {
+            LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.nq, plan->k_h2), fused ? 1 : bp, st));
+        }
     }
     LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
     // ---- h3 (RMS) -> gate|up; epilogue h4 = SiLU(g) u ----------------------------------------------
@@ -1416,6 +1442,7 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     ShardWs W;
     carve_shard(c, S, max_ctx > 0 ? max_ctx : 1, &W);
     const int r = sh->rank;
+    if (w->adapter_mid) return fail(LAROSA_EUNSUPPORTED, "shard_phase: block-wise rotation (adapter_mid) not supported");
     const bool merged = w->adapter && w->adapter_in_down;   // 4 phases: the adapter rides with phase 3
     if (merged && phase == 4) return fail(LAROSA_EINVAL, "shard_phase: no phase 4 when adapter_in_down");
     // phase -> (site input width, k, RMS eps, weights, local output width)

@@ -37,7 +37,7 @@ class LayerWeightsC(ctypes.Structure):
     _fields_ = [("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("w_gu", _vp), ("w_down", _vp),
                 ("adapter", _vp), ("d", _c_i64), ("inter", _c_i64), ("n_q_heads", _c_i64),
                 ("n_kv_heads", _c_i64), ("head_dim", _c_i64), ("rope_theta", ctypes.c_float),
-                ("rms_eps", ctypes.c_float), ("adapter_in_down", _c_i32)]
+                ("rms_eps", ctypes.c_float), ("adapter_in_down", _c_i32), ("adapter_mid", _vp)]
 
 
 class LayerPlanC(ctypes.Structure):
@@ -123,7 +123,7 @@ def lib() -> ctypes.CDLL:
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 2:
+    if L.larosa_abi_version() != 3:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -367,11 +367,13 @@ class LayerWeights:
     b_qkv: Optional[torch.Tensor] = None
     adapter: Optional[torch.Tensor] = None
     adapter_in_down: bool = False   # w_down = Wd Q_{l+1}: r_next = r_mid A_l + y_down (larosa.h)
+    adapter_mid: Optional[torch.Tensor] = None   # Q_B: A_mid = Q_a^T Q_m beside O (larosa.h)
 
     def c(self) -> LayerWeightsC:
         return LayerWeightsC(_ptr(self.w_qkv), _ptr(self.b_qkv), _ptr(self.w_o), _ptr(self.w_gu), _ptr(self.w_down),
                              _ptr(self.adapter), self.d, self.inter, self.n_q_heads, self.n_kv_heads, self.head_dim,
-                             float(self.rope_theta), float(self.rms_eps), int(self.adapter_in_down))
+                             float(self.rope_theta), float(self.rms_eps), int(self.adapter_in_down),
+                             _ptr(self.adapter_mid))
 
 
 @dataclass

@@ -46,32 +46,40 @@ def synth_original_layer(shape: synth.ModelShape, seed: int, device="cpu") -> Or
 
 
 def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
-               q_next: Optional[torch.Tensor], adapter_in_down: bool = False) -> LZ.LayerWeights:
+               q_next: Optional[torch.Tensor], adapter_in_down: bool = False,
+               q_mlp: Optional[torch.Tensor] = None) -> LZ.LayerWeights:
     """Offline transform of one layer (eqs. before/after_merge P:402-410, §3.2):
     W_qkv' = Q_l^T diag(g1) W_qkv;  W_o' = W_o Q_l;  W_gate|up' = Q_l^T diag(g2) [Wg | Wu]
     (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1}.   q_l, q_next: fp32 on device.
     adapter_in_down (needs q_next): W_down' = W_down Q_{l+1} = (W_down Q_l) A_l, and the
-    layer computes r_next = r_mid A_l + y_down (larosa.h)."""
+    layer computes r_next = r_mid A_l + y_down (larosa.h).
+    q_mlp (block-wise rotation Q_B, Table 6): the MLP block runs in q_mlp's basis: W_o' = W_o Q_m,
+    W_gate|up' = Q_m^T diag(g2) [Wg | Wu], A_mid = Q_l^T Q_m, and down / the adapter close from
+    Q_m (A = Q_m^T Q_{l+1}, or W_down' = W_down Q_{l+1} beside down)."""
     dev = orig.wqkv.device
     L, R = LZ.LAROSA_LEFT_QT, LZ.LAROSA_RIGHT_Q
     g1 = orig.gamma1.to(dev, torch.float32).contiguous()
     g2 = orig.gamma2.to(dev, torch.float32).contiguous()
     w_qkv = LZ.fold_rotation(q_l, orig.wqkv, L, gamma=g1)
-    w_o = LZ.fold_rotation(q_l, orig.wo, R)
-    wg = LZ.fold_rotation(q_l, orig.wg, L, gamma=g2)
-    wu = LZ.fold_rotation(q_l, orig.wu, L, gamma=g2)
+    q_m = q_mlp if q_mlp is not None else q_l
+    w_o = LZ.fold_rotation(q_m, orig.wo, R)
+    wg = LZ.fold_rotation(q_m, orig.wg, L, gamma=g2)
+    wu = LZ.fold_rotation(q_m, orig.wu, L, gamma=g2)
     w_gu = LZ.pack_gate_up(wg, wu)
     del wg, wu
     merged = adapter_in_down and q_next is not None
-    w_down = LZ.fold_rotation(q_next if merged else q_l, orig.wd, R)
+    w_down = LZ.fold_rotation(q_next if merged else q_m, orig.wd, R)
     adapter = None
     if q_next is not None:
-        adapter = LZ.fold_rotation(q_l, synth.bf16_bits(q_next).contiguous(), L)
+        adapter = LZ.fold_rotation(q_m, synth.bf16_bits(q_next).contiguous(), L)
+    adapter_mid = None
+    if q_mlp is not None:
+        adapter_mid = LZ.fold_rotation(q_l, synth.bf16_bits(q_mlp).contiguous(), L)
     return LZ.LayerWeights(w_qkv=w_qkv, w_o=w_o, w_gu=w_gu, w_down=w_down, d=shape.d, inter=shape.inter,
                            n_q_heads=shape.hq, n_kv_heads=shape.hkv, head_dim=shape.hd,
                            rope_theta=shape.rope_theta, rms_eps=shape.rms_eps,
                            b_qkv=orig.bqkv.contiguous() if orig.bqkv is not None else None, adapter=adapter,
-                           adapter_in_down=merged)
+                           adapter_in_down=merged, adapter_mid=adapter_mid)
 
 
 def site_plan(shape: synth.ModelShape, p: float, alpha_mode: str = "uniform") -> tuple:

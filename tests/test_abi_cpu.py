@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 14, names
     for n in names:
         assert hasattr(L, n), f"missing export {n}"
-    assert L.larosa_abi_version() == 2
+    assert L.larosa_abi_version() == 3
 
 
 def test_status_strings():

@@ -49,12 +49,14 @@ def unpack_gu(wgu, inter):
     return blk[:, :, 0, :].reshape(d, inter), blk[:, :, 1, :].reshape(d, inter)
 
 
-def build(shape, seed, batch, ctx, max_ctx, p, with_adapter=True, merged=False):
+def build(shape, seed, batch, ctx, max_ctx, p, with_adapter=True, merged=False, qb=False):
     orig = M.synth_original_layer(shape, seed)
     q_l = synth.haar_orthogonal(shape.d, seed=seed + 50).float()
     q_n = synth.haar_orthogonal(shape.d, seed=seed + 51).float() if with_adapter else None
+    q_m = synth.haar_orthogonal(shape.d, seed=seed + 52).float().to(DEV) if qb else None
     origd = M.OriginalLayer(**{k: (v.to(DEV) if v is not None else None) for k, v in orig.__dict__.items()})
-    lw = M.fold_layer(origd, shape, q_l.to(DEV), q_n.to(DEV) if q_n is not None else None, adapter_in_down=merged)
+    lw = M.fold_layer(origd, shape, q_l.to(DEV), q_n.to(DEV) if q_n is not None else None, adapter_in_down=merged,
+                      q_mlp=q_m)
     plan = M.site_plan(shape, p)
     resid = synth.residual_activation(batch, shape.d, seed=seed + 60)
     kc = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), seed + 61, 1.0)
@@ -83,10 +85,16 @@ def run_layer(lw, plan, resid, kc, vc, pos):
     # BASELINE configs[3] shapes: Mistral-7B (GQA 32/8, theta 1e6) and Qwen2.5-7B (d 3584, GQA 28/4,
     # QKV bias, eps 1e-6), batch 1 at 60% / 25% and batch 3
     (synth.MODELS["mistral-7b"], 1, 100, 0.6, True), (synth.MODELS["qwen2.5-7b"], 1, 77, 0.25, True),
-    (synth.MODELS["qwen2.5-7b"], 3, 50, 0.5, False)])
+    (synth.MODELS["qwen2.5-7b"], 3, 50, 0.5, False),
+    # block-wise rotation Q_B (adapter_mid beside O): batch 1 companions, batch 3 CUDA-core,
+    # batch 16 tcgen05, the 7B block
+    (SMALL, 1, 7, 0.5, "qb"), (SMALL_MHA, 3, 40, 0.4, "qb"), (SMALL, 16, 30, 0.5, "qb_merged"),
+    (synth.MODELS["llama2-7b"], 1, 256, 0.5, "qb_merged")])
 def test_layer_p6_sitewise(shape, batch, ctx, p, merged):
     max_ctx = max(ctx, 64)
-    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p, merged=merged)
+    qb = merged in ("qb", "qb_merged")
+    merged = merged is True or merged == "qb_merged"
+    orig, q_l, q_n, lw, plan, resid, kc0, vc0, pos = build(shape, 3, batch, ctx, max_ctx, p, merged=merged, qb=qb)
     st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
     k1, k2, k3, k4 = plan
     hq, hkv, hd, d = shape.hq, shape.hkv, shape.hd, shape.d
@@ -126,7 +134,7 @@ def test_layer_p6_sitewise(shape, batch, ctx, p, merged):
         i2 = tp["idx_h2"][b].cpu().numpy()
         assert np.array_equal(i2, O.topk(h2g, k2))
         assert np.array_equal(f64(tp["vals_h2"][b]), h2g[i2])
-        rmid = r + O.sparse_gemv(Wo, i2, h2g[i2])
+        rmid = (O.rotate(r, w64(lw.adapter_mid)) if qb else r) + O.sparse_gemv(Wo, i2, h2g[i2])
         assert rel_max(f64(tp["r_mid"][b]), rmid) <= 1e-5
         # h3 -> gate|up
         rm = f64(tp["r_mid"][b])
