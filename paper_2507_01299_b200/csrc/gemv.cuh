@@ -159,7 +159,7 @@ struct GemvArgs {
     int d2;
     int n_splits2;
     unsigned long long* tl;            // debug timeline slot (5 x u64) or null
-    int sel_dbg;                       // profiling: bitmask of select phases to skip (0 = none)
+    int sel_dbg;                       // profiling flags (unused by the kernels at present)
     int tc_dbg;                        // profiling (tcgen05 GEMV): 1 skip MMAs, 2 skip values, 4 skip A copies
     // batch-1 split-K reduction through distributed shared memory: the gridDim.y CTAs of a
     // slice form one thread-block cluster (cluster != 0); rank 0 sums the CTAs' fp32 column
@@ -590,8 +590,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     };
     const bool all = flags & kRuleAll, none = flags & kRuleNone;
     int total;
-#pragma unroll 1
-    for (int rep = 0; rep < ((a.sel_dbg & 1) ? 2 : 1); ++rep) {   // profiling: run the mask + list twice
+    {
         for (int j = wid; j < nj; j += NW) {
             const int i = 32 * (split + n_splits * j) + lane;
             bool kp = false;
@@ -603,7 +602,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
             }
         }
         __syncthreads();
-        tl_stamp(a.tl, rep ? 14 : 7);
+        tl_stamp(a.tl, 7);
         const int cj = tid < nj ? wcnt[tid] : 0;
         const int before = block_excl_scan<NT>(cj, scan, &total);
         __syncthreads();
@@ -618,7 +617,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
             }
         }
         __syncthreads();   // list complete; the staged region (aliased by the ring) is dead
-        tl_stamp(a.tl, rep ? 15 : 11);
+        tl_stamp(a.tl, 11);
     }
     return total;
 }
