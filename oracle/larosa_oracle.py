@@ -29,7 +29,8 @@ __all__ = [
     "topk_mask", "sparse_gemv", "dense_gemv", "compute_k", "solve_alpha", "site_ks",
     "std_normal_pdf", "std_normal_cdf", "std_normal_inv_cdf", "theory_relative_error",
     "rope", "decode_attention", "silu", "rmsnorm", "dense_block", "larosa_block",
-    "actual_sparsity", "embed", "lm_head", "greedy", "larosa_decode_step",
+    "actual_sparsity", "embed", "lm_head", "greedy", "larosa_decode_step", "quantize_w4", "dequantize_w4",
+    "W4_GROUP",
 ]
 
 
@@ -459,6 +460,38 @@ def larosa_block(r, wf, cfg, ks, k_cache, v_cache, pos: int, adapter=None, kv_bf
     if adapter is not None:
         r = rotate(r, adapter)
     return r, out
+
+
+# ----------------------------------------------------------------------------------
+# W4A16 weights (quantisation compatibility P:306-344).  The format is this
+# implementation's (the paper fixes none): symmetric int4 per (input row, group of 128 outputs).
+# The integer decisions are taken in fp32 as the header states (the kernel's precision).
+# ----------------------------------------------------------------------------------
+W4_GROUP = 128
+
+
+def quantize_w4(wc_bf16_bits):
+    """(codes uint8 [d_in][d_out] in [0, 15], scale fp16 bits [d_in][d_out/128]) of a bf16
+    weight: scale = RNE_fp16(max|w| / 7) (fp32 divide), q = clamp(rint(w / scale) + 8, 0, 15)
+    (fp32 divide, rint = round half to even); scale 0 -> q = 8."""
+    w = bf16_to_f64(wc_bf16_bits).astype(np.float32)
+    d_in, d_out = w.shape
+    if d_out % W4_GROUP:
+        raise ValueError("quantize_w4: d_out % 128 != 0")
+    g = w.reshape(d_in, d_out // W4_GROUP, W4_GROUP)
+    amax = np.max(np.abs(g), axis=2)
+    scale16 = (amax / np.float32(7.0)).astype(np.float16)
+    s = scale16.astype(np.float32)[:, :, None]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        q = np.where(s > 0, np.clip(np.rint(g / s) + 8, 0, 15), 8)
+    return q.reshape(d_in, d_out).astype(np.uint8), scale16.view(np.uint16)
+
+
+def dequantize_w4(codes, scale_bits) -> np.ndarray:
+    """w[j][o] = (q[j][o] - 8) * S[j][o / 128] in fp64."""
+    codes = np.asarray(codes, dtype=np.float64)
+    s = np.asarray(scale_bits, dtype=np.uint16).view(np.float16).astype(np.float64)
+    return (codes - 8.0) * np.repeat(s, W4_GROUP, axis=1)
 
 
 # ----------------------------------------------------------------------------------

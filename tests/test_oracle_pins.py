@@ -540,3 +540,30 @@ def test_decode_step_p0_equals_dense_model():
     nxt, logits, _ = O.larosa_decode_step(tok, e_f, folded, cfg, (d, d, d, 128), caches_r, pos, h_f, cfg["eps"])
     assert np.linalg.norm(logits - ref_logits) <= 1e-10 * np.linalg.norm(ref_logits)
     assert nxt == int(np.argmax(ref_logits))
+
+
+# ------------------------------------------------------------------ W4A16 (N3)
+def test_w4_worked_example_and_error_bound():
+    """A hand-computed group (bf16(0.7) = 0.69921875 = max |w|; 0.69921875 / 7 = 0.09988839...
+    -> nearest fp16 1637 * 2^-14 = 0.09991455078125 (vs 1636 * 2^-14); w / s rounded half-to-even) and the quantisation bound |w - deq| <= s / 2 on random groups
+    (interior codes), codes in [0, 15], an all-zero group -> scale 0, codes 8, deq 0."""
+    row = np.zeros((1, 128), dtype=np.float32)
+    row[0, :6] = [0.7, -0.35, 0.05, -0.7, 0.25, 0.0]
+    q, sb = O.quantize_w4(O.f64_to_bf16_rne(row))
+    s = float(np.uint16(sb[0, 0]).view(np.float16))
+    assert s == 0.09991455078125
+    wb = O.bf16_to_f64(O.f64_to_bf16_rne(row))[0]
+    # by hand: 0.69921875/s = 6.998 -> 7; -0.349609375/s = -3.499 -> -3; 0.0500488/s = 0.5009
+    # -> 1 (above the midpoint); 0.25/s = 2.5021 -> 3
+    assert list(q[0, :6].astype(int) - 8) == [7, -3, 1, -7, 3, 0]
+    assert np.all(q[0, 6:] == 8)
+    zq, zs = O.quantize_w4(np.zeros((1, 256), dtype=np.uint16))
+    assert np.all(zq == 8) and np.all(zs == 0) and np.all(O.dequantize_w4(zq, zs) == 0)
+    rng = np.random.default_rng(0)
+    w = O.f64_to_bf16_rne(rng.standard_normal((8, 512)).astype(np.float32) * 0.02)
+    q, sb = O.quantize_w4(w)
+    assert q.max() <= 15 and q.min() >= 0
+    deq = O.dequantize_w4(q, sb)
+    wf = O.bf16_to_f64(w)
+    sc = np.repeat(sb.view(np.float16).astype(np.float64), 128, axis=1)
+    assert np.all(np.abs(wf - deq) <= sc / 2 * (1 + 1e-3) + 1e-12)
