@@ -354,6 +354,46 @@ def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
             "pca_rotation_ms": pca_ms}
 
 
+def w4_sites_extra(layers, plan, shape, device, reps=48):
+    """N3: the batch-1 fused Top-K + sparse GEMV per LLaMA2-7B site on W4A16 weights (quantised
+    from the same folded bf16 weights, 8 copies cycled), timed like the bf16 roofline leg:
+    us, algorithmic GB/s (kept rows' int4 bytes + scales) and the speed-up over bf16 at the site."""
+    from paper_2507_01299_b200 import larosa as LZ
+    k1, k2, k3, k4 = plan
+    nq = shape.hq * shape.hd
+    sites = [("qkv", "w_qkv", shape.d, k1, shape.rms_eps), ("o", "w_o", nq, k2, -1.0),
+             ("gate_up", "w_gu", shape.d, k3, shape.rms_eps), ("down", "w_down", shape.inter, k4, -1.0)]
+    out = {}
+    n_in = 8
+    for name, attr, din, k, eps in sites:
+        qw = [LZ.quantize_w4(getattr(l, attr)) for l in layers]
+        dout = qw[0][0].shape[1] * 2
+        xs = [synth.residual_activation(1, din, seed=500 + r)[0].to(device) for r in range(n_in)]
+        wss = [LZ.topk_sparse_gemv_workspace(din, dout, device) for _ in range(n_in)]
+        y = torch.empty((dout,), dtype=torch.float32, device=device)
+        for i in range(n_in):
+            LZ.topk_sparse_gemv_w4(xs[i], k, *qw[0], rms_eps=eps, out=y, ws=wss[i])
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(reps):
+                LZ.topk_sparse_gemv_w4(xs[i % n_in], k, *qw[i % len(qw)], rms_eps=eps, out=y, ws=wss[i % n_in],
+                                       prepared=True)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+        alg = k * (dout // 2 + dout // 128 * 2) + din * 4 + dout * 4
+        out[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k}
+        del qw
+    return out
+
+
 def rotation_variants_extra(device, shape, steps=1000, copies=4, p=0.5):
     """Table 6's rotation variants on the LLaMA2-7B block (batch 1, ctx 256, p = 0.5): Q_L (one
     rotation per layer), Q_B (attention / MLP blocks rotated separately: one more D x D adapter,
@@ -673,6 +713,7 @@ def main():
 
     # ---- dominant kernel roofline: the SELECT GEMV per site, timed live in isolation --------
     gem = time_gemv_sites(layers, plan, shape, device)
+    w4 = None if args.no_sweep else w4_sites_extra(layers, plan, shape, device)
     bytes_step = sum(v["bytes"] for v in gem.values())
     us_gemv = sum(v["us"] for v in gem.values())
     peaks, peak_kind = measured_peaks()
@@ -713,6 +754,8 @@ def main():
                   "calibration_n1": calibration_extra(device),
                   "latency_consistency": latency_consistency_extra(layers, kv, pos, ws_buf, shape, device),
                   "rotation_variants": rotation_variants_extra(device, shape),
+                  "w4a16_sites": {k: dict(v, bf16_us=gem[k if k != "down" else ("down+adapter" if merged else "down")]["us"])
+                                  for k, v in w4.items()},
                   "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
 
     cpu = None

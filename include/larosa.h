@@ -360,6 +360,27 @@ size_t larosa_pca_rotation_workspace_size(int64_t d);
 larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q, float* lam, void* ws, size_t ws_bytes,
                                   larosa_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * W4A16 (the paper's compatibility with weight quantisation):
+ * group-quantised int4 weights in the column-major layout, group size LAROSA_W4_GROUP along
+ * the output dimension of each input row:
+ *   Wq uint8 [d_in][d_out / 2]: byte b of row j = columns 2b (low nibble), 2b + 1 (high)
+ *   S  fp16 bits [d_in][d_out / LAROSA_W4_GROUP];  w[j][o] = (q - 8) * S[j][o / group]
+ * larosa_quantize_w4: from bf16 W [d_in][d_out]: scale = RNE_fp16(max |w| / 7) per (row,
+ *   group) (fp32 divide), q = clamp(rint(w / scale) + 8, 0, 15) (fp32 divide; scale 0 -> 8).
+ *   d_out % 256 == 0.  Asynchronous.
+ * larosa_topk_sparse_gemv_w4: larosa_topk_sparse_gemv on these weights,
+ *   y[o] = sum_{j in S} x[j] s w[j][o]; same selection (Top-K of |x|, ties -> lower index),
+ *   workspace and `prepared` semantics; d_out % 256 == 0; Wq, x, y 16-byte aligned, S 4-byte.
+ * ------------------------------------------------------------------------------ */
+#define LAROSA_W4_GROUP 128
+larosa_status larosa_quantize_w4(const uint16_t* W, int64_t d_in, int64_t d_out, uint8_t* Wq, uint16_t* S,
+                                 larosa_stream_t stream);
+size_t larosa_topk_sparse_gemv_w4_workspace_size(int64_t d_in, int64_t d_out);
+larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in, int64_t k, float rms_eps, const uint8_t* Wq,
+                                         const uint16_t* S, int64_t d_out, float* y, int32_t prepared, void* ws,
+                                         size_t ws_bytes, larosa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

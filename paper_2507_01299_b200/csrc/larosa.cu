@@ -19,6 +19,7 @@
 #include "fold_tc.cuh"
 #include "gemv_tc.cuh"
 #include "calib.cuh"
+#include "gemv_w4.cuh"
 
 #include <cusolverDn.h>
 #include <mutex>
@@ -1623,4 +1624,83 @@ extern "C" larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q
     LAROSA_TRY(cuda_check(cudaStreamSynchronize(st), "pca: synchronize"));
     if (hinfo != 0) return fail(LAROSA_ECUDA, "pca: eigensolver did not converge (info %d)", hinfo);
     return LAROSA_OK;
+}
+
+// ============================================================================== N3 W4A16
+static_assert(LAROSA_W4_GROUP == kW4Group, "W4 group size mismatch");
+extern "C" larosa_status larosa_quantize_w4(const uint16_t* W, int64_t d_in, int64_t d_out, uint8_t* Wq, uint16_t* S,
+                                            larosa_stream_t stream) {
+    if (!W || !Wq || !S) return fail(LAROSA_EINVAL, "quantize_w4: NULL pointer");
+    if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "quantize_w4: d_in, d_out must be > 0");
+    if (d_out % kSliceCols) return fail(LAROSA_EUNSUPPORTED, "quantize_w4: d_out %% 256 != 0");
+    const int64_t units = d_in * (d_out / kW4Group);
+    if (units > (int64_t)1 << 30) return fail(LAROSA_EUNSUPPORTED, "quantize_w4: too large");
+    const unsigned blocks = (unsigned)((units + 7) / 8);
+    quantize_w4_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(W, (int)d_in, (int)d_out, Wq, S);
+    return cuda_check(cudaGetLastError(), "quantize_w4 launch");
+}
+
+extern "C" size_t larosa_topk_sparse_gemv_w4_workspace_size(int64_t d_in, int64_t d_out) {
+    return larosa_topk_sparse_gemv_workspace_size(d_in, d_out);
+}
+
+extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in, int64_t k, float rms_eps,
+                                                    const uint8_t* Wq, const uint16_t* S, int64_t d_out, float* y,
+                                                    int32_t prepared, void* ws, size_t ws_bytes,
+                                                    larosa_stream_t stream) {
+    if (!x || !Wq || !S || !y) return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: NULL pointer");
+    if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: d_in, d_out must be > 0");
+    if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: k outside [0, d_in]");
+    if (d_in > LAROSA_MAX_DIM || d_in % 8) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: d_in");
+    if (d_out % kSliceCols || d_out > (int64_t)64 * kW4SliceCols)
+        return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: d_out must be a multiple of 256 (<= 65536)");
+    if (!aligned16(Wq) || !aligned16(x) || !aligned16(y) || (reinterpret_cast<uintptr_t>(S) & 3))
+        return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: alignment (Wq, x, y 16 B; S 4 B)");
+    const size_t need = larosa_topk_sparse_gemv_workspace_size(d_in, d_out);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "topk_sparse_gemv_w4: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Carver c(ws);
+    unsigned long long* acc;
+    SiteSel sel;
+    carve_topk_gemv(c, d_in, d_out, &acc, &sel);
+    if (rms_eps < 0.f) sel.ssq = nullptr;
+    if (!prepared)
+        LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(d_in)), dim3(kPrepThreads), 0, st, x, (int)d_in,
+                                     sel, c.counters(kPrepBarrier)),
+                              "select prep launch"));
+    // 1024-column slices (512 bytes of int4 per kept row and CTA), one wave of 2 CTAs per SM
+    const int n_sl = (int)((d_out + kW4SliceCols - 1) / kW4SliceCols);
+    const int64_t nwords = (d_in + 31) / 32;
+    const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
+    const int n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
+    const int list_cap = (int)(32 * ((nwords + n_splits - 1) / n_splits));
+    const size_t smem = w4_region_bytes((int)d_in) + (size_t)list_cap * 8 + kGemvMisc * 4 + (size_t)list_cap * 16;
+    GemvArgs a = gemv_args_base();
+    a.ld = d_out;
+    a.d_out = (int)d_out;
+    a.mode = GEMV_SELECT;
+    a.x = x;
+    a.ldx = d_in;
+    a.d_in = (int)d_in;
+    a.sel = sel;
+    a.sel_nssq = (int)((d_in + kSliceCols - 1) / kSliceCols);
+    a.sel_k = (int)k;
+    a.sel_eps = rms_eps;
+    a.batch = 1;
+    a.acc = acc;
+    a.acc_ld = d_out;
+    a.epi = EPI_STORE;
+    a.tickets = c.counters(kGemvTicketBase);
+    a.out = y;
+    a.out_ld = d_out;
+    a.n_splits = n_splits;
+    a.list_cap = list_cap;
+    static bool attr = false;
+    if (!attr) {
+        LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, 227 * 1024), "cudaFuncSetAttribute(gemv_w4)"));
+        attr = true;
+    }
+    if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: shared memory plan too large");
+    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
+                      "gemv_w4 launch");
 }

@@ -96,6 +96,11 @@ def lib() -> ctypes.CDLL:
     L.larosa_topk_sparse_gemv_dense2.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _c_i64, _vp, _vp,
                                                  _c_i64, _vp, _c_i32, _vp, ctypes.c_size_t, _vp]
     L.larosa_embed.argtypes = [_vp, _c_i64, _c_i64, _vp, _c_i32, _vp, _vp]
+    L.larosa_quantize_w4.argtypes = [_vp, _c_i64, _c_i64, _vp, _vp, _vp]
+    L.larosa_topk_sparse_gemv_w4_workspace_size.restype = ctypes.c_size_t
+    L.larosa_topk_sparse_gemv_w4_workspace_size.argtypes = [_c_i64, _c_i64]
+    L.larosa_topk_sparse_gemv_w4.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _vp, _c_i64, _vp, _c_i32, _vp,
+                                             ctypes.c_size_t, _vp]
     L.larosa_calib_covariance_workspace_size.restype = ctypes.c_size_t
     L.larosa_calib_covariance_workspace_size.argtypes = [_c_i64, _c_i64]
     L.larosa_calib_covariance.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _c_i32, _vp, _vp, ctypes.c_size_t, _vp]
@@ -292,6 +297,36 @@ def topk_sparse_gemv_dense2(x: torch.Tensor, k: int, W: torch.Tensor, x2: torch.
         ws = _ws(("topk_sparse_gemv", d_in, ld), nb, W.device)
     _check(L.larosa_topk_sparse_gemv_dense2(_ptr(x), d_in, int(k), float(rms_eps), _ptr(W), ld, ld, _ptr(x2), _ptr(W2),
                                             d2, _ptr(y), int(prepared), _ptr(ws), ws.numel(), _stream(stream)))
+    return y
+
+
+LAROSA_W4_GROUP = 128
+
+
+def quantize_w4(W: torch.Tensor, stream=None):
+    """(Wq uint8 [d_in, d_out/2], S fp16 bits int16 [d_in, d_out/128]) of bf16 bits W [d_in, d_out]
+    (larosa_quantize_w4; symmetric int4 per row and group of 128 outputs)."""
+    d_in, d_out = W.shape
+    Wq = torch.empty((d_in, d_out // 2), dtype=torch.uint8, device=W.device)
+    S = torch.empty((d_in, d_out // LAROSA_W4_GROUP), dtype=torch.int16, device=W.device)
+    _check(lib().larosa_quantize_w4(_ptr(W), d_in, d_out, _ptr(Wq), _ptr(S), _stream(stream)))
+    return Wq, S
+
+
+def topk_sparse_gemv_w4(x: torch.Tensor, k: int, Wq: torch.Tensor, S: torch.Tensor, rms_eps: float = -1.0,
+                        out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, prepared: bool = False,
+                        stream=None) -> torch.Tensor:
+    """Batch 1: y = sum_{j in TopK_k(|x|)} x_j s w4[j] (W4A16 weights; larosa_topk_sparse_gemv_w4)."""
+    x = x.reshape(-1)
+    d_in = Wq.shape[0]
+    d_out = Wq.shape[1] * 2
+    y = out if out is not None else torch.empty((d_out,), dtype=torch.float32, device=Wq.device)
+    L = lib()
+    nb = L.larosa_topk_sparse_gemv_w4_workspace_size(d_in, d_out)
+    if ws is None:
+        ws = _ws(("topk_sparse_gemv_w4", d_in, d_out), nb, Wq.device)
+    _check(L.larosa_topk_sparse_gemv_w4(_ptr(x), d_in, int(k), float(rms_eps), _ptr(Wq), _ptr(S), d_out, _ptr(y),
+                                        int(prepared), _ptr(ws), ws.numel(), _stream(stream)))
     return y
 
 
