@@ -10,3 +10,5 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 8 -c 4 -o gpurun_out/prof_gemv \
     python tools/probe_layer.py > gpurun_out/ncu_full.log 2>&1; echo full_rc=$?
 python tools/layer_timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err; echo tl_rc=$?
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?; tail -1 gpurun_out/smoke.log
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ref.json 2> gpurun_out/ref.err; echo ref_rc=$?; cat gpurun_out/ref.json
