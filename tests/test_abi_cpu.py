@@ -137,3 +137,38 @@ def test_no_cpu_fallback():
     with pytest.raises((ValueError, RuntimeError)):
         LZ.sparse_gemv(torch.zeros((64, 128), dtype=torch.int16), torch.zeros((1, 8), dtype=torch.int32),
                        torch.zeros((1, 8)))
+
+
+def test_new_entry_points_validation():
+    """Argument checks of the dense2, W4A16, calibration and layer-variant entry points (header
+    contracts: NULL -> EINVAL, unsupported shapes -> EUNSUPPORTED, workspace -> EWORKSPACE)."""
+    L = LZ.lib()
+    ws = ctypes.c_void_p(1 << 21)
+    f = ctypes.c_float
+    # dense2: NULL x2 / W2, d2 out of range
+    assert _status("larosa_topk_sparse_gemv_dense2", FAKE, 64, 8, f(-1), FAKE, 128, 128, None, FAKE, 64, FAKE, 0, ws,
+                   1 << 30, None) == 1
+    assert _status("larosa_topk_sparse_gemv_dense2", FAKE, 64, 8, f(-1), FAKE, 128, 128, FAKE, FAKE, 0, FAKE, 0, ws,
+                   1 << 30, None) == 1
+    # W4: d_out not a multiple of 256, k > d_in, NULL scales, workspace too small
+    assert _status("larosa_quantize_w4", FAKE, 64, 200, FAKE, FAKE, None) == 3
+    assert _status("larosa_quantize_w4", FAKE, 64, 256, None, FAKE, None) == 1
+    assert _status("larosa_topk_sparse_gemv_w4", FAKE, 64, 65, f(-1), FAKE, FAKE, 256, FAKE, 0, ws, 1 << 30, None) == 1
+    assert _status("larosa_topk_sparse_gemv_w4", FAKE, 64, 8, f(-1), FAKE, None, 256, FAKE, 0, ws, 1 << 30, None) == 1
+    assert _status("larosa_topk_sparse_gemv_w4", FAKE, 64, 8, f(-1), FAKE, FAKE, 300, FAKE, 0, ws, 1 << 30, None) == 3
+    assert _status("larosa_topk_sparse_gemv_w4", FAKE, 64, 8, f(-1), FAKE, FAKE, 256, FAKE, 0, ws, 16, None) == 6
+    # calibration: NULL, bad dims; PCA: NULL, d too large
+    assert _status("larosa_calib_covariance", None, 64, 64, f(1), 0, FAKE, ws, 1 << 30, None) == 1
+    assert _status("larosa_calib_covariance", FAKE, 0, 64, f(1), 0, FAKE, ws, 1 << 30, None) == 1
+    assert _status("larosa_pca_rotation", None, 64, FAKE, FAKE, ws, 1 << 30, None) == 1
+    assert _status("larosa_pca_rotation", FAKE, 40000, FAKE, FAKE, ws, 1 << 30, None) == 3
+    # layer: adapter_in_down without an adapter
+    w = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, None, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 1, None)
+    p = LZ.LayerPlanC(2048, 2048, 2048, 5504)
+    s = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 1)
+    assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s), None, ws, 1 << 40, None) == 1
+    # shard phase: the block-wise rotation is not supported there
+    w2 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, FAKE)
+    sh = LZ.ShardC(0, 1)
+    assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w2), ctypes.byref(p), ctypes.byref(sh), 1, FAKE, FAKE, FAKE,
+                                             None, None, None, 0, ws, 1 << 40, None) in (1, 3)
