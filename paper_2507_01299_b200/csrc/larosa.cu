@@ -1009,7 +1009,6 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     o->acc_gu = c.take<unsigned long long>((size_t)batch * L.dgu);
     o->acc_down = c.take<unsigned long long>((size_t)batch * L.d);
     o->acc_adp = c.take<unsigned long long>((size_t)batch * L.d);
-    const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
     for (int s = 0; s < 4; ++s) {
         SiteSel& q = o->sel[s];
         q.hist = c.take<uint32_t>(kSelHistAlloc);

@@ -97,7 +97,7 @@ __device__ __forceinline__ uint32_t topk_ld_remote(uint32_t addr) {
 // mode, elements per thread) so each launch only fetches its own (small) code.
 template <int MODE, int EPT>
 __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     int* hist0 = reinterpret_cast<int*>(smem);                 // local histograms (double-buffered)
     int* hist1 = hist0 + kTopkBins;
     int* scr = hist1 + kTopkBins;
