@@ -683,16 +683,24 @@ def main():
     h_out = torch.empty((1, shape.d), dtype=torch.float32).pin_memory()
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
-    # one CUDA graph per layer copy holding the step's H2D copy (pinned host -> resid), the layer
-    # (input from the host: the preparation kernel runs) and the D2H copy of the output
-    capture_graphs(layers, kv, resid, pos, plan, ws_buf, chained=False)   # warm-up outside capture
+    # one CUDA graph per layer copy: the layer reads the step's input from pinned host memory in
+    # its preparation kernel (H2D inside the kernel) and its last epilogue writes the output to
+    # pinned host memory as well (D2H inside the kernel) -- larosa_layer_state.host_in / host_out
+    def io_state(kc, vc):
+        return LZ.LayerState(resid, kc, vc, pos, chained=False, host_in=h_in, host_out=h_out)
+
+    s_io = torch.cuda.Stream()
+    s_io.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_io):
+        for w, (kc, vc) in zip(layers, kv):   # warm-up outside capture
+            LZ.sparse_layer(w, plan, io_state(kc, vc), ws=ws_buf)
+    torch.cuda.current_stream().wait_stream(s_io)
+    torch.cuda.synchronize()
     io_graphs = []
     for w, (kc, vc) in zip(layers, kv):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            resid.copy_(h_in, non_blocking=True)
-            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos, chained=False), ws=ws_buf)
-            h_out.copy_(resid, non_blocking=True)
+            LZ.sparse_layer(w, plan, io_state(kc, vc), ws=ws_buf)
         io_graphs.append(g)
     for i in range(args.warmup):
         io_graphs[i % len(io_graphs)].replay()

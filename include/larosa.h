@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 3
+#define LAROSA_ABI_VERSION 4
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -268,6 +268,13 @@ typedef struct {
      * That call's last epilogue already produced the h1 key histogram and RMS partials of
      * resid, so the preparation kernel is skipped.  0 is always correct. */
     int32_t chained;
+    /* Batch 1, optional (NULL = unused): pinned, device-mapped host buffers of d floats.
+     * host_in (only when chained == 0): the step's input residual is read from it by the
+     * preparation kernel, which also writes resid -- the host-to-device transfer happens inside
+     * the layer's first kernel.  host_out: the layer's last epilogue also writes r_next there
+     * (device-to-host inside the kernel; complete when the stream reaches the layer's end). */
+    const float* host_in;
+    float* host_out;
 } larosa_layer_state;
 
 typedef struct {

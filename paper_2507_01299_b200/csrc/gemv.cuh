@@ -142,6 +142,7 @@ struct GemvArgs {
     int64_t res_ld;
     float* out;                        // [batch][out_ld]
     int64_t out_ld;
+    float* out_host;                       // optional second copy of out (batch 1; mapped host memory)
     SiteSel out_sel;                   // batch 1: next site's selection data (hist null = none)
     float* out_ssq;                    // [batch][out_ssq_ld] per-slice sums of squares or null
     int64_t out_ssq_ld;
@@ -668,6 +669,7 @@ __device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred, const f
                 if (a.bias) v += bf16f(a.bias[o]);
                 if (a.res) v = a.res[(size_t)b * a.res_ld + o] + v;
                 a.out[(size_t)b * a.out_ld + o] = v;
+                if (a.out_host) a.out_host[(size_t)b * a.out_ld + o] = v;
                 has = true;
             }
         }
@@ -974,7 +976,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
 // sum of squares with the exact arithmetic of gemv_epilogue.  bar: 2 zero-at-rest words.
 constexpr int kPrepThreads = kSliceCols;
 __global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* __restrict__ x, int d, SiteSel o,
-                                                                   unsigned* bar) {
+                                                                   unsigned* bar, float* __restrict__ copy_out) {
     __shared__ float sred[kPrepThreads / 32];
     pdl_wait();
     pdl_trigger();
@@ -994,7 +996,10 @@ __global__ void __launch_bounds__(kPrepThreads) select_prep_kernel(const float* 
     }
     __syncthreads();
     const int i = cta * kPrepThreads + tid;
-    const float v = i < d ? x[i] : 0.f;
+    // copy_out != null: x is mapped host memory -- read it uncached (.cv: fetched over the bus
+    // every call, never an L2 hit on an earlier step's line) and store it to the device copy
+    const float v = i < d ? (copy_out ? __ldcv(x + i) : x[i]) : 0.f;
+    if (copy_out && i < d) copy_out[i] = v;
     if (i < d) hist_push(o, v, i);
     if (o.ssq) {
         const float w = slice_ssq_warp(v);

@@ -625,7 +625,7 @@ static larosa_status topk_sparse_gemv_impl(const float* x, int64_t d_in, int64_t
     if (rms_eps < 0.f) sel.ssq = nullptr;
     if (!prepared)
         LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(d_in)), dim3(kPrepThreads), 0, st, x, (int)d_in,
-                                     sel, c.counters(kPrepBarrier)),
+                                     sel, c.counters(kPrepBarrier), (float*)nullptr),
                               "select prep launch"));
     const GemvPlan p = W2 ? plan_gemv_comp(d_out, k, d_in, d2) : plan_gemv(d_out, k, 1, GEMV_SELECT, d_in);
     GemvArgs a = gemv_args_base();
@@ -1037,6 +1037,7 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
         return fail(LAROSA_EINVAL, "sparse_layer: dims must be > 0");
     if (w->n_q_heads % w->n_kv_heads) return fail(LAROSA_ESHAPE, "sparse_layer: Hq %% Hkv != 0");
     if (w->adapter_in_down && !w->adapter) return fail(LAROSA_EINVAL, "sparse_layer: adapter_in_down needs the adapter");
+    if ((s->host_in || s->host_out) && s->batch != 1) return fail(LAROSA_EINVAL, "sparse_layer: host_in/out need batch 1");
     if (w->n_q_heads / w->n_kv_heads > kAttnMaxG) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
     if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: head_dim must be 64 or 128");
     if (w->d % 8 || w->inter % LAROSA_GU_BLOCK) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: d %% 8 or inter %% 64");
@@ -1192,7 +1193,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     if (fused) {
         if (!s->chained && on(0))
             LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(L.d)), dim3(kPrepThreads), 0, st,
-                                         (const float*)s->resid, (int)L.d, W.sel[0], c.counters(kPrepBarrier)),
+                                         s->host_in ? s->host_in : (const float*)s->resid, (int)L.d, W.sel[0],
+                                         c.counters(kPrepBarrier), s->host_in ? s->resid : (float*)nullptr),
                                   "select prep launch"));
     } else if (on(0)) {
         LAROSA_TRY(rule_topk(0, s->resid, L.d, plan->k_h1, w->rms_eps));
@@ -1301,6 +1303,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             a.x2 = W.rmid;
             a.d2 = (int)L.d;
             epi(a, 2, EPI_STORE, nullptr, s->resid, 0);
+            a.out_host = s->host_out;
             LAROSA_TRY(launch_gemv(a, plan_gemv_comp(L.d, plan->k_h4, L.inter, L.d), 1, st));
         } else {
             a.epi = EPI_NONE;
@@ -1325,10 +1328,12 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     if (merged) return LAROSA_OK;   // profiling mask without the down launch
     if (on(8)) {
         GemvArgs a = site_gemv(3, W.h4, L.inter, plan->k_h4, -1.0f, w->w_down, L.d, W.acc_down);
-        if (w->adapter)
+        if (w->adapter) {
             epi(a, 2, EPI_RESID, W.rmid, W.radp, -1);
-        else
+        } else {
             epi(a, 2, EPI_RESID, W.rmid, s->resid, 0);
+            a.out_host = s->host_out;
+        }
         a.zero_hist = fused ? W.sel[2].hist : nullptr;   // h3's consumer (gate|up) is done
         a.tl = tl_slot(4);
         a.zero_words = kSelHistTotal;
@@ -1351,6 +1356,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             a.acc = W.acc_adp;
             a.acc_ld = L.d;
             epi(a, 3, EPI_STORE, nullptr, s->resid, 0);
+            a.out_host = s->host_out;
             a.tl = tl_slot(5);
             LAROSA_TRY(launch_gemv(a, p, bp, st));
         }
@@ -1477,7 +1483,7 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         SiteSel sel = W.sel;
         if (eps < 0.f) sel.ssq = nullptr;
         LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(din)), dim3(kPrepThreads), 0, st, x, (int)din,
-                                     sel, c.counters(kPrepBarrier)),
+                                     sel, c.counters(kPrepBarrier), (float*)nullptr),
                               "select prep launch"));
         a.mode = GEMV_SELECT;
         a.sel = sel;
@@ -1665,7 +1671,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     if (rms_eps < 0.f) sel.ssq = nullptr;
     if (!prepared)
         LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(d_in)), dim3(kPrepThreads), 0, st, x, (int)d_in,
-                                     sel, c.counters(kPrepBarrier)),
+                                     sel, c.counters(kPrepBarrier), (float*)nullptr),
                               "select prep launch"));
     // 1024-column slices (512 bytes of int4 per kept row and CTA), one wave of 2 CTAs per SM
     const int n_sl = (int)((d_out + kW4SliceCols - 1) / kW4SliceCols);

@@ -46,7 +46,7 @@ class LayerPlanC(ctypes.Structure):
 
 class LayerStateC(ctypes.Structure):
     _fields_ = [("resid", _vp), ("k_cache", _vp), ("v_cache", _vp), ("pos", _vp),
-                ("max_ctx", _c_i64), ("batch", _c_i32), ("chained", _c_i32)]
+                ("max_ctx", _c_i64), ("batch", _c_i32), ("chained", _c_i32), ("host_in", _vp), ("host_out", _vp)]
 
 
 class LayerTapsC(ctypes.Structure):
@@ -128,7 +128,7 @@ def lib() -> ctypes.CDLL:
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 3:
+    if L.larosa_abi_version() != 4:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -138,6 +138,15 @@ def _check(status: int):
     if status != 0:
         L = lib()
         raise LarosaError(status, f"{L.larosa_status_string(status).decode()} — {L.larosa_last_error().decode()}")
+
+
+def _host_ptr(t: Optional[torch.Tensor]):
+    """Pinned host tensor -> its address (device-accessible under unified addressing)."""
+    if t is None:
+        return None
+    if t.is_cuda or not t.is_pinned() or not t.is_contiguous():
+        raise ValueError("larosa: host buffers must be contiguous pinned host tensors")
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -418,11 +427,14 @@ class LayerState:
     v_cache: torch.Tensor
     pos: torch.Tensor        # int32 [B] on device
     chained: bool = False    # resid was written by the previous layer call on the same workspace
+    host_in: Optional[torch.Tensor] = None    # pinned host fp32 [1, d]: the input, read in-kernel
+    host_out: Optional[torch.Tensor] = None   # pinned host fp32 [1, d]: the output, written in-kernel
 
     def c(self) -> LayerStateC:
         B = self.resid.shape[0]
         return LayerStateC(_ptr(self.resid), _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.pos),
-                           self.k_cache.shape[2], B, int(self.chained))
+                           self.k_cache.shape[2], B, int(self.chained), _host_ptr(self.host_in),
+                           _host_ptr(self.host_out))
 
 
 TAP_NAMES = [f[0] for f in LayerTapsC._fields_]

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 14, names
     for n in names:
         assert hasattr(L, n), f"missing export {n}"
-    assert L.larosa_abi_version() == 3
+    assert L.larosa_abi_version() == 4
 
 
 def test_status_strings():
@@ -167,6 +167,10 @@ def test_new_entry_points_validation():
     p = LZ.LayerPlanC(2048, 2048, 2048, 5504)
     s = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 1)
     assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s), None, ws, 1 << 40, None) == 1
+    # host buffers need batch 1
+    w.adapter_in_down = 0
+    s3 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 2, 0, FAKE, None)
+    assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s3), None, ws, 1 << 40, None) == 1
     # shard phase: the block-wise rotation is not supported there
     w2 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, FAKE)
     sh = LZ.ShardC(0, 1)

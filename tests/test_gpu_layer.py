@@ -303,3 +303,22 @@ def test_layer_extreme_plans(batch, merged, plan_kind):
             if not np.array_equal(tp[f"idx_h{s}"][b].cpu().numpy(), inter_[f"idx{s}"]):
                 pytest.skip(f"certified near-tie swap at site h{s} (P5, reported)")
         assert rel_max(f64(st.resid[b]), out) <= 1e-4
+
+
+@pytest.mark.parametrize("merged", [True, False])
+def test_layer_host_io_equals_device_io(merged):
+    """larosa_layer_state.host_in / host_out (pinned host buffers read / written inside the
+    layer's first and last kernels) give bit-identical results to device-resident I/O."""
+    shape = SMALL
+    ctx, max_ctx = 12, 32
+    _, _, _, lw, plan, resid, kc0, vc0, pos = build(shape, 23, 1, ctx, max_ctx, 0.5, merged=merged)
+    st = LZ.LayerState(resid.clone().to(DEV), kc0.clone().to(DEV), vc0.clone().to(DEV), pos.to(DEV))
+    LZ.sparse_layer(lw, plan, st)
+    h_in = resid.clone().pin_memory()
+    h_out = torch.zeros_like(resid).pin_memory()
+    dev_buf = torch.full_like(resid, float("nan")).to(DEV)   # must be overwritten from host_in
+    st2 = LZ.LayerState(dev_buf, kc0.clone().to(DEV), vc0.clone().to(DEV), pos.to(DEV), host_in=h_in, host_out=h_out)
+    LZ.sparse_layer(lw, plan, st2)
+    torch.cuda.synchronize()
+    assert torch.equal(st2.resid.cpu(), st.resid.cpu())
+    assert torch.equal(h_out, st.resid.cpu())
