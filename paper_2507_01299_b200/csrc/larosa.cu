@@ -179,6 +179,18 @@ GemvPlan plan_gemv(int64_t d_out, int64_t rows_src, int bp, int mode = GEMV_LIST
             p.n_slices * kMaxGemvCluster * 100 >= target * 85)
             by_target = kMaxGemvCluster;
         p.n_splits = std::max(by_cap, std::min(by_target, by_rows));
+        if (mode == GEMV_DENSE && p.n_slices >= target) {
+            // more slices than slots (the LM head): choose the splits that fill the last wave best
+            double best = 0.0;
+            for (int sp = std::max(1, by_cap); sp <= 8 && rows_src / sp >= 256; ++sp) {
+                const double ctas = (double)p.n_slices * sp, waves = std::ceil(ctas / target);
+                const double eff = ctas / (waves * target);
+                if (eff > best + 0.02) {
+                    best = eff;
+                    p.n_splits = sp;
+                }
+            }
+        }
         p.list_cap = mode == GEMV_SELECT ? (int)(32 * ((nwords + p.n_splits - 1) / p.n_splits))   // interleaved words
                                          : (int)std::max<int64_t>(32, (rows_src + p.n_splits - 1) / p.n_splits + 1);
         p.smem = gemv_smem_bytes(bp, p.list_cap, mode, (int)d_in);
