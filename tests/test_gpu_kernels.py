@@ -299,3 +299,16 @@ def test_topk_sparse_gemv_cluster_reduction_matches():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("d_in,k", [(32768, 16384), (32768, 1), (32760, 32759)])
+def test_topk_sparse_gemv_max_dim(d_in, k):
+    """The largest supported site width (LAROSA_MAX_DIM = 32768) and a ragged one just below it."""
+    x = synth.residual_activation(1, d_in, seed=d_in + k)[0]
+    Wb = synth.gaussian_bf16((d_in, 256), 60 + k % 7, d_in ** -0.5)
+    y = LZ.topk_sparse_gemv(x.to(DEV), k, Wb.to(DEV))
+    ref = _fused_ref(x, k, Wb, -1.0)
+    assert rel_max(f64(y), ref) <= 1e-5
+    with pytest.raises(LZ.LarosaError):
+        LZ.topk_sparse_gemv(torch.zeros(32776, device=DEV), 8, torch.zeros((32776, 256), dtype=torch.int16,
+                                                                           device=DEV))
