@@ -354,6 +354,64 @@ def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
             "pca_rotation_ms": pca_ms}
 
 
+def launch_decomposition(layers, kv, pos, ws_buf, plan, shape, device, reps=20):
+    """Where each SELECT launch's time goes inside the block step (per-CTA %globaltimer stamps,
+    larosa_debug_set_timeline; a separate run after the timed region): per site, the medians
+    over CTAs of the prologue (previous kernel's last exit -> row list ready: dependency release,
+    selection rule, mask and list), the stream (-> main loop done) and the tail (-> the last CTA's
+    exit: split-K reduction, slice ticket, epilogue), and the stream phase's bandwidth on the
+    site's kept-row bytes: over the median CTA's stream window, and over the whole span from the
+    first CTA's prologue end to the last CTA's loop end (for down + adapter the companions start
+    before the SELECT CTAs).  Supplementary to `roofline` (whole launches)."""
+    import ctypes
+    from paper_2507_01299_b200 import larosa as LZ
+    L = LZ.lib()
+    L.larosa_debug_set_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    L.larosa_debug_set_timeline.restype = None
+    n = len(layers)
+    tl = torch.zeros((n, 6, 1024, 16), dtype=torch.int64, device=device)
+    resid = synth.residual_activation(1, shape.d, seed=7).to(device)
+    for i in range(n):
+        LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos, chained=i > 0), ws=ws_buf)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(n):
+            L.larosa_debug_set_timeline(ctypes.c_void_p(tl[i].data_ptr()), 6)
+            LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos, chained=True), ws=ws_buf)
+        L.larosa_debug_set_timeline(None, 0)
+    k1, k2, k3, k4 = plan
+    nbytes = {"qkv": k1 * shape.qkv_out * 2, "o": k2 * shape.d * 2, "gate_up": k3 * 2 * shape.inter * 2,
+              "down+adapter": (k4 + shape.d) * shape.d * 2}
+    slots = {"qkv": (0, 5), "o": (2, 1), "gate_up": (3, 2), "down+adapter": (4, 3)}   # (slot, previous slot)
+    res = {k: {"prologue_us": [], "stream_us": [], "tail_us": [], "span_us": []} for k in nbytes}
+    for r in range(reps + 2):
+        tl.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        if r < 2:
+            continue
+        a = tl.cpu().numpy().astype(np.float64)
+        for li in range(1, n):
+            for name, (sl, prev) in slots.items():
+                pv = a[li - 1][4] if sl == 0 else a[li][prev]
+                t0 = pv[pv[:, 0] > 0][:, 4].max()
+                cur = a[li][sl]
+                cur = cur[cur[:, 0] > 0]
+                pro = np.median(cur[:, 2]) - t0
+                loop = np.median(cur[:, 3]) - t0
+                res[name]["prologue_us"].append(pro / 1e3)
+                res[name]["stream_us"].append((loop - pro) / 1e3)
+                res[name]["tail_us"].append((cur[:, 4].max() - t0 - loop) / 1e3)
+                res[name]["span_us"].append((cur[:, 3].max() - cur[:, 2].min()) / 1e3)
+    out = {}
+    for name, v in res.items():
+        pro, stm, tail, span = (float(np.mean(v[k])) for k in ("prologue_us", "stream_us", "tail_us", "span_us"))
+        out[name] = {"prologue_us": pro, "stream_us": stm, "tail_us": tail,
+                     "stream_phase_gbs_median_cta": nbytes[name] / stm / 1e3 if stm > 0 else None,
+                     "stream_phase_gbs_span": nbytes[name] / span / 1e3 if span > 0 else None}
+    return out
+
+
 def w4_sites_extra(layers, plan, shape, device, reps=48):
     """N3: the batch-1 fused Top-K + sparse GEMV per LLaMA2-7B site on W4A16 weights (quantised
     from the same folded bf16 weights, 8 copies cycled), timed like the bf16 roofline leg:
@@ -739,6 +797,8 @@ def main():
                              "dense adapter rows as companion CTAs)" if merged else
                              "5 site launches of one block step (QKV, O, gate|up, down at their k; adapter at k = D)")
                           + ", each timed back to back in a CUDA graph",
+                "decomposition_in_step": launch_decomposition(layers[:4], kv[:4], pos, ws_buf, plan, shape, device)
+                if merged else None,
                 "algorithmic_bytes_per_step": bytes_step, "gemv_us_per_step": us_gemv,
                 "launches_per_step": len(gem),
                 "peak_kind": f"{peak_kind} copy (hbm_gbs)", "per_site": gem}
