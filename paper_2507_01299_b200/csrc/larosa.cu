@@ -1004,6 +1004,8 @@ LayerDims layer_dims(const larosa_layer_weights* w) {
 }
 
 int attn_chunk(int64_t max_ctx, int units) {
+    static const int forced = env_int("LAROSA_ATTN_CHUNK", 0);   // tuning: 16, 32 or 64 positions
+    if (forced == 16 || forced == 32 || forced == 64) return forced;
     // enough CTAs to cover the SMs: units * n_chunks >= sm_count
     int ch = 4 * kAttnPosPerWarp;
     while (ch > 16 && units * ((max_ctx + ch - 1) / ch) < sm_count()) ch >>= 1;

@@ -1,2 +1,3 @@
-TAG=persm2 python tools/layer_us.py 0.5 3000
-LAROSA_GEMV_CTAS_PER_SM=1 TAG=persm1 python tools/layer_us.py 0.5 3000
+TAG=auto python tools/layer_us.py 0.5 3000
+LAROSA_ATTN_CHUNK=16 TAG=ch16 python tools/layer_us.py 0.5 3000
+LAROSA_ATTN_CHUNK=64 TAG=ch64 python tools/layer_us.py 0.5 3000
