@@ -412,6 +412,39 @@ def launch_decomposition(layers, kv, pos, ws_buf, plan, shape, device, reps=20):
     return out
 
 
+def prefill_extra(layers, shape, device, p=0.5, n_tok=512, reps=10):
+    """N2: a 512-token prompt through the LLaMA2-7B gate|up projection with per-token Top-K
+    (larosa_prefill_sparse_gemm: our selection + hi/lo split, cuBLAS bf16 GEMMs) vs the plain
+    dense bf16 GEMM on unmasked activations (cuBLAS): ms and TFLOP/s of the useful 2 n k d_out."""
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    k = M.site_plan(shape, p)[2]
+    W = layers[0].w_gu
+    d_in, d_out = W.shape
+    X = torch.randn((n_tok, d_in), device=device)
+    Y = torch.empty((n_tok, d_out), device=device)
+    LZ.prefill_sparse_gemm(X, k, W, rms_eps=shape.rms_eps, out=Y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        LZ.prefill_sparse_gemm(X, k, W, rms_eps=shape.rms_eps, out=Y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    Xb, Wb = X.to(torch.bfloat16), W.view(torch.bfloat16)
+    torch.matmul(Xb, Wb)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(Xb, Wb)
+    e1.record()
+    torch.cuda.synchronize()
+    dense_ms = e0.elapsed_time(e1) / reps
+    return {"n_tok": n_tok, "k": k, "ms": ms, "tok_s": n_tok / ms * 1e3, "useful_tflops": 2.0 * n_tok * k * d_out / ms / 1e9,
+            "cublas_dense_bf16_ms": dense_ms}
+
+
 def w4_sites_extra(layers, plan, shape, device, reps=48):
     """N3: the batch-1 fused Top-K + sparse GEMV per LLaMA2-7B site on W4A16 weights (quantised
     from the same folded bf16 weights, 8 copies cycled), timed like the bf16 roofline leg:
@@ -822,6 +855,7 @@ def main():
                   "calibration_n1": calibration_extra(device),
                   "latency_consistency": latency_consistency_extra(layers, kv, pos, ws_buf, shape, device),
                   "rotation_variants": rotation_variants_extra(device, shape),
+                  "prefill_n2": prefill_extra(layers, shape, device),
                   "w4a16_sites": {k: dict(v, bf16_us=gem[k if k != "down" else ("down+adapter" if merged else "down")]["us"])
                                   for k, v in w4.items()},
                   "model_sweep_configs3": model_sweep_extra(device, merged=merged)}

@@ -388,6 +388,20 @@ larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in, int64_t k
                                          const uint16_t* S, int64_t d_out, float* y, int32_t prepared, void* ws,
                                          size_t ws_bytes, larosa_stream_t stream);
 
+/* ------------------------------------------------------------------------------
+ * Prefill (full sparsification of prompt tokens): n_tok tokens, each
+ * with its own exact Top-K (ties -> lower index) and RMS scale as larosa_rotate_topk (R = NULL):
+ *   Y[t][o] = sum_{j in S_t} X[t][j] s_t W[j][o]
+ * X fp32 [n_tok][d_in], W bf16 [d_in][d_out] (Wc layout), Y fp32 [n_tok][d_out].  The selection
+ * is ours (cluster radix select per token); the masked activations are split into bf16 hi + lo
+ * and the two products run as cuBLAS bf16 GEMMs with fp32 accumulation (a plain library GEMM:
+ * at prefill the union of the tokens' kept rows is every row).  n_tok <= 65535.
+ * ------------------------------------------------------------------------------ */
+size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in);
+larosa_status larosa_prefill_sparse_gemm(const float* X, int64_t n_tok, int64_t d_in, int64_t k, float rms_eps,
+                                         const uint16_t* W, int64_t d_out, float* Y, void* ws, size_t ws_bytes,
+                                         larosa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@
 // kernel here.
 #pragma once
 #include "common.cuh"
+#include "gemv.cuh"
 
 namespace larosa {
 
@@ -99,4 +100,27 @@ __global__ void __launch_bounds__(256) pca_order_sign_kernel(const double* __res
     for (int r = threadIdx.x; r < d; r += blockDim.x) Q[(size_t)r * d + c] = (float)(sgn * col[r]);
 }
 
+}  // namespace larosa
+
+namespace larosa {
+// Prefill: every token keeps its own Top-K (full sparsification of
+// prompt tokens P:77).  X_hi / X_lo [n][d] bf16 = split(x_t[i] * s_t) where token t keeps i (its
+// rule: key > Tk or key == Tk and i <= Ti), else 0; the GEMM Y = X_hi W + X_lo W then runs on the
+// tensor cores (cuBLAS, fp32 accumulation; the hi/lo split keeps ~16 mantissa bits of the fp32
+// activations, like the batched tcgen05 GEMV).
+__global__ void prefill_mask_split_kernel(const float* __restrict__ X, int n, int d, const ThreshOut* __restrict__ rules,
+                                          uint16_t* __restrict__ Xhi, uint16_t* __restrict__ Xlo) {
+    const size_t total = (size_t)n * d;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e / d), i = (int)(e % d);
+        const ThreshOut r = rules[t];
+        const float x = X[e];
+        const uint32_t key = __float_as_uint(x) & 0x7fffffffu;
+        const bool keep = key > r.tk || (key == r.tk && i <= r.ti);
+        const float v = keep ? x * r.scale : 0.f;
+        const uint16_t h = f2bf16_rne(v);
+        Xhi[e] = h;
+        Xlo[e] = f2bf16_rne(v - bf16f(h));
+    }
+}
 }  // namespace larosa

@@ -21,6 +21,7 @@
 #include "calib.cuh"
 #include "gemv_w4.cuh"
 
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <mutex>
 
@@ -1722,4 +1723,61 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: shared memory plan too large");
     return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
                       "gemv_w4 launch");
+}
+
+// ============================================================================== N2 prefill
+extern "C" size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in) {
+    if (n_tok <= 0 || d_in <= 0) return 0;
+    return (size_t)n_tok * sizeof(ThreshOut) + 2 * (size_t)n_tok * d_in * 2 + 1024;
+}
+
+namespace {
+std::mutex g_blas_mu;
+cublasHandle_t blas_handle() {
+    static cublasHandle_t h = nullptr;
+    if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
+    return h;
+}
+}  // namespace
+
+extern "C" larosa_status larosa_prefill_sparse_gemm(const float* X, int64_t n_tok, int64_t d_in, int64_t k,
+                                                    float rms_eps, const uint16_t* W, int64_t d_out, float* Y,
+                                                    void* ws, size_t ws_bytes, larosa_stream_t stream) {
+    if (!X || !W || !Y) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: NULL pointer");
+    if (n_tok <= 0 || d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: sizes must be > 0");
+    if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: k outside [0, d_in]");
+    if (d_in > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: d_in > %d", LAROSA_MAX_DIM);
+    if (n_tok > 65535 || d_out > (1 << 30) / n_tok) return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: too large");
+    const size_t need = larosa_prefill_sparse_gemm_workspace_size(n_tok, d_in);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "prefill_sparse_gemm: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Carver c(ws);
+    ThreshOut* rules = c.take<ThreshOut>((size_t)n_tok);
+    uint16_t* xhi = c.take<uint16_t>((size_t)n_tok * d_in);
+    uint16_t* xlo = c.take<uint16_t>((size_t)n_tok * d_in);
+    // every token's exact Top-K rule (one cluster radix select per token, Z10)
+    TopkKernelArgs t = topk_args_base();
+    t.x = X;
+    t.ldx = d_in;
+    t.d = (int)d_in;
+    t.k = (int)k;
+    t.rms_eps = rms_eps;
+    t.rule_out = rules;
+    LAROSA_TRY(launch_topk(t, (int)n_tok, st));
+    prefill_mask_split_kernel<<<1024, 256, 0, st>>>(X, (int)n_tok, (int)d_in, rules, xhi, xlo);
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "prefill mask/split"));
+    // Y^T [d_out][n] = W^T [d_out][d_in] . X^T [d_in][n]  (column-major views of the row-major arrays)
+    std::lock_guard<std::mutex> lk(g_blas_mu);
+    cublasHandle_t h = blas_handle();
+    if (!h) return fail(LAROSA_ECUDA, "prefill_sparse_gemm: cuBLAS unavailable");
+    if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "prefill: cublasSetStream");
+    const float one = 1.0f, zero = 0.0f;
+    for (int part = 0; part < 2; ++part) {
+        const cublasStatus_t r = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_out, (int)n_tok, (int)d_in, &one, W,
+                                              CUDA_R_16BF, (int)d_out, part ? xlo : xhi, CUDA_R_16BF, (int)d_in,
+                                              part ? &one : &zero, Y, CUDA_R_32F, (int)d_out, CUBLAS_COMPUTE_32F,
+                                              CUBLAS_GEMM_DEFAULT);
+        if (r != CUBLAS_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "prefill: cublasGemmEx (%d)", (int)r);
+    }
+    return LAROSA_OK;
 }
