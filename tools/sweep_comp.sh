@@ -1,2 +1,2 @@
-TAG=prefetch python tools/layer_us.py 0.5 3000
-LAROSA_ADAPTER_PREFETCH=0 TAG=noprefetch python tools/layer_us.py 0.5 3000
+TAG=respre python tools/layer_us.py 0.5 3000
+TAG=respre2 python tools/layer_us.py 0.5 3000
