@@ -29,6 +29,16 @@ constexpr int kTcN = 16;             // tokens (UMMA N; batch padded to 16)
 constexpr int kTcChunk = 64;         // kept rows per ring stage (UMMA K = 16 per instruction)
 constexpr int kTcStages = 4;
 constexpr int kTcProdWarps = 4;
+#ifndef LAROSA_TC_VPRE
+#define LAROSA_TC_VPRE 1
+#endif
+constexpr int kTcVPre = LAROSA_TC_VPRE;   // chunks of value look-ahead per producer thread (2-8: slower)
+#ifndef LAROSA_TC_FUSED_HILO
+#define LAROSA_TC_FUSED_HILO 1
+#endif
+// hi and lo as the two 16-column halves of ONE N = 32 MMA (B rows 0-15 = hi, 16-31 = lo are
+// contiguous in the stage): half the MMA instructions, each reading the A tile once
+constexpr bool kTcFused = LAROSA_TC_FUSED_HILO != 0;
 constexpr int kTcThreads = (kTcProdWarps + 1) * 32;
 constexpr int kTcABytes = kTcCols * kTcChunk * 2;              // 16 KB
 constexpr int kTcBBytes = kTcN * kTcChunk * 2;                 // 2 KB (hi, and again lo)
@@ -45,8 +55,11 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(const void* smem, uint32_
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 // kind::f16, A = B = BF16, D = F32, A MN-major, B K-major, M = 128, N = 16
-constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(kTcN >> 3) << 17) |
-                              ((uint32_t)(kTcCols >> 4) << 24);
+__host__ __device__ constexpr uint32_t tc_idesc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcCols >> 4) << 24);
+}
+constexpr uint32_t kTcIdesc = tc_idesc(kTcN);
+constexpr uint32_t kTcIdesc2 = tc_idesc(2 * kTcN);   // fused hi|lo
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gsrc, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
@@ -57,8 +70,22 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// {lo half = bf16(a), hi half = bf16(b)}, round to nearest even
+__device__ __forceinline__ uint32_t cvt_bf16x2(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// DENSE / THRESH (contiguous rows): the A tile comes by TMA, two boxes of 64 rows x 64 columns
+// (128-byte swizzle; box mg at +8 KB, row r at +128 r), i.e. LBO = 8 KB, SBO = 1 KB; LIST
+// (gathered rows) keeps the per-thread cp.async layout (LBO = 1 KB, SBO = 2 KB).
 template <int BP, int MODE>
-__global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a, const __grid_constant__ CUtensorMap tmw) {
+    constexpr bool kTma = MODE != GEMV_LIST;
     static_assert(BP >= 2 && BP <= kTcN, "tcgen05 GEMV: batch 2..16");
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
@@ -74,7 +101,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
 
     if (tid == 0) {
         for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(&full[s], kTcProdWarps * 32);
+            mbar_init(&full[s], kTcProdWarps * 32);   // + the TMA bytes (expect_tx) when kTma
             mbar_init(&empty[s], 1);
         }
         mbar_init(accb, 1);
@@ -105,7 +132,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
         n_list = min(nrows, lo + rps) - lo;
         for (int t = tid; t < n_list; t += kTcThreads) lrow[t] = __ldg(a.rows + lo + t);
     } else {
-        const int rng = (a.d_in + a.n_splits - 1) / a.n_splits;
+        // (ranges in whole chunks: every chunk's 8-row value groups are 32-byte aligned in x)
+        const int rng = ((a.d_in + a.n_splits - 1) / a.n_splits + kTcChunk - 1) / kTcChunk * kTcChunk;
         lo = min(a.d_in, split * rng);
         n_list = min(a.d_in, lo + rng) - lo;
     }
@@ -121,7 +149,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
     if constexpr (MODE == GEMV_THRESH)
         if (tid < kTcProdWarps * 32 && pn < a.batch) prule = a.thr[pn];
     // raw inputs of this thread's 8 values of chunk c (loaded one chunk ahead)
+    // x rows 16-byte aligned: a thread's 8 consecutive values are two 16-byte loads (8 scalar
+    // loads, one 32-byte sector each, made the value staging L1-wavefront bound)
+    const bool xvec = MODE != GEMV_LIST && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) && (a.ldx & 3) == 0;
     auto load_raw = [&](int c, float (&r)[8]) {
+        if constexpr (MODE != GEMV_LIST) {
+            const int e0 = c * kTcChunk + pk8 * 8;
+            if (xvec && e0 + 8 <= n_list) {
+                float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+                if (pn < a.batch && pn < BP) {
+                    const float4* src = reinterpret_cast<const float4*>(a.x + (size_t)pn * a.ldx + lo + e0);
+                    q0 = __ldg(src);
+                    q1 = __ldg(src + 1);
+                }
+                r[0] = q0.x; r[1] = q0.y; r[2] = q0.z; r[3] = q0.w;
+                r[4] = q1.x; r[5] = q1.y; r[6] = q1.z; r[7] = q1.w;
+                return;
+            }
+        }
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
             const int e = c * kTcChunk + pk8 * 8 + h;
@@ -147,16 +192,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
     if (warp < kTcProdWarps) {
         // ---- producers: gather 64 weight rows x 128 columns, and the chunk's values -------------
         const int pt = tid;                                // 0..127
-        float nxt[8];
-        if (n_chunks > 0) load_raw(0, nxt);
-        for (int c = 0; c < n_chunks; ++c) {
-            float cur[8];
+        // the values are loaded kTcVPre chunks ahead (a register ring): with one chunk of
+        // look-ahead their L2 latency, not HBM, paced the ring (~1.4 us per 16 KB chunk)
+        float ring[kTcVPre][8];
 #pragma unroll
-            for (int h = 0; h < 8; ++h) cur[h] = nxt[h];
+        for (int j = 0; j < kTcVPre; ++j)
+            if (j < n_chunks) load_raw(j, ring[j]);
+        for (int c0 = 0; c0 < n_chunks; c0 += kTcVPre)
+#pragma unroll
+        for (int j = 0; j < kTcVPre; ++j) {
+            const int c = c0 + j;
+            if (c >= n_chunks) break;
+            float (&cur)[8] = ring[j];
             const int s = c % kTcStages;
             if (c >= kTcStages) mbar_wait_parity(&empty[s], ((c / kTcStages) & 1) ^ 1);
             unsigned char* st = smem + s * kTcStage;
             // A: 64 rows x 16 chunks of 16 bytes; thread pt takes chunks pt + 128 q
+            if constexpr (kTma) {
+                if (pt == 0 && !(a.tc_dbg & 4)) {
+                    mbar_expect_tx(&full[s], kTcABytes);
+                    tma_load_2d(st, &tmw, col0, lo + c * kTcChunk, &full[s]);
+                    tma_load_2d(st + kTcABytes / 2, &tmw, col0 + 64, lo + c * kTcChunk, &full[s]);
+                }
+            } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int u = pt + 128 * q;
@@ -169,25 +227,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
                 const bool valid = ok && col0 + cc * 8 < a.d_out && !(a.tc_dbg & 4);
                 cp_async16_zfill(dst, valid ? a.W + (size_t)row * a.ld + col0 + cc * 8 : a.W, valid);
             }
+            }
             // B: token n (0..15) x 8 consecutive rows (16 bytes of hi, 16 of lo) per thread
-            if (!(a.tc_dbg & 2)) {
+            if (a.tc_dbg & 16) {
+                const int off = (pn >> 3) * 1024 + (pn & 7) * 128 + ((pk8 ^ (pn & 7)) << 4);
+                *reinterpret_cast<uint4*>(st + kTcABytes + off) = make_uint4(0u, 0u, 0u, 0u);
+                *reinterpret_cast<uint4*>(st + kTcABytes + kTcBBytes + off) = make_uint4(0u, 0u, 0u, 0u);
+            } else if (!(a.tc_dbg & 2)) {
                 uint32_t hi[4], lw[4];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                     const float f0 = finish(c, 2 * h, cur[2 * h]), f1 = finish(c, 2 * h + 1, cur[2 * h + 1]);
-                    const uint16_t h0 = f2bf16_rne(f0), h1 = f2bf16_rne(f1);
-                    hi[h] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-                    lw[h] = (uint32_t)f2bf16_rne(f0 - bf16f(h0)) | ((uint32_t)f2bf16_rne(f1 - bf16f(h1)) << 16);
+                    // packed hardware RNE (cvt.rn.bf16x2: bit-identical to f2bf16_rne on finite values)
+                    hi[h] = cvt_bf16x2(f0, f1);
+                    lw[h] = cvt_bf16x2(f0 - __uint_as_float(hi[h] << 16), f1 - __uint_as_float(hi[h] & 0xffff0000u));
                 }
                 const int off = (pn >> 3) * 1024 + (pn & 7) * 128 + ((pk8 ^ (pn & 7)) << 4);
                 *reinterpret_cast<uint4*>(st + kTcABytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                 *reinterpret_cast<uint4*>(st + kTcABytes + kTcBBytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
-            fence_proxy_async_smem();   // the st.shared values, for the tensor core's async proxy
-            cp_async_mbar_arrive(&full[s]);
-            // the next chunk's values: issued after the fence (which would wait for them), in
-            // flight during the next slot wait
-            if (c + 1 < n_chunks && !(a.tc_dbg & 2)) load_raw(c + 1, nxt);
+            if (!(a.tc_dbg & 8)) fence_proxy_async_smem();   // the st.shared values, for the tensor core's async proxy
+            if constexpr (kTma)
+                mbar_arrive(&full[s]);
+            else
+                cp_async_mbar_arrive(&full[s]);
+            // chunk c + kTcVPre's values: issued after the fence (which would wait for them)
+            if (c + kTcVPre < n_chunks && !(a.tc_dbg & 2)) load_raw(c + kTcVPre, cur);
         }
     } else if (lane == 0) {
         // ---- MMA issuer ------------------------------------------------------------------------
@@ -201,12 +266,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
 #pragma unroll
             for (int ks = 0; ks < kTcChunk / 16; ++ks) {
                 if (16 * ks >= rows) break;
-                const uint64_t da = umma_desc_mn_sw128(st + ks * 4096, 1024, 2048);
+                const uint64_t da = kTma ? umma_desc_mn_sw128(st + ks * 2048, 8192, 1024)
+                                         : umma_desc_mn_sw128(st + ks * 4096, 1024, 2048);
                 const uint64_t dbh = umma_desc_sw128(st + kTcABytes + ks * 32);
                 const uint64_t dbl = umma_desc_sw128(st + kTcABytes + kTcBBytes + ks * 32);
                 if (!(a.tc_dbg & 1)) {
-                    umma_bf16(tmem, da, dbh, kTcIdesc, c > 0 || ks > 0);
-                    umma_bf16(tmem, da, dbl, kTcIdesc, true);
+                    if constexpr (kTcFused) {
+                        umma_bf16(tmem, da, dbh, kTcIdesc2, c > 0 || ks > 0);
+                    } else {
+                        umma_bf16(tmem, da, dbh, kTcIdesc, c > 0 || ks > 0);
+                        umma_bf16(tmem, da, dbl, kTcIdesc, true);
+                    }
                 }
             }
             umma_commit(&empty[s]);
@@ -226,7 +296,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(tmem + ((uint32_t)(32 * warp) << 16)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if constexpr (kTcFused) {   // columns 16-31: the lo halves
+            uint32_t w[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15}, [%16];"
+                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                  "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+                : "r"(tmem + ((uint32_t)(32 * warp) << 16) + 16u));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int b = 0; b < 16; ++b) v[b] = __float_as_uint(__uint_as_float(v[b]) + __uint_as_float(w[b]));
+        } else {
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         const int o = col0 + tid;
         if (o < a.d_out)
 #pragma unroll
@@ -251,29 +334,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
         return;
     }
     if (tid == 0) a.tickets[slice] = 0u;
-    if (tid < kTcCols) {
-        for (int b = 0; b < a.batch; ++b) {
-            unsigned long long* acc = a.acc + (size_t)b * a.acc_ld;
-            if (a.epi == EPI_SILU) {
-                // the 128-column slice is one gate|up block: 64 gate, then the matching 64 up
-                if (tid < kGuBlock && col0 + tid < a.d_out) {
-                    const float g = fix_to_f(__ldcg(acc + col0 + tid));
-                    const float u = fix_to_f(__ldcg(acc + col0 + tid + kGuBlock));
-                    acc[col0 + tid] = 0ull;
-                    acc[col0 + tid + kGuBlock] = 0ull;
-                    a.out[(size_t)b * a.out_ld + slice * kGuBlock + tid] = g / (1.0f + expf(-g)) * u;
+    // (every token's sums are read before any is written: 16 independent L2 reads instead of a
+    // chain of 16 round trips in the launch's tail)
+    if (a.epi == EPI_SILU) {
+        // the 128-column slice is one gate|up block: 64 gate, then the matching 64 up
+        if (tid < kGuBlock && col0 + tid < a.d_out) {
+            float g[BP], u[BP];
+#pragma unroll
+            for (int b = 0; b < BP; ++b)
+                if (b < a.batch) {
+                    const unsigned long long* acc = a.acc + (size_t)b * a.acc_ld + col0 + tid;
+                    g[b] = fix_to_f(__ldcg(acc));
+                    u[b] = fix_to_f(__ldcg(acc + kGuBlock));
                 }
-            } else {
-                const int o = col0 + tid;
-                if (o < a.d_out) {
-                    float v = fix_to_f(__ldcg(acc + o));
-                    acc[o] = 0ull;
-                    if (a.bias) v += bf16f(a.bias[o]);
-                    if (a.res) v = a.res[(size_t)b * a.res_ld + o] + v;
-                    a.out[(size_t)b * a.out_ld + o] = v;
+#pragma unroll
+            for (int b = 0; b < BP; ++b)
+                if (b < a.batch) {
+                    unsigned long long* acc = a.acc + (size_t)b * a.acc_ld + col0 + tid;
+                    acc[0] = 0ull;
+                    acc[kGuBlock] = 0ull;
+                    a.out[(size_t)b * a.out_ld + slice * kGuBlock + tid] = g[b] / (1.0f + expf(-g[b])) * u[b];
                 }
-            }
         }
+    } else if (tid < kTcCols && col0 + tid < a.d_out) {
+        const int o = col0 + tid;
+        float v[BP], r[BP];
+#pragma unroll
+        for (int b = 0; b < BP; ++b)
+            if (b < a.batch) {
+                v[b] = fix_to_f(__ldcg(a.acc + (size_t)b * a.acc_ld + o));
+                r[b] = a.res ? a.res[(size_t)b * a.res_ld + o] : 0.f;
+            }
+        const float bias = a.bias ? bf16f(a.bias[o]) : 0.f;
+#pragma unroll
+        for (int b = 0; b < BP; ++b)
+            if (b < a.batch) {
+                a.acc[(size_t)b * a.acc_ld + o] = 0ull;
+                float y = v[b];
+                if (a.bias) y += bias;
+                if (a.res) y = r[b] + y;
+                a.out[(size_t)b * a.out_ld + o] = y;
+            }
     }
     tl_stamp(a.tl, 4);
 }

@@ -306,7 +306,8 @@ bool use_tc_gemv(int bp) {
 GemvPlan plan_gemv_tc(int64_t d_out, int64_t rows_src) {
     GemvPlan p;
     p.n_slices = (int)((d_out + kTcCols - 1) / kTcCols);
-    const int target = sm_count() * 2;
+    static const int tc_target_pct = env_int("LAROSA_TC_TARGET_PCT", 200);   // CTAs per SM x 100
+    const int target = sm_count() * tc_target_pct / 100;
     const int by_target = std::max(1, target / p.n_slices);
     const int by_rows = (int)std::max<int64_t>(1, rows_src / 64);
     const int by_cap = (int)std::max<int64_t>(1, (rows_src + 8191) / 8192);   // <= 8192 rows per CTA
@@ -315,6 +316,7 @@ GemvPlan plan_gemv_tc(int64_t d_out, int64_t rows_src) {
     p.smem = gemv_tc_smem_bytes(p.list_cap);
     return p;
 }
+bool make_w_mn_map(CUtensorMap* m, const void* W, int64_t d_in, int64_t d_out, int64_t ld);   // (fold section)
 template <int BP, int MODE>
 larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
     const int64_t rows_src = MODE == GEMV_LIST ? (a.nrows_dev ? a.d_in : a.nrows) : a.d_in;
@@ -331,7 +333,11 @@ larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
     aa.list_cap = p.list_cap;
     static const int tc_dbg = env_int("LAROSA_TC_DBG", 0);   // profiling only
     aa.tc_dbg = tc_dbg;
-    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kTcThreads), p.smem, st, aa), "gemv_tc launch");
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    if (MODE != GEMV_LIST && !make_w_mn_map(&tm, a.W, a.d_in, a.d_out, a.ld))
+        return fail(LAROSA_ECUDA, "gemv_tc: cuTensorMapEncodeTiled failed for the weight matrix");
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kTcThreads), p.smem, st, aa, tm), "gemv_tc launch");
 }
 template <int BP>
 larosa_status launch_gemv_tc(const GemvArgs& a, cudaStream_t st) {
@@ -799,6 +805,19 @@ bool make_kmajor_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, 
     cuuint32_t box[2] = {(cuuint32_t)kFoldBK, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// row-major bf16 weights [d_in][ld] (d_out columns used): boxes of 64 columns x 64 rows, 128-byte
+// swizzle; rows >= d_in and columns >= d_out read as zero (gemv_tc DENSE / THRESH)
+bool make_w_mn_map(CUtensorMap* m, const void* W, int64_t d_in, int64_t d_out, int64_t ld) {
+    PFN_encodeTiled_t enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)d_out, (cuuint64_t)d_in};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(W), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
