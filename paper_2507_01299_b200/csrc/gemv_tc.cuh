@@ -4,15 +4,16 @@
 //   acc[b][o] += fix( sum_{r in rows} val(r, b) * W[row(r)][o] )      (same contract as gemv.cuh)
 //
 // As an MMA  D[M = 128 columns][N = 16 tokens] += A[M][K = kept rows] . B[K][N]:
-//   A = the gathered weight rows, MN-major (a row's 128 columns are contiguous in W): each
-//       64-row chunk is copied with per-thread cp.async into the canonical 128-byte-swizzled
+//   A = the weight rows, MN-major (a row's 128 columns are contiguous in W): for contiguous
+//       rows (DENSE, THRESH) each 64-row chunk is two TMA boxes (128-byte swizzle); for gathered
+//       rows (LIST) it is copied with per-thread cp.async into the canonical 128-byte-swizzled
 //       MN-major layout (atoms of 8 rows x 64 columns; next 64 columns +1 KB, next 8 rows +2 KB);
 //       rows past the list are zero-filled (src-size 0);
-//   B = the tokens' values, K-major, split into bf16 hi + lo (two MMAs into the same fp32
-//       accumulator keep ~16 mantissa bits of the fp32 activations), written with st.shared;
-//   D = 16 fp32 TMEM columns x 128 lanes.
+//   B = the tokens' values, K-major, split into bf16 hi + lo (~16 mantissa bits of the fp32
+//       activations), written with st.shared as the two 16-token halves of one N = 32 operand;
+//   D = 32 fp32 TMEM columns x 128 lanes (hi products in 0-15, lo in 16-31, summed on read-out).
 // Warps 0-3 produce (gather + values) into a 4-stage ring whose stages complete through
-// cp.async.mbarrier.arrive; one thread of warp 4 issues tcgen05.mma (M = 128, N = 16, K = 16)
+// cp.async.mbarrier.arrive; one thread of warp 4 issues tcgen05.mma (M = 128, N = 32 = hi | lo, K = 16)
 // and frees stages with tcgen05.commit; warps 0-3 then tcgen05.ld the accumulator (lane =
 // column) and add it into the 64-bit fixed-point accumulators; the last split CTA of a slice
 // finalises it (ticket), as in gemv.cuh.  Row sources: THRESH (every row of the CTA's input

@@ -350,7 +350,7 @@ larosa_status launch_gemv_tc(const GemvArgs& a, cudaStream_t st) {
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
-    if (use_tc_gemv(bp) && a.mode != GEMV_SELECT && (a.epi != EPI_SILU || true)) {
+    if (use_tc_gemv(bp) && a.mode != GEMV_SELECT) {
         if (bp == 8) return launch_gemv_tc<8>(a, st);
         return launch_gemv_tc<16>(a, st);
     }
