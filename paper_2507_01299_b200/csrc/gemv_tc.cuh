@@ -28,7 +28,13 @@ namespace larosa {
 constexpr int kTcCols = 128;         // columns per CTA (UMMA M)
 constexpr int kTcN = 16;             // tokens (UMMA N; batch padded to 16)
 constexpr int kTcChunk = 64;         // kept rows per ring stage (UMMA K = 16 per instruction)
-constexpr int kTcStages = 4;
+#ifndef LAROSA_TC_STAGES
+#define LAROSA_TC_STAGES 2
+#endif
+// ring depth x CTAs per SM (LLaMA3-8B decode, B = 16, p = 0.4: 4 stages x 2 CTAs 7.49 ms, 3 x 3 7.25,
+// 2 x 4 6.48; 6-10 stages x 1 CTA 11.1):
+// per-CTA work, not bytes in flight, paces the stream, so CTAs per SM matter most
+constexpr int kTcStages = LAROSA_TC_STAGES;
 constexpr int kTcProdWarps = 4;
 #ifndef LAROSA_TC_VPRE
 #define LAROSA_TC_VPRE 1

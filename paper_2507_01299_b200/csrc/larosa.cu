@@ -306,7 +306,7 @@ bool use_tc_gemv(int bp) {
 GemvPlan plan_gemv_tc(int64_t d_out, int64_t rows_src) {
     GemvPlan p;
     p.n_slices = (int)((d_out + kTcCols - 1) / kTcCols);
-    static const int tc_target_pct = env_int("LAROSA_TC_TARGET_PCT", 200);   // CTAs per SM x 100
+    static const int tc_target_pct = env_int("LAROSA_TC_TARGET_PCT", 400);   // CTAs per SM x 100
     const int target = sm_count() * tc_target_pct / 100;
     const int by_target = std::max(1, target / p.n_slices);
     const int by_rows = (int)std::max<int64_t>(1, rows_src / 64);
@@ -320,7 +320,11 @@ bool make_w_mn_map(CUtensorMap* m, const void* W, int64_t d_in, int64_t d_out, i
 template <int BP, int MODE>
 larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
     const int64_t rows_src = MODE == GEMV_LIST ? (a.nrows_dev ? a.d_in : a.nrows) : a.d_in;
-    const GemvPlan p = plan_gemv_tc(a.d_out, rows_src);
+    GemvPlan p = plan_gemv_tc(a.d_out, rows_src);
+    if (MODE != GEMV_LIST) {   // contiguous rows: no row list in shared memory
+        p.list_cap = 0;
+        p.smem = gemv_tc_smem_bytes(p.list_cap);
+    }
     auto kern = gemv_tc_kernel<BP, MODE>;
     static bool attr_done = false;
     if (!attr_done) {
