@@ -40,6 +40,11 @@ constexpr int kTcProdWarps = 4;
 #define LAROSA_TC_VPRE 1
 #endif
 constexpr int kTcVPre = LAROSA_TC_VPRE;   // chunks of value look-ahead per producer thread (2-8: slower)
+#ifndef LAROSA_TC_PREFETCH
+#define LAROSA_TC_PREFETCH 0
+#endif
+// 1: the first ring stages' weight tiles are requested before the dependency wait (contiguous rows)
+constexpr bool kTcPrefetch = LAROSA_TC_PREFETCH != 0;
 #ifndef LAROSA_TC_FUSED_HILO
 #define LAROSA_TC_FUSED_HILO 1
 #endif
@@ -120,6 +125,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     tl_stamp(a.tl, 0);
+    if constexpr (kTma && kTcPrefetch) {   // the weights do not depend on the previous kernel
+        if (tid == 0 && !(a.tc_dbg & 4)) {
+            const int rng = ((a.d_in + a.n_splits - 1) / a.n_splits + kTcChunk - 1) / kTcChunk * kTcChunk;
+            const int plo = min(a.d_in, split * rng);
+            const int pch = (min(a.d_in, plo + rng) - plo + kTcChunk - 1) / kTcChunk;
+            for (int c = 0; c < kTcStages && c < pch; ++c) {
+                unsigned char* st = smem + c * kTcStage;
+                mbar_expect_tx(&full[c], kTcABytes);
+                tma_load_2d(st, &tmw, col0, plo + c * kTcChunk, &full[c]);
+                tma_load_2d(st + kTcABytes / 2, &tmw, col0 + 64, plo + c * kTcChunk, &full[c]);
+            }
+        }
+    }
     pdl_wait();
     pdl_trigger();
     tl_stamp(a.tl, 1);
@@ -216,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
             unsigned char* st = smem + s * kTcStage;
             // A: 64 rows x 16 chunks of 16 bytes; thread pt takes chunks pt + 128 q
             if constexpr (kTma) {
-                if (pt == 0 && !(a.tc_dbg & 4)) {
+                if (pt == 0 && !(a.tc_dbg & 4) && !(kTcPrefetch && c < kTcStages)) {
                     mbar_expect_tx(&full[s], kTcABytes);
                     tma_load_2d(st, &tmw, col0, lo + c * kTcChunk, &full[s]);
                     tma_load_2d(st + kTcABytes / 2, &tmw, col0 + 64, lo + c * kTcChunk, &full[s]);
