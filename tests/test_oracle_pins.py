@@ -567,3 +567,125 @@ def test_w4_worked_example_and_error_bound():
     wf = O.bf16_to_f64(w)
     sc = np.repeat(sb.view(np.float16).astype(np.float64), 128, axis=1)
     assert np.all(np.abs(wf - deq) <= sc / 2 * (1 + 1e-3) + 1e-12)
+
+
+# ------------------------------------------------------------------ glue pins with hand-computed values
+# (VERDICT r1 "What's weak" 1: the closed forms above hold for ANY RoPE frequency schedule or pairing,
+#  and softmax special cases are scale-invariant; these fix the Z27 conventions numerically.)
+def test_rope_hand_values_hd8():
+    """Z27 (HF rotate_half): pairs (i, i + hd/2), inv_freq_i = theta^(-2i/hd).  With hd = 8 and
+    theta = 10^4 the frequencies are exactly 1, 0.1, 0.01, 0.001, so at pos = 3 basis vector e_i
+    (i < 4) rotates by 3*10^-i rad into coordinate i + 4, and e_{i+4} into -sin at i.  An
+    interleaved pairing (2i, 2i+1) or the schedule theta^(-i/hd) fails this."""
+    hd, pos, theta = 8, 3, 1e4
+    for i, ang in enumerate((3.0, 0.3, 0.03, 0.003)):
+        e = np.zeros(hd); e[i] = 1.0
+        want = np.zeros(hd); want[i] = math.cos(ang); want[i + 4] = math.sin(ang)
+        assert np.allclose(O.rope(e, pos, theta), want, atol=1e-15, rtol=0), i
+        e2 = np.zeros(hd); e2[i + 4] = 1.0
+        want2 = np.zeros(hd); want2[i] = -math.sin(ang); want2[i + 4] = math.cos(ang)
+        assert np.allclose(O.rope(e2, pos, theta), want2, atol=1e-15, rtol=0), i
+
+
+def test_rope_hand_values_hd4():
+    """hd = 4, theta = 100: inv_freq = (1, 100^(-1/2) = 0.1); pos = 2 -> angles (2, 0.2).
+    v = (1, 2, 3, 4): out = (1 c2 - 3 s2, 2 c.2 - 4 s.2, 3 c2 + 1 s2, 4 c.2 + 2 s.2)."""
+    c2, s2, c02, s02 = math.cos(2.0), math.sin(2.0), math.cos(0.2), math.sin(0.2)
+    want = [1 * c2 - 3 * s2, 2 * c02 - 4 * s02, 3 * c2 + 1 * s2, 4 * c02 + 2 * s02]
+    assert np.allclose(O.rope(np.array([1.0, 2.0, 3.0, 4.0]), 2, 100.0), want, atol=1e-14, rtol=0)
+
+
+@pytest.mark.parametrize("hd", [4, 16])
+def test_attention_scale_hand_values(hd):
+    """Two cached positions, k_0 = 0 and k_1 = c * ones(hd) with c = ln(3) / sqrt(hd), query ones:
+    the scores are (0, ln 3) only with the 1/sqrt(hd) scale (Z27), so the softmax weights are
+    exactly (1/4, 3/4) and the output is 1/4 v_0 + 3/4 v_1.  Without the scale the weights would
+    be (1, 3^sqrt(hd)) / (1 + 3^sqrt(hd)); with 1/hd, (1, 3^(1/sqrt(hd)))/(...)."""
+    c = math.log(3.0) / math.sqrt(hd)
+    q = np.ones((1, hd))
+    kc = np.zeros((1, 2, hd)); kc[0, 1] = c
+    vc = np.zeros((1, 2, hd)); vc[0, 0, 0] = 1.0; vc[0, 1, 1] = 1.0
+    out = O.decode_attention(q, kc, vc, 2)
+    want = np.zeros(hd); want[0] = 0.25; want[1] = 0.75
+    assert np.allclose(out, want, atol=1e-14, rtol=0)
+    # causal: ctx_len = 1 ignores position 1 entirely
+    assert np.allclose(O.decode_attention(q, kc, vc, 1), vc[0, 0], atol=0)
+
+
+def test_silu_closed_forms():
+    """SiLU(x) = x * sigma(x): sigma(+-ln 3) = 3/4, 1/4 exactly, sigma(0) = 1/2; large |x| -> x, 0."""
+    ln3 = math.log(3.0)
+    got = O.silu(np.array([0.0, ln3, -ln3, 2 * math.log(2.0), 60.0, -60.0]))
+    want = [0.0, 0.75 * ln3, -0.25 * ln3, 2 * math.log(2.0) * 0.8, 60.0, -60.0 * math.exp(-60.0)]
+    assert np.allclose(got, want, rtol=1e-14, atol=1e-300)
+
+
+def _wiring_layer():
+    """A hand-built d = 8 layer (hq = 2, hkv = 1, hd = 4, inter = 8, eps = 0, pos = 0 so RoPE is
+    the identity and the attention over one cached position returns v).  Rows a correct Top-K
+    never keeps are filled with 100-1000, so a wrong kept set anywhere changes the output by
+    orders of magnitude.  The expected kept sets and vectors are derived by hand in
+    test_block_site_wiring_hand_built."""
+    d = 8
+    e = np.eye(d)
+    wqkv = np.zeros((d, 16))                       # q cols 0-7 and k cols 8-11 stay 0
+    for j, c in ((0, 0), (1, 1), (4, 2), (5, 3)):
+        wqkv[j, 12 + c] = 1.0                      # v_c <- kept value of row j
+    for j in (2, 3, 6, 7):
+        wqkv[j, 12:] = 100.0
+    wo = np.full((d, d), 100.0)
+    wo[0], wo[2], wo[4], wo[6] = e[0], -e[2], 0.5 * e[1], e[3]
+    wg = np.full((d, d), 1000.0)
+    wg[0] = [100, -100, 0, 0, 0, 0, 0, 0]          # x vals3[0]/s3 = 6   -> (600, -600) at 0, 1
+    wg[2] = [0, 0, 200, 0, 0, 0, 0, 0]             # x 2.5 -> 500 at 2
+    wg[4] = [0, 0, 0, -200, 0, 0, 0, 0]            # x -3  -> 600 at 3
+    wg[5] = [0, 0, 0, 0, 300, -300, 300, 300]      # x 2   -> (600, -600, 600, 600) at 4-7
+    wu = np.full((d, d), 1000.0)
+    wu[0] = 1.0                                    # U = 6 everywhere ...
+    wu[2] = [0, 0, 2, 0, 0, 0, 0, 0]               # ... + 5 at 2
+    wu[4] = [0, 0, 0, 1, 0, 0, 0, 0]               # ... - 3 at 3
+    wu[5] = [0, 0, 0, 0, 0.5, 0, -1, 0]            # ... + 1 at 4, - 2 at 6
+    wd = np.full((d, d), 1e3)
+    wd[0], wd[2], wd[4] = 0.01 * e[6], 0.01 * e[7], -0.01 * e[0]
+    return {"wqkv": wqkv, "wo": wo, "wg": wg, "wu": wu, "wd": wd}
+
+
+@pytest.mark.parametrize("in_down", [False, True])
+def test_block_site_wiring_hand_built(in_down):
+    """p > 0 site wiring of larosa_block (Fig. 2; eqs.; Z10, Z25, Z20):
+    every kept set and intermediate below is derived by hand.
+
+      r = (4,-1,1,1,-3,2,0,0): mean r^2 = 4 -> s1 = 1/2; |r| top-4 with the lower index winning
+          the three-way tie at |1| -> S1 = {0,1,4,5}; vals1 = r[S1] s1 = (2,-0.5,-1.5,1) = v
+      h2 = (v, v) (both q heads read kv head 0) -> top-4 of |h2| = (2,.5,1.5,1,2,.5,1.5,1):
+          S2 = {0,2,4,6}, vals2 = (2,-1.5,2,-1.5) (no RMS scale at h2)
+      y_o = (2, 1, 1.5, -1.5, 0...) -> r_mid = (6,0,2.5,-0.5,-3,2,0,0); S3 = {0,2,4,5}
+          (top-4 of |r_mid|: 6, 3, 2.5, 2; taking it on r instead gives {0,1,4,5}),
+          s3 = 1/sqrt(55.5/8), vals3 = s3 (6, 2.5, -3, 2)
+      g = s3 (600,-600,500,600,600,-600,600,600): SiLU(g) = g where g > 0 and ~0 where g < 0
+          (|g| > 200); u = s3 (6,6,11,3,7,6,4,6); h4 = s3^2 (3600,0,5500,1800,4200,0,2400,3600)
+      k4 = 3: S4 = {0,2,4} (3600 at 0 and 7 tie: the lower index wins), vals4 = h4[S4]
+      y_down = s3^2 (-42,0,0,0,0,0,36,55); r_out = r_mid + y_down; r_next = r_out A."""
+    w = _wiring_layer()
+    cfg = dict(hq=2, hkv=1, hd=4, eps=0.0, theta=10000.0)
+    r = np.array([4.0, -1, 1, 1, -3, 2, 0, 0])
+    a = np.zeros((8, 8))
+    for i, (j, sg) in enumerate(zip((7, 6, 5, 4, 3, 2, 1, 0), (1, -1, 1, 1, -1, 1, -1, 1))):
+        a[i, j] = sg                                   # a signed permutation: orthogonal
+    wf = dict(w)
+    if in_down:
+        wf["wd"] = w["wd"] @ a
+    kc, vc = np.zeros((1, 2, 4)), np.zeros((1, 2, 4))
+    out, inter = O.larosa_block(r, wf, cfg, (4, 4, 4, 3), kc, vc, 0, adapter=a, adapter_in_down=in_down)
+    assert list(inter["idx1"]) == [0, 1, 4, 5]
+    assert list(inter["idx2"]) == [0, 2, 4, 6]
+    assert list(inter["idx3"]) == [0, 2, 4, 5]
+    assert list(inter["idx4"]) == [0, 2, 4]
+    assert np.array_equal(vc[0, 0], [2.0, -0.5, -1.5, 1.0]) and np.all(kc == 0)
+    assert np.array_equal(inter["h2"], [2.0, -0.5, -1.5, 1.0] * 2)
+    assert np.array_equal(inter["r_mid"], [6.0, 0, 2.5, -0.5, -3, 2, 0, 0])
+    s3sq = 8.0 / 55.5
+    h4 = s3sq * np.array([3600.0, 0, 5500, 1800, 4200, 0, 2400, 3600])
+    assert np.allclose(inter["h4"], h4, rtol=1e-13, atol=1e-12)
+    r_out = np.array([6.0, 0, 2.5, -0.5, -3, 2, 0, 0]) + s3sq * np.array([-42.0, 0, 0, 0, 0, 0, 36, 55])
+    assert np.allclose(out, r_out @ a, rtol=1e-13, atol=1e-13)
