@@ -84,8 +84,8 @@ larosa_status larosa_solve_alpha(double alpha1, double alpha3, double m,
  *  side = LAROSA_RIGHT_Q : Wout = W Q.  W [rows = d_in][cols = d], Q [d][d]; gamma
  *      must be NULL.  Used for W_o and W_down so the block output stays in Q_l's
  *      basis (Z21).
- *  The residual adapter A_l = Q_l^T Q_{l+1} is LEFT_QT with Q = Q_l and
- *  W = Q_{l+1} rounded to bf16 (the runtime adapter is bf16 anyway).
+ *  (The residual adapter A_l = Q_l^T Q_{l+1}, has its own call below that keeps
+ *  both fp32 factors split: larosa_residual_adapter.)
  *  W, Wout bf16 row-major with leading dimension `cols`; Wout must not alias W.
  *  Arithmetic: Q (times gamma) is split into bf16 hi + lo parts, the products run on
  *  the tcgen05 tensor cores with fp32 accumulation in TMEM, and Wout is rounded to
@@ -96,6 +96,21 @@ size_t larosa_fold_workspace_size(int64_t rows, int64_t cols, int side);
 larosa_status larosa_fold_rotation(const float* Q, const float* gamma, const uint16_t* W,
                                    uint16_t* Wout, int64_t rows, int64_t cols, int side,
                                    void* ws, size_t ws_bytes, larosa_stream_t stream);
+
+/* ------------------------------------------------------------------------------
+ * Residual adapter A_l = Q_l^T Q_{l+1}   ("residual adapters").
+ *  Q_l, Q_next: fp32 [d][d] row-major (device); A: bf16 [d][d] row-major (device,
+ *  caller-owned, must not alias either factor).  BOTH factors are split into bf16
+ *  hi + lo parts and the three significant products (hi.hi + lo.hi + hi.lo) run on
+ *  the tcgen05 tensor cores into one fp32 TMEM accumulator; A is rounded to bf16 (RNE)
+ *  ONCE -- unlike the LEFT_QT fold of a bf16-rounded Q_{l+1}, which rounds twice.
+ *  d < 128 or d % 128 != 0 uses an fp32 CUDA-core kernel (same single rounding).
+ *  d must be a multiple of 64 (EUNSUPPORTED).  Workspace: larosa_residual_adapter_
+ *  workspace_size(d) bytes (scratch; no zero-fill needed).
+ * ------------------------------------------------------------------------------ */
+size_t larosa_residual_adapter_workspace_size(int64_t d);
+larosa_status larosa_residual_adapter(const float* Q_l, const float* Q_next, uint16_t* A, int64_t d,
+                                      void* ws, size_t ws_bytes, larosa_stream_t stream);
 
 /* Pack separate gate and up weights Wg, Wu [d][inter] into the fused layout the layer
  * uses: Wgu [d][2*inter] with column block t of width 2*LAROSA_GU_BLOCK holding

@@ -198,10 +198,12 @@ namespace larosa {
 //   RIGHT : C[r][j] = sum_m W[r][m] * Q[m][j]                (M = rows, N = K = d)
 // 64x64 output tile per CTA, K step 16, 256 threads x (4x4) outputs, bf16 RNE store.
 // ------------------------------------------------------------------------------------------
+// Wf (LEFT only, may be NULL): an fp32 right factor used instead of the bf16 W (the residual
+// adapter Q_l^T Q_{l+1} with both factors in fp32).
 template <bool LEFT>
 __global__ void __launch_bounds__(256) fold_simt_kernel(const float* __restrict__ Q, const float* __restrict__ gamma,
                                                         const uint16_t* __restrict__ W, uint16_t* __restrict__ out,
-                                                        int M, int N, int K) {
+                                                        int M, int N, int K, const float* __restrict__ Wf) {
     __shared__ float As[16][64 + 4];
     __shared__ float Bs[16][64 + 4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(256) fold_simt_kernel(const float* __restrict_
                 // A[m][kg] = Q[kg][m] * gamma[kg]
                 if (m < M && kg < K) av = Q[(size_t)kg * M + m] * (gamma ? gamma[kg] : 1.f);
                 const int n = n0 + mm;
-                if (n < N && kg < K) bv = bf16f(W[(size_t)kg * N + n]);
+                if (n < N && kg < K) bv = Wf ? Wf[(size_t)kg * N + n] : bf16f(W[(size_t)kg * N + n]);
             } else {
                 if (m < M && kg < K) av = bf16f(W[(size_t)m * K + kg]);
                 const int n = n0 + mm;

@@ -160,8 +160,7 @@ struct GemvArgs {
     int d2;
     int n_splits2;
     unsigned long long* tl;            // debug timeline slot (5 x u64) or null
-    int sel_dbg;                       // profiling flags (unused by the kernels at present)
-    int tc_dbg;                        // profiling (tcgen05 GEMV): 1 skip MMAs, 2 skip values, 4 skip A copies
+    int tc_dbg;                        // profiling (tcgen05 GEMV, -DLAROSA_TC_DEBUG builds only)
     // batch-1 split-K reduction through distributed shared memory: the gridDim.y CTAs of a
     // slice form one thread-block cluster (cluster != 0); rank 0 sums the CTAs' fp32 column
     // partials in rank order and finalises the slice itself (no global accumulators, no ticket)

@@ -12,7 +12,7 @@
 //   B = the tokens' values, K-major, split into bf16 hi + lo (~16 mantissa bits of the fp32
 //       activations), written with st.shared as the two 16-token halves of one N = 32 operand;
 //   D = 32 fp32 TMEM columns x 128 lanes (hi products in 0-15, lo in 16-31, summed on read-out).
-// Warps 0-3 produce (gather + values) into a 4-stage ring whose stages complete through
+// Warps 0-3 produce (gather + values) into a kTcStages-deep ring (2 by default) whose stages complete through
 // cp.async.mbarrier.arrive; one thread of warp 4 issues tcgen05.mma (M = 128, N = 32 = hi | lo, K = 16)
 // and frees stages with tcgen05.commit; warps 0-3 then tcgen05.ld the accumulator (lane =
 // column) and add it into the 64-bit fixed-point accumulators; the last split CTA of a slice
@@ -52,6 +52,21 @@ constexpr bool kTcPrefetch = LAROSA_TC_PREFETCH != 0;
 // contiguous in the stage): half the MMA instructions, each reading the A tile once
 constexpr bool kTcFused = LAROSA_TC_FUSED_HILO != 0;
 constexpr int kTcThreads = (kTcProdWarps + 1) * 32;
+// Profiling switches (1 skip MMAs, 2 skip values, 4 skip A copies, 8 skip the proxy fence, 16
+// constant values) exist only in a -DLAROSA_TC_DEBUG build; the shipped library compiles them out.
+#ifdef LAROSA_TC_DEBUG
+__device__ __forceinline__ int tc_dbg_flags(const GemvArgs& a) { return a.tc_dbg; }
+#else
+__device__ __forceinline__ int tc_dbg_flags(const GemvArgs&) { return 0; }
+#endif
+// The input-row range [lo, lo + n) of split `split` for contiguous rows (DENSE, THRESH): whole
+// 64-row chunks, so every chunk's 8-row value groups are 32-byte aligned in x.  The weight
+// prefetch and the producer loop both use it, so a stage's expect_tx always matches its TMA.
+__device__ __forceinline__ void tc_split_range(int d_in, int n_splits, int split, int& lo, int& n) {
+    const int rng = ((d_in + n_splits - 1) / n_splits + kTcChunk - 1) / kTcChunk * kTcChunk;
+    lo = min(d_in, split * rng);
+    n = min(d_in, lo + rng) - lo;
+}
 constexpr int kTcABytes = kTcCols * kTcChunk * 2;              // 16 KB
 constexpr int kTcBBytes = kTcN * kTcChunk * 2;                 // 2 KB (hi, and again lo)
 constexpr int kTcStage = kTcABytes + 2 * kTcBBytes;            // 20 KB
@@ -126,10 +141,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
     }
     tl_stamp(a.tl, 0);
     if constexpr (kTma && kTcPrefetch) {   // the weights do not depend on the previous kernel
-        if (tid == 0 && !(a.tc_dbg & 4)) {
-            const int rng = ((a.d_in + a.n_splits - 1) / a.n_splits + kTcChunk - 1) / kTcChunk * kTcChunk;
-            const int plo = min(a.d_in, split * rng);
-            const int pch = (min(a.d_in, plo + rng) - plo + kTcChunk - 1) / kTcChunk;
+        if (tid == 0 && !(tc_dbg_flags(a) & 4)) {
+            int plo, pn_rows;
+            tc_split_range(a.d_in, a.n_splits, split, plo, pn_rows);
+            const int pch = (pn_rows + kTcChunk - 1) / kTcChunk;
             for (int c = 0; c < kTcStages && c < pch; ++c) {
                 unsigned char* st = smem + c * kTcStage;
                 mbar_expect_tx(&full[c], kTcABytes);
@@ -157,10 +172,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
         n_list = min(nrows, lo + rps) - lo;
         for (int t = tid; t < n_list; t += kTcThreads) lrow[t] = __ldg(a.rows + lo + t);
     } else {
-        // (ranges in whole chunks: every chunk's 8-row value groups are 32-byte aligned in x)
-        const int rng = ((a.d_in + a.n_splits - 1) / a.n_splits + kTcChunk - 1) / kTcChunk * kTcChunk;
-        lo = min(a.d_in, split * rng);
-        n_list = min(a.d_in, lo + rng) - lo;
+        tc_split_range(a.d_in, a.n_splits, split, lo, n_list);
     }
     __syncthreads();
     tl_stamp(a.tl, 2);
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
             unsigned char* st = smem + s * kTcStage;
             // A: 64 rows x 16 chunks of 16 bytes; thread pt takes chunks pt + 128 q
             if constexpr (kTma) {
-                if (pt == 0 && !(a.tc_dbg & 4) && !(kTcPrefetch && c < kTcStages)) {
+                if (pt == 0 && !(tc_dbg_flags(a) & 4) && !(kTcPrefetch && c < kTcStages)) {
                     mbar_expect_tx(&full[s], kTcABytes);
                     tma_load_2d(st, &tmw, col0, lo + c * kTcChunk, &full[s]);
                     tma_load_2d(st + kTcABytes / 2, &tmw, col0 + 64, lo + c * kTcChunk, &full[s]);
@@ -249,16 +261,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
                 const int row = !ok ? 0 : (MODE == GEMV_LIST ? lrow[e] : lo + e);
                 const int mg = cc >> 3, c8 = cc & 7;       // 64-column group, chunk within it
                 unsigned char* dst = st + ((r >> 3) * 2 + mg) * 1024 + (r & 7) * 128 + ((c8 ^ (r & 7)) << 4);
-                const bool valid = ok && col0 + cc * 8 < a.d_out && !(a.tc_dbg & 4);
+                const bool valid = ok && col0 + cc * 8 < a.d_out && !(tc_dbg_flags(a) & 4);
                 cp_async16_zfill(dst, valid ? a.W + (size_t)row * a.ld + col0 + cc * 8 : a.W, valid);
             }
             }
             // B: token n (0..15) x 8 consecutive rows (16 bytes of hi, 16 of lo) per thread
-            if (a.tc_dbg & 16) {
+            if (tc_dbg_flags(a) & 16) {
                 const int off = (pn >> 3) * 1024 + (pn & 7) * 128 + ((pk8 ^ (pn & 7)) << 4);
                 *reinterpret_cast<uint4*>(st + kTcABytes + off) = make_uint4(0u, 0u, 0u, 0u);
                 *reinterpret_cast<uint4*>(st + kTcABytes + kTcBBytes + off) = make_uint4(0u, 0u, 0u, 0u);
-            } else if (!(a.tc_dbg & 2)) {
+            } else if (!(tc_dbg_flags(a) & 2)) {
                 uint32_t hi[4], lw[4];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
@@ -271,13 +283,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
                 *reinterpret_cast<uint4*>(st + kTcABytes + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                 *reinterpret_cast<uint4*>(st + kTcABytes + kTcBBytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
-            if (!(a.tc_dbg & 8)) fence_proxy_async_smem();   // the st.shared values, for the tensor core's async proxy
+            if (!(tc_dbg_flags(a) & 8)) fence_proxy_async_smem();   // the st.shared values, for the tensor core's async proxy
             if constexpr (kTma)
                 mbar_arrive(&full[s]);
             else
                 cp_async_mbar_arrive(&full[s]);
             // chunk c + kTcVPre's values: issued after the fence (which would wait for them)
-            if (c + kTcVPre < n_chunks && !(a.tc_dbg & 2)) load_raw(c + kTcVPre, cur);
+            if (c + kTcVPre < n_chunks && !(tc_dbg_flags(a) & 2)) load_raw(c + kTcVPre, cur);
         }
     } else if (lane == 0) {
         // ---- MMA issuer ------------------------------------------------------------------------
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
                                          : umma_desc_mn_sw128(st + ks * 4096, 1024, 2048);
                 const uint64_t dbh = umma_desc_sw128(st + kTcABytes + ks * 32);
                 const uint64_t dbl = umma_desc_sw128(st + kTcABytes + kTcBBytes + ks * 32);
-                if (!(a.tc_dbg & 1)) {
+                if (!(tc_dbg_flags(a) & 1)) {
                     if constexpr (kTcFused) {
                         umma_bf16(tmem, da, dbh, kTcIdesc2, c > 0 || ks > 0);
                     } else {

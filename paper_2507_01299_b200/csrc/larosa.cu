@@ -24,6 +24,8 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <mutex>
+#include <set>
+#include <tuple>
 
 using namespace larosa;
 
@@ -93,11 +95,28 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-// Opt a kernel in to > 48 KB dynamic shared memory once per process (per function).
+// Function attributes are per device context: set each (kernel, device, attribute) once, under a
+// lock (calls are re-entrant and a process may drive several GPUs).
+cudaError_t set_func_attr_once(const void* kern, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(kern, dev, (int)attr, value);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, attr, value);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
+
+// Opt a kernel in to > 48 KB dynamic shared memory (once per kernel and device).
 template <typename K>
 cudaError_t allow_smem(K kern, size_t bytes) {
     if (bytes <= 48 * 1024) return cudaSuccess;
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return set_func_attr_once(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)bytes);
 }
 
 // ============================================================================== workspace
@@ -236,15 +255,9 @@ GemvPlan plan_gemv_comp(int64_t d_out, int64_t k, int64_t d_in, int64_t d2) {
 template <int BP, int MODE>
 larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t st) {
     auto kern = gemv_kernel<BP, MODE>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv)"));
-        attr_done = true;
-    }
+    LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv)"));
     if (p.smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "gemv: shared memory plan %zu B too large", p.smem);
     GemvArgs aa = a;
-    static const int sel_dbg = env_int("LAROSA_SEL_DBG", 0);   // profiling only
-    aa.sel_dbg = sel_dbg;
     static const int late = env_int("LAROSA_PDL_LATE", 0);    // tuning
     aa.late_trigger = late;
     aa.n_splits = p.n_splits;
@@ -257,12 +270,9 @@ larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     aa.cluster = 0;
     if (MODE == GEMV_SELECT && BP == 1 && gemv_cluster_enabled() && ny >= 2 && ny <= kMaxGemvCluster &&
         a.batch == 1) {
-        static bool np_done = false;
-        if (!np_done) {
-            LAROSA_TRY(cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                                  "cudaFuncSetAttribute(non-portable cluster)"));
-            np_done = true;
-        }
+        LAROSA_TRY(cuda_check(set_func_attr_once(reinterpret_cast<const void*>(kern),
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                              "cudaFuncSetAttribute(non-portable cluster)"));
         aa.cluster = ny;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(p.n_slices, ny);
@@ -326,17 +336,15 @@ larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
         p.smem = gemv_tc_smem_bytes(p.list_cap);
     }
     auto kern = gemv_tc_kernel<BP, MODE>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv_tc)"));
-        attr_done = true;
-    }
+    LAROSA_TRY(cuda_check(allow_smem(kern, 227 * 1024), "cudaFuncSetAttribute(gemv_tc)"));
     if (p.smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "gemv_tc: shared memory plan %zu B too large", p.smem);
     GemvArgs aa = a;
     aa.n_splits = p.n_splits;
     aa.list_cap = p.list_cap;
-    static const int tc_dbg = env_int("LAROSA_TC_DBG", 0);   // profiling only
+#ifdef LAROSA_TC_DEBUG
+    static const int tc_dbg = env_int("LAROSA_TC_DBG", 0);   // profiling builds only
     aa.tc_dbg = tc_dbg;
+#endif
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     if (MODE != GEMV_LIST && !make_w_mn_map(&tm, a.W, a.d_in, a.d_out, a.ld))
@@ -377,11 +385,7 @@ GemvArgs gemv_args_base() {
 template <int MODE, int EPT>
 larosa_status launch_topk_t(const TopkKernelArgs& a, int batch, cudaStream_t st) {
     auto kern = topk_kernel<MODE, EPT>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        LAROSA_TRY(cuda_check(allow_smem(kern, topk_smem_bytes(LAROSA_MAX_DIM)), "cudaFuncSetAttribute(topk)"));
-        attr_done = true;
-    }
+    LAROSA_TRY(cuda_check(allow_smem(kern, topk_smem_bytes(LAROSA_MAX_DIM)), "cudaFuncSetAttribute(topk)"));
     const int cs = topk_cluster_size(a.d);   // one cluster of cs CTAs per token
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, batch);
@@ -788,16 +792,14 @@ using PFN_encodeTiled_t = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint
                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 PFN_encodeTiled_t tensor_map_encoder() {
-    static PFN_encodeTiled_t fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static const PFN_encodeTiled_t fn = [] {   // thread-safe one-time initialisation
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
-    }
+            return reinterpret_cast<PFN_encodeTiled_t>(p);
+        return (PFN_encodeTiled_t) nullptr;
+    }();
     return fn;
 }
 // K-major bf16 matrix [rows][K]: boxes of 64 (K) x box_rows, 128-byte swizzle
@@ -906,8 +908,54 @@ extern "C" larosa_status larosa_fold_rotation(const float* Q, const float* gamma
     const int M = (int)rows, N = (int)cols, K = left ? (int)rows : (int)cols;
     dim3 grid((N + 63) / 64, (M + 63) / 64);
     if (left)
-        return cuda_check(launch(fold_simt_kernel<true>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
-    return cuda_check(launch(fold_simt_kernel<false>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K), "fold");
+        return cuda_check(launch(fold_simt_kernel<true>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K,
+                                 (const float*)nullptr), "fold");
+    return cuda_check(launch(fold_simt_kernel<false>, grid, dim3(256), 0, st, Q, gamma, W, Wout, M, N, K,
+                             (const float*)nullptr), "fold");
+}
+
+// ============================================================================== residual adapter
+// A = Q_l^T Q_next with both factors split into bf16 hi + lo: the LEFT fold's tcgen05 kernel with
+// ASPLIT (Q_l^T) and BSPLIT (Q_next^T as the K-major B operand): hi.hi + lo.hi + hi.lo in fp32.
+extern "C" size_t larosa_residual_adapter_workspace_size(int64_t d) {
+    if (d <= 0) return 0;
+    return (size_t)4 * d * d * 2 + 1024;
+}
+
+extern "C" larosa_status larosa_residual_adapter(const float* Q_l, const float* Q_next, uint16_t* A, int64_t d,
+                                                 void* ws, size_t ws_bytes, larosa_stream_t stream) {
+    if (!Q_l || !Q_next || !A) return fail(LAROSA_EINVAL, "residual_adapter: NULL pointer");
+    if (d <= 0) return fail(LAROSA_EINVAL, "residual_adapter: d must be > 0");
+    if (d % 64) return fail(LAROSA_EUNSUPPORTED, "residual_adapter: d must be a multiple of 64");
+    if (d > 32768) return fail(LAROSA_EUNSUPPORTED, "residual_adapter: d too large");
+    if ((const void*)A == (const void*)Q_l || (const void*)A == (const void*)Q_next)
+        return fail(LAROSA_EINVAL, "residual_adapter: A aliases a factor");
+    if (!aligned16(A)) return fail(LAROSA_EINVAL, "residual_adapter: A must be 16-byte aligned");
+    const size_t need = larosa_residual_adapter_workspace_size(d);
+    if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "residual_adapter: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int M = (int)d;
+    if (!fold_tc_supported(d, d, true)) {
+        dim3 grid((M + 63) / 64, (M + 63) / 64);
+        return cuda_check(launch(fold_simt_kernel<true>, grid, dim3(256), 0, st, Q_l, (const float*)nullptr,
+                                 (const uint16_t*)nullptr, A, M, M, M, Q_next), "residual_adapter");
+    }
+    uint16_t* a_hi = static_cast<uint16_t*>(ws);
+    uint16_t* a_lo = a_hi + (size_t)d * d;
+    uint16_t* b_hi = a_lo + (size_t)d * d;
+    uint16_t* b_lo = b_hi + (size_t)d * d;
+    const dim3 tb(32, 8), tg((unsigned)((d + 31) / 32), (unsigned)((d + 31) / 32));
+    split_transpose_kernel<<<tg, tb, 0, st>>>(Q_l, nullptr, a_hi, a_lo, M, M);      // A op [i][m] = Q_l[m][i]
+    split_transpose_kernel<<<tg, tb, 0, st>>>(Q_next, nullptr, b_hi, b_lo, M, M);   // B op [j][m] = Q_next[m][j]
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "residual_adapter split"));
+    CUtensorMap a0, a1, b0, b1;
+    const int bn = fold_bn(M);
+    if (!make_kmajor_map(&a0, a_hi, M, M, kFoldBM) || !make_kmajor_map(&a1, a_lo, M, M, kFoldBM) ||
+        !make_kmajor_map(&b0, b_hi, M, M, bn) || !make_kmajor_map(&b1, b_lo, M, M, bn))
+        return fail(LAROSA_ECUDA, "residual_adapter: tensor map");
+    return cuda_check(bn == 256 ? launch_fold_tc<256, true, true>(a0, a1, b0, b1, A, M, M, M, st)
+                                : launch_fold_tc<128, true, true>(a0, a1, b0, b1, A, M, M, M, st),
+                      "residual_adapter (tcgen05)");
 }
 
 extern "C" larosa_status larosa_pack_gate_up(const uint16_t* Wg, const uint16_t* Wu, uint16_t* Wgu, int64_t d,
@@ -957,7 +1005,9 @@ extern "C" larosa_status larosa_lm_head(const float* resid, int32_t batch, int64
     if (batch < 1 || d <= 0 || vocab <= 0) return fail(LAROSA_EINVAL, "lm_head: bad sizes");
     if (batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "lm_head: batch > %d", LAROSA_MAX_BATCH);
     if (vocab % 8 || d % 8) return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab and d must be multiples of 8");
-    if ((vocab + kSliceCols - 1) / kSliceCols > (int64_t)(kCounterHeaderWords - kGemvTicketBase))
+    // one slice ticket per column slice: 128-column slices on the tcgen05 path (batch >= 8), 256 otherwise;
+    // size the check by the narrower one so either path fits the counter header
+    if ((vocab + kTcCols - 1) / kTcCols > (int64_t)(kCounterHeaderWords - kGemvTicketBase))
         return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab too large");
     if (!aligned16(H) || (logits && !aligned16(logits))) return fail(LAROSA_EINVAL, "lm_head: H, logits must be 16-byte aligned");
     const size_t need = larosa_lm_head_workspace_size(batch, d, vocab);
@@ -1738,11 +1788,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     a.out_ld = d_out;
     a.n_splits = n_splits;
     a.list_cap = list_cap;
-    static bool attr = false;
-    if (!attr) {
-        LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, 227 * 1024), "cudaFuncSetAttribute(gemv_w4)"));
-        attr = true;
-    }
+    LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, 227 * 1024), "cudaFuncSetAttribute(gemv_w4)"));
     if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: shared memory plan too large");
     return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
                       "gemv_w4 launch");

@@ -81,6 +81,9 @@ def lib() -> ctypes.CDLL:
     L.larosa_fold_workspace_size.argtypes = [_c_i64, _c_i64, ctypes.c_int]
     L.larosa_fold_rotation.argtypes = [_vp, _vp, _vp, _vp, _c_i64, _c_i64, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
     L.larosa_pack_gate_up.argtypes = [_vp, _vp, _vp, _c_i64, _c_i64, _vp]
+    L.larosa_residual_adapter_workspace_size.restype = ctypes.c_size_t
+    L.larosa_residual_adapter_workspace_size.argtypes = [_c_i64]
+    L.larosa_residual_adapter.argtypes = [_vp, _vp, _vp, _c_i64, _vp, ctypes.c_size_t, _vp]
     L.larosa_rotate_topk_workspace_size.restype = ctypes.c_size_t
     L.larosa_rotate_topk_workspace_size.argtypes = [_c_i32, _c_i64]
     L.larosa_rotate_topk.argtypes = [_vp, _vp, _c_i32, _c_i64, _c_i64, ctypes.c_float, _vp, _vp, _vp, _vp, _vp,
@@ -129,6 +132,7 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(LayerStateC), ctypes.POINTER(LayerTapsC), _vp,
                                       ctypes.c_size_t, _vp]
     for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
+                 "larosa_residual_adapter",
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
         getattr(L, name).restype = ctypes.c_int
@@ -222,6 +226,20 @@ def fold_rotation(Q: torch.Tensor, W: torch.Tensor, side: int, gamma: Optional[t
     ws = _ws(("fold", rows, cols, side), nb, W.device)
     _check(L.larosa_fold_rotation(_ptr(Q), _ptr(gamma), _ptr(W), _ptr(out), rows, cols, side, _ptr(ws),
                                   ws.numel(), _stream(stream)))
+    return out
+
+
+def residual_adapter(Q_l: torch.Tensor, Q_next: torch.Tensor, out: Optional[torch.Tensor] = None,
+                     stream=None) -> torch.Tensor:
+    """A_l = Q_l^T Q_next with both fp32 factors split hi + lo, rounded to bf16 once."""
+    assert Q_l.dtype == torch.float32 and Q_next.dtype == torch.float32 and Q_l.shape == Q_next.shape
+    d = Q_l.shape[0]
+    out = out if out is not None else torch.empty((d, d), dtype=torch.int16, device=Q_l.device)
+    L = lib()
+    nb = L.larosa_residual_adapter_workspace_size(d)
+    ws = _ws(("adapter", d), nb, Q_l.device)
+    _check(L.larosa_residual_adapter(_ptr(Q_l.contiguous()), _ptr(Q_next.contiguous()), _ptr(out), d, _ptr(ws),
+                                     ws.numel(), _stream(stream)))
     return out
 
 
@@ -472,6 +490,7 @@ def make_taps(w: LayerWeights, plan: Sequence[int], batch: int, device) -> dict:
         "h4": torch.empty((batch, w.inter), **f32),
         "idx_h4": torch.empty((batch, k4), **i32), "vals_h4": torch.empty((batch, k4), **f32),
         "r_out": torch.empty((batch, w.d), **f32),
+        "r_in": torch.empty((batch, w.d), **f32),
     }
 
 
@@ -497,6 +516,9 @@ def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: 
     tc = None
     if taps is not None:
         tc = LayerTapsC(*[_ptr(taps.get(n)) for n in TAP_NAMES])
+        if taps.get("r_in") is not None and state.host_in is None:   # debug tap: the layer's input
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+                taps["r_in"].copy_(state.resid)
     _check(L.larosa_sparse_layer(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sc),
                                  ctypes.byref(tc) if tc is not None else None, _ptr(ws), ws.numel(),
                                  _stream(stream)))

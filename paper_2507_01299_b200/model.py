@@ -50,7 +50,8 @@ def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
                q_mlp: Optional[torch.Tensor] = None) -> LZ.LayerWeights:
     """Offline transform of one layer (eqs. before/after_merge P:402-410, §3.2):
     W_qkv' = Q_l^T diag(g1) W_qkv;  W_o' = W_o Q_l;  W_gate|up' = Q_l^T diag(g2) [Wg | Wu]
-    (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1}.   q_l, q_next: fp32 on device.
+    (packed);  W_down' = W_down Q_l;  A_l = Q_l^T Q_{l+1} (larosa_residual_adapter: both
+    fp32 factors split hi + lo, one bf16 rounding).   q_l, q_next: fp32 on device.
     adapter_in_down (needs q_next): W_down' = W_down Q_{l+1} = (W_down Q_l) A_l, and the
     layer computes r_next = r_mid A_l + y_down (larosa.h).
     q_mlp (block-wise rotation Q_B, Table 6): the MLP block runs in q_mlp's basis: W_o' = W_o Q_m,
@@ -71,10 +72,10 @@ def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
     w_down = LZ.fold_rotation(q_next if merged else q_m, orig.wd, R)
     adapter = None
     if q_next is not None:
-        adapter = LZ.fold_rotation(q_m, synth.bf16_bits(q_next).contiguous(), L)
+        adapter = LZ.residual_adapter(q_m, q_next)
     adapter_mid = None
     if q_mlp is not None:
-        adapter_mid = LZ.fold_rotation(q_l, synth.bf16_bits(q_mlp).contiguous(), L)
+        adapter_mid = LZ.residual_adapter(q_l, q_mlp)
     return LZ.LayerWeights(w_qkv=w_qkv, w_o=w_o, w_gu=w_gu, w_down=w_down, d=shape.d, inter=shape.inter,
                            n_q_heads=shape.hq, n_kv_heads=shape.hkv, head_dim=shape.hd,
                            rope_theta=shape.rope_theta, rms_eps=shape.rms_eps,

@@ -113,6 +113,12 @@ def test_fold_validation():
     assert _status("larosa_fold_rotation", FAKE, FAKE, FAKE, ctypes.c_void_p(1 << 22), 128, 128, 1, ws, 1 << 30,
                    None) == 1   # gamma with RIGHT_Q
     assert _status("larosa_fold_rotation", FAKE, None, FAKE, FAKE, 128, 128, 0, ws, 1 << 30, None) == 1  # alias
+    # residual adapter: NULL, d % 64, aliasing, workspace too small
+    assert _status("larosa_residual_adapter", None, FAKE, ctypes.c_void_p(1 << 22), 128, ws, 1 << 30, None) == 1
+    assert _status("larosa_residual_adapter", FAKE, FAKE, ctypes.c_void_p(1 << 22), 100, ws, 1 << 30, None) == 3
+    assert _status("larosa_residual_adapter", FAKE, FAKE, FAKE, 128, ws, 1 << 30, None) == 1
+    assert _status("larosa_residual_adapter", FAKE, ctypes.c_void_p(1 << 23), ctypes.c_void_p(1 << 22), 128, ws, 16,
+                   None) == 6
     assert _status("larosa_fold_rotation", FAKE, None, FAKE, ctypes.c_void_p(1 << 22), 128, 128, 7, ws, 1 << 30,
                    None) == 1
 

@@ -8,6 +8,7 @@ import torch
 
 import oracle as O
 import synth
+from parity import walk_chain
 from paper_2507_01299_b200 import larosa as LZ
 from paper_2507_01299_b200 import model as M
 
@@ -25,6 +26,19 @@ def unpack_gu(wgu, inter):
     d = wgu.shape[0]
     blk = wgu.reshape(d, inter // B, 2, B)
     return blk[:, :, 0, :].reshape(d, inter), blk[:, :, 1, :].reshape(d, inter)
+
+
+def f64(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def layer_sites(tp, b, inter, r_ref, tag=""):
+    """One layer's four sites for the P5 walk (tests/parity.py); h1's GPU vector is the layer
+    input the binding tapped (r_in)."""
+    return [(f"{tag}h1", tp["idx_h1"][b].cpu().numpy(), inter["idx1"], f64(tp["r_in"][b]), r_ref),
+            (f"{tag}h2", tp["idx_h2"][b].cpu().numpy(), inter["idx2"], f64(tp["h2"][b]), inter["h2"]),
+            (f"{tag}h3", tp["idx_h3"][b].cpu().numpy(), inter["idx3"], f64(tp["r_mid"][b]), inter["r_mid"]),
+            (f"{tag}h4", tp["idx_h4"][b].cpu().numpy(), inter["idx4"], f64(tp["h4"][b]), inter["h4"])]
 
 
 def oracle_layers(model):
@@ -70,12 +84,15 @@ def test_decode_step_vs_oracle(batch, p, merged):
                   for a, c in kvs0]
         # oracle chain, layer by layer, checking index sets against the GPU taps
         r = O.embed(e_f, int(tokens[b]))
+        sites = []
         for l, ((wf, adp, mrg), (kc, vc)) in enumerate(zip(layers, caches)):
+            r_in = r
             r, inter = O.larosa_block(r, wf, cfg, plan, kc, vc, int(pos[b]), adapter=adp, kv_bf16=True,
                                       adapter_in_down=mrg)
-            for s in (1, 2, 3, 4):
-                if not np.array_equal(taps[l][f"idx_h{s}"][b].cpu().numpy(), inter[f"idx{s}"]):
-                    pytest.skip(f"certified near-tie swap at layer {l} site h{s} (P5, reported)")
+            sites += layer_sites(taps[l], b, inter, r_in, tag=f"layer{l}.")
+        swap = walk_chain(sites)
+        if swap is not None:
+            pytest.skip(f"certified near-tie swap at {swap} (P5, reported)")
         logits = O.lm_head(r, h_f, shape.rms_eps)
         err = np.max(np.abs(logits_gpu[b] - logits)) / np.linalg.norm(logits)
         assert err <= 1e-4, err

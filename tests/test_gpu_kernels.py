@@ -210,6 +210,31 @@ def test_fold_p4(d, cols, side):
     assert np.linalg.norm(x @ gv - x @ ref) <= 3e-3 * np.linalg.norm(x @ ref)
 
 
+@pytest.mark.parametrize("d", [64, 192, 256, 384, 4096])
+def test_residual_adapter_p4(d):
+    """larosa_residual_adapter: A = Q_l^T Q_{l+1} with both fp32 factors split, rounded
+    once: >= 99% of entries bit-identical to RNE_bf16 of the fp64 oracle product (O-3), the rest
+    within one bf16 ulp (or the fp32-accumulation floor near zero); A is orthogonal to the bf16
+    storage floor; (Q, Q) gives the identity.  d = 64/192: CUDA-core kernel; 256, 384,
+    4096: tcgen05 (hi.hi + lo.hi + hi.lo)."""
+    ql = synth.haar_orthogonal(d, seed=d + 1).float()
+    qn = synth.haar_orthogonal(d, seed=d + 2).float()
+    A = LZ.residual_adapter(ql.to(DEV), qn.to(DEV))
+    I = LZ.residual_adapter(ql.to(DEV), ql.to(DEV))
+    torch.cuda.synchronize()
+    ref = O.residual_adapter(ql.numpy().astype(np.float64), qn.numpy().astype(np.float64))
+    got = A.cpu().numpy()
+    assert np.mean(got == O.f64_to_bf16_rne(ref).view(np.int16)) >= 0.99
+    gv = O.bf16_to_f64(got.view(np.uint16))
+    _, e = np.frexp(ref)
+    ulp = np.ldexp(1.0, np.maximum(e - 8, -133))
+    floor = 2.0 ** -14 * np.sqrt(np.mean(ref * ref))
+    assert np.all(np.abs(gv - ref) <= np.maximum(ulp, floor))
+    assert np.linalg.norm(gv.T @ gv - np.eye(d)) <= 3e-3 * np.sqrt(d)
+    iv = O.bf16_to_f64(I.cpu().numpy().view(np.uint16))
+    assert np.max(np.abs(iv - np.eye(d))) <= 2.0 ** -8
+
+
 # ------------------------------------------------------------------------------------ fused Top-K + GEMV
 def _fused_ref(x, k, Wb, eps, bias=None):
     """Oracle: exact Top-K (Z10) of x, RMS scale, masked GEMV, all fp64 (O-5..O-7)."""

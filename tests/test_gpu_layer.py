@@ -13,6 +13,7 @@ import torch
 
 import oracle as O
 import synth
+from parity import walk_chain
 from paper_2507_01299_b200 import larosa as LZ
 from paper_2507_01299_b200 import model as M
 
@@ -39,6 +40,17 @@ def bf16_ulp(x):
 
 def rel_max(got, ref):
     return float(np.max(np.abs(got - ref)) / max(np.linalg.norm(ref), 1e-300))
+
+
+def layer_sites(tp, b, inter, r_ref, r_gpu=None, tag=""):
+    """The four sites of one layer for the P5 walk (tests/parity.py): GPU index list, oracle index
+    list, and the vector each side selected on (h1: the layer input, h2: attention output,
+    h3: r_mid, h4: SiLU(g)*u)."""
+    r_gpu = r_ref if r_gpu is None else r_gpu
+    return [(f"{tag}h1", tp["idx_h1"][b].cpu().numpy(), inter["idx1"], r_gpu, r_ref),
+            (f"{tag}h2", tp["idx_h2"][b].cpu().numpy(), inter["idx2"], f64(tp["h2"][b]), inter["h2"]),
+            (f"{tag}h3", tp["idx_h3"][b].cpu().numpy(), inter["idx3"], f64(tp["r_mid"][b]), inter["r_mid"]),
+            (f"{tag}h4", tp["idx_h4"][b].cpu().numpy(), inter["idx4"], f64(tp["h4"][b]), inter["h4"])]
 
 
 def unpack_gu(wgu, inter):
@@ -174,9 +186,9 @@ def test_layer_p5_independent_chain(shape, p, merged):
     vc = O.bf16_to_f64(vc0[0].numpy().view(np.uint16))
     out, inter = O.larosa_block(resid[0].numpy().astype(np.float64), wf, cfg, plan, kc, vc, int(pos[0]),
                                 adapter=w64(lw.adapter), kv_bf16=True, adapter_in_down=merged)
-    same = all(np.array_equal(tp[f"idx_h{s}"][0].cpu().numpy(), inter[f"idx{s}"]) for s in (1, 2, 3, 4))
-    if not same:
-        pytest.skip("certified near-tie swap in the independent chain (reported, P5)")
+    swap = walk_chain(layer_sites(tp, 0, inter, resid[0].numpy().astype(np.float64)))
+    if swap is not None:
+        pytest.skip(f"certified near-tie swap at site {swap} of the independent chain (P5, reported)")
     assert rel_max(f64(st.resid[0]), out) <= 1e-4
 
 
@@ -208,7 +220,8 @@ def test_layer_p0_equals_original_dense_layer(shape, batch, merged):
         ref, _ = O.dense_block(r_orig, w, cfg, kc, vc, int(pos[b]), kv_bf16=True)
         got = f64(st.resid[b])
         err = np.linalg.norm(got - ref @ qn) / np.linalg.norm(ref)
-        assert err <= 1e-2, err
+        print(f"p0-gate {shape.name} b{b} merged={merged}: {err:.3e}")
+        assert err <= 3e-3, err
 
 
 @pytest.mark.parametrize("shape,p,merged", [(SMALL, 0.5, False), (synth.MODELS["llama2-7b"], 0.5, False),
@@ -262,20 +275,34 @@ def test_bench_configuration_graph_replay_vs_oracle():
     for i in range(1, n):
         chained[i].replay()
     torch.cuda.synchronize()
+    got_graph = resid.clone()
+    # the same chain launched eagerly with taps from the same initial state: bit-identical to the
+    # replayed graphs (same kernels, fixed-order reductions), and the taps feed the P5 walk
+    for (a, b), (a0, b0) in zip(kv, kv0):
+        a.copy_(a0)
+        b.copy_(b0)
+    resid.copy_(resid0)
+    taps = [LZ.make_taps(lw, plan, 1, DEV) for lw in layers]
+    for i, lw in enumerate(layers):
+        LZ.sparse_layer(lw, plan, LZ.LayerState(resid, kv[i][0], kv[i][1], pos, chained=i > 0), taps=taps[i], ws=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(resid, got_graph)
     cfg = dict(hq=shape.hq, hkv=shape.hkv, hd=shape.hd, eps=shape.rms_eps, theta=shape.rope_theta)
     r = resid0[0].cpu().numpy().astype(np.float64)
+    sites = []
     for i, lw in enumerate(layers):
         wf = {"wqkv": w64(lw.w_qkv), "wo": w64(lw.w_o), "wd": w64(lw.w_down)}
         wf["wg"], wf["wu"] = unpack_gu(w64(lw.w_gu), shape.inter)
         kc = O.bf16_to_f64(kv0[i][0][0].cpu().numpy().view(np.uint16))
         vc = O.bf16_to_f64(kv0[i][1][0].cpu().numpy().view(np.uint16))
+        r_in = r
         r, inter = O.larosa_block(r, wf, cfg, plan, kc, vc, bench.CTX - 1, adapter=w64(lw.adapter), kv_bf16=True,
                                   adapter_in_down=True)
-    got = f64(resid[0])
-    err = rel_max(got, r)
-    if err > 1e-4:
-        pytest.skip(f"near-tie swap in the 3-layer independent chain (P5, reported): {err:.2e}")
-    assert err <= 1e-4
+        sites += layer_sites(taps[i], 0, inter, r_in, f64(taps[i]["r_in"][0]), tag=f"layer{i}.")
+    swap = walk_chain(sites)
+    if swap is not None:
+        pytest.skip(f"certified near-tie swap at {swap} of the 3-layer independent chain (P5, reported)")
+    assert rel_max(f64(got_graph[0]), r) <= 1e-4
 
 
 @pytest.mark.parametrize("batch,merged", [(1, True), (1, False), (2, True), (3, False)])
@@ -299,9 +326,9 @@ def test_layer_extreme_plans(batch, merged, plan_kind):
         vc = O.bf16_to_f64(vc0[b].numpy().view(np.uint16))
         out, inter_ = O.larosa_block(resid[b].numpy().astype(np.float64), wf, cfg, plan, kc, vc, int(pos[b]),
                                      adapter=w64(lw.adapter), kv_bf16=True, adapter_in_down=merged)
-        for s in (1, 2, 3, 4):
-            if not np.array_equal(tp[f"idx_h{s}"][b].cpu().numpy(), inter_[f"idx{s}"]):
-                pytest.skip(f"certified near-tie swap at site h{s} (P5, reported)")
+        swap = walk_chain(layer_sites(tp, b, inter_, resid[b].numpy().astype(np.float64)))
+        if swap is not None:
+            pytest.skip(f"certified near-tie swap at site {swap} (P5, reported)")
         assert rel_max(f64(st.resid[b]), out) <= 1e-4
 
 
