@@ -1,23 +1,28 @@
 #!/usr/bin/env python
 """LaRoSA decode hot path benchmark (driver contract).
 
-Workload (BASELINE.json configs[1]): one LLaMA2-7B decoder block (d 4096, MLP 11008, MHA
-32x128), batch 1, KV context 256, folded random-init weights, at sparsity p (default 0.5,
-uniform alpha), on 1 B200.  A *step* = one decode token through one block: Top-K(h1) ->
-sparse QKV GEMV (+RoPE, KV append) -> attention -> Top-K(h2) -> sparse O GEMV ->
-Top-K(h3) -> sparse gate|up GEMV (+SiLU*) -> Top-K(h4) -> sparse down GEMV -> dense
-adapter GEMV, all through larosa_sparse_layer (C ABI), replayed as CUDA graphs.  Steps
-cycle over 8 distinct layer copies (3.2 GB of weights >> 126 MB L2), and each step's
-input is the previous step's output residual (fresh Top-K sets every step).
+Workload (BASELINE.json configs[2], the largest single-GPU configuration): the LLaMA3-8B-shaped
+full decode step -- 32 folded random-init layers (d 4096, MLP 14336, GQA 32/8 x 128), the
+128,256-token LM head and greedy arg-max -- at batch 1 (default; --batch up to 16), sparsity
+p = 0.4 with uniform alpha, KV context 256.  A *step* = one decode token for every sequence:
+embedding row -> 32 x larosa_sparse_layer (per layer: Top-K(h1) + sparse QKV GEMV (+RoPE, KV
+append) -> attention -> Top-K(h2) + sparse O GEMV -> Top-K(h3) + sparse gate|up GEMV (+SiLU*)
+-> Top-K(h4) + sparse down GEMV with the residual adapter rows beside it) -> RMS + LM head ->
+arg-max, the greedy token fed back as the next step's input, all replayed as one CUDA graph.
+The weights (17 GB) are read once per step, so every step streams from HBM (>> 126 MB L2).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--p 0.5] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--p 0.4] [--batch 1] [--impl reference]
+                  [--workload decode|block|sharded-70b] [--no-extras] [--no-cpu-baseline]
 
-N > 1 (torchrun): every rank runs its own independent decode stream (replicas, weak
-scaling; the 7B block does not shard), timed with CUDA events, max over ranks.
+N > 1 (torchrun): every rank runs its own decode stream of its own model copy (replicas,
+weak scaling: an 8B model fits one B200, so the path does not shard), CUDA-event
+time, max over ranks.  --workload sharded-70b: one LLaMA3-70B layer row-sharded over the ranks
+with NCCL all-gathers (configs[4]); --workload block: the LLaMA2-7B block (configs[1]).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -34,10 +39,10 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 
-METRIC = "decode tokens/s (LLaMA2-7B decoder block, batch 1)"
+METRIC = "decode tokens/s (LLaMA3-8B 32-layer decode step)"
 UNIT = "tok/s"
-CONFIG_NAME = "LLaMA2-7B decoder block (4096 hidden, 11008 MLP) batch 1"
-N_COPIES = 8
+MODEL = "llama3-8b"
+CONFIG_NAME = "LLaMA3-8B full 32-layer decode step (GQA 32/8, 14336 MLP, 128256 vocab)"
 CTX = 256
 
 
@@ -113,16 +118,96 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------------------------ oracle leg
-def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0, merged: bool = True):
-    """Time the fp64 oracle (as it stands) on the same block workload: widened folded-like
-    bf16 weights, n_tokens decode steps.  Returns (tok/s, seconds, threads)."""
-    import oracle as O
+def host_info():
+    """nproc, CPU model and RAM of the box (the oracle's host is stated)."""
+    info = {"nproc": os.cpu_count()}
     try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        threads = os.cpu_count() or 1
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["ram_gb"] = round(int(ln.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
+def source_hash():
+    """Hash of the library sources and the launch-plan code: profiles/traffic.json is used only
+    when it was measured at the same sources (tools/traffic.sh)."""
+    h = hashlib.sha256()
+    files = sorted(os.path.join(ROOT, "paper_2507_01299_b200", "csrc", f)
+                   for f in os.listdir(os.path.join(ROOT, "paper_2507_01299_b200", "csrc")))
+    files += [os.path.join(ROOT, "include", "larosa.h")]
+    for p in files:
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+# ------------------------------------------------------------------------------------ step bytes
+def step_bytes(shape, plan, unions, batch, ctx_lens, n_layers):
+    """Algorithmic bytes of one decode step (SURVEY §8(d) "algorithmic work per unit"):
+    per layer  sum_sites |U_s| D_out,s 2  (|U_s| = k_s at batch 1; the measured union of the
+    tokens' kept sets otherwise)  +  D^2 2 (adapter; the last layer has none)  +  the KV rows read
+    (B 2 Hkv hd ctx 2); plus the LM head D V 2 and the embedding rows B D 2."""
+    d, nq = shape.d, shape.hq * shape.hd
+    douts = (shape.qkv_out, d, 2 * shape.inter, d)
+    kv = sum(2 * shape.hkv * shape.hd * c * 2 for c in ctx_lens)
+    tot = 0
+    for l in range(n_layers):
+        u = unions[l] if unions is not None else plan
+        tot += sum(int(a) * b * 2 for a, b in zip(u, douts)) + kv
+        if l + 1 < n_layers:
+            tot += d * d * 2
+    return tot + d * shape.vocab * 2 + batch * d * 2
+
+
+def measure_unions(run, plan, batch):
+    """|U_s| per layer and site: the union of the batch's kept index sets, from one tapped step."""
+    from paper_2507_01299_b200 import larosa as LZ
+    taps = [LZ.make_taps(w, plan, batch, run.resid.device) for w in run.m.layers]
+    run.step(plan, taps=taps)
+    torch.cuda.synchronize()
+    out = []
+    for t in taps:
+        u = []
+        for s in (1, 2, 3, 4):
+            idx = t[f"idx_h{s}"].cpu().numpy()
+            u.append(int(np.unique(idx).size) if idx.size else 0)
+        out.append(u)
+    return out
+
+
+def launches_per_step(batch, n_layers, merged=True):
+    """Our kernels in one captured decode step: embed; per layer (batch 1) QKV, attention, O,
+    gate|up, down (+ adapter rows) SELECT GEMVs -- 5 -- plus the h1 preparation kernel in the
+    first layer; at batch > 1 a Top-K rule kernel before each of the 4 site GEMVs and a separate
+    dense adapter GEMV (10 per layer, the last layer 9); LM head: RMS, GEMV, arg-max."""
+    if batch == 1:
+        per = [5 if merged else 6] * n_layers
+        per[0] += 1
+        per[-1] -= 0 if merged else 1
+    else:
+        per = [10] * n_layers
+        per[-1] = 9
+    return 1 + sum(per) + 3
+
+
+# ------------------------------------------------------------------------------------ oracle leg
+def oracle_decode_sample(shape, plan, n_tok, threads=None, seed=0):
+    """The fp64 oracle (as it stands: oracle.larosa_block + oracle.lm_head) on the headline
+    workload's shapes: n_tok tokens through ONE LLaMA3-8B layer plus one 1/8 slice of the LM head,
+    extrapolated to the 32-layer step as 32 t_layer + 8 t_head_slice (a layer's fp64 weights are
+    1.8 GB and the model's 64 GB, so the whole model is not materialised).  threads: BLAS threads
+    (threadpoolctl), None = the library default.  Returns (tok/s, seconds measured, threads)."""
+    import oracle as O
+    from threadpoolctl import threadpool_limits, threadpool_info
     d, inter, nq = shape.d, shape.inter, shape.hq * shape.hd
     rng = np.random.default_rng(seed)
 
@@ -135,593 +220,196 @@ def oracle_block_sample(shape, plan, n_tokens: int, seed: int = 0, merged: bool 
           "wu": O.bf16_to_f64(wbits((d, inter), d ** -0.5)),
           "wd": O.bf16_to_f64(wbits((inter, d), inter ** -0.5))}
     adapter = O.bf16_to_f64(wbits((d, d), d ** -0.5))
+    head_slice = O.bf16_to_f64(wbits((d, shape.vocab // 8), d ** -0.5))
     cfg = dict(hq=shape.hq, hkv=shape.hkv, hd=shape.hd, eps=shape.rms_eps, theta=shape.rope_theta)
     kc = rng.standard_normal((shape.hkv, CTX, shape.hd))
     vc = rng.standard_normal((shape.hkv, CTX, shape.hd))
-    r = synth.residual_activation(1, d, seed=1).numpy()[0].astype(np.float64)
-    t0 = time.perf_counter()
-    for _ in range(n_tokens):
-        r, _ = O.larosa_block(r, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True,
-                              adapter_in_down=merged)
-    dt = time.perf_counter() - t0
-    return n_tokens / dt, dt, threads
+    r0 = synth.residual_activation(1, d, seed=1).numpy()[0].astype(np.float64)
+    with threadpool_limits(limits=threads):
+        used = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        O.larosa_block(r0, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True, adapter_in_down=True)
+        t0 = time.perf_counter()
+        r = r0
+        for _ in range(n_tok):
+            r, _ = O.larosa_block(r, wf, cfg, plan, kc, vc, CTX - 1, adapter=adapter, kv_bf16=True,
+                                  adapter_in_down=True)
+        t_layer = (time.perf_counter() - t0) / n_tok
+        t0 = time.perf_counter()
+        O.lm_head(r, head_slice, shape.rms_eps)
+        t_head = (time.perf_counter() - t0) * 8
+    t_step = shape.layers * t_layer + t_head
+    return 1.0 / t_step, n_tok * t_layer + t_head / 8, used
+
+
+def cpu_baseline(shape, plan, n_tok=2):
+    """Oracle tok/s on the box's host cores, 1 thread and all threads (results bit-identical:
+    each output is one fixed-order dot product)."""
+    nproc = os.cpu_count() or 1
+    one, s1, _ = oracle_decode_sample(shape, plan, n_tok, threads=1)
+    alln, s2, used = oracle_decode_sample(shape, plan, n_tok, threads=nproc)
+    return {"value": alln, "unit": UNIT, "cores": used, "kind": "oracle",
+            "sample": f"{n_tok} tokens through one LLaMA3-8B layer + 1/8 of the LM head (fp64 numpy oracle), "
+                      f"extrapolated to the 32-layer step (32 t_layer + t_head); same p and plan",
+            "extrapolated": True, "one_thread_tok_s": one, "all_threads_tok_s": alln,
+            "measured_seconds": s1 + s2, "host": host_info()}
 
 
 def run_reference(args):
+    """--impl reference: the oracle (as it stands) on the same workload and metric; each step = one
+    token through one layer + 1/8 head slice, extrapolated to the 32-layer step."""
     ws, rank, _ = dist_env()
     if ws > 1 and rank != 0:
         return
-    shape = synth.MODELS["llama2-7b"]
     import oracle as O
+    shape = synth.MODELS[MODEL]
     plan = O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter)
-    oracle_block_sample(shape, plan, 1)                       # warm-up (page in, BLAS init)
-    steps = max(1, args.steps if args.steps <= 8 else 8)      # bounded CPU sample
-    tok_s, dt, threads = oracle_block_sample(shape, plan, steps)
+    steps = max(1, min(args.steps, 6))                       # bounded CPU sample
+    tok_s, secs, threads = oracle_decode_sample(shape, plan, steps)
     out = {"impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+           "steps": steps, "warmup": 1, "ms_per_step": 1e3 / tok_s, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "ctx": CTX},
+           "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "ctx": CTX, "batch": 1},
            "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "oracle",
-                            "sample": f"{steps} decode tokens through one LLaMA2-7B block (fp64 numpy oracle)"},
+                            "sample": f"{steps} tokens through one LLaMA3-8B layer + 1/8 LM head (fp64 numpy "
+                                      f"oracle), extrapolated to 32 layers + head", "host": host_info()},
            "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
 
 # ------------------------------------------------------------------------------------ GPU leg
-def build_stack(shape, device, n_copies, seed=0, merged=True, variant="QL"):
-    """variant: QL (one rotation per layer, the paper's method), QB (block-wise: attention and MLP
-    blocks in their own bases, A_mid beside O), QM (one rotation for the whole model: no adapter)."""
-    from paper_2507_01299_b200 import model as M
-    qs = [synth.haar_orthogonal(shape.d, seed=100 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
-    layers = []
-    for i in range(n_copies):
-        orig = M.synth_original_layer(shape, seed + i + 1, device=device)
-        if variant == "QM":
-            layers.append(M.fold_layer(orig, shape, qs[0], None))
-        elif variant == "QB":
-            qm = synth.haar_orthogonal(shape.d, seed=300 + i, device=device, dtype=torch.float32)
-            layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged, q_mlp=qm))
-        else:
-            layers.append(M.fold_layer(orig, shape, qs[i], qs[i + 1], adapter_in_down=merged))
-        del orig
+def capture_step(run, plan, feedback=True):
+    """One CUDA graph of a whole decode step; feedback=True appends the greedy token -> next
+    input copy (device to device), so replays decode a real token sequence."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run.step(plan)
+        if feedback:
+            run.tokens.copy_(run.next_tokens)
+    torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
-    return layers
-
-
-def time_gemv_sites(layers, plan, shape, device, reps=48):
-    """The dominant kernel in isolation: the batch-1 SELECT GEMV (gemv_kernel<1, SELECT>, the
-    exact kernel of the layer step: fused Top-K prologue + kept-row stream + epilogue) per
-    site, on selection data prepared once per input (larosa_topk_sparse_gemv prepared=1),
-    back-to-back launches (PDL) in a CUDA graph, cycling the layer copies (weights >> L2) and
-    8 inputs; CUDA events on the launching stream.  The adapter site runs at k = D; with the
-    adapter folded beside the down projection it is the dense companion of the down launch
-    (larosa_topk_sparse_gemv_dense2), as in the layer."""
-    from paper_2507_01299_b200 import larosa as LZ
-    k1, k2, k3, k4 = plan
-    nq = shape.hq * shape.hd
-    sites = [("qkv", "w_qkv", shape.d, shape.qkv_out, k1, shape.rms_eps), ("o", "w_o", nq, shape.d, k2, -1.0),
-             ("gate_up", "w_gu", shape.d, 2 * shape.inter, k3, shape.rms_eps),
-             ("down", "w_down", shape.inter, shape.d, k4, -1.0), ("adapter", "adapter", shape.d, shape.d, shape.d, -1.0)]
-    merged = layers[0].adapter_in_down
-    if merged:
-        sites[3] = ("down+adapter", "w_down", shape.inter, shape.d, k4, -1.0)
-        sites = sites[:4]
-    res = {}
-    stream = torch.cuda.current_stream()
-    n_in = 8
-    for name, attr, din, dout, k, eps in sites:
-        xs = [synth.residual_activation(1, din, seed=500 + r)[0].to(device) for r in range(n_in)]
-        wss = [LZ.topk_sparse_gemv_workspace(din, dout, device) for _ in range(n_in)]
-        y = torch.empty((dout,), dtype=torch.float32, device=device)
-        dense2 = name == "down+adapter"
-        x2s = [synth.residual_activation(1, shape.d, seed=600 + r)[0].to(device) for r in range(n_in)] if dense2 else None
-
-        def call(i, lw, prepared):
-            if dense2:
-                LZ.topk_sparse_gemv_dense2(xs[i], k, lw.w_down, x2s[i], lw.adapter, out=y, ws=wss[i], prepared=prepared)
-            else:
-                LZ.topk_sparse_gemv(xs[i], k, getattr(lw, attr), rms_eps=eps, out=y, ws=wss[i], prepared=prepared)
-
-        for i in range(n_in):   # prepare each input's selection data once
-            call(i, layers[0], False)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for i in range(reps):
-                call(i % n_in, layers[i % len(layers)], True)
-        g.replay()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(5):
-            g.replay()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
-        alg = k * dout * 2 + din * 2 + dout * 4      # kept rows + 16-bit keys + y
-        if dense2:
-            alg += shape.d * dout * 2 + shape.d * 4    # + every adapter row and its value
-        res[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k, "d_in": din, "d_out": dout}
-    return res
-
-
-def decode_step_extra(device, batches=(1, 16), ps=(0.4, 0.0), reps=20, merged=True):
-    """BASELINE configs[2]: the LLaMA3-8B-shaped full decode step (32 folded layers + LM head,
-    greedy), KV context 256, one CUDA graph per step; tok/s per (batch, p)."""
-    from paper_2507_01299_b200 import model as M
-    shape = synth.MODELS["llama3-8b"]
-    model = M.synth_decode_model(shape, shape.layers, device, seed=1, adapter_in_down=merged)
-    out = {}
-    for B in batches:
-        run = M.DecodeRunner(model, B, 256, device)
-        for kc, vc in run.kv:
-            kc.copy_(synth.gaussian_bf16(kc.shape, 5, 1.0, device))
-            vc.copy_(synth.gaussian_bf16(vc.shape, 6, 1.0, device))
-        run.tokens.copy_(torch.arange(B, dtype=torch.int32) * 37 + 11)
-        run.pos.fill_(255)
-        for p in ps:
-            plan = M.site_plan(shape, p)
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                run.step(plan)
-            torch.cuda.current_stream().wait_stream(s)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                run.step(plan)
-            for _ in range(3):
-                g.replay()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
-                g.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            out[f"B{B}_p{p}"] = {"ms_per_step": ms, "tok_s": B * 1e3 / ms, "plan": list(plan)}
-        del run
-    del model
-    torch.cuda.empty_cache()
-    return out
-
-
-def model_sweep_extra(device, models=("mistral-7b", "qwen2.5-7b"), ps=(0.0, 0.25, 0.4, 0.5, 0.6), steps=400,
-                      copies=4, merged=True):
-    """BASELINE configs[3]: per-layer sparsity sweep of the Mistral-7B and Qwen2.5-7B blocks (batch 1,
-    ctx 256, uniform alpha, plus the paper's alpha at p = 0.5) against the dense bf16 GEMV time
-    (cuBLAS on the same folded weights) and the HBM byte roofline of each plan."""
-    from paper_2507_01299_b200 import larosa as LZ
-    from paper_2507_01299_b200 import model as M
-    peaks, _ = measured_peaks()
-    out = {}
-    for name in models:
-        shape = synth.MODELS[name]
-        layers = build_stack(shape, device, copies, seed=500, merged=merged)
-        kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
-               synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(copies)]
-        pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
-        ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
-        res = {}
-        plans = [(str(p), M.site_plan(shape, p)) for p in ps] + [("0.5_paper_alpha", M.site_plan(shape, 0.5, "paper"))]
-        nq = shape.hq * shape.hd
-        for key, plan in plans:
-            resid = synth.residual_activation(1, shape.d, seed=77).to(device)
-            graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
-            run_steps(graphs, 50, 0)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            run_steps(graphs, steps, 0)
-            e1.record()
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / steps
-            k1, k2, k3, k4 = plan
-            wbytes = 2 * (k1 * shape.qkv_out + k2 * shape.d + k3 * 2 * shape.inter + k4 * shape.d + shape.d * shape.d)
-            kvb = 2 * 2 * shape.hkv * shape.hd * CTX
-            res[key] = {"block_us": us, "tok_s": 1e6 / us, "plan": list(plan), "bytes": wbytes + kvb,
-                        "roofline_us": (wbytes + kvb) / peaks["hbm_gbs"] / 1e3,
-                        "frac_of_roofline": (wbytes + kvb) / peaks["hbm_gbs"] / 1e3 / us}
-            del graphs
-        dense_us, _ = cublas_dense_us(layers, shape, device)
-        res["cublas_dense_4gemv_us"] = dense_us
-        res["speedup_vs_dense_at_0.5"] = dense_us / res["0.5"]["block_us"]
-        out[name] = res
-        del layers, kv, ws_buf
-        torch.cuda.empty_cache()
-    return out
-
-
-def calibration_extra(device, d=4096, n_seq=16, n_tok=2048):
-    """SURVEY §8(f) N1 at the paper's calibration size (16 sequences x 2048 tokens) for
-    a d = 4096 layer: covariance on tcgen05 (TFLOP/s of 2 n d^2) and the fp64 PCA rotation."""
-    from paper_2507_01299_b200 import larosa as LZ
-    X = synth.gaussian_bf16((n_seq * n_tok, d), 3, 1.0, device)
-    C = torch.zeros((d, d), dtype=torch.float32, device=device)
-    LZ.calib_covariance(X, scale=1.0 / n_seq, out=C)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(3):
-        LZ.calib_covariance(X, scale=1.0 / n_seq, out=C)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 3
-    t0 = time.perf_counter()
-    LZ.pca_rotation(C)
-    pca_ms = (time.perf_counter() - t0) * 1e3
-    return {"d": d, "tokens": n_seq * n_tok, "covariance_ms": ms, "covariance_tflops": 2.0 * n_seq * n_tok * d * d / ms / 1e9,
-            "pca_rotation_ms": pca_ms}
-
-
-def launch_decomposition(layers, kv, pos, ws_buf, plan, shape, device, reps=20):
-    """Where each SELECT launch's time goes inside the block step (per-CTA %globaltimer stamps,
-    larosa_debug_set_timeline; a separate run after the timed region): per site, the medians
-    over CTAs of the prologue (previous kernel's last exit -> row list ready: dependency release,
-    selection rule, mask and list), the stream (-> main loop done) and the tail (-> the last CTA's
-    exit: split-K reduction, slice ticket, epilogue), and the stream phase's bandwidth on the
-    site's kept-row bytes: over the median CTA's stream window, and over the whole span from the
-    first CTA's prologue end to the last CTA's loop end (for down + adapter the companions start
-    before the SELECT CTAs).  Supplementary to `roofline` (whole launches)."""
-    import ctypes
-    from paper_2507_01299_b200 import larosa as LZ
-    L = LZ.lib()
-    L.larosa_debug_set_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    L.larosa_debug_set_timeline.restype = None
-    n = len(layers)
-    tl = torch.zeros((n, 6, 1024, 16), dtype=torch.int64, device=device)
-    resid = synth.residual_activation(1, shape.d, seed=7).to(device)
-    for i in range(n):
-        LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos, chained=i > 0), ws=ws_buf)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        for i in range(n):
-            L.larosa_debug_set_timeline(ctypes.c_void_p(tl[i].data_ptr()), 6)
-            LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos, chained=True), ws=ws_buf)
-        L.larosa_debug_set_timeline(None, 0)
-    k1, k2, k3, k4 = plan
-    nbytes = {"qkv": k1 * shape.qkv_out * 2, "o": k2 * shape.d * 2, "gate_up": k3 * 2 * shape.inter * 2,
-              "down+adapter": (k4 + shape.d) * shape.d * 2}
-    slots = {"qkv": (0, 5), "o": (2, 1), "gate_up": (3, 2), "down+adapter": (4, 3)}   # (slot, previous slot)
-    res = {k: {"prologue_us": [], "stream_us": [], "tail_us": [], "span_us": []} for k in nbytes}
-    for r in range(reps + 2):
-        tl.zero_()
-        g.replay()
-        torch.cuda.synchronize()
-        if r < 2:
-            continue
-        a = tl.cpu().numpy().astype(np.float64)
-        for li in range(1, n):
-            for name, (sl, prev) in slots.items():
-                pv = a[li - 1][4] if sl == 0 else a[li][prev]
-                t0 = pv[pv[:, 0] > 0][:, 4].max()
-                cur = a[li][sl]
-                cur = cur[cur[:, 0] > 0]
-                pro = np.median(cur[:, 2]) - t0
-                loop = np.median(cur[:, 3]) - t0
-                res[name]["prologue_us"].append(pro / 1e3)
-                res[name]["stream_us"].append((loop - pro) / 1e3)
-                res[name]["tail_us"].append((cur[:, 4].max() - t0 - loop) / 1e3)
-                res[name]["span_us"].append((cur[:, 3].max() - cur[:, 2].min()) / 1e3)
-    out = {}
-    for name, v in res.items():
-        pro, stm, tail, span = (float(np.mean(v[k])) for k in ("prologue_us", "stream_us", "tail_us", "span_us"))
-        out[name] = {"prologue_us": pro, "stream_us": stm, "tail_us": tail,
-                     "stream_phase_gbs_median_cta": nbytes[name] / stm / 1e3 if stm > 0 else None,
-                     "stream_phase_gbs_span": nbytes[name] / span / 1e3 if span > 0 else None}
-    return out
+        run.step(plan)
+        if feedback:
+            run.tokens.copy_(run.next_tokens)
+    torch.cuda.synchronize()
+    return g
 
 
-def prefill_extra(layers, shape, device, p=0.5, n_tok=512, reps=10):
-    """N2: a 512-token prompt through the LLaMA2-7B gate|up projection with per-token Top-K
-    (larosa_prefill_sparse_gemm: our selection + hi/lo split, cuBLAS bf16 GEMMs) vs the plain
-    dense bf16 GEMM on unmasked activations (cuBLAS): ms and TFLOP/s of the useful 2 n k d_out."""
-    from paper_2507_01299_b200 import larosa as LZ
-    from paper_2507_01299_b200 import model as M
-    k = M.site_plan(shape, p)[2]
-    W = layers[0].w_gu
-    d_in, d_out = W.shape
-    X = torch.randn((n_tok, d_in), device=device)
-    Y = torch.empty((n_tok, d_out), device=device)
-    LZ.prefill_sparse_gemm(X, k, W, rms_eps=shape.rms_eps, out=Y)
+def timed_replays(g, k, ws_n=1, device=None):
+    """k replays between two CUDA events on the replay stream (after a barrier + sync), max over ranks."""
+    torch.cuda.synchronize()
+    if ws_n > 1:
+        torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        LZ.prefill_sparse_gemm(X, k, W, rms_eps=shape.rms_eps, out=Y)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    Xb, Wb = X.to(torch.bfloat16), W.view(torch.bfloat16)
-    torch.matmul(Xb, Wb)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        torch.matmul(Xb, Wb)
-    e1.record()
-    torch.cuda.synchronize()
-    dense_ms = e0.elapsed_time(e1) / reps
-    return {"n_tok": n_tok, "k": k, "ms": ms, "tok_s": n_tok / ms * 1e3, "useful_tflops": 2.0 * n_tok * k * d_out / ms / 1e9,
-            "cublas_dense_bf16_ms": dense_ms}
-
-
-def w4_sites_extra(layers, plan, shape, device, reps=48):
-    """N3: the batch-1 fused Top-K + sparse GEMV per LLaMA2-7B site on W4A16 weights (quantised
-    from the same folded bf16 weights, 8 copies cycled), timed like the bf16 roofline leg:
-    us, algorithmic GB/s (kept rows' int4 bytes + scales) and the speed-up over bf16 at the site."""
-    from paper_2507_01299_b200 import larosa as LZ
-    k1, k2, k3, k4 = plan
-    nq = shape.hq * shape.hd
-    sites = [("qkv", "w_qkv", shape.d, k1, shape.rms_eps), ("o", "w_o", nq, k2, -1.0),
-             ("gate_up", "w_gu", shape.d, k3, shape.rms_eps), ("down", "w_down", shape.inter, k4, -1.0)]
-    out = {}
-    n_in = 8
-    for name, attr, din, k, eps in sites:
-        qw = [LZ.quantize_w4(getattr(l, attr)) for l in layers]
-        dout = qw[0][0].shape[1] * 2
-        xs = [synth.residual_activation(1, din, seed=500 + r)[0].to(device) for r in range(n_in)]
-        wss = [LZ.topk_sparse_gemv_workspace(din, dout, device) for _ in range(n_in)]
-        y = torch.empty((dout,), dtype=torch.float32, device=device)
-        for i in range(n_in):
-            LZ.topk_sparse_gemv_w4(xs[i], k, *qw[0], rms_eps=eps, out=y, ws=wss[i])
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for i in range(reps):
-                LZ.topk_sparse_gemv_w4(xs[i % n_in], k, *qw[i % len(qw)], rms_eps=eps, out=y, ws=wss[i % n_in],
-                                       prepared=True)
+    for _ in range(k):
         g.replay()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(5):
-            g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
-        alg = k * (dout // 2 + dout // 128 * 2) + din * 4 + dout * 4
-        out[name] = {"us": us, "bytes": alg, "gbs": alg / us / 1e3, "k": k}
-        del qw
-    return out
-
-
-def rotation_variants_extra(device, shape, steps=1000, copies=4, p=0.5):
-    """Table 6's rotation variants on the LLaMA2-7B block (batch 1, ctx 256, p = 0.5): Q_L (one
-    rotation per layer), Q_B (attention / MLP blocks rotated separately: one more D x D adapter,
-    riding in the O launch) and Q_M (one rotation for the model: no adapter)."""
-    from paper_2507_01299_b200 import larosa as LZ
-    from paper_2507_01299_b200 import model as M
-    plan = M.site_plan(shape, p)
-    out = {}
-    for v in ("QL", "QB", "QM"):
-        layers = build_stack(shape, device, copies, seed=700, merged=True, variant=v)
-        kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
-               synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(copies)]
-        pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
-        ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
-        resid = synth.residual_activation(1, shape.d, seed=77).to(device)
-        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
-        run_steps(graphs, 50, 0)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        run_steps(graphs, steps, 0)
-        e1.record()
-        torch.cuda.synchronize()
-        out[v] = {"block_us": e0.elapsed_time(e1) * 1e3 / steps}
-        del layers, kv, graphs, ws_buf
-        torch.cuda.empty_cache()
-    return out
-
-
-def latency_consistency_extra(layers, kv, pos, ws_buf, shape, device, steps=600):
-    """SURVEY §8(f) N4 / P:369-370: with exact per-token Top-K every token moves the
-    same bytes, so per-token latency should be as steady as the dense step's.  Per-step device
-    times (CUDA events around each chained step, fresh Top-K sets every step) at p = 0.5 and
-    p = 0: percentiles and the coefficient of variation."""
-    from paper_2507_01299_b200 import model as M
-    out = {}
-    for p in (0.5, 0.0):
-        plan = M.site_plan(shape, p)
-        resid = synth.residual_activation(1, shape.d, seed=91).to(device)
-        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
-        run_steps(graphs, 50, 0)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-        torch.cuda.synchronize()
-        evs[0].record()
-        for i in range(steps):
-            graphs[i % len(graphs)].replay()
-            evs[i + 1].record()
-        torch.cuda.synchronize()
-        t = np.array([evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(steps)])
-        out[str(p)] = {"p10_us": float(np.percentile(t, 10)), "p50_us": float(np.percentile(t, 50)),
-                       "p90_us": float(np.percentile(t, 90)), "p99_us": float(np.percentile(t, 99)),
-                       "cv": float(np.std(t) / np.mean(t))}
-    return out
-
-
-def fold_extra(device):
-    """larosa_fold_rotation on LLaMA2-7B layer shapes: tcgen05 TFLOP/s (2 M N K of the fold)."""
-    from paper_2507_01299_b200 import larosa as LZ
-    d = 4096
-    q = synth.haar_orthogonal(d, 1, device=device, dtype=torch.float32)
-    g = torch.ones(d, device=device)
-    res = {}
-    for name, rows, cols, side in (("w_qkv_left", 4096, 12288, 0), ("w_down_right", 11008, 4096, 1)):
-        W = synth.gaussian_bf16((rows, cols), 2, 0.02, device)
-        out = torch.empty_like(W)
-        LZ.fold_rotation(q, W, side, gamma=g if side == 0 else None, out=out)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(3):
-            LZ.fold_rotation(q, W, side, gamma=g if side == 0 else None, out=out)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 3
-        res[name] = {"ms": ms, "tflops": 2.0 * rows * cols * d / ms / 1e9}
-    return res
-
-
-def cublas_dense_us(layers, shape, device, reps=40):
-    """Dense bf16 GEMV baseline (cuBLAS via torch.matmul) on the same folded weights."""
-    nq = shape.hq * shape.hd
-    mats = [("w_qkv", shape.d), ("w_o", nq), ("w_gu", shape.d), ("w_down", shape.inter)]
-    tot = 0.0
-    per = {}
-    for attr, din in mats:
-        x = torch.randn((1, din), device=device, dtype=torch.bfloat16)
-        ws = [getattr(l, attr).view(torch.bfloat16) for l in layers]
-        for i in range(3):
-            torch.matmul(x, ws[i % len(ws)])
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(reps):
-            torch.matmul(x, ws[i % len(ws)])
-        e1.record()
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / reps
-        per[attr] = us
-        tot += us
-    return tot, per
-
-
-def capture_graphs(layers, stack_kv, resid, pos, plan, ws_buf, chained=True):
-    """One CUDA graph per layer copy.  chained=True: the step's input residual is the
-    previous step's output (its h1 histogram / RMS partials were produced by the previous
-    layer's epilogue); chained=False adds the standalone h1 preparation kernel."""
-    from paper_2507_01299_b200 import larosa as LZ
-    graphs = []
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        for i, (w, (kc, vc)) in enumerate(zip(layers, stack_kv)):     # warm-up outside capture
-            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos, chained=chained and i > 0), ws=ws_buf)
-    torch.cuda.current_stream().wait_stream(s)
+    e1.record()
     torch.cuda.synchronize()
-    for w, (kc, vc) in zip(layers, stack_kv):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            LZ.sparse_layer(w, plan, LZ.LayerState(resid, kc, vc, pos, chained=chained), ws=ws_buf)
-        graphs.append(g)
-    torch.cuda.synchronize()
-    return graphs
-
-
-def run_steps(graphs, k, start):
-    for i in range(k):
-        graphs[(start + i) % len(graphs)].replay()
-
-
-def run_sharded(args):
-    """LLaMA3-70B layer (d 8192, MLP 28672, GQA 64/8) row-sharded over the WORLD_SIZE ranks,
-    batch 1, p = args.p: per layer the 5 library phases of larosa_sparse_layer_shard_phase,
-    each followed by torch.distributed.all_gather_into_tensor (NCCL over NVLink), the whole
-    step captured in one CUDA graph per layer copy.  value = layer tokens/s (strong scaling:
-    the same layer work split over the ranks); max over ranks of the CUDA-event time."""
-    import torch.distributed as dist
-    from paper_2507_01299_b200 import larosa as LZ
-    from paper_2507_01299_b200 import model as M
-    ws_n, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    device = f"cuda:{local}"
-    if ws_n > 1:
-        dist.init_process_group("nccl", device_id=torch.device(device))
-    shape = synth.MODELS["llama3-70b"]
-    n_copies, max_ctx = 4, 256
-    qs = [synth.haar_orthogonal(shape.d, 300 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
-    shards, kvs = [], []
-    for i in range(n_copies):
-        full = M.fold_layer(M.synth_original_layer(shape, 50 + i, device=device), shape, qs[i], qs[i + 1],
-                            adapter_in_down=args.adapter == "down")
-        shards.append(M.ShardedLayer(M.shard_layer(full, rank, ws_n), rank, ws_n, max_ctx, device))
-        del full
-        torch.cuda.empty_cache()
-        hk = shape.hkv // ws_n
-        kvs.append((synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 900 + i, 1.0, device),
-                    synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 950 + i, 1.0, device)))
-    plan = M.site_plan(shape, args.p)
-    pos = torch.full((1,), max_ctx - 1, dtype=torch.int32, device=device)
-    r = synth.residual_activation(1, shape.d, 7)[0].to(device)
-
-    def allgather(local_t, full_t):
-        if ws_n > 1:
-            dist.all_gather_into_tensor(full_t, local_t)
-        else:
-            full_t.copy_(local_t)
-
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        for sh, (kc, vc) in zip(shards, kvs):
-            sh.forward(r, kc, vc, pos, plan, allgather)
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
-    graphs = []
-    for sh, (kc, vc) in zip(shards, kvs):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            sh.forward(r, kc, vc, pos, plan, allgather)
-        graphs.append(g)
-    for i in range(args.warmup):
-        graphs[i % n_copies].replay()
-    torch.cuda.synchronize()
-    if ws_n > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record()
-        for i in range(args.steps):
-            graphs[i % n_copies].replay()
-        e1.record()
-        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if ws_n > 1:
         t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    if rank == 0:
-        out = {"metric": "decode tokens/s (LLaMA3-70B layer, row-sharded, batch 1)", "value": args.steps / (ms / 1e3),
-               "unit": "tok/s", "n_gpus": ws_n, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
-               "config": {"workload": "LLaMA3-70B decoder layer (8192 hidden, 28672 MLP, GQA 64/8) batch 1, "
-                                      "row-sharded", "sparsity": args.p, "plan_k": list(plan), "ctx": max_ctx,
-                          "layer_copies": n_copies,
-                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{shards[0].n_phases()}/layer)",
-                          "l2": "inputs larger than L2: 4 distinct layer shards cycled"},
-               "gpu_launches": (2 * shards[0].n_phases() + 1) * args.steps, "clocks": clk.summary()}
-        print(json.dumps(out))
-    if ws_n > 1:
-        dist.destroy_process_group()
+    return ms
+
+
+def reset_run(run, seed):
+    for kc, vc in run.kv:
+        kc.copy_(synth.gaussian_bf16(kc.shape, seed, 1.0, kc.device))
+        vc.copy_(synth.gaussian_bf16(vc.shape, seed + 1, 1.0, vc.device))
+    b = run.tokens.shape[0]
+    run.tokens.copy_((torch.arange(b, dtype=torch.int32) * 7919 + 11) % run.m.shape.vocab)
+    run.pos.fill_(CTX - 1)
+
+
+def cublas_dense_step_ms(model, batch, device, reps=10):
+    """cuBLAS bf16 dense GEMVs of the whole step (4 projections x 32 layers + the LM head, torch.matmul
+    on the same weights, one CUDA graph); attention excluded (favours this baseline)."""
+    x = {n: torch.randn((batch, n), device=device, dtype=torch.bfloat16) for n in {model.shape.d, model.shape.inter,
+                                                                                   model.shape.hq * model.shape.hd}}
+    mats = []
+    for w in model.layers:
+        mats += [(w.w_qkv, w.d), (w.w_o, w.n_q_heads * w.head_dim), (w.w_gu, w.d), (w.w_down, w.inter)]
+    mats.append((model.head, model.shape.d))
+
+    def body():
+        for W, din in mats:
+            torch.matmul(x[din], W.view(torch.bfloat16))
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        body()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        body()
+    for _ in range(2):
+        g.replay()
+    return timed_replays(g, reps) / reps
+
+
+def own_dense_model(model):
+    """The same model without the method's additions (no adapter, every site at k = D: the SELECT
+    GEMVs take the keep-all rule without a histogram lookup): the library's own dense chain."""
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    layers = [LZ.LayerWeights(**{**w.__dict__, "adapter": None, "adapter_in_down": False}) for w in model.layers]
+    return M.DecodeModel(shape=model.shape, embed=model.embed, layers=layers, head=model.head)
+
+
+def decode_line(run, plan, steps, reps_unions=True):
+    g = capture_step(run, plan)
+    for _ in range(3):
+        g.replay()
+    ms = timed_replays(g, steps) / steps
+    del g
+    return ms
+
+
+def traffic_record(batch, p):
+    """DRAM bytes per step measured by ncu (tools/traffic.sh) at the SAME library sources, else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rec = json.load(f)
+    except Exception:
+        return None, "no profiles/traffic.json"
+    key = f"B{batch}_p{p}"
+    if rec.get("source_hash") != source_hash():
+        return None, f"profiles/traffic.json measured at sources {rec.get('source_hash')} != {source_hash()}"
+    e = rec.get("steps", {}).get(key)
+    if not e:
+        return None, f"no {key} entry in profiles/traffic.json"
+    return e, "ncu dram__bytes_read.sum + dram__bytes_write.sum over every kernel of one step (tools/traffic.sh)"
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4000)
-    ap.add_argument("--warmup", type=int, default=200)
-    ap.add_argument("--p", type=float, default=0.5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--p", type=float, default=0.4)
+    ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--impl", default="larosa", choices=["larosa", "reference"])
-    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--workload", default="decode", choices=["decode", "block", "sharded-70b"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="alias of --no-extras")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="block", choices=["block", "sharded-70b"],
-                    help="block: LLaMA2-7B block (headline; N > 1 = replicas); sharded-70b: one LLaMA3-70B "
-                         "layer row-sharded over the N ranks with NCCL all-gathers (SURVEY §8(e))")
-    ap.add_argument("--adapter", default="down", choices=["down", "separate"],
-                    help="down: adapter folded beside the down projection (one launch, larosa.h "
-                         "adapter_in_down); separate: the literal (r_mid + y_down) A_l adapter GEMV")
+    ap.add_argument("--traffic-probe", action="store_true",
+                    help="build the model, warm up, then run exactly 2 steps eagerly (for ncu; no JSON)")
+    ap.add_argument("--adapter", default="down", choices=["down", "separate"])
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
         return
-
+    import bench_extras as BX
     if args.workload == "sharded-70b":
-        run_sharded(args)
+        BX.run_sharded(args)
         return
     ws_n, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -729,77 +417,64 @@ def main():
     if ws_n > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(device))
-    from paper_2507_01299_b200 import larosa as LZ
+    if args.workload == "block":
+        out = BX.block_c2_extra(device, p=args.p if args.p != 0.4 else 0.5, steps=args.steps * 20,
+                                warmup=args.warmup * 20, merged=args.adapter == "down")
+        if rank == 0:
+            print(json.dumps(out))
+        return
     from paper_2507_01299_b200 import model as M
 
-    shape = synth.MODELS["llama2-7b"]
+    shape = synth.MODELS[MODEL]
     merged = args.adapter == "down"
-    layers = build_stack(shape, device, N_COPIES, seed=10 * rank, merged=merged)
-    kv = [(synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 900 + i, 1.0, device),
-           synth.gaussian_bf16((1, shape.hkv, CTX, shape.hd), 950 + i, 1.0, device)) for i in range(N_COPIES)]
-    pos = torch.full((1,), CTX - 1, dtype=torch.int32, device=device)
-    ws_buf = torch.zeros(LZ.layer_workspace_size(layers[0], 1, CTX), dtype=torch.uint8, device=device)
-    resid0 = synth.residual_activation(1, shape.d, seed=77 + rank).to(device)
+    B = args.batch
+    model = M.synth_decode_model(shape, shape.layers, device, seed=1 + rank, adapter_in_down=merged)
+    run = M.DecodeRunner(model, B, CTX, device)
+    reset_run(run, 5)
+    plan = M.site_plan(shape, args.p)
 
-    def measure(p):
-        plan = M.site_plan(shape, p)
-        resid = resid0.clone()
-        graphs = capture_graphs(layers, kv, resid, pos, plan, ws_buf)
-        run_steps(graphs, args.warmup, 0)
+    if args.traffic_probe:   # tools/traffic.sh: ncu keeps only the kernels inside the NVTX range
+        g = capture_step(run, plan)
+        for _ in range(args.warmup):
+            g.replay()
         torch.cuda.synchronize()
-        if ws_n > 1:
-            torch.distributed.barrier()
+        torch.cuda.nvtx.range_push("traffic_step")
+        g.replay()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        run_steps(graphs, args.steps, args.warmup)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        if ws_n > 1:
-            t = torch.tensor([ms], device=device)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        return plan, graphs, resid, ms
+        torch.cuda.nvtx.range_pop()
+        return
 
     with ClockSampler(local) as clk:
-        plan, graphs, resid, ms = measure(args.p)
+        g = capture_step(run, plan)
+        for _ in range(args.warmup):
+            g.replay()
+        ms = timed_replays(g, args.steps, ws_n, device)
     clocks = clk.summary()
     ms_per_step = ms / args.steps
-    value = ws_n * args.steps / (ms / 1e3)           # tokens through the block, all ranks
+    value = ws_n * B * args.steps / (ms / 1e3)
+    del g
 
-    # ---- end to end through the public API with host buffers (pinned H2D + D2H per step) --
-    h_in = torch.empty((1, shape.d), dtype=torch.float32).pin_memory()
-    h_in.copy_(resid0.cpu())
-    h_out = torch.empty((1, shape.d), dtype=torch.float32).pin_memory()
-    stream = torch.cuda.current_stream()
-    torch.cuda.synchronize()
-    # one CUDA graph per layer copy: the layer reads the step's input from pinned host memory in
-    # its preparation kernel (H2D inside the kernel) and its last epilogue writes the output to
-    # pinned host memory as well (D2H inside the kernel) -- larosa_layer_state.host_in / host_out
-    def io_state(kc, vc):
-        return LZ.LayerState(resid, kc, vc, pos, chained=False, host_in=h_in, host_out=h_out)
+    # ---- end to end through the public API: every step copies the step's input tokens from pinned
+    # host memory and reads the greedy tokens back into pinned host memory, inside the timed region
+    h_tok = torch.empty((args.steps + args.warmup, B), dtype=torch.int32).pin_memory()
+    h_tok.copy_(torch.randint(0, shape.vocab, h_tok.shape, generator=synth.gen(3), dtype=torch.int32))
+    h_out = torch.empty((args.steps + args.warmup, B), dtype=torch.int32).pin_memory()
+    ge = capture_step(run, plan, feedback=False)
 
-    s_io = torch.cuda.Stream()
-    s_io.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s_io):
-        for w, (kc, vc) in zip(layers, kv):   # warm-up outside capture
-            LZ.sparse_layer(w, plan, io_state(kc, vc), ws=ws_buf)
-    torch.cuda.current_stream().wait_stream(s_io)
-    torch.cuda.synchronize()
-    io_graphs = []
-    for w, (kc, vc) in zip(layers, kv):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            LZ.sparse_layer(w, plan, io_state(kc, vc), ws=ws_buf)
-        io_graphs.append(g)
+    def e2e_step(i):
+        run.tokens.copy_(h_tok[i], non_blocking=True)
+        ge.replay()
+        h_out[i].copy_(run.next_tokens, non_blocking=True)
+
     for i in range(args.warmup):
-        io_graphs[i % len(io_graphs)].replay()
+        e2e_step(i)
     torch.cuda.synchronize()
+    if ws_n > 1:
+        torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        io_graphs[i % len(io_graphs)].replay()
+        e2e_step(args.warmup + i)
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -807,83 +482,116 @@ def main():
         t = torch.tensor([e2e_ms], device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": ws_n * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": shape.d * 4,
-           "d2h_bytes_per_step": shape.d * 4}
+    e2e = {"value": ws_n * B * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * 4,
+           "d2h_bytes_per_step": B * 4, "api": "model.DecodeRunner.step (CUDA graph) + pinned token copies"}
+    del ge
 
-    # ---- dominant kernel roofline: the SELECT GEMV per site, timed live in isolation --------
-    gem = time_gemv_sites(layers, plan, shape, device)
-    w4 = None if args.no_sweep else w4_sites_extra(layers, plan, shape, device)
-    bytes_step = sum(v["bytes"] for v in gem.values())
-    us_gemv = sum(v["us"] for v in gem.values())
+    # ---- roofline of the step: algorithmic bytes / step time --------------------------------------
     peaks, peak_kind = measured_peaks()
-    achieved = bytes_step / us_gemv / 1e3
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "gemv_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_step_gemv")
-    except Exception:
-        pass
+    unions = None if B == 1 else measure_unions(run, plan, B)
+    reset_run(run, 5)
+    nbytes = step_bytes(shape, plan, unions, B, [CTX] * B, shape.layers)
+    achieved = nbytes / (ms_per_step * 1e-3) / 1e9
+    traffic, traffic_src = traffic_record(B, args.p)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": "gemv_kernel<1, SELECT>: fused Top-K prologue + kept-row stream + epilogue; the "
-                          + ("4 site launches of one block step (QKV, O, gate|up at their k; down at k4 with the "
-                             "dense adapter rows as companion CTAs)" if merged else
-                             "5 site launches of one block step (QKV, O, gate|up, down at their k; adapter at k = D)")
-                          + ", each timed back to back in a CUDA graph",
-                "decomposition_in_step": launch_decomposition(layers[:4], kv[:4], pos, ws_buf, plan, shape, device)
-                if merged else None,
-                "algorithmic_bytes_per_step": bytes_step, "gemv_us_per_step": us_gemv,
-                "launches_per_step": len(gem),
-                "peak_kind": f"{peak_kind} copy (hbm_gbs)", "per_site": gem}
-
-    # ---- sparsity sweep (0-60%) and cuBLAS dense baseline ----------------------------------
-    sweep = None
-    if not args.no_sweep:
-        sweep = {}
-        for p in (0.0, 0.25, 0.4, 0.5, 0.6):
-            pl, _, _, msp = measure(p)
-            sweep[str(p)] = {"block_us": 1e3 * msp / args.steps, "tok_s": args.steps / (msp / 1e3),
-                             "plan": list(pl)}
-        dense_us, dense_per = cublas_dense_us(layers, shape, device)
-        sweep["cublas_dense_4gemv_us"] = dense_us
-        sweep["cublas_dense_per_gemv_us"] = dense_per
+                "frac": achieved / peaks["hbm_gbs"], "frac_of_8tbs": achieved / 8000.0,
+                "traffic": traffic["dram_bytes_per_step"] if traffic else None, "traffic_source": traffic_src,
+                "kernel": "the whole decode step (every launch of the graph; the SELECT GEMVs are ~86% of its "
+                          "kernel time, profiles/r02/)",
+                "algorithmic_bytes_per_step": nbytes, "unions_per_layer": unions,
+                "peak_kind": f"{peak_kind} copy (hbm_gbs)",
+                "bound_tok_s": B * peaks["hbm_gbs"] * 1e9 / nbytes}
+    if not (args.no_extras or args.no_sweep):
+        gem = BX.time_gemv_sites([w for w in model.layers[:8]], plan, shape, device)
+        gb = sum(v["bytes"] for v in gem.values())
+        gu = sum(v["us"] for v in gem.values())
+        roofline["dominant_kernel"] = {
+            "kernel": "gemv_kernel<1, SELECT> (fused Top-K prologue + kept-row stream + epilogue), the 4 site "
+                      "launches of one LLaMA3-8B layer (down with the adapter rows as companions), each timed "
+                      "back to back in a CUDA graph over 8 layer copies",
+            "achieved": gb / gu / 1e3, "frac": gb / gu / 1e3 / peaks["hbm_gbs"], "algorithmic_bytes": gb,
+            "us": gu, "per_site": gem}
 
     extras = None
-    if not args.no_sweep:
-        extras = {"decode_step_llama3_8b_ctx256": decode_step_extra(device, merged=merged),
-                  "fold_tcgen05": fold_extra(device),
-                  "calibration_n1": calibration_extra(device),
-                  "latency_consistency": latency_consistency_extra(layers, kv, pos, ws_buf, shape, device),
-                  "rotation_variants": rotation_variants_extra(device, shape),
-                  "prefill_n2": prefill_extra(layers, shape, device),
-                  "w4a16_sites": {k: dict(v, bf16_us=gem[k if k != "down" else ("down+adapter" if merged else "down")]["us"])
-                                  for k, v in w4.items()},
-                  "model_sweep_configs3": model_sweep_extra(device, merged=merged)}
+    if not (args.no_extras or args.no_sweep):
+        extras = {}
+        # sparsity sweep of the whole step, the dense baselines and batch 16
+        sweep = {}
+        for pp in (0.0, 0.25, 0.4, 0.5, 0.6):
+            pl = M.site_plan(shape, pp)
+            reset_run(run, 5)
+            t = decode_line(run, pl, 20)
+            sweep[str(pp)] = {"ms_per_step": t, "tok_s": B * 1e3 / t, "plan": list(pl),
+                              "bytes": step_bytes(shape, pl, None, 1, [CTX], shape.layers) if B == 1 else None}
+        dm = own_dense_model(model)
+        drun = M.DecodeRunner(dm, B, CTX, device)
+        reset_run(drun, 5)
+        dense_own = decode_line(drun, M.site_plan(shape, 0.0), 20)
+        del drun, dm
+        dense_cublas = cublas_dense_step_ms(model, B, device)
+        dense = min(dense_own, dense_cublas)
+        dense_bytes = step_bytes(shape, M.site_plan(shape, 0.0), None, 1, [CTX], shape.layers) - \
+            (shape.layers - 1) * shape.d * shape.d * 2
+        for k, v in sweep.items():
+            v["speedup_vs_dense"] = dense / v["ms_per_step"]
+            if v["bytes"]:
+                v["ideal_speedup_bytes"] = dense_bytes / v["bytes"]
+                v["frac"] = v["bytes"] / (v["ms_per_step"] * 1e-3) / 1e9 / peaks["hbm_gbs"]
+        extras["step_sweep"] = sweep
+        extras["dense_baseline"] = {"own_dense_chain_ms": dense_own, "cublas_gemvs_ms": dense_cublas,
+                                    "dense_ms": dense, "dense_bytes": dense_bytes,
+                                    "note": "own: the same step without adapter at k = D (keep-all rule, no "
+                                            "histogram lookup); cuBLAS: torch.matmul GEMVs of the 4 projections x "
+                                            "32 + head, attention excluded; dense = the faster"}
+        if B == 1:
+            del run
+            torch.cuda.empty_cache()
+            b16 = {}
+            run16 = M.DecodeRunner(model, 16, CTX, device)
+            for pp in (0.4, 0.0):
+                pl = M.site_plan(shape, pp)
+                reset_run(run16, 5)
+                t = decode_line(run16, pl, 10)
+                ent = {"ms_per_step": t, "tok_s": 16e3 / t, "plan": list(pl)}
+                if pp > 0:
+                    un = measure_unions(run16, pl, 16)
+                    nb16 = step_bytes(shape, pl, un, 16, [CTX] * 16, shape.layers)
+                    ent.update(bytes=nb16, frac=nb16 / (t * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                               union_fraction=[round(float(np.mean([u[s] for u in un])) / dn, 4) for s, dn in
+                                               enumerate((shape.d, shape.hq * shape.hd, shape.d, shape.inter))])
+                b16[str(pp)] = ent
+            dm = own_dense_model(model)
+            d16 = M.DecodeRunner(dm, 16, CTX, device)
+            reset_run(d16, 5)
+            b16["dense_own_ms"] = decode_line(d16, M.site_plan(shape, 0.0), 10)
+            b16["dense_cublas_ms"] = cublas_dense_step_ms(model, 16, device)
+            del d16, dm, run16
+            extras["batch16"] = b16
+        del model
+        torch.cuda.empty_cache()
+        extras["block_llama2_7b_c2"] = BX.block_c2_extra(device)
+        extras["model_sweep_configs3"] = BX.model_sweep_extra(device, merged=merged)
+        extras["fold_tcgen05"] = BX.fold_extra(device)
+        extras["calibration_n1"] = BX.calibration_extra(device)
+        extras["rotation_variants"] = BX.rotation_variants_extra(device, synth.MODELS["llama2-7b"])
 
     cpu = None
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
         import oracle as O
-        op = O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter)
-        oracle_block_sample(shape, op, 1, merged=merged)
-        tok_s, dt, threads = oracle_block_sample(shape, op, 4, merged=merged)
-        cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": "4 decode tokens through one LLaMA2-7B block (fp64 numpy oracle), same p"}
+        cpu = cpu_baseline(shape, O.site_ks(args.p, (1, 1, 1, 1), shape.d, shape.inter))
 
-    # QKV, attention, O, gate|up, down (+ adapter companion CTAs, or a separate adapter GEMV);
-    # Top-K fused into the GEMVs
-    launches_per_step = 5 if merged else 6
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws_n, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
+               "vs_baseline": None, "dtype": "bf16 weights, fp32 activations/accumulate", "data": "synthetic",
                "config": {"workload": CONFIG_NAME, "sparsity": args.p, "alpha": "uniform", "plan_k": list(plan),
-                          "ctx": CTX, "batch": 1, "layer_copies": N_COPIES,
+                          "ctx": CTX, "batch": B, "layers": shape.layers, "vocab": shape.vocab,
                           "adapter": "folded beside down (one launch)" if merged else "separate GEMV",
-                          "l2": "inputs larger than L2: 8 distinct layer copies (3.2 GB) cycled",
+                          "l2": "inputs larger than L2: every step streams the 17 GB model once",
                           "parallelism": f"replicas x{ws_n}" if ws_n > 1 else "single GPU",
-                          "implied_llama2_7b_32_layer_tok_s": value / ws_n / 32},
-               "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-               "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep, "extras": extras}
+                          "decode": "greedy tokens fed back (device), ctx 256"},
+               "e2e": e2e, "gpu_launches": launches_per_step(B, shape.layers, merged) * args.steps,
+               "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "extras": extras}
         print(json.dumps(out))
     if ws_n > 1:
         torch.distributed.destroy_process_group()

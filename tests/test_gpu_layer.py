@@ -252,7 +252,7 @@ def test_bench_configuration_graph_replay_vs_oracle():
     CUDA graphs (capture_graphs) and replayed; the final residual after 3 chained layers equals
     the oracle chain run on the GPU's own folded weights (P5: identical index sets at every site,
     else a certified near-tie skip) within 1e-4 of its norm."""
-    import bench
+    import bench_extras as bench
     shape = synth.MODELS["llama2-7b"]
     n = 3
     layers = bench.build_stack(shape, DEV, n, seed=0, merged=True)
