@@ -432,25 +432,55 @@ TopkKernelArgs topk_args_base() {
 
 // attention: the n_chunks CTAs of a kv group form one thread-block cluster when n_chunks <= 8
 // (split-KV merge through distributed shared memory), else the ticket merge
+// Attention kernel choice (LAROSA_ATTN: 0 auto, 1 split-KV + ticket merge, 2 split-KV with the
+// cluster merge, 3 single-pass per head / group).  Auto: max_ctx <= 256 -> single pass, else the
+// ticket merge.  Measured (LLaMA3-8B decode step, ctx 256, p = 0.4): B = 1 2.942 / 2.943 / 2.919 ms,
+// B = 16 6.158 / 6.361 / 5.901 ms for modes 1 / 2 / 3 (the cluster merge waits on the slowest chunk
+// CTA and rank 0's DSMEM merge; it stays selectable).
+int attn_mode(int64_t max_ctx, int n_chunks) {
+    static const int forced = env_int("LAROSA_ATTN", 0);
+    if (forced == 2 && n_chunks >= 1 && n_chunks <= 8) return 2;
+    if (forced == 1) return 1;
+    return max_ctx <= kAgMaxCtx ? 3 : 1;
+}
+
 larosa_status launch_attention(AttnArgs aa, int units, int hd, int G, cudaStream_t st) {
-    (void)G;
+    const int mode = attn_mode(aa.max_ctx, aa.n_chunks);
+    if (mode == 3) {
+        // units = batch * Hq query heads: one CTA per head when they fit one wave, else one per group
+        const int hpc = units <= sm_count() ? 1 : G;
+        const size_t smem = attn_group_smem_bytes(hd, hpc);
+        auto kern = hd == 128 ? attn_group_kernel<4> : attn_group_kernel<2>;
+        LAROSA_TRY(cuda_check(allow_smem(kern, smem), "cudaFuncSetAttribute(attention)"));
+        return cuda_check(launch(kern, dim3(units / hpc), dim3(kAgThreads), smem, st, aa, hpc), "attention launch");
+    }
     const size_t smem = attn_smem_bytes(hd);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units, aa.n_chunks);
     cfg.blockDim = dim3(kAttnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     int na = 0;
     if (pdl_enabled()) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
+    if (mode == 2) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = 1;
+        at[na].val.clusterDim.y = aa.n_chunks;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    if (hd == 128) return cuda_check(cudaLaunchKernelEx(&cfg, attention_kernel<4>, aa), "attention launch");
-    return cuda_check(cudaLaunchKernelEx(&cfg, attention_kernel<2>, aa), "attention launch");
+    if (mode == 2)
+        return cuda_check(cudaLaunchKernelEx(&cfg, hd == 128 ? attention_kernel<4, true> : attention_kernel<2, true>, aa),
+                          "attention launch");
+    return cuda_check(cudaLaunchKernelEx(&cfg, hd == 128 ? attention_kernel<4, false> : attention_kernel<2, false>, aa),
+                      "attention launch");
 }
 
 larosa_status launch_union(const uint32_t* mask, int nwords, int batch, int bp, const float* vals, int64_t k, int d,

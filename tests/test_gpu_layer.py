@@ -101,7 +101,10 @@ def run_layer(lw, plan, resid, kc, vc, pos):
     # block-wise rotation Q_B (adapter_mid beside O): batch 1 companions, batch 3 CUDA-core,
     # batch 16 tcgen05, the 7B block
     (SMALL, 1, 7, 0.5, "qb"), (SMALL_MHA, 3, 40, 0.4, "qb"), (SMALL, 16, 30, 0.5, "qb_merged"),
-    (synth.MODELS["llama2-7b"], 1, 256, 0.5, "qb_merged")])
+    (synth.MODELS["llama2-7b"], 1, 256, 0.5, "qb_merged"),
+    # max_ctx > 256: the split-KV attention kernel (chunk CTAs + ticket merge) instead of the
+    # single-pass one (ctx 300 / 400 / 700)
+    (SMALL, 1, 700, 0.5, True), (SMALL_MHA, 3, 300, 0.4, False), (synth.MODELS["llama3-8b"], 2, 400, 0.4, True)])
 def test_layer_p6_sitewise(shape, batch, ctx, p, merged):
     max_ctx = max(ctx, 64)
     qb = merged in ("qb", "qb_merged")
