@@ -402,6 +402,8 @@ def main():
     ap.add_argument("--traffic-probe", action="store_true",
                     help="build the model, warm up, then run exactly 2 steps eagerly (for ncu; no JSON)")
     ap.add_argument("--adapter", default="down", choices=["down", "separate"])
+    ap.add_argument("--model", default=None, help="sharded-70b: llama3-70b (default) or qwen2.5-72b")
+    ap.add_argument("--layers", type=int, default=None, help="sharded-70b: layer count (default: the model's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -427,35 +427,30 @@ def run_steps(graphs, k, start):
 
 
 def run_sharded(args):
-    """LLaMA3-70B layer (d 8192, MLP 28672, GQA 64/8) row-sharded over the WORLD_SIZE ranks,
-    batch 1, p = args.p: per layer the 5 library phases of larosa_sparse_layer_shard_phase,
-    each followed by torch.distributed.all_gather_into_tensor (NCCL over NVLink), the whole
-    step captured in one CUDA graph per layer copy.  value = layer tokens/s (strong scaling:
-    the same layer work split over the ranks); max over ranks of the CUDA-event time."""
+    """BASELINE configs[4]: the LLaMA3-70B decode step (80 folded layers, d 8192, MLP 28672, GQA 64/8,
+    128256 vocab; --model qwen2.5-72b for Qwen2.5-72B) row-sharded over the WORLD_SIZE ranks
+    (SURVEY §8(e)): every rank holds its columns of every projection and of the LM head, the
+    embedding and the residual are replicated; per layer 4 NCCL all-gathers (adapter beside down)
+    plus one for the logits, the whole step captured in one CUDA graph.  value = tokens/s of the
+    job (batch x steps / max-over-ranks CUDA-event time); strong scaling (the same model split)."""
     import torch.distributed as dist
-    from paper_2507_01299_b200 import larosa as LZ
     from paper_2507_01299_b200 import model as M
     ws_n, rank, local = dist_env()
     torch.cuda.set_device(local)
     device = f"cuda:{local}"
     if ws_n > 1:
         dist.init_process_group("nccl", device_id=torch.device(device))
-    shape = synth.MODELS["llama3-70b"]
-    n_copies, max_ctx = 4, 256
-    qs = [synth.haar_orthogonal(shape.d, 300 + i, device=device, dtype=torch.float32) for i in range(n_copies + 1)]
-    shards, kvs = [], []
-    for i in range(n_copies):
-        full = M.fold_layer(M.synth_original_layer(shape, 50 + i, device=device), shape, qs[i], qs[i + 1],
-                            adapter_in_down=args.adapter == "down")
-        shards.append(M.ShardedLayer(M.shard_layer(full, rank, ws_n), rank, ws_n, max_ctx, device))
-        del full
-        torch.cuda.empty_cache()
-        hk = shape.hkv // ws_n
-        kvs.append((synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 900 + i, 1.0, device),
-                    synth.gaussian_bf16((1, hk, max_ctx, shape.hd), 950 + i, 1.0, device)))
+    shape = synth.MODELS[getattr(args, "model", None) or "llama3-70b"]
+    n_layers = getattr(args, "layers", None) or shape.layers
+    B, max_ctx = args.batch, 256
+    model = M.ShardedDecodeModel(shape, n_layers, rank, ws_n, device, seed=3, adapter_in_down=args.adapter == "down")
+    run = M.ShardedDecodeRunner(model, B, max_ctx, device)
+    for kc, vc in run.kv:
+        kc.copy_(synth.gaussian_bf16(kc.shape, 5 + rank, 1.0, device))
+        vc.copy_(synth.gaussian_bf16(vc.shape, 6 + rank, 1.0, device))
+    run.tokens.copy_((torch.arange(B, dtype=torch.int32) * 7919 + 11) % shape.vocab)
+    run.pos.fill_(max_ctx - 1)
     plan = M.site_plan(shape, args.p)
-    pos = torch.full((1,), max_ctx - 1, dtype=torch.int32, device=device)
-    r = synth.residual_activation(1, shape.d, 7)[0].to(device)
 
     def allgather(local_t, full_t):
         if ws_n > 1:
@@ -463,21 +458,21 @@ def run_sharded(args):
         else:
             full_t.copy_(local_t)
 
+    def body():
+        run.step(plan, allgather)
+        run.tokens.copy_(run.next_tokens)
+
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
-        for sh, (kc, vc) in zip(shards, kvs):
-            sh.forward(r, kc, vc, pos, plan, allgather)
+        body()
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
-    graphs = []
-    for sh, (kc, vc) in zip(shards, kvs):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            sh.forward(r, kc, vc, pos, plan, allgather)
-        graphs.append(g)
-    for i in range(args.warmup):
-        graphs[i % n_copies].replay()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        body()
+    for _ in range(args.warmup):
+        g.replay()
     torch.cuda.synchronize()
     if ws_n > 1:
         dist.barrier()
@@ -485,8 +480,8 @@ def run_sharded(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record()
-        for i in range(args.steps):
-            graphs[i % n_copies].replay()
+        for _ in range(args.steps):
+            g.replay()
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -494,22 +489,21 @@ def run_sharded(args):
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    n_ph = run.shards[0].n_phases()
     if rank == 0:
-        out = {"metric": "decode tokens/s (LLaMA3-70B layer, row-sharded, batch 1)", "value": args.steps / (ms / 1e3),
-               "unit": "tok/s", "n_gpus": ws_n, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
-               "config": {"workload": "LLaMA3-70B decoder layer (8192 hidden, 28672 MLP, GQA 64/8) batch 1, "
-                                      "row-sharded", "sparsity": args.p, "plan_k": list(plan), "ctx": max_ctx,
-                          "layer_copies": n_copies,
-                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{shards[0].n_phases()}/layer)",
-                          "l2": "inputs larger than L2: 4 distinct layer shards cycled"},
-               "gpu_launches": (2 * shards[0].n_phases() + 1) * args.steps, "clocks": clk.summary()}
+        out = {"metric": f"decode tokens/s ({shape.name} {n_layers}-layer decode step, row-sharded)",
+               "value": B * args.steps / (ms / 1e3), "unit": "tok/s", "n_gpus": ws_n, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "bf16 weights, fp32 activations/accumulate", "data": "synthetic",
+               "config": {"workload": f"{shape.name} decode step ({n_layers} layers, d {shape.d}, MLP {shape.inter}, "
+                                      f"GQA {shape.hq}/{shape.hkv}), row-sharded", "batch": B, "sparsity": args.p,
+                          "plan_k": list(plan), "ctx": max_ctx,
+                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{n_ph}/layer + logits)",
+                          "l2": "inputs larger than L2: the step streams the whole sharded model"},
+               "gpu_launches": None, "clocks": clk.summary()}
         print(json.dumps(out))
     if ws_n > 1:
         dist.destroy_process_group()
-
-
 
 
 def block_c2_extra(device, p=0.5, steps=2000, warmup=200, merged=True):

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 4
+#define LAROSA_ABI_VERSION 5
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -325,15 +325,17 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
                                   void* ws, size_t ws_bytes, larosa_stream_t stream);
 
 /* ------------------------------------------------------------------------------
- * Row-sharded layer for multi-GPU decode (batch 1).  Every rank holds the
+ * Row-sharded layer for multi-GPU decode (batch 1..16).  Every rank holds the
  * output columns ("rows" of nn.Linear) of each projection and the replicated residual:
  *   w_qkv  [d][(Hq/n + 2 Hkv/n) hd]   this rank's q heads [r Hq/n, ..) | k heads | v heads
  *   b_qkv  [(Hq/n + 2 Hkv/n) hd] or NULL
  *   w_o    [Hq hd][d/n]    w_gu [d][2 inter/n] (packed as larosa_pack_gate_up, the same
  *   inter/n range of gate and up)    w_down [inter][d/n]    adapter [d][d/n] or NULL
  * (the larosa_layer_weights struct keeps the FULL model dims; shard->world = n).
- * The layer runs as 5 phases; after each the caller all-gathers `out` (rank-major = column
- * order at batch 1) into the next phase's `x`:
+ * The layer runs as 5 phases; after each the caller all-gathers `out` into the next phase's
+ * `x` (x, resid [batch][full width]; out [batch][local width]).  At batch 1 the rank-major
+ * gather is already the column order; at batch > 1 larosa_shard_gather_permute turns the
+ * gathered [world][batch][local] blocks into [batch][full]:
  *   0: x = r (full)      -> Top-K h1 (RMS) -> QKV (local heads, RoPE, local KV append)
  *                           -> attention (local heads)                 -> out = h2 [Hq hd / n]
  *   1: x = h2 (full)     -> Top-K h2 -> O (local cols)    -> out = r_mid cols = r + y_o [d/n]
@@ -347,12 +349,18 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
  * resid = the full residual r (phases 1, 3 read r resp. r_mid from it: pass phase 0's x for
  * phase 1 and phase 2's x for phase 3).  Every rank derives the identical Top-K rule from
  * the identical gathered vector, so kept sets agree across ranks by construction.
- * k_cache / v_cache: this rank's [1][Hkv/n][max_ctx][hd].  Requires Hq % n == 0,
- * Hkv % n == 0, d % (8 n) == 0, inter % (64 n) == 0.  One workspace per rank (size query
- * with the shard), zero-filled once.
+ * k_cache / v_cache: this rank's [batch][Hkv/n][max_ctx][hd]; pos [batch].  Requires
+ * Hq % n == 0, Hkv % n == 0, d % (8 n) == 0, inter % (64 n) == 0 (an MLP width that is not,
+ * e.g. Qwen2.5-72B's 29568 at n = 4, 8, is padded with zero gate/up columns and zero down rows:
+ * their h4 entries are exactly 0 and the Top-K with k_h4 <= the true width never prefers them
+ * over a real entry, lower index winning ties -- the padded layer computes the same function;
+ * model.shard_layer does this).  Batch 1: the fused SELECT GEMVs; batch > 1: the cluster Top-K
+ * rule kernel and the union GEMV (tcgen05 at batch >= 8).  One workspace per rank and batch
+ * (size query with the shard), zero-filled once.
  * ------------------------------------------------------------------------------ */
 typedef struct {
     int32_t rank, world;
+    int32_t batch;       /* tokens per step, 1..16 (ABI 5) */
 } larosa_shard;
 size_t larosa_shard_workspace_size(const larosa_layer_weights* w, const larosa_shard* shard, int64_t max_ctx);
 larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, const larosa_layer_plan* plan,
@@ -360,6 +368,18 @@ larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, con
                                               const float* resid, float* out, uint16_t* k_cache,
                                               uint16_t* v_cache, const int32_t* pos, int64_t max_ctx, void* ws,
                                               size_t ws_bytes, larosa_stream_t stream);
+
+/* gathered fp32 [world][batch][d_local] (an NCCL all_gather_into_tensor of every rank's
+ * [batch][d_local] phase output) -> out [batch][world * d_local] (the full vectors in column
+ * order).  out must not alias gathered.  Asynchronous. */
+larosa_status larosa_shard_gather_permute(const float* gathered, int32_t world, int32_t batch,
+                                          int64_t d_local, float* out, larosa_stream_t stream);
+
+/* Greedy token of each row: out[b] = arg-max_{i < n} logits[b][i] (row stride ld), the lowest
+ * index on exact ties -- the decode step's last operation, here for a vocabulary gathered from
+ * column-sharded LM heads.  Asynchronous. */
+larosa_status larosa_argmax(const float* logits, int32_t batch, int64_t n, int64_t ld, int32_t* out,
+                            larosa_stream_t stream);
 
 /* ------------------------------------------------------------------------------
  * Calibration of the rotation (§4.2, eq. 1):

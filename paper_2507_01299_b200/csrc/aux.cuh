@@ -175,6 +175,20 @@ __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* __rest
     }
 }
 
+// gathered [world][batch][dl] (an NCCL rank-major all-gather of per-rank [batch][dl] blocks)
+// -> out [batch][world * dl] (column order of the full vector)
+__global__ void gather_permute_kernel(const float* __restrict__ gathered, int world, int batch, int64_t dl,
+                                      float* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n = (int64_t)world * batch * dl;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % dl, t = i / dl;
+        const int64_t b = t % batch, r = t / batch;
+        out[(size_t)b * world * dl + (size_t)r * dl + c] = gathered[i];
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Wgu[r][t*2B + j] = j < B ? Wg[r][t*B + j] : Wu[r][t*B + j - B]   (B = kGuBlock)
 // ------------------------------------------------------------------------------------------

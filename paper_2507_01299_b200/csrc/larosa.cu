@@ -1487,15 +1487,16 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
 // ============================================================================== sharded layer
 namespace {
 struct ShardWs {
-    SiteSel sel;                       // selection data of the phase input (rebuilt each phase)
-    unsigned long long* acc;           // local projection accumulators (largest phase)
+    SiteSel sel;                       // batch 1: selection data of the phase input (rebuilt each phase)
+    ThreshOut* thr;                    // batch > 1: every token's Top-K rule of the phase input
+    unsigned long long* acc;           // local projection accumulators [batch][largest phase]
     float* attn_part;
     unsigned* attn_cnt;
     unsigned* tickets;
 };
 struct ShardDims {
     int64_t d, inter, nq, hq_l, hkv_l, hd, dl, il, qkv_l;
-    int G;
+    int G, batch;
 };
 ShardDims shard_dims(const larosa_layer_weights* w, const larosa_shard* sh) {
     ShardDims S;
@@ -1510,6 +1511,7 @@ ShardDims shard_dims(const larosa_layer_weights* w, const larosa_shard* sh) {
     S.il = w->inter / n;
     S.qkv_l = (S.hq_l + 2 * S.hkv_l) * S.hd;
     S.G = (int)(S.hkv_l > 0 ? S.hq_l / S.hkv_l : 1);
+    S.batch = sh->batch < 1 ? 1 : sh->batch;
     return S;
 }
 void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
@@ -1517,13 +1519,14 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     ShardWs* q = o ? o : &tmp;
     const int64_t dmax = std::max(std::max(S.d, S.nq), S.inter);
     const int64_t omax = std::max(std::max(S.qkv_l, S.dl), 2 * S.il);
-    q->acc = c.take<unsigned long long>((size_t)omax);
+    q->acc = c.take<unsigned long long>((size_t)S.batch * omax);
     q->sel.hist = c.take<uint32_t>(kSelHistAlloc);
     q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
-    const int ch = attn_chunk(max_ctx, (int)S.hq_l);
+    q->thr = c.take<ThreshOut>((size_t)S.batch);
+    const int ch = attn_chunk(max_ctx, (int)(S.batch * S.hq_l));
     const int nch = (int)((max_ctx + ch - 1) / ch);
-    q->attn_part = c.take<float>((size_t)S.hq_l * nch * (S.hd + 2));
+    q->attn_part = c.take<float>((size_t)S.batch * S.hq_l * nch * (S.hd + 2));
     q->attn_cnt = c.counters(kAttnCounterBase);
     q->tickets = c.counters(kGemvTicketBase);
 }
@@ -1531,11 +1534,15 @@ larosa_status validate_shard(const larosa_layer_weights* w, const larosa_shard* 
     if (!w || !sh) return fail(LAROSA_EINVAL, "shard: NULL struct");
     const int64_t n = sh->world;
     if (n < 1 || sh->rank < 0 || sh->rank >= n) return fail(LAROSA_EINVAL, "shard: bad rank/world");
+    if (sh->batch < 1) return fail(LAROSA_EINVAL, "shard: batch < 1");
+    if (sh->batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "shard: batch > %d", LAROSA_MAX_BATCH);
     if (w->n_q_heads % n || w->n_kv_heads % n) return fail(LAROSA_EUNSUPPORTED, "shard: heads %% world != 0");
     if (w->d % (8 * n)) return fail(LAROSA_EUNSUPPORTED, "shard: d %% (8 world) != 0");
     if (w->inter % (LAROSA_GU_BLOCK * n)) return fail(LAROSA_EUNSUPPORTED, "shard: inter %% (64 world) != 0");
     if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "shard: head_dim must be 64 or 128");
     if (w->d > LAROSA_MAX_DIM || w->inter > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "shard: dims too large");
+    if ((int64_t)sh->batch * (w->n_q_heads / n) > (int64_t)kAttnGroupCounterOff)
+        return fail(LAROSA_EUNSUPPORTED, "shard: batch * Hq/n too large");
     return LAROSA_OK;
 }
 }  // namespace
@@ -1562,6 +1569,8 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "shard_phase: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const ShardDims S = shard_dims(w, sh);
+    const int B = S.batch, bp = pad_batch(B);
+    const bool fused = B == 1;
     Carver c(ws);
     ShardWs W;
     carve_shard(c, S, max_ctx > 0 ? max_ctx : 1, &W);
@@ -1582,6 +1591,9 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     }
     if (!Wt) return fail(LAROSA_EINVAL, "shard_phase: NULL weight for phase %d", phase);
     if (k < 0 || k > din) return fail(LAROSA_EINVAL, "shard_phase: k outside [0, D_in]");
+    const void* ptrs[] = {x, resid, out, Wt, w->adapter, k_cache, v_cache};
+    for (const void* q : ptrs)
+        if (q && !aligned16(q)) return fail(LAROSA_EINVAL, "shard_phase: pointers must be 16-byte aligned");
     GemvArgs a = gemv_args_base();
     a.W = Wt;
     a.ld = dout;
@@ -1589,14 +1601,15 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     a.x = x;
     a.ldx = din;
     a.d_in = (int)din;
-    a.batch = 1;
+    a.batch = B;
     a.acc = W.acc;
     a.acc_ld = dout;
     GemvPlan p;
+    bool dense2 = false;   // batch > 1, merged phase 3: a dense adapter GEMV into the same accumulators
     if (phase == 4) {
         a.mode = GEMV_DENSE;
-        p = plan_gemv(dout, din, 1, GEMV_DENSE, din);
-    } else {
+        p = plan_gemv(dout, din, bp, GEMV_DENSE, din);
+    } else if (fused) {
         // the gathered vector is identical on every rank -> identical selection data
         SiteSel sel = W.sel;
         if (eps < 0.f) sel.ssq = nullptr;
@@ -1615,6 +1628,21 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
             a.d2 = (int)S.d;
             p = plan_gemv_comp(dout, k, din, S.d);
         }
+    } else {
+        // batch > 1: every token's exact rule from the cluster Top-K kernel on the gathered input
+        // (identical on every rank), then the union GEMV (THRESH; tcgen05 at batch >= 8)
+        TopkKernelArgs tk = topk_args_base();
+        tk.x = x;
+        tk.ldx = din;
+        tk.d = (int)din;
+        tk.k = (int)k;
+        tk.rms_eps = eps;
+        tk.rule_out = W.thr;
+        LAROSA_TRY(launch_topk(tk, B, st));
+        a.mode = GEMV_THRESH;
+        a.thr = W.thr;
+        p = plan_gemv(dout, din, bp, GEMV_THRESH, din);
+        dense2 = phase == 3 && merged;
     }
     if (phase != 0) {
         a.epi = phase == 2 ? EPI_SILU : ((phase == 4 || (phase == 3 && merged)) ? EPI_STORE : EPI_RESID);
@@ -1625,10 +1653,30 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         }
         a.out = out;
         a.out_ld = phase == 2 ? S.il : S.dl;
-        return launch_gemv(a, p, 1, st);
+        if (!dense2) return launch_gemv(a, p, fused ? 1 : bp, st);
+        // the sparse down columns leave their sums; the dense adapter GEMV (r_mid rows) finalises
+        const int epi_mode = a.epi;
+        a.epi = EPI_NONE;
+        LAROSA_TRY(launch_gemv(a, p, bp, st));
+        GemvArgs b2 = gemv_args_base();
+        b2.W = w->adapter;
+        b2.ld = dout;
+        b2.d_out = (int)dout;
+        b2.mode = GEMV_DENSE;
+        b2.x = resid;
+        b2.ldx = S.d;
+        b2.d_in = (int)S.d;
+        b2.batch = B;
+        b2.acc = W.acc;
+        b2.acc_ld = dout;
+        b2.epi = epi_mode;
+        b2.tickets = W.tickets;
+        b2.out = out;
+        b2.out_ld = S.dl;
+        return launch_gemv(b2, plan_gemv(dout, S.d, bp, GEMV_DENSE, S.d), bp, st);
     }
     // phase 0: QKV over the local heads (EPI_NONE) then attention writes the local h2
-    LAROSA_TRY(launch_gemv(a, p, 1, st));
+    LAROSA_TRY(launch_gemv(a, p, fused ? 1 : bp, st));
     AttnArgs aa;
     memset(&aa, 0, sizeof(aa));
     aa.acc = W.acc;
@@ -1642,12 +1690,35 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     aa.hq = (int)S.hq_l;
     aa.hkv = (int)S.hkv_l;
     aa.hd = (int)S.hd;
-    aa.chunk = attn_chunk(max_ctx, (int)S.hq_l);
+    aa.chunk = attn_chunk(max_ctx, (int)(B * S.hq_l));
     aa.n_chunks = (int)((max_ctx + aa.chunk - 1) / aa.chunk);
     aa.part = W.attn_part;
     aa.counters = W.attn_cnt;
     aa.out = out;
-    return launch_attention(aa, (int)S.hq_l, (int)S.hd, S.G, st);
+    return launch_attention(aa, (int)(B * S.hq_l), (int)S.hd, S.G, st);
+}
+
+// gathered [world][batch][d_local] (rank-major all-gather) -> out [batch][world * d_local]
+extern "C" larosa_status larosa_shard_gather_permute(const float* gathered, int32_t world, int32_t batch,
+                                                     int64_t d_local, float* out, larosa_stream_t stream) {
+    if (!gathered || !out) return fail(LAROSA_EINVAL, "shard_gather_permute: NULL pointer");
+    if (world < 1 || batch < 1 || d_local <= 0) return fail(LAROSA_EINVAL, "shard_gather_permute: bad sizes");
+    if ((const void*)gathered == (const void*)out) return fail(LAROSA_EINVAL, "shard_gather_permute: out aliases input");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n = (int64_t)world * batch * d_local;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    return cuda_check(launch(gather_permute_kernel, dim3(grid), dim3(256), 0, st, gathered, world, batch, d_local, out),
+                      "gather_permute launch");
+}
+
+extern "C" larosa_status larosa_argmax(const float* logits, int32_t batch, int64_t n, int64_t ld, int32_t* out,
+                                       larosa_stream_t stream) {
+    if (!logits || !out) return fail(LAROSA_EINVAL, "argmax: NULL pointer");
+    if (batch < 1 || n <= 0 || ld < n) return fail(LAROSA_EINVAL, "argmax: bad sizes");
+    if (n > INT32_MAX) return fail(LAROSA_EUNSUPPORTED, "argmax: n too large");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return cuda_check(launch(argmax_kernel, dim3(batch), dim3(kRowThreads), 0, st, logits, ld, (int)n, out),
+                      "argmax launch");
 }
 
 

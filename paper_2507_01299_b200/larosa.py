@@ -56,7 +56,7 @@ class LayerTapsC(ctypes.Structure):
 
 
 class ShardC(ctypes.Structure):
-    _fields_ = [("rank", _c_i32), ("world", _c_i32)]
+    _fields_ = [("rank", _c_i32), ("world", _c_i32), ("batch", _c_i32)]
 
 
 _LIB = None
@@ -122,6 +122,8 @@ def lib() -> ctypes.CDLL:
     L.larosa_sparse_layer_shard_phase.argtypes = [ctypes.POINTER(LayerWeightsC), ctypes.POINTER(LayerPlanC),
                                                   ctypes.POINTER(ShardC), _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                                   _c_i64, _vp, ctypes.c_size_t, _vp]
+    L.larosa_shard_gather_permute.argtypes = [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp]
+    L.larosa_argmax.argtypes = [_vp, _c_i32, _c_i64, _c_i64, _vp, _vp]
     L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
     L.larosa_debug_set_layer_phases.restype = None
     L.larosa_gemv_plan_info.argtypes = [_c_i64, _c_i64, _c_i32, ctypes.POINTER(_c_i32)]
@@ -134,9 +136,10 @@ def lib() -> ctypes.CDLL:
     for name in ("larosa_compute_k", "larosa_solve_alpha", "larosa_fold_rotation", "larosa_pack_gate_up",
                  "larosa_residual_adapter",
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
-                 "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase"):
+                 "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase", "larosa_shard_gather_permute",
+                 "larosa_argmax"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 4:
+    if L.larosa_abi_version() != 5:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -404,6 +407,20 @@ def pca_rotation(C: torch.Tensor, stream=None):
     return Q, lam
 
 
+def shard_gather_permute(gathered: torch.Tensor, world: int, batch: int, out: torch.Tensor, stream=None):
+    """[world][batch][local] (rank-major all-gather) -> out [batch][world * local]."""
+    d_local = gathered.numel() // (world * batch)
+    _check(lib().larosa_shard_gather_permute(_ptr(gathered), world, batch, d_local, _ptr(out), _stream(stream)))
+    return out
+
+
+def argmax(logits: torch.Tensor, out: torch.Tensor, stream=None):
+    """out[b] = arg-max of logits[b] (lowest index on ties)."""
+    B, n = logits.shape
+    _check(lib().larosa_argmax(_ptr(logits), B, n, logits.stride(0), _ptr(out), _stream(stream)))
+    return out
+
+
 def embed(E: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """resid[b] = E'[tokens[b]] (E' = E Q_0, bf16 bits [vocab, d]; tokens int32 [B] on device)."""
     vocab, d = E.shape
@@ -525,9 +542,9 @@ def sparse_layer(w: LayerWeights, plan: Sequence[int], state: LayerState, taps: 
 
 
 # ------------------------------------------------------------------------------- sharding
-def shard_workspace_size(w: LayerWeights, rank: int, world: int, max_ctx: int) -> int:
+def shard_workspace_size(w: LayerWeights, rank: int, world: int, max_ctx: int, batch: int = 1) -> int:
     wc = w.c()
-    sh = ShardC(rank, world)
+    sh = ShardC(rank, world, batch)
     n = lib().larosa_shard_workspace_size(ctypes.byref(wc), ctypes.byref(sh), max_ctx)
     if n == 0:
         raise LarosaError(3, "shard configuration unsupported (see larosa.h)")
@@ -539,10 +556,11 @@ def shard_phase(w: LayerWeights, plan: Sequence[int], rank: int, world: int, pha
                 k_cache: Optional[torch.Tensor] = None, v_cache: Optional[torch.Tensor] = None,
                 pos: Optional[torch.Tensor] = None, max_ctx: int = 0, stream=None):
     """One phase of the row-sharded layer (larosa_sparse_layer_shard_phase); ``w`` holds this
-    rank's shard with the FULL model dims."""
+    rank's shard with the FULL model dims.  x / resid [batch][full] (or [full] at batch 1),
+    out [batch][local]."""
     wc = w.c()
     pc = LayerPlanC(*[int(k) for k in plan[:5]], *([0] if len(plan) < 5 else []))
-    sh = ShardC(rank, world)
+    sh = ShardC(rank, world, x.shape[0] if x.dim() == 2 else 1)
     _check(lib().larosa_sparse_layer_shard_phase(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sh), int(phase),
                                                  _ptr(x), _ptr(resid), _ptr(out), _ptr(k_cache), _ptr(v_cache),
                                                  _ptr(pos), int(max_ctx), _ptr(ws), ws.numel(), _stream(stream)))

@@ -169,11 +169,32 @@ class DecodeRunner:
 
 
 # ------------------------------------------------------------------------------- multi-GPU
+def shard_inter(inter: int, world: int) -> int:
+    """The MLP width a world-size-n shard uses: inter rounded up to a multiple of 64 n (the
+    gate|up interleave block per rank).  Qwen2.5-72B: 29568 -> 29696 at n = 4, 8 (larosa.h)."""
+    q = LZ.LAROSA_GU_BLOCK * world
+    return (inter + q - 1) // q * q
+
+
+def pad_inter(w: LZ.LayerWeights, inter_p: int) -> LZ.LayerWeights:
+    """Zero-pad the MLP width to inter_p: extra zero gate|up column blocks (SiLU(0) * 0 = 0, so the
+    padded h4 entries are exactly 0) and zero down rows (never selected while k_h4 <= the true
+    width: a real entry beats a padded 0, the lower index winning ties).  Same function."""
+    if inter_p == w.inter:
+        return w
+    extra = inter_p - w.inter
+    gu = torch.cat([w.w_gu, torch.zeros((w.d, 2 * extra), dtype=w.w_gu.dtype, device=w.w_gu.device)], dim=1)
+    dn = torch.cat([w.w_down, torch.zeros((extra, w.w_down.shape[1]), dtype=w.w_down.dtype, device=w.w_down.device)])
+    return LZ.LayerWeights(**{**w.__dict__, "w_gu": gu.contiguous(), "w_down": dn.contiguous(), "inter": inter_p})
+
+
 def shard_layer(w: LZ.LayerWeights, rank: int, world: int) -> LZ.LayerWeights:
     """This rank's output columns of every projection (SURVEY §8(e) partitioning; offline data
     layout, like loading a checkpoint shard): q heads [r Hq/n, (r+1) Hq/n) with the matching
     kv heads, d/n columns of W_o / W_down / adapter, the same inter/n range of gate and up (a
-    contiguous column range of the packed W_gate|up).  Dims stay the full model's."""
+    contiguous column range of the packed W_gate|up).  Dims stay the full model's; an MLP width
+    that is not a multiple of 64 n is zero-padded first (pad_inter)."""
+    w = pad_inter(w, shard_inter(w.inter, world))
     n, hd = world, w.head_dim
     nq, nk = w.n_q_heads * hd, w.n_kv_heads * hd
     ql, kl = nq // n, nk // n
@@ -203,21 +224,25 @@ def shard_kv(cache: torch.Tensor, rank: int, world: int) -> torch.Tensor:
 
 
 class ShardedLayer:
-    """One rank's view of a row-sharded LaRoSA layer at batch 1: five library phases, each
-    followed by an all-gather of the phase output (rank-major concatenation = column order).
-    ``allgather(local, full)`` is torch.distributed.all_gather_into_tensor over NCCL on a real
-    multi-GPU run (CUDA-graph capturable)."""
+    """One rank's view of a row-sharded LaRoSA layer (batch 1..16): four or five library phases,
+    each followed by an all-gather of the phase output.  ``allgather(local, gathered)`` is
+    torch.distributed.all_gather_into_tensor over NCCL on a real multi-GPU run (CUDA-graph
+    capturable): rank-major [world][batch][local]; at batch 1 that is already the column order,
+    at batch > 1 larosa_shard_gather_permute reorders it to [batch][full]."""
 
-    def __init__(self, w_shard: LZ.LayerWeights, rank: int, world: int, max_ctx: int, device):
-        self.w, self.rank, self.world, self.max_ctx = w_shard, rank, world, max_ctx
+    def __init__(self, w_shard: LZ.LayerWeights, rank: int, world: int, max_ctx: int, device, batch: int = 1):
+        self.w, self.rank, self.world, self.max_ctx, self.batch = w_shard, rank, world, max_ctx, batch
         d, nq, inter = w_shard.d, w_shard.n_q_heads * w_shard.head_dim, w_shard.inter
-        n = world
+        n, B = world, batch
         f32 = dict(dtype=torch.float32, device=device)
-        self.ws = torch.zeros(LZ.shard_workspace_size(w_shard, rank, world, max_ctx), dtype=torch.uint8, device=device)
-        self.local = {0: torch.zeros(nq // n, **f32), 1: torch.zeros(d // n, **f32), 2: torch.zeros(inter // n, **f32),
-                      3: torch.zeros(d // n, **f32), 4: torch.zeros(d // n, **f32)}
-        self.full = {0: torch.zeros(nq, **f32), 1: torch.zeros(d, **f32), 2: torch.zeros(inter, **f32),
-                     3: torch.zeros(d, **f32)}
+        self.ws = torch.zeros(LZ.shard_workspace_size(w_shard, rank, world, max_ctx, batch), dtype=torch.uint8,
+                              device=device)
+        self.local = {0: torch.zeros((B, nq // n), **f32), 1: torch.zeros((B, d // n), **f32),
+                      2: torch.zeros((B, inter // n), **f32), 3: torch.zeros((B, d // n), **f32),
+                      4: torch.zeros((B, d // n), **f32)}
+        self.full = {0: torch.zeros((B, nq), **f32), 1: torch.zeros((B, d), **f32), 2: torch.zeros((B, inter), **f32),
+                     3: torch.zeros((B, d), **f32)}
+        self.stage = torch.zeros((n * B * max(nq, d, inter) // n,), **f32) if B > 1 else None
 
     def run_phase(self, phase: int, x: torch.Tensor, resid: Optional[torch.Tensor], k_cache, v_cache, pos,
                   plan, stream=None) -> torch.Tensor:
@@ -230,7 +255,7 @@ class ShardedLayer:
         return 5 if self.w.adapter is not None and not self.w.adapter_in_down else 4
 
     def inputs(self, phase: int, r: torch.Tensor):
-        """(x, resid) of a phase given the layer input r and the gathered earlier outputs."""
+        """(x, resid) of a phase given the layer input r [batch][d] and the gathered earlier outputs."""
         if phase == 0:
             return r, None
         if phase == 1:
@@ -241,11 +266,96 @@ class ShardedLayer:
             return self.full[2], self.full[1]
         return self.full[3], None
 
+    def gather(self, local: torch.Tensor, full: torch.Tensor, allgather, stream=None):
+        """All ranks' phase outputs -> the full [batch][width] vector(s)."""
+        if self.batch == 1:
+            allgather(local.view(-1), full.view(-1))
+            return
+        st = self.stage[:local.numel() * self.world]
+        allgather(local.view(-1), st)
+        LZ.shard_gather_permute(st, self.world, self.batch, full, stream=stream)
+
     def forward(self, r: torch.Tensor, k_cache, v_cache, pos, plan, allgather, stream=None) -> torch.Tensor:
-        """r: the full residual [d] (replicated); returns it updated in place (next layer's input)."""
+        """r: the full residual [batch][d] (replicated); returns it updated in place (next layer's input)."""
         last = self.n_phases() - 1
         for ph in range(last + 1):
             x, res = self.inputs(ph, r)
             out = self.run_phase(ph, x, res, k_cache, v_cache, pos, plan, stream)
-            allgather(out, r if ph == last else self.full[ph])
+            self.gather(out, r if ph == last else self.full[ph], allgather, stream)
         return r
+
+
+class ShardedDecodeModel:
+    """One rank's share of a whole LaRoSA model for row-sharded decoding (SURVEY §8(a) a7 with
+    §8(e)): the replicated folded embedding E' = E Q_0, every layer's shard, and the rank's vocab
+    columns of the folded head H' = Q_{L-1}^T diag(gamma_f) H (the head is column-sharded too:
+    every rank computes its logits slice, an all-gather reassembles the logits, greedy on them)."""
+
+    def __init__(self, shape: synth.ModelShape, n_layers: int, rank: int, world: int, device, seed: int = 0,
+                 adapter_in_down: bool = True, vocab: Optional[int] = None):
+        self.shape, self.rank, self.world = shape, rank, world
+        vocab = vocab or shape.vocab
+        if vocab % (8 * world):
+            raise ValueError("vocab must be a multiple of 8 * world")
+        d = shape.d
+        q_prev = synth.haar_orthogonal(d, 7000 + 100 * seed, device=device, dtype=torch.float32)
+        E = synth.gaussian_bf16((vocab, d), 9000 + seed, 1.0, device)
+        self.embed = LZ.fold_rotation(q_prev, E, LZ.LAROSA_RIGHT_Q)
+        del E
+        self.layers = []
+        for l in range(n_layers):
+            q_next = synth.haar_orthogonal(d, 7000 + 100 * seed + l + 1, device=device, dtype=torch.float32) \
+                if l + 1 < n_layers else None
+            full = fold_layer(synth_original_layer(shape, 10 * seed + l + 1, device=device), shape, q_prev, q_next,
+                              adapter_in_down=adapter_in_down)
+            self.layers.append(shard_layer(full, rank, world))
+            del full
+            q_prev = q_next if q_next is not None else q_prev
+        vl = vocab // world
+        H = synth.gaussian_bf16((d, vocab), 9100 + seed, d ** -0.5, device)
+        gf = (1.0 + 0.1 * synth.gaussian((d,), 9200 + seed, device=device)).float().contiguous()
+        self.head = LZ.fold_rotation(q_prev, H[:, rank * vl:(rank + 1) * vl].contiguous(), LZ.LAROSA_LEFT_QT, gamma=gf)
+        del H
+        self.vocab = vocab
+        torch.cuda.empty_cache()
+
+
+class ShardedDecodeRunner:
+    """Decode steps of a ShardedDecodeModel on this rank (batch 1..16): embed (replicated) ->
+    every layer's ShardedLayer.forward (4 all-gathers per layer with the adapter beside down) ->
+    this rank's LM-head slice -> all-gather of the logits -> greedy.  ``allgather`` as in
+    ShardedLayer; CUDA-graph capturable."""
+
+    def __init__(self, model: ShardedDecodeModel, batch: int, max_ctx: int, device):
+        self.m, self.batch = model, batch
+        s, n, r = model.shape, model.world, model.rank
+        self.shards = [ShardedLayer(w, r, n, max_ctx, device, batch) for w in model.layers]
+        hk = s.hkv // n
+        self.kv = [(torch.zeros((batch, hk, max_ctx, s.hd), dtype=torch.int16, device=device),
+                    torch.zeros((batch, hk, max_ctx, s.hd), dtype=torch.int16, device=device)) for _ in model.layers]
+        f32 = dict(dtype=torch.float32, device=device)
+        self.resid = torch.zeros((batch, s.d), **f32)
+        self.tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.next_tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.pos = torch.zeros((batch,), dtype=torch.int32, device=device)
+        vl = model.vocab // n
+        self.logits_local = torch.zeros((batch, vl), **f32)
+        self.logits = torch.zeros((batch, model.vocab), **f32)
+        self.stage = torch.zeros((n * batch * vl,), **f32)
+        self.local_tok = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.head_ws = torch.zeros(LZ.lib().larosa_lm_head_workspace_size(batch, s.d, vl), dtype=torch.uint8,
+                                   device=device)
+
+    def step(self, plan: Sequence[int], allgather, stream=None):
+        LZ.embed(self.m.embed, self.tokens, out=self.resid, stream=stream)
+        for sh, (kc, vc) in zip(self.shards, self.kv):
+            sh.forward(self.resid, kc, vc, self.pos, plan, allgather, stream)
+        LZ.lm_head(self.resid, self.m.head, self.m.shape.rms_eps, logits=self.logits_local,
+                   next_token=self.local_tok, ws=self.head_ws, stream=stream)
+        if self.batch == 1:
+            allgather(self.logits_local.view(-1), self.logits.view(-1))
+        else:
+            allgather(self.logits_local.view(-1), self.stage)
+            LZ.shard_gather_permute(self.stage, self.m.world, self.batch, self.logits, stream=stream)
+        LZ.argmax(self.logits, self.next_tokens, stream=stream)
+        return self.next_tokens

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 14, names
     for n in names:
         assert hasattr(L, n), f"missing export {n}"
-    assert L.larosa_abi_version() == 4
+    assert L.larosa_abi_version() == 5
 
 
 def test_status_strings():
@@ -179,6 +179,19 @@ def test_new_entry_points_validation():
     assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s3), None, ws, 1 << 40, None) == 1
     # shard phase: the block-wise rotation is not supported there
     w2 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, FAKE)
-    sh = LZ.ShardC(0, 1)
+    sh = LZ.ShardC(0, 1, 1)
     assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w2), ctypes.byref(p), ctypes.byref(sh), 1, FAKE, FAKE, FAKE,
                                              None, None, None, 0, ws, 1 << 40, None) in (1, 3)
+    # shard batch: 0 is invalid, > 16 unsupported (ABI 5)
+    w2.adapter_mid = None
+    for b, st in ((0, 1), (17, 3)):
+        shb = LZ.ShardC(0, 1, b)
+        assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w2), ctypes.byref(p), ctypes.byref(shb), 1, FAKE, FAKE,
+                                                 FAKE, None, None, None, 0, ws, 1 << 40, None) == st
+        assert L.larosa_shard_workspace_size(ctypes.byref(w2), ctypes.byref(shb), 256) == 0
+    # gather permute / argmax argument checks
+    assert L.larosa_shard_gather_permute(None, 2, 1, 64, FAKE, None) == 1
+    assert L.larosa_shard_gather_permute(FAKE, 0, 1, 64, ctypes.c_void_p(1 << 22), None) == 1
+    assert L.larosa_shard_gather_permute(FAKE, 2, 1, 64, FAKE, None) == 1          # aliasing
+    assert L.larosa_argmax(FAKE, 1, 100, 50, FAKE, None) == 1                      # ld < n
+    assert L.larosa_argmax(None, 1, 100, 100, FAKE, None) == 1

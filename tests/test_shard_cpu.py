@@ -163,3 +163,86 @@ def test_shard_layer_partition_covers_columns():
         cat = torch.cat([s.w_qkv for s in sh], dim=1)
         q = torch.cat([cat[:, r * (ql + 2 * kl):r * (ql + 2 * kl) + ql] for r in range(world)], dim=1)
         assert torch.equal(q, lw.w_qkv[:, :nq])
+
+
+def test_shard_inter_padding_is_exact():
+    """model.shard_inter / pad_inter (larosa.h: an MLP width that is not a multiple of 64 n is
+    zero-padded): Qwen2.5-72B's 29568 -> 29696 at n = 4 and 8, unchanged at n = 1, 2; the padded
+    packed gate|up keeps every original column block in place and appends zero blocks; down gets
+    zero rows; each rank's shard then holds exactly 2 inter_p / n gate|up columns."""
+    assert M.shard_inter(29568, 1) == 29568 and M.shard_inter(29568, 2) == 29568
+    assert M.shard_inter(29568, 4) == 29696 and M.shard_inter(29568, 8) == 29696
+    assert M.shard_inter(28672, 8) == 28672 and M.shard_inter(14336, 8) == 14336
+    w, *_ = toy(13)
+    lw = layer_weights(w)
+    inter_p = INTER + 2 * B_GU
+    pw = M.pad_inter(lw, inter_p)
+    assert pw.inter == inter_p
+    assert torch.equal(pw.w_gu[:, :2 * INTER], lw.w_gu) and torch.all(pw.w_gu[:, 2 * INTER:] == 0)
+    assert torch.equal(pw.w_down[:INTER], lw.w_down) and torch.all(pw.w_down[INTER:] == 0)
+    g, u = unpack_gu(pw.w_gu.numpy())
+    g0, u0 = unpack_gu(lw.w_gu.numpy())
+    assert np.array_equal(g[:, :INTER], g0) and np.array_equal(u[:, :INTER], u0)
+    # the padded layer computes the same function (oracle, p = 0.5): padded h4 entries are 0 and
+    # never selected, the output is identical
+    wf = {"wqkv": w["wqkv"], "bqkv": w["bqkv"], "wo": w["wo"], "wg": w["wg"], "wu": w["wu"], "wd": w["wd"]}
+    wp = dict(wf, wg=g, wu=u, wd=pw.w_down.numpy())
+    cfg = dict(hq=HQ, hkv=HKV, hd=HD, eps=1e-6, theta=10000.0)
+    _, kc, vc, r = toy(13)
+    plan = O.site_ks(0.5, (1, 1, 1, 1), D, INTER)
+    a, ia = O.larosa_block(r, wf, cfg, plan, kc.copy(), vc.copy(), CTX - 1, adapter=w["adapter"])
+    b, ib = O.larosa_block(r, wp, cfg, plan, kc.copy(), vc.copy(), CTX - 1, adapter=w["adapter"])
+    assert np.array_equal(ia["idx4"], ib["idx4"]) and np.all(ib["h4"][INTER:] == 0)
+    assert np.array_equal(a, b)
+
+
+def worker_batch(rank, world, port, q):
+    """Batch-2 phase outputs gathered rank-major [world][batch][local] and re-ordered to
+    [batch][full] (the larosa_shard_gather_permute contract) reproduce the unsharded oracle layer
+    for both tokens."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, kc, vc, r0 = toy(21)
+        rng = np.random.default_rng(3)
+        rs = [r0, rng.standard_normal(D)]
+        plan = O.site_ks(0.4, (1, 1, 1, 1), D, INTER)
+        plan = (plan[0], O.compute_k(1.0, 0.4, HQ * HD), plan[2], plan[3])
+        ws = M.shard_layer(layer_weights(w, True), rank, world)
+        hk = HKV // world
+        pos = CTX - 1
+        full = {}
+        caches = [(kc[rank * hk:(rank + 1) * hk].copy(), vc[rank * hk:(rank + 1) * hk].copy()) for _ in rs]
+        for ph in range(4):
+            outs = []
+            for b in range(2):
+                xin = rs[b] if ph == 0 else full[ph - 1][b]
+                res = {1: rs[b], 3: full.get(1, [None, None])[b]}.get(ph)
+                outs.append(oracle_phase(ph, ws, plan, xin, res, *caches[b], pos, rank, world, True))
+            out = torch.from_numpy(np.stack(outs))                     # [batch][local]
+            g = torch.empty(out.numel() * world, dtype=out.dtype)
+            dist.all_gather_into_tensor(g, out.reshape(-1))
+            full[ph] = g.numpy().reshape(world, 2, -1).transpose(1, 0, 2).reshape(2, -1)   # permute
+        wf = {"wqkv": w["wqkv"], "bqkv": w["bqkv"], "wo": w["wo"], "wg": w["wg"], "wu": w["wu"], "wd": w["wd"]}
+        cfg = dict(hq=HQ, hkv=HKV, hd=HD, eps=1e-6, theta=10000.0)
+        ok = True
+        for b in range(2):
+            ref, _ = O.larosa_block(rs[b], wf, cfg, plan, kc.copy(), vc.copy(), pos, adapter=w["adapter"],
+                                    adapter_in_down=True)
+            ok &= bool(np.max(np.abs(full[3][b] - ref)) <= 1e-12 * np.linalg.norm(ref))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_layer_gloo_batch2_gather_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker_batch, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
