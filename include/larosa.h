@@ -427,15 +427,20 @@ larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in, int64_t k
  * Prefill (full sparsification of prompt tokens): n_tok tokens, each
  * with its own exact Top-K (ties -> lower index) and RMS scale as larosa_rotate_topk (R = NULL):
  *   Y[t][o] = sum_{j in S_t} X[t][j] s_t W[j][o]
- * X fp32 [n_tok][d_in], W bf16 [d_in][d_out] (Wc layout), Y fp32 [n_tok][d_out].  The selection
- * is ours (cluster radix select per token); the masked activations are split into bf16 hi + lo
- * and the two products run as cuBLAS bf16 GEMMs with fp32 accumulation (a plain library GEMM:
- * at prefill the union of the tokens' kept rows is every row).  n_tok <= 65535.
+ * X fp32 [n_tok][d_in], W bf16 [d_in][d_out] (Wc layout, 16-byte aligned), Y fp32 [n_tok][d_out].
+ * All on our kernels: a per-token selection kernel (exact k-th key by a bitwise search of
+ * block-wide counts, index tie-break, fixed-order RMS sum) writes the masked activations
+ * x_j s_t (0 where not kept) as bf16 -- split = 1 also writes the bf16 remainder, ~16 mantissa
+ * bits in total -- and a tcgen05 GEMM (128 output columns x 256 tokens per CTA, TMA operands, TMEM
+ * accumulator) multiplies them with W, skipping every 64-row block of W that no token of its
+ * 256-token tile keeps.  split = 0: one bf16 MMA per block (activation rounding 2^-9 relative:
+ * max |dY| / ||Y||_2 ~ 3e-5 at d_out 22016, inside north_star's 1e-3); split = 1: two MMAs.
+ * d_in, d_out multiples of 8; d_in <= 32768.  Workspace: the size query (scratch, no zero-fill).
  * ------------------------------------------------------------------------------ */
-size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in);
+size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in, int32_t split);
 larosa_status larosa_prefill_sparse_gemm(const float* X, int64_t n_tok, int64_t d_in, int64_t k, float rms_eps,
-                                         const uint16_t* W, int64_t d_out, float* Y, void* ws, size_t ws_bytes,
-                                         larosa_stream_t stream);
+                                         const uint16_t* W, int64_t d_out, float* Y, int32_t split, void* ws,
+                                         size_t ws_bytes, larosa_stream_t stream);
 
 #ifdef __cplusplus
 }

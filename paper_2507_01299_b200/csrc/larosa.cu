@@ -20,8 +20,8 @@
 #include "gemv_tc.cuh"
 #include "calib.cuh"
 #include "gemv_w4.cuh"
+#include "prefill_tc.cuh"
 
-#include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <mutex>
 #include <set>
@@ -1896,58 +1896,66 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
 }
 
 // ============================================================================== N2 prefill
-extern "C" size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in) {
-    if (n_tok <= 0 || d_in <= 0) return 0;
-    return (size_t)n_tok * sizeof(ThreshOut) + 2 * (size_t)n_tok * d_in * 2 + 1024;
-}
-
 namespace {
-std::mutex g_blas_mu;
-cublasHandle_t blas_handle() {
-    static cublasHandle_t h = nullptr;
-    if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-    return h;
+struct PrefillWs {
+    uint16_t *xh, *xl;
+    uint8_t* anyk;
+    int64_t n_pad;
+};
+void carve_prefill(Carver& c, int64_t n_tok, int64_t d_in, int split, PrefillWs* o) {
+    PrefillWs tmp;
+    PrefillWs* q = o ? o : &tmp;
+    q->n_pad = (n_tok + kPfTok - 1) / kPfTok * kPfTok;
+    q->xh = c.take<uint16_t>((size_t)n_tok * d_in);
+    q->xl = split ? c.take<uint16_t>((size_t)n_tok * d_in) : nullptr;
+    q->anyk = c.take<uint8_t>((size_t)((d_in + kPfK - 1) / kPfK) * q->n_pad);
 }
 }  // namespace
 
+extern "C" size_t larosa_prefill_sparse_gemm_workspace_size(int64_t n_tok, int64_t d_in, int32_t split) {
+    if (n_tok <= 0 || d_in <= 0) return 0;
+    Carver c(nullptr);
+    carve_prefill(c, n_tok, d_in, split, nullptr);
+    return c.size();
+}
+
 extern "C" larosa_status larosa_prefill_sparse_gemm(const float* X, int64_t n_tok, int64_t d_in, int64_t k,
                                                     float rms_eps, const uint16_t* W, int64_t d_out, float* Y,
-                                                    void* ws, size_t ws_bytes, larosa_stream_t stream) {
+                                                    int32_t split, void* ws, size_t ws_bytes, larosa_stream_t stream) {
     if (!X || !W || !Y) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: NULL pointer");
     if (n_tok <= 0 || d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: sizes must be > 0");
     if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: k outside [0, d_in]");
     if (d_in > LAROSA_MAX_DIM) return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: d_in > %d", LAROSA_MAX_DIM);
-    if (n_tok > 65535 || d_out > (1 << 30) / n_tok) return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: too large");
-    const size_t need = larosa_prefill_sparse_gemm_workspace_size(n_tok, d_in);
+    if (d_in % 8 || d_out % 8) return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: d_in and d_out must be multiples of 8");
+    if (n_tok > 65535 * (int64_t)kPfTok || d_out > (int64_t)65535 * kPfCols)
+        return fail(LAROSA_EUNSUPPORTED, "prefill_sparse_gemm: too large");
+    if (!aligned16(W)) return fail(LAROSA_EINVAL, "prefill_sparse_gemm: W must be 16-byte aligned");
+    const size_t need = larosa_prefill_sparse_gemm_workspace_size(n_tok, d_in, split);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "prefill_sparse_gemm: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
-    ThreshOut* rules = c.take<ThreshOut>((size_t)n_tok);
-    uint16_t* xhi = c.take<uint16_t>((size_t)n_tok * d_in);
-    uint16_t* xlo = c.take<uint16_t>((size_t)n_tok * d_in);
-    // every token's exact Top-K rule (one cluster radix select per token, Z10)
-    TopkKernelArgs t = topk_args_base();
-    t.x = X;
-    t.ldx = d_in;
-    t.d = (int)d_in;
-    t.k = (int)k;
-    t.rms_eps = rms_eps;
-    t.rule_out = rules;
-    LAROSA_TRY(launch_topk(t, (int)n_tok, st));
-    prefill_mask_split_kernel<<<1024, 256, 0, st>>>(X, (int)n_tok, (int)d_in, rules, xhi, xlo);
-    LAROSA_TRY(cuda_check(cudaGetLastError(), "prefill mask/split"));
-    // Y^T [d_out][n] = W^T [d_out][d_in] . X^T [d_in][n]  (column-major views of the row-major arrays)
-    std::lock_guard<std::mutex> lk(g_blas_mu);
-    cublasHandle_t h = blas_handle();
-    if (!h) return fail(LAROSA_ECUDA, "prefill_sparse_gemm: cuBLAS unavailable");
-    if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "prefill: cublasSetStream");
-    const float one = 1.0f, zero = 0.0f;
-    for (int part = 0; part < 2; ++part) {
-        const cublasStatus_t r = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_out, (int)n_tok, (int)d_in, &one, W,
-                                              CUDA_R_16BF, (int)d_out, part ? xlo : xhi, CUDA_R_16BF, (int)d_in,
-                                              part ? &one : &zero, Y, CUDA_R_32F, (int)d_out, CUBLAS_COMPUTE_32F,
-                                              CUBLAS_GEMM_DEFAULT);
-        if (r != CUBLAS_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "prefill: cublasGemmEx (%d)", (int)r);
+    PrefillWs P;
+    carve_prefill(c, n_tok, d_in, split, &P);
+    // every token's exact Top-K (Z10) + RMS scale -> masked bf16 rows and per-block "any kept"
+    const size_t rsmem = (size_t)d_in * 4 + 128;
+    LAROSA_TRY(cuda_check(allow_smem(prefill_rule_mask_kernel, rsmem), "cudaFuncSetAttribute(prefill rule)"));
+    LAROSA_TRY(cuda_check(launch(prefill_rule_mask_kernel, dim3((unsigned)n_tok), dim3(kPfThreads), rsmem, st, X,
+                                 (int)n_tok, (int)d_in, (int)k, rms_eps, P.xh, P.xl, P.anyk, (int)P.n_pad),
+                          "prefill rule launch"));
+    CUtensorMap tw, txh, txl;
+    if (!make_w_mn_map(&tw, W, d_in, d_out, d_out) || !make_kmajor_map(&txh, P.xh, n_tok, d_in, kPfTok) ||
+        (split && !make_kmajor_map(&txl, P.xl, n_tok, d_in, kPfTok)))
+        return fail(LAROSA_ECUDA, "prefill_sparse_gemm: tensor map");
+    if (!split) txl = txh;
+    const dim3 grid((unsigned)((d_out + kPfCols - 1) / kPfCols), (unsigned)((n_tok + kPfTok - 1) / kPfTok));
+    if (split) {
+        LAROSA_TRY(cuda_check(allow_smem(prefill_tc_kernel<true>, pf_smem_bytes(true)), "cudaFuncSetAttribute(prefill)"));
+        return cuda_check(launch(prefill_tc_kernel<true>, grid, dim3(kPfGemmThreads), pf_smem_bytes(true), st, tw, txh,
+                                 txl, (const uint8_t*)P.anyk, (int)P.n_pad, (int)n_tok, (int)d_in, (int)d_out, Y),
+                          "prefill gemm launch");
     }
-    return LAROSA_OK;
+    LAROSA_TRY(cuda_check(allow_smem(prefill_tc_kernel<false>, pf_smem_bytes(false)), "cudaFuncSetAttribute(prefill)"));
+    return cuda_check(launch(prefill_tc_kernel<false>, grid, dim3(kPfGemmThreads), pf_smem_bytes(false), st, tw, txh,
+                             txl, (const uint8_t*)P.anyk, (int)P.n_pad, (int)n_tok, (int)d_in, (int)d_out, Y),
+                      "prefill gemm launch");
 }

@@ -105,9 +105,9 @@ def lib() -> ctypes.CDLL:
     L.larosa_topk_sparse_gemv_w4.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _vp, _vp, _c_i64, _vp, _c_i32, _vp,
                                              ctypes.c_size_t, _vp]
     L.larosa_prefill_sparse_gemm_workspace_size.restype = ctypes.c_size_t
-    L.larosa_prefill_sparse_gemm_workspace_size.argtypes = [_c_i64, _c_i64]
-    L.larosa_prefill_sparse_gemm.argtypes = [_vp, _c_i64, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _vp, _vp,
-                                             ctypes.c_size_t, _vp]
+    L.larosa_prefill_sparse_gemm_workspace_size.argtypes = [_c_i64, _c_i64, _c_i32]
+    L.larosa_prefill_sparse_gemm.argtypes = [_vp, _c_i64, _c_i64, _c_i64, ctypes.c_float, _vp, _c_i64, _vp, _c_i32,
+                                             _vp, ctypes.c_size_t, _vp]
     L.larosa_calib_covariance_workspace_size.restype = ctypes.c_size_t
     L.larosa_calib_covariance_workspace_size.argtypes = [_c_i64, _c_i64]
     L.larosa_calib_covariance.argtypes = [_vp, _c_i64, _c_i64, ctypes.c_float, _c_i32, _vp, _vp, ctypes.c_size_t, _vp]
@@ -365,16 +365,17 @@ def topk_sparse_gemv_w4(x: torch.Tensor, k: int, Wq: torch.Tensor, S: torch.Tens
 
 
 def prefill_sparse_gemm(X: torch.Tensor, k: int, W: torch.Tensor, rms_eps: float = -1.0,
-                        out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """Y[t] = sum_{j in TopK_k(|X[t]|)} X[t][j] s_t W[j] for every prompt token t (N2)."""
+                        out: Optional[torch.Tensor] = None, split: bool = False, stream=None) -> torch.Tensor:
+    """Y[t] = sum_{j in TopK_k(|X[t]|)} X[t][j] s_t W[j] for every prompt token t (N2).
+    split: bf16 hi + lo activations (two MMAs) instead of one bf16 operand."""
     n, d_in = X.shape
     d_out = W.shape[1]
     Y = out if out is not None else torch.empty((n, d_out), dtype=torch.float32, device=W.device)
     L = lib()
-    nb = L.larosa_prefill_sparse_gemm_workspace_size(n, d_in)
-    ws = _ws(("prefill", n, d_in), nb, W.device)
+    nb = L.larosa_prefill_sparse_gemm_workspace_size(n, d_in, int(split))
+    ws = _ws(("prefill", n, d_in, int(split)), nb, W.device)
     _check(L.larosa_prefill_sparse_gemm(_ptr(X.contiguous()), n, d_in, int(k), float(rms_eps), _ptr(W), d_out, _ptr(Y),
-                                        _ptr(ws), ws.numel(), _stream(stream)))
+                                        int(split), _ptr(ws), ws.numel(), _stream(stream)))
     return Y
 
 
