@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 SRC_DIR := paper_2507_01299_b200/csrc
 LIB := paper_2507_01299_b200/lib/liblarosa.so
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -shared -Iinclude \
-           --expt-relaxed-constexpr -Xptxas -v -lcusolver -Xlinker -rpath=/usr/local/cuda/lib64
+           --expt-relaxed-constexpr -Xptxas -v -Xlinker -rpath=/usr/local/cuda/lib64
 
 SRCS := $(SRC_DIR)/larosa.cu
 HDRS := $(wildcard $(SRC_DIR)/*.cuh) include/larosa.h

@@ -392,8 +392,11 @@ larosa_status larosa_argmax(const float* logits, int32_t batch, int64_t n, int64
  * larosa_pca_rotation: Q fp32 [d][d] row-major with Q[:, i] the eigenvector of the i-th
  *   largest eigenvalue of C (symmetrised), lam fp32 [d] the eigenvalues descending (negative
  *   round-off clamped to 0); each eigenvector's largest-|entry| component is positive (lowest
- *   row on ties) -- SURVEY Z7.  fp64 symmetric eigensolver (cuSOLVER syevd).  Synchronises the
- *   stream; LAROSA_ECUDA if the solver does not converge.  Offline (calibration) path.
+ *   row on ties) -- SURVEY Z7.  Our fp64 cyclic two-sided Jacobi (the oracle's rotation, Z8)
+ *   parallelised by a round-robin ordering: each sweep is d-1 rounds of d/2 disjoint rotations
+ *   applied at once (captured as one CUDA graph), until off(A) <= 1e-12 ||A||_F, at most 100
+ *   sweeps.  Synchronises the stream; LAROSA_ECUDA if it does not converge.  Offline path
+ *   (workspace: 2 d^2 doubles + small arrays).
  * ------------------------------------------------------------------------------ */
 size_t larosa_calib_covariance_workspace_size(int64_t n_tok, int64_t d);
 larosa_status larosa_calib_covariance(const uint16_t* X, int64_t n_tok, int64_t d, float scale, int32_t accumulate,

@@ -22,7 +22,6 @@
 #include "gemv_w4.cuh"
 #include "prefill_tc.cuh"
 
-#include <cusolverDn.h>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -1764,29 +1763,33 @@ extern "C" larosa_status larosa_calib_covariance(const uint16_t* X, int64_t n_to
 }
 
 namespace {
-std::mutex g_solver_mu;
-cusolverDnHandle_t solver_handle() {
-    static cusolverDnHandle_t h = nullptr;
-    if (!h && cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) h = nullptr;
-    return h;
-}
-int64_t pca_lwork(int64_t d) {
-    cusolverDnHandle_t h = solver_handle();
-    if (!h) return -1;
-    int lwork = 0;
-    if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d,
-                                    nullptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
-        return -1;
-    return lwork;
+std::mutex g_solver_mu;   // the Jacobi sweep graph is captured per call on a private stream
+struct JacobiWs {
+    double *A, *V, *part, *norms;
+    int* pq;
+    double2* cs;
+    int* order;
+};
+constexpr int kJacobiNormCtas = 512;
+void carve_jacobi(Carver& c, int64_t d, JacobiWs* o) {
+    JacobiWs tmp;
+    JacobiWs* q = o ? o : &tmp;
+    const int64_t n = d + (d & 1);
+    q->A = c.take<double>((size_t)n * n);
+    q->V = c.take<double>((size_t)n * n);
+    q->part = c.take<double>(2 * kJacobiNormCtas);
+    q->norms = c.take<double>(2);
+    q->pq = c.take<int>((size_t)n);
+    q->cs = c.take<double2>((size_t)n / 2);
+    q->order = c.take<int>((size_t)d);
 }
 }  // namespace
 
 extern "C" size_t larosa_pca_rotation_workspace_size(int64_t d) {
     if (d <= 0 || d > 32768) return 0;
-    std::lock_guard<std::mutex> lk(g_solver_mu);
-    const int64_t lw = pca_lwork(d);
-    if (lw < 0) return 0;
-    return (size_t)d * d * 8 + (size_t)d * 8 + 256 + (size_t)lw * 8 + 1024;
+    Carver c(nullptr);
+    carve_jacobi(c, d, nullptr);
+    return c.size();
 }
 
 extern "C" larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q, float* lam, void* ws,
@@ -1795,29 +1798,75 @@ extern "C" larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q
     if (d <= 0) return fail(LAROSA_EINVAL, "pca_rotation: d must be > 0");
     if (d > 32768) return fail(LAROSA_EUNSUPPORTED, "pca_rotation: d > 32768");
     const size_t need = larosa_pca_rotation_workspace_size(d);
-    if (need == 0) return fail(LAROSA_ECUDA, "pca_rotation: cuSOLVER unavailable");
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "pca_rotation: workspace %zu < %zu", ws_bytes, need);
     std::lock_guard<std::mutex> lk(g_solver_mu);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    double* A = static_cast<double*>(ws);
-    double* w = A + (size_t)d * d;
-    int* info = reinterpret_cast<int*>(w + d);
-    double* work = reinterpret_cast<double*>(reinterpret_cast<char*>(info) + 256);
-    const int64_t lw = pca_lwork(d);
-    f32_to_f64_sym_kernel<<<1024, 256, 0, st>>>(C, A, (int)d);
-    LAROSA_TRY(cuda_check(cudaGetLastError(), "pca: symmetrise"));
-    cusolverDnHandle_t h = solver_handle();
-    if (cusolverDnSetStream(h, st) != CUSOLVER_STATUS_SUCCESS) return fail(LAROSA_ECUDA, "pca: cusolverDnSetStream");
-    if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, A, (int)d, w, work, (int)lw,
-                         info) != CUSOLVER_STATUS_SUCCESS)
-        return fail(LAROSA_ECUDA, "pca: cusolverDnDsyevd");
-    pca_order_sign_kernel<<<(unsigned)d, 256, 0, st>>>(A, w, (int)d, Q, lam);
-    LAROSA_TRY(cuda_check(cudaGetLastError(), "pca: order/sign"));
-    int hinfo = 0;
-    LAROSA_TRY(cuda_check(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st), "pca: info"));
-    LAROSA_TRY(cuda_check(cudaStreamSynchronize(st), "pca: synchronize"));
-    if (hinfo != 0) return fail(LAROSA_ECUDA, "pca: eigensolver did not converge (info %d)", hinfo);
-    return LAROSA_OK;
+    Carver c(ws);
+    JacobiWs J;
+    carve_jacobi(c, d, &J);
+    const int di = (int)d, n = di + (di & 1), npairs = n / 2;
+    jacobi_init_kernel<<<1024, 256, 0, st>>>(C, J.A, J.V, di, n);
+    LAROSA_TRY(cuda_check(cudaGetLastError(), "pca: init"));
+    // one sweep (n - 1 rounds of disjoint rotations) as a CUDA graph on a private stream
+    cudaStream_t ps;
+    LAROSA_TRY(cuda_check(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "pca: stream"));
+    cudaEvent_t ev;
+    LAROSA_TRY(cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "pca: event"));
+    LAROSA_TRY(cuda_check(cudaEventRecord(ev, st), "pca: event record"));
+    LAROSA_TRY(cuda_check(cudaStreamWaitEvent(ps, ev, 0), "pca: stream wait"));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    larosa_status status = LAROSA_OK;
+    do {
+        if (cudaStreamBeginCapture(ps, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            status = fail(LAROSA_ECUDA, "pca: begin capture");
+            break;
+        }
+        const dim3 ga((unsigned)((npairs + 15) / 16), (unsigned)((npairs + 15) / 16));
+        const unsigned gv = (unsigned)(((size_t)n * npairs + 255) / 256);
+        for (int r = 0; r < n - 1; ++r) {
+            jacobi_angles_kernel<<<(npairs + 127) / 128, 128, 0, ps>>>(J.A, n, r, J.pq, J.cs);
+            jacobi_rotate_a_kernel<<<ga, 256, 0, ps>>>(J.A, n, npairs, J.pq, J.cs);
+            jacobi_rotate_v_kernel<<<gv, 256, 0, ps>>>(J.V, n, npairs, J.pq, J.cs);
+        }
+        jacobi_norms_kernel<<<kJacobiNormCtas, 256, 0, ps>>>(J.A, n, J.part);
+        jacobi_norms_final_kernel<<<1, 32, 0, ps>>>(J.part, kJacobiNormCtas, J.norms);
+        if (cudaStreamEndCapture(ps, &graph) != cudaSuccess || !graph) {
+            status = fail(LAROSA_ECUDA, "pca: end capture");
+            break;
+        }
+        if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            status = fail(LAROSA_ECUDA, "pca: graph instantiate");
+            break;
+        }
+        // sweeps until off(A) <= 1e-12 ||A||_F (the oracle's criterion, Z8), at most 100
+        bool done = false;
+        for (int sweep = 0; sweep < 100 && status == LAROSA_OK; ++sweep) {
+            double h[2];
+            if (cudaGraphLaunch(exec, ps) != cudaSuccess ||
+                cudaMemcpyAsync(h, J.norms, sizeof(h), cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
+                cudaStreamSynchronize(ps) != cudaSuccess) {
+                status = fail(LAROSA_ECUDA, "pca: sweep");
+                break;
+            }
+            if (std::sqrt(h[0]) <= 1e-12 * std::sqrt(h[1])) {
+                done = true;
+                break;
+            }
+        }
+        if (status == LAROSA_OK && !done) status = fail(LAROSA_ECUDA, "pca: Jacobi did not converge in 100 sweeps");
+        if (status != LAROSA_OK) break;
+        eig_rank_kernel<<<(di + 255) / 256, 256, 0, ps>>>(J.A, di, n, J.order);
+        pca_order_sign_kernel<<<(unsigned)di, 256, 0, ps>>>(J.V, J.A, J.order, di, n, Q, lam);
+        if (cudaGetLastError() != cudaSuccess || cudaEventRecord(ev, ps) != cudaSuccess ||
+            cudaStreamWaitEvent(st, ev, 0) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+            status = fail(LAROSA_ECUDA, "pca: order/sign");
+    } while (false);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(ps);
+    return status;
 }
 
 // ============================================================================== N3 W4A16

@@ -400,7 +400,7 @@ def pca_rotation(C: torch.Tensor, stream=None):
     L = lib()
     nb = L.larosa_pca_rotation_workspace_size(d)
     if nb == 0:
-        raise LarosaError(4, "pca_rotation: cuSOLVER unavailable")
+        raise LarosaError(1, "pca_rotation: bad d")
     ws = _ws(("pca", d), nb, C.device)
     Q = torch.empty((d, d), dtype=torch.float32, device=C.device)
     lam = torch.empty((d,), dtype=torch.float32, device=C.device)

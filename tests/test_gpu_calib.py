@@ -74,3 +74,23 @@ def test_calibration_pipeline_invariance():
     y_ref = x @ w64(W)
     y = z @ w64(Wf)
     assert np.linalg.norm(y - y_ref) <= 3e-3 * np.linalg.norm(y_ref)
+
+
+@pytest.mark.parametrize("d", [255, 4096])
+def test_pca_rotation_d4096_vs_lapack(d):
+    """SURVEY §8(f) N1 at the hidden width of the 7B/8B models: C = Q0 diag(lambda) Q0^T with
+    distinct eigenvalues lambda_i = 1 + i (Haar Q0), given in fp32; our GPU Jacobi's Q and lambda
+    against the oracle's build_rotation_lapack on the same fp32 matrix (the fp64 eigenvector
+    perturbation bound eps ||C|| / gap ~ 5e-13 is far below the fp32 output rounding); Q^T Q = I;
+    odd d exercises the phantom index of the round-robin pairing."""
+    q0 = synth.haar_orthogonal(d, 77).double().numpy()
+    lam0 = 1.0 + np.arange(d, dtype=np.float64)
+    C = ((q0 * lam0) @ q0.T).astype(np.float32)
+    C = 0.5 * (C + C.T)
+    q_ref, lam_ref = O.build_rotation_lapack(C.astype(np.float64))
+    Q, lam = LZ.pca_rotation(torch.from_numpy(C).to(DEV))
+    Q, lam = Q.cpu().double().numpy(), lam.cpu().double().numpy()
+    assert np.all(np.diff(lam) <= 0)
+    assert np.max(np.abs(lam - lam_ref)) <= 1e-6 * lam_ref[0]
+    assert np.max(np.abs(Q - q_ref)) <= 1e-5
+    assert np.max(np.abs(Q.T @ Q - np.eye(d))) <= 1e-5

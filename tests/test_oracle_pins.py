@@ -689,3 +689,15 @@ def test_block_site_wiring_hand_built(in_down):
     assert np.allclose(inter["h4"], h4, rtol=1e-13, atol=1e-12)
     r_out = np.array([6.0, 0, 2.5, -0.5, -3, 2, 0, 0]) + s3sq * np.array([-42.0, 0, 0, 0, 0, 0, 36, 55])
     assert np.allclose(out, r_out @ a, rtol=1e-13, atol=1e-13)
+
+
+def test_build_rotation_lapack_equals_jacobi():
+    """build_rotation_lapack (LAPACK eigh as the eigendecomposition step) equals the Jacobi
+    build_rotation on distinct-eigenvalue covariances (same order and sign rule, Z7)."""
+    for d, seed in ((8, 1), (48, 2)):
+        seqs = synth.toy_calibration(d=d, n_seq=8, n_tok=16, seed=seed)
+        C = O.covariance([s.numpy() for s in seqs])
+        q1, l1 = O.build_rotation(C)
+        q2, l2 = O.build_rotation_lapack(C)
+        assert np.max(np.abs(l1 - l2)) <= 1e-12 * l1[0]
+        assert np.max(np.abs(q1 - q2)) <= 1e-9
