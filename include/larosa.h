@@ -57,6 +57,18 @@ typedef enum {
 } larosa_status;
 
 int larosa_abi_version(void);
+
+/* Device-side error bits of a workspace (every call that carves a workspace records here):
+ *   LAROSA_ERR_KEEP_ALL      a SELECT GEMV found its site histogram inconsistent and used the
+ *                            keep-all rule (sparse -> dense; never expected: a bug indicator);
+ *   LAROSA_ERR_FIX_OVERFLOW  a GEMV column could leave the +-2^31 range of the 64-bit fixed point
+ *                            (32 fraction bits) of the deterministic split-K reduction: one of its
+ *                            n partials had |s| >= 2^31 / n (sufficient for no overflow otherwise).
+ * Reads the word into *flags (host), optionally clears it; synchronises the stream.  The
+ * workspace header's last counter word holds it (zero at rest like the others). */
+#define LAROSA_ERR_KEEP_ALL 1u
+#define LAROSA_ERR_FIX_OVERFLOW 2u
+larosa_status larosa_error_flags(void* ws, int32_t clear, uint32_t* flags /* host */, larosa_stream_t stream);
 const char* larosa_status_string(int status);
 /* Thread-local detail of the last non-OK status returned on this thread. */
 const char* larosa_last_error(void);

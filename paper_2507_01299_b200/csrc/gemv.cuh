@@ -166,7 +166,12 @@ struct GemvArgs {
     // partials in rank order and finalises the slice itself (no global accumulators, no ticket)
     int cluster;
     int late_trigger;                  // tuning: 1 = release dependents after the main loop, not at entry
+    uint32_t* err;                     // the workspace's error word (larosa_error_flags) or null
 };
+
+// error bits of a workspace's error word (larosa.h larosa_error_flags)
+constexpr uint32_t kErrKeepAll = 1u;    // SELECT: inconsistent histogram -> the keep-all rule was used
+constexpr uint32_t kErrFixOverflow = 2u;  // a partial sum |s| >= 2^31 does not fit the 64-bit fixed point
 
 __host__ __device__ constexpr size_t gemv_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -195,6 +200,13 @@ __device__ __forceinline__ unsigned long long f_to_fix(float v) {
 }
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// one fixed-point partial into an accumulator.  The sum of a column's gridDim.y partials stays
+// inside the fixed point's +-2^31 when every partial is below 2^31 / gridDim.y: a partial at or
+// above that bound is flagged (a sufficient condition; it may also flag sums that cancel).
+__device__ __forceinline__ void red_fix(unsigned long long* p, float s, uint32_t* err) {
+    if (err && !(fabsf(s) * (float)gridDim.y < 2147483648.0f)) atomicOr(err, kErrFixOverflow);
+    red_add_u64(p, f_to_fix(s));
 }
 __device__ __forceinline__ void red_add_u32(uint32_t* p, uint32_t v) {
     asm volatile("red.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -367,7 +379,8 @@ __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, in
 
 template <int NT>
 __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
-                             unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr, int guess = 0) {
+                             unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr, int guess = 0,
+                             uint32_t* err = nullptr) {
     static_assert(NT >= 64, "two warps");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
@@ -422,7 +435,8 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
             }
             tl_stamp(tl, 8);
             if (!ok1 || !ok2) {
-                flags = kRuleAll;   // inconsistent histogram: keep-all (bounded, never faults)
+                flags = kRuleAll;   // inconsistent histogram: keep-all (bounded, never faults), flagged
+                if (err && lane == 0) atomicOr(err, kErrKeepAll);
             } else {
                 b16 = 256 * cb + fb;
                 if (cnt == rem) {
@@ -565,7 +579,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the CTA's words land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
     compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R,
-                     a.tl, guess);
+                     a.tl, guess, a.err);
     const uint32_t tk = R->tk;
     const int ti = R->ti;
     const int flags = R->flags;
@@ -943,7 +957,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
             float s = 0.f;
 #pragma unroll
             for (int w = 0; w < kGemvWarps; ++w) s += part[((size_t)w * BP + b) * kSliceCols + c];
-            red_add_u64(a.acc + (size_t)b * a.acc_ld + o, f_to_fix(s));
+            red_fix(a.acc + (size_t)b * a.acc_ld + o, s, a.err);
         }
     }
     if (a.epi == EPI_NONE) {

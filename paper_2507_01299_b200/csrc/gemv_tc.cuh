@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
         if (o < a.d_out)
 #pragma unroll
             for (int b = 0; b < BP; ++b)
-                if (b < a.batch) red_add_u64(a.acc + (size_t)b * a.acc_ld + o, f_to_fix(__uint_as_float(v[b])));
+                if (b < a.batch) red_fix(a.acc + (size_t)b * a.acc_ld + o, __uint_as_float(v[b]), a.err);
     }
     tc_fence_before();
     __syncthreads();

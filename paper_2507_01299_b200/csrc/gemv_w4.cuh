@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
             float s = 0.f;
 #pragma unroll
             for (int w = 0; w < kGemvWarps; ++w) s += part[(size_t)w * kW4SliceCols + c];
-            red_add_u64(a.acc + o, f_to_fix(s));
+            red_fix(a.acc + o, s, a.err);
         }
     }
     __syncthreads();

@@ -127,6 +127,7 @@ constexpr size_t kCounterHeaderWords = 8192;   // attention tickets
 constexpr size_t kAttnCounterBase = 0;        // [0, 4096): attention group tickets
 constexpr size_t kGemvTicketBase = 4096;      // + 256 j: slice tickets of the j-th epilogue GEMV
 constexpr size_t kPrepBarrier = 6000;         // 2 words: grid barrier of select_prep_kernel
+constexpr size_t kErrWord = kCounterHeaderWords - 1;   // error bits (kErrKeepAll, kErrFixOverflow)
 
 struct Carver {
     char* base;      // nullptr -> size query
@@ -374,9 +375,17 @@ larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStre
     }
 }
 
+// the error word of the workspace the current API call carved (one call at a time per host thread)
+thread_local uint32_t* t_err_word = nullptr;
+struct ErrScope {
+    uint32_t* prev;
+    explicit ErrScope(const Carver& c) : prev(t_err_word) { t_err_word = c.counters(kErrWord); }
+    ~ErrScope() { t_err_word = prev; }
+};
 GemvArgs gemv_args_base() {
     GemvArgs a;
     memset(&a, 0, sizeof(a));
+    a.err = t_err_word;
     return a;
 }
 
@@ -495,6 +504,15 @@ larosa_status launch_union(const uint32_t* mask, int nwords, int batch, int bp, 
 // ============================================================================== basics
 extern "C" int larosa_abi_version(void) { return LAROSA_ABI_VERSION; }
 
+extern "C" larosa_status larosa_error_flags(void* ws, int32_t clear, uint32_t* flags, larosa_stream_t stream) {
+    if (!ws || !flags) return fail(LAROSA_EINVAL, "error_flags: NULL pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint32_t* w = static_cast<uint32_t*>(ws) + kErrWord;
+    LAROSA_TRY(cuda_check(cudaMemcpyAsync(flags, w, sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "error_flags: read"));
+    if (clear) LAROSA_TRY(cuda_check(cudaMemsetAsync(w, 0, sizeof(uint32_t), st), "error_flags: clear"));
+    return cuda_check(cudaStreamSynchronize(st), "error_flags: synchronize");
+}
+
 extern "C" const char* larosa_status_string(int s) {
     switch (s) {
         case LAROSA_OK: return "LAROSA_OK";
@@ -585,6 +603,7 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
     Carver c(ws);
+    ErrScope err_scope(c);
     unsigned long long* acc = nullptr;
     uint32_t* mask = nullptr;
     int32_t* rows = nullptr;
@@ -675,6 +694,7 @@ static larosa_status topk_sparse_gemv_impl(const float* x, int64_t d_in, int64_t
     const size_t need = larosa_topk_sparse_gemv_workspace_size(d_in, d_out);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "topk_sparse_gemv: workspace %zu < %zu", ws_bytes, need);
     Carver c(ws);
+    ErrScope err_scope(c);
     unsigned long long* acc;
     SiteSel sel;
     carve_topk_gemv(c, d_in, d_out, &acc, &sel);
@@ -775,6 +795,7 @@ extern "C" larosa_status larosa_rotate_topk(const float* x, const uint16_t* R, i
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "rotate_topk: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
+    ErrScope err_scope(c);
     unsigned long long* acc;
     float* xbuf;
     carve_rotate_topk(c, batch, d, &acc, &xbuf);
@@ -1036,13 +1057,14 @@ extern "C" larosa_status larosa_lm_head(const float* resid, int32_t batch, int64
     if (vocab % 8 || d % 8) return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab and d must be multiples of 8");
     // one slice ticket per column slice: 128-column slices on the tcgen05 path (batch >= 8), 256 otherwise;
     // size the check by the narrower one so either path fits the counter header
-    if ((vocab + kTcCols - 1) / kTcCols > (int64_t)(kCounterHeaderWords - kGemvTicketBase))
+    if ((vocab + kTcCols - 1) / kTcCols > (int64_t)(kPrepBarrier - kGemvTicketBase))
         return fail(LAROSA_EUNSUPPORTED, "lm_head: vocab too large");
     if (!aligned16(H) || (logits && !aligned16(logits))) return fail(LAROSA_EINVAL, "lm_head: H, logits must be 16-byte aligned");
     const size_t need = larosa_lm_head_workspace_size(batch, d, vocab);
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "lm_head: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
+    ErrScope err_scope(c);
     unsigned long long* acc;
     float *xs, *lg;
     carve_lm_head(c, batch, d, vocab, &acc, &xs, &lg);
@@ -1228,6 +1250,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     const int B = s->batch, bp = pad_batch(B);
     const bool fused = B == 1;
     Carver c(ws);
+    ErrScope err_scope(c);
     LayerWs W;
     carve_layer(c, L, B, s->max_ctx, &W);
     larosa_layer_taps T;
@@ -1571,6 +1594,7 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     const int B = S.batch, bp = pad_batch(B);
     const bool fused = B == 1;
     Carver c(ws);
+    ErrScope err_scope(c);
     ShardWs W;
     carve_shard(c, S, max_ctx > 0 ? max_ctx : 1, &W);
     const int r = sh->rank;
@@ -1802,6 +1826,7 @@ extern "C" larosa_status larosa_pca_rotation(const float* C, int64_t d, float* Q
     std::lock_guard<std::mutex> lk(g_solver_mu);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
+    ErrScope err_scope(c);
     JacobiWs J;
     carve_jacobi(c, d, &J);
     const int di = (int)d, n = di + (di & 1), npairs = n / 2;
@@ -1903,6 +1928,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "topk_sparse_gemv_w4: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
+    ErrScope err_scope(c);
     unsigned long long* acc;
     SiteSel sel;
     carve_topk_gemv(c, d_in, d_out, &acc, &sel);
@@ -1983,6 +2009,7 @@ extern "C" larosa_status larosa_prefill_sparse_gemm(const float* X, int64_t n_to
     if (!ws || ws_bytes < need) return fail(LAROSA_EWORKSPACE, "prefill_sparse_gemm: workspace %zu < %zu", ws_bytes, need);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Carver c(ws);
+    ErrScope err_scope(c);
     PrefillWs P;
     carve_prefill(c, n_tok, d_in, split, &P);
     // every token's exact Top-K (Z10) + RMS scale -> masked bf16 rows and per-block "any kept"

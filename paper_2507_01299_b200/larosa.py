@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
                                                   ctypes.POINTER(ShardC), _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                                   _c_i64, _vp, ctypes.c_size_t, _vp]
     L.larosa_shard_gather_permute.argtypes = [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp]
+    L.larosa_error_flags.argtypes = [_vp, _c_i32, ctypes.POINTER(ctypes.c_uint32), _vp]
+    L.larosa_error_flags.restype = ctypes.c_int
     L.larosa_argmax.argtypes = [_vp, _c_i32, _c_i64, _c_i64, _vp, _vp]
     L.larosa_debug_set_layer_phases.argtypes = [ctypes.c_int]
     L.larosa_debug_set_layer_phases.restype = None
@@ -272,7 +274,8 @@ def rotate_topk(x: torch.Tensor, R: Optional[torch.Tensor], k: int, rms_eps: flo
 
 
 def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Optional[torch.Tensor] = None,
-                d_out: Optional[int] = None, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                d_out: Optional[int] = None, out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
     """y[b] = bias + sum_t vals[b,t] W[idx[b,t]]  (W: bf16 bits [d_in, ld])."""
     d_in, ld = W.shape
     d_out = ld if d_out is None else d_out
@@ -283,7 +286,8 @@ def sparse_gemv(W: torch.Tensor, idx: torch.Tensor, vals: torch.Tensor, bias: Op
     y = out if out is not None else torch.empty((B, d_out), dtype=torch.float32, device=dev)
     L = lib()
     nb = L.larosa_sparse_gemv_workspace_size(B, d_in, k, d_out)
-    ws = _ws(("sparse_gemv", B, d_in, d_out), nb, dev)
+    if ws is None:
+        ws = _ws(("sparse_gemv", B, d_in, d_out), nb, dev)
     _check(L.larosa_sparse_gemv(_ptr(W), d_in, d_out, ld, _ptr(idx) if k else None, _ptr(vals) if k else None,
                                 B, k, _ptr(bias), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)))
     return y
@@ -406,6 +410,26 @@ def pca_rotation(C: torch.Tensor, stream=None):
     lam = torch.empty((d,), dtype=torch.float32, device=C.device)
     _check(L.larosa_pca_rotation(_ptr(C.contiguous()), d, _ptr(Q), _ptr(lam), _ptr(ws), ws.numel(), _stream(stream)))
     return Q, lam
+
+
+LAROSA_ERR_KEEP_ALL = 1
+LAROSA_ERR_FIX_OVERFLOW = 2
+
+
+def error_flags(ws: torch.Tensor, clear: bool = True, stream=None) -> int:
+    """The workspace's device error bits (LAROSA_ERR_*); synchronises the stream."""
+    v = ctypes.c_uint32(0)
+    _check(lib().larosa_error_flags(_ptr(ws), int(clear), ctypes.byref(v), _stream(stream)))
+    return int(v.value)
+
+
+_HEADER_WS = ("rotate_topk", "sparse_gemv", "topk_sparse_gemv", "topk_sparse_gemv_w4", "prefill", "pca", "lm_head",
+              "layer")   # call kinds whose workspace starts with the counter header (larosa_error_flags)
+
+
+def workspaces():
+    """Every cached workspace buffer of a call kind that carries the error word (for tests)."""
+    return [w.buf for (tag, _), w in _WS.items() if w.buf is not None and tag[0] in _HEADER_WS]
 
 
 def shard_gather_permute(gathered: torch.Tensor, world: int, batch: int, out: torch.Tensor, stream=None):

@@ -25,3 +25,19 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _device_error_flags(request):
+    """After every GPU test: no workspace the binding cached may carry a device error bit
+    (larosa_error_flags: keep-all fallback of an inconsistent Top-K histogram, fixed-point
+    overflow).  Tests that provoke one on purpose clear it themselves."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import torch
+    if not torch.cuda.is_available():
+        return
+    from paper_2507_01299_b200 import larosa as LZ
+    bad = [(i, f) for i, ws in enumerate(LZ.workspaces()) for f in [LZ.error_flags(ws)] if f]
+    assert not bad, f"device error flags set in cached workspaces: {bad}"

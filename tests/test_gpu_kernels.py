@@ -337,3 +337,29 @@ def test_topk_sparse_gemv_max_dim(d_in, k):
     with pytest.raises(LZ.LarosaError):
         LZ.topk_sparse_gemv(torch.zeros(32776, device=DEV), 8, torch.zeros((32776, 256), dtype=torch.int16,
                                                                            device=DEV))
+
+
+
+def test_error_flags_fixed_point_overflow_and_keep_all():
+    """larosa_error_flags: a partial sum beyond the 64-bit fixed point (|s| >= 2^31) sets
+    LAROSA_ERR_FIX_OVERFLOW; a fused Top-K GEMV told its selection data is prepared when the
+    workspace holds none (an all-zero histogram, inconsistent with k) takes the keep-all rule and
+    sets LAROSA_ERR_KEEP_ALL; normal calls leave the word 0."""
+    d_in, d_out = 256, 256
+    W = torch.ones((d_in, d_out), dtype=torch.bfloat16).view(torch.int16).to(DEV)
+    x = torch.full((1, d_in), 1.0e8, device=DEV)
+    idx = torch.arange(d_in, dtype=torch.int32, device=DEV).view(1, -1)
+    ws = torch.zeros(LZ.lib().larosa_sparse_gemv_workspace_size(1, d_in, d_in, d_out), dtype=torch.uint8, device=DEV)
+    y = torch.empty((1, d_out), device=DEV)
+    LZ.sparse_gemv(W, idx, x, out=y, ws=ws)          # 256 x 1e8 per column: > 2^31
+    assert LZ.error_flags(ws) & LZ.LAROSA_ERR_FIX_OVERFLOW
+    assert LZ.error_flags(ws) == 0                     # cleared by the first read
+    LZ.sparse_gemv(W, idx, x * 1e-8, out=y, ws=ws)
+    assert LZ.error_flags(ws) == 0
+    ws2 = LZ.topk_sparse_gemv_workspace(d_in, d_out, DEV)
+    xv = torch.randn((d_in,), device=DEV)
+    y2 = torch.empty((d_out,), device=DEV)
+    LZ.topk_sparse_gemv(xv, 64, W, out=y2, ws=ws2, prepared=True)   # nothing was prepared
+    assert LZ.error_flags(ws2) & LZ.LAROSA_ERR_KEEP_ALL
+    LZ.topk_sparse_gemv(xv, 64, W, out=y2, ws=ws2, prepared=False)
+    assert LZ.error_flags(ws2) == 0
