@@ -167,6 +167,7 @@ struct GemvArgs {
     int cluster;
     int late_trigger;                  // tuning: 1 = release dependents after the main loop, not at entry
     uint32_t* err;                     // the workspace's error word (larosa_error_flags) or null
+    const void* img;                   // batch >= 8, contiguous rows: the pre-built token operand (gemv_img.cuh)
 };
 
 // error bits of a workspace's error word (larosa.h larosa_error_flags)

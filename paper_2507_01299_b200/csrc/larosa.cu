@@ -21,6 +21,7 @@
 #include "calib.cuh"
 #include "gemv_w4.cuh"
 #include "prefill_tc.cuh"
+#include "gemv_img.cuh"
 
 #include <mutex>
 #include <set>
@@ -351,6 +352,46 @@ larosa_status launch_gemv_tc_bm(const GemvArgs& a, cudaStream_t st) {
         return fail(LAROSA_ECUDA, "gemv_tc: cuTensorMapEncodeTiled failed for the weight matrix");
     return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kTcThreads), p.smem, st, aa, tm), "gemv_tc launch");
 }
+// batch >= 8 with a pre-built token image (gemv_img.cuh): weight tiles by TMA, the image by bulk copy
+GemvPlan plan_gemv_img(int64_t d_out, int64_t d_in) {
+    GemvPlan p;
+    p.n_slices = (int)((d_out + kTcCols - 1) / kTcCols);
+    static const int target_pct = env_int("LAROSA_IMG_TARGET_PCT", 200);   // CTAs per SM x 100
+    const int target = sm_count() * target_pct / 100;
+    const int by_rows = (int)std::max<int64_t>(1, d_in / 64);
+    p.n_splits = std::max(1, std::min(target / p.n_slices, by_rows));
+    p.list_cap = 0;
+    p.smem = gemv_img_smem_bytes();
+    return p;
+}
+template <int BP>
+larosa_status launch_gemv_img(const GemvArgs& a, cudaStream_t st) {
+    const GemvPlan p = plan_gemv_img(a.d_out, a.d_in);
+    auto kern = gemv_img_kernel<BP>;
+    LAROSA_TRY(cuda_check(allow_smem(kern, p.smem), "cudaFuncSetAttribute(gemv_img)"));
+    GemvArgs aa = a;
+    aa.n_splits = p.n_splits;
+    CUtensorMap tm;
+    if (!make_w_mn_map(&tm, a.W, a.d_in, a.d_out, a.ld))
+        return fail(LAROSA_ECUDA, "gemv_img: cuTensorMapEncodeTiled failed for the weight matrix");
+    return cuda_check(launch(kern, dim3(p.n_slices, p.n_splits), dim3(kImgThreads), p.smem, st, aa, tm), "gemv_img launch");
+}
+size_t img_bytes(int64_t d) { return (size_t)((d + kTcChunk - 1) / kTcChunk) * kImgChunkBytes; }
+larosa_status launch_rule_image(const float* x, int64_t ldx, int64_t d, int64_t k, float eps, int batch, ThreshOut* rule,
+                                void* img, void* img_raw, cudaStream_t st) {
+    const size_t smem = rule_image_smem_bytes((int)d);
+    LAROSA_TRY(cuda_check(allow_smem(rule_image_kernel, smem), "cudaFuncSetAttribute(rule_image)"));
+    return cuda_check(launch(rule_image_kernel, dim3(batch), dim3(kRiThreads), smem, st, x, ldx, (int)d, (int)k, eps, rule,
+                             static_cast<unsigned char*>(img), static_cast<unsigned char*>(img_raw)),
+                      "rule_image launch");
+}
+larosa_status launch_dense_image(const float* x, int64_t ldx, int64_t d, int batch, void* img, cudaStream_t st) {
+    const int groups = (int)((d + 7) / 8);
+    return cuda_check(launch(dense_image_kernel, dim3((unsigned)((groups + 255) / 256), batch), dim3(256), 0, st, x, ldx,
+                             (int)d, static_cast<unsigned char*>(img)),
+                      "dense_image launch");
+}
+
 template <int BP>
 larosa_status launch_gemv_tc(const GemvArgs& a, cudaStream_t st) {
     switch (a.mode) {
@@ -362,6 +403,10 @@ larosa_status launch_gemv_tc(const GemvArgs& a, cudaStream_t st) {
 }
 
 larosa_status launch_gemv(const GemvArgs& a, const GemvPlan& p, int bp, cudaStream_t st) {
+    if (use_tc_gemv(bp) && a.img && (a.mode == GEMV_THRESH || a.mode == GEMV_DENSE)) {
+        if (bp == 8) return launch_gemv_img<8>(a, st);
+        return launch_gemv_img<16>(a, st);
+    }
     if (use_tc_gemv(bp) && a.mode != GEMV_SELECT) {
         if (bp == 8) return launch_gemv_tc<8>(a, st);
         return launch_gemv_tc<16>(a, st);
@@ -1032,13 +1077,15 @@ extern "C" larosa_status larosa_embed(const uint16_t* E, int64_t vocab, int64_t 
 }
 
 static void carve_lm_head(Carver& c, int32_t batch, int64_t d, int64_t vocab, unsigned long long** acc, float** xs,
-                          float** logits) {
+                          float** logits, unsigned char** img = nullptr) {
     unsigned long long* a = c.take<unsigned long long>((size_t)batch * vocab);
     float* x = c.take<float>((size_t)batch * d);
     float* l = c.take<float>((size_t)batch * vocab);
+    unsigned char* im = batch >= 8 ? c.take<unsigned char>(img_bytes(d)) : nullptr;
     if (acc) *acc = a;
     if (xs) *xs = x;
     if (logits) *logits = l;
+    if (img) *img = im;
 }
 
 extern "C" size_t larosa_lm_head_workspace_size(int32_t batch, int64_t d, int64_t vocab) {
@@ -1067,13 +1114,18 @@ extern "C" larosa_status larosa_lm_head(const float* resid, int32_t batch, int64
     ErrScope err_scope(c);
     unsigned long long* acc;
     float *xs, *lg;
-    carve_lm_head(c, batch, d, vocab, &acc, &xs, &lg);
+    unsigned char* img;
+    carve_lm_head(c, batch, d, vocab, &acc, &xs, &lg, &img);
     if (!logits) logits = lg;
     LAROSA_TRY(cuda_check(launch(rms_rows_kernel, dim3(batch), dim3(kRowThreads), 0, st, resid, (int)d, rms_eps, xs),
                           "rms launch"));
     const int bp = pad_batch(batch);
     const GemvPlan p = plan_gemv(vocab, d, bp, GEMV_DENSE, d);
     GemvArgs a = gemv_args_base();
+    if (use_tc_gemv(bp) && img) {   // the scaled rows as the tensor-core GEMV's token image
+        LAROSA_TRY(launch_dense_image(xs, d, d, batch, img, st));
+        a.img = img;
+    }
     a.W = H;
     a.ld = vocab;
     a.d_out = (int)vocab;
@@ -1107,6 +1159,8 @@ struct LayerWs {
     float* attn_part;
     unsigned* attn_cnt;
     unsigned* tickets[4]; // slice tickets of the O, gate|up, down, adapter GEMV epilogues
+    unsigned char* img[4];   // batch >= 8: the sites' token operand images (gemv_img.cuh)
+    unsigned char* img_raw[2];   // batch >= 8: unmasked images of h1 (A_mid) and h3 (the adapter)
 };
 
 struct LayerDims {
@@ -1164,6 +1218,14 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
     o->attn_part = c.take<float>((size_t)batch * L.hq * nch * (L.hd + 2));
     o->attn_cnt = c.counters(kAttnCounterBase);
     for (int j = 0; j < 4; ++j) o->tickets[j] = c.counters(kGemvTicketBase + 256 * j);
+    if (batch >= 8) {
+        const int64_t din[4] = {L.d, L.nq, L.d, L.inter};
+        for (int j = 0; j < 4; ++j) o->img[j] = c.take<unsigned char>(img_bytes(din[j]));
+        for (int j = 0; j < 2; ++j) o->img_raw[j] = c.take<unsigned char>(img_bytes(L.d));
+    } else {
+        for (int j = 0; j < 4; ++j) o->img[j] = nullptr;
+        o->img_raw[0] = o->img_raw[1] = nullptr;
+    }
 }
 
 larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_plan* p, const larosa_layer_state* s) {
@@ -1274,16 +1336,33 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         tk.vals = vals;
         return launch_topk(tk, B, st);
     };
-    // batch > 1: every token's selection rule from the cluster Top-K kernel
+    // batch > 1: every token's selection rule (and at batch >= 8 the site's token image; for h1 / h3
+    // also the unmasked image the dense A_mid / adapter GEMV reads) from one CTA per token
+    // tuning (B = 16 LLaMA3-8B layer, in graph: 0 180 us, 1 233 us, 2 172 us): 1 = rule_image_kernel
+    // (rule + image in one CTA per token, large shared memory: no early residency), 2 = the cluster Top-K rule +
+    // rule_apply_image_kernel, 0 = the cluster Top-K rule and gemv_tc (no image)
+    static const int rule_kernel = env_int("LAROSA_RULE_KERNEL", 2);
+    const bool img_path = !fused && use_tc_gemv(bp) && W.img[0] != nullptr && rule_kernel != 0;
     auto rule_topk = [&](int si, const float* x, int64_t din, int64_t k, float eps) -> larosa_status {
-        TopkKernelArgs r = topk_args_base();
-        r.x = x;
-        r.ldx = din;
-        r.d = (int)din;
-        r.k = (int)k;
-        r.rms_eps = eps;
-        r.rule_out = W.thr[si];
-        return launch_topk(r, B, st);
+        void* raw = nullptr;
+        if (img_path && si == 0 && w->adapter_mid) raw = W.img_raw[0];
+        if (img_path && si == 2 && w->adapter && w->adapter_in_down) raw = W.img_raw[1];
+        if (rule_kernel != 1) {   // the cluster Top-K rule (+ the image from it, mode 2)
+            TopkKernelArgs r = topk_args_base();
+            r.x = x;
+            r.ldx = din;
+            r.d = (int)din;
+            r.k = (int)k;
+            r.rms_eps = eps;
+            r.rule_out = W.thr[si];
+            LAROSA_TRY(launch_topk(r, B, st));
+            if (!img_path) return LAROSA_OK;
+            const int groups = (int)((din + 7) / 8);
+            return cuda_check(launch(rule_apply_image_kernel, dim3((unsigned)((groups + 255) / 256), B), dim3(256), 0, st,
+                                     x, din, (int)din, (const ThreshOut*)W.thr[si], W.img[si], (unsigned char*)raw),
+                              "rule_apply_image launch");
+        }
+        return launch_rule_image(x, din, din, k, eps, B, W.thr[si], img_path ? W.img[si] : nullptr, raw, st);
     };
     // the GEMV of site si on the site vector x (SELECT at batch 1, THRESH otherwise)
     auto site_gemv = [&](int si, const float* x, int64_t din, int64_t k, float eps, const uint16_t* Wt, int64_t dout,
@@ -1308,6 +1387,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         } else {
             a.mode = GEMV_THRESH;
             a.thr = W.thr[si];
+            if (img_path) a.img = W.img[si];
         }
         return a;
     };
@@ -1409,6 +1489,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             b.batch = B;
             b.acc = W.acc_o;
             b.acc_ld = L.d;
+            if (img_path) b.img = W.img_raw[0];
             epi(b, 0, epi_mode, nullptr, W.rmid, 2);
             LAROSA_TRY(launch_gemv(b, plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d), bp, st));
         } else {
@@ -1459,6 +1540,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             b.batch = B;
             b.acc = W.acc_down;
             b.acc_ld = L.d;
+            if (img_path) b.img = W.img_raw[1];
             epi(b, 3, EPI_STORE, nullptr, s->resid, 0);
             b.tl = tl_slot(5);
             LAROSA_TRY(launch_gemv(b, plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d), bp, st));
@@ -1511,6 +1593,7 @@ namespace {
 struct ShardWs {
     SiteSel sel;                       // batch 1: selection data of the phase input (rebuilt each phase)
     ThreshOut* thr;                    // batch > 1: every token's Top-K rule of the phase input
+    unsigned char *img, *img2;         // batch >= 8: token images of the phase input / of resid
     unsigned long long* acc;           // local projection accumulators [batch][largest phase]
     float* attn_part;
     unsigned* attn_cnt;
@@ -1546,6 +1629,8 @@ void carve_shard(Carver& c, const ShardDims& S, int64_t max_ctx, ShardWs* o) {
     q->sel.pool = c.take<uint2>((size_t)kSelFine * kPoolCap);
     q->sel.ssq = c.take<float>((size_t)(dmax + kSliceCols - 1) / kSliceCols);
     q->thr = c.take<ThreshOut>((size_t)S.batch);
+    q->img = S.batch >= 8 ? c.take<unsigned char>(img_bytes(dmax)) : nullptr;
+    q->img2 = S.batch >= 8 ? c.take<unsigned char>(img_bytes(S.d)) : nullptr;
     const int ch = attn_chunk(max_ctx, (int)(S.batch * S.hq_l));
     const int nch = (int)((max_ctx + ch - 1) / ch);
     q->attn_part = c.take<float>((size_t)S.batch * S.hq_l * nch * (S.hd + 2));
@@ -1629,9 +1714,14 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     a.acc_ld = dout;
     GemvPlan p;
     bool dense2 = false;   // batch > 1, merged phase 3: a dense adapter GEMV into the same accumulators
+    const bool img_path = !fused && use_tc_gemv(bp) && W.img;
     if (phase == 4) {
         a.mode = GEMV_DENSE;
         p = plan_gemv(dout, din, bp, GEMV_DENSE, din);
+        if (img_path) {
+            LAROSA_TRY(launch_dense_image(x, din, din, B, W.img, st));
+            a.img = W.img;
+        }
     } else if (fused) {
         // the gathered vector is identical on every rank -> identical selection data
         SiteSel sel = W.sel;
@@ -1654,7 +1744,7 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     } else {
         // batch > 1: every token's exact rule from the cluster Top-K kernel on the gathered input
         // (identical on every rank), then the union GEMV (THRESH; tcgen05 at batch >= 8)
-        TopkKernelArgs tk = topk_args_base();
+        TopkKernelArgs tk = topk_args_base();   // every token's rule (the cluster Top-K kernel)
         tk.x = x;
         tk.ldx = din;
         tk.d = (int)din;
@@ -1662,8 +1752,15 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         tk.rms_eps = eps;
         tk.rule_out = W.thr;
         LAROSA_TRY(launch_topk(tk, B, st));
+        if (img_path) {                          // and the token image from it
+            const int groups = (int)((din + 7) / 8);
+            LAROSA_TRY(cuda_check(launch(rule_apply_image_kernel, dim3((unsigned)((groups + 255) / 256), B), dim3(256), 0,
+                                         st, x, din, (int)din, (const ThreshOut*)W.thr, W.img, (unsigned char*)nullptr),
+                                  "rule_apply_image launch"));
+        }
         a.mode = GEMV_THRESH;
         a.thr = W.thr;
+        if (img_path) a.img = W.img;
         p = plan_gemv(dout, din, bp, GEMV_THRESH, din);
         dense2 = phase == 3 && merged;
     }
@@ -1696,6 +1793,10 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         b2.tickets = W.tickets;
         b2.out = out;
         b2.out_ld = S.dl;
+        if (img_path) {
+            LAROSA_TRY(launch_dense_image(resid, S.d, S.d, B, W.img2, st));
+            b2.img = W.img2;
+        }
         return launch_gemv(b2, plan_gemv(dout, S.d, bp, GEMV_DENSE, S.d), bp, st);
     }
     // phase 0: QKV over the local heads (EPI_NONE) then attention writes the local h2
