@@ -50,6 +50,23 @@ __host__ __device__ inline size_t attn_smem_bytes(int hd) {
     return sizeof(float) * ((size_t)hd + 8 + 4 * (size_t)hd) + 4 * (size_t)hd + 16 + sizeof(float) * ((size_t)hd + 2);
 }
 
+// RoPE (HF rotate_half): cos / sin of the pair (i, i + hd/2) at position p -- the
+// inverse frequency and the angle in fp64, reduced to [-pi, pi], then fp32 sincos (as rope_pair)
+__device__ __forceinline__ float2 rope_cs(int i, int hd, int p, float theta) {
+    const double inv_freq = exp(-(2.0 * i / hd) * log((double)theta));
+    double ang = (double)p * inv_freq;
+    ang = fma(-6.283185307179586476925, rint(ang * 0.15915494309189533577), ang);
+    float sn, cn;
+    sincosf((float)ang, &sn, &cn);
+    return make_float2(cn, sn);
+}
+__device__ __forceinline__ void rope_apply(float& y1, float& y2, float2 cs) {
+    const float r1 = fmaf(y1, cs.x, -y2 * cs.y);
+    const float r2 = fmaf(y2, cs.x, y1 * cs.y);
+    y1 = r1;
+    y2 = r2;
+}
+
 // RoPE (HF rotate_half) of the pair (i, i + hd/2) at position p, in fp64
 // (inverse frequency and angle in fp64, reduced to [-pi, pi] in fp64, then fp32 sincos:
 // accurate to a few fp32 ulp at any position, without the long fp64 sincos routine)
@@ -364,9 +381,10 @@ constexpr int kAgPos = 16;                          // positions per warp
 constexpr int kAgMaxCtx = kAgWarps * kAgPos;        // 256
 __host__ __device__ inline size_t attn_group_smem_bytes(int hd, int hpc) {
     // V rows bf16 [256][hd] + q [hpc][hd] + (m, l) [16][hpc][2] + o [16][hpc][hd] (fp32) + new k/v
-    // bf16 [2][hd] + flags
+    // bf16 [2][hd] + flags + the RoPE (cos, sin) table [hd/2]
     return 2 * (size_t)kAgMaxCtx * hd +
-           sizeof(float) * ((size_t)hpc * hd + 32 * (size_t)hpc + 16 * (size_t)hpc * hd) + 4 * (size_t)hd + 16;
+           sizeof(float) * ((size_t)hpc * hd + 32 * (size_t)hpc + 16 * (size_t)hpc * hd) + 4 * (size_t)hd + 16 +
+           sizeof(float2) * (size_t)hd / 2;
 }
 
 template <int DPL>
@@ -381,6 +399,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
     float* so = sml + 32 * hpc;                    // [16][hpc][hd]
     uint16_t* snew = reinterpret_cast<uint16_t*>(so + 16 * hpc * hd);   // [2][hd]
     int* sflag = reinterpret_cast<int*>(snew + 2 * hd);
+    float2* scs = reinterpret_cast<float2*>(sflag + 4);                  // [hd/2] RoPE (cos, sin)
     const int u = blockIdx.x;
     const int b = u / (a.hkv * nsub), g = (u / nsub) % a.hkv, hs = u % nsub;
     const int h0 = g * G + hs * hpc;
@@ -419,9 +438,12 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
         }
         cp_async_commit();
     }
+    // the rotation angles depend on the position only (not on the previous kernel)
+    for (int i = tid; i < half; i += kAgThreads) scs[i] = rope_cs(i, hd, pnew, a.theta);
     pdl_wait();
     pdl_trigger();
     tl_stamp(a.tl, 1);
+    __syncthreads();
     if (a.zero_hist) {
         const int nct = gridDim.x;
         for (int i = blockIdx.x * kAgThreads + tid; i < a.zero_words; i += nct * kAgThreads) a.zero_hist[i] = 0u;
@@ -434,7 +456,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
         const int hh = i / half, j = i % half;
         const int col = (h0 + hh) * hd + j;
         float y1 = yval(col), y2 = yval(col + half);
-        rope_pair(y1, y2, j, hd, pnew, a.theta);
+        rope_apply(y1, y2, scs[j]);
         sq[hh * hd + j] = y1;
         sq[hh * hd + j + half] = y2;
         if (a.q_out) {
@@ -448,7 +470,7 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
         uint16_t* vdst = a.vc + kvbase + (size_t)pnew * hd;
         for (int i = tid; i < half; i += kAgThreads) {
             float y1 = yval(nq + g * hd + i), y2 = yval(nq + g * hd + i + half);
-            rope_pair(y1, y2, i, hd, pnew, a.theta);
+            rope_apply(y1, y2, scs[i]);
             const uint16_t k1 = f2bf16_rne(y1), k2 = f2bf16_rne(y2);
             snew[i] = k1;
             snew[i + half] = k2;

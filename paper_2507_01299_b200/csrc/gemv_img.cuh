@@ -391,6 +391,159 @@ __global__ void __launch_bounds__(kRiThreads) rule_image_kernel(const float* __r
     }
 }
 
+// Register-resident variant (LAROSA_RULE_KERNEL=3): x_b lives in registers (EPT values per thread,
+// element e * 512 + tid), so the CTA needs only the 16 KB histogram in shared memory and can become
+// resident while the producer GEMV still runs (programmatic dependent launch).  Same rule: 3-level
+// radix select, then the need-th lowest index among keys equal to the k-th (the equal keys are
+// compacted -- usually one -- and warp 0 picks; a bitwise index search over block counts if more
+// than kRiEqCap share the key).  RMS: per-thread sums in element order, fixed-order tree.  The image
+// is written value by value (2-byte stores, 8 consecutive lanes fill one 16-byte group).
+constexpr int kRiEqCap = 1024;
+template <int EPT>
+__global__ void __launch_bounds__(kRiThreads) rule_image_reg_kernel(const float* __restrict__ X, int64_t ldx, int d,
+                                                                    int k, float eps, ThreshOut* __restrict__ rule,
+                                                                    unsigned char* __restrict__ img,
+                                                                    unsigned char* __restrict__ img_raw) {
+    __shared__ int hist[kRiBins];
+    __shared__ int eqi[kRiEqCap];
+    __shared__ int misc[32];
+    __shared__ int wsum[16];
+    __shared__ float fred[16];
+    constexpr int NW = kRiThreads / 32;
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < kRiBins; i += kRiThreads) hist[i] = 0;
+    if (tid < 32) misc[tid] = 0;
+    pdl_wait();
+    pdl_trigger();
+    const float* x = X + (size_t)b * ldx;
+    float v[EPT];
+    uint32_t key[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const int i = e * kRiThreads + tid;
+        v[e] = i < d ? x[i] : 0.f;
+        key[e] = i < d ? key_of(v[e]) : 0xffffffffu;   // past the end: never binned, never kept
+    }
+    __syncthreads();
+    uint32_t tk = 0u;
+    int ti = 0x7fffffff;
+    if (k <= 0) {
+        tk = 0xffffffffu;
+        ti = -1;
+    } else if (k < d) {
+        uint32_t prefix = 0u, pmask = 0u;
+        int rank = k;
+#pragma unroll 1
+        for (int lv = 0; lv < 3; ++lv) {
+            const int sh = lv == 0 ? 19 : (lv == 1 ? 7 : 0);
+            const uint32_t wm = lv == 2 ? 0x7fu : 0xfffu;
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const bool ok = key[e] != 0xffffffffu && (key[e] & pmask) == prefix;
+                const uint32_t bin = ok ? (key[e] >> sh) & wm : 0xffffffffu;
+                const unsigned act = __ballot_sync(0xffffffffu, ok);
+                if (ok) {
+                    const unsigned peers = __match_any_sync(act, bin);
+                    if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+                }
+            }
+            __syncthreads();
+            ri_find(hist, rank, misc, wsum);
+            prefix |= (uint32_t)misc[0] << sh;
+            pmask |= wm << sh;
+            rank = misc[1];
+            for (int i = tid; i < kRiBins; i += kRiThreads) hist[i] = 0;
+            __syncthreads();
+        }
+        tk = prefix;
+        const int need = rank;
+        // compact the indices of the keys equal to tk
+#pragma unroll
+        for (int e = 0; e < EPT; ++e)
+            if (key[e] == tk) {
+                const int slot = atomicAdd(&misc[4], 1);
+                if (slot < kRiEqCap) eqi[slot] = e * kRiThreads + tid;
+            }
+        __syncthreads();
+        const int neq = misc[4];
+        if (neq <= kRiEqCap) {
+            if (wid == 0) {   // the need-th smallest index: bitwise search over the index bits
+                int idx = 0;
+#pragma unroll 1
+                for (int bit = 15; bit >= 0; --bit) {
+                    const int cnd = idx | (1 << bit);
+                    int n = 0;
+                    for (int q = lane; q < neq; q += 32) n += eqi[q] < cnd;
+                    n = __reduce_add_sync(0xffffffffu, n);
+                    if (n < need) idx = cnd;
+                }
+                if (lane == 0) misc[5] = idx;
+            }
+        } else {
+#pragma unroll 1
+            for (int bit = 15; bit >= 0; --bit) {
+                const int cnd = misc[6] | (1 << bit);
+                int n = 0;
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) n += key[e] == tk && e * kRiThreads + tid < cnd;
+                n = __reduce_add_sync(0xffffffffu, n);
+                if (lane == 0) wsum[wid] = n;
+                __syncthreads();
+                int t = 0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) t += wsum[w];
+                if (tid == 0 && t < need) misc[6] = cnd;
+                __syncthreads();
+            }
+            if (tid == 0) misc[5] = misc[6];
+        }
+        __syncthreads();
+        ti = misc[5];
+    }
+    float s = 1.f;
+    if (eps >= 0.f) {
+        float q = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) q = fmaf(v[e], v[e], q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) fred[wid] = q;
+        __syncthreads();
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += fred[w];
+        s = 1.0f / sqrtf(t / (float)d + eps);
+    }
+    if (tid == 0) {
+        ThreshOut r;
+        r.tk = tk;
+        r.ti = ti;
+        r.scale = s;
+        r.pad = 0;
+        rule[b] = r;
+    }
+    if (!img) return;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+        const int i = e * kRiThreads + tid;
+        if (i >= d) break;
+        const bool kp = key[e] > tk || (key[e] == tk && i <= ti);
+        const float f = kp ? v[e] * s : 0.f;
+        const uint16_t h = f2bf16_rne(f);
+        const uint16_t l = f2bf16_rne(f - bf16f(h));
+        unsigned char* ch = img + (size_t)(i >> 6) * kImgChunkBytes;
+        const int kk = i & 63;
+        *reinterpret_cast<uint16_t*>(ch + img_off(b, kk)) = h;
+        *reinterpret_cast<uint16_t*>(ch + img_off(16 + b, kk)) = l;
+        if (img_raw) {
+            const uint16_t rh = f2bf16_rne(v[e]);
+            unsigned char* cr = img_raw + (size_t)(i >> 6) * kImgChunkBytes;
+            *reinterpret_cast<uint16_t*>(cr + img_off(b, kk)) = rh;
+            *reinterpret_cast<uint16_t*>(cr + img_off(16 + b, kk)) = f2bf16_rne(v[e] - bf16f(rh));
+        }
+    }
+}
+
 // Image from per-token rules computed elsewhere (the cluster Top-K kernel): token b's values, masked
 // by its rule and scaled, split hi/lo; img_raw (optional): unmasked, unscaled.  grid = (groups/256, B)
 __global__ void rule_apply_image_kernel(const float* __restrict__ X, int64_t ldx, int d, const ThreshOut* __restrict__ rules,

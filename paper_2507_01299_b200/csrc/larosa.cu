@@ -385,6 +385,19 @@ larosa_status launch_rule_image(const float* x, int64_t ldx, int64_t d, int64_t 
                              static_cast<unsigned char*>(img), static_cast<unsigned char*>(img_raw)),
                       "rule_image launch");
 }
+larosa_status launch_rule_image_reg(const float* x, int64_t ldx, int64_t d, int64_t k, float eps, int batch,
+                                    ThreshOut* rule, void* img, void* img_raw, cudaStream_t st) {
+    unsigned char* im = static_cast<unsigned char*>(img);
+    unsigned char* ir = static_cast<unsigned char*>(img_raw);
+    const dim3 g(batch), blk(kRiThreads);
+    if (d <= 8 * kRiThreads)
+        return cuda_check(launch(rule_image_reg_kernel<8>, g, blk, 0, st, x, ldx, (int)d, (int)k, eps, rule, im, ir), "rule_image_reg");
+    if (d <= 16 * kRiThreads)
+        return cuda_check(launch(rule_image_reg_kernel<16>, g, blk, 0, st, x, ldx, (int)d, (int)k, eps, rule, im, ir), "rule_image_reg");
+    if (d <= 32 * kRiThreads)
+        return cuda_check(launch(rule_image_reg_kernel<32>, g, blk, 0, st, x, ldx, (int)d, (int)k, eps, rule, im, ir), "rule_image_reg");
+    return cuda_check(launch(rule_image_reg_kernel<64>, g, blk, 0, st, x, ldx, (int)d, (int)k, eps, rule, im, ir), "rule_image_reg");
+}
 larosa_status launch_dense_image(const float* x, int64_t ldx, int64_t d, int batch, void* img, cudaStream_t st) {
     const int groups = (int)((d + 7) / 8);
     return cuda_check(launch(dense_image_kernel, dim3((unsigned)((groups + 255) / 256), batch), dim3(256), 0, st, x, ldx,
@@ -1347,6 +1360,8 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         void* raw = nullptr;
         if (img_path && si == 0 && w->adapter_mid) raw = W.img_raw[0];
         if (img_path && si == 2 && w->adapter && w->adapter_in_down) raw = W.img_raw[1];
+        if (rule_kernel == 3) return launch_rule_image_reg(x, din, din, k, eps, B, W.thr[si], img_path ? W.img[si] : nullptr,
+                                                           raw, st);
         if (rule_kernel != 1) {   // the cluster Top-K rule (+ the image from it, mode 2)
             TopkKernelArgs r = topk_args_base();
             r.x = x;
