@@ -71,6 +71,7 @@ enum GemvEpi : int { EPI_NONE = 0, EPI_STORE = 1, EPI_RESID = 2, EPI_SILU = 3 };
 // from the 16-bit keys; an element whose 16-bit key equals tk's top 16 bits is decided by the
 // boundary table (idx, keep) -- or, if flags & kRuleExact, from its exact key in x.
 constexpr int kRuleAll = 1, kRuleNone = 2, kRuleEdgeAll = 4, kRuleExact = 8;
+constexpr int kRulePending = 16;   // the boundary bucket's pool lookup is still to come (select_rows)
 constexpr int kRuleTable = 64;
 struct __align__(16) SelRule {
     uint32_t tk;
@@ -168,6 +169,7 @@ struct GemvArgs {
     int late_trigger;                  // tuning: 1 = release dependents after the main loop, not at entry
     uint32_t* err;                     // the workspace's error word (larosa_error_flags) or null
     const void* img;                   // batch >= 8, contiguous rows: the pre-built token operand (gemv_img.cuh)
+    int comp_late;                     // tuning: companions issue their first stages after the dependency wait
 };
 
 // error bits of a workspace's error word (larosa.h larosa_error_flags)
@@ -378,10 +380,42 @@ __device__ __forceinline__ bool warp_suffix256(const uint32_t* bins, int rem, in
     return suffix256(a, b, rem, bin, rem_in, cnt);
 }
 
+// warp-wide: the exact rule inside the k-th key's 16-bit bucket b16 (cnt entries, rem of them kept)
+// from the bucket's pool of (key, index) entries: Tk, Ti and the keep table of the entries' indices
+__device__ __forceinline__ void rule_pool(const SiteSel& sel, int b16, int rem, int cnt, SelRule* R, uint32_t& tk,
+                                          int& ti, int& nb, unsigned long long& keep) {
+    const int lane = threadIdx.x & 31;
+    const uint2 e0 = lane < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane)) : make_uint2(0u, 0x7fffffffu);
+    const uint2 e1 = lane + 32 < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane + 32)) : make_uint2(0u, 0x7fffffffu);
+    int r0 = 0, r1b = 0;
+    for (int q = 0; q < cnt; ++q) {
+        const uint32_t kq = __shfl_sync(0xffffffffu, q < 32 ? e0.x : e1.x, q & 31);
+        const uint32_t iq = __shfl_sync(0xffffffffu, q < 32 ? e0.y : e1.y, q & 31);
+        r0 += kq > e0.x || (kq == e0.x && iq < e0.y);
+        r1b += kq > e1.x || (kq == e1.x && iq < e1.y);
+    }
+    const bool h0 = lane < cnt && r0 == rem - 1, h1 = lane + 32 < cnt && r1b == rem - 1;
+    const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
+    const int s0 = __ffs(b0 ? b0 : b1) - 1;
+    const uint32_t hk0 = __shfl_sync(0xffffffffu, e0.x, s0), hi0 = __shfl_sync(0xffffffffu, e0.y, s0);
+    const uint32_t hk1 = __shfl_sync(0xffffffffu, e1.x, s0), hi1 = __shfl_sync(0xffffffffu, e1.y, s0);
+    tk = b0 ? hk0 : hk1;
+    ti = (int)(b0 ? hi0 : hi1);
+    nb = cnt;
+    const unsigned k0 = __ballot_sync(0xffffffffu, lane < cnt && r0 < rem);
+    const unsigned k1 = __ballot_sync(0xffffffffu, lane + 32 < cnt && r1b < rem);
+    keep = (unsigned long long)k0 | ((unsigned long long)k1 << 32);
+    if (lane < cnt) R->idx[lane] = (int)e0.y;
+    if (lane + 32 < cnt) R->idx[lane + 32] = (int)e1.y;
+}
+
+// defer_pool: when the boundary bucket needs its pool, return with kRulePending (tk = the bucket's
+// lower edge, misc[1..3] = b16 / rem / cnt) and let the caller's warp 0 resolve it (rule_pool)
+// while the other warps compute the definite keep masks
 template <int NT>
 __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
                              unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr, int guess = 0,
-                             uint32_t* err = nullptr) {
+                             uint32_t* err = nullptr, bool defer_pool = false) {
     static_assert(NT >= 64, "two warps");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
@@ -443,30 +477,11 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
                 if (cnt == rem) {
                     tk = (uint32_t)b16 << 15;   // the 16-bit bucket is taken whole: key >= tk
                     flags = kRuleEdgeAll;
+                } else if (cnt <= kPoolCap && defer_pool) {
+                    tk = (uint32_t)b16 << 15;   // only the 16-bit bucket is known yet
+                    flags = kRulePending;
                 } else if (cnt <= kPoolCap) {
-                    const uint2 e0 = lane < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane)) : make_uint2(0u, 0x7fffffffu);
-                    const uint2 e1 = lane + 32 < cnt ? __ldca(sel.pool + sel_pool_idx(b16, lane + 32))
-                                                     : make_uint2(0u, 0x7fffffffu);
-                    int r0 = 0, r1b = 0;
-                    for (int q = 0; q < cnt; ++q) {
-                        const uint32_t kq = __shfl_sync(0xffffffffu, q < 32 ? e0.x : e1.x, q & 31);
-                        const uint32_t iq = __shfl_sync(0xffffffffu, q < 32 ? e0.y : e1.y, q & 31);
-                        r0 += kq > e0.x || (kq == e0.x && iq < e0.y);
-                        r1b += kq > e1.x || (kq == e1.x && iq < e1.y);
-                    }
-                    const bool h0 = lane < cnt && r0 == rem - 1, h1 = lane + 32 < cnt && r1b == rem - 1;
-                    const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
-                    const int s0 = __ffs(b0 ? b0 : b1) - 1;
-                    const uint32_t hk0 = __shfl_sync(0xffffffffu, e0.x, s0), hi0 = __shfl_sync(0xffffffffu, e0.y, s0);
-                    const uint32_t hk1 = __shfl_sync(0xffffffffu, e1.x, s0), hi1 = __shfl_sync(0xffffffffu, e1.y, s0);
-                    tk = b0 ? hk0 : hk1;
-                    ti = (int)(b0 ? hi0 : hi1);
-                    nb = cnt;
-                    const unsigned k0 = __ballot_sync(0xffffffffu, lane < cnt && r0 < rem);
-                    const unsigned k1 = __ballot_sync(0xffffffffu, lane + 32 < cnt && r1b < rem);
-                    keep = (unsigned long long)k0 | ((unsigned long long)k1 << 32);
-                    if (lane < cnt) R->idx[lane] = (int)e0.y;
-                    if (lane + 32 < cnt) R->idx[lane + 32] = (int)e1.y;
+                    rule_pool(sel, b16, rem, cnt, R, tk, ti, nb, keep);
                     tl_stamp(tl, 9);
                 } else {
                     status = 1;      // overflow: block-wide fallback below
@@ -551,7 +566,7 @@ __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, f
 constexpr int kSelMaxWords = 256;
 __host__ __device__ constexpr size_t sel_mask_off(int d) { return (size_t)kSelMaxWords * 128; }
 __host__ __device__ constexpr size_t sel_region_bytes(int d) {
-    return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 8 + rule_scratch_bytes(), 128);
+    return gemv_align(sel_mask_off(d) + (size_t)kSelMaxWords * 12 + rule_scratch_bytes(), 128);
 }
 __host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
     return mode == GEMV_SELECT && sel_region_bytes(d_in) > gemv_ring_bytes(bp) ? sel_region_bytes(d_in)
@@ -579,19 +594,73 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     cp_async_commit();
     // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the CTA's words land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
-    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, region + sel_mask_off(d) + kSelMaxWords * 8, R,
-                     a.tl, guess, a.err);
+    unsigned char* rscratch = region + sel_mask_off(d) + kSelMaxWords * 8;
+    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, rscratch, R, a.tl, guess, a.err, true);
+    const int* rmisc = reinterpret_cast<const int*>(rscratch);
+    const int flags0 = R->flags;
+    if (tid == 0) reinterpret_cast<float*>(misc)[4] = R->scale;
+    cp_async_wait<0>();
+    __syncthreads();
+    tl_stamp(a.tl, 5);
+    uint32_t* bmk = reinterpret_cast<uint32_t*>(rscratch + rule_scratch_bytes());   // pending: boundary lanes per word
+    int total;
+    if (flags0 & kRulePending) {
+        // warp 0 resolves the boundary bucket from its pool while warps 1.. mark the definite rows
+        // (16-bit key above the bucket) and the boundary elements of every word
+        const uint32_t t16 = R->tk >> 15;
+        if (wid == 0) {
+            uint32_t tk;
+            int ti, nb;
+            unsigned long long keep;
+            rule_pool(a.sel, rmisc[1], rmisc[2], rmisc[3], R, tk, ti, nb, keep);
+            if (lane == 0) {
+                R->tk = tk;
+                R->ti = ti;
+                R->nb = nb;
+                R->keep = keep;
+                R->flags = 0;
+            }
+            tl_stamp(a.tl, 9);
+        } else {
+            for (int j = wid - 1; j < nj; j += NW - 1) {
+                const int i = 32 * (split + n_splits * j) + lane;
+                const uint32_t k16 = i < d ? key_of(xs[32 * j + lane]) >> 15 : 0u;
+                const uint32_t m = __ballot_sync(0xffffffffu, i < d && k16 > t16);
+                const uint32_t bm = __ballot_sync(0xffffffffu, i < d && k16 == t16);
+                if (lane == 0) {
+                    wmk[j] = m;
+                    wcnt[j] = __popc(m);
+                    bmk[j] = bm;
+                }
+            }
+        }
+        __syncthreads();
+        // the boundary elements by the pool's keep table
+        const int nbt = R->nb;
+        const unsigned long long keepm = R->keep;
+        for (int j = wid; j < nj; j += NW) {
+            const uint32_t bm = bmk[j];
+            if (!bm) continue;
+            const int i = 32 * (split + n_splits * j) + lane;
+            bool kp = false;
+            if ((bm >> lane) & 1u)
+                for (int q = 0; q < nbt; ++q)
+                    if (R->idx[q] == i) kp = (keepm >> q) & 1ull;
+            const uint32_t m = __ballot_sync(0xffffffffu, kp);
+            if (lane == 0) {
+                wmk[j] |= m;
+                wcnt[j] += __popc(m);
+            }
+        }
+        __syncthreads();
+    } else {
     const uint32_t tk = R->tk;
     const int ti = R->ti;
     const int flags = R->flags;
     const int nbt = R->nb;
     const unsigned long long keepm = R->keep;
     const int* tab = R->idx;
-    if (tid == 0) reinterpret_cast<float*>(misc)[4] = R->scale;
     const uint32_t t16 = tk >> 15;
-    cp_async_wait<0>();
-    __syncthreads();
-    tl_stamp(a.tl, 5);
     auto keep16 = [&](uint32_t key, int i) -> bool {
         const uint32_t k16 = key >> 15;
         if (k16 != t16) return k16 > t16;
@@ -604,8 +673,6 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
         return key > tk || (key == tk && i <= ti);
     };
     const bool all = flags & kRuleAll, none = flags & kRuleNone;
-    int total;
-    {
         for (int j = wid; j < nj; j += NW) {
             const int i = 32 * (split + n_splits * j) + lane;
             bool kp = false;
@@ -617,6 +684,8 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
             }
         }
         __syncthreads();
+    }
+    {
         tl_stamp(a.tl, 7);
         const int cj = tid < nj ? wcnt[tid] : 0;
         const int before = block_excl_scan<NT>(cj, scan, &total);
@@ -735,7 +804,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     const uint16_t* wcol = Wb + col0;
     // companion: the weights of the first kStages stages do not depend on the previous kernel
     const int c_my = c_n > warp ? (c_n - warp + kGemvWarps - 1) / kGemvWarps : 0;
-    if (comp) {
+    auto comp_prefetch = [&]() {
 #pragma unroll
         for (int st = 0; st < kStages; ++st) {
             unsigned char* dst = mychunk + (size_t)st * (kStageRows * kSliceCols * 2);
@@ -747,7 +816,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
             }
             cp_async_commit();
         }
-    }
+    };
+    if (comp && !a.comp_late) comp_prefetch();
 
     // SELECT: the coarse-bucket guess left by this site's previous consumer (written by a kernel
     // that completed before the previous one; any value is safe, a wrong one costs a round trip)
@@ -759,6 +829,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     pdl_wait();       // the row source comes from the previous kernel
     if (!a.late_trigger) pdl_trigger();
     tl_stamp(a.tl, 1);
+    if (comp && a.comp_late) comp_prefetch();   // (tuning: not while the previous kernel's prologue runs)
     if (a.zero_hist) {   // a histogram whose consumer has completed (kernel-boundary ordered)
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
         for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;

@@ -261,6 +261,8 @@ larosa_status launch_gemv_bm(const GemvArgs& a, const GemvPlan& p, cudaStream_t 
     GemvArgs aa = a;
     static const int late = env_int("LAROSA_PDL_LATE", 0);    // tuning
     aa.late_trigger = late;
+    static const int comp_late = env_int("LAROSA_COMP_LATE", 0);   // tuning
+    aa.comp_late = comp_late;
     aa.n_splits = p.n_splits;
     aa.n_splits2 = p.n_splits2;
     aa.list_cap = p.list_cap;
