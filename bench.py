@@ -151,18 +151,20 @@ def source_hash():
 
 
 # ------------------------------------------------------------------------------------ step bytes
-def step_bytes(shape, plan, unions, batch, ctx_lens, n_layers):
+def step_bytes(shape, plan, unions, batch, ctx_lens, n_layers, w4=False):
     """Algorithmic bytes of one decode step (SURVEY §8(d) "algorithmic work per unit"):
     per layer  sum_sites |U_s| D_out,s 2  (|U_s| = k_s at batch 1; the measured union of the
     tokens' kept sets otherwise)  +  D^2 2 (adapter; the last layer has none)  +  the KV rows read
-    (B 2 Hkv hd ctx 2); plus the LM head D V 2 and the embedding rows B D 2."""
+    (B 2 Hkv hd ctx 2); plus the LM head D V 2 and the embedding rows B D 2.  w4: a kept row of a
+    site costs D_out / 2 code bytes + D_out / 128 fp16 scales instead of 2 D_out."""
     d, nq = shape.d, shape.hq * shape.hd
     douts = (shape.qkv_out, d, 2 * shape.inter, d)
     kv = sum(2 * shape.hkv * shape.hd * c * 2 for c in ctx_lens)
+    row = (lambda n: n // 2 + 2 * (n // 128)) if w4 else (lambda n: 2 * n)
     tot = 0
     for l in range(n_layers):
         u = unions[l] if unions is not None else plan
-        tot += sum(int(a) * b * 2 for a, b in zip(u, douts)) + kv
+        tot += sum(int(a) * row(b) for a, b in zip(u, douts)) + kv
         if l + 1 < n_layers:
             tot += d * d * 2
     return tot + d * shape.vocab * 2 + batch * d * 2
@@ -360,6 +362,26 @@ def own_dense_model(model):
     from paper_2507_01299_b200 import model as M
     layers = [LZ.LayerWeights(**{**w.__dict__, "adapter": None, "adapter_in_down": False}) for w in model.layers]
     return M.DecodeModel(shape=model.shape, embed=model.embed, layers=layers, head=model.head)
+
+
+def w4_decode_extra(shape, device, peaks, ps=(0.0, 0.4, 0.5), steps=20):
+    """N3: the same decode step with W4A16 weights at all four sites of every layer (larosa.h ABI 6;
+    literal adapter form, bf16 head), batch 1, one CUDA graph per step (tests/test_gpu_w4_layer.py
+    is its parity)."""
+    from paper_2507_01299_b200 import model as M
+    model = M.synth_decode_model(shape, shape.layers, device, seed=1, w4=True)
+    run = M.DecodeRunner(model, 1, CTX, device)
+    out = {"weights": "int4 codes + fp16 scales per 128 outputs, all 4 sites; adapter separate; head bf16"}
+    for pp in ps:
+        pl = M.site_plan(shape, pp)
+        reset_run(run, 5)
+        t = decode_line(run, pl, steps)
+        nb = step_bytes(shape, pl, None, 1, [CTX], shape.layers, w4=True)
+        out[str(pp)] = {"ms_per_step": t, "tok_s": 1e3 / t, "plan": list(pl), "bytes": nb,
+                        "frac": nb / (t * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    del run, model
+    torch.cuda.empty_cache()
+    return out
 
 
 def decode_line(run, plan, steps, reps_unions=True):
@@ -571,6 +593,7 @@ def main():
             extras["batch16"] = b16
         del model
         torch.cuda.empty_cache()
+        extras["w4a16_decode"] = w4_decode_extra(shape, device, peaks)
         extras["block_llama2_7b_c2"] = BX.block_c2_extra(device)
         extras["model_sweep_configs3"] = BX.model_sweep_extra(device, merged=merged)
         extras["fold_tcgen05"] = BX.fold_extra(device)

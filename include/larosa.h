@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 5
+#define LAROSA_ABI_VERSION 6
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -276,6 +276,13 @@ typedef struct {
      * Q_m's basis (adapter = Q_m^T Q_a', or w_down = Wd Q_a' with adapter_in_down).  NULL: Q_L
      * (one rotation per layer).  Not supported by larosa_sparse_layer_shard_phase. */
     const uint16_t* adapter_mid;
+    /* W4A16 sites (ABI 6): for site s (0 QKV, 1 O, 2 gate|up, 3 down) either NULL
+     * (the bf16 w_* above) or the int4 codes [d_in][d_out/2] and fp16 group scales
+     * [d_in][d_out/128] of larosa_quantize_w4 of that (folded) weight; the site then streams the
+     * codes with the same fused Top-K prologue and epilogue (batch 1 only, EUNSUPPORTED otherwise;
+     * the down site needs the literal adapter form, adapter_in_down = 0). */
+    const uint8_t* w4_codes[4];
+    const uint16_t* w4_scales[4];
 } larosa_layer_weights;
 
 typedef struct {
@@ -368,7 +375,7 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
  * over a real entry, lower index winning ties -- the padded layer computes the same function;
  * model.shard_layer does this).  Batch 1: the fused SELECT GEMVs; batch > 1: the cluster Top-K
  * rule kernel and the union GEMV (tcgen05 at batch >= 8).  One workspace per rank and batch
- * (size query with the shard), zero-filled once.
+ * (size query with the shard), zero-filled once.  W4 sites (w4_codes) are EUNSUPPORTED here.
  * ------------------------------------------------------------------------------ */
 typedef struct {
     int32_t rank, world;

@@ -55,6 +55,14 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     if (threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
     pdl_wait();
     pdl_trigger();
+    if (a.zero_hist) {   // (decoder layer) a histogram / accumulators whose consumer has completed
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;
+    }
+    if (a.zero_acc) {
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_acc_words; i += nct * kGemvThreads) a.zero_acc[i] = 0ull;
+    }
     const int n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
     // the kept rows' 8 group scales of this slice (16 bytes), once, before the stream
     const int g0 = slice * (kW4SliceCols / kW4Group);
@@ -138,17 +146,19 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
             red_fix(a.acc + o, s, a.err);
         }
     }
+    if (a.epi == EPI_NONE) return;    // the consumer kernel reads the accumulators (QKV -> attention)
     __syncthreads();
     if (threadIdx.x == 0) misc[0] = atom_add_acq_rel_gpu(a.tickets + slice, 1u) == gridDim.y - 1u;
     __syncthreads();
     if (!misc[0]) return;
     if (threadIdx.x == 0) a.tickets[slice] = 0u;
-    // the last split of the slice: y = the column sums (EPI_STORE), accumulators re-zeroed
-    for (int c = threadIdx.x; c < kW4SliceCols; c += kGemvThreads) {
-        const int o = slice * kW4SliceCols + c;
-        if (o >= a.d_out) break;
-        a.out[o] = fix_to_f(__ldcg(a.acc + o));
-        a.acc[o] = 0ull;
+    // the last split of the slice finalises its 1024 columns as four 256-column slices of the bf16
+    // kernel's epilogue (bias / residual / SiLU(g) u, accumulators re-zeroed, and at batch 1 the next
+    // site's histogram and RMS partials): the same output layout and selection data
+    for (int j = 0; j < kW4SliceCols / kSliceCols; ++j) {
+        const int vs = slice * (kW4SliceCols / kSliceCols) + j;
+        if (vs * kSliceCols >= a.d_out) break;
+        gemv_epilogue<1>(a, vs, reinterpret_cast<float*>(misc + 16));
     }
 }
 

@@ -23,6 +23,7 @@
 #include "prefill_tc.cuh"
 #include "gemv_img.cuh"
 
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -95,19 +96,25 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-// Function attributes are per device context: set each (kernel, device, attribute) once, under a
-// lock (calls are re-entrant and a process may drive several GPUs).
+// Function attributes are per device context: track the value of each (kernel, device, attribute)
+// under a lock (calls are re-entrant and a process may drive several GPUs) and call the driver only
+// when it changes; the dynamic shared memory limit only ever grows (a launch needing less than the
+// current limit is valid, and lowering it would break a later larger launch).
 cudaError_t set_func_attr_once(const void* kern, cudaFuncAttribute attr, int value) {
     static std::mutex mu;
-    static std::set<std::tuple<const void*, int, int, int>> done;
+    static std::map<std::tuple<const void*, int, int>, int> cur;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    const auto key = std::make_tuple(kern, dev, (int)attr, value);
+    const auto key = std::make_tuple(kern, dev, (int)attr);
     std::lock_guard<std::mutex> lk(mu);
-    if (done.count(key)) return cudaSuccess;
+    const auto it = cur.find(key);
+    if (it != cur.end()) {
+        if (it->second == value) return cudaSuccess;
+        if (attr == cudaFuncAttributeMaxDynamicSharedMemorySize && it->second > value) return cudaSuccess;
+    }
     e = cudaFuncSetAttribute(kern, attr, value);
-    if (e == cudaSuccess) done.insert(key);
+    if (e == cudaSuccess) cur[key] = value;
     return e;
 }
 
@@ -447,6 +454,24 @@ GemvArgs gemv_args_base() {
     memset(&a, 0, sizeof(a));
     a.err = t_err_word;
     return a;
+}
+
+// W4A16 SELECT GEMV (gemv_w4.cuh) with the layer's epilogue: 1024-column slices, one wave of 2 CTAs
+// per SM (the plan of larosa_topk_sparse_gemv_w4)
+larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, cudaStream_t st) {
+    const int64_t d_in = a.d_in, d_out = a.d_out, k = a.sel_k;
+    if (d_out % kSliceCols || d_out > (int64_t)64 * kW4SliceCols)
+        return fail(LAROSA_EUNSUPPORTED, "W4 site: d_out must be a multiple of 256 (<= 65536)");
+    const int n_sl = (int)((d_out + kW4SliceCols - 1) / kW4SliceCols);
+    const int64_t nwords = (d_in + 31) / 32;
+    const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
+    a.n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
+    a.list_cap = (int)(32 * ((nwords + a.n_splits - 1) / a.n_splits));
+    const size_t smem = w4_region_bytes((int)d_in) + (size_t)a.list_cap * 8 + kGemvMisc * 4 + (size_t)a.list_cap * 16;
+    if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "W4 site: shared memory plan too large");
+    LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, smem), "cudaFuncSetAttribute(gemv_w4)"));
+    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, a.n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
+                      "gemv_w4 launch");
 }
 
 // ============================================================================== small launches
@@ -1245,7 +1270,9 @@ void carve_layer(Carver& c, const LayerDims& L, int batch, int64_t max_ctx, Laye
 
 larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_plan* p, const larosa_layer_state* s) {
     if (!w || !p || !s) return fail(LAROSA_EINVAL, "sparse_layer: NULL struct");
-    if (!w->w_qkv || !w->w_o || !w->w_gu || !w->w_down) return fail(LAROSA_EINVAL, "sparse_layer: NULL weight");
+    if ((!w->w_qkv && !w->w4_codes[0]) || (!w->w_o && !w->w4_codes[1]) || (!w->w_gu && !w->w4_codes[2]) ||
+        (!w->w_down && !w->w4_codes[3]))
+        return fail(LAROSA_EINVAL, "sparse_layer: NULL weight");
     if (!s->resid || !s->k_cache || !s->v_cache || !s->pos) return fail(LAROSA_EINVAL, "sparse_layer: NULL state");
     if (s->batch < 1) return fail(LAROSA_EINVAL, "sparse_layer: batch < 1");
     if (s->batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: batch > 16");
@@ -1253,6 +1280,21 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
         return fail(LAROSA_EINVAL, "sparse_layer: dims must be > 0");
     if (w->n_q_heads % w->n_kv_heads) return fail(LAROSA_ESHAPE, "sparse_layer: Hq %% Hkv != 0");
     if (w->adapter_in_down && !w->adapter) return fail(LAROSA_EINVAL, "sparse_layer: adapter_in_down needs the adapter");
+    for (int j = 0; j < 4; ++j) {
+        if (!w->w4_codes[j] != !w->w4_scales[j]) return fail(LAROSA_EINVAL, "sparse_layer: W4 site %d needs codes and scales", j);
+        if (w->w4_codes[j] && s->batch != 1) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: W4 sites need batch 1");
+        if (w->w4_codes[j] && (!aligned16(w->w4_codes[j]) || (reinterpret_cast<uintptr_t>(w->w4_scales[j]) & 3)))
+            return fail(LAROSA_EINVAL, "sparse_layer: W4 codes 16-byte, scales 4-byte aligned");
+    }
+    {
+        const int64_t douts[4] = {(w->n_q_heads + 2 * w->n_kv_heads) * w->head_dim, w->d, 2 * w->inter, w->d};
+        for (int j = 0; j < 4; ++j)
+            if (w->w4_codes[j] && douts[j] % 256)
+                return fail(LAROSA_EUNSUPPORTED, "sparse_layer: W4 site %d needs D_out %% 256 == 0", j);
+    }
+    if (w->w4_codes[3] && w->adapter_in_down)
+        return fail(LAROSA_EUNSUPPORTED, "sparse_layer: a W4 down site needs the literal adapter (adapter_in_down = 0)");
+    if (w->w4_codes[1] && w->adapter_mid) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: a W4 O site with adapter_mid");
     if ((s->host_in || s->host_out) && s->batch != 1) return fail(LAROSA_EINVAL, "sparse_layer: host_in/out need batch 1");
     if (w->n_q_heads / w->n_kv_heads > kAttnMaxG) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
     if (w->head_dim != 64 && w->head_dim != 128) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: head_dim must be 64 or 128");
@@ -1411,6 +1453,11 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
     auto plan_site = [&](int64_t dout, int64_t din, int64_t k) {
         return fused ? plan_gemv(dout, k, 1, GEMV_SELECT, din) : plan_gemv(dout, din, bp, GEMV_THRESH, din);
     };
+    // site si's GEMV: the W4A16 kernel when the site has int4 weights (batch 1), else the bf16 one
+    auto site_launch = [&](const GemvArgs& a, int si, const GemvPlan& p, int bpl) -> larosa_status {
+        if (w->w4_codes[si]) return launch_gemv_w4(a, w->w4_codes[si], w->w4_scales[si], st);
+        return launch_gemv(a, p, bpl, st);
+    };
     // epilogue of a site GEMV; `next` = the site whose selection data it produces (-1: none)
     auto epi = [&](GemvArgs& a, int j, int mode, const float* res, float* out, int next) {
         a.epi = mode;
@@ -1442,7 +1489,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.zero_hist = fused ? W.sel[3].hist : nullptr;   // h4's consumer (previous layer's down GEMV) is done
         a.tl = tl_slot(0);
         a.zero_words = kSelHistTotal;
-        LAROSA_TRY(launch_gemv(a, plan_site(L.nqkv, L.d, plan->k_h1), fused ? 1 : bp, st));
+        LAROSA_TRY(site_launch(a, 0, plan_site(L.nqkv, L.d, plan->k_h1), fused ? 1 : bp));
     }
     // ---- attention (finalises q / new k, v from acc_qkv, re-zeroes it) -> h2 ---------------------
     {
@@ -1510,7 +1557,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             epi(b, 0, epi_mode, nullptr, W.rmid, 2);
             LAROSA_TRY(launch_gemv(b, plan_gemv(L.d, L.d, bp, GEMV_DENSE, L.d), bp, st));
         } else {
-            LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.nq, plan->k_h2), fused ? 1 : bp, st));
+            LAROSA_TRY(site_launch(a, 1, plan_site(L.d, L.nq, plan->k_h2), fused ? 1 : bp));
         }
     }
     LAROSA_TRY(tap_copy(T.r_mid, W.rmid, sizeof(float) * B * L.d, st));
@@ -1523,7 +1570,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.tl = tl_slot(3);
         a.zero_hist = fused ? W.sel[1].hist : nullptr;   // h2's consumer (O) is done
         a.zero_words = kSelHistTotal;
-        LAROSA_TRY(launch_gemv(a, plan_site(L.dgu, L.d, plan->k_h3), fused ? 1 : bp, st));
+        LAROSA_TRY(site_launch(a, 2, plan_site(L.dgu, L.d, plan->k_h3), fused ? 1 : bp));
     }
     LAROSA_TRY(tap_copy(T.h4, W.h4, sizeof(float) * B * L.inter, st));
     // ---- h4 -> down; epilogue r_mid + y_down (-> adapter input, or the next layer's r) ------------
@@ -1576,7 +1623,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
         a.zero_hist = fused ? W.sel[2].hist : nullptr;   // h3's consumer (gate|up) is done
         a.tl = tl_slot(4);
         a.zero_words = kSelHistTotal;
-        LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.inter, plan->k_h4), fused ? 1 : bp, st));
+        LAROSA_TRY(site_launch(a, 3, plan_site(L.d, L.inter, plan->k_h4), fused ? 1 : bp));
     }
     // ---- residual adapter r <- (r_mid + y_down) . A_l (dense GEMV) -------------------------
     if (w->adapter) {
@@ -1659,6 +1706,8 @@ larosa_status validate_shard(const larosa_layer_weights* w, const larosa_shard* 
     const int64_t n = sh->world;
     if (n < 1 || sh->rank < 0 || sh->rank >= n) return fail(LAROSA_EINVAL, "shard: bad rank/world");
     if (sh->batch < 1) return fail(LAROSA_EINVAL, "shard: batch < 1");
+    for (int j = 0; j < 4; ++j)
+        if (w->w4_codes[j] || w->w4_scales[j]) return fail(LAROSA_EUNSUPPORTED, "shard: W4 sites are not sharded");
     if (sh->batch > LAROSA_MAX_BATCH) return fail(LAROSA_EUNSUPPORTED, "shard: batch > %d", LAROSA_MAX_BATCH);
     if (w->n_q_heads % n || w->n_kv_heads % n) return fail(LAROSA_EUNSUPPORTED, "shard: heads %% world != 0");
     if (w->d % (8 * n)) return fail(LAROSA_EUNSUPPORTED, "shard: d %% (8 world) != 0");

@@ -37,7 +37,8 @@ class LayerWeightsC(ctypes.Structure):
     _fields_ = [("w_qkv", _vp), ("b_qkv", _vp), ("w_o", _vp), ("w_gu", _vp), ("w_down", _vp),
                 ("adapter", _vp), ("d", _c_i64), ("inter", _c_i64), ("n_q_heads", _c_i64),
                 ("n_kv_heads", _c_i64), ("head_dim", _c_i64), ("rope_theta", ctypes.c_float),
-                ("rms_eps", ctypes.c_float), ("adapter_in_down", _c_i32), ("adapter_mid", _vp)]
+                ("rms_eps", ctypes.c_float), ("adapter_in_down", _c_i32), ("adapter_mid", _vp),
+                ("w4_codes", _vp * 4), ("w4_scales", _vp * 4)]
 
 
 class LayerPlanC(ctypes.Structure):
@@ -141,7 +142,7 @@ def lib() -> ctypes.CDLL:
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase", "larosa_shard_gather_permute",
                  "larosa_argmax"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 5:
+    if L.larosa_abi_version() != 6:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -490,12 +491,19 @@ class LayerWeights:
     adapter: Optional[torch.Tensor] = None
     adapter_in_down: bool = False   # w_down = Wd Q_{l+1}: r_next = r_mid A_l + y_down (larosa.h)
     adapter_mid: Optional[torch.Tensor] = None   # Q_B: A_mid = Q_a^T Q_m beside O (larosa.h)
+    # W4A16 sites (ABI 6): per site (QKV, O, gate|up, down) None or (codes, scales) of quantize_w4
+    w4: Optional[list] = None
 
     def c(self) -> LayerWeightsC:
-        return LayerWeightsC(_ptr(self.w_qkv), _ptr(self.b_qkv), _ptr(self.w_o), _ptr(self.w_gu), _ptr(self.w_down),
-                             _ptr(self.adapter), self.d, self.inter, self.n_q_heads, self.n_kv_heads, self.head_dim,
-                             float(self.rope_theta), float(self.rms_eps), int(self.adapter_in_down),
-                             _ptr(self.adapter_mid))
+        c = LayerWeightsC(_ptr(self.w_qkv), _ptr(self.b_qkv), _ptr(self.w_o), _ptr(self.w_gu), _ptr(self.w_down),
+                          _ptr(self.adapter), self.d, self.inter, self.n_q_heads, self.n_kv_heads, self.head_dim,
+                          float(self.rope_theta), float(self.rms_eps), int(self.adapter_in_down),
+                          _ptr(self.adapter_mid))
+        for j, qs in enumerate(self.w4 or []):
+            if qs is not None:
+                c.w4_codes[j] = _ptr(qs[0])
+                c.w4_scales[j] = _ptr(qs[1])
+        return c
 
 
 @dataclass

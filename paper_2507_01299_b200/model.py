@@ -7,6 +7,7 @@ seeded random weights (synth) and moves tensors.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -83,6 +84,20 @@ def fold_layer(orig: OriginalLayer, shape: synth.ModelShape, q_l: torch.Tensor,
                            adapter_in_down=merged, adapter_mid=adapter_mid)
 
 
+W4_SITES = ("w_qkv", "w_o", "w_gu", "w_down")
+
+
+def quantize_layer_w4(lw: LZ.LayerWeights, sites=(0, 1, 2, 3), drop_bf16: bool = False) -> LZ.LayerWeights:
+    """The layer with W4A16 weights (larosa_quantize_w4 of the folded bf16 weights) at the given
+    sites (0 QKV, 1 O, 2 gate|up, 3 down).  A W4 down site needs the literal
+    adapter form (adapter_in_down False); drop_bf16 releases the bf16 copies of those sites."""
+    if 3 in sites and lw.adapter_in_down:
+        raise ValueError("quantize_layer_w4: a W4 down site needs adapter_in_down=False")
+    w4 = [LZ.quantize_w4(getattr(lw, W4_SITES[j])) if j in sites else None for j in range(4)]
+    kw = {W4_SITES[j]: None for j in sites} if drop_bf16 else {}
+    return dataclasses.replace(lw, w4=w4, **kw)
+
+
 def site_plan(shape: synth.ModelShape, p: float, alpha_mode: str = "uniform") -> tuple:
     """Per-site kept counts (k_h1, k_h2, k_h3, k_h4) via larosa_compute_k with
     uniform alpha or the paper's App. B coefficients (alpha2/alpha4 from the constraints)."""
@@ -109,9 +124,10 @@ class DecodeModel:
 
 
 def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int = 0,
-                       vocab: Optional[int] = None, adapter_in_down: bool = False) -> DecodeModel:
+                       vocab: Optional[int] = None, adapter_in_down: bool = False, w4: bool = False) -> DecodeModel:
     """Random-init model of the given shape (synthetic weights), folded with
-    the library's own tensor-core fold."""
+    the library's own tensor-core fold; w4: every layer's four sites as W4A16 weights (the bf16
+    copies released; literal adapter form)."""
     vocab = vocab or shape.vocab
     d = shape.d
     qs = [synth.haar_orthogonal(d, 7000 + 100 * seed + l, device=device, dtype=torch.float32)
@@ -122,8 +138,10 @@ def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int
     layers = []
     for l in range(n_layers):
         orig = synth_original_layer(shape, 10 * seed + l + 1, device=device)
-        layers.append(fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None,
-                                 adapter_in_down=adapter_in_down))
+        lw = fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None,
+                        adapter_in_down=adapter_in_down and not w4)
+        layers.append(quantize_layer_w4(lw, drop_bf16=True) if w4 else lw)
+        del lw
         del orig
     H = synth.gaussian_bf16((d, vocab), 9100 + seed, d ** -0.5, device)
     gf = (1.0 + 0.1 * synth.gaussian((d,), 9200 + seed, device=device)).float().contiguous()

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 14, names
     for n in names:
         assert hasattr(L, n), f"missing export {n}"
-    assert L.larosa_abi_version() == 5
+    assert L.larosa_abi_version() == 6
 
 
 def test_status_strings():
@@ -177,6 +177,30 @@ def test_new_entry_points_validation():
     w.adapter_in_down = 0
     s3 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 2, 0, FAKE, None)
     assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s3), None, ws, 1 << 40, None) == 1
+    # W4 sites (ABI 6): codes without scales, batch > 1, a W4 down site beside a merged adapter,
+    # D_out % 256 (gate|up of inter 11008 + 64), and a NULL bf16 weight without W4 codes
+    s1 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 1)
+    s2 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 2)
+    w4 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, None)
+    w4.w4_codes[0] = FAKE
+    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 1
+    w4.w4_scales[0] = FAKE
+    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s2), None, ws, 1 << 40, None) == 3
+    w4.w4_codes[3] = w4.w4_scales[3] = FAKE
+    w4.adapter_in_down = 1
+    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 3
+    w4.adapter_in_down = 0
+    w4.inter = 11008 + 64
+    w4.w4_codes[2] = w4.w4_scales[2] = FAKE
+    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 3
+    w4.inter = 11008
+    w4.w4_codes[2] = w4.w4_scales[2] = None
+    w4.w_gu = None
+    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 1
+    sh1 = LZ.ShardC(0, 1, 1)
+    w4.w_gu = FAKE
+    assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(sh1), 1, FAKE, FAKE,
+                                             FAKE, None, None, None, 0, ws, 1 << 40, None) == 3
     # shard phase: the block-wise rotation is not supported there
     w2 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, FAKE)
     sh = LZ.ShardC(0, 1, 1)
