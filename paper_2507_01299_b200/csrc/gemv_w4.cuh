@@ -38,6 +38,114 @@ __host__ __device__ constexpr size_t w4_region_bytes(int d_in) {
     return gemv_x_bytes(1, GEMV_SELECT, d_in) > (size_t)kGemvWarps * kW4SliceCols * 4 ? gemv_x_bytes(1, GEMV_SELECT, d_in)
                                                                                       : (size_t)kGemvWarps * kW4SliceCols * 4;
 }
+// the whole plan: region, row list + values, misc, 8 fp16 scales and 8 fp32 b = v s per kept row
+__host__ __device__ constexpr size_t w4_smem_bytes(int d_in, int list_cap) {
+    return w4_region_bytes(d_in) + (size_t)list_cap * 8 + kGemvMisc * 4 + (size_t)list_cap * 16 + (size_t)list_cap * 32;
+}
+
+// (x & m) | c in one LOP3 (the compiler splits it when both are immediates)
+__device__ __forceinline__ uint32_t and_or(uint32_t x, uint32_t m, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(x), "r"(m), "r"(c));
+    return d;
+}
+
+// 16 + q as fp32 from a byte whose bits 3-6 hold q and bit 7 is set: bytes {0, 0, 0x80 | q << 3, 0x41}
+// (2^4 has its mantissa LSB at bit 19, so q lands on weight 1)
+template <int BB>
+__device__ __forceinline__ float w4_f16q(uint32_t pre) {
+    return __uint_as_float(__byte_perm(pre, 0x41u, 0x4055u + 0x100u * BB));
+}
+
+// Batch-1 finalisation of NV consecutive 256-column slices (vs0 .. vs0 + nv - 1) by one CTA: the
+// same arithmetic and outputs as NV calls of gemv_epilogue<1>, with every accumulator load issued
+// before any result is used (one L2 round trip instead of NV) and one barrier pair for the RMS
+// partials.  sred: NV * 8 floats.
+template <int NV>
+__device__ void gemv_epilogue_b1_multi(const GemvArgs& a, int vs0, int nv, float* sred) {
+    const int c = threadIdx.x, lane = c & 31, wid = c >> 5;
+    float v[NV];
+    int idx[NV];
+    bool has[NV];
+    const bool silu = a.epi == EPI_SILU;
+    // pass 1: every accumulator (and bias / residual) load issued, predicated, none used yet
+    unsigned long long r0[NV], r1[NV];
+    float add[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int slice = vs0 + j, base = slice * kSliceCols;
+        int o0;
+        if (silu) {   // slice = 2 gate|up blocks of 128 columns (64 gate, then the matching 64 up)
+            const int blk = c / kGuBlock, q = c % kGuBlock;
+            o0 = base + blk * 2 * kGuBlock + q;
+            has[j] = j < nv && c < 2 * kGuBlock && o0 < a.d_out;
+            idx[j] = slice * 2 * kGuBlock + blk * kGuBlock + q;
+        } else {
+            o0 = base + c;
+            has[j] = j < nv && o0 < a.d_out;
+            idx[j] = o0;
+        }
+        r0[j] = has[j] ? __ldcg(a.acc + o0) : 0ull;
+        r1[j] = has[j] && silu ? __ldcg(a.acc + o0 + kGuBlock) : 0ull;
+        float t = 0.f;
+        if (has[j] && !silu && a.bias) t = bf16f(a.bias[o0]);
+        add[j] = t;
+        v[j] = has[j] && !silu && a.res ? a.res[o0] : 0.f;
+    }
+    // pass 2: re-zero the accumulators, finalise
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (!has[j]) {
+            v[j] = 0.f;
+            continue;
+        }
+        const int o0 = silu ? (vs0 + j) * kSliceCols + (c / kGuBlock) * 2 * kGuBlock + c % kGuBlock : idx[j];
+        a.acc[o0] = 0ull;
+        if (silu) {
+            a.acc[o0 + kGuBlock] = 0ull;
+            const float g = fix_to_f(r0[j]), u = fix_to_f(r1[j]);
+            v[j] = g / (1.0f + expf(-g)) * u;
+        } else {
+            float y = fix_to_f(r0[j]);
+            if (a.bias) y += add[j];
+            if (a.res) y = v[j] + y;
+            v[j] = y;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (!has[j]) continue;
+        a.out[idx[j]] = v[j];
+        if (a.out_host) a.out_host[idx[j]] = v[j];
+    }
+    if (a.out_sel.hist) {   // hist_push of every value, the NV slot atomics in flight together
+        uint32_t slot[NV], key[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            slot[j] = 0xffffffffu;
+            key[j] = key_of(v[j]);
+            if (!has[j]) continue;
+            const uint32_t k16 = key[j] >> 15;
+            const unsigned am = __activemask();
+            const unsigned peers = __match_any_sync(am, k16 >> 8);
+            if (lane == __ffs(peers) - 1) red_add_u32(a.out_sel.hist + sel_coarse_idx(k16 >> 8), __popc(peers));
+            slot[j] = atomicAdd(a.out_sel.hist + sel_fine_idx(k16), 1u);
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (slot[j] < (uint32_t)kPoolCap)
+                a.out_sel.pool[sel_pool_idx(key[j] >> 15, slot[j])] = make_uint2(key[j], (uint32_t)idx[j]);
+    }
+    if (a.out_ssq) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const float w = slice_ssq_warp(v[j]);
+            if (lane == 0) sred[j * 8 + wid] = w;
+        }
+        __syncthreads();
+        if (c < nv) a.out_ssq[vs0 + c] = slice_ssq_combine(sred + c * 8);
+    }
+}
 
 __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const GemvArgs a, const uint8_t* __restrict__ Wq,
                                                                         const uint16_t* __restrict__ S) {
@@ -49,12 +157,15 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                     // [cap]
     int* misc = reinterpret_cast<int*>(lval + a.list_cap);                         // [kGemvMisc]
     uint4* lsc = reinterpret_cast<uint4*>(misc + kGemvMisc);                       // [cap] 8 fp16 scales
+    float4* lb = reinterpret_cast<float4*>(lsc + a.list_cap);                      // [cap][2] b = v s per group
     const int ngroups = a.d_out / kW4Group;
 
     int sel_guess = 0;
     if (threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
+    tl_stamp(a.tl, 0);
     pdl_wait();
     pdl_trigger();
+    tl_stamp(a.tl, 1);
     if (a.zero_hist) {   // (decoder layer) a histogram / accumulators whose consumer has completed
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
         for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;
@@ -76,17 +187,12 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
             for (int q = 0; q < 8; ++q) d[q] = q < ng ? src[q] : (uint16_t)0;
         }
     }
-    cp_async_commit();
-    const float sel_scale = reinterpret_cast<const float*>(misc)[4];
-    cp_async_wait<0>();
-    __syncthreads();
-
-    // warp w takes list entries w + 8 m; lane l owns columns 32 l .. 32 l + 31 of the slice and
-    // copies exactly those 16 bytes of each row (no cross-lane dependency in the ring)
+    // the first stages of the stream go out with the scales (the row list is complete and the
+    // staged selection data the ring aliases is dead)
+    unsigned char* mychunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 16 * lane;
     const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
     const int colb = slice * kW4SliceCols + 32 * lane;
     const bool lane_on = colb < a.d_out;
-    unsigned char* mychunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 16 * lane;
     const uint8_t* wl = Wq + colb / 2;
     const size_t ldq = (size_t)a.d_out / 2;
     auto issue = [&](int m) {
@@ -94,39 +200,63 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
                                  wl + (size_t)lrow[warp + kGemvWarps * m] * ldq, lane_on);
         cp_async_commit();
     };
+    cp_async_commit();   // the scales: the group before the stream's first kW4Stages groups
 #pragma unroll
     for (int m = 0; m < kW4Stages; ++m) issue(m);
+    cp_async_wait<kW4Stages>();
+    __syncthreads();
+    // b[t][g] = (x_j s_rms) S[j][g0 + g] for each kept row, once per CTA (the stream reads one float)
+    {
+        const float sel_scale = reinterpret_cast<const float*>(misc)[4];
+        for (int t = threadIdx.x; t < n_list; t += kGemvThreads) {
+            const uint4 sc = lsc[t];
+            const float v = lval[t] * sel_scale;
+            auto h = [](uint32_t w, int hi) { return half_bits_to_f((uint16_t)(hi ? (w >> 16) : (w & 0xffffu))); };
+            lb[2 * t] = make_float4(v * h(sc.x, 0), v * h(sc.x, 1), v * h(sc.y, 0), v * h(sc.y, 1));
+            lb[2 * t + 1] = make_float4(v * h(sc.z, 0), v * h(sc.z, 1), v * h(sc.w, 0), v * h(sc.w, 1));
+        }
+    }
+    __syncthreads();
+    tl_stamp(a.tl, 2);
+
+    // warp w takes list entries w + 8 m; lane l owns columns 32 l .. 32 l + 31 of the slice (one
+    // scale group: l / 4) and copies exactly those 16 bytes of each row (no cross-lane dependency);
+    // the first kW4Stages rows are in flight since the prologue
     float2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
-    const int gsel = lane >> 2;   // the lane's 32 columns lie in group (32 lane) / 128 of the slice
+    const float* lbf = reinterpret_cast<const float*>(lb) + (lane >> 2);
+    // sum_j b_j (16 + q_j) accumulated, sum_j b_j beside it: y = acc - 24 sum_j b_j at the end
+    // (16 + q is one byte permute of a pre-shifted code byte; the offset costs ~3 bits of the fp32
+    // sums, far inside the 1e-5 parity bound)
+    float bsum = 0.f;
+    const uint32_t hibit = 0x80808080u, nmask = 0x78787878u;
     for (int m = 0; m < n_my; ++m) {
         cp_async_wait<kW4Stages - 1>();
         const int pos = warp + kGemvWarps * m;
         const uint4 q4 = lds128(mychunk + (size_t)(m % kW4Stages) * kW4RowBytes);
-        const uint4 sc = lsc[pos];
-        const int gw = gsel >> 1;
-        const uint32_t sw = gw == 0 ? sc.x : (gw == 1 ? sc.y : (gw == 2 ? sc.z : sc.w));
-        const float s = half_bits_to_f((uint16_t)((gsel & 1) ? (sw >> 16) : (sw & 0xffffu)));
-        const float v = lval[pos] * sel_scale * s;
+        const float b = lbf[(size_t)pos * 8];
+        bsum += b;
         const uint32_t qw[4] = {q4.x, q4.y, q4.z, q4.w};
-        // nibbles -> fp32 with one byte permute each: 0x4B0000nn is 2^23 + nn, so
-        // (2^23 + nn) - (2^23 + 8) = nn - 8 exactly; paired subtract + paired FMA
 #pragma unroll
         for (int wi = 0; wi < 4; ++wi) {
-            const uint32_t lo = qw[wi] & 0x0F0F0F0Fu, hi = (qw[wi] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                float2 w = make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540u + b)),
-                                       __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540u + b)));
-                fadd2_const(w, -8388616.0f);
-                ffma2(acc[4 * wi + b], w.x, w.y, v);
-            }
+            const uint32_t lo = and_or(qw[wi] << 3, nmask, hibit);   // low nibbles at bits 3-6
+            const uint32_t hi = and_or(qw[wi] >> 1, nmask, hibit);   // high nibbles at bits 3-6
+            ffma2(acc[4 * wi + 0], w4_f16q<0>(lo), w4_f16q<0>(hi), b);
+            ffma2(acc[4 * wi + 1], w4_f16q<1>(lo), w4_f16q<1>(hi), b);
+            ffma2(acc[4 * wi + 2], w4_f16q<2>(lo), w4_f16q<2>(hi), b);
+            ffma2(acc[4 * wi + 3], w4_f16q<3>(lo), w4_f16q<3>(hi), b);
         }
         issue(m + kW4Stages);
     }
     cp_async_wait<0>();
     __syncthreads();
+    tl_stamp(a.tl, 3);
+    {
+        const float corr = -24.0f * bsum;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) fadd2_const(acc[j], corr);
+    }
     // fixed-order sum of the 8 warps' partials, one fixed-point red per column (4 per thread)
     float* part = reinterpret_cast<float*>(smem);   // [8][1024]
     {
@@ -146,20 +276,28 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
             red_fix(a.acc + o, s, a.err);
         }
     }
-    if (a.epi == EPI_NONE) return;    // the consumer kernel reads the accumulators (QKV -> attention)
+    if (a.epi == EPI_NONE) {   // the consumer kernel reads the accumulators (QKV -> attention)
+        tl_stamp(a.tl, 4);
+        return;
+    }
     __syncthreads();
     if (threadIdx.x == 0) misc[0] = atom_add_acq_rel_gpu(a.tickets + slice, 1u) == gridDim.y - 1u;
+    tl_stamp(a.tl, 12);
     __syncthreads();
-    if (!misc[0]) return;
+    if (!misc[0]) {
+        tl_stamp(a.tl, 4);
+        return;
+    }
     if (threadIdx.x == 0) a.tickets[slice] = 0u;
+    tl_stamp(a.tl, 13);
     // the last split of the slice finalises its 1024 columns as four 256-column slices of the bf16
     // kernel's epilogue (bias / residual / SiLU(g) u, accumulators re-zeroed, and at batch 1 the next
     // site's histogram and RMS partials): the same output layout and selection data
-    for (int j = 0; j < kW4SliceCols / kSliceCols; ++j) {
-        const int vs = slice * (kW4SliceCols / kSliceCols) + j;
-        if (vs * kSliceCols >= a.d_out) break;
-        gemv_epilogue<1>(a, vs, reinterpret_cast<float*>(misc + 16));
-    }
+    constexpr int kNv = kW4SliceCols / kSliceCols;
+    const int vs0 = slice * kNv;
+    const int nv = min(kNv, (a.d_out - vs0 * kSliceCols + kSliceCols - 1) / kSliceCols);
+    gemv_epilogue_b1_multi<kNv>(a, vs0, nv, reinterpret_cast<float*>(misc + 16));
+    tl_stamp(a.tl, 4);
 }
 
 // Quantisation (offline): per row j and group g, scale = RNE_fp16(max_o |w| / 7) (fp32 divide);

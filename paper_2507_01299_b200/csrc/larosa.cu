@@ -467,7 +467,7 @@ larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, c
     const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
     a.n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
     a.list_cap = (int)(32 * ((nwords + a.n_splits - 1) / a.n_splits));
-    const size_t smem = w4_region_bytes((int)d_in) + (size_t)a.list_cap * 8 + kGemvMisc * 4 + (size_t)a.list_cap * 16;
+    const size_t smem = w4_smem_bytes((int)d_in, a.list_cap);
     if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "W4 site: shared memory plan too large");
     LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, smem), "cudaFuncSetAttribute(gemv_w4)"));
     return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, a.n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
@@ -2110,7 +2110,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
     const int n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
     const int list_cap = (int)(32 * ((nwords + n_splits - 1) / n_splits));
-    const size_t smem = w4_region_bytes((int)d_in) + (size_t)list_cap * 8 + kGemvMisc * 4 + (size_t)list_cap * 16;
+    const size_t smem = w4_smem_bytes((int)d_in, list_cap);
     GemvArgs a = gemv_args_base();
     a.ld = d_out;
     a.d_out = (int)d_out;

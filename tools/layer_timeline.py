@@ -26,13 +26,18 @@ def main():
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--adapter", default="down", choices=["down", "separate"])
+    ap.add_argument("--w4", action="store_true", help="W4A16 weights at all four sites (separate adapter)")
     args = ap.parse_args()
+    if args.w4:
+        args.adapter = "separate"
     shape = synth.MODELS[args.model]
     n = 4
     qs = [synth.haar_orthogonal(shape.d, 100 + i, device=DEV, dtype=torch.float32) for i in range(n + 1)]
     merged = args.adapter == "down"
     layers = [M.fold_layer(M.synth_original_layer(shape, i + 1, device=DEV), shape, qs[i], qs[i + 1],
                            adapter_in_down=merged) for i in range(n)]
+    if args.w4:
+        layers = [M.quantize_layer_w4(w, drop_bf16=True) for w in layers]
     ctx = 256
     kv = [(synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 900 + i, 1.0, DEV),
            synth.gaussian_bf16((1, shape.hkv, ctx, shape.hd), 950 + i, 1.0, DEV)) for i in range(n)]
@@ -59,7 +64,7 @@ def main():
         torch.cuda.synchronize()
         if r >= 3:
             acc.append(tl.cpu().numpy().astype(np.float64))
-    out = {"model": args.model, "p": args.p, "plan": list(plan), "kernels": {}}
+    out = {"model": args.model, "p": args.p, "plan": list(plan), "w4": args.w4, "kernels": {}}
     last = 4 if merged else 5
     lay = []
     for a in acc:
