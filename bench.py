@@ -366,12 +366,13 @@ def own_dense_model(model):
 
 def w4_decode_extra(shape, device, peaks, ps=(0.0, 0.4, 0.5), steps=20):
     """N3: the same decode step with W4A16 weights at all four sites of every layer (larosa.h ABI 6;
-    literal adapter form, bf16 head), batch 1, one CUDA graph per step (tests/test_gpu_w4_layer.py
+    adapter beside down, bf16 head), batch 1, one CUDA graph per step (tests/test_gpu_w4_layer.py
     is its parity)."""
     from paper_2507_01299_b200 import model as M
-    model = M.synth_decode_model(shape, shape.layers, device, seed=1, w4=True)
+    model = M.synth_decode_model(shape, shape.layers, device, seed=1, w4=True, adapter_in_down=True)
     run = M.DecodeRunner(model, 1, CTX, device)
-    out = {"weights": "int4 codes + fp16 scales per 128 outputs, all 4 sites; adapter separate; head bf16"}
+    out = {"weights": "int4 codes + fp16 scales per 128 outputs, all 4 sites; adapter bf16 beside down "
+                      "(companion CTAs of the W4 down launch); head bf16"}
     for pp in ps:
         pl = M.site_plan(shape, pp)
         reset_run(run, 5)

@@ -280,7 +280,7 @@ typedef struct {
      * (the bf16 w_* above) or the int4 codes [d_in][d_out/2] and fp16 group scales
      * [d_in][d_out/128] of larosa_quantize_w4 of that (folded) weight; the site then streams the
      * codes with the same fused Top-K prologue and epilogue (batch 1 only, EUNSUPPORTED otherwise;
-     * the down site needs the literal adapter form, adapter_in_down = 0). */
+     * with adapter_in_down the adapter rows stream as bf16 companion CTAs of the W4 down launch). */
     const uint8_t* w4_codes[4];
     const uint16_t* w4_scales[4];
 } larosa_layer_weights;

@@ -19,6 +19,8 @@ constexpr int kW4Group = 128;                 // == LAROSA_W4_GROUP
 constexpr int kW4SliceCols = 1024;            // columns per CTA: a kept row's slice segment is 512 B
 constexpr int kW4Stages = 16;                 // rows in flight per warp (one 512-byte row per stage): 64 KB per CTA
 constexpr int kW4RowBytes = kW4SliceCols / 2;
+constexpr int kW4CompRowBytes = kW4SliceCols * 2;                        // a companion bf16 row segment
+constexpr int kW4CompStages = kW4Stages * kW4RowBytes / kW4CompRowBytes;  // 4 rows per warp
 
 __device__ __forceinline__ float half_bits_to_f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 // paired fp32 add of a constant: {w.x, w.y} += {c, c}
@@ -150,8 +152,17 @@ __device__ void gemv_epilogue_b1_multi(const GemvArgs& a, int vs0, int nv, float
 __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const GemvArgs a, const uint8_t* __restrict__ Wq,
                                                                         const uint16_t* __restrict__ S) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int slice = blockIdx.x, split = blockIdx.y;
+    // blockIdx.y < n_splits2: companion CTAs streaming dense bf16 rows [c_lo, c_lo + c_n) of W2
+    // (ld = d_out) against x2 into the same accumulators (the residual adapter beside down)
+    const int slice = blockIdx.x, split = (int)blockIdx.y - a.n_splits2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool comp = split < 0;
+    int c_lo = 0, c_n = 0;
+    if (comp) {
+        const int rng = (a.d2 + a.n_splits2 - 1) / a.n_splits2;
+        c_lo = min(a.d2, (int)blockIdx.y * rng);
+        c_n = min(a.d2, c_lo + rng) - c_lo;
+    }
     const size_t rb = w4_region_bytes(a.d_in);
     int* lrow = reinterpret_cast<int*>(smem + rb);                                 // [cap]
     float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                     // [cap]
@@ -160,8 +171,26 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     float4* lb = reinterpret_cast<float4*>(lsc + a.list_cap);                      // [cap][2] b = v s per group
     const int ngroups = a.d_out / kW4Group;
 
+    const int colb = slice * kW4SliceCols + 32 * lane;
+    const bool lane_on = colb < a.d_out;
+    // companion ring: per warp kW4CompStages rows of 2 KB (lane l: the 64 bytes of its 32 columns)
+    unsigned char* cchunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 64 * lane;
+    const int c_my = c_n > warp ? (c_n - warp + kGemvWarps - 1) / kGemvWarps : 0;
+    auto comp_issue = [&](int m) {
+        if (m < c_my) {
+            const uint16_t* src = a.W2 + (size_t)(c_lo + warp + kGemvWarps * m) * a.d_out + colb;
+            unsigned char* dst = cchunk + (size_t)(m % kW4CompStages) * kW4CompRowBytes;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16(dst + 16 * q, src + 8 * q, lane_on);
+        }
+        cp_async_commit();
+    };
+    if (comp) {   // the first stages do not depend on the previous kernel
+#pragma unroll
+        for (int m = 0; m < kW4CompStages; ++m) comp_issue(m);
+    }
     int sel_guess = 0;
-    if (threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
+    if (!comp && threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
     tl_stamp(a.tl, 0);
     pdl_wait();
     pdl_trigger();
@@ -174,7 +203,32 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
         for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_acc_words; i += nct * kGemvThreads) a.zero_acc[i] = 0ull;
     }
-    const int n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
+    float2 acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
+    float bsum = 0.f;
+    int n_list;
+    if (comp) {
+        n_list = c_n;
+        for (int t = threadIdx.x; t < c_n; t += kGemvThreads) lval[t] = __ldcg(a.x2 + c_lo + t);
+        __syncthreads();
+        tl_stamp(a.tl, 2);
+        for (int m = 0; m < c_my; ++m) {
+            cp_async_wait<kW4CompStages - 1>();
+            const unsigned char* src = cchunk + (size_t)(m % kW4CompStages) * kW4CompRowBytes;
+            const float v = lval[warp + kGemvWarps * m];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 w = lds128(src + 16 * q);
+                ffma2(acc[4 * q + 0], bf16lo(w.x), bf16hi(w.x), v);
+                ffma2(acc[4 * q + 1], bf16lo(w.y), bf16hi(w.y), v);
+                ffma2(acc[4 * q + 2], bf16lo(w.z), bf16hi(w.z), v);
+                ffma2(acc[4 * q + 3], bf16lo(w.w), bf16hi(w.w), v);
+            }
+            comp_issue(m + kW4CompStages);
+        }
+    } else {
+    n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
     // the kept rows' 8 group scales of this slice (16 bytes), once, before the stream
     const int g0 = slice * (kW4SliceCols / kW4Group);
     const int ng = min(kW4SliceCols / kW4Group, ngroups - g0);
@@ -191,8 +245,6 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     // staged selection data the ring aliases is dead)
     unsigned char* mychunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 16 * lane;
     const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
-    const int colb = slice * kW4SliceCols + 32 * lane;
-    const bool lane_on = colb < a.d_out;
     const uint8_t* wl = Wq + colb / 2;
     const size_t ldq = (size_t)a.d_out / 2;
     auto issue = [&](int m) {
@@ -222,14 +274,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     // warp w takes list entries w + 8 m; lane l owns columns 32 l .. 32 l + 31 of the slice (one
     // scale group: l / 4) and copies exactly those 16 bytes of each row (no cross-lane dependency);
     // the first kW4Stages rows are in flight since the prologue
-    float2 acc[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
     const float* lbf = reinterpret_cast<const float*>(lb) + (lane >> 2);
     // sum_j b_j (16 + q_j) accumulated, sum_j b_j beside it: y = acc - 24 sum_j b_j at the end
     // (16 + q is one byte permute of a pre-shifted code byte; the offset costs ~3 bits of the fp32
     // sums, far inside the 1e-5 parity bound)
-    float bsum = 0.f;
     const uint32_t hibit = 0x80808080u, nmask = 0x78787878u;
     for (int m = 0; m < n_my; ++m) {
         cp_async_wait<kW4Stages - 1>();
@@ -249,6 +297,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
         }
         issue(m + kW4Stages);
     }
+    }   // SELECT split
     cp_async_wait<0>();
     __syncthreads();
     tl_stamp(a.tl, 3);

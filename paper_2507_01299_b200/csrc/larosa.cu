@@ -466,11 +466,29 @@ larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, c
     const int64_t nwords = (d_in + 31) / 32;
     const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
     a.n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
+    a.n_splits2 = 0;
+    if (a.W2) {   // companions (dense bf16 rows of W2): one wave split between the two row sets by bytes,
+                  // an int4 byte weighted 3x (the SELECT CTAs' prologue and dequantisation; measured on
+                  // the LLaMA3-8B down site: 40% companions, layer 84.2 -> 82.4 us)
+        static const int pct_env = env_int("LAROSA_W4_COMP_PCT", 0);   // tuning
+        const int total = std::max(2, sm_count() * 2 / n_sl);
+        const double main_b = (double)k * (kW4RowBytes + 2 * kW4SliceCols / kW4Group);
+        const double comp_b = (double)a.d2 * kW4CompRowBytes;
+        int n2 = pct_env > 0 ? (total * pct_env + 50) / 100 : (int)(total * comp_b / (3.0 * main_b + comp_b) + 0.5);
+        n2 = std::max(1, std::min(n2, total - by_cap));
+        a.n_splits = std::max(by_cap, total - n2);
+        a.n_splits2 = n2;
+    }
     a.list_cap = (int)(32 * ((nwords + a.n_splits - 1) / a.n_splits));
+    if (a.W2) {   // a companion's values live in the list: c_n <= list_cap
+        a.n_splits2 = std::max<int>(a.n_splits2, (int)((a.d2 + a.list_cap - 1) / a.list_cap));
+        if (a.n_splits + a.n_splits2 > 65535) return fail(LAROSA_EUNSUPPORTED, "W4 site: too many CTAs");
+    }
     const size_t smem = w4_smem_bytes((int)d_in, a.list_cap);
     if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "W4 site: shared memory plan too large");
     LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, smem), "cudaFuncSetAttribute(gemv_w4)"));
-    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, a.n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
+    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, a.n_splits + a.n_splits2), dim3(kGemvThreads), smem, st, a,
+                             Wq, S),
                       "gemv_w4 launch");
 }
 
@@ -1292,8 +1310,6 @@ larosa_status validate_layer(const larosa_layer_weights* w, const larosa_layer_p
             if (w->w4_codes[j] && douts[j] % 256)
                 return fail(LAROSA_EUNSUPPORTED, "sparse_layer: W4 site %d needs D_out %% 256 == 0", j);
     }
-    if (w->w4_codes[3] && w->adapter_in_down)
-        return fail(LAROSA_EUNSUPPORTED, "sparse_layer: a W4 down site needs the literal adapter (adapter_in_down = 0)");
     if (w->w4_codes[1] && w->adapter_mid) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: a W4 O site with adapter_mid");
     if ((s->host_in || s->host_out) && s->batch != 1) return fail(LAROSA_EINVAL, "sparse_layer: host_in/out need batch 1");
     if (w->n_q_heads / w->n_kv_heads > kAttnMaxG) return fail(LAROSA_EUNSUPPORTED, "sparse_layer: GQA group > 8");
@@ -1589,7 +1605,10 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             a.d2 = (int)L.d;
             epi(a, 2, EPI_STORE, nullptr, s->resid, 0);
             a.out_host = s->host_out;
-            LAROSA_TRY(launch_gemv(a, plan_gemv_comp(L.d, plan->k_h4, L.inter, L.d), 1, st));
+            if (w->w4_codes[3])
+                LAROSA_TRY(launch_gemv_w4(a, w->w4_codes[3], w->w4_scales[3], st));
+            else
+                LAROSA_TRY(launch_gemv(a, plan_gemv_comp(L.d, plan->k_h4, L.inter, L.d), 1, st));
         } else {
             a.epi = EPI_NONE;
             LAROSA_TRY(launch_gemv(a, plan_site(L.d, L.inter, plan->k_h4), bp, st));

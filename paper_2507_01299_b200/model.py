@@ -89,10 +89,8 @@ W4_SITES = ("w_qkv", "w_o", "w_gu", "w_down")
 
 def quantize_layer_w4(lw: LZ.LayerWeights, sites=(0, 1, 2, 3), drop_bf16: bool = False) -> LZ.LayerWeights:
     """The layer with W4A16 weights (larosa_quantize_w4 of the folded bf16 weights) at the given
-    sites (0 QKV, 1 O, 2 gate|up, 3 down).  A W4 down site needs the literal
-    adapter form (adapter_in_down False); drop_bf16 releases the bf16 copies of those sites."""
-    if 3 in sites and lw.adapter_in_down:
-        raise ValueError("quantize_layer_w4: a W4 down site needs adapter_in_down=False")
+    sites (0 QKV, 1 O, 2 gate|up, 3 down): the folded weights as they are (with
+    adapter_in_down the down weight is W_down Q_{l+1}); drop_bf16 releases the bf16 copies."""
     w4 = [LZ.quantize_w4(getattr(lw, W4_SITES[j])) if j in sites else None for j in range(4)]
     kw = {W4_SITES[j]: None for j in sites} if drop_bf16 else {}
     return dataclasses.replace(lw, w4=w4, **kw)
@@ -127,7 +125,7 @@ def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int
                        vocab: Optional[int] = None, adapter_in_down: bool = False, w4: bool = False) -> DecodeModel:
     """Random-init model of the given shape (synthetic weights), folded with
     the library's own tensor-core fold; w4: every layer's four sites as W4A16 weights (the bf16
-    copies released; literal adapter form)."""
+    copies released)."""
     vocab = vocab or shape.vocab
     d = shape.d
     qs = [synth.haar_orthogonal(d, 7000 + 100 * seed + l, device=device, dtype=torch.float32)
@@ -139,7 +137,7 @@ def synth_decode_model(shape: synth.ModelShape, n_layers: int, device, seed: int
     for l in range(n_layers):
         orig = synth_original_layer(shape, 10 * seed + l + 1, device=device)
         lw = fold_layer(orig, shape, qs[l], qs[l + 1] if l + 1 < n_layers else None,
-                        adapter_in_down=adapter_in_down and not w4)
+                        adapter_in_down=adapter_in_down)
         layers.append(quantize_layer_w4(lw, drop_bf16=True) if w4 else lw)
         del lw
         del orig

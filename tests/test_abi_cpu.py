@@ -177,8 +177,7 @@ def test_new_entry_points_validation():
     w.adapter_in_down = 0
     s3 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 2, 0, FAKE, None)
     assert L.larosa_sparse_layer(ctypes.byref(w), ctypes.byref(p), ctypes.byref(s3), None, ws, 1 << 40, None) == 1
-    # W4 sites (ABI 6): codes without scales, batch > 1, a W4 down site beside a merged adapter,
-    # D_out % 256 (gate|up of inter 11008 + 64), and a NULL bf16 weight without W4 codes
+    # W4 sites (ABI 6): codes without scales, batch > 1, D_out % 256 (gate|up of inter 11008 + 64), and a NULL bf16 weight without W4 codes
     s1 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 1)
     s2 = LZ.LayerStateC(FAKE, FAKE, FAKE, FAKE, 256, 2)
     w4 = LZ.LayerWeightsC(FAKE, None, FAKE, FAKE, FAKE, FAKE, 4096, 11008, 32, 32, 128, 1e4, 1e-5, 0, None)
@@ -187,9 +186,6 @@ def test_new_entry_points_validation():
     w4.w4_scales[0] = FAKE
     assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s2), None, ws, 1 << 40, None) == 3
     w4.w4_codes[3] = w4.w4_scales[3] = FAKE
-    w4.adapter_in_down = 1
-    assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 3
-    w4.adapter_in_down = 0
     w4.inter = 11008 + 64
     w4.w4_codes[2] = w4.w4_scales[2] = FAKE
     assert L.larosa_sparse_layer(ctypes.byref(w4), ctypes.byref(p), ctypes.byref(s1), None, ws, 1 << 40, None) == 3

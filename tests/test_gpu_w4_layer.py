@@ -1,6 +1,6 @@
 """GPU parity of the W4A16 decoder layer and decode step (larosa.h ABI 6):
 larosa_sparse_layer with int4 weights at some or all of its four sites (batch 1: the fused
-Top-K prologue of the bf16 path, then the int4 stream; literal adapter form), site by site
+Top-K prologue of the bf16 path, then the int4 stream; either adapter form), site by site
 against the oracle (P6, tests/layer_check.py).  The oracle quantises the folded bf16 weights
 itself (O.quantize_w4, P:306-344 reading in DESIGN.md), the GPU codes and scales must equal its
 codes bit for bit, and the oracle's dequantised matrices stand in for the bf16 ones."""
@@ -53,10 +53,15 @@ def oracle_weights_w4(lw4, inter):
     (SMALL, 7, 0.5, (0, 1, 2, 3), True), (SMALL_MHA, 40, 0.4, (0, 3), True), (SMALL, 20, 0.5, (1, 2), False),
     (synth.MODELS["llama3-8b"], 200, 0.4, (0, 1, 2, 3), True),
     (synth.MODELS["qwen2.5-7b"], 77, 0.25, (0, 1, 2, 3), True),   # QKV bias on the W4 QKV site
-    (synth.MODELS["llama2-7b"], 256, 0.5, (2, 3), False)])
+    (synth.MODELS["llama2-7b"], 256, 0.5, (2, 3), False),
+    # adapter folded beside down (W4 codes of W_down Q_{l+1}, the adapter rows as bf16 companion CTAs)
+    (SMALL, 9, 0.5, (0, 1, 2, 3), "merged"), (SMALL_MHA, 30, 0.25, (3,), "merged"),
+    (synth.MODELS["llama3-8b"], 150, 0.4, (0, 1, 2, 3), "merged"),
+    (synth.MODELS["mistral-7b"], 90, 0.6, (0, 1, 2, 3), "merged")])
 def test_w4_layer_p6_sitewise(shape, ctx, p, sites, adapter):
     max_ctx = max(ctx, 64)
-    _, _, _, lw, plan, resid, kc0, vc0, pos = build(shape, 13, 1, ctx, max_ctx, p, with_adapter=adapter)
+    _, _, _, lw, plan, resid, kc0, vc0, pos = build(shape, 13, 1, ctx, max_ctx, p, with_adapter=bool(adapter),
+                                                    merged=adapter == "merged")
     lw4 = M.quantize_layer_w4(lw, sites)
     st, tp = run_layer(lw4, plan, resid, kc0, vc0, pos)
     ow = oracle_weights_w4(lw4, shape.inter)
@@ -87,17 +92,15 @@ def test_w4_layer_rejections():
     st = LZ.LayerState(resid.clone().to(DEV), kc0.clone().to(DEV), vc0.clone().to(DEV), pos.to(DEV))
     with pytest.raises(RuntimeError, match="W4 sites need batch 1"):
         LZ.sparse_layer(lw4, plan, st)
-    _, _, _, lwm, *_ = build(shape, 19, 1, 9, 64, 0.5, merged=True)
-    with pytest.raises(ValueError):
-        M.quantize_layer_w4(lwm)
 
 
 def test_w4_decode_step_llama3_8b():
-    """Two chained W4 layers + the LM head (batch 1, the decode step of the W4 bench extra):
+    """Two chained W4 layers (adapter beside down) + the LM head (batch 1, the decode step of the W4
+    bench extra):
     P6 at every site of both layers and the logits on the GPU's final residual."""
     shape = synth.MODELS["llama3-8b"]
     n_layers, max_ctx, ctx, p = 2, 256, 180, 0.4
-    model = M.synth_decode_model(shape, n_layers, DEV, seed=5, vocab=32768)
+    model = M.synth_decode_model(shape, n_layers, DEV, seed=5, vocab=32768, adapter_in_down=True)
     model.layers = [M.quantize_layer_w4(w) for w in model.layers]
     run = M.DecodeRunner(model, 1, max_ctx, DEV)
     g = torch.Generator().manual_seed(23)

@@ -26,10 +26,8 @@ def main():
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--adapter", default="down", choices=["down", "separate"])
-    ap.add_argument("--w4", action="store_true", help="W4A16 weights at all four sites (separate adapter)")
+    ap.add_argument("--w4", action="store_true", help="W4A16 weights at all four sites")
     args = ap.parse_args()
-    if args.w4:
-        args.adapter = "separate"
     shape = synth.MODELS[args.model]
     n = 4
     qs = [synth.haar_orthogonal(shape.d, 100 + i, device=DEV, dtype=torch.float32) for i in range(n + 1)]
