@@ -19,10 +19,11 @@
 //           gemv_tc.cuh.
 #pragma once
 #include "gemv_tc.cuh"
+#include "img_layout.cuh"
 
 namespace larosa {
 
-constexpr int kImgChunkBytes = 2 * kTcBBytes;           // 4 KB: 32 MMA rows (16 hi, 16 lo) x 64 K x bf16
+static_assert(kImgChunkBytes == 2 * kTcBBytes, "image chunk = 32 MMA rows (16 hi, 16 lo) x 64 K x bf16");
 constexpr int kImgStageBytes = kTcABytes + kImgChunkBytes;   // 20 KB
 #ifndef LAROSA_IMG_STAGES
 #define LAROSA_IMG_STAGES 4
@@ -31,10 +32,6 @@ constexpr int kImgStages = LAROSA_IMG_STAGES;
 constexpr int kImgThreads = 192;
 __host__ __device__ constexpr size_t gemv_img_smem_bytes() { return 1024 + (size_t)kImgStages * kImgStageBytes + 128; }
 
-// byte offset of value (MMA row n in 0..31, K index k in 0..63) inside a chunk's 4 KB image
-__host__ __device__ constexpr int img_off(int n, int k) {
-    return (n >> 3) * 1024 + (n & 7) * 128 + ((((k >> 3) ^ (n & 7))) << 4) + (k & 7) * 2;
-}
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(smem_dst)),

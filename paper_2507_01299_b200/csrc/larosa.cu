@@ -1430,6 +1430,13 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             r.k = (int)k;
             r.rms_eps = eps;
             r.rule_out = W.thr[si];
+            // (tuning: 0 = the image from a separate rule_apply_image launch)
+            static const int topk_image = env_int("LAROSA_TOPK_IMAGE", 1);
+            if (img_path && topk_image) {   // the cluster Top-K kernel writes the image too
+                r.img = W.img[si];
+                r.img_raw = (unsigned char*)raw;
+                return launch_topk(r, B, st);
+            }
             LAROSA_TRY(launch_topk(r, B, st));
             if (!img_path) return LAROSA_OK;
             const int groups = (int)((din + 7) / 8);

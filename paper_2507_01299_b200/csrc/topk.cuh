@@ -22,6 +22,7 @@
 #pragma once
 #include "common.cuh"
 #include "gemv.cuh"   // fixed-point accumulator helpers, kGuBlock
+#include "img_layout.cuh"
 
 namespace larosa {
 
@@ -67,7 +68,27 @@ struct TopkKernelArgs {
     unsigned long long* acc; int64_t acc_ld;              // SRC_RESID_ACC / SRC_SILU_GU
     unsigned long long* zero; int64_t zero_ld; int zero_n; // optional extra zeroing per token
     ThreshOut* rule_out;  // [batch] if set: emit the selection rule (no idx/vals lists)
+    unsigned char* img;      // rule mode, batch 2-16: also write the token image (img_layout.cuh) of
+    unsigned char* img_raw;  // the masked scaled values, and optionally of the raw values
 };
+
+// token b's element i = v of the image: masked and scaled (keep ? v s : 0) split bf16 hi | lo, and
+// the raw value split the same way (the arithmetic of rule_apply_image_kernel)
+__device__ __forceinline__ void topk_img_put(unsigned char* img, unsigned char* raw, int b, int i, float v, bool keep,
+                                             float s) {
+    const float f = keep ? v * s : 0.f;
+    const uint16_t h = f2bf16_rne(f);
+    const int kk = i & (kImgChunkK - 1);
+    unsigned char* ch = img + (size_t)(i / kImgChunkK) * kImgChunkBytes;
+    *reinterpret_cast<uint16_t*>(ch + img_off(b, kk)) = h;
+    *reinterpret_cast<uint16_t*>(ch + img_off(16 + b, kk)) = f2bf16_rne(f - bf16f(h));
+    if (raw) {
+        const uint16_t rh = f2bf16_rne(v);
+        unsigned char* cr = raw + (size_t)(i / kImgChunkK) * kImgChunkBytes;
+        *reinterpret_cast<uint16_t*>(cr + img_off(b, kk)) = rh;
+        *reinterpret_cast<uint16_t*>(cr + img_off(16 + b, kk)) = f2bf16_rne(v - bf16f(rh));
+    }
+}
 
 __device__ __forceinline__ void topk_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -277,7 +298,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
     // ---- rule mode: publish (Tk, Ti, s) instead of the index list ------------------------
     // keep i iff key > Tk or (key == Tk and i <= Ti)  (the consumer GEMV selects its rows)
     if (a.rule_out && (exact_ge || !tie_mode)) {
-        if (rank == 0 && tid == 0) {
+        if ((rank == 0 && tid == 0) || a.img) {   // (every thread needs the scale for the image)
             float tot = 0.f;
             uint32_t psq[kTopkMaxCluster];
 #pragma unroll
@@ -286,12 +307,21 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
 #pragma unroll
             for (int q = 0; q < kTopkMaxCluster; ++q)
                 if (q < cs) tot += __uint_as_float(psq[q]);
-            ThreshOut r;
-            r.tk = thr;
-            r.ti = 0x7fffffff;   // key == Tk (the bucket's lower edge) is kept too
-            r.scale = a.rms_eps >= 0.f ? 1.0f / sqrtf(tot / (float)d + a.rms_eps) : 1.0f;
-            r.pad = 0;
-            a.rule_out[b] = r;
+            const float scale = a.rms_eps >= 0.f ? 1.0f / sqrtf(tot / (float)d + a.rms_eps) : 1.0f;
+            if (rank == 0 && tid == 0) {
+                ThreshOut r;
+                r.tk = thr;
+                r.ti = 0x7fffffff;   // key == Tk (the bucket's lower edge) is kept too
+                r.scale = scale;
+                r.pad = 0;
+                a.rule_out[b] = r;
+            }
+            if (a.img) {
+#pragma unroll
+                for (int j = 0; j < EPT; ++j)
+                    if (VALID(j)) topk_img_put(a.img, a.img_raw, b, lo + j * NT + tid, __uint_as_float(xv[j]), KEY(j) >= thr,
+                                               scale);
+            }
         }
         topk_cluster_sync();   // rank 0 read the others' published partials
         return;
@@ -399,6 +429,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
                 r.pad = 0;
                 a.rule_out[b] = r;
             }
+            if (a.img && valid) topk_img_put(a.img, a.img_raw, b, i, __uint_as_float(xv[j]), sel, scale);
         } else if (sel) {
             out_idx[pos] = i;
             out_vals[pos] = __uint_as_float(xv[j]) * scale;
