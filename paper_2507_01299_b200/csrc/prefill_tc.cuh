@@ -34,7 +34,15 @@ constexpr int kPfBBytes = kPfTok * kPfK * 2;      // 32 KB
 constexpr int kPfGemmThreads = 192;
 
 __host__ __device__ constexpr int pf_stage_bytes(bool split) { return kPfABytes + (split ? 2 : 1) * kPfBBytes; }
-__host__ __device__ constexpr int pf_stages(bool split) { return split ? 2 : 4; }
+// bf16 mode: 2 stages of 48 KB and 2 CTAs per SM (one CTA's epilogue overlaps the other's MMAs):
+// 512 tokens x 4096 x 22016 0.131 -> 0.119 ms, 2048 tokens 0.475 -> 0.406 ms vs 4 stages, 1 CTA/SM
+#ifndef LAROSA_PF_STAGES
+#define LAROSA_PF_STAGES 2
+#endif
+#ifndef LAROSA_PF_MINB
+#define LAROSA_PF_MINB 2
+#endif
+__host__ __device__ constexpr int pf_stages(bool split) { return split ? 2 : LAROSA_PF_STAGES; }
 __host__ __device__ constexpr size_t pf_smem_bytes(bool split) {
     return 1024 + (size_t)pf_stages(split) * pf_stage_bytes(split) + 128 + 2 * 512;
 }
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(kPfThreads) prefill_rule_mask_kernel(const flo
 
 // ---- 2. the masked GEMM on tcgen05 ---------------------------------------------------------------
 template <bool SPLIT>
-__global__ void __launch_bounds__(kPfGemmThreads, 1)
+__global__ void __launch_bounds__(kPfGemmThreads, LAROSA_PF_MINB)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap tXh,
                       const __grid_constant__ CUtensorMap tXl, const uint8_t* __restrict__ anyk, int n_tok_pad,
                       int n_tok, int d_in, int d_out, float* __restrict__ Y) {
