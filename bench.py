@@ -427,6 +427,8 @@ def main():
     ap.add_argument("--adapter", default="down", choices=["down", "separate"])
     ap.add_argument("--model", default=None, help="sharded-70b: llama3-70b (default) or qwen2.5-72b")
     ap.add_argument("--layers", type=int, default=None, help="sharded-70b: layer count (default: the model's)")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "p2p"],
+                    help="sharded-70b: NCCL all-gathers, or the phase kernels' P2P push into symmetric memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

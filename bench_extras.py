@@ -450,7 +450,16 @@ def run_sharded(args):
     n_layers = getattr(args, "layers", None) or shape.layers
     B, max_ctx = args.batch, 256
     model = M.ShardedDecodeModel(shape, n_layers, rank, ws_n, device, seed=3, adapter_in_down=args.adapter == "down")
-    run = M.ShardedDecodeRunner(model, B, max_ctx, device)
+    collective = getattr(args, "collective", "nccl")
+    if collective == "p2p":   # the phase kernels push into every rank's symmetric buffers
+        if ws_n == 1 and not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(device))
+        space = M.PeerSpace.symmetric(M.ShardedDecodeRunner.peer_bytes(model, B), device)
+        run = M.ShardedDecodeRunner(model, B, max_ctx, device, space=space)
+    else:
+        run = M.ShardedDecodeRunner(model, B, max_ctx, device)
     for kc, vc in run.kv:
         kc.copy_(synth.gaussian_bf16(kc.shape, 5 + rank, 1.0, device))
         vc.copy_(synth.gaussian_bf16(vc.shape, 6 + rank, 1.0, device))
@@ -504,11 +513,14 @@ def run_sharded(args):
                "config": {"workload": f"{shape.name} decode step ({n_layers} layers, d {shape.d}, MLP {shape.inter}, "
                                       f"GQA {shape.hq}/{shape.hkv}), row-sharded", "batch": B, "sparsity": args.p,
                           "plan_k": list(plan), "ctx": max_ctx,
-                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{n_ph}/layer + logits)",
+                          "parallelism": f"tp{ws_n} (row-sharded, NCCL all-gather x{n_ph}/layer + logits)"
+                          if collective != "p2p" else
+                          f"tp{ws_n} (row-sharded, P2P push from the phase kernels into symmetric memory "
+                          f"x{n_ph}/layer + logits, device-side counters)", "collective": collective,
                           "l2": "inputs larger than L2: the step streams the whole sharded model"},
                "gpu_launches": None, "clocks": clk.summary()}
         print(json.dumps(out))
-    if ws_n > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

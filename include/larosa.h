@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LAROSA_ABI_VERSION 6
+#define LAROSA_ABI_VERSION 7
 #define LAROSA_MAX_BATCH 16          /* decode batch 1..16 (BASELINE.json north_star) */
 #define LAROSA_MAX_DIM 32768         /* largest D_in of any site (Qwen2.5-72B I = 29568) */
 #define LAROSA_GU_BLOCK 64           /* gate|up interleave block, see larosa_pack_gate_up */
@@ -380,6 +380,16 @@ larosa_status larosa_sparse_layer(const larosa_layer_weights* w, const larosa_la
 typedef struct {
     int32_t rank, world;
     int32_t batch;       /* tokens per step, 1..16 (ABI 5) */
+    /* P2P push of the phase output instead of an all-gather (ABI 7; NULL = off):
+     * DEVICE arrays of `world` addresses -- peer_dst[p]: rank p's gathered buffer for this phase's
+     * output ([batch][peer_ld] fp32, e.g. torch symmetric memory mapped over NVLink), already offset
+     * to THIS rank's first column; peer_flag[p]: rank p's uint32 arrival counter.  The kernel that
+     * produces `out` also stores every value into every rank's buffer and then adds the number of
+     * values it stored to every rank's counter (release, system scope); each rank then calls
+     * larosa_shard_wait(its counter, batch * world * d_local) before reading its buffer. */
+    const uint64_t* peer_dst;
+    const uint64_t* peer_flag;
+    int64_t peer_ld;
 } larosa_shard;
 size_t larosa_shard_workspace_size(const larosa_layer_weights* w, const larosa_shard* shard, int64_t max_ctx);
 larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, const larosa_layer_plan* plan,
@@ -387,6 +397,19 @@ larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weights* w, con
                                               const float* resid, float* out, uint16_t* k_cache,
                                               uint16_t* v_cache, const int32_t* pos, int64_t max_ctx, void* ws,
                                               size_t ws_bytes, larosa_stream_t stream);
+
+/* The consumer side of the P2P push (ABI 7): *expected += count, then wait (one device thread,
+ * acquire at system scope) until the arrival counter *flag has reached *expected (wrap-safe).
+ * expected: a device word of the caller's, zero at first use, only ever touched by this call.
+ * Graph capturable; the following kernels in the stream see every pushed value. */
+larosa_status larosa_shard_wait(const uint32_t* flag, uint32_t* expected, uint32_t count, larosa_stream_t stream);
+
+/* P2P all-gather of an arbitrary [batch][d_local] fp32 slice (src row stride src_ld): every value
+ * into every rank's buffer (peer_dst / peer_flag / peer_ld as in larosa_shard), then the counters
+ * (the LM head's logits in the sharded decode step).  ABI 7. */
+larosa_status larosa_peer_push(const float* src, int32_t batch, int64_t d_local, int64_t src_ld,
+                               const uint64_t* peer_dst, const uint64_t* peer_flag, int32_t world,
+                               int64_t peer_ld, larosa_stream_t stream);
 
 /* gathered fp32 [world][batch][d_local] (an NCCL all_gather_into_tensor of every rank's
  * [batch][d_local] phase output) -> out [batch][world * d_local] (the full vectors in column

@@ -41,6 +41,7 @@ struct AttnArgs {
     int zero_words;
     unsigned long long* tl;   // debug timeline slot or null
     int keep_acc;          // 1: leave the QKV accumulators to the next kernel to re-zero (batch-1 layer)
+    PeerOut peer;          // sharded phase 0: push h2 to every rank (n = 0: off)
 };
 
 constexpr int kAttnGroupCounterOff = 2048;   // counters: [0, B Hq) head tickets, then group tickets
@@ -287,11 +288,13 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
                 }
                 const float hv = Ov / L;
                 a.out[(size_t)b * a.hq * hd + (size_t)h * hd + dd] = hv;
+                if (a.peer.n) peer_put(a.peer, b, h * hd + dd, hv);
                 if (a.out_sel.hist) hist_push(a.out_sel, hv, h * hd + dd);
             }
         }
         cluster_sync_all();                 // rank 0 has read every CTA's shared memory
         if (cluster_ctarank() != 0) return;
+        peer_signal(a.peer, (unsigned)hd);
         tl_stamp(a.tl, 6);
     } else {
     fence_acq_rel_gpu();
@@ -338,8 +341,10 @@ __device__ void attention_body(const AttnArgs& a, float* asmem) {
         }
         const float hv = Ov / L;
         a.out[(size_t)b * a.hq * hd + (size_t)h * hd + dd] = hv;
+        if (a.peer.n) peer_put(a.peer, b, h * hd + dd, hv);
         if (a.out_sel.hist) hist_push(a.out_sel, hv, h * hd + dd);
     }
+    peer_signal(a.peer, (unsigned)hd);
     tl_stamp(a.tl, 6);
     }
     if (a.keep_acc) return;   // the O GEMV re-zeroes the QKV accumulators after this kernel
@@ -569,8 +574,10 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
         const float hv = Ov / L;
         const int col = (h0 + hh) * hd + dd;
         a.out[(size_t)b * nq + col] = hv;
+        if (a.peer.n) peer_put(a.peer, b, col, hv);
         if (a.out_sel.hist) hist_push(a.out_sel, hv, col);
     }
+    peer_signal(a.peer, (unsigned)(hpc * hd));
     tl_stamp(a.tl, 6);
     if (a.keep_acc) {
         tl_stamp(a.tl, 4);

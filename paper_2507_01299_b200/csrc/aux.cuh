@@ -264,4 +264,41 @@ __global__ void __launch_bounds__(256) fold_simt_kernel(const float* __restrict_
             if (m < M && n < N) out[(size_t)m * N + n] = f2bf16_rne(acc[i][j]);
         }
 }
+// ---- P2P push / wait of the sharded decode step (larosa_peer_push / _shard_wait)
+__global__ void peer_push_kernel(const float* __restrict__ src, int batch, int d_local, int64_t src_ld, PeerOut peer) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n = (int64_t)batch * d_local;
+    unsigned cnt = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(i / d_local), c = (int)(i % d_local);
+        peer_put(peer, b, c, src[(size_t)b * src_ld + c]);
+    }
+    // values stored by this CTA (the grid-stride ranges are disjoint and cover [0, n))
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x)
+        cnt += (unsigned)(n - i0 < (int64_t)blockDim.x ? n - i0 : (int64_t)blockDim.x);
+    peer_signal(peer, cnt);
+}
+
+#ifndef LAROSA_PEER_SLEEP
+#define LAROSA_PEER_SLEEP 0
+#endif
+__global__ void peer_wait_kernel(const uint32_t* flag, uint32_t* expected, uint32_t count) {
+    pdl_wait();   // the stream's previous kernel (this rank's own producer) is complete
+    if (threadIdx.x == 0) {
+        const uint32_t t = *expected + count;
+        *expected = t;
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if ((int32_t)(v - t) >= 0) break;
+#if LAROSA_PEER_SLEEP
+            __nanosleep(LAROSA_PEER_SLEEP);
+#endif
+        }
+    }
+    __syncthreads();
+    pdl_trigger();
+}
+
 }  // namespace larosa

@@ -35,6 +35,47 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // trigger: allow the next kernel in the stream to start its prologue early.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---- peer push of a sharded phase's output ----------------------------------
+// The producing kernel stores every output value straight into every rank's gathered buffer (peer
+// device memory over NVLink, e.g. torch symmetric memory) and then adds the number of values it
+// wrote to every rank's arrival counter (release, system scope); the consumer waits until its
+// counter reaches batch x the full width (larosa_shard_wait).  n = 0: off.
+struct PeerOut {
+    const unsigned long long* dst;    // [n] device addresses: rank p's buffer, at this rank's column 0
+    const unsigned long long* flag;   // [n] device addresses: rank p's uint32 arrival counter
+    int n;
+    int ld;                           // token stride of the gathered buffers (floats): the full width
+};
+__device__ __forceinline__ void peer_put(const PeerOut& P, int b, int col, float v) {
+    for (int q = 0; q < P.n; ++q) reinterpret_cast<float*>(P.dst[q])[(size_t)b * P.ld + col] = v;
+}
+// called by EVERY thread of the CTA after all of its peer_put calls; cnt = values the CTA wrote
+#ifndef LAROSA_PEER_FENCE
+#define LAROSA_PEER_FENCE 0   // 1: every thread also fences its own stores (fence.acq_rel.sys)
+#endif
+__device__ __forceinline__ void peer_signal(const PeerOut& P, unsigned cnt) {
+    if (P.n == 0) return;
+    if (LAROSA_PEER_FENCE) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    // the CTA barrier puts every thread's stores before thread 0's release in causality order, and
+    // a release is cumulative (the arrive pattern of a grid barrier: bar.sync, then one red.release)
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt)
+        for (int q = 0; q < P.n; ++q)
+            asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(P.flag[q]), "r"(cnt) : "memory");
+}
+
+// the push of a finalised column block [col0, col0 + ncols) x batch of `out` (written by this
+// CTA; thread t re-reads column col0 + t, t < ncols <= blockDim.x) + the signal; out of line so
+// the hot kernels' register allocation does not see it.  Every thread of the CTA calls it.
+__device__ __noinline__ void peer_push_cols(const PeerOut P, const float* out, int64_t out_ld, int batch, int col0,
+                                            int ncols) {
+    __syncthreads();   // the block's writes of `out` are visible to all of its threads
+    const int t = threadIdx.x;
+    if (t < ncols)
+        for (int b = 0; b < batch; ++b) peer_put(P, b, col0 + t, out[(size_t)b * out_ld + col0 + t]);
+    peer_signal(P, (unsigned)(batch * (ncols > 0 ? ncols : 0)));
+}
+
 // ---- debug timeline (profiling aid; null pointer = off) -----------------------------------
 // Per CTA (linear id c < 1024): tl[c * 16 + i] = %globaltimer (ns) at point i: 0 entry, 1 after
 // griddepcontrol.wait, 2 after the prologue, 3 after the main loop, 4 exit.

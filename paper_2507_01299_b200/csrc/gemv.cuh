@@ -170,6 +170,7 @@ struct GemvArgs {
     uint32_t* err;                     // the workspace's error word (larosa_error_flags) or null
     const void* img;                   // batch >= 8, contiguous rows: the pre-built token operand (gemv_img.cuh)
     int comp_late;                     // tuning: companions issue their first stages after the dependency wait
+    PeerOut peer;                      // sharded phases: push every output value to every rank (n = 0: off)
 };
 
 // error bits of a workspace's error word (larosa.h larosa_error_flags)
@@ -768,6 +769,13 @@ __device__ void gemv_epilogue(const GemvArgs& a, int slice, float* sred, const f
             if (c == 0) a.out_ssq[(size_t)b * a.out_ssq_ld + slice] = slice_ssq_combine(sred);
             __syncthreads();
         }
+    }
+    if (a.peer.n) {   // the slice's outputs (thread c wrote output column c of the block) to every rank
+        if (a.epi == EPI_SILU)
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, slice * 2 * kGuBlock,
+                           kGuBlock * min(2, max(0, (a.d_out - base + 2 * kGuBlock - 1) / (2 * kGuBlock))));
+        else
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, base, min(kSliceCols, max(0, a.d_out - base)));
     }
 }
 

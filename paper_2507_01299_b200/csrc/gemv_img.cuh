@@ -160,9 +160,9 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
     __syncthreads();
     if (!*flag) return;
     if (tid == 0) a.tickets[slice] = 0u;
-    const int e = tid - 64;                       // epilogue threads 0..127
-    if (e < 0) return;
-    if (a.epi == EPI_SILU) {
+    const int e = tid - 64;                       // epilogue threads 0..127 (tid 0..63 idle)
+    if (e < 0) {
+    } else if (a.epi == EPI_SILU) {
         if (e < kGuBlock && col0 + e < a.d_out) {
             float g[BP], u[BP];
 #pragma unroll
@@ -200,6 +200,12 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
                 if (a.res) y = r[b] + y;
                 a.out[(size_t)b * a.out_ld + o] = y;
             }
+    }
+    if (a.peer.n) {   // the block's outputs to every rank (thread e wrote output column e)
+        if (a.epi == EPI_SILU)
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, slice * kGuBlock, min(kGuBlock, max(0, a.d_out - col0)));
+        else
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, col0, min(kTcCols, max(0, a.d_out - col0)));
     }
 }
 

@@ -413,6 +413,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
                 a.out[(size_t)b * a.out_ld + o] = y;
             }
     }
+    if (a.peer.n) {   // the block's outputs to every rank (thread tid wrote output column tid)
+        if (a.epi == EPI_SILU)
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, slice * kGuBlock, min(kGuBlock, max(0, a.d_out - col0)));
+        else
+            peer_push_cols(a.peer, a.out, a.out_ld, a.batch, col0, min(kTcCols, max(0, a.d_out - col0)));
+    }
     tl_stamp(a.tl, 4);
 }
 

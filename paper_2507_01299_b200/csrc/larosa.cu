@@ -1794,6 +1794,16 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     const void* ptrs[] = {x, resid, out, Wt, w->adapter, k_cache, v_cache};
     for (const void* q : ptrs)
         if (q && !aligned16(q)) return fail(LAROSA_EINVAL, "shard_phase: pointers must be 16-byte aligned");
+    PeerOut peer;
+    memset(&peer, 0, sizeof(peer));
+    if (sh->peer_dst || sh->peer_flag) {
+        if (!sh->peer_dst || !sh->peer_flag || sh->peer_ld <= 0)
+            return fail(LAROSA_EINVAL, "shard_phase: peer_dst, peer_flag and peer_ld go together");
+        peer.dst = reinterpret_cast<const unsigned long long*>(sh->peer_dst);
+        peer.flag = reinterpret_cast<const unsigned long long*>(sh->peer_flag);
+        peer.n = sh->world;
+        peer.ld = (int)sh->peer_ld;
+    }
     GemvArgs a = gemv_args_base();
     a.W = Wt;
     a.ld = dout;
@@ -1865,7 +1875,10 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         }
         a.out = out;
         a.out_ld = phase == 2 ? S.il : S.dl;
-        if (!dense2) return launch_gemv(a, p, fused ? 1 : bp, st);
+        if (!dense2) {
+            a.peer = peer;
+            return launch_gemv(a, p, fused ? 1 : bp, st);
+        }
         // the sparse down columns leave their sums; the dense adapter GEMV (r_mid rows) finalises
         const int epi_mode = a.epi;
         a.epi = EPI_NONE;
@@ -1885,6 +1898,7 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
         b2.tickets = W.tickets;
         b2.out = out;
         b2.out_ld = S.dl;
+        b2.peer = peer;
         if (img_path) {
             LAROSA_TRY(launch_dense_image(resid, S.d, S.d, B, W.img2, st));
             b2.img = W.img2;
@@ -1911,7 +1925,34 @@ extern "C" larosa_status larosa_sparse_layer_shard_phase(const larosa_layer_weig
     aa.part = W.attn_part;
     aa.counters = W.attn_cnt;
     aa.out = out;
+    aa.peer = peer;
     return launch_attention(aa, (int)(B * S.hq_l), (int)S.hd, S.G, st);
+}
+
+extern "C" larosa_status larosa_shard_wait(const uint32_t* flag, uint32_t* expected, uint32_t count,
+                                           larosa_stream_t stream) {
+    if (!flag || !expected) return fail(LAROSA_EINVAL, "shard_wait: NULL pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return cuda_check(launch(peer_wait_kernel, dim3(1), dim3(32), 0, st, flag, expected, count), "shard_wait launch");
+}
+
+extern "C" larosa_status larosa_peer_push(const float* src, int32_t batch, int64_t d_local, int64_t src_ld,
+                                          const uint64_t* peer_dst, const uint64_t* peer_flag, int32_t world,
+                                          int64_t peer_ld, larosa_stream_t stream) {
+    if (!src || !peer_dst || !peer_flag) return fail(LAROSA_EINVAL, "peer_push: NULL pointer");
+    if (batch < 1 || d_local <= 0 || src_ld < d_local || world < 1 || peer_ld < d_local)
+        return fail(LAROSA_EINVAL, "peer_push: bad sizes");
+    if ((int64_t)batch * d_local > INT32_MAX) return fail(LAROSA_EUNSUPPORTED, "peer_push: too large");
+    PeerOut peer;
+    peer.dst = reinterpret_cast<const unsigned long long*>(peer_dst);
+    peer.flag = reinterpret_cast<const unsigned long long*>(peer_flag);
+    peer.n = world;
+    peer.ld = (int)peer_ld;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n = (int64_t)batch * d_local;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    return cuda_check(launch(peer_push_kernel, dim3(grid), dim3(256), 0, st, src, batch, (int)d_local, src_ld, peer),
+                      "peer_push launch");
 }
 
 // gathered [world][batch][d_local] (rank-major all-gather) -> out [batch][world * d_local]

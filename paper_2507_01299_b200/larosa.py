@@ -57,7 +57,8 @@ class LayerTapsC(ctypes.Structure):
 
 
 class ShardC(ctypes.Structure):
-    _fields_ = [("rank", _c_i32), ("world", _c_i32), ("batch", _c_i32)]
+    _fields_ = [("rank", _c_i32), ("world", _c_i32), ("batch", _c_i32), ("peer_dst", _vp), ("peer_flag", _vp),
+                ("peer_ld", _c_i64)]
 
 
 _LIB = None
@@ -124,6 +125,8 @@ def lib() -> ctypes.CDLL:
                                                   ctypes.POINTER(ShardC), _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
                                                   _c_i64, _vp, ctypes.c_size_t, _vp]
     L.larosa_shard_gather_permute.argtypes = [_vp, _c_i32, _c_i32, _c_i64, _vp, _vp]
+    L.larosa_shard_wait.argtypes = [_vp, _vp, ctypes.c_uint32, _vp]
+    L.larosa_peer_push.argtypes = [_vp, _c_i32, _c_i64, _c_i64, _vp, _vp, _c_i32, _c_i64, _vp]
     L.larosa_error_flags.argtypes = [_vp, _c_i32, ctypes.POINTER(ctypes.c_uint32), _vp]
     L.larosa_error_flags.restype = ctypes.c_int
     L.larosa_argmax.argtypes = [_vp, _c_i32, _c_i64, _c_i64, _vp, _vp]
@@ -140,9 +143,9 @@ def lib() -> ctypes.CDLL:
                  "larosa_residual_adapter",
                  "larosa_rotate_topk", "larosa_sparse_gemv", "larosa_topk_sparse_gemv", "larosa_sparse_layer",
                  "larosa_embed", "larosa_lm_head", "larosa_sparse_layer_shard_phase", "larosa_shard_gather_permute",
-                 "larosa_argmax"):
+                 "larosa_argmax", "larosa_shard_wait", "larosa_peer_push"):
         getattr(L, name).restype = ctypes.c_int
-    if L.larosa_abi_version() != 6:
+    if L.larosa_abi_version() != 7:
         raise RuntimeError("liblarosa ABI version mismatch")
     _LIB = L
     return L
@@ -440,6 +443,30 @@ def shard_gather_permute(gathered: torch.Tensor, world: int, batch: int, out: to
     return out
 
 
+@dataclass
+class PeerTarget:
+    """Where a sharded phase pushes its output (larosa_shard.peer_*): device int64 arrays of every
+    rank's destination address (at this rank's first column) and arrival-counter address, and the
+    token stride of the destination buffers (floats)."""
+    dst: torch.Tensor    # int64 [world] on device
+    flag: torch.Tensor   # int64 [world] on device
+    ld: int
+
+
+def shard_wait(flag: torch.Tensor, expected: torch.Tensor, count: int, stream=None):
+    """Wait (on the device) until this rank's arrival counter has grown by `count` more values
+    (larosa_shard_wait); flag / expected: one-element int32 device tensors."""
+    _check(lib().larosa_shard_wait(_ptr(flag), _ptr(expected), ctypes.c_uint32(int(count) & 0xffffffff),
+                                   _stream(stream)))
+
+
+def peer_push(src: torch.Tensor, target: PeerTarget, world: int, stream=None):
+    """Push a [batch][d_local] fp32 slice into every rank's buffer + counters (larosa_peer_push)."""
+    B, dl = src.shape
+    _check(lib().larosa_peer_push(_ptr(src), B, dl, src.stride(0), _ptr(target.dst), _ptr(target.flag), world,
+                                  int(target.ld), _stream(stream)))
+
+
 def argmax(logits: torch.Tensor, out: torch.Tensor, stream=None):
     """out[b] = arg-max of logits[b] (lowest index on ties)."""
     B, n = logits.shape
@@ -587,13 +614,18 @@ def shard_workspace_size(w: LayerWeights, rank: int, world: int, max_ctx: int, b
 def shard_phase(w: LayerWeights, plan: Sequence[int], rank: int, world: int, phase: int, x: torch.Tensor,
                 out: torch.Tensor, ws: torch.Tensor, resid: Optional[torch.Tensor] = None,
                 k_cache: Optional[torch.Tensor] = None, v_cache: Optional[torch.Tensor] = None,
-                pos: Optional[torch.Tensor] = None, max_ctx: int = 0, stream=None):
+                pos: Optional[torch.Tensor] = None, max_ctx: int = 0, stream=None,
+                peer: Optional[PeerTarget] = None):
     """One phase of the row-sharded layer (larosa_sparse_layer_shard_phase); ``w`` holds this
     rank's shard with the FULL model dims.  x / resid [batch][full] (or [full] at batch 1),
-    out [batch][local]."""
+    out [batch][local]; peer: also push the output to every rank (then shard_wait)."""
     wc = w.c()
     pc = LayerPlanC(*[int(k) for k in plan[:5]], *([0] if len(plan) < 5 else []))
     sh = ShardC(rank, world, x.shape[0] if x.dim() == 2 else 1)
+    if peer is not None:
+        sh.peer_dst = _ptr(peer.dst)
+        sh.peer_flag = _ptr(peer.flag)
+        sh.peer_ld = int(peer.ld)
     _check(lib().larosa_sparse_layer_shard_phase(ctypes.byref(wc), ctypes.byref(pc), ctypes.byref(sh), int(phase),
                                                  _ptr(x), _ptr(resid), _ptr(out), _ptr(k_cache), _ptr(v_cache),
                                                  _ptr(pos), int(max_ctx), _ptr(ws), ws.numel(), _stream(stream)))

@@ -11,6 +11,7 @@ import dataclasses
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import numpy as np
 import torch
 
 import synth
@@ -239,14 +240,76 @@ def shard_kv(cache: torch.Tensor, rank: int, world: int) -> torch.Tensor:
     return cache[:, rank * h:(rank + 1) * h].contiguous()
 
 
+class PeerSpace:
+    """The buffer arena of the P2P push: every rank carves the same layout from
+    its arena, so a buffer's offset names it on every rank; bases[p] = rank p's arena address.  On a
+    multi-GPU run the arena is torch symmetric memory (``PeerSpace.symmetric``: peer addresses mapped
+    over NVLink); the single-GPU lockstep emulation uses one ordinary arena per emulated rank
+    (``PeerSpace.emulated``)."""
+
+    ALIGN = 256
+
+    def __init__(self, arena: torch.Tensor, bases: Sequence[int], rank: int):
+        self.arena, self.bases, self.rank, self.off = arena, [int(b) for b in bases], rank, 0
+        self.world = len(self.bases)
+
+    def take(self, shape, dtype=torch.float32) -> torch.Tensor:
+        """A zeroed view of the next free bytes (the same offset on every rank for the same calls)."""
+        n = int(np.prod(shape)) * torch.tensor([], dtype=dtype).element_size()
+        if self.off + n > self.arena.numel():
+            raise ValueError("PeerSpace: arena too small")
+        t = self.arena[self.off:self.off + n].view(dtype).view(*shape)
+        t.zero_()
+        self.off += (n + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        return t
+
+    def addr(self, t: torch.Tensor, rank: int) -> int:
+        return self.bases[rank] + (t.data_ptr() - self.arena.data_ptr())
+
+    def target(self, buf: torch.Tensor, col0: int, flag: torch.Tensor) -> LZ.PeerTarget:
+        """Push into every rank's copy of buf [batch][full] at column col0, counted on flag."""
+        dev = self.arena.device
+        dst = torch.tensor([self.addr(buf, p) + 4 * col0 for p in range(self.world)], dtype=torch.int64, device=dev)
+        fl = torch.tensor([self.addr(flag, p) for p in range(self.world)], dtype=torch.int64, device=dev)
+        return LZ.PeerTarget(dst, fl, buf.shape[-1])
+
+    @staticmethod
+    def symmetric(nbytes: int, device, group=None) -> "PeerSpace":
+        """A torch symmetric-memory arena, rendezvous over `group` (collective: every rank calls it)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        arena = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        hdl = symm_mem.rendezvous(arena, group if group is not None else dist.group.WORLD)
+        return PeerSpace(arena, list(hdl.buffer_ptrs), hdl.rank)
+
+    @staticmethod
+    def emulated(nbytes: int, device, world: int) -> List["PeerSpace"]:
+        arenas = [torch.zeros(nbytes, dtype=torch.uint8, device=device) for _ in range(world)]
+        bases = [a.data_ptr() for a in arenas]
+        return [PeerSpace(a, bases, r) for r, a in enumerate(arenas)]
+
+
+def shard_layer_peer_bytes(shape_d: int, nq: int, inter_p: int, batch: int) -> int:
+    """Arena bytes one ShardedLayer takes in P2P mode (4 gathered buffers + counters)."""
+    a = PeerSpace.ALIGN
+    rnd = lambda n: (n + a - 1) // a * a
+    return sum(rnd(batch * w * 4) for w in (nq, shape_d, inter_p, shape_d)) + rnd(8 * 4)
+
+
 class ShardedLayer:
     """One rank's view of a row-sharded LaRoSA layer (batch 1..16): four or five library phases,
-    each followed by an all-gather of the phase output.  ``allgather(local, gathered)`` is
-    torch.distributed.all_gather_into_tensor over NCCL on a real multi-GPU run (CUDA-graph
-    capturable): rank-major [world][batch][local]; at batch 1 that is already the column order,
-    at batch > 1 larosa_shard_gather_permute reorders it to [batch][full]."""
+    each followed by an exchange of the phase output.  NCCL: ``allgather(local, gathered)`` is
+    torch.distributed.all_gather_into_tensor (CUDA-graph capturable): rank-major
+    [world][batch][local]; at batch 1 that is already the column order, at batch > 1
+    larosa_shard_gather_permute reorders it to [batch][full].  P2P (``space`` given, SURVEY §8(e)
+    v2): the kernel producing a phase output stores it straight into every rank's gathered buffer
+    (this layer's buffers live in the PeerSpace arena; the last phase writes the residual ``resid``,
+    also in the arena) and bumps every rank's counter; larosa_shard_wait then orders the next phase
+    after all ranks' pushes.  Each layer has its own buffers and counters, so a rank that runs ahead
+    never overwrites a buffer a slower rank still reads (every phase needs every rank's output)."""
 
-    def __init__(self, w_shard: LZ.LayerWeights, rank: int, world: int, max_ctx: int, device, batch: int = 1):
+    def __init__(self, w_shard: LZ.LayerWeights, rank: int, world: int, max_ctx: int, device, batch: int = 1,
+                 space: Optional[PeerSpace] = None, resid: Optional[torch.Tensor] = None):
         self.w, self.rank, self.world, self.max_ctx, self.batch = w_shard, rank, world, max_ctx, batch
         d, nq, inter = w_shard.d, w_shard.n_q_heads * w_shard.head_dim, w_shard.inter
         n, B = world, batch
@@ -256,15 +319,34 @@ class ShardedLayer:
         self.local = {0: torch.zeros((B, nq // n), **f32), 1: torch.zeros((B, d // n), **f32),
                       2: torch.zeros((B, inter // n), **f32), 3: torch.zeros((B, d // n), **f32),
                       4: torch.zeros((B, d // n), **f32)}
-        self.full = {0: torch.zeros((B, nq), **f32), 1: torch.zeros((B, d), **f32), 2: torch.zeros((B, inter), **f32),
-                     3: torch.zeros((B, d), **f32)}
-        self.stage = torch.zeros((n * B * max(nq, d, inter) // n,), **f32) if B > 1 else None
+        self.space = space
+        if space is None:
+            self.full = {0: torch.zeros((B, nq), **f32), 1: torch.zeros((B, d), **f32),
+                         2: torch.zeros((B, inter), **f32), 3: torch.zeros((B, d), **f32)}
+            self.stage = torch.zeros((n * B * max(nq, d, inter) // n,), **f32) if B > 1 else None
+        else:
+            if resid is None or resid.shape != (B, d):
+                raise ValueError("ShardedLayer: P2P mode needs the arena residual [batch][d]")
+            self.full = {0: space.take((B, nq)), 1: space.take((B, d)), 2: space.take((B, inter)),
+                         3: space.take((B, d))}
+            self.flags = space.take((8,), torch.int32)           # arrival counters (peers add into them)
+            self.expected = torch.zeros((8,), dtype=torch.int32, device=device)
+            last = self.n_phases() - 1
+            widths = {0: nq, 1: d, 2: inter, 3: d, 4: d}
+            self.targets = {ph: space.target(resid if ph == last else self.full[ph], rank * widths[ph] // n,
+                                             self.flags[ph:ph + 1]) for ph in range(last + 1)}
+            self.counts = {ph: B * widths[ph] for ph in range(last + 1)}
 
     def run_phase(self, phase: int, x: torch.Tensor, resid: Optional[torch.Tensor], k_cache, v_cache, pos,
                   plan, stream=None) -> torch.Tensor:
         LZ.shard_phase(self.w, plan, self.rank, self.world, phase, x, self.local[phase], self.ws, resid=resid,
-                       k_cache=k_cache, v_cache=v_cache, pos=pos, max_ctx=self.max_ctx, stream=stream)
+                       k_cache=k_cache, v_cache=v_cache, pos=pos, max_ctx=self.max_ctx, stream=stream,
+                       peer=self.targets[phase] if self.space is not None else None)
         return self.local[phase]
+
+    def wait_phase(self, phase: int, stream=None):
+        """P2P: until every rank's push of this phase output has landed in this rank's buffer."""
+        LZ.shard_wait(self.flags[phase:phase + 1], self.expected[phase:phase + 1], self.counts[phase], stream)
 
     def n_phases(self) -> int:
         """5 with the literal adapter phase; 4 without an adapter or with it folded beside down."""
@@ -292,12 +374,16 @@ class ShardedLayer:
         LZ.shard_gather_permute(st, self.world, self.batch, full, stream=stream)
 
     def forward(self, r: torch.Tensor, k_cache, v_cache, pos, plan, allgather, stream=None) -> torch.Tensor:
-        """r: the full residual [batch][d] (replicated); returns it updated in place (next layer's input)."""
+        """r: the full residual [batch][d] (replicated); returns it updated in place (next layer's input).
+        P2P mode: r must be the arena residual the layer was built with; allgather is unused."""
         last = self.n_phases() - 1
         for ph in range(last + 1):
             x, res = self.inputs(ph, r)
             out = self.run_phase(ph, x, res, k_cache, v_cache, pos, plan, stream)
-            self.gather(out, r if ph == last else self.full[ph], allgather, stream)
+            if self.space is not None:
+                self.wait_phase(ph, stream)
+            else:
+                self.gather(out, r if ph == last else self.full[ph], allgather, stream)
         return r
 
 
@@ -342,21 +428,40 @@ class ShardedDecodeRunner:
     this rank's LM-head slice -> all-gather of the logits -> greedy.  ``allgather`` as in
     ShardedLayer; CUDA-graph capturable."""
 
-    def __init__(self, model: ShardedDecodeModel, batch: int, max_ctx: int, device):
-        self.m, self.batch = model, batch
+    @staticmethod
+    def peer_bytes(model: "ShardedDecodeModel", batch: int) -> int:
+        """Arena bytes of the P2P mode (every layer's buffers, the residual, the logits, counters)."""
+        s, w0 = model.shape, model.layers[0]
+        a = PeerSpace.ALIGN
+        rnd = lambda n: (n + a - 1) // a * a
+        per = shard_layer_peer_bytes(s.d, s.hq * s.hd, w0.inter, batch)
+        return len(model.layers) * per + rnd(batch * s.d * 4) + rnd(batch * model.vocab * 4) + rnd(8 * 4)
+
+    def __init__(self, model: ShardedDecodeModel, batch: int, max_ctx: int, device,
+                 space: Optional[PeerSpace] = None):
+        self.m, self.batch, self.space = model, batch, space
         s, n, r = model.shape, model.world, model.rank
-        self.shards = [ShardedLayer(w, r, n, max_ctx, device, batch) for w in model.layers]
+        f32 = dict(dtype=torch.float32, device=device)
+        if space is not None:   # P2P: the residual, every layer's gathered buffers and the logits in the arena
+            self.resid = space.take((batch, s.d))
+            self.shards = [ShardedLayer(w, r, n, max_ctx, device, batch, space=space, resid=self.resid)
+                           for w in model.layers]
+            self.logits = space.take((batch, model.vocab))
+            self.head_flag = space.take((8,), torch.int32)
+            self.head_expected = torch.zeros((8,), dtype=torch.int32, device=device)
+            self.head_target = space.target(self.logits, r * (model.vocab // n), self.head_flag[0:1])
+        else:
+            self.resid = torch.zeros((batch, s.d), **f32)
+            self.shards = [ShardedLayer(w, r, n, max_ctx, device, batch) for w in model.layers]
+            self.logits = torch.zeros((batch, model.vocab), **f32)
         hk = s.hkv // n
         self.kv = [(torch.zeros((batch, hk, max_ctx, s.hd), dtype=torch.int16, device=device),
                     torch.zeros((batch, hk, max_ctx, s.hd), dtype=torch.int16, device=device)) for _ in model.layers]
-        f32 = dict(dtype=torch.float32, device=device)
-        self.resid = torch.zeros((batch, s.d), **f32)
         self.tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
         self.next_tokens = torch.zeros((batch,), dtype=torch.int32, device=device)
         self.pos = torch.zeros((batch,), dtype=torch.int32, device=device)
         vl = model.vocab // n
         self.logits_local = torch.zeros((batch, vl), **f32)
-        self.logits = torch.zeros((batch, model.vocab), **f32)
         self.stage = torch.zeros((n * batch * vl,), **f32)
         self.local_tok = torch.zeros((batch,), dtype=torch.int32, device=device)
         self.head_ws = torch.zeros(LZ.lib().larosa_lm_head_workspace_size(batch, s.d, vl), dtype=torch.uint8,
@@ -368,10 +473,19 @@ class ShardedDecodeRunner:
             sh.forward(self.resid, kc, vc, self.pos, plan, allgather, stream)
         LZ.lm_head(self.resid, self.m.head, self.m.shape.rms_eps, logits=self.logits_local,
                    next_token=self.local_tok, ws=self.head_ws, stream=stream)
-        if self.batch == 1:
+        if self.space is not None:
+            self.push_logits(stream)
+            self.wait_logits(stream)
+        elif self.batch == 1:
             allgather(self.logits_local.view(-1), self.logits.view(-1))
         else:
             allgather(self.logits_local.view(-1), self.stage)
             LZ.shard_gather_permute(self.stage, self.m.world, self.batch, self.logits, stream=stream)
         LZ.argmax(self.logits, self.next_tokens, stream=stream)
         return self.next_tokens
+
+    def push_logits(self, stream=None):
+        LZ.peer_push(self.logits_local, self.head_target, self.m.world, stream)
+
+    def wait_logits(self, stream=None):
+        LZ.shard_wait(self.head_flag[0:1], self.head_expected[0:1], self.batch * self.m.vocab, stream)

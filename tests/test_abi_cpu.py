@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 14, names
     for n in names:
         assert hasattr(L, n), f"missing export {n}"
-    assert L.larosa_abi_version() == 6
+    assert L.larosa_abi_version() == 7
 
 
 def test_status_strings():
@@ -209,6 +209,17 @@ def test_new_entry_points_validation():
         assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w2), ctypes.byref(p), ctypes.byref(shb), 1, FAKE, FAKE,
                                                  FAKE, None, None, None, 0, ws, 1 << 40, None) == st
         assert L.larosa_shard_workspace_size(ctypes.byref(w2), ctypes.byref(shb), 256) == 0
+    # P2P push (ABI 7): peer_dst without peer_flag, NULL pointers, bad sizes
+    shp = LZ.ShardC(0, 1, 1)
+    shp.peer_dst = FAKE
+    w2.adapter_mid = None
+    assert L.larosa_sparse_layer_shard_phase(ctypes.byref(w2), ctypes.byref(p), ctypes.byref(shp), 1, FAKE, FAKE,
+                                             FAKE, None, None, None, 0, ws, 1 << 40, None) == 1
+    assert L.larosa_shard_wait(None, FAKE, 1, None) == 1
+    assert L.larosa_shard_wait(FAKE, None, 1, None) == 1
+    assert L.larosa_peer_push(None, 1, 64, 64, FAKE, FAKE, 1, 64, None) == 1
+    assert L.larosa_peer_push(FAKE, 1, 64, 32, FAKE, FAKE, 1, 64, None) == 1     # src_ld < d_local
+    assert L.larosa_peer_push(FAKE, 1, 64, 64, FAKE, FAKE, 0, 64, None) == 1     # world 0
     # gather permute / argmax argument checks
     assert L.larosa_shard_gather_permute(None, 2, 1, 64, FAKE, None) == 1
     assert L.larosa_shard_gather_permute(FAKE, 0, 1, 64, ctypes.c_void_p(1 << 22), None) == 1

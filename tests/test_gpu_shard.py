@@ -237,3 +237,184 @@ def test_gather_permute_and_argmax():
     nt = torch.empty((2,), dtype=torch.int32, device=DEV)
     LZ.argmax(lg, nt)
     assert nt.cpu().tolist() == [17, 0]
+
+
+# ---- P2P push instead of the all-gather ---------------------------------------
+def lockstep_p2p_phase(shards, ph, runs_resid, kvs, pos, plan):
+    """Every emulated rank runs phase ph (its kernels store the output into every rank's arena
+    buffer and bump every rank's counter), THEN every rank waits on its own counter: no kernel
+    waits on a kernel that has not been launched before it."""
+    outs = []
+    for sh, r, (kc, vc) in zip(shards, runs_resid, kvs):
+        x, res = sh.inputs(ph, r)
+        outs.append(sh.run_phase(ph, x, res, kc, vc, pos, plan).clone())
+    for sh in shards:
+        sh.wait_phase(ph)
+    return outs
+
+
+@pytest.mark.parametrize("shape,world,batch,merged", [
+    (SMALL_MHA, 1, 1, True), (SMALL_MHA, 2, 1, True), (SMALL_MHA, 4, 1, False), (SMALL_MHA, 2, 3, True),
+    (SMALL_MHA, 4, 16, True), (SMALL_MHA, 2, 8, False), (synth.MODELS["llama3-70b"], 8, 1, True),
+    (synth.MODELS["qwen2.5-72b"], 8, 16, True)])
+def test_shard_layer_p2p_equals_allgather(shape, world, batch, merged):
+    """The P2P push path gives bit-identical gathered vectors, phase outputs and final residual to
+    the all-gather path, on every rank, for two consecutive layer invocations (the counters keep
+    counting)."""
+    lw = M.fold_layer(M.synth_original_layer(shape, 23, device=DEV), shape,
+                      synth.haar_orthogonal(shape.d, 33, device=DEV, dtype=torch.float32),
+                      synth.haar_orthogonal(shape.d, 34, device=DEV, dtype=torch.float32), adapter_in_down=merged)
+    plan = M.site_plan(shape, 0.5)
+    max_ctx = 64
+    kc = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), 45, 1.0, DEV)
+    vc = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), 46, 1.0, DEV)
+    r0 = synth.residual_activation(batch, shape.d, 47).to(DEV)
+    posd = torch.randint(20, max_ctx, (batch,), generator=synth.gen(48), dtype=torch.int32).to(DEV)
+    shards_w = [M.shard_layer(lw, r, world) for r in range(world)]
+    del lw
+    nq, inter_p = shape.hq * shape.hd, shards_w[0].inter
+    nbytes = M.shard_layer_peer_bytes(shape.d, nq, inter_p, batch) + (batch * shape.d * 4 + 1024)
+    spaces = M.PeerSpace.emulated(nbytes, DEV, world)
+    rs_p = [sp.take((batch, shape.d)) for sp in spaces]
+    p2p = [M.ShardedLayer(shards_w[r], r, world, max_ctx, DEV, batch, space=spaces[r], resid=rs_p[r])
+           for r in range(world)]
+    ag = [M.ShardedLayer(shards_w[r], r, world, max_ctx, DEV, batch) for r in range(world)]
+    kv_a = [(M.shard_kv(kc, r, world), M.shard_kv(vc, r, world)) for r in range(world)]
+    kv_p = [(a.clone(), b.clone()) for a, b in kv_a]
+    rs_a = [r0.clone() for _ in range(world)]
+    for r in rs_p:
+        r.copy_(r0)
+    last = ag[0].n_phases() - 1
+    for rep in range(2):
+        for ph in range(last + 1):
+            outs_a = []
+            for sh, r, (kcr, vcr) in zip(ag, rs_a, kv_a):
+                x, res = sh.inputs(ph, r)
+                outs_a.append(sh.run_phase(ph, x, res, kcr, vcr, posd, plan).clone())
+            lockstep_gather(ag, outs_a, [r if ph == last else sh.full[ph] for sh, r in zip(ag, rs_a)])
+            outs_p = lockstep_p2p_phase(p2p, ph, rs_p, kv_p, posd, plan)
+            torch.cuda.synchronize()
+            for r in range(world):
+                assert torch.equal(outs_p[r], outs_a[r]), (rep, ph, r)
+                got = rs_p[r] if ph == last else p2p[r].full[ph]
+                want = rs_a[r] if ph == last else ag[r].full[ph]
+                assert torch.equal(got, want), (rep, ph, r)
+    for r in range(world):
+        assert torch.equal(kv_p[r][0], kv_a[r][0]) and torch.equal(kv_p[r][1], kv_a[r][1])
+        assert int(p2p[r].expected[0]) == 2 * batch * nq
+
+
+@pytest.mark.parametrize("world,batch", [(2, 1), (4, 16)])
+def test_sharded_decode_step_p2p_emulated(world, batch):
+    """The sharded decode step with the P2P push (layers and the gathered logits) equals the
+    all-gather step bit for bit on every rank, over three consecutive steps (greedy tokens fed
+    back)."""
+    shape = synth.ModelShape("small-dec", 256, 512, 4, 4, 64, 3, 1024, True, 1e-6, 10000.0)
+    n_layers, max_ctx = 3, 32
+    models = [M.ShardedDecodeModel(shape, n_layers, r, world, DEV, seed=4) for r in range(world)]
+    nbytes = M.ShardedDecodeRunner.peer_bytes(models[0], batch)
+    spaces = M.PeerSpace.emulated(nbytes, DEV, world)
+    runs_a = [M.ShardedDecodeRunner(m, batch, max_ctx, DEV) for m in models]
+    runs_p = [M.ShardedDecodeRunner(m, batch, max_ctx, DEV, space=sp) for m, sp in zip(models, spaces)]
+    for l in range(n_layers):
+        a = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), 300 + l, 1.0, DEV)
+        b = synth.gaussian_bf16((batch, shape.hkv, max_ctx, shape.hd), 400 + l, 1.0, DEV)
+        for run in runs_a + runs_p:
+            run.kv[l][0].copy_(M.shard_kv(a, run.m.rank, world))
+            run.kv[l][1].copy_(M.shard_kv(b, run.m.rank, world))
+    g = synth.gen(9)
+    tokens = torch.randint(0, shape.vocab, (batch,), generator=g, dtype=torch.int32)
+    pos = torch.randint(5, max_ctx - 4, (batch,), generator=g, dtype=torch.int32)
+    for run in runs_a + runs_p:
+        run.tokens.copy_(tokens)
+        run.pos.copy_(pos)
+    plan = M.site_plan(shape, 0.5)
+    for step in range(3):
+        for runs, p2p in ((runs_a, False), (runs_p, True)):
+            for run in runs:
+                LZ.embed(run.m.embed, run.tokens, out=run.resid)
+            for l in range(n_layers):
+                shards = [run.shards[l] for run in runs]
+                last = shards[0].n_phases() - 1
+                for ph in range(last + 1):
+                    if p2p:
+                        lockstep_p2p_phase(shards, ph, [run.resid for run in runs], [run.kv[l] for run in runs],
+                                           runs[0].pos, plan)
+                        continue
+                    outs = []
+                    for sh, run in zip(shards, runs):
+                        x, res = sh.inputs(ph, run.resid)
+                        outs.append(sh.run_phase(ph, x, res, *run.kv[l], run.pos, plan).clone())
+                    lockstep_gather(shards, outs, [run.resid if ph == last else sh.full[ph]
+                                                   for sh, run in zip(shards, runs)])
+            for run in runs:
+                LZ.lm_head(run.resid, run.m.head, shape.rms_eps, logits=run.logits_local, next_token=run.local_tok,
+                           ws=run.head_ws)
+            if p2p:
+                for run in runs:
+                    run.push_logits()
+                for run in runs:
+                    run.wait_logits()
+            else:
+                stacked = torch.stack([run.logits_local.clone() for run in runs]).reshape(-1)
+                for run in runs:
+                    if batch == 1:
+                        run.logits.view(-1).copy_(stacked)
+                    else:
+                        run.stage.copy_(stacked)
+                        LZ.shard_gather_permute(run.stage, world, batch, run.logits)
+            for run in runs:
+                LZ.argmax(run.logits, run.next_tokens)
+                run.tokens.copy_(run.next_tokens)
+                run.pos.add_(1)
+        torch.cuda.synchronize()
+        for ra, rp in zip(runs_a, runs_p):
+            assert torch.equal(rp.logits, ra.logits), step
+            assert torch.equal(rp.next_tokens, ra.next_tokens), step
+            assert torch.equal(rp.resid, ra.resid), step
+
+
+def test_p2p_symmetric_memory_world1():
+    """The real P2P setup at world 1: torch symmetric memory + rendezvous (NCCL group over
+    127.0.0.1) and ShardedDecodeRunner.step (push + wait on the device) equal the all-gather step,
+    also when the step is captured in a CUDA graph and replayed."""
+    import os
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    shape = synth.ModelShape("small-dec", 256, 512, 4, 4, 64, 2, 1024, True, 1e-6, 10000.0)
+    model = M.ShardedDecodeModel(shape, 2, 0, 1, DEV, seed=6)
+    try:
+        space = M.PeerSpace.symmetric(M.ShardedDecodeRunner.peer_bytes(model, 1), DEV)
+    except Exception as e:   # pragma: no cover - reported, not hidden
+        pytest.fail(f"torch symmetric memory unavailable: {e!r}")
+    run_p = M.ShardedDecodeRunner(model, 1, 32, DEV, space=space)
+    run_a = M.ShardedDecodeRunner(model, 1, 32, DEV)
+    for run in (run_a, run_p):
+        run.tokens.fill_(77)
+        run.pos.fill_(9)
+    plan = M.site_plan(shape, 0.5)
+    ag = lambda local, dst: dst.copy_(local)
+    run_a.step(plan, ag)
+    run_p.step(plan, None)
+    torch.cuda.synchronize()
+    assert torch.equal(run_p.logits, run_a.logits) and torch.equal(run_p.next_tokens, run_a.next_tokens)
+    # graph capture + two replays (the counters advance on the device)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        run_p.step(plan, None)
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        run_p.step(plan, None)
+    for _ in range(2):
+        g.replay()
+        run_a.step(plan, ag)
+    torch.cuda.synchronize()
+    assert torch.equal(run_p.logits, run_a.logits)
+    assert int(run_p.shards[0].expected[0]) == 4 * shape.hq * shape.hd   # 4 executions (capture runs nothing)
+    del g
+    dist.destroy_process_group()

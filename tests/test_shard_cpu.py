@@ -246,3 +246,31 @@ def test_sharded_layer_gloo_batch2_gather_order():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def test_peer_space_layout():
+    """P2P arena (model.PeerSpace): the same take() sequence gives the same offsets on every rank,
+    so rank p's copy of a buffer is bases[p] + offset; targets point at this rank's column block;
+    takes are 256-byte aligned and zeroed; an over-full arena raises."""
+    import torch
+    from paper_2507_01299_b200 import model as M
+    world = 3
+    spaces = M.PeerSpace.emulated(8192, "cpu", world)
+    bufs = []
+    for sp in spaces:
+        sp.arena.fill_(7)
+        a = sp.take((2, 10))
+        f = sp.take((8,), torch.int32)
+        b = sp.take((3, 5))
+        bufs.append((a, f, b))
+        assert (a == 0).all() and (f == 0).all()
+    offs = [[t.data_ptr() - sp.arena.data_ptr() for t in bs] for sp, bs in zip(spaces, bufs)]
+    assert all(o == offs[0] for o in offs) and offs[0] == [0, 256, 512]
+    for r, sp in enumerate(spaces):
+        a, f, b = bufs[r]
+        tg = sp.target(a, col0=r * 3, flag=f[2:3])
+        assert tg.ld == 10
+        assert tg.dst.tolist() == [spaces[p].arena.data_ptr() + 4 * r * 3 for p in range(world)]
+        assert tg.flag.tolist() == [spaces[p].arena.data_ptr() + 256 + 8 for p in range(world)]
+    with pytest.raises(ValueError):
+        spaces[0].take((4096,))
