@@ -1,4 +1,4 @@
-"""One LLaMA2-7B layer, a few decode steps (for an ncu launch list)."""
+"""One layer (LLaMA2-7B, or argv[2]), a few decode steps at p = argv[1] (for an ncu capture)."""
 import os
 import sys
 
@@ -9,7 +9,7 @@ import synth  # noqa: E402
 from paper_2507_01299_b200 import larosa as LZ  # noqa: E402
 from paper_2507_01299_b200 import model as M  # noqa: E402
 
-shape = synth.MODELS["llama2-7b"]
+shape = synth.MODELS[sys.argv[2] if len(sys.argv) > 2 else "llama2-7b"]
 p = float(sys.argv[1]) if len(sys.argv) > 1 else 0.5
 dev = "cuda:0"
 q0 = synth.haar_orthogonal(shape.d, 1, device=dev, dtype=torch.float32)
