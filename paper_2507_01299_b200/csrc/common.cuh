@@ -91,6 +91,14 @@ __device__ __forceinline__ void tl_stamp(unsigned long long* tl, int i) {
     }
 }
 
+// the same, from whichever single thread calls it
+__device__ __forceinline__ void tl_stamp_any(unsigned long long* tl, int i) {
+    if (tl) {
+        const int c = blockIdx.y * gridDim.x + blockIdx.x;
+        if (c < 1024) tl[c * 16 + i] = gtime();
+    }
+}
+
 // ---- thread-block clusters / distributed shared memory -----------------------------------
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
     int lo, n_rows;
     tc_split_range(a.d_in, a.n_splits, split, lo, n_rows);
     const int n_chunks = (n_rows + kTcChunk - 1) / kTcChunk;
+    tl_stamp(a.tl, 0);
 
     if (tid == 0) {
         for (int s = 0; s < kImgStages; ++s) {
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
                 tma_load_2d(st + kTcABytes / 2, &tmw, col0 + 64, lo + c * kTcChunk, &full[c]);
             }
             pdl_wait();       // the token image comes from the previous kernel
+            tl_stamp_any(a.tl, 1);
             for (int c = 0; c < pre; ++c)
                 bulk_g2s(smem + c * kImgStageBytes + kTcABytes, img + (size_t)c * kImgChunkBytes, kImgChunkBytes, &full[c]);
             for (int c = pre; c < n_chunks; ++c) {
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
         const int q = warp & 3;
         mbar_wait_parity(accb, 0);
         tc_fence_after();
+        if (tid == 64) tl_stamp_any(a.tl, 3);   // the accumulator is complete
         uint32_t v[16], w[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -153,12 +156,20 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
     tc_fence_before();
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
-    if (a.epi == EPI_NONE) return;
+    if (a.epi == EPI_NONE) {
+        tl_stamp(a.tl, 4);
+        return;
+    }
 
     // ---- the last split CTA of this slice finalises its 128 columns (as gemv_tc.cuh) -------------
     if (tid == 0) *flag = atom_add_acq_rel_gpu(a.tickets + slice, 1u) == gridDim.y - 1u;
+    tl_stamp(a.tl, 12);
     __syncthreads();
-    if (!*flag) return;
+    if (!*flag) {
+        tl_stamp(a.tl, 4);
+        return;
+    }
+    tl_stamp(a.tl, 13);
     if (tid == 0) a.tickets[slice] = 0u;
     const int e = tid - 64;                       // epilogue threads 0..127 (tid 0..63 idle)
     if (e < 0) {
@@ -201,6 +212,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) gemv_img_kernel(const GemvArgs
                 a.out[(size_t)b * a.out_ld + o] = y;
             }
     }
+    tl_stamp(a.tl, 4);
     if (a.peer.n) {   // the block's outputs to every rank (thread e wrote output column e)
         if (a.epi == EPI_SILU)
             peer_push_cols(a.peer, a.out, a.out_ld, a.batch, slice * kGuBlock, min(kGuBlock, max(0, a.d_out - col0)));
