@@ -597,6 +597,7 @@ def main():
         del model
         torch.cuda.empty_cache()
         extras["w4a16_decode"] = w4_decode_extra(shape, device, peaks)
+        extras["sparse_gemv_list_sweep"] = BX.list_gemv_sweep_extra(device, peaks)
         extras["block_llama2_7b_c2"] = BX.block_c2_extra(device)
         extras["model_sweep_configs3"] = BX.model_sweep_extra(device, merged=merged)
         extras["fold_tcgen05"] = BX.fold_extra(device)

@@ -98,6 +98,61 @@ def time_gemv_sites(layers, plan, shape, device, reps=48):
     return res
 
 
+def list_gemv_sweep_extra(device, peaks, shape_name="llama3-8b", ps=(0.25, 0.4, 0.5, 0.6), n_copies=8, reps=64):
+    """north_star's "sparse-GEMV HBM GB/s (% of peak) vs sparsity": larosa_sparse_gemv (the LIST
+    entry: the kept-index list and values given, as larosa_rotate_topk emits them; batch 1) on each
+    projection of the layer, back-to-back launches in a CUDA graph cycling n_copies layer copies
+    (weights >> L2); GB/s on the selected-column bytes k d_out 2 (+ the index/value list and y)."""
+    from paper_2507_01299_b200 import larosa as LZ
+    from paper_2507_01299_b200 import model as M
+    shape = synth.MODELS[shape_name]
+    layers = build_stack(shape, device, n_copies, seed=40)
+    nq = shape.hq * shape.hd
+    sites = [("qkv", "w_qkv", shape.d, shape.qkv_out), ("o", "w_o", nq, shape.d),
+             ("gate_up", "w_gu", shape.d, 2 * shape.inter), ("down", "w_down", shape.inter, shape.d)]
+    g0 = torch.Generator().manual_seed(77)
+    out = {"workload": f"{shape.name} projections, batch 1, larosa_sparse_gemv (LIST)", "peak_gbs": peaks["hbm_gbs"]}
+    stream = torch.cuda.current_stream()
+    for p in ps:
+        plan = M.site_plan(shape, p)
+        row = {}
+        tot_b, tot_us = 0, 0.0
+        for (name, attr, din, dout), k in zip(sites, plan):
+            n_in = 8
+            idx = [torch.sort(torch.randperm(din, generator=g0)[:k])[0].to(torch.int32).to(device) for _ in range(n_in)]
+            vals = [torch.randn((k,), generator=g0).to(device) for _ in range(n_in)]
+            y = torch.empty((1, dout), dtype=torch.float32, device=device)
+            ws = torch.zeros(LZ.lib().larosa_sparse_gemv_workspace_size(1, din, k, dout), dtype=torch.uint8,
+                             device=device)
+            LZ.sparse_gemv(getattr(layers[0], attr), idx[0], vals[0], out=y, ws=ws)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(reps):
+                    LZ.sparse_gemv(getattr(layers[i % n_copies], attr), idx[i % n_in], vals[i % n_in], out=y, ws=ws)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / (5 * reps)
+            sel = k * dout * 2
+            alg = sel + k * 8 + dout * 4
+            row[name] = {"k": k, "us": round(us, 3), "selected_bytes": sel, "gbs": round(alg / us / 1e3, 1),
+                         "frac": round(alg / us / 1e3 / peaks["hbm_gbs"], 3)}
+            tot_b += alg
+            tot_us += us
+            del g
+        row["all_sites"] = {"gbs": round(tot_b / tot_us / 1e3, 1), "frac": round(tot_b / tot_us / 1e3 / peaks["hbm_gbs"], 3)}
+        out[str(p)] = row
+    del layers
+    torch.cuda.empty_cache()
+    return out
+
+
 def model_sweep_extra(device, models=("mistral-7b", "qwen2.5-7b"), ps=(0.0, 0.25, 0.4, 0.5, 0.6), steps=400,
                       copies=4, merged=True):
     """BASELINE configs[3]: per-layer sparsity sweep of the Mistral-7B and Qwen2.5-7B blocks (batch 1,
