@@ -528,7 +528,23 @@ larosa_status launch_topk_m(const TopkKernelArgs& a, int batch, cudaStream_t st)
     return launch_topk_t<MODE, 8>(a, batch, st);
 }
 
+template <int EPT>
+larosa_status launch_rule_select_t(const TopkKernelArgs& a, int batch, cudaStream_t st) {
+    return cuda_check(launch(rule_select_kernel<EPT>, dim3(batch), dim3(kRsThreads), 0, st, a), "rule_select launch");
+}
+
 larosa_status launch_topk(const TopkKernelArgs& a, int batch, cudaStream_t st) {
+    // the per-token rule from a plain source (the batch 2-16 layer and shard phases): one CTA per
+    // token (tuning: LAROSA_RULE_CTA=0 = the cluster kernel)
+    static const int rule_cta = env_int("LAROSA_RULE_CTA", 1);
+    if (rule_cta && a.rule_out && a.mode == SRC_PLAIN && !a.idx && !a.vals && !a.mask && !a.xr_out && !a.zero &&
+        !a.scale && a.d <= kRsThreads * 32) {
+        const int ept = (a.d + kRsThreads - 1) / kRsThreads;
+        if (ept <= 4) return launch_rule_select_t<4>(a, batch, st);
+        if (ept <= 8) return launch_rule_select_t<8>(a, batch, st);
+        if (ept <= 16) return launch_rule_select_t<16>(a, batch, st);
+        return launch_rule_select_t<32>(a, batch, st);
+    }
     if (a.mode == SRC_RESID_ACC) return launch_topk_m<SRC_RESID_ACC>(a, batch, st);
     if (a.mode == SRC_SILU_GU) return launch_topk_m<SRC_SILU_GU>(a, batch, st);
     return launch_topk_m<SRC_PLAIN>(a, batch, st);
@@ -1430,6 +1446,7 @@ extern "C" larosa_status larosa_sparse_layer(const larosa_layer_weights* w, cons
             r.k = (int)k;
             r.rms_eps = eps;
             r.rule_out = W.thr[si];
+            r.tl = tl_slot(6 + si);
             // (tuning: 0 = the image from a separate rule_apply_image launch)
             static const int topk_image = env_int("LAROSA_TOPK_IMAGE", 1);
             if (img_path && topk_image) {   // the cluster Top-K kernel writes the image too

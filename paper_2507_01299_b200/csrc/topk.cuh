@@ -70,6 +70,7 @@ struct TopkKernelArgs {
     ThreshOut* rule_out;  // [batch] if set: emit the selection rule (no idx/vals lists)
     unsigned char* img;      // rule mode, batch 2-16: also write the token image (img_layout.cuh) of
     unsigned char* img_raw;  // the masked scaled values, and optionally of the raw values
+    unsigned long long* tl;  // debug timeline slot or null
 };
 
 // token b's element i = v of the image: masked and scaled (keep ? v s : 0) split bf16 hi | lo, and
@@ -128,8 +129,10 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
     int* s_pub = scr + 96;                                      // [96, 100)  published: n_gt, n_eq, ssq bits
     int* s_res = scr + 100;                                     // [100, 104) bucket result (owner CTA)
     int* mh = scr + 128;                                        // merged histogram slice (<= 4096)
+    tl_stamp(a.tl, 0);
     pdl_wait();
     pdl_trigger();
+    tl_stamp(a.tl, 1);
 
     const int d = a.d, k = a.k;
     const int b = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
         s_pub[2] = __float_as_int(t);
     }
     topk_cluster_sync();   // CTA 0's histograms are zero before anyone adds into them
+    tl_stamp(a.tl, 2);
 
     // ---- 2. radix select of the k-th largest key ----------------------------------------
     // per pass: local histograms (smem atomics) -> cluster barrier -> CTA r merges bin slice
@@ -286,6 +290,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
             const int cnt = (int)topk_ld_remote(res_remote + 8);
             prefix |= (uint32_t)bstar << sh;
             pmask |= dmask << sh;
+            tl_stamp(a.tl, 5 + pass);
             if (cnt == rem) {
                 exact_ge = true;
                 break;
@@ -323,7 +328,9 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
                                                scale);
             }
         }
+        tl_stamp(a.tl, 8);
         topk_cluster_sync();   // rank 0 read the others' published partials
+        tl_stamp(a.tl, 4);
         return;
     }
 
@@ -443,6 +450,204 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(TopkKernelArgs a)
 #undef KEY
 #undef VALID
     topk_cluster_sync();   // peers may still read this CTA's published counts
+}
+
+// ---- the per-token selection RULE at batch > 1 on one CTA per token (no cluster) -------------------
+// The rule kernel of the batch 2-16 layer (rule mode, plain source): token b's exact Top-K rule
+// (lower index on ties, Z10), its RMS scale and -- if img is set -- the token image, from ONE
+// 1024-thread CTA (element i = thread t + 1024 j, coalesced).  The k-th key is located by at most
+// three 11/11/9-bit digit histograms in shared memory; as soon as the boundary bucket holds
+// <= kRsCand keys they are gathered and ranked exactly by (key desc, index asc), which yields
+// (Tk, Ti) directly (usually after the first digit).  A bucket of > kRsCand identical 31-bit keys
+// takes the index-ordered walk.  No cluster barriers or distributed shared memory: the cluster
+// kernel's 6+ cluster-wide barriers per token were the batch-16 rule's cost.
+constexpr int kRsThreads = 1024;
+constexpr int kRsBins = 2048;
+constexpr int kRsCand = 256;
+
+template <int EPT>
+__global__ void __launch_bounds__(kRsThreads, 1) rule_select_kernel(const TopkKernelArgs a) {
+    constexpr int NT = kRsThreads;
+    __shared__ int hist[kRsBins];
+    __shared__ __align__(16) uint32_t ck[kRsCand];
+    __shared__ __align__(16) int ci[kRsCand];
+    __shared__ int sw[NT / 32 + 1];
+    __shared__ float fsw[NT / 32];
+    __shared__ int misc[8];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int d = a.d, k = a.k;
+    tl_stamp(a.tl, 0);
+    for (int i = tid; i < kRsBins; i += NT) hist[i] = 0;
+    pdl_wait();
+    pdl_trigger();
+    tl_stamp(a.tl, 1);
+    const float* x = a.x + (size_t)b * a.ldx;
+    uint32_t xb[EPT];
+    float ssq = 0.f;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+        const int i = tid + NT * j;
+        const float v = i < d ? x[i] : 0.f;
+        xb[j] = __float_as_uint(v);
+        ssq = fmaf(v, v, ssq);
+    }
+    const float tot = block_sum<NT>(ssq, fsw);   // (fixed order; contains the barrier after the zeroing)
+    const float scale = a.rms_eps >= 0.f ? 1.0f / sqrtf(tot / (float)d + a.rms_eps) : 1.0f;
+    tl_stamp(a.tl, 2);
+#define RS_KEY(j) (xb[j] & 0x7fffffffu)
+#define RS_VALID(j) (tid + NT * (j) < d)
+    uint32_t tk = 0u;
+    int ti = 0x7fffffff;
+    if (k <= 0) {
+        tk = 0xffffffffu;   // keys < 2^31: nothing is kept
+        ti = -1;
+    } else if (k < d) {
+        uint32_t prefix = 0u, pmask = 0u;
+        int rem = k;
+#pragma unroll 1
+        for (int L = 0; L < 3; ++L) {
+            const int sh = L == 0 ? 20 : (L == 1 ? 9 : 0);
+            const int nb = L == 2 ? 512 : kRsBins;
+            const uint32_t dm = (uint32_t)(nb - 1);
+            if (L > 0) {
+                for (int i = tid; i < nb; i += NT) hist[i] = 0;
+                __syncthreads();
+            }
+            // (plain shared atomics: warp aggregation by match.any measured slower here)
+            const int lane = tid & 31;
+#pragma unroll
+            for (int j = 0; j < EPT; ++j)
+                if (RS_VALID(j) && (RS_KEY(j) & pmask) == prefix) atomicAdd(&hist[(RS_KEY(j) >> sh) & dm], 1);
+            __syncthreads();
+            if (L == 0) tl_stamp(a.tl, 9);
+            // thread t owns bins [nb - bpt (t + 1), nb - bpt t) (top bins first)
+            const int bpt = (nb + NT - 1) / NT;
+            const int hi = nb - bpt * tid;
+            int c = 0;
+            for (int q = hi - 1; q >= max(0, hi - bpt); --q) c += hist[q];
+            int total;
+            const int above = block_excl_scan<NT>(c, sw, &total);
+            if (c > 0 && above < rem && rem <= above + c) {
+                int acc = above;
+                for (int q = hi - 1; q >= max(0, hi - bpt); --q) {
+                    if (acc + hist[q] >= rem) {
+                        misc[0] = q;
+                        misc[1] = rem - acc;
+                        misc[2] = hist[q];
+                        break;
+                    }
+                    acc += hist[q];
+                }
+            }
+            if (tid == 0) misc[3] = 0;
+            __syncthreads();
+            const int bin = misc[0], cnt = misc[2];
+            if (L == 0) tl_stamp(a.tl, 10);
+            rem = misc[1];
+            prefix |= (uint32_t)bin << sh;
+            pmask |= dm << sh;
+            if (cnt == rem) {            // the bucket is taken whole: key >= prefix
+                tk = prefix;
+                ti = 0x7fffffff;
+                break;
+            }
+            if (cnt <= kRsCand) {        // gather the bucket and rank it exactly
+#pragma unroll
+                for (int j = 0; j < EPT; ++j) {
+                    const bool in = RS_VALID(j) && (RS_KEY(j) & pmask) == prefix;
+                    const unsigned m = __ballot_sync(0xffffffffu, in);
+                    if (m) {             // one counter atomic per warp
+                        int base = 0;
+                        if (lane == __ffs(m) - 1) base = atomicAdd(&misc[3], __popc(m));
+                        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+                        if (in) {
+                            const int slot = base + __popc(m & ((1u << lane) - 1u));
+                            ck[slot] = RS_KEY(j);
+                            ci[slot] = tid + NT * j;
+                        }
+                    }
+                }
+                __syncthreads();
+                tl_stamp(a.tl, 11);
+                // rank: 4 threads per candidate (adjacent lanes), each over a quarter of the bucket,
+                // 4 candidates per 16-byte shared load
+                {
+                    const int cnd = tid >> 2, part = tid & 3;
+                    const int cnt4 = (cnt + 3) & ~3;
+                    for (int u = cnt + tid; u < cnt4; u += NT) {   // pad to a multiple of 4 (never ranks above)
+                        ck[u] = 0u;
+                        ci[u] = 0x7fffffff;
+                    }
+                    __syncthreads();
+                    int r = 0;
+                    uint32_t mk = 0u;
+                    int mi = 0;
+                    if (cnd < cnt) {
+                        mk = ck[cnd];
+                        mi = ci[cnd];
+                        const int q4 = cnt4 / 4;                    // 4-key groups
+                        for (int g4 = part; g4 < q4; g4 += 4) {
+                            const uint4 kk = reinterpret_cast<const uint4*>(ck)[g4];
+                            const int4 ii = reinterpret_cast<const int4*>(ci)[g4];
+                            r += (kk.x > mk || (kk.x == mk && ii.x < mi)) + (kk.y > mk || (kk.y == mk && ii.y < mi)) +
+                                 (kk.z > mk || (kk.z == mk && ii.z < mi)) + (kk.w > mk || (kk.w == mk && ii.w < mi));
+                        }
+                    }
+                    r += __shfl_xor_sync(0xffffffffu, r, 1);
+                    r += __shfl_xor_sync(0xffffffffu, r, 2);
+                    if (cnd < cnt && part == 0 && r == rem - 1) {
+                        misc[4] = (int)mk;
+                        misc[5] = mi;
+                    }
+                }
+                __syncthreads();
+                tk = (uint32_t)misc[4];
+                ti = misc[5];
+                break;
+            }
+            if (L == 2) {                // > kRsCand identical keys: the rem-th lowest index among them
+                tk = prefix;
+                uint32_t eqm = 0u;       // (a register bit mask: xb stays in registers)
+#pragma unroll
+                for (int j = 0; j < EPT; ++j)
+                    if (RS_VALID(j) && RS_KEY(j) == prefix) eqm |= 1u << j;
+                int base = 0;
+#pragma unroll 1
+                for (int j = 0; j < EPT; ++j) {
+                    const bool eq = (eqm >> j) & 1u;
+                    int tot_j;
+                    const int pos = block_excl_scan<NT>(eq ? 1 : 0, sw, &tot_j);
+                    if (eq && base + pos == rem - 1) misc[6] = tid + NT * j;
+                    base += tot_j;
+                    __syncthreads();
+                    if (base >= rem) break;
+                }
+                __syncthreads();
+                ti = misc[6];
+            }
+        }
+    }
+    tl_stamp(a.tl, 5);
+    if (tid == 0) {
+        ThreshOut r;
+        r.tk = tk;
+        r.ti = ti;
+        r.scale = scale;
+        r.pad = 0;
+        a.rule_out[b] = r;
+    }
+    if (a.img) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j)
+            if (RS_VALID(j)) {
+                const uint32_t key = RS_KEY(j);
+                const int i = tid + NT * j;
+                topk_img_put(a.img, a.img_raw, b, i, __uint_as_float(xb[j]), key > tk || (key == tk && i <= ti), scale);
+            }
+    }
+#undef RS_KEY
+#undef RS_VALID
+    tl_stamp(a.tl, 4);
 }
 
 }  // namespace larosa

@@ -352,3 +352,31 @@ def test_layer_host_io_equals_device_io(merged):
     torch.cuda.synchronize()
     assert torch.equal(st2.resid.cpu(), st.resid.cpu())
     assert torch.equal(h_out, st.resid.cpu())
+
+
+@pytest.mark.parametrize("batch,merged", [(16, True), (3, False), (8, True)])
+def test_layer_batch_rule_degenerate_tokens(batch, merged):
+    """Batch > 1 selection rule (one CTA per token, rule_select_kernel) on degenerate tokens, site by
+    site against the oracle (P6): a constant vector (every key equal: the k lowest indices), 3000
+    equal maxima with smaller noise (the boundary inside > 256 identical keys: the index-ordered
+    walk), a vector of zeros with 100 non-zeros (the boundary among the zeros, -0 included), and
+    random tokens."""
+    from layer_check import OracleWeights, p6_layer
+    shape = synth.MODELS["llama3-8b"]
+    max_ctx = 64
+    _, _, _, lw, plan, resid, kc0, vc0, pos = build(shape, 29, batch, 40, max_ctx, 0.4, merged=merged)
+    d = shape.d
+    g = torch.Generator().manual_seed(31)
+    resid[0] = 0.5
+    resid[1] = 0.1 * torch.randn(d, generator=g)
+    resid[1, :3000] = 1.0
+    resid[2] = 0.0
+    resid[2, torch.randperm(d, generator=g)[:100]] = torch.randn(100, generator=g)
+    resid[2, 1::7] = -0.0
+    st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
+    ow = OracleWeights(lw)
+    kc_gpu = st.k_cache.cpu().numpy().view(np.uint16)
+    vc_gpu = st.v_cache.cpu().numpy().view(np.uint16)
+    for b in range(batch):
+        p6_layer(ow, shape, plan, tp, b, resid[b].numpy().astype(np.float64), kc0[b].numpy().view(np.uint16),
+                 kc_gpu[b], vc_gpu[b], int(pos[b]), f64(st.resid[b]))

@@ -3,7 +3,7 @@ subprocess): the batch-16 rule / token-image paths (LAROSA_RULE_KERNEL 0: cluste
 gemv_tc; 1: rule_image_kernel; 2: cluster Top-K + rule_apply_image (default); 3: register-resident
 rule_image) and the attention kernels (LAROSA_ATTN 1: split-KV ticket merge; 2: cluster DSMEM
 merge; default: single pass).  Every variant computes the same exact kept sets, so the image paths
-(1, 2, 3) must agree bit for bit and every variant must match the default within fp32 rounding."""
+must agree with the default within fp32 rounding (their RMS sums run in different fixed orders)."""
 import os
 import subprocess
 import sys
@@ -46,12 +46,17 @@ def run(env, B, max_ctx, tmp, tag):
 
 
 def test_rule_kernel_variants(tmp_path):
+    """Every rule / image path computes the same exact kept sets; their RMS scales are summed in
+    different (each fixed) orders, so the outputs agree within fp32 rounding.  The default rule
+    kernel (one CTA per token) and the cluster kernel (LAROSA_RULE_CTA=0) feed the same image."""
     ref = run({}, 16, 64, tmp_path, "default")
     outs = {m: run({"LAROSA_RULE_KERNEL": m}, 16, 64, tmp_path, f"rk{m}") for m in ("0", "1", "2", "3")}
+    outs["cluster"] = run({"LAROSA_RULE_CTA": "0"}, 16, 64, tmp_path, "cluster")
     assert np.array_equal(outs["2"], ref)
-    assert np.array_equal(outs["1"], ref) and np.array_equal(outs["3"], ref)
-    for b in range(16):
-        assert np.max(np.abs(outs["0"][b] - ref[b])) <= 1e-5 * np.linalg.norm(ref[b])
+    assert np.array_equal(outs["1"], outs["3"])
+    for m, o in outs.items():
+        for b in range(16):
+            assert np.max(np.abs(o[b] - ref[b])) <= 1e-5 * np.linalg.norm(ref[b]), (m, b)
 
 
 @pytest.mark.parametrize("B,max_ctx", [(1, 64), (3, 200), (16, 256)])

@@ -38,13 +38,13 @@ def main():
     L = LZ.lib()
     L.larosa_debug_set_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.larosa_debug_set_timeline.restype = None
-    tl = torch.zeros((n, 6, 1024, 16), dtype=torch.int64, device=DEV)
+    tl = torch.zeros((n, 10, 1024, 16), dtype=torch.int64, device=DEV)
     for i in range(n):
         LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos), ws=wsb)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for i in range(n):
-            L.larosa_debug_set_timeline(ctypes.c_void_p(tl[i].data_ptr()), 6)
+            L.larosa_debug_set_timeline(ctypes.c_void_p(tl[i].data_ptr()), 10)
             LZ.sparse_layer(layers[i], plan, LZ.LayerState(resid, *kv[i], pos), ws=wsb)
         L.larosa_debug_set_timeline(None, 0)
     acc = []
@@ -73,6 +73,25 @@ def main():
                 st.setdefault("ctas", []).append(int(live.sum()))
         out["kernels"][NAMES[k]] = {kk: round(float(np.mean(v)) / (1e3 if kk != "ctas" else 1), 2)
                                     for kk, v in st.items()}
+    # the Top-K rule kernels (slots 6-9: sites h1..h4), phases relative to their dependency release
+    for si in range(4):
+        st = {}
+        for a in acc:
+            for li in range(1, n):
+                cur = a[li][6 + si]
+                live = cur[:, 1] > 0
+                if not live.any():
+                    continue
+                c = cur[live]
+                t1 = c[:, 1].min()
+                for i, key in ((2, "loaded"), (9, "hist0"), (10, "scan0"), (11, "gathered"), (5, "pass0/rule"),
+                               (6, "pass1"), (8, "rule_image"), (4, "exit")):
+                    col = c[:, i][c[:, i] > 0] - t1
+                    if col.size:
+                        st.setdefault(f"{key}_max", []).append(col.max())
+                st.setdefault("ctas", []).append(int(live.sum()))
+        out["kernels"][f"topk_h{si + 1}"] = {kk: round(float(np.mean(v)) / (1e3 if kk != "ctas" else 1), 2)
+                                             for kk, v in st.items()}
     print(json.dumps(out))
 
 
