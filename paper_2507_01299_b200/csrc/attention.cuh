@@ -518,25 +518,36 @@ __global__ void __launch_bounds__(kAgThreads, 1) attn_group_kernel(const AttnArg
             }
             s[i] = acc;
         }
+        // transpose-reduce of the 16 partial dot products: at each butterfly level a lane keeps the
+        // half of its values its partner does not, so 8 + 4 + 2 + 1 + 1 shuffles (not 5 x 16) leave
+        // the full score of position pl = (lane >> 1) & 15 in lanes 2 pl and 2 pl + 1
+        static_assert(kAgPos == 16, "transpose-reduce of 16 positions");
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        for (int lvl = 0; lvl < 4; ++lvl) {
+            const int ob = 16 >> lvl, nh = 8 >> lvl;
+            const bool up = (lane & ob) != 0;
 #pragma unroll
-            for (int i = 0; i < kAgPos; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
-        float m = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < kAgPos; ++i) {
-            s[i] = (warp * kAgPos + i < ctx) ? s[i] * scale : -INFINITY;
-            m = fmaxf(m, s[i]);
+            for (int i = 0; i < nh; ++i) {
+                const float send = up ? s[i] : s[i + nh];
+                const float keep = up ? s[i + nh] : s[i];
+                s[i] = keep + __shfl_xor_sync(0xffffffffu, send, ob);
+            }
         }
-        float l = 0.f, o[DPL];
+        const int pl = (lane >> 1) & 15;
+        const bool live = warp * kAgPos + pl < ctx;
+        const float full_s = s[0] + __shfl_xor_sync(0xffffffffu, s[0], 1);   // (every lane shuffles)
+        const float sc = live ? full_s * scale : -INFINITY;
+        const float m = warp_max(sc);
+        const float ex = live ? expf(sc - m) : 0.f;
+        const float l = warp_sum((lane & 1) ? 0.f : ex);   // each position once (lanes 2 pl)
+        float o[DPL];
 #pragma unroll
         for (int t = 0; t < DPL; ++t) o[t] = 0.f;
 #pragma unroll
         for (int i = 0; i < kAgPos; ++i) {
             const int p = warp * kAgPos + i;
+            const float e = __shfl_sync(0xffffffffu, ex, 2 * i);
             if (p < ctx) {
-                const float e = expf(s[i] - m);
-                l += e;
                 const uint32_t* vrow = reinterpret_cast<const uint32_t*>(sv + (size_t)p * hd + lane * DPL);
 #pragma unroll
                 for (int t = 0; t < DPL / 2; ++t) {

@@ -575,7 +575,9 @@ larosa_status launch_attention(AttnArgs aa, int units, int hd, int G, cudaStream
     const int mode = attn_mode(aa.max_ctx, aa.n_chunks);
     if (mode == 3) {
         // units = batch * Hq query heads: one CTA per head when they fit one wave, else one per group
-        const int hpc = units <= sm_count() ? 1 : G;
+        static const int hpc_env = env_int("LAROSA_ATTN_HPC", 0);   // tuning
+        int hpc = units <= sm_count() ? 1 : G;
+        if (hpc_env > 0 && G % hpc_env == 0) hpc = hpc_env;
         const size_t smem = attn_group_smem_bytes(hd, hpc);
         auto kern = hd == 128 ? attn_group_kernel<4> : attn_group_kernel<2>;
         LAROSA_TRY(cuda_check(allow_smem(kern, smem), "cudaFuncSetAttribute(attention)"));

@@ -73,6 +73,23 @@ def main():
                 st.setdefault("ctas", []).append(int(live.sum()))
         out["kernels"][NAMES[k]] = {kk: round(float(np.mean(v)) / (1e3 if kk != "ctas" else 1), 2)
                                     for kk, v in st.items()}
+    # attention (slot 1): phases relative to its dependency release
+    st = {}
+    for a in acc:
+        for li in range(1, n):
+            cur = a[li][1]
+            live = cur[:, 1] > 0
+            if not live.any():
+                continue
+            c = cur[live]
+            t1 = c[:, 1].min()
+            for i, key in ((0, "entry"), (2, "q_kv_ready"), (3, "scores_pv"), (6, "merged"), (4, "exit")):
+                col = c[:, i][c[:, i] > 0] - t1
+                if col.size:
+                    st.setdefault(f"{key}_med", []).append(np.median(col))
+                    st.setdefault(f"{key}_max", []).append(col.max())
+            st.setdefault("ctas", []).append(int(live.sum()))
+    out["kernels"]["attention"] = {kk: round(float(np.mean(v)) / (1e3 if kk != "ctas" else 1), 2) for kk, v in st.items()}
     # the Top-K rule kernels (slots 6-9: sites h1..h4), phases relative to their dependency release
     for si in range(4):
         st = {}
