@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for v in liblarosa_pf0 liblarosa liblarosa_pfall liblarosa_pf0 liblarosa liblarosa_pfall; do
+  LAROSA_LIB=$PWD/paper_2507_01299_b200/lib/$v.so timeout 300 python tools/layer_timeline.py --model llama3-8b --p 0.4 > gpurun_out/tl_$v.json 2>&1
+  echo "$v $(python -c "import json;d=json.loads(open('gpurun_out/tl_$v.json').read().strip().splitlines()[-1]);print(d['layer_us'], {k:(v.get('prologue_med'), v.get('loop_med'), v.get('exit_max')) for k,v in d['kernels'].items()})")"
+done
