@@ -156,6 +156,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvArgs a
     pdl_wait();
     pdl_trigger();
     tl_stamp(a.tl, 1);
+    if (a.zero_hist) {   // words whose consumer has completed (the LIST path's token masks)
+        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+        for (int i = cta * kTcThreads + tid; i < a.zero_words; i += nct * kTcThreads) a.zero_hist[i] = 0u;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();

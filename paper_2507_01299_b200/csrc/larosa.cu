@@ -751,8 +751,11 @@ extern "C" larosa_status larosa_sparse_gemv(const uint16_t* W, int64_t d_in, int
         a.vs_b = k;
         a.nrows = (int)k;
     } else {
+        // the token masks are zero at rest: the GEMV below re-zeroes them once the union kernel
+        // has consumed them (no memset on the path)
         const int nw = (int)((d_in + 31) / 32);
-        LAROSA_TRY(cuda_check(cudaMemsetAsync(mask, 0, sizeof(uint32_t) * (size_t)batch * nw, st), "memset mask"));
+        a.zero_hist = mask;
+        a.zero_words = batch * nw;
         if (k > 0) {
             const int64_t n = (int64_t)batch * k;
             const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
