@@ -16,11 +16,35 @@
 namespace larosa {
 
 constexpr int kW4Group = 128;                 // == LAROSA_W4_GROUP
-constexpr int kW4SliceCols = 1024;            // columns per CTA: a kept row's slice segment is 512 B
-constexpr int kW4Stages = 16;                 // rows in flight per warp (one 512-byte row per stage): 64 KB per CTA
-constexpr int kW4RowBytes = kW4SliceCols / 2;
-constexpr int kW4CompRowBytes = kW4SliceCols * 2;                        // a companion bf16 row segment
-constexpr int kW4CompStages = kW4Stages * kW4RowBytes / kW4CompRowBytes;  // 4 rows per warp
+// Slice width (columns per CTA) per launch: 512 (256 B per kept row, lane = 16 columns: twice the
+// finalising CTAs, half the reds and epilogue work per CTA -- the small sites, whose tails were
+// longer than their streams) or 1024 (512 B, lane = 32 columns: 16-byte loads -- the large sites)
+template <int SC>
+struct W4Cfg {
+    static constexpr int kSliceCols = SC;
+    static constexpr int kLaneCols = SC / 32;                 // columns per lane
+    static constexpr int kLaneBytes = kLaneCols / 2;          // int4 bytes per lane and row (16 or 8)
+    static constexpr int kGroups = SC / kW4Group;             // scale groups per slice (8 or 4)
+    static constexpr int kRowBytes = SC / 2;
+    static constexpr int kStages = 8192 / kRowBytes;          // rows in flight per warp: 8 KB ring per warp
+    static constexpr int kCompRowBytes = SC * 2;              // a companion bf16 row segment
+    static constexpr int kCompStages = kStages * kRowBytes / kCompRowBytes;
+    static_assert(kLaneBytes == 16 || kLaneBytes == 8, "W4 lane width");
+    static_assert(kW4Group % kLaneCols == 0, "a lane's columns lie in one scale group");
+};
+
+// cp.async of N (8 or 16) bytes; 8 bytes only exists in the L1-allocating (.ca) form
+template <int N>
+__device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, bool pred) {
+    if constexpr (N == 16) {
+        cp_async16(smem_dst, gsrc, pred);
+    } else {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                     "@p cp.async.ca.shared.global [%0], [%1], 8;\n\t}" ::"r"(smem_u32(smem_dst)),
+                     "l"(gsrc), "r"((int)pred)
+                     : "memory");
+    }
+}
 
 __device__ __forceinline__ float half_bits_to_f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 // paired fp32 add of a constant: {w.x, w.y} += {c, c}
@@ -35,14 +59,17 @@ __device__ __forceinline__ void fadd2_const(float2& w, float c) {
 // Shared memory: [ring 8 warps x 4 stages x 512 B | selection staging (aliased)] [row list + values]
 // [misc] [row scales: 8 fp16 per kept row].  The partial sums (8 warps x 1024 fp32) alias the ring
 // and the staging at the end.
-static_assert((size_t)kGemvWarps * kW4Stages * kW4RowBytes <= (size_t)kGemvWarps * kWarpRingBytes, "W4 ring size");
+static_assert((size_t)kGemvWarps * 8192 <= (size_t)kGemvWarps * kWarpRingBytes, "W4 ring size");
+template <int SC>
 __host__ __device__ constexpr size_t w4_region_bytes(int d_in) {
-    return gemv_x_bytes(1, GEMV_SELECT, d_in) > (size_t)kGemvWarps * kW4SliceCols * 4 ? gemv_x_bytes(1, GEMV_SELECT, d_in)
-                                                                                      : (size_t)kGemvWarps * kW4SliceCols * 4;
+    return gemv_x_bytes(1, GEMV_SELECT, d_in) > (size_t)kGemvWarps * SC * 4 ? gemv_x_bytes(1, GEMV_SELECT, d_in)
+                                                                           : (size_t)kGemvWarps * SC * 4;
 }
-// the whole plan: region, row list + values, misc, 8 fp16 scales and 8 fp32 b = v s per kept row
+// the whole plan: region, row list + values, misc, the fp16 scales and fp32 b = v s per kept row
+template <int SC>
 __host__ __device__ constexpr size_t w4_smem_bytes(int d_in, int list_cap) {
-    return w4_region_bytes(d_in) + (size_t)list_cap * 8 + kGemvMisc * 4 + (size_t)list_cap * 16 + (size_t)list_cap * 32;
+    return w4_region_bytes<SC>(d_in) + (size_t)list_cap * 8 + kGemvMisc * 4 + (size_t)list_cap * 2 * W4Cfg<SC>::kGroups +
+           (size_t)list_cap * 4 * W4Cfg<SC>::kGroups + 16;
 }
 
 // (x & m) | c in one LOP3 (the compiler splits it when both are immediates)
@@ -149,8 +176,10 @@ __device__ void gemv_epilogue_b1_multi(const GemvArgs& a, int vs0, int nv, float
     }
 }
 
+template <int SC>
 __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const GemvArgs a, const uint8_t* __restrict__ Wq,
                                                                         const uint16_t* __restrict__ S) {
+    using C = W4Cfg<SC>;
     extern __shared__ __align__(128) unsigned char smem[];
     // blockIdx.y < n_splits2: companion CTAs streaming dense bf16 rows [c_lo, c_lo + c_n) of W2
     // (ld = d_out) against x2 into the same accumulators (the residual adapter beside down)
@@ -163,31 +192,31 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
         c_lo = min(a.d2, (int)blockIdx.y * rng);
         c_n = min(a.d2, c_lo + rng) - c_lo;
     }
-    const size_t rb = w4_region_bytes(a.d_in);
+    const size_t rb = w4_region_bytes<SC>(a.d_in);
     int* lrow = reinterpret_cast<int*>(smem + rb);                                 // [cap]
     float* lval = reinterpret_cast<float*>(lrow + a.list_cap);                     // [cap]
     int* misc = reinterpret_cast<int*>(lval + a.list_cap);                         // [kGemvMisc]
-    uint4* lsc = reinterpret_cast<uint4*>(misc + kGemvMisc);                       // [cap] 8 fp16 scales
-    float4* lb = reinterpret_cast<float4*>(lsc + a.list_cap);                      // [cap][2] b = v s per group
+    uint16_t* lsc = reinterpret_cast<uint16_t*>(misc + kGemvMisc);                 // [cap][C::kGroups] fp16 scales
+    float* lb = reinterpret_cast<float*>(lsc + (size_t)a.list_cap * C::kGroups);     // [cap][C::kGroups] b = v s
     const int ngroups = a.d_out / kW4Group;
 
-    const int colb = slice * kW4SliceCols + 32 * lane;
+    const int colb = slice * C::kSliceCols + C::kLaneCols * lane;
     const bool lane_on = colb < a.d_out;
-    // companion ring: per warp kW4CompStages rows of 2 KB (lane l: the 64 bytes of its 32 columns)
-    unsigned char* cchunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 64 * lane;
+    // companion ring: per warp C::kCompStages bf16 row segments (lane l: the 2 C::kLaneCols bytes of its columns)
+    unsigned char* cchunk = smem + (size_t)warp * C::kStages * C::kRowBytes + 2 * C::kLaneCols * lane;
     const int c_my = c_n > warp ? (c_n - warp + kGemvWarps - 1) / kGemvWarps : 0;
     auto comp_issue = [&](int m) {
         if (m < c_my) {
             const uint16_t* src = a.W2 + (size_t)(c_lo + warp + kGemvWarps * m) * a.d_out + colb;
-            unsigned char* dst = cchunk + (size_t)(m % kW4CompStages) * kW4CompRowBytes;
+            unsigned char* dst = cchunk + (size_t)(m % C::kCompStages) * C::kCompRowBytes;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) cp_async16(dst + 16 * q, src + 8 * q, lane_on);
+            for (int q = 0; q < C::kLaneCols / 8; ++q) cp_async16(dst + 16 * q, src + 8 * q, lane_on);
         }
         cp_async_commit();
     };
     if (comp) {   // the first stages do not depend on the previous kernel
 #pragma unroll
-        for (int m = 0; m < kW4CompStages; ++m) comp_issue(m);
+        for (int m = 0; m < C::kCompStages; ++m) comp_issue(m);
     }
     int sel_guess = 0;
     if (!comp && threadIdx.x == 0) sel_guess = (int)__ldcg(a.sel.hist + kSelHistTotal);
@@ -203,9 +232,9 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
         const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
         for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_acc_words; i += nct * kGemvThreads) a.zero_acc[i] = 0ull;
     }
-    float2 acc[16];
+    float2 acc[C::kLaneCols / 2];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < C::kLaneCols / 2; ++j) acc[j] = make_float2(0.f, 0.f);
     float bsum = 0.f;
     int n_list;
     if (comp) {
@@ -214,58 +243,56 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
         __syncthreads();
         tl_stamp(a.tl, 2);
         for (int m = 0; m < c_my; ++m) {
-            cp_async_wait<kW4CompStages - 1>();
-            const unsigned char* src = cchunk + (size_t)(m % kW4CompStages) * kW4CompRowBytes;
+            cp_async_wait<C::kCompStages - 1>();
+            const unsigned char* src = cchunk + (size_t)(m % C::kCompStages) * C::kCompRowBytes;
             const float v = lval[warp + kGemvWarps * m];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < C::kLaneCols / 8; ++q) {
                 const uint4 w = lds128(src + 16 * q);
                 ffma2(acc[4 * q + 0], bf16lo(w.x), bf16hi(w.x), v);
                 ffma2(acc[4 * q + 1], bf16lo(w.y), bf16hi(w.y), v);
                 ffma2(acc[4 * q + 2], bf16lo(w.z), bf16hi(w.z), v);
                 ffma2(acc[4 * q + 3], bf16lo(w.w), bf16hi(w.w), v);
             }
-            comp_issue(m + kW4CompStages);
+            comp_issue(m + C::kCompStages);
         }
     } else {
     n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
     // the kept rows' 8 group scales of this slice (16 bytes), once, before the stream
-    const int g0 = slice * (kW4SliceCols / kW4Group);
-    const int ng = min(kW4SliceCols / kW4Group, ngroups - g0);
+    const int g0 = slice * C::kGroups;
+    const int ng = min(C::kGroups, ngroups - g0);
     for (int t = threadIdx.x; t < n_list; t += kGemvThreads) {
         const uint16_t* src = S + (size_t)lrow[t] * ngroups + g0;
-        if (ng == 8 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            cp_async16(lsc + t, src, true);
+        if (ng == C::kGroups && (reinterpret_cast<uintptr_t>(src) & (2 * C::kGroups - 1)) == 0) {
+            cp_async_n<2 * C::kGroups>(lsc + (size_t)t * C::kGroups, src, true);
         } else {
-            uint16_t* d = reinterpret_cast<uint16_t*>(lsc + t);
-            for (int q = 0; q < 8; ++q) d[q] = q < ng ? src[q] : (uint16_t)0;
+            uint16_t* d = lsc + (size_t)t * C::kGroups;
+            for (int q = 0; q < C::kGroups; ++q) d[q] = q < ng ? src[q] : (uint16_t)0;
         }
     }
     // the first stages of the stream go out with the scales (the row list is complete and the
     // staged selection data the ring aliases is dead)
-    unsigned char* mychunk = smem + (size_t)warp * kW4Stages * kW4RowBytes + 16 * lane;
+    unsigned char* mychunk = smem + (size_t)warp * C::kStages * C::kRowBytes + C::kLaneBytes * lane;
     const int n_my = n_list > warp ? (n_list - warp + kGemvWarps - 1) / kGemvWarps : 0;
     const uint8_t* wl = Wq + colb / 2;
     const size_t ldq = (size_t)a.d_out / 2;
     auto issue = [&](int m) {
-        if (m < n_my) cp_async16(mychunk + (size_t)(m % kW4Stages) * kW4RowBytes,
-                                 wl + (size_t)lrow[warp + kGemvWarps * m] * ldq, lane_on);
+        if (m < n_my) cp_async_n<C::kLaneBytes>(mychunk + (size_t)(m % C::kStages) * C::kRowBytes,
+                                               wl + (size_t)lrow[warp + kGemvWarps * m] * ldq, lane_on);
         cp_async_commit();
     };
-    cp_async_commit();   // the scales: the group before the stream's first kW4Stages groups
+    cp_async_commit();   // the scales: the group before the stream's first C::kStages groups
 #pragma unroll
-    for (int m = 0; m < kW4Stages; ++m) issue(m);
-    cp_async_wait<kW4Stages>();
+    for (int m = 0; m < C::kStages; ++m) issue(m);
+    cp_async_wait<C::kStages>();
     __syncthreads();
     // b[t][g] = (x_j s_rms) S[j][g0 + g] for each kept row, once per CTA (the stream reads one float)
     {
         const float sel_scale = reinterpret_cast<const float*>(misc)[4];
         for (int t = threadIdx.x; t < n_list; t += kGemvThreads) {
-            const uint4 sc = lsc[t];
             const float v = lval[t] * sel_scale;
-            auto h = [](uint32_t w, int hi) { return half_bits_to_f((uint16_t)(hi ? (w >> 16) : (w & 0xffffu))); };
-            lb[2 * t] = make_float4(v * h(sc.x, 0), v * h(sc.x, 1), v * h(sc.y, 0), v * h(sc.y, 1));
-            lb[2 * t + 1] = make_float4(v * h(sc.z, 0), v * h(sc.z, 1), v * h(sc.w, 0), v * h(sc.w, 1));
+#pragma unroll
+            for (int q = 0; q < C::kGroups; ++q) lb[(size_t)t * C::kGroups + q] = v * half_bits_to_f(lsc[(size_t)t * C::kGroups + q]);
         }
     }
     __syncthreads();
@@ -273,21 +300,31 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
 
     // warp w takes list entries w + 8 m; lane l owns columns 32 l .. 32 l + 31 of the slice (one
     // scale group: l / 4) and copies exactly those 16 bytes of each row (no cross-lane dependency);
-    // the first kW4Stages rows are in flight since the prologue
-    const float* lbf = reinterpret_cast<const float*>(lb) + (lane >> 2);
+    // the first C::kStages rows are in flight since the prologue
+    const float* lbf = lb + (C::kLaneCols * lane) / kW4Group;   // the lane's scale group
     // sum_j b_j (16 + q_j) accumulated, sum_j b_j beside it: y = acc - 24 sum_j b_j at the end
     // (16 + q is one byte permute of a pre-shifted code byte; the offset costs ~3 bits of the fp32
     // sums, far inside the 1e-5 parity bound)
     const uint32_t hibit = 0x80808080u, nmask = 0x78787878u;
     for (int m = 0; m < n_my; ++m) {
-        cp_async_wait<kW4Stages - 1>();
+        cp_async_wait<C::kStages - 1>();
         const int pos = warp + kGemvWarps * m;
-        const uint4 q4 = lds128(mychunk + (size_t)(m % kW4Stages) * kW4RowBytes);
-        const float b = lbf[(size_t)pos * 8];
+        uint32_t qw[C::kLaneBytes / 4];
+        if constexpr (C::kLaneBytes == 16) {
+            const uint4 q4 = lds128(mychunk + (size_t)(m % C::kStages) * C::kRowBytes);
+            qw[0] = q4.x;
+            qw[1] = q4.y;
+            qw[2] = q4.z;
+            qw[3] = q4.w;
+        } else {
+            const uint2 q2 = *reinterpret_cast<const uint2*>(mychunk + (size_t)(m % C::kStages) * C::kRowBytes);
+            qw[0] = q2.x;
+            qw[1] = q2.y;
+        }
+        const float b = lbf[(size_t)pos * C::kGroups];
         bsum += b;
-        const uint32_t qw[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-        for (int wi = 0; wi < 4; ++wi) {
+        for (int wi = 0; wi < C::kLaneBytes / 4; ++wi) {
             const uint32_t lo = and_or(qw[wi] << 3, nmask, hibit);   // low nibbles at bits 3-6
             const uint32_t hi = and_or(qw[wi] >> 1, nmask, hibit);   // high nibbles at bits 3-6
             ffma2(acc[4 * wi + 0], w4_f16q<0>(lo), w4_f16q<0>(hi), b);
@@ -295,7 +332,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
             ffma2(acc[4 * wi + 2], w4_f16q<2>(lo), w4_f16q<2>(hi), b);
             ffma2(acc[4 * wi + 3], w4_f16q<3>(lo), w4_f16q<3>(hi), b);
         }
-        issue(m + kW4Stages);
+        issue(m + C::kStages);
     }
     }   // SELECT split
     cp_async_wait<0>();
@@ -304,24 +341,24 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     {
         const float corr = -24.0f * bsum;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) fadd2_const(acc[j], corr);
+        for (int j = 0; j < C::kLaneCols / 2; ++j) fadd2_const(acc[j], corr);
     }
     // fixed-order sum of the 8 warps' partials, one fixed-point red per column (4 per thread)
     float* part = reinterpret_cast<float*>(smem);   // [8][1024]
     {
-        float* p = part + (size_t)warp * kW4SliceCols + 32 * lane;
+        float* p = part + (size_t)warp * C::kSliceCols + C::kLaneCols * lane;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < C::kLaneCols / 4; ++j)
             reinterpret_cast<float4*>(p)[j] = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
     }
     __syncthreads();
     if (n_list > 0) {
-        for (int c = threadIdx.x; c < kW4SliceCols; c += kGemvThreads) {
-            const int o = slice * kW4SliceCols + c;
+        for (int c = threadIdx.x; c < C::kSliceCols; c += kGemvThreads) {
+            const int o = slice * C::kSliceCols + c;
             if (o >= a.d_out) break;
             float s = 0.f;
 #pragma unroll
-            for (int w = 0; w < kGemvWarps; ++w) s += part[(size_t)w * kW4SliceCols + c];
+            for (int w = 0; w < kGemvWarps; ++w) s += part[(size_t)w * C::kSliceCols + c];
             red_fix(a.acc + o, s, a.err);
         }
     }
@@ -342,7 +379,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_w4_select_kernel(const G
     // the last split of the slice finalises its 1024 columns as four 256-column slices of the bf16
     // kernel's epilogue (bias / residual / SiLU(g) u, accumulators re-zeroed, and at batch 1 the next
     // site's histogram and RMS partials): the same output layout and selection data
-    constexpr int kNv = kW4SliceCols / kSliceCols;
+    constexpr int kNv = C::kSliceCols / kSliceCols;
     const int vs0 = slice * kNv;
     const int nv = min(kNv, (a.d_out - vs0 * kSliceCols + kSliceCols - 1) / kSliceCols);
     gemv_epilogue_b1_multi<kNv>(a, vs0, nv, reinterpret_cast<float*>(misc + 16));

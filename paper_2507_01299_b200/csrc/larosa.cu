@@ -456,13 +456,13 @@ GemvArgs gemv_args_base() {
     return a;
 }
 
-// W4A16 SELECT GEMV (gemv_w4.cuh) with the layer's epilogue: 1024-column slices, one wave of 2 CTAs
-// per SM (the plan of larosa_topk_sparse_gemv_w4)
-larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, cudaStream_t st) {
+// W4A16 SELECT GEMV (gemv_w4.cuh) with the layer's epilogue: SC-column slices, one wave of 2 CTAs
+// per SM
+template <int SC>
+larosa_status launch_gemv_w4_t(GemvArgs a, const uint8_t* Wq, const uint16_t* S, cudaStream_t st) {
+    using C = W4Cfg<SC>;
     const int64_t d_in = a.d_in, d_out = a.d_out, k = a.sel_k;
-    if (d_out % kSliceCols || d_out > (int64_t)64 * kW4SliceCols)
-        return fail(LAROSA_EUNSUPPORTED, "W4 site: d_out must be a multiple of 256 (<= 65536)");
-    const int n_sl = (int)((d_out + kW4SliceCols - 1) / kW4SliceCols);
+    const int n_sl = (int)((d_out + SC - 1) / SC);
     const int64_t nwords = (d_in + 31) / 32;
     const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
     a.n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
@@ -472,8 +472,8 @@ larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, c
                   // the LLaMA3-8B down site: 40% companions, layer 84.2 -> 82.4 us)
         static const int pct_env = env_int("LAROSA_W4_COMP_PCT", 0);   // tuning
         const int total = std::max(2, sm_count() * 2 / n_sl);
-        const double main_b = (double)k * (kW4RowBytes + 2 * kW4SliceCols / kW4Group);
-        const double comp_b = (double)a.d2 * kW4CompRowBytes;
+        const double main_b = (double)k * (C::kRowBytes + 2 * C::kGroups);
+        const double comp_b = (double)a.d2 * C::kCompRowBytes;
         int n2 = pct_env > 0 ? (total * pct_env + 50) / 100 : (int)(total * comp_b / (3.0 * main_b + comp_b) + 0.5);
         n2 = std::max(1, std::min(n2, total - by_cap));
         a.n_splits = std::max(by_cap, total - n2);
@@ -484,12 +484,24 @@ larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, c
         a.n_splits2 = std::max<int>(a.n_splits2, (int)((a.d2 + a.list_cap - 1) / a.list_cap));
         if (a.n_splits + a.n_splits2 > 65535) return fail(LAROSA_EUNSUPPORTED, "W4 site: too many CTAs");
     }
-    const size_t smem = w4_smem_bytes((int)d_in, a.list_cap);
+    const size_t smem = w4_smem_bytes<SC>((int)d_in, a.list_cap);
     if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "W4 site: shared memory plan too large");
-    LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, smem), "cudaFuncSetAttribute(gemv_w4)"));
-    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, a.n_splits + a.n_splits2), dim3(kGemvThreads), smem, st, a,
-                             Wq, S),
+    LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel<SC>, smem), "cudaFuncSetAttribute(gemv_w4)"));
+    return cuda_check(launch(gemv_w4_select_kernel<SC>, dim3(n_sl, a.n_splits + a.n_splits2), dim3(kGemvThreads), smem,
+                             st, a, Wq, S),
                       "gemv_w4 launch");
+}
+
+// slice width: 512 for a site of <= 4096 outputs without companions (the O projection: its tail was
+// longer than its stream at 1024), 1024 otherwise (16-byte loads stream the large sites faster).
+// Measured on the LLaMA3-8B W4 layer: O 16.4 -> 13.4 us at 512; gate|up 23.1 vs 26.0, down 19.5 vs
+// 22.3 us in favour of 1024.
+larosa_status launch_gemv_w4(GemvArgs a, const uint8_t* Wq, const uint16_t* S, cudaStream_t st) {
+    if (a.d_out % kSliceCols || a.d_out > 65536)
+        return fail(LAROSA_EUNSUPPORTED, "W4 site: d_out must be a multiple of 256 (<= 65536)");
+    static const int forced = env_int("LAROSA_W4_SLICE", 0);   // tuning: 512 or 1024
+    const int sc = forced == 512 || forced == 1024 ? forced : (a.d_out <= 4096 && !a.W2 ? 512 : 1024);
+    return sc == 512 ? launch_gemv_w4_t<512>(a, Wq, S, st) : launch_gemv_w4_t<1024>(a, Wq, S, st);
 }
 
 // ============================================================================== small launches
@@ -2176,7 +2188,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     if (d_in <= 0 || d_out <= 0) return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: d_in, d_out must be > 0");
     if (k < 0 || k > d_in) return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: k outside [0, d_in]");
     if (d_in > LAROSA_MAX_DIM || d_in % 8) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: d_in");
-    if (d_out % kSliceCols || d_out > (int64_t)64 * kW4SliceCols)
+    if (d_out % kSliceCols || d_out > (int64_t)65536)
         return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: d_out must be a multiple of 256 (<= 65536)");
     if (!aligned16(Wq) || !aligned16(x) || !aligned16(y) || (reinterpret_cast<uintptr_t>(S) & 3))
         return fail(LAROSA_EINVAL, "topk_sparse_gemv_w4: alignment (Wq, x, y 16 B; S 4 B)");
@@ -2193,13 +2205,6 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
         LAROSA_TRY(cuda_check(launch(select_prep_kernel, dim3(n_slices_of(d_in)), dim3(kPrepThreads), 0, st, x, (int)d_in,
                                      sel, c.counters(kPrepBarrier), (float*)nullptr),
                               "select prep launch"));
-    // 1024-column slices (512 bytes of int4 per kept row and CTA), one wave of 2 CTAs per SM
-    const int n_sl = (int)((d_out + kW4SliceCols - 1) / kW4SliceCols);
-    const int64_t nwords = (d_in + 31) / 32;
-    const int by_cap = (int)std::max<int64_t>(1, (nwords + kSelMaxWords - 1) / kSelMaxWords);
-    const int n_splits = std::max(by_cap, std::min(std::max(1, sm_count() * 2 / n_sl), (int)std::max<int64_t>(1, k / 16)));
-    const int list_cap = (int)(32 * ((nwords + n_splits - 1) / n_splits));
-    const size_t smem = w4_smem_bytes((int)d_in, list_cap);
     GemvArgs a = gemv_args_base();
     a.ld = d_out;
     a.d_out = (int)d_out;
@@ -2218,12 +2223,7 @@ extern "C" larosa_status larosa_topk_sparse_gemv_w4(const float* x, int64_t d_in
     a.tickets = c.counters(kGemvTicketBase);
     a.out = y;
     a.out_ld = d_out;
-    a.n_splits = n_splits;
-    a.list_cap = list_cap;
-    LAROSA_TRY(cuda_check(allow_smem(gemv_w4_select_kernel, 227 * 1024), "cudaFuncSetAttribute(gemv_w4)"));
-    if (smem > 227 * 1024) return fail(LAROSA_EUNSUPPORTED, "topk_sparse_gemv_w4: shared memory plan too large");
-    return cuda_check(launch(gemv_w4_select_kernel, dim3(n_sl, n_splits), dim3(kGemvThreads), smem, st, a, Wq, S),
-                      "gemv_w4 launch");
+    return launch_gemv_w4(a, Wq, S, st);
 }
 
 // ============================================================================== N2 prefill
