@@ -85,7 +85,8 @@ def main():
                     live = live & ((cur[:, 5] > 0) == sel)
                 c = cur[live] - t0
                 for i, key in enumerate(["entry", "wait", "prologue", "loop", "exit", "sel_hist", "rule_coarse", "sel_mask",
-                                          "rule_fine", "rule_pool", "rule_ssq", "list", "ticket", "epi", "mask2", "list2"]):
+                                          "rule_fine", "rule_pool", "rule_ssq", "list", "ticket", "epi", "lookup_data",
+                                          "unused"]):
                     col = c[:, i]
                     col = col[cur[live][:, i] > 0]
                     if col.size:
