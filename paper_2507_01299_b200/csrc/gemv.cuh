@@ -413,16 +413,31 @@ __device__ __forceinline__ void rule_pool(const SiteSel& sel, int b16, int rem, 
 // defer_pool: when the boundary bucket needs its pool, return with kRulePending (tk = the bucket's
 // lower edge, misc[1..3] = b16 / rem / cnt) and let the caller's warp 0 resolve it (rule_pool)
 // while the other warps compute the definite keep masks
+// (zero job: words whose consumer has completed, cleared by warps 2.. while warp 0 looks the rule up and
+// warp 1 sums the squares -- not ahead of warp 0's loads in program order)
+struct ZeroJob {
+    uint32_t* w32;
+    int n32;
+    unsigned long long* w64;
+    int n64;
+};
+// this CTA's share of a zero job: nz threads per CTA (t < nz), the same partition in every CTA of the grid
+__device__ __forceinline__ void zero_share(const ZeroJob& zj, int t, int nz) {
+    const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
+    for (int i = cta * nz + t; i < zj.n32; i += nct * nz) zj.w32[i] = 0u;
+    for (int i = cta * nz + t; i < zj.n64; i += nct * nz) zj.w64[i] = 0ull;
+}
 template <int NT>
 __device__ void compute_rule(const SiteSel& sel, const float* x, int d, int k, float eps, int nssq,
                              unsigned char* scratch, SelRule* R, unsigned long long* tl = nullptr, int guess = 0,
-                             uint32_t* err = nullptr, bool defer_pool = false) {
+                             uint32_t* err = nullptr, bool defer_pool = false, const ZeroJob* zj = nullptr) {
     static_assert(NT >= 64, "two warps");
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int* misc = reinterpret_cast<int*>(scratch);           // [0] status, [1..3] b16/rem/cnt, [4] scale
     int* shist = misc + 16;                                 // fallback: <= 256 padded bins
     int* scan = shist + 272;
     float* fmisc = reinterpret_cast<float*>(misc);
+    if (zj && wid >= 2) zero_share(*zj, tid - 64, NT - 64);
     if (wid == 1) {
         const float sc = eps >= 0.f ? rms_scale_from_parts(sel.ssq, nssq, d, eps, lane) : 1.0f;
         if (lane == 0) fmisc[4] = sc;
@@ -582,7 +597,7 @@ __host__ __device__ constexpr size_t gemv_x_bytes(int bp, int mode, int d_in) {
 
 // Returns the number of rows placed in lrow (ascending); misc[4] receives the RMS scale.
 __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* region, int* lrow, float* lval, int* misc,
-                                           int split, int n_splits, int guess) {
+                                           int split, int n_splits, int guess, const ZeroJob* zj = nullptr) {
     constexpr int NT = kGemvThreads, NW = kGemvWarps;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int d = a.d_in;
@@ -602,7 +617,7 @@ __device__ __forceinline__ int select_rows(const GemvArgs& a, unsigned char* reg
     // the exact rule, computed by warps 0 (selection) and 1 (RMS scale) while the CTA's words land
     SelRule* R = reinterpret_cast<SelRule*>(misc + 48);
     unsigned char* rscratch = region + sel_mask_off(d) + kSelMaxWords * 8;
-    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, rscratch, R, a.tl, guess, a.err, true);
+    compute_rule<NT>(a.sel, a.x, d, a.sel_k, a.sel_eps, a.sel_nssq, rscratch, R, a.tl, guess, a.err, true, zj);
     const int* rmisc = reinterpret_cast<const int*>(rscratch);
     const int flags0 = R->flags;
     if (tid == 0) reinterpret_cast<float*>(misc)[4] = R->scale;
@@ -844,13 +859,20 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
     if (!a.late_trigger) pdl_trigger();
     tl_stamp(a.tl, 1);
     if (comp && a.comp_late) comp_prefetch();   // (tuning: not while the previous kernel's prologue runs)
-    if (a.zero_hist) {   // a histogram whose consumer has completed (kernel-boundary ordered)
-        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
-        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_words; i += nct * kGemvThreads) a.zero_hist[i] = 0u;
-    }
-    if (a.zero_acc) {    // accumulators whose consumer has completed
-        const int nct = gridDim.x * gridDim.y, cta = blockIdx.y * gridDim.x + blockIdx.x;
-        for (int i = cta * kGemvThreads + threadIdx.x; i < a.zero_acc_words; i += nct * kGemvThreads) a.zero_acc[i] = 0ull;
+    // words whose consumer has completed (kernel-boundary ordered): a histogram, accumulators.  A
+    // SELECT CTA clears them inside the rule lookup with its otherwise idle warps (every CTA of the
+    // grid takes a share; the companions' shares too); the other modes clear them here
+    ZeroJob zj;
+    zj.w32 = a.zero_hist;
+    zj.n32 = a.zero_hist ? a.zero_words : 0;
+    zj.w64 = a.zero_acc;
+    zj.n64 = a.zero_acc ? a.zero_acc_words : 0;
+    // (one partition for the whole grid: kGemvThreads - 64 threads per CTA in SELECT launches, whose
+    // companion CTAs clear their share here with the same partition)
+    const bool zero_in_rule = MODE == GEMV_SELECT && !comp;
+    if (!zero_in_rule && (zj.n32 || zj.n64)) {
+        const int nz = MODE == GEMV_SELECT ? kGemvThreads - 64 : kGemvThreads;
+        if ((int)threadIdx.x < nz) zero_share(zj, threadIdx.x, nz);
     }
 
     // ---- 1. this CTA's row list in shared memory (ascending) ------------------------------
@@ -863,7 +885,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const GemvArgs a) {
             for (int t = threadIdx.x; t < c_n; t += kGemvThreads) lval[t] = __ldcg(a.x2 + c_lo + t);
             __syncthreads();
         } else {
-            n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess);
+            n_list = select_rows(a, smem, lrow, lval, misc, split, a.n_splits, sel_guess, &zj);
         }
     } else if constexpr (MODE == GEMV_LIST) {
         const int nrows = a.nrows_dev ? *a.nrows_dev : a.nrows;
