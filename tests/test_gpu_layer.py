@@ -380,3 +380,23 @@ def test_layer_batch_rule_degenerate_tokens(batch, merged):
     for b in range(batch):
         p6_layer(ow, shape, plan, tp, b, resid[b].numpy().astype(np.float64), kc0[b].numpy().view(np.uint16),
                  kc_gpu[b], vc_gpu[b], int(pos[b]), f64(st.resid[b]))
+
+
+@pytest.mark.parametrize("batch", [3, 16])
+@pytest.mark.parametrize("plan_kind", ["edges_a", "edges_b"])
+def test_layer_batch_rule_edge_k(batch, plan_kind):
+    """Batch > 1 selection rule at the edge counts (k = 0, 1, D - 1, D at the four sites), site by
+    site against the oracle (P6)."""
+    from layer_check import OracleWeights, p6_layer
+    shape = SMALL
+    max_ctx = 64
+    _, _, _, lw, _, resid, kc0, vc0, pos = build(shape, 37, batch, 30, max_ctx, 0.5)
+    nq = shape.hq * shape.hd
+    plan = (0, 1, shape.d - 1, shape.inter) if plan_kind == "edges_a" else (shape.d, nq - 1, 1, 0)
+    st, tp = run_layer(lw, plan, resid, kc0, vc0, pos)
+    ow = OracleWeights(lw)
+    kc_gpu = st.k_cache.cpu().numpy().view(np.uint16)
+    vc_gpu = st.v_cache.cpu().numpy().view(np.uint16)
+    for b in range(batch):
+        p6_layer(ow, shape, plan, tp, b, resid[b].numpy().astype(np.float64), kc0[b].numpy().view(np.uint16),
+                 kc_gpu[b], vc_gpu[b], int(pos[b]), f64(st.resid[b]))
