@@ -129,3 +129,18 @@ def test_w4_decode_step_llama3_8b():
     ref = O.lm_head(r_final[0], O.bf16_to_f64(model.head.cpu().numpy().view(np.uint16)), shape.rms_eps)
     assert np.max(np.abs(logits - ref)) <= 1e-5 * np.linalg.norm(ref)
     assert int(nxt[0]) == int(np.argmax(logits))
+
+
+@pytest.mark.parametrize("merged", [False, True])
+def test_w4_layer_edge_k(merged):
+    """W4 sites at the edge counts (k = 0, 1, D - 1, D and the reverse), P6 against the oracle."""
+    shape = SMALL
+    nq = shape.hq * shape.hd
+    for plan in ((0, 1, shape.d - 1, shape.inter), (shape.d, nq - 1, 1, 0)):
+        _, _, _, lw, _, resid, kc0, vc0, pos = build(shape, 41, 1, 12, 64, 0.5, with_adapter=True, merged=merged)
+        lw4 = M.quantize_layer_w4(lw)
+        st, tp = run_layer(lw4, plan, resid, kc0, vc0, pos)
+        ow = oracle_weights_w4(lw4, shape.inter)
+        p6_layer(ow, shape, plan, tp, 0, resid[0].numpy().astype(np.float64), kc0[0].numpy().view(np.uint16),
+                 st.k_cache[0].cpu().numpy().view(np.uint16), st.v_cache[0].cpu().numpy().view(np.uint16),
+                 int(pos[0]), f64(st.resid[0]))
